@@ -1,0 +1,136 @@
+/* mpcgemm.h -- C ABI of the B200 (sm_100a) Ozaki-scheme complex multiple-precision GEMM.
+ *
+ * Operation (Eq. 1):  C := A B,  A in C^{m x k}, B in C^{k x n}, with the
+ * complex product formed by the 4M method (Eq. 5) or the 3M method
+ * (Eq. 6), and every real product computed by the Ozaki scheme
+ * (Algorithm 2) on INT8 tensor cores.  DESIGN.md states the readings
+ * (Z1..Z24) under which the result is defined; it is bit-identical to oracle/mpref.c
+ * orc_cgemm_ozaki() for the same s:
+ *
+ *   eA_i = max exponent over the nonzero entries of row i of Re A and Im A    (mu_A)
+ *   eB_j = max exponent over the nonzero entries of column j of Re B, Im B   (mu_B)
+ *   W = 8 s - 3;  X(x) = sign(x) floor(|x| 2^(W - e))  (e = eA_i or eB_j)
+ *   slices: X = sum_{alpha=1..s} d_alpha 256^(s-alpha), d_alpha in [-128,127] (unique
+ *           balanced radix-256 digits); 3M sums use X(Re) + X(Im) exactly
+ *   real product P = sum_{alpha+beta <= s+1} (D^A_alpha D^B_beta) 256^(s+1-alpha-beta)
+ *           exact in integers, value P * 2^(eA_i + eB_j + 6 - 8(s+1))
+ *   4M: Re = P(ReA,ReB) - P(ImA,ImB), Im = P(ReA,ImB) + P(ImA,ReB)
+ *   3M: T1 = P(ReA,ReB), T2 = P(ImA,ImB), T3 = P(ReA+ImA, ReB+ImB), Re = T1 - T2, Im = T3 - T1 - T2
+ *   output: each part rounded once to nearest-even at prec bits.
+ *
+ * Element format (MPFR convention; planar complex):
+ *   value = (-1)^sign * N * 2^(exp - 64 L),  N = sum_l limbs[l] 2^(64 l),  L = ceil(prec/64)
+ *   nonzero: top bit of limbs[L-1] set, the low 64L-prec bits zero; |exp| <= 2^61
+ *   zero:    all limbs zero (sign and exp ignored on input; written as +0, exp 0)
+ *   Matrices are row-major with leading dimension ld (entries); limbs are entry-major
+ *   (entry e's limbs at limbs[e*L .. e*L+L-1]).  No NaN / Inf encoding exists.
+ *
+ * Ownership: the caller owns A, B and C (DEVICE memory for mpcgemm/mpcgemm_ex/
+ * mpcgemm_rho_bounds; HOST memory for mpcgemm_host).  The library never frees them and
+ * owns only its workspace (a per-device grow-only cache released by mpcgemm_release(),
+ * or caller memory via opts->workspace).  C must not overlap A or B.  Calls are
+ * stream-ordered on opts->stream (NULL: the legacy default stream); A and B must stay
+ * unchanged until the stream passes the call.  The host blocks only to read back the
+ * 24-byte pre-pass result when slices == 0 (auto).
+ *
+ * Errors: return 0 = OK, > 0 warning, < 0 error.  No exceptions, no abort, no printing.
+ * On an error detected before launch C is untouched; after a CUDA error C is undefined
+ * and mpcgemm_last_error() describes it (thread-local).
+ */
+#ifndef MPCGEMM_H
+#define MPCGEMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPCGEMM_OK                  0
+#define MPCGEMM_ERR_ARG            -1   /* null pointer, m/n/k < 0, ld < cols, bad method      */
+#define MPCGEMM_ERR_PREC           -2   /* prec outside [2, 4096]                              */
+#define MPCGEMM_ERR_EXP_RANGE      -3   /* |exp| > 2^61 (validate mode)                        */
+#define MPCGEMM_ERR_NOT_NORMALIZED -4   /* nonzero mantissa without top bit / low bits set     */
+#define MPCGEMM_ERR_ALIAS          -5   /* C overlaps A or B                                   */
+#define MPCGEMM_ERR_NOMEM          -6   /* workspace allocation failed / too small             */
+#define MPCGEMM_ERR_CUDA           -7   /* CUDA runtime error (see mpcgemm_last_error)         */
+#define MPCGEMM_ERR_SLICES         -8   /* forced or derived slice count outside [1, 1024]     */
+
+typedef struct {
+    uint8_t  *sign;   /* [rows*ld]      0 = +, 1 = -                                          */
+    int64_t  *exp;    /* [rows*ld]      MPFR exponent: |x| in [2^(exp-1), 2^exp)              */
+    uint64_t *limbs;  /* [rows*ld*L]    little-endian limbs, entry-major                      */
+    int64_t   ld;     /* leading dimension in entries, >= cols                                */
+} mpc_rmat;
+
+typedef struct { mpc_rmat re, im; } mpc_cmat;   /* planar complex, one prec for all parts   */
+
+typedef enum { MPCGEMM_3M = 3, MPCGEMM_4M = 4 } mpcgemm_method;
+
+typedef struct {
+    void    *stream;          /* cudaStream_t; NULL = legacy default stream                   */
+    int32_t  slices;          /* 0 = auto (pre-pass + slice rule); > 0 forces s               */
+    int32_t  validate;        /* 1 = check normalization / exponent range on device first      */
+    void    *workspace;       /* NULL = library-managed per-device cache                       */
+    size_t   workspace_bytes; /* size of caller workspace (>= mpcgemm_workspace_size)          */
+} mpcgemm_opts;
+
+typedef struct {
+    int32_t slices;           /* s used                                                        */
+    int32_t certified;        /* 1 if s came from the certified rule or was forced             */
+    int64_t minT, minT1, maxD2;   /* pre-pass integers (-1 when not computed)                  */
+    double  log2_rho_hat;     /* the rule's log2 rho-hat                                       */
+    int64_t mma_instructions; /* tcgen05.mma count issued by the slice GEMM (K=32 each)         */
+    int64_t work_units;       /* slice-GEMM work units (tile, diagonal, chunk, product)         */
+} mpcgemm_report;
+
+/* C := A B (auto slice count).  Device pointers.  m, n, k >= 0 (empty: nothing written for
+ * m*n == 0; k == 0 writes zeros).  2 <= prec <= 4096. */
+int mpcgemm(int64_t m, int64_t n, int64_t k, int32_t prec,
+            const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C, mpcgemm_method method);
+
+/* as mpcgemm, with options (stream, forced slice count, workspace) and an optional report. */
+int mpcgemm_ex(int64_t m, int64_t n, int64_t k, int32_t prec,
+               const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C, mpcgemm_method method,
+               const mpcgemm_opts *opts, mpcgemm_report *rep);
+
+/* End-to-end call on HOST buffers: copies A and B to the device, computes, copies C back
+ * (all inside the call; blocks until C is on the host).  Host pointers; pinned memory
+ * recommended.  Uses the library workspace cache plus a device staging cache. */
+int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec,
+                 const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C, mpcgemm_method method,
+                 const mpcgemm_opts *opts, mpcgemm_report *rep);
+
+/* The rho-hat pre-pass on this process's A rows:
+ *   out[0] = minT  = min_ij T_ij, T = t u (INT8 GEMM), over nonzero rows/columns with
+ *                    (|A||B|)_ij != 0  (-1: no such pair)
+ *   out[1] = minT1, out[2] = maxD2: the second stage (exact max-plus exponent bound),
+ *            computed when out[0] == 0 or full != 0; otherwise out[1] = out[0], out[2] = -1.
+ * Multi-GPU: ranks all-reduce MIN of out[0]; if the result is 0 every rank calls again with
+ * full = 1 and ranks all-reduce MIN out[1] (ignoring -1) and MAX out[2]; then
+ * mpcgemm_slices_for() on the reduced integers gives the common s.  Synchronizes the stream. */
+int mpcgemm_rho_bounds(int64_t m, int64_t n, int64_t k, int32_t prec,
+                       const mpc_cmat *A, const mpc_cmat *B, int32_t full,
+                       const mpcgemm_opts *opts, int64_t out[3]);
+
+/* The slice-count rule:  log2rho = log2(k) + 14 - log2(minT) (minT > 0), or the max of that
+ * with minT1 and log2(k) + 2 + maxD2 (minT == 0), or 0 (minT < 0);
+ * s = min{ s >= 1 : 8 s >= prec - 4 + log2(c s) + log2rho + 0.1 }, c = 3 (4M), 4 (3M).
+ * Returns s, or MPCGEMM_ERR_SLICES if s > 1024. */
+int mpcgemm_slices_for(int32_t prec, mpcgemm_method method, int64_t k,
+                       int64_t minT, int64_t minT1, int64_t maxD2);
+
+/* Device workspace bytes for one call with s slices. */
+size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec,
+                              mpcgemm_method method, int32_t slices);
+
+const char *mpcgemm_strerror(int code);
+const char *mpcgemm_last_error(void);   /* thread-local detail of the last error              */
+void mpcgemm_release(void);              /* frees the cached workspace of the current device   */
+int  mpcgemm_version(void);              /* ABI version (100 * major + minor)                  */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPCGEMM_H */

@@ -1,0 +1,165 @@
+"""CPU oracle (TEST INFRASTRUCTURE ONLY) -- ctypes wrapper around oracle/mpref.c.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import this module.  It never imports the CUDA path (paper_2307_06072_b200) and the
+CUDA path never imports it.  See oracle/mpref.c for the paper passages each function
+follows, and DESIGN.md "Oracle" for the readings.
+
+Pins (tests/test_oracle_*.py): brute-force Fractions on 2x2/3x3, independent RNE,
+B = I, integer-entry closure, SPEC worked examples, 3M == 4M exact, scaling, transposition,
+zero rows, rounded-mode 3M/4M agreement; the Ozaki oracle is pinned by digit-reconstruction
+identities, exact closure, the closed-form error bound and the s-saturation sweep.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+from mpgen import CMat, RMat, empty_rmat, limbs_for
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mpref.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle/mpref.c -> oracle/liboracle.so (gcc, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _RM(ctypes.Structure):
+    _fields_ = [("sign", ctypes.c_void_p), ("exp", ctypes.c_void_p), ("limbs", ctypes.c_void_p),
+                ("ld", ctypes.c_int64), ("L", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            P = ctypes.POINTER(_RM)
+            i64, i32, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+            L.orc_cgemm_exact.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, i64, vp, vp, i32]
+            L.orc_cgemm_exact.restype = ctypes.c_int
+            L.orc_cgemm_ozaki.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, i64, vp, vp, i32]
+            L.orc_cgemm_ozaki.restype = ctypes.c_int
+            L.orc_exponents.argtypes = [i64, i64, i64, P, P, P, P, vp, vp, vp, vp]
+            L.orc_split.argtypes = [ctypes.c_int, i64, i64, P, P, i32, i32, vp]
+            L.orc_split.restype = ctypes.c_int
+            L.orc_rho_bounds.argtypes = [i64, i64, i64, P, P, P, P, vp, i32]
+            L.orc_rho_bounds.restype = ctypes.c_int
+            L.orc_slices_for.argtypes = [i32, i32, i64, i64, i64, i64]
+            L.orc_slices_for.restype = ctypes.c_int32
+            _lib = L
+    return _lib
+
+
+def _rm(M: RMat) -> _RM:
+    for a in (M.sign, M.exp, M.limbs):
+        assert a.flags["C_CONTIGUOUS"]
+    return _RM(M.sign.ctypes.data, M.exp.ctypes.data, M.limbs.ctypes.data, M.shape[1], M.L, 0)
+
+
+def _ptr(x):
+    return ctypes.byref(x)
+
+
+def _form(method) -> int:
+    return {"3M": 3, "4M": 4, 3: 3, 4: 4}[method]
+
+
+def _run(fn, A: CMat, B: CMat, prec_out, form, extra, samples, nthreads):
+    m, k = A.shape
+    k2, n = B.shape
+    assert k == k2
+    if samples is None:
+        Cre, Cim = empty_rmat(m, n, prec_out), empty_rmat(m, n, prec_out)
+        ns, si, sj = -1, None, None
+    else:
+        si = np.ascontiguousarray(np.asarray(samples[0], dtype=np.int64))
+        sj = np.ascontiguousarray(np.asarray(samples[1], dtype=np.int64))
+        ns = len(si)
+        Cre, Cim = empty_rmat(1, max(ns, 1), prec_out), empty_rmat(1, max(ns, 1), prec_out)
+    args = [_rm(A.re), _rm(A.im), _rm(B.re), _rm(B.im), _rm(Cre), _rm(Cim)]
+    rc = fn(m, n, k, *[_ptr(a) for a in args], prec_out, _form(form), extra, ns,
+            si.ctypes.data if si is not None else None, sj.ctypes.data if sj is not None else None, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle returned {rc}")
+    C = CMat(Cre, Cim)
+    if samples is not None:
+        C = C.cols(0, ns)
+    return C
+
+
+def exact(A: CMat, B: CMat, prec_out: int, method="4M", rounded_prec: int = 0, samples=None, nthreads: int = 0) -> CMat:
+    """Plain definition C = AB (Eq. 2 + Eq. 3 for 4M, Eq. 4 for 3M), exact, one RNE to
+    prec_out.  rounded_prec > 0: MPC-like per-operation rounding (Eq. 5 / Eq. 6).
+    samples = (rows, cols) index arrays -> a 1 x len(samples) result."""
+    return _run(lib().orc_cgemm_exact, A, B, prec_out, method, rounded_prec, samples, nthreads)
+
+
+def ozaki(A: CMat, B: CMat, prec_out: int, method="3M", s: int | None = None, samples=None, nthreads: int = 0) -> CMat:
+    """Algorithm 2 step by step (DESIGN.md readings), s slices (auto rule if None)."""
+    if s is None:
+        s, _ = auto_slices(A, B, A.prec, method)
+    return _run(lib().orc_cgemm_ozaki, A, B, prec_out, method, s, samples, nthreads)
+
+
+def exponents(A: CMat, B: CMat):
+    m, k = A.shape
+    n = B.shape[1]
+    eA, eB = np.zeros(m, np.int64), np.zeros(n, np.int64)
+    nzA, nzB = np.zeros(m, np.uint8), np.zeros(n, np.uint8)
+    a = [_rm(A.re), _rm(A.im), _rm(B.re), _rm(B.im)]
+    lib().orc_exponents(m, n, k, *[_ptr(x) for x in a], eA.ctypes.data, eB.ctypes.data, nzA.ctypes.data, nzB.ctypes.data)
+    return eA, eB, nzA.astype(bool), nzB.astype(bool)
+
+
+def split(P: CMat, side: int, s: int, nparts: int) -> np.ndarray:
+    """Digit planes int8[nparts, s, lines, k]: side 0 = rows of A (P is m x k), side 1 =
+    columns of B (P is k x n)."""
+    rows, cols = P.shape
+    lines, k = (rows, cols) if side == 0 else (cols, rows)
+    dig = np.zeros((nparts, s, lines, k), np.int8)
+    rc = lib().orc_split(side, lines, k, _ptr(_rm(P.re)), _ptr(_rm(P.im)), s, nparts, dig.ctypes.data)
+    if rc:
+        raise RuntimeError(f"orc_split returned {rc}")
+    return dig
+
+
+def rho_minT(A: CMat, B: CMat, nthreads: int = 0) -> int:
+    return rho_bounds(A, B, nthreads)[0]
+
+
+def rho_bounds(A: CMat, B: CMat, nthreads: int = 0):
+    """(minT, minT1, maxD2): the integers of the two-stage rho-hat pre-pass."""
+    m, k = A.shape
+    n = B.shape[1]
+    out = (ctypes.c_int64 * 3)()
+    a = [_rm(A.re), _rm(A.im), _rm(B.re), _rm(B.im)]
+    rc = lib().orc_rho_bounds(m, n, k, *[_ptr(x) for x in a], ctypes.addressof(out), nthreads)
+    if rc:
+        raise RuntimeError(f"orc_rho_bounds returned {rc}")
+    return tuple(int(v) for v in out)
+
+
+def slices_for(prec: int, method, k: int, minT: int, minT1: int | None = None, maxD2: int = -1):
+    """The slice-count rule; returns (s, ok)."""
+    minT1 = minT if minT1 is None else minT1
+    s = lib().orc_slices_for(prec, _form(method), k, minT, minT1, maxD2)
+    return s, s > 0
+
+
+def auto_slices(A: CMat, B: CMat, prec: int, method, nthreads: int = 0):
+    return slices_for(prec, method, A.shape[1], *rho_bounds(A, B, nthreads))

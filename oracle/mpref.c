@@ -1,0 +1,684 @@
+/* oracle/mpref.c -- CPU oracle for the Ozaki-scheme complex multiple-precision GEMM.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load or call this library.  It shares no
+ * code, header, table or helper with the CUDA path (paper_2307_06072_b200/), and never
+ * imports it.  Plain, slow, obviously-correct code: exact big integers built from
+ * uint64 limbs and unsigned __int128 schoolbook products (no GMP), one rounding.
+ *
+ * Two oracles (DESIGN.md section "Oracle"):
+ *  (1) orc_cgemm_exact  -- the plain definition C := AB (Eq. 1-2) with
+ *      the complex product of Eq. 3 (4M) or Eq. 4 (3M),
+ *      every sum exact, ONE round-to-nearest-even to prec_out (reading Z8).
+ *      "rounded" mode: the MPC-like variant where each real GEMM (Eq. 5/6,
+ *      PAPER.md:81-97) is exact then rounded, and every combination/sum is rounded.
+ *  (2) orc_cgemm_ozaki  -- Algorithm 2 step by step, under the
+ *      readings Z1/Z3/Z5/Z7/Z10/Z11 of DESIGN.md: per-row (per-column) exponent mu
+ *      (common to Re/Im), fixed-point truncation to
+ *      W = 8s-3 bits, the slices A_alpha = the s digits of the unique balanced radix-256
+ *      representation (digit set [-128,127]), the triangle beta <= d-alpha+1
+ *      (PAPER.md:174-177), exact accumulation (Z7) and one RNE rounding;
+ *      complex forms by Eq. 5 (4M) / Eq. 6 (3M).
+ *  plus the slice-count rule:
+ *      t_ik = floor(max(|ReA_ik|,|ImA_ik|) 2^(7-eA_i)), u_kj likewise, T = t u,
+ *      log2rho = log2((double)k) + 14.0 - log2((double)minT),
+ *      s = min{ s >= 1 : 8 s >= prec - 4 + log2(c_M s) + log2rho + 0.1 }, c_4M = 3, c_3M = 4.
+ *
+ * Element format (MPFR convention): value = (-1)^sign * N * 2^(exp - 64 L),
+ * N = little-endian limbs; zero <=> all limbs zero.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef unsigned __int128 u128;
+
+typedef struct {
+    uint8_t *sign;
+    int64_t *exp;
+    uint64_t *limbs;
+    int64_t ld;
+    int32_t L;
+    int32_t pad_;
+} orc_rmat;
+
+/* ------------------------------------------------------------------ exact numbers */
+/* value = (-1)^neg * mag * 2^e ; mag has n limbs (n == 0 <=> zero); own != 0 => malloc'ed */
+typedef struct { int neg; int64_t e; int n; uint64_t *m; int own; } xn;
+
+static void xn_free(xn *v) { if (v->own && v->m) free(v->m); v->m = NULL; v->n = 0; v->own = 0; }
+
+static int is_zero_limbs(const uint64_t *p, int n) {
+    for (int i = 0; i < n; i++) if (p[i]) return 0;
+    return 1;
+}
+
+static xn entry_of(const orc_rmat *M, int64_t r, int64_t c) {
+    int64_t idx = r * M->ld + c;
+    xn v;
+    v.m = M->limbs + idx * M->L;
+    v.n = is_zero_limbs(v.m, M->L) ? 0 : M->L;
+    v.neg = v.n ? (M->sign[idx] != 0) : 0;
+    v.e = M->exp[idx] - 64 * (int64_t)M->L;
+    v.own = 0;
+    return v;
+}
+
+static int bitlen_limbs(const uint64_t *p, int n) {
+    for (int i = n - 1; i >= 0; i--)
+        if (p[i]) return 64 * i + (64 - __builtin_clzll(p[i]));
+    return 0;
+}
+
+static int getbit(const uint64_t *p, int n, int64_t pos) {
+    if (pos < 0 || pos >= 64 * (int64_t)n) return 0;
+    return (int)((p[pos >> 6] >> (pos & 63)) & 1u);
+}
+
+/* r[0..nr) = (p >> sh) truncated to nr limbs (sh >= 0) */
+static void shr_limbs(uint64_t *r, int nr, const uint64_t *p, int np, int64_t sh) {
+    int64_t lo = sh >> 6; int bs = (int)(sh & 63);
+    for (int i = 0; i < nr; i++) {
+        int64_t a = lo + i;
+        uint64_t v = 0;
+        if (a < np) v = p[a] >> bs;
+        if (bs && a + 1 < np) v |= p[a + 1] << (64 - bs);
+        r[i] = v;
+    }
+}
+
+/* r[0..nr) = (p << sh) truncated to nr limbs (sh >= 0) */
+static void shl_limbs(uint64_t *r, int nr, const uint64_t *p, int np, int64_t sh) {
+    int64_t lo = sh >> 6; int bs = (int)(sh & 63);
+    for (int i = 0; i < nr; i++) {
+        int64_t a = i - lo;           /* source limb */
+        uint64_t v = 0;
+        if (a >= 0 && a < np) v = p[a] << bs;
+        if (bs && a - 1 >= 0 && a - 1 < np) v |= p[a - 1] >> (64 - bs);
+        r[i] = v;
+    }
+}
+
+/* magnitude product r[0..na+nb) = a * b (schoolbook) */
+static void mulmag(uint64_t *r, const uint64_t *a, int na, const uint64_t *b, int nb) {
+    memset(r, 0, sizeof(uint64_t) * (size_t)(na + nb));
+    for (int i = 0; i < na; i++) {
+        uint64_t carry = 0;
+        for (int j = 0; j < nb; j++) {
+            u128 t = (u128)a[i] * b[j] + r[i + j] + carry;
+            r[i + j] = (uint64_t)t;
+            carry = (uint64_t)(t >> 64);
+        }
+        r[i + nb] = carry;
+    }
+}
+
+/* two's complement accumulator acc[0..na) += (neg ? -1 : +1) * (p << sh), sh >= 0 */
+static void addsh(uint64_t *acc, int na, const uint64_t *p, int np, int64_t sh, int neg) {
+    int64_t lo = sh >> 6; int bs = (int)(sh & 63);
+    uint64_t c = 0;
+    int64_t idx = lo;
+    for (int i = 0; i <= np; i++, idx++) {
+        uint64_t v = (i < np) ? (p[i] << bs) : 0;
+        if (bs && i > 0) v |= p[i - 1] >> (64 - bs);
+        if (idx >= na) break;
+        if (!neg) {
+            u128 t = (u128)acc[idx] + v + c;
+            acc[idx] = (uint64_t)t; c = (uint64_t)(t >> 64);
+        } else {
+            u128 t = (u128)acc[idx] - v - c;
+            acc[idx] = (uint64_t)t; c = (t >> 64) ? 1 : 0;
+        }
+    }
+    for (; c && idx < na; idx++) {
+        if (!neg) { acc[idx] += 1; c = (acc[idx] == 0); }
+        else      { c = (acc[idx] == 0); acc[idx] -= 1; }
+    }
+}
+
+/* two's complement acc (na limbs) * 2^e  ->  xn (owning) */
+static xn xn_from_acc(const uint64_t *acc, int na, int64_t e) {
+    xn v; v.own = 1; v.e = e;
+    v.neg = (int)(acc[na - 1] >> 63);
+    v.m = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(na > 0 ? na : 1));
+    if (v.neg) {
+        uint64_t c = 1;
+        for (int i = 0; i < na; i++) { uint64_t x = ~acc[i] + c; c = (c && x == 0); v.m[i] = x; }
+    } else {
+        memcpy(v.m, acc, sizeof(uint64_t) * (size_t)na);
+    }
+    int b = bitlen_limbs(v.m, na);
+    v.n = (b + 63) / 64;
+    if (!v.n) v.neg = 0;
+    return v;
+}
+
+/* exact a + (sub ? -b : b) */
+static xn xn_add(const xn *a, const xn *b, int sub) {
+    int64_t emin = 0, top = 0; int any = 0;
+    const xn *t[2] = {a, b};
+    for (int q = 0; q < 2; q++) {
+        if (!t[q]->n) continue;
+        int64_t hi = t[q]->e + 64 * (int64_t)t[q]->n;
+        if (!any || t[q]->e < emin) emin = t[q]->e;
+        if (!any || hi > top) top = hi;
+        any = 1;
+    }
+    if (!any) { xn z = {0, 0, 0, NULL, 0}; return z; }
+    int na = (int)((top - emin) / 64) + 3;
+    uint64_t *acc = (uint64_t *)calloc((size_t)na, sizeof(uint64_t));
+    if (a->n) addsh(acc, na, a->m, a->n, a->e - emin, a->neg);
+    if (b->n) addsh(acc, na, b->m, b->n, b->e - emin, b->neg ^ sub);
+    xn r = xn_from_acc(acc, na, emin);
+    free(acc);
+    return r;
+}
+
+/* RNE of v to prec bits, stored in ABI element format with Lout limbs (Z8) */
+static void xn_store(const xn *v, int prec, uint8_t *sign, int64_t *exp, uint64_t *limbs, int Lout) {
+    int b = v->n ? bitlen_limbs(v->m, v->n) : 0;
+    memset(limbs, 0, sizeof(uint64_t) * (size_t)Lout);
+    if (b == 0) { *sign = 0; *exp = 0; return; }
+    int64_t E = v->e + b;
+    int nq = (prec + 63) / 64 + 1;
+    uint64_t q[nq];
+    if (b <= prec) {
+        shl_limbs(limbs, Lout, v->m, v->n, 64 * (int64_t)Lout - b);
+    } else {
+        int64_t sh = b - prec;
+        shr_limbs(q, nq, v->m, v->n, sh);
+        int rbit = getbit(v->m, v->n, sh - 1);
+        int sticky = 0;                        /* OR of the bits below the round bit */
+        int64_t full = (sh - 1) >> 6;
+        for (int64_t q2 = 0; q2 < full && q2 < v->n && !sticky; q2++) if (v->m[q2]) sticky = 1;
+        if (!sticky && full < v->n && ((sh - 1) & 63))
+            if (v->m[full] & ((1ULL << ((sh - 1) & 63)) - 1)) sticky = 1;
+        if (rbit && (sticky || (q[0] & 1))) {
+            uint64_t c = 1;
+            for (int i = 0; i < nq && c; i++) { q[i] += 1; c = (q[i] == 0); }
+            if (bitlen_limbs(q, nq) > prec) {     /* carry-out: 2^prec -> 2^(prec-1), exp + 1 */
+                uint64_t t2[nq];
+                shr_limbs(t2, nq, q, nq, 1);
+                memcpy(q, t2, sizeof(t2));
+                E += 1;
+            }
+        }
+        shl_limbs(limbs, Lout, q, nq, 64 * (int64_t)Lout - prec);
+    }
+    *sign = (uint8_t)v->neg;
+    *exp = E;
+}
+
+/* RNE of v to prec bits as an exact number (for the MPC-like rounded mode) */
+static xn xn_round(const xn *v, int prec) {
+    int L = (prec + 63) / 64;
+    xn r; r.own = 1; r.m = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)L);
+    uint8_t s; int64_t E;
+    xn_store(v, prec, &s, &E, r.m, L);
+    r.n = is_zero_limbs(r.m, L) ? 0 : L;
+    r.neg = r.n ? s : 0;
+    r.e = E - 64 * (int64_t)L;
+    return r;
+}
+
+/* exact sum_v sg[v] * sum_k X[v][k] * Y[v][k]   (Eq. 2) */
+static xn dot_exact(int64_t k, int nv, xn *const *X, xn *const *Y, const int *sg) {
+    int64_t emin = 0, top = 0; int any = 0, maxn = 0;
+    for (int v = 0; v < nv; v++)
+        for (int64_t q = 0; q < k; q++) {
+            const xn *x = &X[v][q], *y = &Y[v][q];
+            if (!x->n || !y->n) continue;
+            int64_t lo = x->e + y->e, hi = lo + 64 * (int64_t)(x->n + y->n);
+            if (!any || lo < emin) emin = lo;
+            if (!any || hi > top) top = hi;
+            if (x->n + y->n > maxn) maxn = x->n + y->n;
+            any = 1;
+        }
+    if (!any) { xn z = {0, 0, 0, NULL, 0}; return z; }
+    int cntbits = 2; while ((1LL << cntbits) < k * nv + 1) cntbits++;
+    int na = (int)((top - emin + cntbits + 2) / 64) + 2;
+    uint64_t *acc = (uint64_t *)calloc((size_t)na, sizeof(uint64_t));
+    uint64_t *prod = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)maxn);
+    for (int v = 0; v < nv; v++)
+        for (int64_t q = 0; q < k; q++) {
+            const xn *x = &X[v][q], *y = &Y[v][q];
+            if (!x->n || !y->n) continue;
+            mulmag(prod, x->m, x->n, y->m, y->n);
+            addsh(acc, na, prod, x->n + y->n, x->e + y->e - emin, x->neg ^ y->neg ^ (sg[v] < 0));
+        }
+    xn r = xn_from_acc(acc, na, emin);
+    free(acc); free(prod);
+    return r;
+}
+
+static int nthreads_of(int32_t req) {
+#ifdef _OPENMP
+    return req > 0 ? req : omp_get_max_threads();
+#else
+    (void)req; return 1;
+#endif
+}
+
+static void out_ptrs(orc_rmat *C, int64_t oi, uint8_t **s, int64_t **e, uint64_t **l) {
+    *s = C->sign + oi; *e = C->exp + oi; *l = C->limbs + oi * C->L;
+}
+
+/* ------------------------------------------------------------------ oracle (1): exact */
+/* form 4: Eq. 3 / Eq. 5 ; form 3: Eq. 4 / Eq. 6.
+ * rounded_prec == 0 : every operation exact, one RNE to prec_out.
+ * rounded_prec  > 0 : MPC-like: the 3M sums ReA+ImA, ReB+ImB, each real GEMM and every
+ *                     combination are rounded to rounded_prec (then output RNE to prec_out).
+ * nsamp < 0 : all m x n outputs at C[i*ld+j];  nsamp >= 0 : outputs (si[t], sj[t]) at C[t]. */
+int orc_cgemm_exact(int64_t m, int64_t n, int64_t k,
+                    const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                    orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t rounded_prec,
+                    int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
+{
+    if (m < 0 || n < 0 || k < 0 || (form != 3 && form != 4) || prec_out < 2) return -1;
+    int64_t total = nsamp < 0 ? m * n : nsamp;
+    int nt = nthreads_of(nthreads);
+    int err = 0;
+    #pragma omp parallel num_threads(nt)
+    {
+        xn *ar = (xn *)malloc(sizeof(xn) * (size_t)(k + 1)), *ai = (xn *)malloc(sizeof(xn) * (size_t)(k + 1));
+        xn *br = (xn *)malloc(sizeof(xn) * (size_t)(k + 1)), *bi = (xn *)malloc(sizeof(xn) * (size_t)(k + 1));
+        xn *as = (xn *)malloc(sizeof(xn) * (size_t)(k + 1)), *bs = (xn *)malloc(sizeof(xn) * (size_t)(k + 1));
+        #pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < total; t++) {
+            int64_t i = nsamp < 0 ? t / (n ? n : 1) : si[t];
+            int64_t j = nsamp < 0 ? t % (n ? n : 1) : sj[t];
+            int64_t oi = nsamp < 0 ? i * Cre->ld + j : t;
+            if (i < 0 || i >= m || j < 0 || j >= n) { err = -1; continue; }
+            for (int64_t q = 0; q < k; q++) {
+                ar[q] = entry_of(Are, i, q); ai[q] = entry_of(Aim, i, q);
+                br[q] = entry_of(Bre, q, j); bi[q] = entry_of(Bim, q, j);
+            }
+            xn re, im;
+            if (form == 4 && !rounded_prec) {
+                /* Eq. 3: Re = sum ReA ReB - ImA ImB ; Im = sum ReA ImB + ImA ReB, exact */
+                xn *X1[2] = {ar, ai}, *Y1[2] = {br, bi}; int s1[2] = {+1, -1};
+                xn *X2[2] = {ar, ai}, *Y2[2] = {bi, br}; int s2[2] = {+1, +1};
+                re = dot_exact(k, 2, X1, Y1, s1);
+                im = dot_exact(k, 2, X2, Y2, s2);
+            } else if (form == 4) {
+                /* Eq. 5 with each real GEMM rounded, then the +/- rounded */
+                int one = 1;
+                xn *P[4]; xn p1, p2, p3, p4;
+                p1 = dot_exact(k, 1, (xn *[]){ar}, (xn *[]){br}, &one);
+                p2 = dot_exact(k, 1, (xn *[]){ai}, (xn *[]){bi}, &one);
+                p3 = dot_exact(k, 1, (xn *[]){ar}, (xn *[]){bi}, &one);
+                p4 = dot_exact(k, 1, (xn *[]){ai}, (xn *[]){br}, &one);
+                P[0] = &p1; P[1] = &p2; P[2] = &p3; P[3] = &p4;
+                xn r[4];
+                for (int q = 0; q < 4; q++) r[q] = xn_round(P[q], rounded_prec);
+                xn t1 = xn_add(&r[0], &r[1], 1), t2 = xn_add(&r[2], &r[3], 0);
+                re = xn_round(&t1, rounded_prec); im = xn_round(&t2, rounded_prec);
+                xn_free(&t1); xn_free(&t2);
+                for (int q = 0; q < 4; q++) { xn_free(&r[q]); xn_free(P[q]); }
+            } else {
+                /* Eq. 4 / Eq. 6: T1 = ReA ReB, T2 = ImA ImB, T3 = (ReA+ImA)(ReB+ImB);
+                   Re = T1 - T2 ; Im = T3 - T1 - T2 */
+                for (int64_t q = 0; q < k; q++) {
+                    as[q] = xn_add(&ar[q], &ai[q], 0);
+                    bs[q] = xn_add(&br[q], &bi[q], 0);
+                    if (rounded_prec) {
+                        xn ra = xn_round(&as[q], rounded_prec), rb = xn_round(&bs[q], rounded_prec);
+                        xn_free(&as[q]); xn_free(&bs[q]); as[q] = ra; bs[q] = rb;
+                    }
+                }
+                int one = 1;
+                xn T1 = dot_exact(k, 1, (xn *[]){ar}, (xn *[]){br}, &one);
+                xn T2 = dot_exact(k, 1, (xn *[]){ai}, (xn *[]){bi}, &one);
+                xn T3 = dot_exact(k, 1, (xn *[]){as}, (xn *[]){bs}, &one);
+                if (rounded_prec) {
+                    xn r1 = xn_round(&T1, rounded_prec), r2 = xn_round(&T2, rounded_prec), r3 = xn_round(&T3, rounded_prec);
+                    xn_free(&T1); xn_free(&T2); xn_free(&T3); T1 = r1; T2 = r2; T3 = r3;
+                }
+                xn d = xn_add(&T1, &T2, 1);
+                xn u = xn_add(&T3, &T1, 1);
+                if (rounded_prec) {
+                    re = xn_round(&d, rounded_prec); xn_free(&d);
+                    xn ur = xn_round(&u, rounded_prec); xn_free(&u);
+                    xn w = xn_add(&ur, &T2, 1); xn_free(&ur);
+                    im = xn_round(&w, rounded_prec); xn_free(&w);
+                } else {
+                    re = d;
+                    im = xn_add(&u, &T2, 1); xn_free(&u);
+                }
+                xn_free(&T1); xn_free(&T2); xn_free(&T3);
+                for (int64_t q = 0; q < k; q++) { xn_free(&as[q]); xn_free(&bs[q]); }
+            }
+            uint8_t *s; int64_t *e; uint64_t *l;
+            out_ptrs(Cre, oi, &s, &e, &l); xn_store(&re, prec_out, s, e, l, Cre->L);
+            out_ptrs(Cim, oi, &s, &e, &l); xn_store(&im, prec_out, s, e, l, Cim->L);
+            xn_free(&re); xn_free(&im);
+        }
+        free(ar); free(ai); free(br); free(bi); free(as); free(bs);
+    }
+    return err;
+}
+
+/* ------------------------------------------------------------------ oracle (2): Ozaki */
+/* mu of Algorithm 2 in exponent form (reading Z3): e = max exponent
+ * over the nonzero entries of row i (A, side 0) or column j (B, side 1), common to Re and
+ * Im (Z10).  Returns 1 if the row/column has a nonzero entry, else 0 (e=0). */
+static int line_exponent(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64_t idx, int64_t len, int64_t *e) {
+    int any = 0; int64_t best = 0;
+    for (int64_t q = 0; q < len; q++) {
+        for (int p = 0; p < 2; p++) {
+            const orc_rmat *M = p ? Pim : Pre;
+            xn v = side == 0 ? entry_of(M, idx, q) : entry_of(M, q, idx);
+            if (!v.n) continue;
+            int64_t ex = v.e + 64 * (int64_t)M->L;
+            if (!any || ex > best) best = ex;
+            any = 1;
+        }
+    }
+    *e = any ? best : 0;
+    return any;
+}
+
+/* fixed-point value (reading Z5): X = sign * floor(|x| * 2^(W - e)), returned as a two's
+ * complement integer in nx limbs.  |x| = N 2^(exp - 64L). */
+static void fixed_point(const xn *x, int64_t e, int64_t W, uint64_t *X, int nx) {
+    memset(X, 0, sizeof(uint64_t) * (size_t)nx);
+    if (!x->n) return;
+    int64_t sh = x->e + W - e;        /* X = floor(N * 2^sh) */
+    if (sh >= 0) shl_limbs(X, nx, x->m, x->n, sh);
+    else shr_limbs(X, nx, x->m, x->n, -sh);
+    if (x->neg) {
+        uint64_t c = 1;
+        for (int i = 0; i < nx; i++) { uint64_t t = ~X[i] + c; c = (c && t == 0); X[i] = t; }
+    }
+}
+
+static void add_tc(uint64_t *r, const uint64_t *a, const uint64_t *b, int n) {
+    uint64_t c = 0;
+    for (int i = 0; i < n; i++) { u128 t = (u128)a[i] + b[i] + c; r[i] = (uint64_t)t; c = (uint64_t)(t >> 64); }
+}
+
+/* the unique balanced radix-256 digits (digit set [-128,127]) of the two's complement
+ * integer X: X = sum_{alpha=1..s} d[alpha-1] 256^(s-alpha).  Slice A_alpha of Algorithm 2
+ * is d[alpha-1] * 2^(e + 3 - 8 alpha).  Returns 0 on success, -1 if X
+ * does not fit s digits. */
+static int balanced_digits(const uint64_t *X, int nx, int s, int8_t *d) {
+    int c = 0;
+    for (int t = 0; t < s; t++) {
+        int byte = (int)((X[t / 8] >> (8 * (t % 8))) & 0xFF);
+        int v = byte + c;
+        int dig = v >= 128 ? v - 256 : v;
+        c = v >= 128;
+        d[s - 1 - t] = (int8_t)dig;
+    }
+    /* the bytes above must be the sign extension cancelled by the final carry */
+    int neg = (int)(X[nx - 1] >> 63);
+    for (int t = s; t < 8 * nx; t++) {
+        int byte = (int)((X[t / 8] >> (8 * (t % 8))) & 0xFF);
+        if (byte != (neg ? 0xFF : 0)) return -1;
+    }
+    return (neg ? (c == 1) : (c == 0)) ? 0 : -1;
+}
+
+/* digit planes of one line (row i of A, or column j of B), parts 0 = Re, 1 = Im,
+ * 2 = Re + Im (exact fixed-point sum, reading Z11).  dig[part][alpha][q] for q < len. */
+static int line_digits(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64_t idx, int64_t len,
+                       int64_t e, int s, int nparts, int8_t *dig) {
+    int64_t W = 8 * (int64_t)s - 3;
+    int nx = (8 * s + 64) / 64 + 1;
+    uint64_t X[3][nx];
+    int8_t d[s];
+    for (int64_t q = 0; q < len; q++) {
+        for (int p = 0; p < 2; p++) {
+            const orc_rmat *M = p ? Pim : Pre;
+            xn v = side == 0 ? entry_of(M, idx, q) : entry_of(M, q, idx);
+            fixed_point(&v, e, W, X[p], nx);
+        }
+        add_tc(X[2], X[0], X[1], nx);
+        for (int p = 0; p < nparts; p++) {
+            if (balanced_digits(X[p], nx, s, d)) return -1;
+            for (int a = 0; a < s; a++) dig[((int64_t)p * s + a) * len + q] = d[a];
+        }
+    }
+    return 0;
+}
+
+/* Algorithm 2's product for one output element and one (A part, B part):
+ * C = sum_{alpha=1..d} sum_{beta=1..d-alpha+1} (A_alpha B_beta)_ij,
+ * accumulated exactly (Z7) as the integer  sum (dA_alpha . dB_beta) 256^(s+1-alpha-beta)
+ * into the two's complement accumulator acc (na limbs, weight 2^(eA+eB+6-8(s+1))). */
+static void ozaki_pair(const int8_t *da, const int8_t *db, int64_t k, int s, uint64_t *acc, int na, int neg) {
+    for (int alpha = 1; alpha <= s; alpha++) {
+        const int8_t *xa = da + (int64_t)(alpha - 1) * k;
+        for (int beta = 1; beta <= s - alpha + 1; beta++) {
+            const int8_t *yb = db + (int64_t)(beta - 1) * k;
+            int64_t dot = 0;                                   /* C_alpha,beta := A_alpha B_beta */
+            for (int64_t q = 0; q < k; q++) dot += (int64_t)xa[q] * (int64_t)yb[q];
+            if (!dot) continue;
+            uint64_t mag = (uint64_t)(dot < 0 ? -dot : dot);
+            addsh(acc, na, &mag, 1, 8 * (int64_t)(s + 1 - alpha - beta), neg ^ (dot < 0));
+        }
+    }
+}
+
+int orc_cgemm_ozaki(int64_t m, int64_t n, int64_t k,
+                    const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                    orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
+                    int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
+{
+    if (m < 0 || n < 0 || k < 0 || (form != 3 && form != 4) || s < 1 || prec_out < 2) return -1;
+    int64_t total = nsamp < 0 ? m * n : nsamp;
+    int nt = nthreads_of(nthreads);
+    int nparts = form == 3 ? 3 : 2;
+    int err = 0;
+    int cnt = 2; while ((1LL << cnt) < 4 * k + 1) cnt++;
+    int na = (8 * s + 14 + cnt + 64) / 64 + 2;
+    #pragma omp parallel num_threads(nt)
+    {
+        int8_t *da = (int8_t *)malloc((size_t)nparts * s * (k ? k : 1));
+        int8_t *db = (int8_t *)malloc((size_t)nparts * s * (k ? k : 1));
+        uint64_t *acc[3];
+        for (int q = 0; q < 3; q++) acc[q] = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)na);
+        #pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < total; t++) {
+            int64_t i = nsamp < 0 ? t / (n ? n : 1) : si[t];
+            int64_t j = nsamp < 0 ? t % (n ? n : 1) : sj[t];
+            int64_t oi = nsamp < 0 ? i * Cre->ld + j : t;
+            if (i < 0 || i >= m || j < 0 || j >= n) { err = -1; continue; }
+            int64_t eA, eB;
+            line_exponent(Are, Aim, 0, i, k, &eA);
+            line_exponent(Bre, Bim, 1, j, k, &eB);
+            if (line_digits(Are, Aim, 0, i, k, eA, s, nparts, da) ||
+                line_digits(Bre, Bim, 1, j, k, eB, s, nparts, db)) { err = -2; continue; }
+            const int64_t pl = (int64_t)s * k;
+            for (int q = 0; q < 3; q++) memset(acc[q], 0, sizeof(uint64_t) * (size_t)na);
+            if (form == 4) {
+                /* Eq. 5: Re = ReA ReB - ImA ImB ; Im = ReA ImB + ImA ReB  (each by Alg. 2) */
+                ozaki_pair(da, db, k, s, acc[0], na, 0);
+                ozaki_pair(da + pl, db + pl, k, s, acc[0], na, 1);
+                ozaki_pair(da, db + pl, k, s, acc[1], na, 0);
+                ozaki_pair(da + pl, db, k, s, acc[1], na, 0);
+            } else {
+                /* Eq. 6: T1 = ReA ReB, T2 = ImA ImB, T3 = (ReA+ImA)(ReB+ImB) (each by Alg. 2);
+                   Re = T1 - T2 ; Im = T3 - T1 - T2 */
+                ozaki_pair(da, db, k, s, acc[0], na, 0);                /* T1 */
+                ozaki_pair(da + pl, db + pl, k, s, acc[1], na, 0);      /* T2 */
+                ozaki_pair(da + 2 * pl, db + 2 * pl, k, s, acc[2], na, 0); /* T3 */
+            }
+            int64_t e0 = eA + eB + 6 - 8 * (int64_t)(s + 1);
+            xn re, im;
+            if (form == 4) {
+                re = xn_from_acc(acc[0], na, e0);
+                im = xn_from_acc(acc[1], na, e0);
+            } else {
+                xn T1 = xn_from_acc(acc[0], na, e0), T2 = xn_from_acc(acc[1], na, e0), T3 = xn_from_acc(acc[2], na, e0);
+                re = xn_add(&T1, &T2, 1);
+                xn u = xn_add(&T3, &T1, 1);
+                im = xn_add(&u, &T2, 1);
+                xn_free(&u); xn_free(&T1); xn_free(&T2); xn_free(&T3);
+            }
+            uint8_t *sg; int64_t *ex; uint64_t *lb;
+            out_ptrs(Cre, oi, &sg, &ex, &lb); xn_store(&re, prec_out, sg, ex, lb, Cre->L);
+            out_ptrs(Cim, oi, &sg, &ex, &lb); xn_store(&im, prec_out, sg, ex, lb, Cim->L);
+            xn_free(&re); xn_free(&im);
+        }
+        free(da); free(db);
+        for (int q = 0; q < 3; q++) free(acc[q]);
+    }
+    return err;
+}
+
+/* exponents eA[m] (rows of A), eB[n] (columns of B) and nonzero flags */
+int orc_exponents(int64_t m, int64_t n, int64_t k,
+                  const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                  int64_t *eA, int64_t *eB, uint8_t *nzA, uint8_t *nzB)
+{
+    for (int64_t i = 0; i < m; i++) nzA[i] = (uint8_t)line_exponent(Are, Aim, 0, i, k, &eA[i]);
+    for (int64_t j = 0; j < n; j++) nzB[j] = (uint8_t)line_exponent(Bre, Bim, 1, j, k, &eB[j]);
+    return 0;
+}
+
+/* digit planes (slices of Algorithm 2 under the readings) of A (side 0: dig[part][alpha][i][q],
+ * q < k) or B (side 1: dig[part][alpha][j][q], i.e. column j of B as a line).  nparts = 2
+ * (Re, Im) or 3 (Re, Im, Re+Im). */
+int orc_split(int side, int64_t rows, int64_t k, const orc_rmat *Pre, const orc_rmat *Pim,
+              int32_t s, int32_t nparts, int8_t *dig)
+{
+    int8_t *tmp = (int8_t *)malloc((size_t)nparts * s * (k ? k : 1));
+    int rc = 0;
+    for (int64_t r = 0; r < rows && !rc; r++) {
+        int64_t e;
+        line_exponent(Pre, Pim, side, r, k, &e);
+        if (line_digits(Pre, Pim, side, r, k, e, s, nparts, tmp)) { rc = -2; break; }
+        for (int p = 0; p < nparts; p++)
+            for (int a = 0; a < s; a++)
+                memcpy(dig + (((int64_t)p * s + a) * rows + r) * k, tmp + ((int64_t)p * s + a) * k, (size_t)k);
+    }
+    free(tmp);
+    return rc;
+}
+
+/* ------------------------------------------------------------------ slice-count rule */
+/* t = floor(max(|Re|,|Im|) * 2^(7 - e)) in [0,127] for one entry */
+static int top7(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64_t idx, int64_t q, int64_t e) {
+    int best = 0;
+    for (int p = 0; p < 2; p++) {
+        const orc_rmat *M = p ? Pim : Pre;
+        xn v = side == 0 ? entry_of(M, idx, q) : entry_of(M, q, idx);
+        if (!v.n) continue;
+        uint64_t X[2];
+        int64_t sh = v.e + 7 - e;
+        if (sh >= 0) shl_limbs(X, 2, v.m, v.n, sh); else shr_limbs(X, 2, v.m, v.n, -sh);
+        int t = (int)X[0];
+        if (X[1] || X[0] > 127) return -1;    /* cannot happen for exp <= e */
+        if (t > best) best = t;
+    }
+    return best;
+}
+
+/* entry exponent for the max-plus bound: max(exp Re, exp Im) over the nonzero parts,
+ * so |a| >= 2^(e-1); returns 0 if the entry is zero */
+static int entry_mpexp(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64_t idx, int64_t q, int64_t *e) {
+    int any = 0;
+    for (int p = 0; p < 2; p++) {
+        const orc_rmat *M = p ? Pim : Pre;
+        xn v = side == 0 ? entry_of(M, idx, q) : entry_of(M, q, idx);
+        if (!v.n) continue;
+        int64_t ex = v.e + 64 * (int64_t)M->L;
+        if (!any || ex > *e) *e = ex;
+        any = 1;
+    }
+    return any;
+}
+
+/* The rho-hat pre-pass.  Over the pairs (i, j) of a nonzero row
+ * of A and a nonzero column of B:
+ *   T_ij  = sum_k t_ik u_kj   (bound 1: rho_ij <= k 2^14 / T_ij when T_ij > 0)
+ *   D_ij  = eA_i + eB_j - max_k (e_ik + e_kj)   over k with a_ik, b_kj both nonzero
+ *           (bound 2: rho_ij <= k 2^(2 + D_ij); no such k <=> (|A||B|)_ij = 0, pair skipped)
+ * out[0] = min_ij T_ij (-1: no pair).  If out[0] == 0 the combined rule needs, with each
+ * pair assigned to bound 2 iff T_ij == 0 or (D_ij < 12 and T_ij 2^D_ij < 2^12):
+ * out[1] = min T_ij over bound-1 pairs (-1: none), out[2] = max D_ij over bound-2 pairs
+ * (-1: none).  When out[0] != 0, out[1] = out[0] and out[2] = -1. */
+int orc_rho_bounds(int64_t m, int64_t n, int64_t k,
+                   const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                   int64_t *out, int32_t nthreads)
+{
+    int64_t *eA = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m + 1)), *eB = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    uint8_t *nzA = (uint8_t *)malloc((size_t)m + 1), *nzB = (uint8_t *)malloc((size_t)n + 1);
+    int32_t *t = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m * k + 1));
+    int32_t *u = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n * k + 1));
+    int64_t *ea = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m * k + 1));
+    int64_t *eb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n * k + 1));
+    uint8_t *za = (uint8_t *)malloc((size_t)(m * k + 1)), *zb = (uint8_t *)malloc((size_t)(n * k + 1));
+    orc_exponents(m, n, k, Are, Aim, Bre, Bim, eA, eB, nzA, nzB);
+    int rc = 0;
+    for (int64_t i = 0; i < m; i++) for (int64_t q = 0; q < k; q++) {
+        int v = top7(Are, Aim, 0, i, q, eA[i]); if (v < 0) rc = -2; t[i * k + q] = v;
+        za[i * k + q] = (uint8_t)entry_mpexp(Are, Aim, 0, i, q, &ea[i * k + q]); }
+    for (int64_t j = 0; j < n; j++) for (int64_t q = 0; q < k; q++) {
+        int v = top7(Bre, Bim, 1, j, q, eB[j]); if (v < 0) rc = -2; u[j * k + q] = v;
+        zb[j * k + q] = (uint8_t)entry_mpexp(Bre, Bim, 1, j, q, &eb[j * k + q]); }
+    int nt = nthreads_of(nthreads);
+    int64_t mn = -1, mn1 = -1, mx2 = -1;
+    #pragma omp parallel num_threads(nt)
+    {
+        int64_t loc = -1, loc1 = -1, loc2 = -1;
+        #pragma omp for schedule(dynamic, 1)
+        for (int64_t i = 0; i < m; i++) {
+            if (!nzA[i]) continue;
+            for (int64_t j = 0; j < n; j++) {
+                if (!nzB[j]) continue;
+                int64_t T = 0, mp = 0; int has = 0;
+                for (int64_t q = 0; q < k; q++) {
+                    T += (int64_t)t[i * k + q] * u[j * k + q];
+                    if (za[i * k + q] && zb[j * k + q]) {
+                        int64_t x = ea[i * k + q] + eb[j * k + q];
+                        if (!has || x > mp) mp = x;
+                        has = 1;
+                    }
+                }
+                if (!has) continue;                     /* (|A||B|)_ij = 0: C_ij = 0 exactly */
+                if (loc < 0 || T < loc) loc = T;
+                int64_t D = eA[i] + eB[j] - mp;
+                int use2 = (T == 0) || (D < 12 && (T << D) < 4096);
+                if (use2) { if (D > loc2) loc2 = D; }
+                else if (loc1 < 0 || T < loc1) loc1 = T;
+            }
+        }
+        #pragma omp critical
+        {
+            if (loc >= 0 && (mn < 0 || loc < mn)) mn = loc;
+            if (loc1 >= 0 && (mn1 < 0 || loc1 < mn1)) mn1 = loc1;
+            if (loc2 > mx2) mx2 = loc2;
+        }
+    }
+    out[0] = mn;
+    if (mn != 0) { out[1] = mn; out[2] = -1; } else { out[1] = mn1; out[2] = mx2; }
+    free(eA); free(eB); free(nzA); free(nzB); free(t); free(u); free(ea); free(eb); free(za); free(zb);
+    return rc;
+}
+
+/* the slice-count rule from the pre-pass integers:
+ *   minT > 0 : log2rho = log2((double)k) + 14.0 - log2((double)minT)
+ *   minT == 0: log2rho = max( log2((double)k) + 14.0 - log2((double)minT1)   [minT1 >= 1],
+ *                             log2((double)k) + 2.0 + (double)maxD2 )          [maxD2 >= 0]
+ *   minT < 0 : log2rho = 0 (the product is identically zero)
+ *   s = min{ s >= 1 : 8.0 s >= prec - 4.0 + log2(c_M s) + log2rho + 0.1 }, c_4M = 3, c_3M = 4 */
+int32_t orc_slices_for(int32_t prec, int32_t form, int64_t k, int64_t minT, int64_t minT1, int64_t maxD2) {
+    double c = form == 3 ? 4.0 : 3.0;
+    double log2rho = 0.0;
+    if (minT > 0) log2rho = log2((double)k) + 14.0 - log2((double)minT);
+    else if (minT == 0) {
+        log2rho = -1e300;
+        if (minT1 >= 1) log2rho = log2((double)k) + 14.0 - log2((double)minT1);
+        if (maxD2 >= 0) { double b2 = log2((double)k) + 2.0 + (double)maxD2; if (b2 > log2rho) log2rho = b2; }
+        if (log2rho < -1e299) log2rho = 0.0;
+    }
+    for (int32_t s = 1; s < 1000000; s++)
+        if (8.0 * s >= (double)prec - 4.0 + log2(c * s) + log2rho + 0.1) return s;
+    return -1;
+}
