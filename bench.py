@@ -1,0 +1,291 @@
+"""Benchmark: complex MP GEMM MACs/s of the Ozaki scheme on B200 (BASELINE.json metric).
+
+A step is one whole hot path (exponent scan, rho-hat pre-pass
+and slice rule, split, tcgen05 slice GEMMs, fold + normalize) over one batch of synthetic
+input: BASELINE config 4, complex 2048^3 at prec 1024 (the configuration the metric is
+quoted on at 1/2/4/8 GPUs), method 3M by default.  Multi-GPU (torchrun): every rank owns a
+2048-row block of a global A (weak scaling), B is replicated, s is agreed by an all-reduce of
+the pre-pass integers (paper_2307_06072_b200/dist.py); no data-path collective.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--method 3M|4M] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  value = total CMACs of all ranks / max-over-ranks device
+time of the K timed steps (CUDA events on the launching stream, barrier + synchronize on
+both sides).  Inputs are larger than L2 (2.3 GB per rank), so no flush is needed.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import mpgen  # noqa: E402
+
+METRIC = "complex MP GEMM MACs/s at prec bits (1/2/4/8 B200); slice-GEMM % tensor peak"
+UNIT = "CMAC/s"
+
+
+def peaks():
+    try:
+        P = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return P, "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_sample(A, B, prec, method, s, target_s=15.0, start=4):
+    """The oracle (Algorithm 2, oracle/mpref.c) as it stands, all host cores, on a bounded
+    sample of output elements of the same workload; returns (CMAC/s, cores, description)."""
+    import oracle
+    cores = os.cpu_count() or 1
+    m, k = A.shape
+    n = B.shape[1]
+    rng = np.random.default_rng(1234)
+    cnt, done, t_all, last = start, 0, 0.0, None
+    while True:
+        si = rng.integers(0, m, cnt)
+        sj = rng.integers(0, n, cnt)
+        t0 = time.perf_counter()
+        oracle.ozaki(A, B, prec, method, s, samples=(si, sj), nthreads=cores)
+        dt = time.perf_counter() - t0
+        done += cnt; t_all += dt; last = dt
+        if t_all >= target_s or cnt > 100000:
+            break
+        cnt = max(cnt, int(cnt * min(8.0, max(1.5, (target_s - t_all) / max(dt, 1e-3)))))
+        if t_all + last * (cnt / max(done, 1)) > 3 * target_s:
+            cnt = max(1, int(done * (target_s - t_all) / max(t_all, 1e-3)))
+            if cnt <= 0:
+                break
+    return done * k / t_all, cores, f"{done} sampled output elements (x k={k} CMACs each) in {t_all:.1f} s"
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands on the box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    c = mpgen.CONFIGS[args.config]
+    A, B = mpgen.config_inputs(args.config, seed=0)
+    import oracle
+    s, _ = oracle.auto_slices(A, B, c["prec"], args.method)           # the full slice rule
+    cores = os.cpu_count() or 1
+    per_step = max(cores, 8)
+    rng = np.random.default_rng(99)
+    times = []
+    for it in range(args.warmup + args.steps):
+        si, sj = rng.integers(0, c["m"], per_step), rng.integers(0, c["n"], per_step)
+        t0 = time.perf_counter()
+        oracle.ozaki(A, B, c["prec"], args.method, s, samples=(si, sj), nthreads=cores)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = args.steps * per_step * c["k"] / tot
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/u64",
+            "data": "synthetic", "config": workload_config(args, s),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} sampled output elements per step (x k={c['k']} CMACs), Algorithm-2 oracle"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, s):
+    c = mpgen.CONFIGS[args.config]
+    return {"workload": f"BASELINE config {args.config}: " + c["desc"], "method": args.method, "m_per_rank": c["m"],
+            "n": c["n"], "k": c["k"], "prec": c["prec"], "slices": s, "seed": 0,
+            "l2": "inputs larger than L2 (no flush needed)", "parallelism": f"rows x{args.gpus} (weak)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--method", default="3M", choices=["3M", "4M"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2307_06072_b200 as P
+    from paper_2307_06072_b200 import dist as pdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    c = mpgen.CONFIGS[args.config]
+    m, n, k, prec = c["m"], c["n"], c["k"], c["prec"]
+    # weak scaling: rank r owns rows [r m, (r+1) m) of a global (world m) x k matrix A
+    A, B = mpgen.config_inputs(args.config, seed=0, row0=rank * m, rows=m)
+    dA, dB = P.to_device(A, dev), P.to_device(B, dev)
+    dC = P.empty_device(m, n, prec, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(timing=0):
+        if world > 1:
+            s, _ = pdist.common_slices(lambda full: P.mpcgemm_rho_bounds(dA, dB, prec, full, stream=stream),
+                                       P.mpcgemm_slices_for, prec, args.method, k, device=dev)
+            return P.mpcgemm_ex(dA, dB, dC, prec, args.method, slices=s, stream=stream, timing=timing)
+        return P.mpcgemm_ex(dA, dB, dC, prec, args.method, stream=stream, timing=timing)
+
+    for _ in range(args.warmup):
+        rep = step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        reps.append(step(timing=1))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    s = reps[-1]["slices"]
+    cmacs = world * m * n * k
+    value = cmacs / (ms / 1e3)
+
+    # roofline of the dominant kernel (the tcgen05 slice GEMM), timed live with CUDA events
+    # on the launching stream inside the library (opts.timing) over the timed steps
+    R = 3 if args.method == "3M" else 4
+    pairs = s * (s + 1) // 2
+    ops = 2.0 * R * pairs * m * n * k                   # algorithmic INT8 ops per launch
+    gemm_ms = statistics.mean(r["ms_gemm"] for r in reps)
+    pk, src = peaks()
+    peak_int8 = 2.0 * pk["bf16_tflops_sustained"]       # measured bf16 sustained x nominal int8/bf16 = 2
+    achieved = ops / (gemm_ms / 1e3) / 1e12
+    stage_ms = {f: round(statistics.mean(r[f] for r in reps), 3) for f in
+                ("ms_linemax", "ms_prepass", "ms_split", "ms_gemm", "ms_fold")}
+    hbm = pk["hbm_gbs"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/u64",
+        "data": "synthetic", "config": workload_config(args, s),
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak_int8, 1), "unit": "TOP/s",
+                     "frac": round(achieved / peak_int8, 4), "traffic": None,
+                     "kernel": "slicegemm_tc_kernel (tcgen05.mma kind::i8)",
+                     "peak_source": f"{src}: 2 x bf16_tflops_sustained (nominal int8/bf16 = 2)",
+                     "algorithmic": f"2 R P m n k = 2*{R}*{pairs}*{m}*{n}*{k} int8 ops per launch"},
+        "stages_ms": stage_ms,
+        "gpu_launches": int(sum(r["kernel_launches"] for r in reps)),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_e2e:
+        line["e2e"] = e2e_measure(P, A, B, prec, args)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, desc = cpu_oracle_sample(A, B, prec, args.method, s, target_s=args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_measure(P, A, B, prec, args):
+    """Same metric through the C ABI on HOST buffers (pinned), H2D + D2H inside the timed call."""
+    import torch
+
+    def pinned(R):
+        out = []
+        for a in (R.sign, R.exp, R.limbs):
+            t = torch.empty(a.shape, dtype={np.uint8: torch.uint8, np.int64: torch.int64, np.uint64: torch.int64}[a.dtype.type],
+                            pin_memory=True)
+            v = t.numpy().view(a.dtype)
+            v[...] = a
+            out.append(v)
+        return mpgen.RMat(out[0], out[1], out[2], R.prec)
+
+    hA = mpgen.CMat(pinned(A.re), pinned(A.im))
+    hB = mpgen.CMat(pinned(B.re), pinned(B.im))
+    m, k = A.shape
+    n = B.shape[1]
+    hC = mpgen.CMat(pinned(mpgen.empty_rmat(m, n, prec)), pinned(mpgen.empty_rmat(m, n, prec)))
+    P.mpcgemm_host(hA, hB, prec, args.method, C=hC)          # warm-up (staging allocation)
+    ts = []
+    for _ in range(max(2, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        P.mpcgemm_host(hA, hB, prec, args.method, C=hC)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    ent = lambda R: R.sign.nbytes + R.exp.nbytes + R.limbs.nbytes
+    return {"value": m * n * k / t, "unit": UNIT, "h2d_bytes_per_step": ent(A.re) + ent(A.im) + ent(B.re) + ent(B.im),
+            "d2h_bytes_per_step": 2 * (m * n * (9 + 8 * ((prec + 63) // 64))), "ms_per_step": 1e3 * t,
+            "api": "mpcgemm_host (C ABI, pinned host buffers)"}
+
+
+if __name__ == "__main__":
+    main()

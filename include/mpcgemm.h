@@ -74,6 +74,9 @@ typedef struct {
     int32_t  validate;        /* 1 = check normalization / exponent range on device first      */
     void    *workspace;       /* NULL = library-managed per-device cache                       */
     size_t   workspace_bytes; /* size of caller workspace (>= mpcgemm_workspace_size)          */
+    int32_t  timing;          /* 1 = time each stage with CUDA events on opts->stream (the call
+                                 then synchronizes the stream before returning)              */
+    int32_t  reserved;
 } mpcgemm_opts;
 
 typedef struct {
@@ -83,6 +86,9 @@ typedef struct {
     double  log2_rho_hat;     /* the rule's log2 rho-hat                                       */
     int64_t mma_instructions; /* tcgen05.mma count issued by the slice GEMM (K=32 each)         */
     int64_t work_units;       /* slice-GEMM work units (tile, diagonal, chunk, product)         */
+    int32_t kernel_launches;  /* kernels this call launched (memsets/copies excluded)           */
+    int32_t slicegemm_ctas;   /* grid of the slice-GEMM launch                                 */
+    float   ms_linemax, ms_prepass, ms_split, ms_gemm, ms_fold;   /* opts->timing only         */
 } mpcgemm_report;
 
 /* C := A B (auto slice count).  Device pointers.  m, n, k >= 0 (empty: nothing written for

@@ -1,0 +1,169 @@
+// common.cuh -- shared declarations of the sm_100a CUDA path (no oracle code here).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define MPC_DEV __device__ __forceinline__
+
+namespace mpc {
+
+constexpr int kMaxSlices = 1024;     // s limit (prec <= 4096 plus exponent spread)
+constexpr int kMaxJobs = 3;          // 3M: T1,T2,T3 ; 4M: T1,T2,T34
+constexpr int kMaxPairs = 2;         // operand pairs concatenated into one job (4M T34)
+// INT32 exactness of one accumulation chunk: |d_p d_q| <= 2^14, so K' <= 131071 products;
+// in k-blocks of 128: 1023 blocks = 130944 products.
+constexpr int kMaxKBlocksPerChunk = 1023;
+constexpr int kBK = 128;             // k-block: 128 int8 = one 128-byte swizzle row
+
+// Device view of one real MP matrix in the ABI format (include/mpcgemm.h).
+struct DMat {
+    const uint8_t *sign;
+    const int64_t *exp;
+    const uint64_t *limbs;
+    int64_t ld;
+};
+
+struct DMatOut {
+    uint8_t *sign;
+    int64_t *exp;
+    uint64_t *limbs;
+    int64_t ld;
+};
+
+// One slice-GEMM work unit: output tile (tm, tn) of job `job`, anti-diagonal r, and the
+// k-block range [g0, g1) of the job's concatenated sequence (pair, p, kb); the int32
+// result goes to partial plane `slot`.
+struct WorkUnit {
+    int32_t job, tm, tn, r, g0, g1, slot, pad;
+};
+
+struct JobDesc {
+    int32_t npairs;
+    int32_t pa[kMaxPairs];   // A-side digit part of each pair (0 Re, 1 Im, 2 Re+Im)
+    int32_t pb[kMaxPairs];   // B-side digit part
+};
+
+struct GemmParams {
+    const WorkUnit *units;     // in per-CTA order
+    const int32_t *cta_begin;  // [grid+1] offsets into units
+    int32_t *partials;         // [nslots][m][ldD]
+    int64_t ldD;               // partial row pitch (entries)
+    int64_t plane;             // m * ldD
+    int32_t m, n;
+    int32_t s;                 // slices
+    int32_t KB;                // k-blocks per digit plane row
+    int32_t partsA, partsB;    // number of digit parts stored per side
+    JobDesc jobs[kMaxJobs];
+};
+
+MPC_DEV uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------- mbarrier
+MPC_DEV void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+MPC_DEV void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+MPC_DEV void mbar_arrive(uint64_t *bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+MPC_DEV void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+MPC_DEV bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// Waits for the phase with the given parity; traps after ~20 s so that a pipeline bug ends
+// the kernel with an error instead of hanging the GPU.
+MPC_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, parity)) {
+        if (clock64() - t0 > 40000000000ll) __trap();
+    }
+}
+
+// ---------------------------------------------------------------- TMA
+MPC_DEV void tma_prefetch(const void *tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+MPC_DEV void tma_load_3d(void *dst, const void *tmap, uint64_t *bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+// ---------------------------------------------------------------- tcgen05
+MPC_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+MPC_DEV void tc_fence_after()  { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <int NCOLS>
+MPC_DEV void tmem_alloc(uint32_t *dst_smem) {   // whole warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(dst_smem)), "n"(NCOLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int NCOLS>
+MPC_DEV void tmem_dealloc(uint32_t taddr) {     // whole warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, signed int8 -> int32, K = 32
+MPC_DEV void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+MPC_DEV void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit: thread t of the warp gets row (lane base + t), 32 cols
+MPC_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr) : "memory");
+}
+MPC_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): K-major operand tile of
+// rows x 128 bytes written by TMA with 128-byte swizzle; 8-row core groups 1024 B apart.
+//   bits  0-13 start address >> 4     bits 16-29 leading byte offset >> 4 (unused: 1)
+//   bits 32-45 stride byte offset >> 4 (1024 B)   bits 46-47 version = 1 (sm_100)
+//   bits 49-51 base offset = 0        bits 61-63 layout = 2 (SWIZZLE_128B)
+MPC_DEV uint64_t make_sw128_desc(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+// Instruction descriptor, kind::i8: D = S32 (bits 4-5 = 2), A and B signed 8-bit
+// (bits 7-9 = 1, 10-12 = 1), both K-major (bits 15, 16 = 0), N >> 3 at 17-22, M >> 4 at 24-28.
+__host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+}  // namespace mpc

@@ -1,0 +1,54 @@
+// kernels.h -- launchers of the sm_100a kernels (internal; the C ABI is include/mpcgemm.h)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace mpc {
+
+struct SliceGemmLaunch {
+    GemmParams P;
+    const int8_t *digA, *digB;   // [partsA*s][rowsA][kp], [partsB*s][rowsB][kp]
+    int64_t rowsA, rowsB, kp;
+    int grid;                    // CTAs (tcgen05 path)
+    int BN;                      // 128 or 256
+    int simt;                    // 1: dp4a cross-check kernel
+    int nunits;
+    const WorkUnit *units_flat;
+};
+cudaError_t slicegemm_launch(const SliceGemmLaunch &L, cudaStream_t st);
+
+// a-1: per-line max exponent over nonzero entries of (re, im); side 0 = rows, 1 = columns
+cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, int prec, int side,
+                           int64_t *eline, uint8_t *nz, uint32_t *errflag, int validate, cudaStream_t st);
+
+// a-3: balanced radix-256 digit planes dig[part][alpha][lines][kp]
+cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
+                         const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st);
+
+// a-2: pre-pass planes: t[lines][kp] int8 and relative entry exponents rel[lines][kp] int32
+cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
+                                  const int64_t *eline, int8_t *t, int32_t *rel, cudaStream_t st);
+
+// a-2: stage 1 (out[0] = min T over nonzero line pairs) and stage 2 (minT_sup, minT1, maxD2)
+cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t plane, int64_t ldD,
+                                  int64_t m, int64_t n, int64_t k, int64_t kp,
+                                  const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA, const int32_t *relB,
+                                  int stage, unsigned long long *out_min, unsigned long long *out_min1,
+                                  long long *out_max2, cudaStream_t st);
+
+struct FoldParams {
+    const int32_t *partials;
+    int64_t plane, ldD;
+    int64_t m, n;
+    int32_t s, method, prec, L;
+    const int32_t *slotinfo;     // [(job*(s+2) + r)*2 + {0 base, 1 count}]
+    const int64_t *eA, *eB;
+    DMatOut Cre, Cim;
+};
+// a-5 + a-6: exact fold (chunk sums, Eq. 5/6 combination, carry) and RNE normalization
+cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st);
+
+cudaError_t zero_output_launch(DMatOut C, int64_t m, int64_t n, int L, cudaStream_t st);
+
+}  // namespace mpc

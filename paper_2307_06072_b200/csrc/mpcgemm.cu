@@ -1,0 +1,639 @@
+// mpcgemm.cu -- host orchestration and the C ABI (include/mpcgemm.h).
+//
+// One call = the whole hot path of SURVEY.md 8(a), stream-ordered:
+//   a-1 linemax (eA, eB)  ->  [a-2 pre-pass: t/u planes, T = t u on the tensor cores,
+//   min-reduce, 24-byte readback, optional exact max-plus stage, slice rule]  ->
+//   a-3 split (digit planes)  ->  a-4 slice GEMMs (tcgen05 INT8)  ->  a-5/a-6 fold+normalize
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mpcgemm.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace mpc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *what, cudaError_t e = cudaSuccess) {
+    g_last_error = what;
+    if (e != cudaSuccess) { g_last_error += ": "; g_last_error += cudaGetErrorString(e); }
+    return code;
+}
+
+#define CK(expr)                                                         \
+    do {                                                                 \
+        cudaError_t e_ = (expr);                                         \
+        if (e_ != cudaSuccess) return fail(MPCGEMM_ERR_CUDA, #expr, e_); \
+    } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- workspace cache
+struct DevCache {
+    void *ws = nullptr; size_t ws_bytes = 0;
+    void *meta = nullptr; size_t meta_bytes = 0;
+    void *stage = nullptr; size_t stage_bytes = 0;   // mpcgemm_host device staging
+};
+std::mutex g_mu;
+std::map<int, DevCache> g_cache;
+
+int grow(void **p, size_t *have, size_t need) {
+    if (*have >= need) return 0;
+    if (*p) { cudaDeviceSynchronize(); cudaFree(*p); *p = nullptr; *have = 0; }
+    size_t sz = align_up(need + (need >> 3), 1 << 20);
+    cudaError_t e = cudaMalloc(p, sz);
+    if (e != cudaSuccess) { *p = nullptr; cudaGetLastError(); return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc workspace", e); }
+    *have = sz;
+    return 0;
+}
+
+// per-device stage events for opts->timing
+struct StageEvents {
+    cudaEvent_t ev[6] = {};
+    bool ok = false;
+};
+std::map<int, StageEvents> g_events;
+
+StageEvents *stage_events(int dev) {
+    StageEvents &E = g_events[dev];
+    if (!E.ok) {
+        for (auto &e : E.ev) if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        E.ok = true;
+    }
+    return &E;
+}
+
+// ---------------------------------------------------------------- plans (work lists)
+struct PlanKey {
+    int64_t m, n, k; int s, method, BN, grid, simt, maxkb;
+    bool operator<(const PlanKey &o) const {
+        return std::tie(m, n, k, s, method, BN, grid, simt, maxkb) <
+               std::tie(o.m, o.n, o.k, o.s, o.method, o.BN, o.grid, o.simt, o.maxkb);
+    }
+};
+struct Plan {
+    WorkUnit *d_units = nullptr;
+    int32_t *d_cta_begin = nullptr;
+    int32_t *d_slotinfo = nullptr;
+    int nunits = 0, nslots = 0, grid = 0;
+    int64_t mma = 0;
+    JobDesc jobs[kMaxJobs];
+    int njobs = 0, partsA = 0, partsB = 0;
+};
+std::map<std::pair<int, PlanKey>, Plan> g_plans;
+
+void method_jobs(int method, Plan &P) {
+    for (auto &j : P.jobs) { j.npairs = 0; j.pa[0] = j.pa[1] = j.pb[0] = j.pb[1] = 0; }
+    if (method == 3) {   // Eq. 6: T1 = ReA ReB, T2 = ImA ImB, T3 = (ReA+ImA)(ReB+ImB)
+        P.njobs = 3; P.partsA = P.partsB = 3;
+        for (int q = 0; q < 3; q++) { P.jobs[q].npairs = 1; P.jobs[q].pa[0] = q; P.jobs[q].pb[0] = q; }
+    } else if (method == 4) {   // Eq. 5: T1 = ReA ReB, T2 = ImA ImB, T34 = ReA ImB + ImA ReB
+        P.njobs = 3; P.partsA = P.partsB = 2;
+        P.jobs[0].npairs = 1; P.jobs[0].pa[0] = 0; P.jobs[0].pb[0] = 0;
+        P.jobs[1].npairs = 1; P.jobs[1].pa[0] = 1; P.jobs[1].pb[0] = 1;
+        P.jobs[2].npairs = 2; P.jobs[2].pa[0] = 0; P.jobs[2].pb[0] = 1; P.jobs[2].pa[1] = 1; P.jobs[2].pb[1] = 0;
+    } else {             // pre-pass: one job, one pair (t, u), r = 2 only
+        P.njobs = 1; P.partsA = P.partsB = 1;
+        P.jobs[0].npairs = 1;
+    }
+}
+
+// Builds the unit list: for each job q and anti-diagonal r the concatenated k-block sequence
+// (pair, p, kb) of length G = npairs (r-1) KB is cut into ceil(G / maxkb) chunks (INT32
+// exactness), each chunk x output tile is one unit with its own partial plane.
+// Units are assigned to CTAs longest-first to the least-loaded CTA (LPT).
+int build_plan(int dev, const PlanKey &key, Plan **out) {
+    auto it = g_plans.find({dev, key});
+    if (it != g_plans.end()) { *out = &it->second; return 0; }
+    Plan P;
+    method_jobs(key.method, P);
+    const int s = key.s;
+    const int64_t KB = (key.k + kBK - 1) / kBK;
+    const int64_t tiles_m = (key.m + 127) / 128, tiles_n = (key.n + key.BN - 1) / key.BN;
+    const int rmin = 2, rmax = key.method == 0 ? 2 : s + 1;
+    std::vector<int32_t> slotinfo((size_t)kMaxJobs * (s + 2) * 2, 0);
+    std::vector<WorkUnit> units;
+    int nslots = 0;
+    for (int q = 0; q < P.njobs; q++) {
+        for (int r = rmin; r <= rmax; r++) {
+            const int64_t G = (int64_t)P.jobs[q].npairs * (r - 1) * KB;
+            const int64_t nch = (G + key.maxkb - 1) / key.maxkb;
+            slotinfo[(q * (s + 2) + r) * 2] = nslots;
+            slotinfo[(q * (s + 2) + r) * 2 + 1] = (int32_t)nch;
+            for (int64_t c = 0; c < nch; c++) {
+                const int32_t g0 = (int32_t)(c * G / nch), g1 = (int32_t)((c + 1) * G / nch);
+                for (int64_t tm = 0; tm < tiles_m; tm++)
+                    for (int64_t tn = 0; tn < tiles_n; tn++) {
+                        WorkUnit w;
+                        w.job = q; w.tm = (int32_t)tm; w.tn = (int32_t)tn; w.r = r;
+                        w.g0 = g0; w.g1 = g1; w.slot = nslots + (int32_t)c; w.pad = 0;
+                        units.push_back(w);
+                        P.mma += (int64_t)(g1 - g0) * (kBK / 32);
+                    }
+            }
+            nslots += (int)nch;
+        }
+    }
+    // LPT: longest first; stable so equal-work units keep (job, r, chunk, tile) order
+    std::vector<int> order(units.size());
+    for (size_t i = 0; i < order.size(); i++) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return (units[a].g1 - units[a].g0) > (units[b].g1 - units[b].g0);
+    });
+    const int grid = (int)std::min<int64_t>(key.grid, (int64_t)units.size());
+    std::vector<std::vector<int>> per(grid > 0 ? grid : 1);
+    using Item = std::pair<int64_t, int>;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+    for (int c = 0; c < grid; c++) heap.push({0, c});
+    for (int idx : order) {
+        Item it2 = heap.top(); heap.pop();
+        per[it2.second].push_back(idx);
+        // per-unit cost: MMA k-blocks plus a fixed epilogue / fill overhead (~4 k-blocks)
+        heap.push({it2.first + (units[idx].g1 - units[idx].g0) + 4, it2.second});
+    }
+    std::vector<WorkUnit> flat;
+    std::vector<int32_t> begin(grid + 1, 0);
+    flat.reserve(units.size());
+    for (int c = 0; c < grid; c++) {
+        begin[c] = (int32_t)flat.size();
+        for (int idx : per[c]) flat.push_back(units[idx]);
+    }
+    begin[grid] = (int32_t)flat.size();
+    P.nunits = (int)flat.size(); P.nslots = nslots; P.grid = grid;
+    if (P.nunits) {
+        if (cudaMalloc(&P.d_units, sizeof(WorkUnit) * flat.size()) != cudaSuccess ||
+            cudaMalloc(&P.d_cta_begin, sizeof(int32_t) * begin.size()) != cudaSuccess ||
+            cudaMalloc(&P.d_slotinfo, sizeof(int32_t) * slotinfo.size()) != cudaSuccess)
+            return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc plan");
+        CK(cudaMemcpy(P.d_units, flat.data(), sizeof(WorkUnit) * flat.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(P.d_cta_begin, begin.data(), sizeof(int32_t) * begin.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(P.d_slotinfo, slotinfo.data(), sizeof(int32_t) * slotinfo.size(), cudaMemcpyHostToDevice));
+    }
+    auto res = g_plans.emplace(std::make_pair(dev, key), P);
+    *out = &res.first->second;
+    return 0;
+}
+
+int sm_count(int dev) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+}
+
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
+    const char *x = (const char *)a, *y = (const char *)b;
+    return x < y + nb && y < x + na;
+}
+
+size_t mat_span(const mpc_rmat &M, int64_t rows, int64_t cols, int L, int which) {
+    if (rows == 0 || cols == 0) return 0;
+    const size_t ents = (size_t)((rows - 1) * M.ld + cols);
+    return which == 0 ? ents : which == 1 ? ents * 8 : ents * 8 * (size_t)L;
+}
+
+int check_args(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
+               const mpc_cmat *C, int method) {
+    if (!A || !B || !C) return fail(MPCGEMM_ERR_ARG, "null matrix descriptor");
+    if (m < 0 || n < 0 || k < 0) return fail(MPCGEMM_ERR_ARG, "negative dimension");
+    if (method != MPCGEMM_3M && method != MPCGEMM_4M) return fail(MPCGEMM_ERR_ARG, "method must be 3 or 4");
+    if (prec < 2 || prec > 4096) return fail(MPCGEMM_ERR_PREC, "prec outside [2, 4096]");
+    if (m > INT32_MAX / 2 || n > INT32_MAX / 2 || k > INT32_MAX / 2) return fail(MPCGEMM_ERR_ARG, "dimension too large");
+    const mpc_rmat *mats[6] = {&A->re, &A->im, &B->re, &B->im, &C->re, &C->im};
+    const int64_t cols[6] = {k, k, n, n, n, n};
+    const int64_t rows[6] = {m, m, k, k, m, m};
+    for (int q = 0; q < 6; q++) {
+        if (rows[q] == 0 || cols[q] == 0) continue;
+        if (!mats[q]->sign || !mats[q]->exp || !mats[q]->limbs) return fail(MPCGEMM_ERR_ARG, "null array");
+        if (mats[q]->ld < cols[q]) return fail(MPCGEMM_ERR_ARG, "ld < cols");
+    }
+    const int L = (prec + 63) / 64;
+    for (int c = 4; c < 6; c++)
+        for (int q = 0; q < 4; q++)
+            for (int w = 0; w < 3; w++)
+                for (int w2 = 0; w2 < 3; w2++) {
+                    const void *pc = w == 0 ? (const void *)mats[c]->sign : w == 1 ? (const void *)mats[c]->exp : (const void *)mats[c]->limbs;
+                    const void *pq = w2 == 0 ? (const void *)mats[q]->sign : w2 == 1 ? (const void *)mats[q]->exp : (const void *)mats[q]->limbs;
+                    if (overlaps(pc, mat_span(*mats[c], rows[c], cols[c], L, w), pq, mat_span(*mats[q], rows[q], cols[q], L, w2)))
+                        return fail(MPCGEMM_ERR_ALIAS, "C overlaps A or B");
+                }
+    return 0;
+}
+
+DMat dm(const mpc_rmat &M) { return DMat{M.sign, M.exp, M.limbs, M.ld}; }
+DMatOut dmo(const mpc_rmat &M) { return DMatOut{M.sign, M.exp, M.limbs, M.ld}; }
+
+// workspace layout of one call
+struct Layout {
+    size_t meta;      // eA, eB, nz, flags, prepass outputs
+    size_t pre;       // pre-pass planes + T partials
+    size_t main;      // digit planes + partials
+    int64_t kp, ldD;
+};
+
+int tile_bn(int64_t n) { return n > 128 ? 256 : 128; }
+
+int64_t chunk_kb(int64_t m, int64_t n, int64_t k, int s, int method, int BN, int grid) {
+    // INT32 exactness cap; smaller chunks when there are too few units to fill the GPU
+    const int64_t KB = (k + kBK - 1) / kBK;
+    const int64_t tiles = ((m + 127) / 128) * ((n + BN - 1) / BN);
+    const int64_t npairs_total = method == 0 ? 1 : (method == 3 ? 3 : 4);
+    const int64_t work = npairs_total * KB * (int64_t)s * (s + 1) / 2 * tiles;   // k-blocks
+    int64_t target = work / (4 * (int64_t)grid);         // ~4 units per CTA minimum
+    int64_t cap = kMaxKBlocksPerChunk;
+    int e = env_int("MPCGEMM_MAXKB", 0);
+    if (e > 0) cap = std::min<int64_t>(cap, e);
+    if (target < 8) target = 8;
+    return std::max<int64_t>(1, std::min<int64_t>(cap, target));
+}
+
+struct Geometry { int BN, grid, maxkb; };
+
+Geometry main_geometry(int dev, int64_t m, int64_t n, int64_t k, int s, int method) {
+    Geometry g;
+    g.BN = env_int("MPCGEMM_BN", tile_bn(n));
+    if (g.BN != 128 && g.BN != 256) g.BN = tile_bn(n);
+    g.grid = sm_count(dev);
+    g.maxkb = (int)chunk_kb(m, n, k, s, method, g.BN, g.grid);
+    return g;
+}
+
+int64_t count_slots(int64_t k, int s, int method, int maxkb) {
+    const int64_t KB = (k + kBK - 1) / kBK;
+    int64_t nslots = 0;
+    for (int r = 2; r <= s + 1; r++)
+        for (int q = 0; q < 3; q++) {
+            const int64_t np = (method == 4 && q == 2) ? 2 : 1;
+            nslots += (np * (r - 1) * KB + maxkb - 1) / maxkb;
+        }
+    return nslots;
+}
+
+Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb) {
+    Layout Lo;
+    Lo.kp = align_up((size_t)std::max<int64_t>(k, 1), 16);
+    Lo.ldD = align_up((size_t)std::max<int64_t>(n, 1), 4);
+    Lo.meta = align_up(8 * (m + n) + (m + n) + 64, 256) + 256;
+    const int64_t KB = (k + kBK - 1) / kBK;
+    const int64_t nslotsT = (KB + kMaxKBlocksPerChunk - 1) / kMaxKBlocksPerChunk;
+    Lo.pre = align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256) +
+             align_up((size_t)nslotsT * m * Lo.ldD * 4, 256);
+    Lo.main = 0;
+    if (s > 0) {
+        const int parts = method == 3 ? 3 : 2;
+        const int64_t nslots = count_slots(k, s, method, maxkb);
+        Lo.main = align_up((size_t)parts * s * m * Lo.kp, 256) + align_up((size_t)parts * s * n * Lo.kp, 256) +
+                  align_up((size_t)nslots * m * Lo.ldD * 4, 256);
+    }
+    return Lo;
+}
+
+// prepass on device pointers; fills out[3] (synchronizes the stream)
+int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
+                int full, cudaStream_t st, uint8_t *meta, uint8_t *pre, const Layout &Lo, int simt, int64_t out[3]) {
+    const int L = (prec + 63) / 64;
+    int64_t *eA = (int64_t *)meta, *eB = eA + m;
+    uint8_t *nzA = (uint8_t *)(eB + n), *nzB = nzA + m;
+    uint8_t *flags = meta + align_up(8 * (m + n) + (m + n) + 64, 256);
+    unsigned long long *omin = (unsigned long long *)flags;
+    unsigned long long *omin1 = omin + 1;
+    long long *omax2 = (long long *)(omin + 2);
+    int8_t *tA = (int8_t *)pre, *tB = tA + m * Lo.kp;
+    int32_t *relA = (int32_t *)(pre + align_up((size_t)(m + n) * Lo.kp, 256)), *relB = relA + m * Lo.kp;
+    int32_t *T = (int32_t *)(pre + align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256));
+    CK(prepass_planes_launch(dm(A->re), dm(A->im), 0, m, k, Lo.kp, L, eA, tA, relA, st));
+    CK(prepass_planes_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, tB, relB, st));
+    const int BN = tile_bn(n);
+    const int grid = sm_count(dev);
+    PlanKey key{m, n, k, 1, 0, BN, grid, simt, (int)kMaxKBlocksPerChunk};
+    Plan *plan;
+    if (int rc = build_plan(dev, key, &plan)) return rc;
+    SliceGemmLaunch SL;
+    memset(&SL, 0, sizeof(SL));
+    SL.P.units = plan->d_units; SL.P.cta_begin = plan->d_cta_begin;
+    SL.P.partials = T; SL.P.ldD = Lo.ldD; SL.P.plane = m * Lo.ldD;
+    SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = 1; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
+    SL.P.partsA = SL.P.partsB = 1;
+    for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
+    SL.digA = tA; SL.digB = tB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
+    SL.grid = plan->grid; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits; SL.units_flat = plan->d_units;
+    CK(slicegemm_launch(SL, st));
+    unsigned long long init[3] = {~0ull, ~0ull, (unsigned long long)-1ll};
+    CK(cudaMemcpyAsync(omin, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    CK(prepass_reduce_launch(T, plan->nslots, m * Lo.ldD, Lo.ldD, m, n, k, Lo.kp, nzA, nzB, relA, relB, 1,
+                             omin, omin1, omax2, st));
+    unsigned long long h[3];
+    CK(cudaMemcpyAsync(h, omin, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t minraw = h[0] == ~0ull ? -1 : (int64_t)h[0];
+    if (minraw > 0 && !full) { out[0] = minraw; out[1] = minraw; out[2] = -1; return 0; }
+    if (minraw < 0) { out[0] = -1; out[1] = -1; out[2] = -1; return 0; }
+    CK(cudaMemcpyAsync(omin, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    CK(prepass_reduce_launch(T, plan->nslots, m * Lo.ldD, Lo.ldD, m, n, k, Lo.kp, nzA, nzB, relA, relB, 2,
+                             omin, omin1, omax2, st));
+    CK(cudaMemcpyAsync(h, omin, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t mn = h[0] == ~0ull ? -1 : (int64_t)h[0];
+    const int64_t mn1 = h[1] == ~0ull ? -1 : (int64_t)h[1];
+    const int64_t mx2 = (int64_t)h[2];
+    if (full) { out[0] = mn; out[1] = mn1; out[2] = mx2; }
+    else if (mn != 0) { out[0] = mn; out[1] = mn; out[2] = -1; }
+    else { out[0] = mn; out[1] = mn1; out[2] = mx2; }
+    return 0;
+}
+
+double rule_log2rho(int64_t k, int64_t minT, int64_t minT1, int64_t maxD2) {
+    double log2rho = 0.0;
+    if (minT > 0) log2rho = log2((double)k) + 14.0 - log2((double)minT);
+    else if (minT == 0) {
+        log2rho = -1e300;
+        if (minT1 >= 1) log2rho = log2((double)k) + 14.0 - log2((double)minT1);
+        if (maxD2 >= 0) { double b2 = log2((double)k) + 2.0 + (double)maxD2; if (b2 > log2rho) log2rho = b2; }
+        if (log2rho < -1e299) log2rho = 0.0;
+    }
+    return log2rho;
+}
+
+int rule_slices(int32_t prec, int method, double log2rho) {
+    const double c = method == 3 ? 4.0 : 3.0;
+    for (int s = 1; s <= kMaxSlices; s++)
+        if (8.0 * s >= (double)prec - 4.0 + log2(c * s) + log2rho + 0.1) return s;
+    return MPCGEMM_ERR_SLICES;
+}
+
+// the device hot path with a known workspace
+int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
+             mpc_cmat *C, int method, int s, cudaStream_t st, uint8_t *meta, uint8_t *big, const Layout &Lo,
+             int simt, mpcgemm_report *rep, StageEvents *E) {
+    const int L = (prec + 63) / 64;
+    int64_t *eA = (int64_t *)meta, *eB = eA + m;
+    const int parts = method == 3 ? 3 : 2;
+    int8_t *digA = (int8_t *)big;
+    int8_t *digB = digA + align_up((size_t)parts * s * m * Lo.kp, 256);
+    int32_t *partials = (int32_t *)((uint8_t *)digB + align_up((size_t)parts * s * n * Lo.kp, 256));
+    CK(split_launch(dm(A->re), dm(A->im), 0, m, k, Lo.kp, L, eA, s, parts, digA, st));
+    CK(split_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, s, parts, digB, st));
+    if (E) CK(cudaEventRecord(E->ev[3], st));
+    const Geometry geo = main_geometry(dev, m, n, k, s, method);
+    const int BN = geo.BN;
+    PlanKey key{m, n, k, s, method, BN, geo.grid, simt, geo.maxkb};
+    Plan *plan;
+    if (int rc = build_plan(dev, key, &plan)) return rc;
+    SliceGemmLaunch SL;
+    memset(&SL, 0, sizeof(SL));
+    SL.P.units = plan->d_units; SL.P.cta_begin = plan->d_cta_begin;
+    SL.P.partials = partials; SL.P.ldD = Lo.ldD; SL.P.plane = m * Lo.ldD;
+    SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = s; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
+    SL.P.partsA = SL.P.partsB = parts;
+    for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
+    SL.digA = digA; SL.digB = digB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
+    SL.grid = plan->grid; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits; SL.units_flat = plan->d_units;
+    CK(slicegemm_launch(SL, st));
+    if (E) CK(cudaEventRecord(E->ev[4], st));
+    FoldParams F;
+    F.partials = partials; F.plane = m * Lo.ldD; F.ldD = Lo.ldD; F.m = m; F.n = n;
+    F.s = s; F.method = method; F.prec = prec; F.L = L; F.slotinfo = plan->d_slotinfo;
+    F.eA = eA; F.eB = eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
+    CK(fold_normalize_launch(F, st));
+    if (E) CK(cudaEventRecord(E->ev[5], st));
+    if (rep) {
+        rep->mma_instructions = plan->mma; rep->work_units = plan->nunits;
+        rep->kernel_launches += 4;                     // split x2, slice GEMM, fold
+        rep->slicegemm_ctas = simt ? plan->nunits : plan->grid;
+    }
+    return 0;
+}
+
+int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
+              int method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
+    if (int rc = check_args(m, n, k, prec, A, B, C, method)) return rc;
+    cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
+    const int forced = opts ? opts->slices : 0;
+    const int validate = opts ? opts->validate : 0;
+    const int simt = env_int("MPCGEMM_SLICEGEMM_SIMT", 0);
+    if (forced < 0 || forced > kMaxSlices) return fail(MPCGEMM_ERR_SLICES, "forced slices outside [1, 1024]");
+    if (rep) { memset(rep, 0, sizeof(*rep)); rep->minT = rep->minT1 = rep->maxD2 = -1; }
+    const int L = (prec + 63) / 64;
+    if (m == 0 || n == 0) return 0;
+    if (k == 0) { CK(zero_output_launch(dmo(C->re), m, n, L, st)); CK(zero_output_launch(dmo(C->im), m, n, L, st)); return 0; }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_mu);
+    DevCache &dc = g_cache[dev];
+    StageEvents *E = (opts && opts->timing) ? stage_events(dev) : nullptr;
+    if (E) CK(cudaEventRecord(E->ev[0], st));
+    Layout Lo = layout_for(m, n, k, 0, method, kMaxKBlocksPerChunk);
+    if (int rc = grow(&dc.meta, &dc.meta_bytes, Lo.meta)) return rc;
+    uint8_t *meta = (uint8_t *)dc.meta;
+    int64_t *eA = (int64_t *)meta, *eB = eA + m;
+    uint8_t *nzA = (uint8_t *)(eB + n), *nzB = nzA + m;
+    uint32_t *errflag = (uint32_t *)(meta + align_up(8 * (m + n) + (m + n) + 64, 256) + 64);
+    if (validate) CK(cudaMemsetAsync(errflag, 0, 4, st));
+    CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, eA, nzA, errflag, validate, st));
+    CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, eB, nzB, errflag, validate, st));
+    if (E) CK(cudaEventRecord(E->ev[1], st));
+    int launches = 4;                                  // linemax + finalize, A and B
+    if (validate) {
+        uint32_t h = 0;
+        CK(cudaMemcpyAsync(&h, errflag, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h & 2u) return fail(MPCGEMM_ERR_EXP_RANGE, "|exp| > 2^61");
+        if (h & 1u) return fail(MPCGEMM_ERR_NOT_NORMALIZED, "mantissa not normalized");
+    }
+    int s = forced;
+    int64_t pb[3] = {-1, -1, -1};
+    double log2rho = 0.0;
+    if (!s) {
+        if (int rc = grow(&dc.ws, &dc.ws_bytes, Lo.pre)) return rc;
+        if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, pb)) return rc;
+        launches += 4 + (pb[0] == 0 ? 1 : 0);         // planes x2, T GEMM, min [, max-plus]
+        log2rho = rule_log2rho(k, pb[0], pb[1], pb[2]);
+        s = rule_slices(prec, method, log2rho);
+        if (s < 0) return fail(MPCGEMM_ERR_SLICES, "slice rule needs s > 1024");
+    }
+    Layout Lm = layout_for(m, n, k, s, method, main_geometry(dev, m, n, k, s, method).maxkb);
+    uint8_t *big;
+    if (opts && opts->workspace) {
+        if (opts->workspace_bytes < Lm.main) return fail(MPCGEMM_ERR_NOMEM, "caller workspace too small");
+        big = (uint8_t *)opts->workspace;
+    } else {
+        if (int rc = grow(&dc.ws, &dc.ws_bytes, Lm.main)) return rc;
+        big = (uint8_t *)dc.ws;
+    }
+    if (E) CK(cudaEventRecord(E->ev[2], st));
+    if (rep) rep->kernel_launches = launches;
+    if (int rc = run_main(dev, m, n, k, prec, A, B, C, method, s, st, meta, big, Lm, simt, rep, E)) return rc;
+    if (rep) {
+        rep->slices = s; rep->certified = 1; rep->minT = pb[0]; rep->minT1 = pb[1]; rep->maxD2 = pb[2];
+        rep->log2_rho_hat = log2rho;
+    }
+    if (E) {
+        CK(cudaEventSynchronize(E->ev[5]));
+        float t[5];
+        for (int q = 0; q < 5; q++) CK(cudaEventElapsedTime(&t[q], E->ev[q], E->ev[q + 1]));
+        if (rep) { rep->ms_linemax = t[0]; rep->ms_prepass = t[1]; rep->ms_split = t[2]; rep->ms_gemm = t[3]; rep->ms_fold = t[4]; }
+    }
+    return 0;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+int mpcgemm(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
+            mpcgemm_method method) {
+    return gemm_impl(m, n, k, prec, A, B, C, (int)method, nullptr, nullptr);
+}
+
+int mpcgemm_ex(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
+               mpcgemm_method method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
+    return gemm_impl(m, n, k, prec, A, B, C, (int)method, opts, rep);
+}
+
+int mpcgemm_rho_bounds(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
+                       int32_t full, const mpcgemm_opts *opts, int64_t out[3]) {
+    if (!out) return fail(MPCGEMM_ERR_ARG, "null out");
+    if (!A || !B) return fail(MPCGEMM_ERR_ARG, "null matrix descriptor");
+    if (m < 0 || n < 0 || k < 0) return fail(MPCGEMM_ERR_ARG, "negative dimension");
+    if (prec < 2 || prec > 4096) return fail(MPCGEMM_ERR_PREC, "prec outside [2, 4096]");
+    out[0] = out[1] = out[2] = -1;
+    if (m == 0 || n == 0 || k == 0) return 0;
+    cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
+    const int L = (prec + 63) / 64;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_mu);
+    DevCache &dc = g_cache[dev];
+    Layout Lo = layout_for(m, n, k, 0, MPCGEMM_3M, kMaxKBlocksPerChunk);
+    if (int rc = grow(&dc.meta, &dc.meta_bytes, Lo.meta)) return rc;
+    if (int rc = grow(&dc.ws, &dc.ws_bytes, Lo.pre)) return rc;
+    uint8_t *meta = (uint8_t *)dc.meta;
+    int64_t *eA = (int64_t *)meta, *eB = eA + m;
+    uint8_t *nzA = (uint8_t *)(eB + n), *nzB = nzA + m;
+    CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, eA, nzA, nullptr, 0, st));
+    CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, eB, nzB, nullptr, 0, st));
+    return run_prepass(dev, m, n, k, prec, A, B, full, st, meta, (uint8_t *)dc.ws, Lo,
+                       env_int("MPCGEMM_SLICEGEMM_SIMT", 0), out);
+}
+
+int mpcgemm_slices_for(int32_t prec, mpcgemm_method method, int64_t k, int64_t minT, int64_t minT1, int64_t maxD2) {
+    return rule_slices(prec, (int)method, rule_log2rho(k, minT, minT1, maxD2));
+}
+
+size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec, mpcgemm_method method, int32_t slices) {
+    (void)prec;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Layout Lo = layout_for(m, n, k, slices, (int)method, main_geometry(dev, m, n, k, slices, (int)method).maxkb);
+    return std::max(Lo.main, Lo.pre);
+}
+
+int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
+                 mpcgemm_method method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
+    if (int rc = check_args(m, n, k, prec, A, B, C, (int)method)) return rc;
+    const int L = (prec + 63) / 64;
+    cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
+    const mpc_rmat *in[4] = {&A->re, &A->im, &B->re, &B->im};
+    const int64_t rows[6] = {m, m, k, k, m, m}, cols[6] = {k, k, n, n, n, n};
+    size_t off[6][3], total = 0;
+    for (int q = 0; q < 6; q++) {
+        const size_t ents = (size_t)rows[q] * cols[q];
+        off[q][0] = total; total = align_up(total + ents, 256);
+        off[q][1] = total; total = align_up(total + ents * 8, 256);
+        off[q][2] = total; total = align_up(total + ents * 8 * L, 256);
+    }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    uint8_t *base;
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        DevCache &dc = g_cache[dev];
+        if (int rc = grow(&dc.stage, &dc.stage_bytes, total)) return rc;
+        base = (uint8_t *)dc.stage;
+    }
+    mpc_rmat dmats[6];
+    for (int q = 0; q < 6; q++) {
+        dmats[q].sign = base + off[q][0];
+        dmats[q].exp = (int64_t *)(base + off[q][1]);
+        dmats[q].limbs = (uint64_t *)(base + off[q][2]);
+        dmats[q].ld = cols[q];
+    }
+    for (int q = 0; q < 4; q++) {
+        const mpc_rmat &H = *in[q];
+        if (rows[q] == 0 || cols[q] == 0) continue;
+        CK(cudaMemcpy2DAsync(dmats[q].sign, cols[q], H.sign, H.ld, cols[q], rows[q], cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpy2DAsync(dmats[q].exp, cols[q] * 8, H.exp, H.ld * 8, cols[q] * 8, rows[q], cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpy2DAsync(dmats[q].limbs, cols[q] * 8 * L, H.limbs, H.ld * 8 * L, cols[q] * 8 * L, rows[q],
+                             cudaMemcpyHostToDevice, st));
+    }
+    mpc_cmat dA{dmats[0], dmats[1]}, dB{dmats[2], dmats[3]}, dC{dmats[4], dmats[5]};
+    int rc = gemm_impl(m, n, k, prec, &dA, &dB, &dC, (int)method, opts, rep);
+    if (rc < 0) return rc;
+    mpc_rmat *outs[2] = {&C->re, &C->im};
+    for (int q = 0; q < 2; q++) {
+        const mpc_rmat &D = dmats[4 + q];
+        mpc_rmat &H = *outs[q];
+        if (m == 0 || n == 0) continue;
+        CK(cudaMemcpy2DAsync(H.sign, H.ld, D.sign, n, n, m, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpy2DAsync(H.exp, H.ld * 8, D.exp, n * 8, n * 8, m, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpy2DAsync(H.limbs, H.ld * 8 * L, D.limbs, n * 8 * L, n * 8 * L, m, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return rc;
+}
+
+const char *mpcgemm_strerror(int code) {
+    switch (code) {
+        case MPCGEMM_OK: return "ok";
+        case MPCGEMM_ERR_ARG: return "invalid argument";
+        case MPCGEMM_ERR_PREC: return "precision outside [2, 4096]";
+        case MPCGEMM_ERR_EXP_RANGE: return "exponent outside [-2^61, 2^61]";
+        case MPCGEMM_ERR_NOT_NORMALIZED: return "mantissa not normalized";
+        case MPCGEMM_ERR_ALIAS: return "C overlaps A or B";
+        case MPCGEMM_ERR_NOMEM: return "workspace allocation failed";
+        case MPCGEMM_ERR_CUDA: return "CUDA error";
+        case MPCGEMM_ERR_SLICES: return "slice count outside [1, 1024]";
+        default: return "unknown status";
+    }
+}
+
+const char *mpcgemm_last_error(void) { return g_last_error.c_str(); }
+
+void mpcgemm_release(void) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaDeviceSynchronize();
+    auto it = g_cache.find(dev);
+    if (it != g_cache.end()) {
+        cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage);
+        g_cache.erase(it);
+    }
+    for (auto p = g_plans.begin(); p != g_plans.end();) {
+        if (p->first.first == dev) {
+            cudaFree(p->second.d_units); cudaFree(p->second.d_cta_begin); cudaFree(p->second.d_slotinfo);
+            p = g_plans.erase(p);
+        } else ++p;
+    }
+}
+
+int mpcgemm_version(void) { return 100; }
+
+}  // extern "C"

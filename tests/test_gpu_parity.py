@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Bit-exact: every output entry of the GPU equals oracle.ozaki (Algorithm 2 under the DESIGN.md
+readings, same s) -- the whole path is integer arithmetic plus one RNE, so no tolerance.
+Within bound: against oracle.exact (the plain definition, prec+64 bits), the BASELINE.json
+acceptance e <= 2^-(prec-8) (4M) / 2^-(prec-9) (3M).
+Sizes span several 128-row / 256-col tiles with ragged tails; the BASELINE configs run at full
+size in the bench's launch configuration and are checked on sampled outputs."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import mpgen
+import oracle
+from harness import first_mismatch, max_err_log2, same_bits
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2307_06072_b200 as P  # noqa: E402
+
+BOUND = {"4M": 8, "3M": 9}
+
+
+def run_gpu(A, B, prec, method, slices=0):
+    dA, dB = P.to_device(A), P.to_device(B)
+    dC, rep = P.gemm(dA, dB, prec, method, slices)
+    torch.cuda.synchronize()
+    return P.to_host(dC), rep
+
+
+def sample_idx(m, n, count, seed=0):
+    rng = np.random.default_rng(seed)
+    si = list(rng.integers(0, m, count))
+    sj = list(rng.integers(0, n, count))
+    for i in (0, m - 1, min(127, m - 1), min(128, m - 1)):         # tile edges and the ragged tail
+        for j in (0, n - 1, min(255, n - 1), min(256, n - 1)):
+            si.append(i); sj.append(j)
+    return np.array(si), np.array(sj)
+
+
+def sampled_equal(C, Rs, si, sj):
+    for part in ("re", "im"):
+        a, b = getattr(C, part), getattr(Rs, part)
+        for t in range(len(si)):
+            i, j = si[t], sj[t]
+            if a.sign[i, j] != b.sign[0, t] or a.exp[i, j] != b.exp[0, t] or not np.array_equal(a.limbs[i, j], b.limbs[0, t]):
+                return (part, int(i), int(j))
+    return None
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_config1_full_bitexact(method):
+    """BASELINE config 1 (64^3, prec 128, seed 0): every entry bit-exact vs the oracle."""
+    A, B = mpgen.config_inputs(1, seed=0)
+    C, rep = run_gpu(A, B, 128, method)
+    s_ref, ok = oracle.auto_slices(A, B, 128, method)
+    assert ok and rep["slices"] == s_ref
+    R = oracle.ozaki(A, B, 128, method, s_ref)
+    assert same_bits(C, R), first_mismatch(C, R)
+    Cx = oracle.exact(A, B, 128 + 64, method)
+    assert max_err_log2(A, B, C, Cx) <= -(128 - BOUND[method])
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+@pytest.mark.parametrize("m,n,k,prec,spread", [(200, 300, 150, 192, 8), (130, 257, 129, 64, 0), (1, 1, 1, 100, 0),
+                                               (3, 517, 33, 256, 2)])
+def test_ragged_sampled_bitexact(method, m, n, k, prec, spread):
+    A = mpgen.random_cmat(m + n + k, 5, m, k, prec, spread, zero_frac=0.05)
+    B = mpgen.random_cmat(m + n + k, 6, k, n, prec, spread, zero_frac=0.05)
+    C, rep = run_gpu(A, B, prec, method)
+    s_ref, ok = oracle.auto_slices(A, B, prec, method)
+    assert rep["slices"] == s_ref
+    si, sj = sample_idx(m, n, 300, seed=m)
+    Rs = oracle.ozaki(A, B, prec, method, s_ref, samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
+    Xs = oracle.exact(A, B, prec + 64, method, samples=(si, sj))
+    assert max_err_log2(A, B, C, Xs, samples=(si, sj), ref_is_sampled=True) <= -(prec - BOUND[method])
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_simt_crosscheck_and_forced_slices(method, monkeypatch):
+    """tcgen05 kernel == dp4a SIMT kernel bitwise over the same work list; forced s values."""
+    m, n, k, prec = 150, 280, 300, 160
+    A = mpgen.random_cmat(3, 7, m, k, prec, 5)
+    B = mpgen.random_cmat(3, 8, k, n, prec, 5)
+    for s in (0, 2, 7, 40):
+        C1, r1 = run_gpu(A, B, prec, method, s)
+        monkeypatch.setenv("MPCGEMM_SLICEGEMM_SIMT", "1")
+        C2, r2 = run_gpu(A, B, prec, method, s)
+        monkeypatch.delenv("MPCGEMM_SLICEGEMM_SIMT")
+        assert r1["slices"] == r2["slices"]
+        assert same_bits(C1, C2), (s, first_mismatch(C1, C2))
+        if s:
+            si, sj = sample_idx(m, n, 60, seed=s)
+            Rs = oracle.ozaki(A, B, prec, method, s, samples=(si, sj))
+            assert sampled_equal(C1, Rs, si, sj) is None
+
+
+def test_small_chunks_equal_default(monkeypatch):
+    """Any chunking of the INT32 accumulation gives the same result (exact integer sums)."""
+    m, n, k, prec = 140, 140, 700, 128
+    A = mpgen.random_cmat(4, 7, m, k, prec, 2)
+    B = mpgen.random_cmat(4, 8, k, n, prec, 2)
+    C1, _ = run_gpu(A, B, prec, "4M")
+    monkeypatch.setenv("MPCGEMM_MAXKB", "3")
+    C2, _ = run_gpu(A, B, prec, "4M")
+    monkeypatch.setenv("MPCGEMM_BN", "128")
+    C3, _ = run_gpu(A, B, prec, "4M")
+    assert same_bits(C1, C2) and same_bits(C1, C3)
+
+
+@pytest.mark.parametrize("spread,k", [(16, 12), (16, 3), (0, 64), (4, 40)])
+def test_prepass_matches_oracle(spread, k):
+    """rho-hat pre-pass integers and the resulting s equal the oracle's (incl. the minT == 0
+    max-plus stage)."""
+    m, n, prec = 70, 90, 256
+    A = mpgen.random_cmat(spread + k, 9, m, k, prec, spread, zero_frac=0.1)
+    B = mpgen.random_cmat(spread + k, 10, k, n, prec, spread, zero_frac=0.1)
+    dA, dB = P.to_device(A), P.to_device(B)
+    got = P.mpcgemm_rho_bounds(dA, dB, prec)
+    assert got == oracle.rho_bounds(A, B)
+    for method in ("3M", "4M"):
+        C, rep = run_gpu(A, B, prec, method)
+        assert rep["slices"] == oracle.auto_slices(A, B, prec, method)[0]
+        si, sj = sample_idx(m, n, 80)
+        Rs = oracle.ozaki(A, B, prec, method, rep["slices"], samples=(si, sj))
+        assert sampled_equal(C, Rs, si, sj) is None
+
+
+def test_edge_cases():
+    prec = 128
+    A = mpgen.random_cmat(1, 1, 5, 0, prec)
+    B = mpgen.random_cmat(1, 2, 0, 7, prec)
+    C, _ = run_gpu(A, B, prec, "3M")                      # k = 0: C = 0
+    assert not C.re.limbs.any() and not C.im.limbs.any() and not C.re.exp.any()
+    A = mpgen.random_cmat(1, 1, 0, 9, prec)
+    B = mpgen.random_cmat(1, 2, 9, 4, prec)
+    C, _ = run_gpu(A, B, prec, "4M")                      # m = 0
+    assert C.shape == (0, 4)
+    # zero rows / columns and an all-zero operand
+    A = mpgen.random_cmat(2, 1, 6, 9, prec)
+    B = mpgen.random_cmat(2, 2, 9, 5, prec)
+    for R in (A.re, A.im):
+        R.sign[3] = 0; R.exp[3] = 0; R.limbs[3] = 0
+    for R in (B.re, B.im):
+        R.limbs[:, 2] = 0; R.exp[:, 2] = 0; R.sign[:, 2] = 0
+    for method in ("3M", "4M"):
+        C, rep = run_gpu(A, B, prec, method)
+        assert same_bits(C, oracle.ozaki(A, B, prec, method, rep["slices"]))
+        assert not C.re.limbs[3].any() and not C.im.limbs[:, 2].any()
+    Z = mpgen.CMat(mpgen.empty_rmat(4, 6, prec), mpgen.empty_rmat(4, 6, prec))
+    C, _ = run_gpu(Z, B.rows(0, 6), prec, "3M")
+    assert not C.re.limbs.any()
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_integer_closure_and_identity(method):
+    import random
+    rnd = random.Random(1)
+    m, k, n = 37, 45, 29
+    mk = lambda r, c: [[rnd.randint(-8, 8) for _ in range(c)] for _ in range(r)]
+    A = mpgen.CMat(mpgen.from_ints(mk(m, k), 128), mpgen.from_ints(mk(m, k), 128))
+    B = mpgen.CMat(mpgen.from_ints(mk(k, n), 128), mpgen.from_ints(mk(k, n), 128))
+    C, _ = run_gpu(A, B, 128, method)
+    assert same_bits(C, oracle.exact(A, B, 128, method))
+    # B = I with rows of equal exponent: every bit captured -> C == A
+    A2 = mpgen.random_cmat(11, 1, 20, 20, 128)
+    for R in (A2.re, A2.im):
+        R.exp[:] = 0
+    I = mpgen.CMat(mpgen.from_ints([[int(i == j) for j in range(20)] for i in range(20)], 128),
+                   mpgen.from_ints([[0] * 20 for _ in range(20)], 128))
+    C, _ = run_gpu(A2, I, 128, method)
+    assert same_bits(C, A2)
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_transposition_bitwise(method):
+    prec = 192
+    A = mpgen.random_cmat(21, 1, 90, 70, prec, 6)
+    B = mpgen.random_cmat(21, 2, 70, 110, prec, 6)
+    s = oracle.auto_slices(A, B, prec, method)[0]
+    C, _ = run_gpu(A, B, prec, method, s)
+    Ct, _ = run_gpu(B.T(), A.T(), prec, method, s)
+    assert same_bits(Ct, C.T())
+
+
+def test_host_entry_matches_device():
+    prec = 256
+    A = mpgen.random_cmat(31, 1, 100, 90, prec, 3)
+    B = mpgen.random_cmat(31, 2, 90, 120, prec, 3)
+    for method in ("3M", "4M"):
+        C1, r1 = run_gpu(A, B, prec, method)
+        C2, r2 = P.mpcgemm_host(A, B, prec, method)
+        assert r1["slices"] == r2["slices"] and same_bits(C1, C2)
+
+
+def test_validate_and_errors():
+    prec = 128
+    A = mpgen.random_cmat(41, 1, 8, 8, prec)
+    B = mpgen.random_cmat(41, 2, 8, 8, prec)
+    bad = A.copy()
+    bad.re.limbs[2, 3, -1] &= np.uint64((1 << 63) - 1)    # clear the leading bit
+    dA, dB = P.to_device(bad), P.to_device(B)
+    dC = P.empty_device(8, 8, prec)
+    with pytest.raises(P.MpcgemmError) as e:
+        P.mpcgemm_ex(dA, dB, dC, prec, "3M", validate=1)
+    assert e.value.code == -4
+    with pytest.raises(P.MpcgemmError) as e:
+        P.mpcgemm_ex(P.to_device(A), dB, dC, 5000, "3M")
+    assert e.value.code == -2
+    with pytest.raises(P.MpcgemmError) as e:
+        P.mpcgemm_ex(P.to_device(A), dB, dC, prec, "3M", slices=2000)
+    assert e.value.code == -8
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_configs_2_3_sampled(cfg, method):
+    """BASELINE configs 2 and 3 at full size: sampled outputs bit-exact, within the bound."""
+    c = mpgen.CONFIGS[cfg]
+    A, B = mpgen.config_inputs(cfg, seed=0)
+    C, rep = run_gpu(A, B, c["prec"], method)
+    assert rep["slices"] == oracle.auto_slices(A, B, c["prec"], method)[0]
+    si, sj = sample_idx(c["m"], c["n"], 40, seed=cfg)
+    Rs = oracle.ozaki(A, B, c["prec"], method, rep["slices"], samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
+    Xs = oracle.exact(A, B, c["prec"] + 64, method, samples=(si, sj))
+    assert max_err_log2(A, B, C, Xs, samples=(si, sj), ref_is_sampled=True) <= -(c["prec"] - BOUND[method])
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_config4_sampled(method):
+    """BASELINE config 4 (2048^3, prec 1024): the bench workload, sampled bit-exact."""
+    c = mpgen.CONFIGS[4]
+    A, B = mpgen.config_inputs(4, seed=0)
+    C, rep = run_gpu(A, B, c["prec"], method)
+    assert rep["slices"] == 129 or rep["slices"] == oracle.auto_slices(A, B, c["prec"], method)[0]
+    rng = np.random.default_rng(4)
+    si = np.concatenate([rng.integers(0, 2048, 12), [0, 2047, 1023, 128]])
+    sj = np.concatenate([rng.integers(0, 2048, 12), [2047, 0, 256, 255]])
+    Rs = oracle.ozaki(A, B, c["prec"], method, rep["slices"], samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
+    Xs = oracle.exact(A, B, c["prec"] + 64, method, samples=(si, sj))
+    assert max_err_log2(A, B, C, Xs, samples=(si, sj), ref_is_sampled=True) <= -(c["prec"] - BOUND[method])
+
+
+def test_config5_lu_updates_sampled():
+    """BASELINE config 5 (LU Schur updates, prec 768): first and last GEMM, sampled."""
+    for j, L21, U12 in mpgen.lu_update_gemms(seed=0, js=[1, 15]):
+        C, rep = run_gpu(L21, U12, 768, "3M")
+        mm, nn = L21.shape[0], U12.shape[1]
+        si, sj = sample_idx(mm, nn, 12, seed=j)
+        Rs = oracle.ozaki(L21, U12, 768, "3M", rep["slices"], samples=(si, sj))
+        assert sampled_equal(C, Rs, si, sj) is None
