@@ -30,12 +30,17 @@ struct DMatOut {
     int64_t ld;
 };
 
-// One slice-GEMM work unit: output tile (tm, tn) of job `job`, anti-diagonal r, and the
-// k-block range [g0, g1) of the job's concatenated sequence (pair, p, kb); the int32
-// result goes to partial plane `slot`.
+// One slice-GEMM work unit on output tile (tm, tn) of job `job` (job_g = job | G << 8):
+//  G = 1: one chunk of anti-diagonal r -- the k-blocks g in [a, b) of the job's concatenated
+//         sequence (pair, p = 1..r-1, kb) -- into partial plane slot0;
+//  G = 2: anti-diagonals r and r+1 together over the k-blocks kb in [a, b) of every pair and
+//         every p, into planes slot0 (D_r) and slot1 (D_{r+1}); each A_p / B_q tile is
+//         loaded once and feeds both diagonals.
 struct WorkUnit {
-    int32_t job, tm, tn, r, g0, g1, slot, pad;
+    int32_t job_g, tm, tn, r, a, b, slot0, slot1;
 };
+__host__ __device__ __forceinline__ int unit_job(const WorkUnit &w) { return w.job_g & 0xFF; }
+__host__ __device__ __forceinline__ int unit_G(const WorkUnit &w) { return w.job_g >> 8; }
 
 struct JobDesc {
     int32_t npairs;
@@ -44,8 +49,9 @@ struct JobDesc {
 };
 
 struct GemmParams {
-    const WorkUnit *units;     // in per-CTA order
-    const int32_t *cta_begin;  // [grid+1] offsets into units
+    const WorkUnit *units;     // global order: size-descending, tiles of one (job, r, chunk) contiguous
+    int32_t nunits;
+    int32_t *counter;          // dynamic scheduler: next unit (zeroed before each launch)
     int32_t *partials;         // [nslots][m][ldD]
     int64_t ldD;               // partial row pitch (entries)
     int64_t plane;             // m * ldD
@@ -101,6 +107,12 @@ MPC_DEV void tma_load_3d(void *dst, const void *tmap, uint64_t *bar, int c0, int
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4, %5}], [%2];"
         ::"r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+// 1-D bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0)
+MPC_DEV void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
 // ---------------------------------------------------------------- tcgen05

@@ -39,6 +39,7 @@ int fail(int code, const char *what, cudaError_t e = cudaSuccess) {
     } while (0)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+int env_int(const char *name, int dflt);
 
 // ---------------------------------------------------------------- workspace cache
 struct DevCache {
@@ -77,15 +78,15 @@ StageEvents *stage_events(int dev) {
 
 // ---------------------------------------------------------------- plans (work lists)
 struct PlanKey {
-    int64_t m, n, k; int s, method, BN, grid, simt, maxkb;
+    int64_t m, n, k; int s, method, BN, grid, simt, maxkb, g2;
     bool operator<(const PlanKey &o) const {
-        return std::tie(m, n, k, s, method, BN, grid, simt, maxkb) <
-               std::tie(o.m, o.n, o.k, o.s, o.method, o.BN, o.grid, o.simt, o.maxkb);
+        return std::tie(m, n, k, s, method, BN, grid, simt, maxkb, g2) <
+               std::tie(o.m, o.n, o.k, o.s, o.method, o.BN, o.grid, o.simt, o.maxkb, o.g2);
     }
 };
 struct Plan {
     WorkUnit *d_units = nullptr;
-    int32_t *d_cta_begin = nullptr;
+    int32_t *d_counter = nullptr;
     int32_t *d_slotinfo = nullptr;
     int nunits = 0, nslots = 0, grid = 0;
     int64_t mma = 0;
@@ -110,10 +111,42 @@ void method_jobs(int method, Plan &P) {
     }
 }
 
-// Builds the unit list: for each job q and anti-diagonal r the concatenated k-block sequence
-// (pair, p, kb) of length G = npairs (r-1) KB is cut into ceil(G / maxkb) chunks (INT32
-// exactness), each chunk x output tile is one unit with its own partial plane.
-// Units are assigned to CTAs longest-first to the least-loaded CTA (LPT).
+// Diagonal segments of one job: either a pair (r, r+1) sharing operand tiles (G = 2, the kb
+// range cut into nch chunks so that each accumulator sums <= kMaxKBlocksPerChunk k-blocks) or
+// a single diagonal r (G = 1, its concatenated (pair, p, kb) sequence cut into nch chunks).
+struct Segment { int q, r, G; int64_t nch; };
+
+int64_t exact_cap();
+
+std::vector<Segment> diag_segments(const Plan &P, int64_t KB, int s, int method, int target, bool g2) {
+    std::vector<Segment> segs;
+    const int rmax = method == 0 ? 2 : s + 1;
+    const int64_t cap = exact_cap();
+    for (int q = 0; q < P.njobs; q++) {
+        const int64_t np = P.jobs[q].npairs;
+        int r = 2;
+        while (r <= rmax) {
+            if (g2 && r + 1 <= rmax && np * r <= cap) {
+                // D_{r+1} sums np * r k-blocks per kb: exact if np * r * kbc <= cap
+                int64_t kbc = std::min<int64_t>(KB, cap / (np * r));
+                kbc = std::max<int64_t>(1, std::min<int64_t>(kbc, target / (np * (2 * r - 1))));
+                segs.push_back({q, r, 2, (KB + kbc - 1) / kbc});
+                r += 2;
+            } else {
+                const int64_t G = np * (r - 1) * KB;
+                const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(cap, target));
+                segs.push_back({q, r, 1, (G + chunk - 1) / chunk});
+                r += 1;
+            }
+        }
+    }
+    return segs;
+}
+
+bool g2_enabled() { return env_int("MPCGEMM_G2", 1) != 0; }
+
+// Builds the unit list (segments x chunks x output tiles), each unit with its own partial
+// planes, and the slot table (job, r) -> (first plane, chunk count) used by the fold.
 int build_plan(int dev, const PlanKey &key, Plan **out) {
     auto it = g_plans.find({dev, key});
     if (it != g_plans.end()) { *out = &it->second; return 0; }
@@ -122,63 +155,57 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
     const int s = key.s;
     const int64_t KB = (key.k + kBK - 1) / kBK;
     const int64_t tiles_m = (key.m + 127) / 128, tiles_n = (key.n + key.BN - 1) / key.BN;
-    const int rmin = 2, rmax = key.method == 0 ? 2 : s + 1;
     std::vector<int32_t> slotinfo((size_t)kMaxJobs * (s + 2) * 2, 0);
     std::vector<WorkUnit> units;
     int nslots = 0;
-    for (int q = 0; q < P.njobs; q++) {
-        for (int r = rmin; r <= rmax; r++) {
-            const int64_t G = (int64_t)P.jobs[q].npairs * (r - 1) * KB;
-            const int64_t nch = (G + key.maxkb - 1) / key.maxkb;
+    for (const Segment &sg : diag_segments(P, KB, s, key.method, key.maxkb, key.g2)) {
+        const int q = sg.q, r = sg.r;
+        const int64_t np = P.jobs[q].npairs;
+        if (sg.G == 2) {
             slotinfo[(q * (s + 2) + r) * 2] = nslots;
-            slotinfo[(q * (s + 2) + r) * 2 + 1] = (int32_t)nch;
-            for (int64_t c = 0; c < nch; c++) {
-                const int32_t g0 = (int32_t)(c * G / nch), g1 = (int32_t)((c + 1) * G / nch);
+            slotinfo[(q * (s + 2) + r) * 2 + 1] = (int32_t)sg.nch;
+            slotinfo[(q * (s + 2) + r + 1) * 2] = nslots + (int32_t)sg.nch;
+            slotinfo[(q * (s + 2) + r + 1) * 2 + 1] = (int32_t)sg.nch;
+            for (int64_t c = 0; c < sg.nch; c++) {
+                const int32_t a = (int32_t)(c * KB / sg.nch), b = (int32_t)((c + 1) * KB / sg.nch);
                 for (int64_t tm = 0; tm < tiles_m; tm++)
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
-                        WorkUnit w;
-                        w.job = q; w.tm = (int32_t)tm; w.tn = (int32_t)tn; w.r = r;
-                        w.g0 = g0; w.g1 = g1; w.slot = nslots + (int32_t)c; w.pad = 0;
-                        units.push_back(w);
-                        P.mma += (int64_t)(g1 - g0) * (kBK / 32);
+                        units.push_back({q | (2 << 8), (int32_t)tm, (int32_t)tn, r, a, b,
+                                         nslots + (int32_t)c, nslots + (int32_t)(sg.nch + c)});
+                        P.mma += np * (b - a) * (2 * r - 1) * (kBK / 32);
                     }
             }
-            nslots += (int)nch;
+            nslots += 2 * (int)sg.nch;
+        } else {
+            const int64_t G = np * (r - 1) * KB;
+            slotinfo[(q * (s + 2) + r) * 2] = nslots;
+            slotinfo[(q * (s + 2) + r) * 2 + 1] = (int32_t)sg.nch;
+            for (int64_t c = 0; c < sg.nch; c++) {
+                const int32_t a = (int32_t)(c * G / sg.nch), b = (int32_t)((c + 1) * G / sg.nch);
+                for (int64_t tm = 0; tm < tiles_m; tm++)
+                    for (int64_t tn = 0; tn < tiles_n; tn++) {
+                        units.push_back({q | (1 << 8), (int32_t)tm, (int32_t)tn, r, a, b, nslots + (int32_t)c, -1});
+                        P.mma += (int64_t)(b - a) * (kBK / 32);
+                    }
+            }
+            nslots += (int)sg.nch;
         }
     }
-    // LPT: longest first; stable so equal-work units keep (job, r, chunk, tile) order
-    std::vector<int> order(units.size());
-    for (size_t i = 0; i < order.size(); i++) order[i] = (int)i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        return (units[a].g1 - units[a].g0) > (units[b].g1 - units[b].g0);
-    });
+    // global order for the dynamic scheduler: longest first (LPT tail), stable so that the
+    // tiles of one (job, r, chunk) stay contiguous and co-running CTAs share operand planes
+    auto work = [&](const WorkUnit &w) -> int64_t {
+        return unit_G(w) == 2 ? (int64_t)P.jobs[unit_job(w)].npairs * (w.b - w.a) * (2 * w.r - 1) : (int64_t)(w.b - w.a);
+    };
+    std::stable_sort(units.begin(), units.end(), [&](const WorkUnit &a, const WorkUnit &b) { return work(a) > work(b); });
     const int grid = (int)std::min<int64_t>(key.grid, (int64_t)units.size());
-    std::vector<std::vector<int>> per(grid > 0 ? grid : 1);
-    using Item = std::pair<int64_t, int>;
-    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
-    for (int c = 0; c < grid; c++) heap.push({0, c});
-    for (int idx : order) {
-        Item it2 = heap.top(); heap.pop();
-        per[it2.second].push_back(idx);
-        // per-unit cost: MMA k-blocks plus a fixed epilogue / fill overhead (~4 k-blocks)
-        heap.push({it2.first + (units[idx].g1 - units[idx].g0) + 4, it2.second});
-    }
-    std::vector<WorkUnit> flat;
-    std::vector<int32_t> begin(grid + 1, 0);
-    flat.reserve(units.size());
-    for (int c = 0; c < grid; c++) {
-        begin[c] = (int32_t)flat.size();
-        for (int idx : per[c]) flat.push_back(units[idx]);
-    }
-    begin[grid] = (int32_t)flat.size();
+    const std::vector<WorkUnit> &flat = units;
     P.nunits = (int)flat.size(); P.nslots = nslots; P.grid = grid;
     if (P.nunits) {
         if (cudaMalloc(&P.d_units, sizeof(WorkUnit) * flat.size()) != cudaSuccess ||
-            cudaMalloc(&P.d_cta_begin, sizeof(int32_t) * begin.size()) != cudaSuccess ||
+            cudaMalloc(&P.d_counter, sizeof(int32_t)) != cudaSuccess ||
             cudaMalloc(&P.d_slotinfo, sizeof(int32_t) * slotinfo.size()) != cudaSuccess)
             return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc plan");
         CK(cudaMemcpy(P.d_units, flat.data(), sizeof(WorkUnit) * flat.size(), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(P.d_cta_begin, begin.data(), sizeof(int32_t) * begin.size(), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(P.d_slotinfo, slotinfo.data(), sizeof(int32_t) * slotinfo.size(), cudaMemcpyHostToDevice));
     }
     auto res = g_plans.emplace(std::make_pair(dev, key), P);
@@ -249,18 +276,21 @@ struct Layout {
 
 int tile_bn(int64_t n) { return n > 128 ? 256 : 128; }
 
+// Load-balance target for the MMA k-blocks of one unit: at least ~4 units per CTA.  (The
+// INT32 exactness cap is separate: exact_cap().)
 int64_t chunk_kb(int64_t m, int64_t n, int64_t k, int s, int method, int BN, int grid) {
-    // INT32 exactness cap; smaller chunks when there are too few units to fill the GPU
     const int64_t KB = (k + kBK - 1) / kBK;
     const int64_t tiles = ((m + 127) / 128) * ((n + BN - 1) / BN);
     const int64_t npairs_total = method == 0 ? 1 : (method == 3 ? 3 : 4);
     const int64_t work = npairs_total * KB * (int64_t)s * (s + 1) / 2 * tiles;   // k-blocks
-    int64_t target = work / (4 * (int64_t)grid);         // ~4 units per CTA minimum
-    int64_t cap = kMaxKBlocksPerChunk;
+    int64_t target = work / (4 * (int64_t)grid);
+    return std::max<int64_t>(8, std::min<int64_t>(target, 1 << 30));
+}
+
+// k-blocks one INT32 accumulator may sum; MPCGEMM_MAXKB lowers it
+int64_t exact_cap() {
     int e = env_int("MPCGEMM_MAXKB", 0);
-    if (e > 0) cap = std::min<int64_t>(cap, e);
-    if (target < 8) target = 8;
-    return std::max<int64_t>(1, std::min<int64_t>(cap, target));
+    return e > 0 ? std::min<int64_t>(kMaxKBlocksPerChunk, e) : kMaxKBlocksPerChunk;
 }
 
 struct Geometry { int BN, grid, maxkb; };
@@ -275,14 +305,12 @@ Geometry main_geometry(int dev, int64_t m, int64_t n, int64_t k, int s, int meth
 }
 
 int64_t count_slots(int64_t k, int s, int method, int maxkb) {
-    const int64_t KB = (k + kBK - 1) / kBK;
-    int64_t nslots = 0;
-    for (int r = 2; r <= s + 1; r++)
-        for (int q = 0; q < 3; q++) {
-            const int64_t np = (method == 4 && q == 2) ? 2 : 1;
-            nslots += (np * (r - 1) * KB + maxkb - 1) / maxkb;
-        }
-    return nslots;
+    Plan P;
+    method_jobs(method, P);
+    int64_t n = 0;
+    for (const Segment &sg : diag_segments(P, (k + kBK - 1) / kBK, s, method, maxkb, g2_enabled()))
+        n += sg.G * sg.nch;
+    return n;
 }
 
 Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb) {
@@ -291,7 +319,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb)
     Lo.ldD = align_up((size_t)std::max<int64_t>(n, 1), 4);
     Lo.meta = align_up(8 * (m + n) + (m + n) + 64, 256) + 256;
     const int64_t KB = (k + kBK - 1) / kBK;
-    const int64_t nslotsT = (KB + kMaxKBlocksPerChunk - 1) / kMaxKBlocksPerChunk;
+    const int64_t nslotsT = (KB + exact_cap() - 1) / exact_cap();
     Lo.pre = align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256) +
              align_up((size_t)nslotsT * m * Lo.ldD * 4, 256);
     Lo.main = 0;
@@ -321,12 +349,12 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     CK(prepass_planes_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, tB, relB, st));
     const int BN = tile_bn(n);
     const int grid = sm_count(dev);
-    PlanKey key{m, n, k, 1, 0, BN, grid, simt, (int)kMaxKBlocksPerChunk};
+    PlanKey key{m, n, k, 1, 0, BN, grid, simt, (int)kMaxKBlocksPerChunk, 0};
     Plan *plan;
     if (int rc = build_plan(dev, key, &plan)) return rc;
     SliceGemmLaunch SL;
     memset(&SL, 0, sizeof(SL));
-    SL.P.units = plan->d_units; SL.P.cta_begin = plan->d_cta_begin;
+    SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
     SL.P.partials = T; SL.P.ldD = Lo.ldD; SL.P.plane = m * Lo.ldD;
     SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = 1; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
     SL.P.partsA = SL.P.partsB = 1;
@@ -392,12 +420,12 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     if (E) CK(cudaEventRecord(E->ev[3], st));
     const Geometry geo = main_geometry(dev, m, n, k, s, method);
     const int BN = geo.BN;
-    PlanKey key{m, n, k, s, method, BN, geo.grid, simt, geo.maxkb};
+    PlanKey key{m, n, k, s, method, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0};
     Plan *plan;
     if (int rc = build_plan(dev, key, &plan)) return rc;
     SliceGemmLaunch SL;
     memset(&SL, 0, sizeof(SL));
-    SL.P.units = plan->d_units; SL.P.cta_begin = plan->d_cta_begin;
+    SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
     SL.P.partials = partials; SL.P.ldD = Lo.ldD; SL.P.plane = m * Lo.ldD;
     SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = s; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
     SL.P.partsA = SL.P.partsB = parts;
@@ -628,7 +656,7 @@ void mpcgemm_release(void) {
     }
     for (auto p = g_plans.begin(); p != g_plans.end();) {
         if (p->first.first == dev) {
-            cudaFree(p->second.d_units); cudaFree(p->second.d_cta_begin); cudaFree(p->second.d_slotinfo);
+            cudaFree(p->second.d_units); cudaFree(p->second.d_counter); cudaFree(p->second.d_slotinfo);
             p = g_plans.erase(p);
         } else ++p;
     }

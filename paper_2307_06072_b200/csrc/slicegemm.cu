@@ -1,19 +1,21 @@
 // slicegemm.cu -- the triangle of slice products of Algorithm 2 on the
 // sm_100a INT8 tensor cores.
 //
-// For every work unit (job, output tile, anti-diagonal r, k-block chunk [g0, g1)) it
-// computes, exactly in INT32,
-//     D = sum_{g in [g0,g1)}  A_{pa, p}[tile rows, kb] . B_{pb, r-p}[tile cols, kb]^T
-// where g enumerates (pair, p = 1..r-1, kb) of the job's concatenated K' = npairs (r-1) k,
-// i.e. one chunk of  D_r = sum_{alpha+beta=r} A_alpha B_beta  (the anti-diagonal form of
-// the triangle beta <= d - alpha + 1), and stores D to partial plane `slot`.
+// Anti-diagonal form of the triangle beta <= d - alpha + 1:  for r = 2..s+1
+//     D_r = sum_{alpha + beta = r} A_alpha B_beta        (int32, exact: DESIGN.md "Exactness")
+// is computed per output tile and written to int32 partial planes; the fold kernel sums them
+// with weights 256^(s+1-r).  Work units (common.cuh) are either one chunk of one diagonal
+// (G = 1) or a pair of adjacent diagonals (G = 2) sharing every operand tile:
+//     step p = 1..r:  load A_p, B_{r+1-p};  D_{r+1} += A_p B_{r+1-p};  D_r += A_{p-1} B_{r+1-p}
+// so each 48 KB stage feeds 8 MMAs instead of 4 (half the L2 / HBM bytes per MMA).
 //
-// Kernel structure (one CTA per SM, persistent over a host-balanced unit list):
-//   warp 0 lane 0 : TMA producer, STAGES-deep ring of (A 128x128 B, B BNx128 B) int8 tiles
+// Kernel structure (one CTA per SM, persistent; units from a global atomic counter in a
+// locality-friendly order):
+//   warp 0 lane 0 : scheduler + TMA producer, STAGES-deep ring of (A 128x128 B, B BNx128 B)
 //   warp 1        : TMEM allocator; lane 0 issues tcgen05.mma.cta_group::1.kind::i8
-//                   (M=128, N=BN, K=32; 4 per 128-byte k-block) into a double-buffered
-//                   TMEM accumulator (2 x BN columns)
-//   warps 4..7    : epilogue, tcgen05.ld 32x32b -> registers -> int32 partial plane
+//                   (M = 128, N = BN, K = 32; 4 per 128-byte k-block) into two BN-column
+//                   accumulators (D_r at column 0, D_{r+1} at column BN)
+//   warps 4..7    : epilogue, tcgen05.ld 32x32b -> registers -> int32 partial planes
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -29,9 +31,13 @@ struct TcCfg {
     static constexpr int A_BYTES = kBM * kBK;
     static constexpr int B_BYTES = BN * kBK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256 /*barriers*/;
+    static constexpr int TMEM_COLS = 2 * BN;           // two accumulators
+    static constexpr int QN = 8;                       // unit-index queue depth
+    static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 512 /*barriers, queue*/;
 };
+
+// digit planes of step (pair, p, kb) of a unit
+struct StepPlanes { int planeA, planeB, kb; };
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
@@ -45,14 +51,19 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     uint8_t *sB = smem + STAGES * Cfg::A_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * Cfg::B_BYTES);
     uint64_t *empty = full + STAGES;
-    uint64_t *tfull = empty + STAGES;
-    uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *tfull = empty + STAGES;                 // accumulators ready (MMA -> epilogue)
+    uint64_t *tempty = tfull + 1;                     // accumulators drained (epilogue -> MMA)
+    uint64_t *qfull = tempty + 1;                     // unit-index queue (producer -> MMA, epilogue)
+    uint64_t *qempty = qfull + Cfg::QN;
+    int32_t *uq = reinterpret_cast<int32_t *>(qempty + Cfg::QN);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(uq + Cfg::QN);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 128);
+        for (int i = 0; i < Cfg::QN; i++) { mbar_init(&qfull[i], 1); mbar_init(&qempty[i], 1 + 4); }
         fence_barrier_init();
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
@@ -63,29 +74,46 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int ubeg = P.cta_begin[blockIdx.x], uend = P.cta_begin[blockIdx.x + 1];
     const int s = P.s, KB = P.KB;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- TMA producer
+            // ---------------- scheduler + TMA producer: units are taken in list order from a
+            // global counter, so co-running CTAs work on neighbouring tiles of the same
+            // (job, r, chunk) and share the digit-plane tiles in L2
             int stage = 0; uint32_t phase = 0;
-            for (int u = ubeg; u < uend; u++) {
+            int qs = 0; uint32_t qph = 0;
+            auto load = [&](int planeA, int planeB, int kb, int tm, int tn) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+                tma_load_3d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, tm * kBM, planeA);
+                tma_load_3d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, tn * BN, planeB);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            };
+            for (;;) {
+                int u = atomicAdd(P.counter, 1);
+                if (u >= P.nunits) u = -1;
+                mbar_wait(&qempty[qs], qph ^ 1);
+                *reinterpret_cast<volatile int32_t *>(&uq[qs]) = u;
+                mbar_arrive(&qfull[qs]);
+                if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
+                if (u < 0) break;
                 const WorkUnit w = P.units[u];
-                const JobDesc &J = P.jobs[w.job];
-                const int per_pair = (w.r - 1) * KB;
-                for (int g = w.g0; g < w.g1; g++) {
-                    const int pair = g / per_pair;
-                    const int rem = g - pair * per_pair;
-                    const int p0 = rem / KB;              // alpha - 1
-                    const int kb = rem - p0 * KB;
-                    const int planeA = J.pa[pair] * s + p0;
-                    const int planeB = J.pb[pair] * s + (w.r - 2 - p0);   // beta - 1, beta = r - alpha
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-                    tma_load_3d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, w.tm * kBM, planeA);
-                    tma_load_3d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, w.tn * BN, planeB);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                const JobDesc &J = P.jobs[unit_job(w)];
+                if (unit_G(w) == 2) {
+                    for (int pr = 0; pr < J.npairs; pr++)
+                        for (int kb = w.a; kb < w.b; kb++)
+                            for (int p = 1; p <= w.r; p++)          // A_p, B_{r+1-p}
+                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), kb, w.tm, w.tn);
+                } else {
+                    const int per_pair = (w.r - 1) * KB;
+                    for (int g = w.a; g < w.b; g++) {
+                        const int pair = g / per_pair;
+                        const int rem = g - pair * per_pair;
+                        const int p0 = rem / KB;                    // alpha - 1
+                        const int kb = rem - p0 * KB;
+                        load(J.pa[pair] * s + p0, J.pb[pair] * s + (w.r - 2 - p0), kb, w.tm, w.tn);
+                    }
                 }
             }
         }
@@ -94,60 +122,103 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         if (lane == 0) {
             // ---------------- MMA issuer
             constexpr uint32_t idesc = make_idesc_i8(kBM, BN);
+            const uint32_t d0 = tmem_base, d1 = tmem_base + (uint32_t)BN;
             int stage = 0; uint32_t phase = 0;
-            int buf = 0; uint32_t tphase = 0;
-            for (int u = ubeg; u < uend; u++) {
+            uint32_t tphase = 0;
+            int qs = 0; uint32_t qph = 0;
+            for (;;) {
+                mbar_wait(&qfull[qs], qph);
+                const int u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
+                mbar_arrive(&qempty[qs]);
+                if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
+                if (u < 0) break;
                 const WorkUnit w = P.units[u];
-                mbar_wait(&tempty[buf], tphase ^ 1);
+                const JobDesc &J = P.jobs[unit_job(w)];
+                mbar_wait(tempty, tphase ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)(buf * BN);
-                for (int g = w.g0; g < w.g1; g++) {
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
-                    const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+                if (unit_G(w) == 2) {
+                    int prev = 0;
+                    for (int pr = 0; pr < J.npairs; pr++)
+                        for (int kb = w.a; kb < w.b; kb++)
+                            for (int p = 1; p <= w.r; p++) {
+                                mbar_wait(&full[stage], phase);
+                                tc_fence_after();
+                                const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+                                const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+                                const bool first = (pr == 0 && kb == w.a);
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 32; kk++) {
-                        mma_i8(d_tmem, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                               (g > w.g0 || kk > 0) ? 1u : 0u);
+                                for (int kk = 0; kk < kBK / 32; kk++)   // D_{r+1} += A_p B_{r+1-p}
+                                    mma_i8(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                           (first && p == 1 && kk == 0) ? 0u : 1u);
+                                if (p >= 2) {                           // D_r += A_{p-1} B_{r+1-p}
+                                    const uint32_t ap = smem_u32(sA + prev * Cfg::A_BYTES);
+#pragma unroll
+                                    for (int kk = 0; kk < kBK / 32; kk++)
+                                        mma_i8(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                               (first && p == 2 && kk == 0) ? 0u : 1u);
+                                    mma_commit(&empty[prev]);           // A_{p-1} no longer needed
+                                }
+                                if (p == w.r) mma_commit(&empty[stage]);   // A_r pairs only with B_1
+                                prev = stage;
+                                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                            }
+                } else {
+                    for (int g = w.a; g < w.b; g++) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 32; kk++)
+                            mma_i8(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                   (g > w.a || kk > 0) ? 1u : 0u);
+                        mma_commit(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit(&empty[stage]);                // frees the smem slot when done
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(&tfull[buf]);                      // accumulator ready
-                buf ^= 1; if (buf == 0) tphase ^= 1;
+                mma_commit(tfull);                            // accumulators ready
+                tphase ^= 1;
             }
         }
         __syncwarp();
     } else if (warp >= 4) {
-        // ---------------- epilogue: TMEM -> registers -> int32 partial plane
+        // ---------------- epilogue: TMEM -> registers -> int32 partial planes
         const int q = warp & 3;                               // TMEM lane quarter of this warp
-        int buf = 0; uint32_t tphase = 0;
-        for (int u = ubeg; u < uend; u++) {
+        uint32_t tphase = 0;
+        int qs = 0; uint32_t qph = 0;
+        for (;;) {
+            mbar_wait(&qfull[qs], qph);
+            const int u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&qempty[qs]);
+            if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
+            if (u < 0) break;
             const WorkUnit w = P.units[u];
-            mbar_wait(&tfull[buf], tphase);
+            mbar_wait(tfull, tphase);
             tc_fence_after();
             const int row = w.tm * kBM + q * 32 + lane;
-            int32_t *out = P.partials + (int64_t)w.slot * P.plane + (int64_t)row * P.ldD;
+            for (int acc = 0; acc < unit_G(w); acc++) {
+                int32_t *out = P.partials + (int64_t)(acc ? w.slot1 : w.slot0) * P.plane + (int64_t)row * P.ldD;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; c++) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + c * 32), v);
-                tmem_ld_wait();
-                const int col0 = w.tn * BN + c * 32;
-                if (row < P.m) {
+                for (int c = 0; c < BN / 32; c++) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+                    tmem_ld_wait();
+                    const int col0 = w.tn * BN + c * 32;
+                    if (row < P.m) {
 #pragma unroll
-                    for (int g4 = 0; g4 < 8; g4++) {
-                        if (col0 + 4 * g4 < P.ldD) {
-                            int4 val = make_int4((int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2], (int)v[4 * g4 + 3]);
-                            *reinterpret_cast<int4 *>(out + col0 + 4 * g4) = val;
+                        for (int g4 = 0; g4 < 8; g4++) {
+                            if (col0 + 4 * g4 < P.ldD) {
+                                int4 val = make_int4((int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2], (int)v[4 * g4 + 3]);
+                                *reinterpret_cast<int4 *>(out + col0 + 4 * g4) = val;
+                            }
                         }
                     }
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[buf]);
-            buf ^= 1; if (buf == 0) tphase ^= 1;
+            mbar_arrive(tempty);
+            tphase ^= 1;
         }
     }
     tc_fence_before();
@@ -158,8 +229,8 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 
 // ------------------------------------------------------------------ SIMT cross-check kernel
 // Same work list and output, computed with dp4a on CUDA cores (used by the tests to check
-// the tensor-core kernel bitwise; selected with MPCGEMM_SLICEGEMM=simt).  One CTA per
-// (unit, 32x32 subtile), one thread per output element.
+// the tensor-core kernel bitwise; selected with MPCGEMM_SLICEGEMM_SIMT=1).  One CTA per
+// (unit, 32x32 subtile), one thread per 4 output elements of each accumulator.
 __global__ void __launch_bounds__(256)
 slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict__ digB,
                       int64_t rowsA, int64_t rowsB, int64_t kp, const WorkUnit *units, int BN,
@@ -168,24 +239,44 @@ slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict_
     __shared__ int32_t sa[32][kBK / 4 + 1];
     __shared__ int32_t sb[32][kBK / 4 + 1];
     const WorkUnit w = units[blockIdx.x];
-    const JobDesc &J = P.jobs[w.job];
+    const JobDesc &J = P.jobs[unit_job(w)];
+    const int G = unit_G(w);
     const int sub = blockIdx.y;                   // 32x32 subtile index within 128 x BN
     const int sub_m = sub % (kBM / 32), sub_n = sub / (kBM / 32);
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;   // 32 x 8
     const int64_t row0 = (int64_t)w.tm * kBM + sub_m * 32;
     const int64_t col0 = (int64_t)w.tn * BN + sub_n * 32;
-    int32_t acc[4] = {0, 0, 0, 0};
-    const int per_pair = (w.r - 1) * P.KB;
-    for (int g = w.g0; g < w.g1; g++) {
-        const int pair = g / per_pair;
-        const int rem = g - pair * per_pair;
-        const int p0 = rem / P.KB;
-        const int kb = rem - p0 * P.KB;
-        const int8_t *pa = digA + ((int64_t)(J.pa[pair] * P.s + p0) * rowsA) * kp;
-        const int8_t *pb = digB + ((int64_t)(J.pb[pair] * P.s + (w.r - 2 - p0)) * rowsB) * kp;
+    int32_t acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    // enumerate (accumulator, A plane, B plane, kb) exactly as the tensor-core kernel pairs them
+    const int npairs = J.npairs;
+    const int nsteps = G == 2 ? npairs * (w.b - w.a) * w.r * 2 : (w.b - w.a);
+    for (int t = 0; t < nsteps; t++) {
+        int which, planeA, planeB, kb;
+        if (G == 2) {
+            int x = t;
+            const int half = x & 1; x >>= 1;          // 0: D_{r+1} (A_p, B_{r+1-p}); 1: D_r (A_p, B_{r-p})
+            const int p = x % w.r + 1; x /= w.r;
+            kb = w.a + x % (w.b - w.a); x /= (w.b - w.a);
+            const int pr = x;
+            if (half == 0) { which = 1; planeA = J.pa[pr] * P.s + p - 1; planeB = J.pb[pr] * P.s + (w.r - p); }
+            else {
+                if (p >= w.r) continue;
+                which = 0; planeA = J.pa[pr] * P.s + p - 1; planeB = J.pb[pr] * P.s + (w.r - 1 - p);
+            }
+        } else {
+            const int g = w.a + t;
+            const int per_pair = (w.r - 1) * P.KB;
+            const int pair = g / per_pair;
+            const int rem = g - pair * per_pair;
+            const int p0 = rem / P.KB;
+            kb = rem - p0 * P.KB;
+            which = 0; planeA = J.pa[pair] * P.s + p0; planeB = J.pb[pair] * P.s + (w.r - 2 - p0);
+        }
+        const int8_t *pa = digA + ((int64_t)planeA * rowsA) * kp;
+        const int8_t *pb = digB + ((int64_t)planeB * rowsB) * kp;
         __syncthreads();
-        for (int t = threadIdx.x; t < 32 * (kBK / 4); t += 256) {
-            int rr = t / (kBK / 4), cc = t % (kBK / 4);
+        for (int q = threadIdx.x; q < 32 * (kBK / 4); q += 256) {
+            int rr = q / (kBK / 4), cc = q % (kBK / 4);
             int64_t kk = (int64_t)kb * kBK + cc * 4;
             int32_t va = 0, vb = 0;
             if (row0 + rr < rowsA && kk < kp) va = *reinterpret_cast<const int32_t *>(pa + (row0 + rr) * kp + kk);
@@ -195,14 +286,19 @@ slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict_
         __syncthreads();
         for (int e = 0; e < 4; e++) {
             const int r_ = ty * 4 + e;
+            int32_t v = acc[which][e];
 #pragma unroll 8
-            for (int cc = 0; cc < kBK / 4; cc++) acc[e] = __dp4a(sa[r_][cc], sb[tx][cc], acc[e]);
+            for (int cc = 0; cc < kBK / 4; cc++) v = __dp4a(sa[r_][cc], sb[tx][cc], v);
+            acc[which][e] = v;
         }
     }
-    for (int e = 0; e < 4; e++) {
-        const int64_t row = row0 + ty * 4 + e, col = col0 + tx;
-        if (row < P.m && col < P.ldD) P.partials[(int64_t)w.slot * P.plane + row * P.ldD + col] = acc[e];
-    }
+    for (int a = 0; a < G; a++)
+        for (int e = 0; e < 4; e++) {
+            const int64_t row = row0 + ty * 4 + e, col = col0 + tx;
+            const int slot = a ? w.slot1 : w.slot0;
+            // G = 2 keeps D_r in acc[0] and D_{r+1} in acc[1]
+            if (row < P.m && col < P.ldD) P.partials[(int64_t)slot * P.plane + row * P.ldD + col] = acc[a][e];
+        }
 }
 
 // ------------------------------------------------------------------ host side
@@ -240,6 +336,8 @@ static cudaError_t launch_tc(const SliceGemmLaunch &L, cudaStream_t st) {
     if (make_plane_map(&tb, L.digB, (int64_t)L.P.partsB * L.P.s, L.rowsB, L.kp, BN)) return cudaErrorInvalidValue;
     auto kern = slicegemm_tc_kernel<BN, STAGES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(L.P.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     kern<<<L.grid, 256, Cfg::SMEM, st>>>(ta, tb, L.P);
     return cudaGetLastError();

@@ -115,82 +115,112 @@ cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, 
 }
 
 // ================================================================== a-3: split into digit planes
-// Streams the bytes of X = floor(N 2^(W - e + exp - 64L)) from the least significant one:
-// byte t of X = bits [pos0 + 8t, pos0 + 8t + 8) of N, pos0 = 64L - W + e - exp.
-struct ByteStream {
+// X = sign * floor(|x| 2^(W - e)), W = 8s - 3 (reading Z5), as a two's complement integer;
+// its s balanced radix-256 digits (digit set [-128,127]) are the bytes of Z = X + H,
+// H = sum_t 128 * 256^t, minus 128 (Z's bytes are the unique base-256 digits of X + H, and
+// X + H = sum (d_t + 128) 256^t with d_t + 128 in [0,255]).  So the split is word arithmetic:
+// funnel-shift the mantissa into 64-bit words of X, negate (two's complement) for x < 0, add
+// Re + Im for the 3M sum part, add H with carry, and XOR 0x80 into every byte.
+// Each thread handles VEC = 4 consecutive k of one line, so each digit-plane store is one
+// coalesced 32-bit write.
+struct WordStream {
     const uint64_t *N;
     int L;
-    int64_t pos;     // bit position of the next byte
-    int64_t li;      // cached limb index
-    uint64_t lo, hi;
+    int64_t li;          // limb index of the low part of the next word
+    int bo;              // bit offset inside it
+    uint64_t lo;
     MPC_DEV void init(const uint64_t *N_, int L_, int64_t pos0, bool zero) {
-        N = N_; L = zero ? 0 : L_; pos = pos0;
-        li = pos >= 0 ? (pos >> 6) : -((-pos + 63) >> 6);
-        lo = limb_at(N, L, li); hi = limb_at(N, L, li + 1);
+        N = N_; L = zero ? 0 : L_;
+        li = pos0 >= 0 ? (pos0 >> 6) : -((-pos0 + 63) >> 6);     // floor(pos0 / 64)
+        bo = (int)(pos0 - (li << 6));
+        lo = limb_at(N, L, li);
     }
-    MPC_DEV uint32_t next() {
-        const int64_t l = pos >= 0 ? (pos >> 6) : -((-pos + 63) >> 6);   // floor(pos / 64)
-        if (l != li) {
-            if (l == li + 1) { lo = hi; hi = limb_at(N, L, l + 1); }
-            else { lo = limb_at(N, L, l); hi = limb_at(N, L, l + 1); }
-            li = l;
-        }
-        const int bo = (int)(pos - (l << 6));
-        uint64_t v = bo ? ((lo >> bo) | (hi << (64 - bo))) : lo;
-        pos += 8;
-        return (uint32_t)(v & 0xFF);
+    MPC_DEV uint64_t next() {
+        const uint64_t hi = limb_at(N, L, li + 1);
+        const uint64_t v = bo ? ((lo >> bo) | (hi << (64 - bo))) : lo;
+        lo = hi; li++;
+        return v;
     }
 };
 
-__global__ void split_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
-                             const int64_t *__restrict__ eline, int s, int nparts, int8_t *__restrict__ dig)
+constexpr int kSplitVec = 4;
+constexpr uint64_t kH = 0x8080808080808080ull;
+
+__global__ void __launch_bounds__(128)
+split_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
+             const int64_t *__restrict__ eline, int s, int nparts, int8_t *__restrict__ dig)
 {
-    const int64_t kk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (kk >= kp) return;
+    const int64_t kk0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kSplitVec;
+    if (kk0 >= kp) return;
     const int64_t plane = lines * kp;
+    const int64_t W = 8 * (int64_t)s - 3;
     for (int64_t line = blockIdx.y; line < lines; line += gridDim.y) {
-        int8_t *out = dig + line * kp + kk;
-        if (kk >= k) {
-            for (int a = 0; a < nparts * s; a++) out[(int64_t)a * plane] = 0;
-            continue;
-        }
         const int64_t e = eline[line];
-        const int64_t W = 8 * (int64_t)s - 3;
-        ByteStream bs[2];
-        uint32_t neg[2], nc[2];
+        WordStream ws[kSplitVec][2];
+        uint64_t nc[kSplitVec][2];
+        uint32_t neg[kSplitVec][2];
+        uint64_t csum[kSplitVec];
+        uint64_t ch[kSplitVec][3];
 #pragma unroll
-        for (int p = 0; p < 2; p++) {
-            const DMat &M = p ? im : re;
-            const int64_t idx = side == 0 ? line * M.ld + kk : kk * M.ld + line;
-            const uint64_t *N = M.limbs + idx * L;
-            const bool zero = __ldg(N + L - 1) == 0;
-            const int64_t ex = __ldg(M.exp + idx);
-            bs[p].init(N, L, 64 * (int64_t)L - W + e - ex, zero);
-            neg[p] = zero ? 0u : (uint32_t)__ldg(M.sign + idx);
-            nc[p] = 1;                              // +1 of the two's complement negation
-        }
-        uint32_t csum = 0;                          // carry of the 3M byte-stream addition
-        uint32_t rc[3] = {0, 0, 0};                 // balanced-recoding carries
-        for (int t = 0; t < s; t++) {
-            uint32_t y[3];
+        for (int v = 0; v < kSplitVec; v++) {
+            const int64_t kk = kk0 + v;
 #pragma unroll
             for (int p = 0; p < 2; p++) {
-                uint32_t b = bs[p].next();
-                if (neg[p]) { uint32_t v = (~b & 0xFFu) + nc[p]; nc[p] = v >> 8; b = v & 0xFFu; }
-                y[p] = b;
+                const DMat &M = p ? im : re;
+                if (kk < k) {
+                    const int64_t idx = side == 0 ? line * M.ld + kk : kk * M.ld + line;
+                    const uint64_t *N = M.limbs + idx * L;
+                    const bool zero = __ldg(N + L - 1) == 0;
+                    const int64_t ex = __ldg(M.exp + idx);
+                    ws[v][p].init(N, L, 64 * (int64_t)L - W + e - ex, zero);
+                    neg[v][p] = zero ? 0u : (uint32_t)__ldg(M.sign + idx);
+                } else {
+                    ws[v][p].init(nullptr, 0, 0, true);
+                    neg[v][p] = 0u;
+                }
+                nc[v][p] = 1;
             }
-            {
-                uint32_t v = y[0] + y[1] + csum;
-                csum = v >> 8; y[2] = v & 0xFFu;
+            csum[v] = 0;
+            ch[v][0] = ch[v][1] = ch[v][2] = 0;
+        }
+        int8_t *out = dig + line * kp + kk0;
+        const int nwords = (s + 7) / 8;
+        for (int w = 0; w < nwords; w++) {
+            uint64_t dw[3][kSplitVec];
+#pragma unroll
+            for (int v = 0; v < kSplitVec; v++) {
+                uint64_t y[3];
+#pragma unroll
+                for (int p = 0; p < 2; p++) {
+                    uint64_t x = ws[v][p].next();
+                    if (neg[v][p]) { const uint64_t t = ~x + nc[v][p]; nc[v][p] = (nc[v][p] && t == 0) ? 1ull : 0ull; x = t; }
+                    y[p] = x;
+                }
+                {   // 3M: Re + Im (two's complement, with carry)
+                    const uint64_t t = y[0] + y[1];
+                    const uint64_t c1 = t < y[0];
+                    y[2] = t + csum[v];
+                    csum[v] = c1 | (y[2] < t);
+                }
+#pragma unroll
+                for (int p = 0; p < 3; p++) {            // + H with carry, XOR 0x80 per byte
+                    const uint64_t t = y[p] + kH;
+                    const uint64_t c1 = t < y[p];
+                    const uint64_t z = t + ch[v][p];
+                    ch[v][p] = c1 | (z < t);
+                    dw[p][v] = z ^ kH;
+                }
             }
-            const int64_t a = s - 1 - t;            // plane of digit alpha = s - t
+            const int nb = min(8, s - 8 * w);
 #pragma unroll
             for (int p = 0; p < 3; p++) {
-                if (p < nparts) {
-                    uint32_t v = y[p] + rc[p];
-                    int d = v >= 128u ? (int)v - 256 : (int)v;
-                    rc[p] = v >= 128u;
-                    out[((int64_t)p * s + a) * plane] = (int8_t)d;
+                if (p >= nparts) break;
+                for (int bt = 0; bt < nb; bt++) {
+                    const int t = 8 * w + bt;            // digit t from the bottom -> plane s-1-t
+                    uint32_t packed = 0;
+#pragma unroll
+                    for (int v = 0; v < kSplitVec; v++) packed |= (uint32_t)((dw[p][v] >> (8 * bt)) & 0xFF) << (8 * v);
+                    *reinterpret_cast<uint32_t *>(out + ((int64_t)p * s + (s - 1 - t)) * plane) = packed;
                 }
             }
         }
@@ -201,7 +231,8 @@ cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, i
                          const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st)
 {
     if (lines == 0 || kp == 0) return cudaSuccess;
-    dim3 grid((unsigned)((kp + 127) / 128), (unsigned)(lines < 65535 ? lines : 65535));
+    const int64_t threads = (kp + kSplitVec - 1) / kSplitVec;
+    dim3 grid((unsigned)((threads + 127) / 128), (unsigned)(lines < 65535 ? lines : 65535));
     split_kernel<<<grid, 128, 0, st>>>(re, im, side, lines, k, kp, L, eline, s, nparts, dig);
     return cudaGetLastError();
 }
@@ -367,113 +398,216 @@ cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t plane, i
 }
 
 // ================================================================== a-5 + a-6: fold and normalize
-constexpr int kLcMax = kMaxSlices / 8 + 4;
+// One thread per output element (i, j); a block covers FOLD_T consecutive j of one row.
+// The two's complement fixed-point accumulator of each part lives in shared memory as
+// fix[part][limb][thread] (column per thread: conflict-free), built bottom-up:
+//     carry += D_r ; emit byte (carry & 0xFF) ; carry >>= 8        r = s+1 .. 2
+// with D_r the Eq. 5 / Eq. 6 combination of the job partials (sum of their chunks), then the
+// final carry sign-extended at bit 8s.  normalize_store rounds it once (RNE) to prec bits.
+struct FixView {
+    const uint64_t *base;   // fix[0][thread]
+    int stride;             // threads per block
+    int n;                  // limbs
+    MPC_DEV uint64_t at(int64_t l) const { return (l >= 0 && l < n) ? base[l * stride] : 0ull; }
+    MPC_DEV uint64_t bits64(int64_t pos) const {
+        if (pos <= -64) return 0;
+        if (pos < 0) return at(0) << (-pos);
+        const int64_t li = pos >> 6;
+        const int bo = (int)(pos & 63);
+        const uint64_t lo = at(li);
+        if (!bo) return lo;
+        return (lo >> bo) | (at(li + 1) << (64 - bo));
+    }
+};
 
-// two's complement fix[0..Lc) -> RNE to prec bits in the ABI format
-MPC_DEV void normalize_store(uint64_t *fix, int Lc, int64_t e0, int prec, int L,
+MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, int prec, int L,
                              uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
 {
-    const bool neg = (int64_t)fix[Lc - 1] < 0;
-    if (neg) {                                        // magnitude
+    const bool neg = (int64_t)fix[(int64_t)(Lc - 1) * stride] < 0;
+    if (neg) {                                        // magnitude, in place
         uint64_t c = 1;
-        for (int l = 0; l < Lc; l++) { uint64_t x = ~fix[l] + c; c = (c && x == 0); fix[l] = x; }
+        for (int l = 0; l < Lc; l++) {
+            const uint64_t x = ~fix[(int64_t)l * stride] + c;
+            c = (c && x == 0);
+            fix[(int64_t)l * stride] = x;
+        }
     }
     int b = 0;
-    for (int l = Lc - 1; l >= 0; l--)
-        if (fix[l]) { b = 64 * l + 64 - __clzll((long long)fix[l]); break; }
+    for (int l = Lc - 1; l >= 0; l--) {
+        const uint64_t v = fix[(int64_t)l * stride];
+        if (v) { b = 64 * l + 64 - __clzll((long long)v); break; }
+    }
     if (b == 0) {
         *sign_out = 0; *exp_out = 0;
         for (int l = 0; l < L; l++) limbs_out[l] = 0;
         return;
     }
+    const FixView F{fix, stride, Lc};
     int64_t E = e0 + b;
-    // top-aligned window of 64L bits ending at bit b
-    uint64_t out[64];
-    const int64_t base = (int64_t)b - 64 * L;
-    for (int l = 0; l < L; l++) out[l] = bits64(fix, Lc, base + 64 * l);
-    const int drop = 64 * L - prec;                   // low bits of the window below prec
-    // round bit = bit (b - prec - 1) of the magnitude; sticky = any lower bit
+    const int64_t base = (int64_t)b - 64 * L;         // window = bits [b - 64L, b)
+    const int drop = 64 * L - prec;
+    // round bit = bit (b - prec - 1); sticky = OR of the bits below it
     const int64_t rpos = (int64_t)b - prec - 1;
     int rbit = 0, sticky = 0;
     if (rpos >= 0) {
-        rbit = (int)((fix[rpos >> 6] >> (rpos & 63)) & 1);
+        rbit = (int)((F.at(rpos >> 6) >> (rpos & 63)) & 1);
         const int64_t full = rpos >> 6;
-        for (int64_t l = 0; l < full && !sticky; l++) if (fix[l]) sticky = 1;
-        if (!sticky && (rpos & 63)) if (fix[full] & ((1ull << (rpos & 63)) - 1)) sticky = 1;
+        for (int64_t l = 0; l < full && !sticky; l++) if (F.at(l)) sticky = 1;
+        if (!sticky && (rpos & 63) && (F.at(full) & ((1ull << (rpos & 63)) - 1))) sticky = 1;
     }
-    if (drop) out[0] &= ~((1ull << drop) - 1);
-    const int lsb = (int)((out[0] >> drop) & 1);
-    if (rbit && (sticky || lsb)) {
-        uint64_t c = 1ull << drop;
-        for (int l = 0; l < L && c; l++) { uint64_t x = out[l] + c; c = x < out[l] ? 1 : 0; out[l] = x; }
-        if (c) {                                      // carry-out: 2^prec -> 2^(prec-1)
-            for (int l = 0; l < L; l++) out[l] = 0;
-            out[L - 1] = 1ull << 63;
-            E += 1;
+    const uint64_t w0 = F.bits64(base) & (drop ? ~((1ull << drop) - 1) : ~0ull);
+    const int lsb = (int)((w0 >> drop) & 1);
+    bool up = rbit && (sticky || lsb);
+    if (up) {                                         // carry-out iff all kept bits are 1
+        bool allones = (w0 | ((1ull << drop) - 1)) == ~0ull || (drop == 0 && w0 == ~0ull);
+        for (int l = 1; l < L && allones; l++) allones = F.bits64(base + 64 * l) == ~0ull;
+        if (allones) {
+            for (int l = 0; l < L - 1; l++) limbs_out[l] = 0;
+            limbs_out[L - 1] = 1ull << 63;
+            *sign_out = neg ? 1 : 0;
+            *exp_out = E + 1;
+            return;
         }
+    }
+    uint64_t c = up ? (1ull << drop) : 0ull;
+    for (int l = 0; l < L; l++) {
+        uint64_t w = l == 0 ? w0 : F.bits64(base + 64 * l);
+        const uint64_t x = w + c;
+        c = (x < w) ? 1ull : 0ull;
+        limbs_out[l] = x;
     }
     *sign_out = neg ? 1 : 0;
     *exp_out = E;
-    for (int l = 0; l < L; l++) limbs_out[l] = out[l];
 }
 
-__global__ void __launch_bounds__(128)
+// The partial planes are streamed by a producer warp with cp.async.bulk: for each slot (in
+// the order r = s+1..2, job, chunk) the contiguous strip partials[slot][i][j0 .. j0+T) lands in
+// a RING-deep shared-memory ring, so ~RING KB per block are in flight regardless of the
+// consumers' registers.  T consumer threads (one output j each) run the carry chains.
+constexpr int kFoldRing = 24;
+
+template <int kFoldT>
+__global__ void __launch_bounds__(kFoldT + 32)
 fold_normalize_kernel(const FoldParams F)
 {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t i = blockIdx.y;
-    if (j >= F.n || i >= F.m) return;
+    extern __shared__ __align__(128) uint8_t fsm_raw[];
     const int s = F.s;
     const int Lc = s / 8 + 3;
-    uint64_t fix[2][kLcMax];
-    uint64_t cur[2] = {0, 0};
-    int64_t carry[2] = {0, 0};
-    const int64_t off = i * F.ldD + j;
+    int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                       // [RING][T]
+    uint64_t *fix = reinterpret_cast<uint64_t *>(fsm_raw + kFoldRing * kFoldT * 4);  // [2][Lc][T]
+    int32_t *slots = reinterpret_cast<int32_t *>(fix + 2 * (int64_t)Lc * kFoldT);  // [job][r][base,cnt]
+    uint64_t *full = reinterpret_cast<uint64_t *>(slots + kMaxJobs * (s + 2) * 2 + 2);
+    full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
+    uint64_t *empty = full + kFoldRing;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nsi = kMaxJobs * (s + 2) * 2;
+    for (int q = tid; q < nsi; q += blockDim.x) slots[q] = F.slotinfo[q];
+    if (tid == 0) {
+        for (int e = 0; e < kFoldRing; e++) { mbar_init(&full[e], 1); mbar_init(&empty[e], kFoldT / 32); }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int64_t i = blockIdx.y;
+    const int64_t j0 = (int64_t)blockIdx.x * kFoldT;
+    if (warp == kFoldT / 32) {
+        // ---------------- producer warp
+        if (lane == 0) {
+            const int64_t cols = F.ldD - j0 < kFoldT ? F.ldD - j0 : kFoldT;     // ldD % 4 == 0
+            const uint32_t bytes = (uint32_t)(cols * 4);
+            const int32_t *row = F.partials + i * F.ldD + j0;
+            int e = 0; uint32_t ph = 0;
+            for (int r = s + 1; r >= 2; r--)
+                for (int q = 0; q < kMaxJobs; q++) {
+                    const int base = slots[(q * (s + 2) + r) * 2], cnt = slots[(q * (s + 2) + r) * 2 + 1];
+                    for (int c = 0; c < cnt; c++) {
+                        mbar_wait(&empty[e], ph ^ 1);
+                        mbar_arrive_expect_tx(&full[e], bytes);
+                        bulk_load(ring + e * kFoldT, row + (int64_t)(base + c) * F.plane, bytes, &full[e]);
+                        if (++e == kFoldRing) { e = 0; ph ^= 1; }
+                    }
+                }
+        }
+        return;
+    }
+    // ---------------- consumers: one output element j per thread
+    const int64_t j = j0 + tid;
+    uint64_t cur0 = 0, cur1 = 0;
+    int64_t c0 = 0, c1 = 0;
+    int e = 0; uint32_t ph = 0;
+    uint64_t *fix0 = fix + tid, *fix1 = fix + (int64_t)Lc * kFoldT + tid;
     for (int r = s + 1; r >= 2; r--) {
         int64_t t[kMaxJobs];
 #pragma unroll
         for (int q = 0; q < kMaxJobs; q++) {
-            const int base = F.slotinfo[(q * (s + 2) + r) * 2], cnt = F.slotinfo[(q * (s + 2) + r) * 2 + 1];
+            const int cnt = slots[(q * (s + 2) + r) * 2 + 1];
             int64_t v = 0;
-            for (int c = 0; c < cnt; c++) v += __ldg(F.partials + (int64_t)(base + c) * F.plane + off);
+            for (int c = 0; c < cnt; c++) {
+                mbar_wait(&full[e], ph);
+                v += ring[e * kFoldT + tid];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[e]);
+                if (++e == kFoldRing) { e = 0; ph ^= 1; }
+            }
             t[q] = v;
         }
-        int64_t d[2];
-        if (F.method == 3) { d[0] = t[0] - t[1]; d[1] = t[2] - t[0] - t[1]; }   // Eq. 6
-        else               { d[0] = t[0] - t[1]; d[1] = t[2]; }                 // Eq. 5
-        const int b = s + 1 - r;                                                // byte index
-#pragma unroll
-        for (int p = 0; p < 2; p++) {
-            carry[p] += d[p];
-            cur[p] |= (uint64_t)(carry[p] & 0xFF) << (8 * (b & 7));
-            carry[p] >>= 8;                                                     // arithmetic
-            if ((b & 7) == 7) { fix[p][b >> 3] = cur[p]; cur[p] = 0; }
+        int64_t d0, d1;
+        if (F.method == 3) { d0 = t[0] - t[1]; d1 = t[2] - t[0] - t[1]; }   // Eq. 6
+        else               { d0 = t[0] - t[1]; d1 = t[2]; }                 // Eq. 5
+        const int b = s + 1 - r;                                            // byte index
+        const int sh = 8 * (b & 7);
+        c0 += d0; cur0 |= (uint64_t)(c0 & 0xFF) << sh; c0 >>= 8;            // arithmetic shift
+        c1 += d1; cur1 |= (uint64_t)(c1 & 0xFF) << sh; c1 >>= 8;
+        if ((b & 7) == 7) {
+            fix0[(int64_t)(b >> 3) * kFoldT] = cur0; fix1[(int64_t)(b >> 3) * kFoldT] = cur1;
+            cur0 = 0; cur1 = 0;
         }
     }
-    // append the final carry at bit 8s, sign-extended
+    if (j >= F.n) return;
+    // the final carry at bit 8s, sign-extended to Lc limbs
     const int l0 = s >> 3, o = 8 * (s & 7);
-#pragma unroll
-    for (int p = 0; p < 2; p++) {
-        const uint64_t c = (uint64_t)carry[p];
-        const uint64_t sext = carry[p] < 0 ? ~0ull : 0ull;
-        fix[p][l0] = cur[p] | (c << o);
-        fix[p][l0 + 1] = o ? ((c >> (64 - o)) | (sext << o)) : sext;
-        for (int l = l0 + 2; l < Lc; l++) fix[p][l] = sext;
+    {
+        const uint64_t c = (uint64_t)c0, sx = c0 < 0 ? ~0ull : 0ull;
+        fix0[(int64_t)l0 * kFoldT] = cur0 | (c << o);
+        fix0[(int64_t)(l0 + 1) * kFoldT] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
+        for (int l = l0 + 2; l < Lc; l++) fix0[(int64_t)l * kFoldT] = sx;
+    }
+    {
+        const uint64_t c = (uint64_t)c1, sx = c1 < 0 ? ~0ull : 0ull;
+        fix1[(int64_t)l0 * kFoldT] = cur1 | (c << o);
+        fix1[(int64_t)(l0 + 1) * kFoldT] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
+        for (int l = l0 + 2; l < Lc; l++) fix1[(int64_t)l * kFoldT] = sx;
     }
     const int64_t e0 = F.eA[i] + F.eB[j] + 6 - 8 * (int64_t)(s + 1);
     const int64_t oi = i * F.Cre.ld + j;
-    normalize_store(fix[0], Lc, e0, F.prec, F.L, F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
+    normalize_store(fix0, kFoldT, Lc, e0, F.prec, F.L, F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
     const int64_t oj = i * F.Cim.ld + j;
-    normalize_store(fix[1], Lc, e0, F.prec, F.L, F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
+    normalize_store(fix1, kFoldT, Lc, e0, F.prec, F.L, F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
+}
+
+size_t fold_smem(int s, int T) {
+    const int Lc = s / 8 + 3;
+    return (size_t)kFoldRing * T * 4 + (size_t)2 * Lc * T * 8 + (size_t)kMaxJobs * (s + 2) * 2 * 4 + 16 +
+           (size_t)2 * kFoldRing * 8 + 16;
+}
+
+template <int T>
+static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
+    const size_t sm = fold_smem(F.s, T);
+    cudaError_t e = cudaFuncSetAttribute(fold_normalize_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((F.n + T - 1) / T), (unsigned)F.m);
+    fold_normalize_kernel<T><<<grid, T + 32, sm, st>>>(F);
+    return cudaGetLastError();
 }
 
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
 {
     if (F.m == 0 || F.n == 0) return cudaSuccess;
-    if (F.s > kMaxSlices) return cudaErrorInvalidValue;
-    dim3 grid((unsigned)((F.n + 127) / 128), (unsigned)F.m);
-    fold_normalize_kernel<<<grid, 128, 0, st>>>(F);
-    return cudaGetLastError();
+    if (F.s > kMaxSlices || (F.ldD % 4) != 0) return cudaErrorInvalidValue;
+    if (fold_smem(F.s, 256) <= 112 * 1024) return fold_launch_t<256>(F, st);     // 2 blocks / SM
+    if (fold_smem(F.s, 256) <= 220 * 1024) return fold_launch_t<256>(F, st);
+    return fold_launch_t<64>(F, st);                                              // s up to 1024
 }
 
 __global__ void zero_output_kernel(DMatOut C, int64_t m, int64_t n, int L) {

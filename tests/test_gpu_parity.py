@@ -94,8 +94,12 @@ def test_simt_crosscheck_and_forced_slices(method, monkeypatch):
         monkeypatch.setenv("MPCGEMM_SLICEGEMM_SIMT", "1")
         C2, r2 = run_gpu(A, B, prec, method, s)
         monkeypatch.delenv("MPCGEMM_SLICEGEMM_SIMT")
-        assert r1["slices"] == r2["slices"]
+        monkeypatch.setenv("MPCGEMM_G2", "0")                  # single-diagonal units only
+        C3, r3 = run_gpu(A, B, prec, method, s)
+        monkeypatch.delenv("MPCGEMM_G2")
+        assert r1["slices"] == r2["slices"] == r3["slices"]
         assert same_bits(C1, C2), (s, first_mismatch(C1, C2))
+        assert same_bits(C1, C3), (s, first_mismatch(C1, C3))
         if s:
             si, sj = sample_idx(m, n, 60, seed=s)
             Rs = oracle.ozaki(A, B, prec, method, s, samples=(si, sj))
@@ -112,7 +116,9 @@ def test_small_chunks_equal_default(monkeypatch):
     C2, _ = run_gpu(A, B, prec, "4M")
     monkeypatch.setenv("MPCGEMM_BN", "128")
     C3, _ = run_gpu(A, B, prec, "4M")
-    assert same_bits(C1, C2) and same_bits(C1, C3)
+    monkeypatch.setenv("MPCGEMM_G2", "0")
+    C4, _ = run_gpu(A, B, prec, "4M")
+    assert same_bits(C1, C2) and same_bits(C1, C3) and same_bits(C1, C4)
 
 
 @pytest.mark.parametrize("spread,k", [(16, 12), (16, 3), (0, 64), (4, 40)])
@@ -258,3 +264,15 @@ def test_config5_lu_updates_sampled():
         si, sj = sample_idx(mm, nn, 12, seed=j)
         Rs = oracle.ozaki(L21, U12, 768, "3M", rep["slices"], samples=(si, sj))
         assert sampled_equal(C, Rs, si, sj) is None
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_large_forced_slices(method):
+    """s = 420 (fold with a 64-thread block; W = 3357 bits): sampled bit-exact."""
+    m, n, k, prec = 40, 70, 20, 128
+    A = mpgen.random_cmat(8, 1, m, k, prec, 30)
+    B = mpgen.random_cmat(8, 2, k, n, prec, 30)
+    C, rep = run_gpu(A, B, prec, method, 420)
+    si, sj = sample_idx(m, n, 30, seed=5)
+    Rs = oracle.ozaki(A, B, prec, method, 420, samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
