@@ -57,7 +57,7 @@ def lib():
             L.orc_exponents.argtypes = [i64, i64, i64, P, P, P, P, vp, vp, vp, vp]
             L.orc_split.argtypes = [ctypes.c_int, i64, i64, P, P, i32, i32, vp]
             L.orc_split.restype = ctypes.c_int
-            L.orc_rho_bounds.argtypes = [i64, i64, i64, P, P, P, P, vp, i32]
+            L.orc_rho_bounds.argtypes = [i64, i64, i64, P, P, P, P, vp, i32, i32]
             L.orc_rho_bounds.restype = ctypes.c_int
             L.orc_slices_for.argtypes = [i32, i32, i64, i64, i64, i64]
             L.orc_slices_for.restype = ctypes.c_int32
@@ -142,13 +142,13 @@ def rho_minT(A: CMat, B: CMat, nthreads: int = 0) -> int:
     return rho_bounds(A, B, nthreads)[0]
 
 
-def rho_bounds(A: CMat, B: CMat, nthreads: int = 0):
+def rho_bounds(A: CMat, B: CMat, nthreads: int = 0, full: int = 0):
     """(minT, minT1, maxD2): the integers of the two-stage rho-hat pre-pass."""
     m, k = A.shape
     n = B.shape[1]
     out = (ctypes.c_int64 * 3)()
     a = [_rm(A.re), _rm(A.im), _rm(B.re), _rm(B.im)]
-    rc = lib().orc_rho_bounds(m, n, k, *[_ptr(x) for x in a], ctypes.addressof(out), nthreads)
+    rc = lib().orc_rho_bounds(m, n, k, *[_ptr(x) for x in a], ctypes.addressof(out), nthreads, full)
     if rc:
         raise RuntimeError(f"orc_rho_bounds returned {rc}")
     return tuple(int(v) for v in out)

@@ -602,10 +602,11 @@ static int entry_mpexp(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64
  * out[0] = min_ij T_ij (-1: no pair).  If out[0] == 0 the combined rule needs, with each
  * pair assigned to bound 2 iff T_ij == 0 or (D_ij < 12 and T_ij 2^D_ij < 2^12):
  * out[1] = min T_ij over bound-1 pairs (-1: none), out[2] = max D_ij over bound-2 pairs
- * (-1: none).  When out[0] != 0, out[1] = out[0] and out[2] = -1. */
+ * (-1: none).  When out[0] != 0 and !full, out[1] = out[0] and out[2] = -1 (full: the
+ * bound-1 / bound-2 split is always reported; used by multi-rank reductions). */
 int orc_rho_bounds(int64_t m, int64_t n, int64_t k,
                    const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
-                   int64_t *out, int32_t nthreads)
+                   int64_t *out, int32_t nthreads, int32_t full)
 {
     int64_t *eA = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m + 1)), *eB = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
     uint8_t *nzA = (uint8_t *)malloc((size_t)m + 1), *nzB = (uint8_t *)malloc((size_t)n + 1);
@@ -657,7 +658,7 @@ int orc_rho_bounds(int64_t m, int64_t n, int64_t k,
         }
     }
     out[0] = mn;
-    if (mn != 0) { out[1] = mn; out[2] = -1; } else { out[1] = mn1; out[2] = mx2; }
+    if (mn != 0 && !full) { out[1] = mn; out[2] = -1; } else { out[1] = mn1; out[2] = mx2; }
     free(eA); free(eB); free(nzA); free(nzB); free(t); free(u); free(ea); free(eb); free(za); free(zb);
     return rc;
 }

@@ -62,20 +62,29 @@ def gather_rows(local: torch.Tensor, m: int, device, group=None) -> torch.Tensor
     return torch.cat([parts[r][: row_range(m, r, world)[1] - row_range(m, r, world)[0]] for r in range(world)], 0)
 
 
+def orchestrate(bounds_fn, slices_fn, local_fn, prec: int, method, k: int, device="cpu", group=None):
+    """The per-rank protocol, independent of where the compute runs: agree on s through the
+    pre-pass all-reduce, then compute this rank's rows with it.  Returns (s, bounds, local)."""
+    s, bounds = common_slices(bounds_fn, slices_fn, prec, method, k, device=device, group=group)
+    return s, bounds, local_fn(s)
+
+
 def gemm(A_local: "_m.DevCMat", B: "_m.DevCMat", m: int, prec: int | None = None, method="3M",
          group=None, gather: bool = False, stream=None, timing: int = 0):
-    """C rows of this rank := A_local B with the globally agreed s; optionally gathers all of C
-    (as torch tensors) onto every rank.  Returns (C_local DevCMat, report, C_full or None)."""
+    """C rows of this rank := A_local B with the globally agreed s (NCCL all-reduce of the
+    pre-pass integers); optionally all-gathers every C row block onto every rank (as torch
+    tensors).  Returns (C_local DevCMat, report, C_full dict or None)."""
     prec = A_local.prec if prec is None else prec
     k = B.shape[0]
-    s, bounds = common_slices(lambda full: _m.mpcgemm_rho_bounds(A_local, B, prec, full, stream=stream),
-                              _m.mpcgemm_slices_for, prec, method, k, device=A_local.re.sign.device, group=group)
-    C = _m.empty_device(A_local.shape[0], B.shape[1], prec, device=A_local.re.sign.device)
-    rep = _m.mpcgemm_ex(A_local, B, C, prec, method, slices=s, stream=stream, timing=timing)
+    dev = A_local.re.sign.device
+    C = _m.empty_device(A_local.shape[0], B.shape[1], prec, device=dev)
+    s, bounds, rep = orchestrate(lambda full: _m.mpcgemm_rho_bounds(A_local, B, prec, full, stream=stream),
+                                 _m.mpcgemm_slices_for,
+                                 lambda s_: _m.mpcgemm_ex(A_local, B, C, prec, method, slices=s_, stream=stream, timing=timing),
+                                 prec, method, k, device=dev, group=group)
     rep["bounds"] = bounds
     full = None
     if gather:
-        dev = A_local.re.sign.device
         full = {p: {f: gather_rows(getattr(getattr(C, p), f), m, dev, group) for f in ("sign", "exp", "limbs")}
                 for p in ("re", "im")}
     return C, rep, full

@@ -1,0 +1,78 @@
+"""Multi-rank host logic of the driver (paper_2307_06072_b200/dist.py) on CPU with gloo,
+world size 2: row partition, the two-round all-reduce of the pre-pass integers (common s),
+and the all-gather of C row blocks.  The per-rank compute is a stand-in (the oracle: tests
+may call it); on GPUs the same protocol runs with the C ABI over NCCL."""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import mpgen
+import oracle
+from paper_2307_06072_b200.dist import gather_rows, orchestrate, row_range
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _to_t(R):
+    return {"sign": torch.from_numpy(R.sign.copy()), "exp": torch.from_numpy(R.exp.copy()),
+            "limbs": torch.from_numpy(R.limbs.view(np.int64).copy())}
+
+
+def _worker(rank, world, port, case, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, n, k, prec, spread, method = case
+    A = mpgen.random_cmat(77, 1, m, k, prec, spread, zero_frac=0.1)
+    B = mpgen.random_cmat(77, 2, k, n, prec, spread, zero_frac=0.1)
+    r0, r1 = row_range(m, rank, world)
+    Al = A.rows(r0, r1)
+    s, bounds, C = orchestrate(lambda full: oracle.rho_bounds(Al, B, full=full),
+                               lambda *a: oracle.slices_for(*a)[0],
+                               lambda s_: oracle.ozaki(Al, B, prec, method, s_),
+                               prec, method, k)
+    full = {p: {f: gather_rows(t, m, "cpu") for f, t in _to_t(getattr(C, p)).items()} for p in ("re", "im")}
+    if rank == 0:
+        np.savez(os.path.join(outdir, "out.npz"), s=s, b0=bounds[0], b1=bounds[1], b2=bounds[2],
+                 **{f"{p}_{f}": full[p][f].numpy() for p in ("re", "im") for f in ("sign", "exp", "limbs")})
+    dist.destroy_process_group()
+
+
+def test_row_range_partition():
+    for m in (0, 1, 7, 8, 2048, 2049):
+        for w in (1, 2, 3, 8):
+            rr = [row_range(m, r, w) for r in range(w)]
+            assert rr[0][0] == 0 and rr[-1][1] == m
+            assert all(rr[i][1] == rr[i + 1][0] for i in range(w - 1))
+            assert max(b - a for a, b in rr) - min(b - a for a, b in rr) <= 1
+
+
+@pytest.mark.parametrize("case", [(7, 9, 11, 128, 4, "3M"),      # ragged rows
+                                  (9, 6, 12, 256, 16, "4M"),     # minT == 0: second round
+                                  (1, 5, 8, 128, 0, "3M")])      # one rank without rows
+def test_two_ranks_gloo(case):
+    m, n, k, prec, spread, method = case
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), case, d), nprocs=2, join=True)
+        z = np.load(os.path.join(d, "out.npz"))
+        A = mpgen.random_cmat(77, 1, m, k, prec, spread, zero_frac=0.1)
+        B = mpgen.random_cmat(77, 2, k, n, prec, spread, zero_frac=0.1)
+        s_ref, _ = oracle.auto_slices(A, B, prec, method)
+        assert int(z["s"]) == s_ref                    # same s as one process on all rows
+        R = oracle.ozaki(A, B, prec, method, s_ref)
+        for p in ("re", "im"):
+            Rp = getattr(R, p)
+            assert np.array_equal(z[f"{p}_sign"], Rp.sign)
+            assert np.array_equal(z[f"{p}_exp"], Rp.exp)
+            assert np.array_equal(z[f"{p}_limbs"].view(np.uint64), Rp.limbs)
