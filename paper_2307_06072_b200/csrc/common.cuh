@@ -48,13 +48,26 @@ struct JobDesc {
     int32_t pb[kMaxPairs];   // B-side digit part
 };
 
+// int32 partial planes, tile-blocked: [128-row block][256-column strip][slot][128][256].  One
+// GEMM unit writes one contiguous 128 KB block (write locality); the fold's 128 blocks of one
+// (row block, strip) run together and stream every slot block.  Slots are numbered in the
+// fold's consumption order (r = s+1..2, job, chunk).
+constexpr int kStrip = 256;
+constexpr int kRowBlk = 128;
+constexpr int64_t kTileElems = (int64_t)kRowBlk * kStrip;
+__host__ __device__ __forceinline__ int64_t part_off(int64_t row, int64_t col, int64_t slot, int64_t nslots,
+                                                     int64_t nstrips) {
+    return (((row >> 7) * nstrips + (col >> 8)) * nslots + slot) * kTileElems + (row & (kRowBlk - 1)) * kStrip +
+           (col & (kStrip - 1));
+}
+
 struct GemmParams {
     const WorkUnit *units;     // global order: size-descending, tiles of one (job, r, chunk) contiguous
     int32_t nunits;
     int32_t *counter;          // dynamic scheduler: next unit (zeroed before each launch)
-    int32_t *partials;         // [nslots][m][ldD]
-    int64_t ldD;               // partial row pitch (entries)
-    int64_t plane;             // m * ldD
+    int32_t *partials;         // part_off layout
+    int64_t nslots;            // partial planes
+    int64_t nstrips;           // ceil(n / 256)
     int32_t m, n;
     int32_t s;                 // slices
     int32_t KB;                // k-blocks per digit plane row
@@ -113,6 +126,17 @@ MPC_DEV void tma_load_3d(void *dst, const void *tmap, uint64_t *bar, int c0, int
 MPC_DEV void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// L2 cache policies (createpolicy) and a 16-byte store carrying one
+MPC_DEV uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+MPC_DEV void st_global_v4_hint(void *ptr, int a, int b, int c, int d, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;"
+                 ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d), "l"(pol) : "memory");
 }
 
 // ---------------------------------------------------------------- tcgen05

@@ -31,15 +31,15 @@ cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int
                                   const int64_t *eline, int8_t *t, int32_t *rel, cudaStream_t st);
 
 // a-2: stage 1 (out[0] = min T over nonzero line pairs) and stage 2 (minT_sup, minT1, maxD2)
-cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t plane, int64_t ldD,
+cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t nstrips,
                                   int64_t m, int64_t n, int64_t k, int64_t kp,
                                   const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA, const int32_t *relB,
                                   int stage, unsigned long long *out_min, unsigned long long *out_min1,
                                   long long *out_max2, cudaStream_t st);
 
 struct FoldParams {
-    const int32_t *partials;
-    int64_t plane, ldD;
+    const int32_t *partials;     // part_off layout
+    int64_t nslots, nstrips;
     int64_t m, n;
     int32_t s, method, prec, L;
     const int32_t *slotinfo;     // [(job*(s+2) + r)*2 + {0 base, 1 count}]

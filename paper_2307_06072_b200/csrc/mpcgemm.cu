@@ -156,43 +156,44 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
     const int64_t KB = (key.k + kBK - 1) / kBK;
     const int64_t tiles_m = (key.m + 127) / 128, tiles_n = (key.n + key.BN - 1) / key.BN;
     std::vector<int32_t> slotinfo((size_t)kMaxJobs * (s + 2) * 2, 0);
-    std::vector<WorkUnit> units;
+    const std::vector<Segment> segs = diag_segments(P, KB, s, key.method, key.maxkb, key.g2);
+    // slot numbers follow the fold's consumption order: r = s+1 .. 2, job, chunk
+    for (const Segment &sg : segs)
+        for (int d = 0; d < sg.G; d++) slotinfo[(sg.q * (s + 2) + sg.r + d) * 2 + 1] = (int32_t)sg.nch;
     int nslots = 0;
-    for (const Segment &sg : diag_segments(P, KB, s, key.method, key.maxkb, key.g2)) {
+    const int rtop = key.method == 0 ? 2 : s + 1;
+    for (int r = rtop; r >= 2; r--)
+        for (int q = 0; q < P.njobs; q++) {
+            slotinfo[(q * (s + 2) + r) * 2] = nslots;
+            nslots += slotinfo[(q * (s + 2) + r) * 2 + 1];
+        }
+    auto base = [&](int q, int r) { return slotinfo[(q * (s + 2) + r) * 2]; };
+    std::vector<WorkUnit> units;
+    for (const Segment &sg : segs) {
         const int q = sg.q, r = sg.r;
         const int64_t np = P.jobs[q].npairs;
         if (sg.G == 2) {
-            slotinfo[(q * (s + 2) + r) * 2] = nslots;
-            slotinfo[(q * (s + 2) + r) * 2 + 1] = (int32_t)sg.nch;
-            slotinfo[(q * (s + 2) + r + 1) * 2] = nslots + (int32_t)sg.nch;
-            slotinfo[(q * (s + 2) + r + 1) * 2 + 1] = (int32_t)sg.nch;
             for (int64_t c = 0; c < sg.nch; c++) {
                 const int32_t a = (int32_t)(c * KB / sg.nch), b = (int32_t)((c + 1) * KB / sg.nch);
                 for (int64_t tm = 0; tm < tiles_m; tm++)
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
                         units.push_back({q | (2 << 8), (int32_t)tm, (int32_t)tn, r, a, b,
-                                         nslots + (int32_t)c, nslots + (int32_t)(sg.nch + c)});
+                                         base(q, r) + (int32_t)c, base(q, r + 1) + (int32_t)c});
                         P.mma += np * (b - a) * (2 * r - 1) * (kBK / 32);
                     }
             }
-            nslots += 2 * (int)sg.nch;
         } else {
             const int64_t G = np * (r - 1) * KB;
-            slotinfo[(q * (s + 2) + r) * 2] = nslots;
-            slotinfo[(q * (s + 2) + r) * 2 + 1] = (int32_t)sg.nch;
             for (int64_t c = 0; c < sg.nch; c++) {
                 const int32_t a = (int32_t)(c * G / sg.nch), b = (int32_t)((c + 1) * G / sg.nch);
                 for (int64_t tm = 0; tm < tiles_m; tm++)
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
-                        units.push_back({q | (1 << 8), (int32_t)tm, (int32_t)tn, r, a, b, nslots + (int32_t)c, -1});
+                        units.push_back({q | (1 << 8), (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
                         P.mma += (int64_t)(b - a) * (kBK / 32);
                     }
             }
-            nslots += (int)sg.nch;
         }
     }
-    // global order for the dynamic scheduler: longest first (LPT tail), stable so that the
-    // tiles of one (job, r, chunk) stay contiguous and co-running CTAs share operand planes
     auto work = [&](const WorkUnit &w) -> int64_t {
         return unit_G(w) == 2 ? (int64_t)P.jobs[unit_job(w)].npairs * (w.b - w.a) * (2 * w.r - 1) : (int64_t)(w.b - w.a);
     };
@@ -271,7 +272,7 @@ struct Layout {
     size_t meta;      // eA, eB, nz, flags, prepass outputs
     size_t pre;       // pre-pass planes + T partials
     size_t main;      // digit planes + partials
-    int64_t kp, ldD;
+    int64_t kp, nstrips;
 };
 
 int tile_bn(int64_t n) { return n > 128 ? 256 : 128; }
@@ -316,18 +317,18 @@ int64_t count_slots(int64_t k, int s, int method, int maxkb) {
 Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb) {
     Layout Lo;
     Lo.kp = align_up((size_t)std::max<int64_t>(k, 1), 16);
-    Lo.ldD = align_up((size_t)std::max<int64_t>(n, 1), 4);
+    Lo.nstrips = (std::max<int64_t>(n, 1) + kStrip - 1) / kStrip;
     Lo.meta = align_up(8 * (m + n) + (m + n) + 64, 256) + 256;
     const int64_t KB = (k + kBK - 1) / kBK;
     const int64_t nslotsT = (KB + exact_cap() - 1) / exact_cap();
     Lo.pre = align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256) +
-             align_up((size_t)nslotsT * m * Lo.ldD * 4, 256);
+             align_up((size_t)nslotsT * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256);
     Lo.main = 0;
     if (s > 0) {
         const int parts = method == 3 ? 3 : 2;
         const int64_t nslots = count_slots(k, s, method, maxkb);
         Lo.main = align_up((size_t)parts * s * m * Lo.kp, 256) + align_up((size_t)parts * s * n * Lo.kp, 256) +
-                  align_up((size_t)nslots * m * Lo.ldD * 4, 256);
+                  align_up((size_t)nslots * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256);
     }
     return Lo;
 }
@@ -355,7 +356,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     SliceGemmLaunch SL;
     memset(&SL, 0, sizeof(SL));
     SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
-    SL.P.partials = T; SL.P.ldD = Lo.ldD; SL.P.plane = m * Lo.ldD;
+    SL.P.partials = T; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
     SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = 1; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
     SL.P.partsA = SL.P.partsB = 1;
     for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
@@ -364,7 +365,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     CK(slicegemm_launch(SL, st));
     unsigned long long init[3] = {~0ull, ~0ull, (unsigned long long)-1ll};
     CK(cudaMemcpyAsync(omin, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    CK(prepass_reduce_launch(T, plan->nslots, m * Lo.ldD, Lo.ldD, m, n, k, Lo.kp, nzA, nzB, relA, relB, 1,
+    CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, nzA, nzB, relA, relB, 1,
                              omin, omin1, omax2, st));
     unsigned long long h[3];
     CK(cudaMemcpyAsync(h, omin, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -373,7 +374,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     if (minraw > 0 && !full) { out[0] = minraw; out[1] = minraw; out[2] = -1; return 0; }
     if (minraw < 0) { out[0] = -1; out[1] = -1; out[2] = -1; return 0; }
     CK(cudaMemcpyAsync(omin, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    CK(prepass_reduce_launch(T, plan->nslots, m * Lo.ldD, Lo.ldD, m, n, k, Lo.kp, nzA, nzB, relA, relB, 2,
+    CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, nzA, nzB, relA, relB, 2,
                              omin, omin1, omax2, st));
     CK(cudaMemcpyAsync(h, omin, sizeof(h), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -426,7 +427,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     SliceGemmLaunch SL;
     memset(&SL, 0, sizeof(SL));
     SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
-    SL.P.partials = partials; SL.P.ldD = Lo.ldD; SL.P.plane = m * Lo.ldD;
+    SL.P.partials = partials; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
     SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = s; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
     SL.P.partsA = SL.P.partsB = parts;
     for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
@@ -435,7 +436,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     CK(slicegemm_launch(SL, st));
     if (E) CK(cudaEventRecord(E->ev[4], st));
     FoldParams F;
-    F.partials = partials; F.plane = m * Lo.ldD; F.ldD = Lo.ldD; F.m = m; F.n = n;
+    F.partials = partials; F.nslots = plan->nslots; F.nstrips = Lo.nstrips; F.m = m; F.n = n;
     F.s = s; F.method = method; F.prec = prec; F.L = L; F.slotinfo = plan->d_slotinfo;
     F.eA = eA; F.eB = eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
     CK(fold_normalize_launch(F, st));

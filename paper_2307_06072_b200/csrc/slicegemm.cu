@@ -184,6 +184,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers -> int32 partial planes
         const int q = warp & 3;                               // TMEM lane quarter of this warp
+        const uint64_t pol = l2_policy_evict_first();         // partials: streaming, keep operands in L2
         uint32_t tphase = 0;
         int qs = 0; uint32_t qph = 0;
         for (;;) {
@@ -198,21 +199,19 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             tc_fence_after();
             const int row = w.tm * kBM + q * 32 + lane;
             for (int acc = 0; acc < unit_G(w); acc++) {
-                int32_t *out = P.partials + (int64_t)(acc ? w.slot1 : w.slot0) * P.plane + (int64_t)row * P.ldD;
+                const int64_t slot = acc ? w.slot1 : w.slot0;
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; c++) {
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
                     tmem_ld_wait();
-                    const int col0 = w.tn * BN + c * 32;
+                    const int col0 = w.tn * BN + c * 32;      // 32 columns inside one 256-column strip
                     if (row < P.m) {
+                        int32_t *out = P.partials + part_off(row, col0, slot, P.nslots, P.nstrips);
 #pragma unroll
-                        for (int g4 = 0; g4 < 8; g4++) {
-                            if (col0 + 4 * g4 < P.ldD) {
-                                int4 val = make_int4((int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2], (int)v[4 * g4 + 3]);
-                                *reinterpret_cast<int4 *>(out + col0 + 4 * g4) = val;
-                            }
-                        }
+                        for (int g4 = 0; g4 < 8; g4++)
+                            st_global_v4_hint(out + 4 * g4, (int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2],
+                                              (int)v[4 * g4 + 3], pol);
                     }
                 }
             }
@@ -297,7 +296,7 @@ slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict_
             const int64_t row = row0 + ty * 4 + e, col = col0 + tx;
             const int slot = a ? w.slot1 : w.slot0;
             // G = 2 keeps D_r in acc[0] and D_{r+1} in acc[1]
-            if (row < P.m && col < P.ldD) P.partials[(int64_t)slot * P.plane + row * P.ldD + col] = acc[a][e];
+            if (row < P.m && col < P.nstrips * kStrip) P.partials[part_off(row, col, slot, P.nslots, P.nstrips)] = acc[a][e];
         }
 }
 

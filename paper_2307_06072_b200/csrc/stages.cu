@@ -146,7 +146,7 @@ struct WordStream {
 constexpr int kSplitVec = 4;
 constexpr uint64_t kH = 0x8080808080808080ull;
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
 split_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
              const int64_t *__restrict__ eline, int s, int nparts, int8_t *__restrict__ dig)
 {
@@ -297,14 +297,14 @@ cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int
     return cudaGetLastError();
 }
 
-MPC_DEV int64_t sum_T(const int32_t *T, int nslots, int64_t plane, int64_t off) {
+MPC_DEV int64_t sum_T(const int32_t *T, int nslots, int64_t nstrips, int64_t i, int64_t j) {
     int64_t v = 0;
-    for (int q = 0; q < nslots; q++) v += T[(int64_t)q * plane + off];
+    for (int q = 0; q < nslots; q++) v += T[part_off(i, j, q, nslots, nstrips)];
     return v;
 }
 
 // stage 1: min over nonzero line pairs of T_ij
-__global__ void prepass_min_kernel(const int32_t *T, int nslots, int64_t plane, int64_t ldD, int64_t m, int64_t n,
+__global__ void prepass_min_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
                                    const uint8_t *nzA, const uint8_t *nzB, unsigned long long *out_min)
 {
     unsigned long long best = ULLONG_MAX;
@@ -312,7 +312,7 @@ __global__ void prepass_min_kernel(const int32_t *T, int nslots, int64_t plane, 
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / n, j = t - i * n;
         if (!nzA[i] || !nzB[j]) continue;
-        const unsigned long long v = (unsigned long long)sum_T(T, nslots, plane, i * ldD + j);
+        const unsigned long long v = (unsigned long long)sum_T(T, nslots, nstrips, i, j);
         best = v < best ? v : best;
     }
 #pragma unroll
@@ -325,7 +325,7 @@ __global__ void prepass_min_kernel(const int32_t *T, int nslots, int64_t plane, 
 
 // stage 2: exact max-plus exponent bound and the per-pair bound choice
 __global__ void __launch_bounds__(256)
-prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t plane, int64_t ldD, int64_t m, int64_t n,
+prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
                        int64_t k, int64_t kp, const uint8_t *nzA, const uint8_t *nzB,
                        const int32_t *relA, const int32_t *relB,
                        unsigned long long *out_min, unsigned long long *out_min1, long long *out_max2)
@@ -358,7 +358,7 @@ prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t plane, int64_t ldD,
         const int64_t i = i0 + ty * 4 + e, j = j0 + tx;
         if (i >= m || j >= n || !nzA[i] || !nzB[j]) continue;
         if (mp[e] <= kRelSentinel) continue;                // no common support: (|A||B|)_ij = 0
-        const int64_t Tv = sum_T(T, nslots, plane, i * ldD + j);
+        const int64_t Tv = sum_T(T, nslots, nstrips, i, j);
         const int64_t D = -(int64_t)mp[e];
         lmin = (unsigned long long)Tv < lmin ? (unsigned long long)Tv : lmin;
         const bool use2 = (Tv == 0) || (D < 12 && (Tv << D) < 4096);
@@ -378,7 +378,7 @@ prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t plane, int64_t ldD,
     }
 }
 
-cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t plane, int64_t ldD,
+cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t nstrips,
                                   int64_t m, int64_t n, int64_t k, int64_t kp,
                                   const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA, const int32_t *relB,
                                   int stage, unsigned long long *out_min, unsigned long long *out_min1,
@@ -388,10 +388,10 @@ cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t plane, i
     if (stage == 1) {
         int64_t blocks = (m * n + 255) / 256;
         if (blocks > 148 * 16) blocks = 148 * 16;
-        prepass_min_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, nslots, plane, ldD, m, n, nzA, nzB, out_min);
+        prepass_min_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, nslots, nstrips, m, n, nzA, nzB, out_min);
     } else {
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
-        prepass_maxplus_kernel<<<grid, 256, 0, st>>>(T, nslots, plane, ldD, m, n, k, kp, nzA, nzB, relA, relB,
+        prepass_maxplus_kernel<<<grid, 256, 0, st>>>(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB,
                                                      out_min, out_min1, out_max2);
     }
     return cudaGetLastError();
@@ -484,7 +484,8 @@ MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, int 
 // the order r = s+1..2, job, chunk) the contiguous strip partials[slot][i][j0 .. j0+T) lands in
 // a RING-deep shared-memory ring, so ~RING KB per block are in flight regardless of the
 // consumers' registers.  T consumer threads (one output j each) run the carry chains.
-constexpr int kFoldRing = 24;
+constexpr int kFoldRing = 4;           // entries
+constexpr int kFoldPer = 8;            // slots per entry (one 8 KB bulk copy at T = 256)
 
 template <int kFoldT>
 __global__ void __launch_bounds__(kFoldT + 32)
@@ -493,8 +494,8 @@ fold_normalize_kernel(const FoldParams F)
     extern __shared__ __align__(128) uint8_t fsm_raw[];
     const int s = F.s;
     const int Lc = s / 8 + 3;
-    int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                       // [RING][T]
-    uint64_t *fix = reinterpret_cast<uint64_t *>(fsm_raw + kFoldRing * kFoldT * 4);  // [2][Lc][T]
+    int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                       // [RING][PER][T]
+    uint64_t *fix = reinterpret_cast<uint64_t *>(fsm_raw + kFoldRing * kFoldPer * kFoldT * 4);  // [2][Lc][T]
     int32_t *slots = reinterpret_cast<int32_t *>(fix + 2 * (int64_t)Lc * kFoldT);  // [job][r][base,cnt]
     uint64_t *full = reinterpret_cast<uint64_t *>(slots + kMaxJobs * (s + 2) * 2 + 2);
     full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
@@ -508,25 +509,26 @@ fold_normalize_kernel(const FoldParams F)
         fence_barrier_init();
     }
     __syncthreads();
-    const int64_t i = blockIdx.y;
-    const int64_t j0 = (int64_t)blockIdx.x * kFoldT;
+    // block (x, y): row i = (y / nsub) * 128 + x, columns j0 = (y % nsub) * T, so the 128 blocks
+    // of one (row block, strip) are adjacent in launch order
+    const int64_t nsub = (F.n + kFoldT - 1) / kFoldT;
+    const int64_t i = (int64_t)(blockIdx.y / nsub) * kRowBlk + blockIdx.x;
+    const int64_t j0 = (int64_t)(blockIdx.y % nsub) * kFoldT;   // kFoldT divides the 256-column strip
+    if (i >= F.m) return;
     if (warp == kFoldT / 32) {
-        // ---------------- producer warp
+        // ---------------- producer warp: streams this (row, strip)'s slots 0..nslots-1 (the
+        // consumption order) into the ring, kFoldPer slots per entry, one expect_tx per entry
         if (lane == 0) {
-            const int64_t cols = F.ldD - j0 < kFoldT ? F.ldD - j0 : kFoldT;     // ldD % 4 == 0
-            const uint32_t bytes = (uint32_t)(cols * 4);
-            const int32_t *row = F.partials + i * F.ldD + j0;
+            const int32_t *region = F.partials + part_off(i, j0, 0, F.nslots, F.nstrips);   // slot 0
             int e = 0; uint32_t ph = 0;
-            for (int r = s + 1; r >= 2; r--)
-                for (int q = 0; q < kMaxJobs; q++) {
-                    const int base = slots[(q * (s + 2) + r) * 2], cnt = slots[(q * (s + 2) + r) * 2 + 1];
-                    for (int c = 0; c < cnt; c++) {
-                        mbar_wait(&empty[e], ph ^ 1);
-                        mbar_arrive_expect_tx(&full[e], bytes);
-                        bulk_load(ring + e * kFoldT, row + (int64_t)(base + c) * F.plane, bytes, &full[e]);
-                        if (++e == kFoldRing) { e = 0; ph ^= 1; }
-                    }
-                }
+            for (int64_t sl = 0; sl < F.nslots; sl += kFoldPer) {
+                const int cnt = (int)(F.nslots - sl < kFoldPer ? F.nslots - sl : kFoldPer);
+                mbar_wait(&empty[e], ph ^ 1);
+                mbar_arrive_expect_tx(&full[e], (uint32_t)(cnt * kFoldT * 4));
+                for (int f = 0; f < cnt; f++)                   // slot blocks are kTileElems apart
+                    bulk_load(ring + (e * kFoldPer + f) * kFoldT, region + (sl + f) * kTileElems, kFoldT * 4, &full[e]);
+                if (++e == kFoldRing) { e = 0; ph ^= 1; }
+            }
         }
         return;
     }
@@ -534,7 +536,7 @@ fold_normalize_kernel(const FoldParams F)
     const int64_t j = j0 + tid;
     uint64_t cur0 = 0, cur1 = 0;
     int64_t c0 = 0, c1 = 0;
-    int e = 0; uint32_t ph = 0;
+    int e = 0, fill = 0; uint32_t ph = 0;
     uint64_t *fix0 = fix + tid, *fix1 = fix + (int64_t)Lc * kFoldT + tid;
     for (int r = s + 1; r >= 2; r--) {
         int64_t t[kMaxJobs];
@@ -543,11 +545,14 @@ fold_normalize_kernel(const FoldParams F)
             const int cnt = slots[(q * (s + 2) + r) * 2 + 1];
             int64_t v = 0;
             for (int c = 0; c < cnt; c++) {
-                mbar_wait(&full[e], ph);
-                v += ring[e * kFoldT + tid];
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[e]);
-                if (++e == kFoldRing) { e = 0; ph ^= 1; }
+                if (fill == 0) mbar_wait(&full[e], ph);
+                v += ring[(e * kFoldPer + fill) * kFoldT + tid];
+                if (++fill == kFoldPer) {
+                    fill = 0;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[e]);
+                    if (++e == kFoldRing) { e = 0; ph ^= 1; }
+                }
             }
             t[q] = v;
         }
@@ -587,7 +592,7 @@ fold_normalize_kernel(const FoldParams F)
 
 size_t fold_smem(int s, int T) {
     const int Lc = s / 8 + 3;
-    return (size_t)kFoldRing * T * 4 + (size_t)2 * Lc * T * 8 + (size_t)kMaxJobs * (s + 2) * 2 * 4 + 16 +
+    return (size_t)kFoldRing * kFoldPer * T * 4 + (size_t)2 * Lc * T * 8 + (size_t)kMaxJobs * (s + 2) * 2 * 4 + 16 +
            (size_t)2 * kFoldRing * 8 + 16;
 }
 
@@ -596,7 +601,7 @@ static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
     const size_t sm = fold_smem(F.s, T);
     cudaError_t e = cudaFuncSetAttribute(fold_normalize_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)((F.n + T - 1) / T), (unsigned)F.m);
+    dim3 grid(kRowBlk, (unsigned)(((F.n + T - 1) / T) * ((F.m + kRowBlk - 1) / kRowBlk)));
     fold_normalize_kernel<T><<<grid, T + 32, sm, st>>>(F);
     return cudaGetLastError();
 }
@@ -604,7 +609,7 @@ static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
 {
     if (F.m == 0 || F.n == 0) return cudaSuccess;
-    if (F.s > kMaxSlices || (F.ldD % 4) != 0) return cudaErrorInvalidValue;
+    if (F.s > kMaxSlices) return cudaErrorInvalidValue;
     if (fold_smem(F.s, 256) <= 112 * 1024) return fold_launch_t<256>(F, st);     // 2 blocks / SM
     if (fold_smem(F.s, 256) <= 220 * 1024) return fold_launch_t<256>(F, st);
     return fold_launch_t<64>(F, st);                                              // s up to 1024

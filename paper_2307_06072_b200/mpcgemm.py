@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpcgemm.so")
+LIB_PATH = os.environ.get("MPCGEMM_LIB") or os.path.join(_HERE, "libmpcgemm.so")   # override: A/B testing
 _lock = threading.Lock()
 _lib = None
 
