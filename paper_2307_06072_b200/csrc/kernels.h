@@ -11,6 +11,7 @@ struct SliceGemmLaunch {
     const int8_t *digA, *digB;   // [partsA*s][rowsA][kp], [partsB*s][rowsB][kp]
     int64_t rowsA, rowsB, kp;
     int grid;                    // CTAs (tcgen05 path)
+    int BM;                      // 128 (one CTA per tile) or 256 (CTA pair, cta_group::2)
     int BN;                      // 128 or 256
     int simt;                    // 1: dp4a cross-check kernel
     int nunits;

@@ -78,10 +78,10 @@ StageEvents *stage_events(int dev) {
 
 // ---------------------------------------------------------------- plans (work lists)
 struct PlanKey {
-    int64_t m, n, k; int s, method, BN, grid, simt, maxkb, g2;
+    int64_t m, n, k; int s, method, BM, BN, grid, simt, maxkb, g2, order;
     bool operator<(const PlanKey &o) const {
-        return std::tie(m, n, k, s, method, BN, grid, simt, maxkb, g2) <
-               std::tie(o.m, o.n, o.k, o.s, o.method, o.BN, o.grid, o.simt, o.maxkb, o.g2);
+        return std::tie(m, n, k, s, method, BM, BN, grid, simt, maxkb, g2, order) <
+               std::tie(o.m, o.n, o.k, o.s, o.method, o.BM, o.BN, o.grid, o.simt, o.maxkb, o.g2, o.order);
     }
 };
 struct Plan {
@@ -154,7 +154,7 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
     method_jobs(key.method, P);
     const int s = key.s;
     const int64_t KB = (key.k + kBK - 1) / kBK;
-    const int64_t tiles_m = (key.m + 127) / 128, tiles_n = (key.n + key.BN - 1) / key.BN;
+    const int64_t tiles_m = (key.m + key.BM - 1) / key.BM, tiles_n = (key.n + key.BN - 1) / key.BN;
     std::vector<int32_t> slotinfo((size_t)kMaxJobs * (s + 2) * 2, 0);
     const std::vector<Segment> segs = diag_segments(P, KB, s, key.method, key.maxkb, key.g2);
     // slot numbers follow the fold's consumption order: r = s+1 .. 2, job, chunk
@@ -197,8 +197,18 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
     auto work = [&](const WorkUnit &w) -> int64_t {
         return unit_G(w) == 2 ? (int64_t)P.jobs[unit_job(w)].npairs * (w.b - w.a) * (2 * w.r - 1) : (int64_t)(w.b - w.a);
     };
-    std::stable_sort(units.begin(), units.end(), [&](const WorkUnit &a, const WorkUnit &b) { return work(a) > work(b); });
-    const int grid = (int)std::min<int64_t>(key.grid, (int64_t)units.size());
+    if (key.order == 1) {
+        // job-major, then longest first: co-running units are neighbouring diagonal pairs of
+        // one job and read mostly the same digit planes; the tail is the last job's smallest
+        std::stable_sort(units.begin(), units.end(), [&](const WorkUnit &a, const WorkUnit &b) {
+            if (unit_job(a) != unit_job(b)) return unit_job(a) < unit_job(b);
+            return work(a) > work(b);
+        });
+    } else {
+        std::stable_sort(units.begin(), units.end(), [&](const WorkUnit &a, const WorkUnit &b) { return work(a) > work(b); });
+    }
+    int grid = (int)std::min<int64_t>(key.grid, (int64_t)units.size() * (key.BM == 256 ? 2 : 1));
+    if (key.BM == 256) grid = std::max(2, grid & ~1);          // CTA pairs
     const std::vector<WorkUnit> &flat = units;
     P.nunits = (int)flat.size(); P.nslots = nslots; P.grid = grid;
     if (P.nunits) {
@@ -279,9 +289,9 @@ int tile_bn(int64_t n) { return n > 128 ? 256 : 128; }
 
 // Load-balance target for the MMA k-blocks of one unit: at least ~4 units per CTA.  (The
 // INT32 exactness cap is separate: exact_cap().)
-int64_t chunk_kb(int64_t m, int64_t n, int64_t k, int s, int method, int BN, int grid) {
+int64_t chunk_kb(int64_t m, int64_t n, int64_t k, int s, int method, int BM, int BN, int grid) {
     const int64_t KB = (k + kBK - 1) / kBK;
-    const int64_t tiles = ((m + 127) / 128) * ((n + BN - 1) / BN);
+    const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN) * (BM / 128);   // in 128-row CTA tiles
     const int64_t npairs_total = method == 0 ? 1 : (method == 3 ? 3 : 4);
     const int64_t work = npairs_total * KB * (int64_t)s * (s + 1) / 2 * tiles;   // k-blocks
     int64_t target = work / (4 * (int64_t)grid);
@@ -294,14 +304,15 @@ int64_t exact_cap() {
     return e > 0 ? std::min<int64_t>(kMaxKBlocksPerChunk, e) : kMaxKBlocksPerChunk;
 }
 
-struct Geometry { int BN, grid, maxkb; };
+struct Geometry { int BM, BN, grid, maxkb; };
 
 Geometry main_geometry(int dev, int64_t m, int64_t n, int64_t k, int s, int method) {
     Geometry g;
     g.BN = env_int("MPCGEMM_BN", tile_bn(n));
     if (g.BN != 128 && g.BN != 256) g.BN = tile_bn(n);
+    g.BM = (g.BN == 256 && env_int("MPCGEMM_CTA2", 1)) ? 256 : 128;   // CTA pairs for wide tiles
     g.grid = sm_count(dev);
-    g.maxkb = (int)chunk_kb(m, n, k, s, method, g.BN, g.grid);
+    g.maxkb = (int)chunk_kb(m, n, k, s, method, g.BM, g.BN, g.grid);
     return g;
 }
 
@@ -350,7 +361,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     CK(prepass_planes_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, tB, relB, st));
     const int BN = tile_bn(n);
     const int grid = sm_count(dev);
-    PlanKey key{m, n, k, 1, 0, BN, grid, simt, (int)kMaxKBlocksPerChunk, 0};
+    PlanKey key{m, n, k, 1, 0, 128, BN, grid, simt, (int)kMaxKBlocksPerChunk, 0, 0};
     Plan *plan;
     if (int rc = build_plan(dev, key, &plan)) return rc;
     SliceGemmLaunch SL;
@@ -361,7 +372,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     SL.P.partsA = SL.P.partsB = 1;
     for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
     SL.digA = tA; SL.digB = tB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
-    SL.grid = plan->grid; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits; SL.units_flat = plan->d_units;
+    SL.grid = plan->grid; SL.BM = 128; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits; SL.units_flat = plan->d_units;
     CK(slicegemm_launch(SL, st));
     unsigned long long init[3] = {~0ull, ~0ull, (unsigned long long)-1ll};
     CK(cudaMemcpyAsync(omin, init, sizeof(init), cudaMemcpyHostToDevice, st));
@@ -421,7 +432,8 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     if (E) CK(cudaEventRecord(E->ev[3], st));
     const Geometry geo = main_geometry(dev, m, n, k, s, method);
     const int BN = geo.BN;
-    PlanKey key{m, n, k, s, method, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0};
+    PlanKey key{m, n, k, s, method, geo.BM, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0,
+                env_int("MPCGEMM_ORDER", 1)};
     Plan *plan;
     if (int rc = build_plan(dev, key, &plan)) return rc;
     SliceGemmLaunch SL;
@@ -432,7 +444,8 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     SL.P.partsA = SL.P.partsB = parts;
     for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
     SL.digA = digA; SL.digB = digB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
-    SL.grid = plan->grid; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits; SL.units_flat = plan->d_units;
+    SL.grid = plan->grid; SL.BM = geo.BM; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits;
+    SL.units_flat = plan->d_units;
     CK(slicegemm_launch(SL, st));
     if (E) CK(cudaEventRecord(E->ev[4], st));
     FoldParams F;

@@ -226,13 +226,232 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
+// ------------------------------------------------------------------ CTA-pair (cta_group::2) kernel
+// Same work units on 256 x 256 output tiles computed by a CTA pair: each CTA loads its 128 rows
+// of the A tile and its 128 rows of the B tile (32 KB per stage instead of 48 KB), the even CTA
+// issues tcgen05.mma.cta_group::2 (M = 256, N = 256) and each CTA's TMEM holds its 128 rows of
+// both accumulators.  The even CTA schedules units and forwards each index to its peer.
+template <int STAGES>
+struct Tc2Cfg {
+    static constexpr int BN = 256;                     // pair tile 256 x 256
+    static constexpr int A_BYTES = 128 * kBK;          // this CTA's half of the A tile
+    static constexpr int B_BYTES = 128 * kBK;          // this CTA's half of the B tile
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = 512;
+    static constexpr int QN = 8;
+    static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 512;
+};
+
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ GemmParams P)
+{
+    using Cfg = Tc2Cfg<STAGES>;
+    constexpr int BN = Cfg::BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + STAGES * Cfg::A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * Cfg::B_BYTES);   // leader's used
+    uint64_t *empty = full + STAGES;                  // both CTAs (multicast commit)
+    uint64_t *tfull = empty + STAGES;                 // both CTAs (multicast commit)
+    uint64_t *tempty = tfull + 1;                     // leader's used: 2 x 128 epilogue arrivals
+    uint64_t *qfull = tempty + 1;                     // both CTAs (leader producer arrives on both)
+    uint64_t *qempty = qfull + Cfg::QN;               // leader's used: 10 arrivals
+    int32_t *uq = reinterpret_cast<int32_t *>(qempty + Cfg::QN);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(uq + Cfg::QN);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < STAGES; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 2 * 128);
+        for (int i = 0; i < Cfg::QN; i++) { mbar_init(&qfull[i], 1); mbar_init(&qempty[i], 1 + 4 + 1 + 4); }
+        fence_barrier_init();
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+    }
+    if (warp == 1) tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t lead_qempty = mapa_rank(smem_u32(qempty), 0);
+    const uint32_t lead_tempty = mapa_rank(smem_u32(tempty), 0);
+    const uint32_t peer_uq = mapa_rank(smem_u32(uq), 1);
+    const uint32_t peer_qfull = mapa_rank(smem_u32(qfull), 1);
+    const int s = P.s, KB = P.KB;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- (leader) scheduler + both CTAs' TMA producers
+            int stage = 0; uint32_t phase = 0;
+            int qs = 0; uint32_t qph = 0;
+            auto load = [&](int planeA, int planeB, int kb, int tm, int tn) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+                tma_load_3d_2sm(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, tm * 256 + (int)rank * 128, planeA);
+                tma_load_3d_2sm(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, tn * 256 + (int)rank * 128, planeB);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            };
+            for (;;) {
+                int u;
+                if (rank == 0) {
+                    u = atomicAdd(P.counter, 1);
+                    if (u >= P.nunits) u = -1;
+                    mbar_wait_cluster(&qempty[qs], qph ^ 1);
+                    *reinterpret_cast<volatile int32_t *>(&uq[qs]) = u;
+                    st_remote_u32(peer_uq + 4 * qs, (uint32_t)u);
+                    mbar_arrive(&qfull[qs]);
+                    mbar_arrive_remote(peer_qfull + 8 * qs);
+                } else {
+                    mbar_wait_cluster(&qfull[qs], qph);
+                    u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
+                    mbar_arrive_remote(lead_qempty + 8 * qs);
+                }
+                if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
+                if (u < 0) break;
+                const WorkUnit w = P.units[u];
+                const JobDesc &J = P.jobs[unit_job(w)];
+                if (unit_G(w) == 2) {
+                    for (int pr = 0; pr < J.npairs; pr++)
+                        for (int kb = w.a; kb < w.b; kb++)
+                            for (int p = 1; p <= w.r; p++)          // A_p, B_{r+1-p}
+                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), kb, w.tm, w.tn);
+                } else {
+                    const int per_pair = (w.r - 1) * KB;
+                    for (int g = w.a; g < w.b; g++) {
+                        const int pair = g / per_pair;
+                        const int rem = g - pair * per_pair;
+                        const int p0 = rem / KB;
+                        const int kb = rem - p0 * KB;
+                        load(J.pa[pair] * s + p0, J.pb[pair] * s + (w.r - 2 - p0), kb, w.tm, w.tn);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            // ---------------- MMA issuer (leader CTA only)
+            constexpr uint32_t idesc = make_idesc_i8(256, BN);
+            const uint32_t d0 = tmem_base, d1 = tmem_base + (uint32_t)BN;
+            int stage = 0; uint32_t phase = 0;
+            uint32_t tphase = 0;
+            int qs = 0; uint32_t qph = 0;
+            for (;;) {
+                mbar_wait_cluster(&qfull[qs], qph);
+                const int u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
+                mbar_arrive(&qempty[qs]);
+                if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
+                if (u < 0) break;
+                const WorkUnit w = P.units[u];
+                const JobDesc &J = P.jobs[unit_job(w)];
+                mbar_wait_cluster(tempty, tphase ^ 1);
+                tc_fence_after();
+                if (unit_G(w) == 2) {
+                    int prev = 0;
+                    for (int pr = 0; pr < J.npairs; pr++)
+                        for (int kb = w.a; kb < w.b; kb++)
+                            for (int p = 1; p <= w.r; p++) {
+                                mbar_wait(&full[stage], phase);
+                                tc_fence_after();
+                                const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+                                const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+                                const bool first = (pr == 0 && kb == w.a);
+#pragma unroll
+                                for (int kk = 0; kk < kBK / 32; kk++)   // D_{r+1} += A_p B_{r+1-p}
+                                    mma_i8_2sm(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                               (first && p == 1 && kk == 0) ? 0u : 1u);
+                                if (p >= 2) {                           // D_r += A_{p-1} B_{r+1-p}
+                                    const uint32_t ap = smem_u32(sA + prev * Cfg::A_BYTES);
+#pragma unroll
+                                    for (int kk = 0; kk < kBK / 32; kk++)
+                                        mma_i8_2sm(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                                   (first && p == 2 && kk == 0) ? 0u : 1u);
+                                    mma_commit_2sm(&empty[prev]);
+                                }
+                                if (p == w.r) mma_commit_2sm(&empty[stage]);
+                                prev = stage;
+                                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                            }
+                } else {
+                    for (int g = w.a; g < w.b; g++) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 32; kk++)
+                            mma_i8_2sm(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                       (g > w.a || kk > 0) ? 1u : 0u);
+                        mma_commit_2sm(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+                mma_commit_2sm(tfull);                        // both CTAs' accumulators ready
+                tphase ^= 1;
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ---------------- epilogue (both CTAs): this CTA's 128 rows of the pair tile
+        const int q = warp & 3;
+        const uint64_t pol = l2_policy_evict_first();
+        uint32_t tphase = 0;
+        int qs = 0; uint32_t qph = 0;
+        for (;;) {
+            mbar_wait_cluster(&qfull[qs], qph);
+            const int u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0) mbar_arrive(&qempty[qs]);
+                else mbar_arrive_remote(lead_qempty + 8 * qs);
+            }
+            if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
+            if (u < 0) break;
+            const WorkUnit w = P.units[u];
+            mbar_wait(tfull, tphase);
+            tc_fence_after();
+            const int row = w.tm * 256 + (int)rank * 128 + q * 32 + lane;
+            for (int acc = 0; acc < unit_G(w); acc++) {
+                const int64_t slot = acc ? w.slot1 : w.slot0;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; c++) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+                    tmem_ld_wait();
+                    const int col0 = w.tn * BN + c * 32;
+                    if (row < P.m) {
+                        int32_t *out = P.partials + part_off(row, col0, slot, P.nslots, P.nstrips);
+#pragma unroll
+                        for (int g4 = 0; g4 < 8; g4++)
+                            st_global_v4_hint(out + 4 * g4, (int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2],
+                                              (int)v[4 * g4 + 3], pol);
+                    }
+                }
+            }
+            tc_fence_before();
+            if (rank == 0) mbar_arrive(tempty);
+            else mbar_arrive_remote(lead_tempty);
+            tphase ^= 1;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc_2sm<Cfg::TMEM_COLS>(tmem_base);
+}
+
 // ------------------------------------------------------------------ SIMT cross-check kernel
 // Same work list and output, computed with dp4a on CUDA cores (used by the tests to check
 // the tensor-core kernel bitwise; selected with MPCGEMM_SLICEGEMM_SIMT=1).  One CTA per
 // (unit, 32x32 subtile), one thread per 4 output elements of each accumulator.
 __global__ void __launch_bounds__(256)
 slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict__ digB,
-                      int64_t rowsA, int64_t rowsB, int64_t kp, const WorkUnit *units, int BN,
+                      int64_t rowsA, int64_t rowsB, int64_t kp, const WorkUnit *units, int BM, int BN,
                       const GemmParams P)
 {
     __shared__ int32_t sa[32][kBK / 4 + 1];
@@ -240,10 +459,10 @@ slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict_
     const WorkUnit w = units[blockIdx.x];
     const JobDesc &J = P.jobs[unit_job(w)];
     const int G = unit_G(w);
-    const int sub = blockIdx.y;                   // 32x32 subtile index within 128 x BN
-    const int sub_m = sub % (kBM / 32), sub_n = sub / (kBM / 32);
+    const int sub = blockIdx.y;                   // 32x32 subtile index within BM x BN
+    const int sub_m = sub % (BM / 32), sub_n = sub / (BM / 32);
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;   // 32 x 8
-    const int64_t row0 = (int64_t)w.tm * kBM + sub_m * 32;
+    const int64_t row0 = (int64_t)w.tm * BM + sub_m * 32;
     const int64_t col0 = (int64_t)w.tn * BN + sub_n * 32;
     int32_t acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
     // enumerate (accumulator, A plane, B plane, kb) exactly as the tensor-core kernel pairs them
@@ -342,13 +561,29 @@ static cudaError_t launch_tc(const SliceGemmLaunch &L, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+template <int STAGES>
+static cudaError_t launch_tc2(const SliceGemmLaunch &L, cudaStream_t st) {
+    using Cfg = Tc2Cfg<STAGES>;
+    CUtensorMap ta, tb;
+    if (make_plane_map(&ta, L.digA, (int64_t)L.P.partsA * L.P.s, L.rowsA, L.kp, 128)) return cudaErrorInvalidValue;
+    if (make_plane_map(&tb, L.digB, (int64_t)L.P.partsB * L.P.s, L.rowsB, L.kp, 128)) return cudaErrorInvalidValue;
+    auto kern = slicegemm_tc2_kernel<STAGES>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(L.P.counter, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    kern<<<L.grid & ~1, 256, Cfg::SMEM, st>>>(ta, tb, L.P);
+    return cudaGetLastError();
+}
+
 cudaError_t slicegemm_launch(const SliceGemmLaunch &L, cudaStream_t st) {
     if (L.grid <= 0) return cudaSuccess;
     if (L.simt) {
-        dim3 grid(L.nunits, (kBM / 32) * (L.BN / 32));
-        slicegemm_simt_kernel<<<grid, 256, 0, st>>>(L.digA, L.digB, L.rowsA, L.rowsB, L.kp, L.units_flat, L.BN, L.P);
+        dim3 grid(L.nunits, (L.BM / 32) * (L.BN / 32));
+        slicegemm_simt_kernel<<<grid, 256, 0, st>>>(L.digA, L.digB, L.rowsA, L.rowsB, L.kp, L.units_flat, L.BM, L.BN, L.P);
         return cudaGetLastError();
     }
+    if (L.BM == 256) return launch_tc2<6>(L, st);
     if (L.BN == 256) return launch_tc<256, 4>(L, st);
     if (L.BN == 128) return launch_tc<128, 6>(L, st);
     return cudaErrorInvalidValue;

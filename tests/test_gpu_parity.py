@@ -97,9 +97,13 @@ def test_simt_crosscheck_and_forced_slices(method, monkeypatch):
         monkeypatch.setenv("MPCGEMM_G2", "0")                  # single-diagonal units only
         C3, r3 = run_gpu(A, B, prec, method, s)
         monkeypatch.delenv("MPCGEMM_G2")
-        assert r1["slices"] == r2["slices"] == r3["slices"]
+        monkeypatch.setenv("MPCGEMM_CTA2", "0")                # one CTA per 128-row tile
+        C4, r4 = run_gpu(A, B, prec, method, s)
+        monkeypatch.delenv("MPCGEMM_CTA2")
+        assert r1["slices"] == r2["slices"] == r3["slices"] == r4["slices"]
         assert same_bits(C1, C2), (s, first_mismatch(C1, C2))
         assert same_bits(C1, C3), (s, first_mismatch(C1, C3))
+        assert same_bits(C1, C4), (s, first_mismatch(C1, C4))
         if s:
             si, sj = sample_idx(m, n, 60, seed=s)
             Rs = oracle.ozaki(A, B, prec, method, s, samples=(si, sj))
@@ -118,7 +122,10 @@ def test_small_chunks_equal_default(monkeypatch):
     C3, _ = run_gpu(A, B, prec, "4M")
     monkeypatch.setenv("MPCGEMM_G2", "0")
     C4, _ = run_gpu(A, B, prec, "4M")
-    assert same_bits(C1, C2) and same_bits(C1, C3) and same_bits(C1, C4)
+    monkeypatch.setenv("MPCGEMM_BN", "256")
+    monkeypatch.setenv("MPCGEMM_CTA2", "0")
+    C5, _ = run_gpu(A, B, prec, "4M")
+    assert same_bits(C1, C2) and same_bits(C1, C3) and same_bits(C1, C4) and same_bits(C1, C5)
 
 
 @pytest.mark.parametrize("spread,k", [(16, 12), (16, 3), (0, 64), (4, 40)])
