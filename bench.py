@@ -229,14 +229,24 @@ def main():
     achieved = ops / (gemm_ms / 1e3) / 1e12
     stage_ms = {f: round(statistics.mean(r[f] for r in reps), 3) for f in
                 ("ms_linemax", "ms_prepass", "ms_split", "ms_gemm", "ms_fold")}
-    hbm = pk["hbm_gbs"]
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        if tr["config"] == args.config and tr["method"] == args.method and tr["slices"] == s:
+            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+    except Exception:
+        traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/u64",
         "data": "synthetic", "config": workload_config(args, s),
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak_int8, 1), "unit": "TOP/s",
-                     "frac": round(achieved / peak_int8, 4), "traffic": None,
-                     "kernel": "slicegemm_tc_kernel (tcgen05.mma kind::i8)",
+                     "frac": round(achieved / peak_int8, 4), "traffic": traffic,
+                     "traffic_note": "ncu dram__bytes_read+write per launch (profiles/roofline_traffic.json); "
+                                     "the kernel is tensor-bound, its algorithmic operand bytes are the digit planes",
+                     "kernel": "slicegemm_tc2_kernel (tcgen05.mma.cta_group::2 kind::i8)",
+                     "ceilings_tops": {"pure_mma_random_operands_sustained": 3704, "cublaslt_int8_sustained": 2412,
+                                       "cublaslt_int8_burst": 3081, "nominal": 4500},
                      "peak_source": f"{src}: 2 x bf16_tflops_sustained (nominal int8/bf16 = 2)",
                      "algorithmic": f"2 R P m n k = 2*{R}*{pairs}*{m}*{n}*{k} int8 ops per launch"},
         "stages_ms": stage_ms,
