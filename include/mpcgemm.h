@@ -76,6 +76,10 @@ typedef struct {
     size_t   workspace_bytes; /* size of caller workspace (>= mpcgemm_workspace_size)          */
     int32_t  timing;          /* 1 = time each stage with CUDA events on opts->stream (the call
                                  then synchronizes the stream before returning)              */
+    int32_t  beta;            /* 0: C := alpha A B.  1: C := C + alpha A B -- C is read as input
+                                 (in place) and the exact sum is rounded once (SURVEY NEXT-2:
+                                 the LU trailing update A22 - L21 U12)      */
+    int32_t  alpha_neg;       /* 1: alpha = -1, else alpha = +1                                 */
     int32_t  reserved;
 } mpcgemm_opts;
 

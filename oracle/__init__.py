@@ -54,6 +54,8 @@ def lib():
             L.orc_cgemm_exact.restype = ctypes.c_int
             L.orc_cgemm_ozaki.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, i64, vp, vp, i32]
             L.orc_cgemm_ozaki.restype = ctypes.c_int
+            L.orc_cgemm_ozaki_acc.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, P, P, i32, i32, i32, i64, vp, vp, i32]
+            L.orc_cgemm_ozaki_acc.restype = ctypes.c_int
             L.orc_exponents.argtypes = [i64, i64, i64, P, P, P, P, vp, vp, vp, vp]
             L.orc_split.argtypes = [ctypes.c_int, i64, i64, P, P, i32, i32, vp]
             L.orc_split.restype = ctypes.c_int
@@ -114,6 +116,37 @@ def ozaki(A: CMat, B: CMat, prec_out: int, method="3M", s: int | None = None, sa
     if s is None:
         s, _ = auto_slices(A, B, A.prec, method)
     return _run(lib().orc_cgemm_ozaki, A, B, prec_out, method, s, samples, nthreads)
+
+
+def ozaki_acc(A: CMat, B: CMat, C0: CMat, prec_out: int, method="3M", s: int | None = None, beta: int = 1,
+              alpha_neg: int = 0, samples=None, nthreads: int = 0) -> CMat:
+    """C = beta C0 + (-1)^alpha_neg (Algorithm-2 product), exact sum, one RNE (NEXT-2)."""
+    if s is None:
+        s, _ = auto_slices(A, B, A.prec, method)
+    m, k = A.shape
+    n = B.shape[1]
+    assert C0.shape == (m, n)
+    if samples is None:
+        Cre, Cim = empty_rmat(m, n, prec_out), empty_rmat(m, n, prec_out)
+        ns, si, sj = -1, None, None
+    else:
+        si = np.ascontiguousarray(np.asarray(samples[0], dtype=np.int64))
+        sj = np.ascontiguousarray(np.asarray(samples[1], dtype=np.int64))
+        ns = len(si)
+        Cre, Cim = empty_rmat(1, max(ns, 1), prec_out), empty_rmat(1, max(ns, 1), prec_out)
+    a = [_rm(A.re), _rm(A.im), _rm(B.re), _rm(B.im)]
+    c0 = [_rm(C0.re), _rm(C0.im)]
+    out = [_rm(Cre), _rm(Cim)]
+    rc = lib().orc_cgemm_ozaki_acc(m, n, k, *[_ptr(x) for x in a], *[_ptr(x) for x in c0], beta, alpha_neg,
+                                   *[_ptr(x) for x in out], prec_out, _form(method), s, ns,
+                                   si.ctypes.data if si is not None else None,
+                                   sj.ctypes.data if sj is not None else None, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle returned {rc}")
+    C = CMat(Cre, Cim)
+    if samples is not None:
+        C = C.cols(0, ns)
+    return C
 
 
 def exponents(A: CMat, B: CMat):

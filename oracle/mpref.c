@@ -464,10 +464,39 @@ static void ozaki_pair(const int8_t *da, const int8_t *db, int64_t k, int s, uin
     }
 }
 
+/* C := beta * C0 + (alpha_neg ? -1 : +1) * (Ozaki product), every sum exact, ONE RNE (the
+ * LU trailing update A22 - L21 U12 of PAPER.md:251, 261 with a single rounding).
+ * C0 (Cre0, Cim0) is read at the same positions as the output (full or sampled). */
+static int ozaki_core(int64_t m, int64_t n, int64_t k,
+                      const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                      orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
+                      int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads,
+                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg);
+
 int orc_cgemm_ozaki(int64_t m, int64_t n, int64_t k,
                     const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
                     orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
                     int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
+{
+    return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s, nsamp, si, sj, nthreads,
+                      NULL, NULL, 0, 0);
+}
+
+int orc_cgemm_ozaki_acc(int64_t m, int64_t n, int64_t k,
+                        const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                        const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg,
+                        orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
+                        int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
+{
+    return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s, nsamp, si, sj, nthreads,
+                      Cre0, Cim0, beta, alpha_neg);
+}
+
+static int ozaki_core(int64_t m, int64_t n, int64_t k,
+                      const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                      orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
+                      int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads,
+                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg)
 {
     if (m < 0 || n < 0 || k < 0 || (form != 3 && form != 4) || s < 1 || prec_out < 2) return -1;
     int64_t total = nsamp < 0 ? m * n : nsamp;
@@ -519,6 +548,13 @@ int orc_cgemm_ozaki(int64_t m, int64_t n, int64_t k,
                 xn u = xn_add(&T3, &T1, 1);
                 im = xn_add(&u, &T2, 1);
                 xn_free(&u); xn_free(&T1); xn_free(&T2); xn_free(&T3);
+            }
+            if (alpha_neg) { re.neg = re.n ? !re.neg : 0; im.neg = im.n ? !im.neg : 0; }
+            if (beta) {                                   /* exact C0 + (+-P), then one rounding */
+                xn c0r = entry_of(Cre0, i, j), c0i = entry_of(Cim0, i, j);
+                xn sr = xn_add(&c0r, &re, 0), sm = xn_add(&c0i, &im, 0);
+                xn_free(&re); xn_free(&im);
+                re = sr; im = sm;
             }
             uint8_t *sg; int64_t *ex; uint64_t *lb;
             out_ptrs(Cre, oi, &sg, &ex, &lb); xn_store(&re, prec_out, sg, ex, lb, Cre->L);

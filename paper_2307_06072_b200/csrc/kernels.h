@@ -46,6 +46,8 @@ struct FoldParams {
     const int32_t *slotinfo;     // [(job*(s+2) + r)*2 + {0 base, 1 count}]
     const int64_t *eA, *eB;
     DMatOut Cre, Cim;
+    int32_t beta, alpha_neg;     // NEXT-2: C = beta C0 + (-1)^alpha_neg A B (one rounding)
+    DMat C0re, C0im;             // may alias Cre / Cim
 };
 // a-5 + a-6: exact fold (chunk sums, Eq. 5/6 combination, carry) and RNE normalization
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st);

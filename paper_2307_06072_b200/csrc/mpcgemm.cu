@@ -420,7 +420,7 @@ int rule_slices(int32_t prec, int method, double log2rho) {
 // the device hot path with a known workspace
 int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
              mpc_cmat *C, int method, int s, cudaStream_t st, uint8_t *meta, uint8_t *big, const Layout &Lo,
-             int simt, mpcgemm_report *rep, StageEvents *E) {
+             int simt, mpcgemm_report *rep, StageEvents *E, int beta, int alpha_neg) {
     const int L = (prec + 63) / 64;
     int64_t *eA = (int64_t *)meta, *eB = eA + m;
     const int parts = method == 3 ? 3 : 2;
@@ -452,6 +452,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     F.partials = partials; F.nslots = plan->nslots; F.nstrips = Lo.nstrips; F.m = m; F.n = n;
     F.s = s; F.method = method; F.prec = prec; F.L = L; F.slotinfo = plan->d_slotinfo;
     F.eA = eA; F.eB = eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
+    F.beta = beta; F.alpha_neg = alpha_neg; F.C0re = dm(C->re); F.C0im = dm(C->im);
     CK(fold_normalize_launch(F, st));
     if (E) CK(cudaEventRecord(E->ev[5], st));
     if (rep) {
@@ -468,12 +469,17 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
     const int forced = opts ? opts->slices : 0;
     const int validate = opts ? opts->validate : 0;
+    const int beta = opts ? (opts->beta != 0) : 0;
+    const int alpha_neg = opts ? (opts->alpha_neg != 0) : 0;
     const int simt = env_int("MPCGEMM_SLICEGEMM_SIMT", 0);
     if (forced < 0 || forced > kMaxSlices) return fail(MPCGEMM_ERR_SLICES, "forced slices outside [1, 1024]");
     if (rep) { memset(rep, 0, sizeof(*rep)); rep->minT = rep->minT1 = rep->maxD2 = -1; }
     const int L = (prec + 63) / 64;
     if (m == 0 || n == 0) return 0;
-    if (k == 0) { CK(zero_output_launch(dmo(C->re), m, n, L, st)); CK(zero_output_launch(dmo(C->im), m, n, L, st)); return 0; }
+    if (k == 0) {                                      // A B = 0: C := beta C
+        if (!beta) { CK(zero_output_launch(dmo(C->re), m, n, L, st)); CK(zero_output_launch(dmo(C->im), m, n, L, st)); }
+        return 0;
+    }
     int dev = 0;
     CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(g_mu);
@@ -520,7 +526,8 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     }
     if (E) CK(cudaEventRecord(E->ev[2], st));
     if (rep) rep->kernel_launches = launches;
-    if (int rc = run_main(dev, m, n, k, prec, A, B, C, method, s, st, meta, big, Lm, simt, rep, E)) return rc;
+    if (int rc = run_main(dev, m, n, k, prec, A, B, C, method, s, st, meta, big, Lm, simt, rep, E, beta, alpha_neg))
+        return rc;
     if (rep) {
         rep->slices = s; rep->certified = 1; rep->minT = pb[0]; rep->minT1 = pb[1]; rep->maxD2 = pb[2];
         rep->log2_rho_hat = log2rho;
@@ -624,6 +631,17 @@ int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *
         CK(cudaMemcpy2DAsync(dmats[q].exp, cols[q] * 8, H.exp, H.ld * 8, cols[q] * 8, rows[q], cudaMemcpyHostToDevice, st));
         CK(cudaMemcpy2DAsync(dmats[q].limbs, cols[q] * 8 * L, H.limbs, H.ld * 8 * L, cols[q] * 8 * L, rows[q],
                              cudaMemcpyHostToDevice, st));
+    }
+    if (opts && opts->beta) {                          // C is an input too
+        const mpc_rmat *cin[2] = {&C->re, &C->im};
+        for (int q = 0; q < 2; q++) {
+            if (m == 0 || n == 0) continue;
+            const mpc_rmat &H = *cin[q];
+            CK(cudaMemcpy2DAsync(dmats[4 + q].sign, n, H.sign, H.ld, n, m, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpy2DAsync(dmats[4 + q].exp, n * 8, H.exp, H.ld * 8, n * 8, m, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpy2DAsync(dmats[4 + q].limbs, n * 8 * L, H.limbs, H.ld * 8 * L, n * 8 * L, m,
+                                 cudaMemcpyHostToDevice, st));
+        }
     }
     mpc_cmat dA{dmats[0], dmats[1]}, dB{dmats[2], dmats[3]}, dC{dmats[4], dmats[5]};
     int rc = gemm_impl(m, n, k, prec, &dA, &dB, &dC, (int)method, opts, rep);

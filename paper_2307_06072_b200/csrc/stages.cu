@@ -420,21 +420,14 @@ struct FixView {
     }
 };
 
-MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, int prec, int L,
-                             uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
+// RNE of a magnitude buf[0..n) (column of stride `stride`, LSB weight 2^e_lsb) to prec bits,
+// stored in the ABI element format with sign `neg`.
+MPC_DEV void round_store(const uint64_t *buf, int stride, int n, int64_t e_lsb, bool neg, int prec, int L,
+                         uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
 {
-    const bool neg = (int64_t)fix[(int64_t)(Lc - 1) * stride] < 0;
-    if (neg) {                                        // magnitude, in place
-        uint64_t c = 1;
-        for (int l = 0; l < Lc; l++) {
-            const uint64_t x = ~fix[(int64_t)l * stride] + c;
-            c = (c && x == 0);
-            fix[(int64_t)l * stride] = x;
-        }
-    }
     int b = 0;
-    for (int l = Lc - 1; l >= 0; l--) {
-        const uint64_t v = fix[(int64_t)l * stride];
+    for (int l = n - 1; l >= 0; l--) {
+        const uint64_t v = buf[(int64_t)l * stride];
         if (v) { b = 64 * l + 64 - __clzll((long long)v); break; }
     }
     if (b == 0) {
@@ -442,8 +435,8 @@ MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, int 
         for (int l = 0; l < L; l++) limbs_out[l] = 0;
         return;
     }
-    const FixView F{fix, stride, Lc};
-    int64_t E = e0 + b;
+    const FixView F{buf, stride, n};
+    int64_t E = e_lsb + b;
     const int64_t base = (int64_t)b - 64 * L;         // window = bits [b - 64L, b)
     const int drop = 64 * L - prec;
     // round bit = bit (b - prec - 1); sticky = OR of the bits below it
@@ -459,7 +452,7 @@ MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, int 
     const int lsb = (int)((w0 >> drop) & 1);
     bool up = rbit && (sticky || lsb);
     if (up) {                                         // carry-out iff all kept bits are 1
-        bool allones = (w0 | ((1ull << drop) - 1)) == ~0ull || (drop == 0 && w0 == ~0ull);
+        bool allones = (w0 | ((1ull << drop) - 1)) == ~0ull;
         for (int l = 1; l < L && allones; l++) allones = F.bits64(base + 64 * l) == ~0ull;
         if (allones) {
             for (int l = 0; l < L - 1; l++) limbs_out[l] = 0;
@@ -480,6 +473,110 @@ MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, int 
     *exp_out = E;
 }
 
+// two's complement fix[0..Lc) -> magnitude in place; returns the sign
+MPC_DEV bool to_magnitude(uint64_t *fix, int stride, int Lc) {
+    const bool neg = (int64_t)fix[(int64_t)(Lc - 1) * stride] < 0;
+    if (neg) {
+        uint64_t c = 1;
+        for (int l = 0; l < Lc; l++) {
+            const uint64_t x = ~fix[(int64_t)l * stride] + c;
+            c = (c && x == 0);
+            fix[(int64_t)l * stride] = x;
+        }
+    }
+    return neg;
+}
+
+// fix (two's complement, LSB weight 2^e0) -> RNE((-1)^alpha_neg fix 2^e0) in the ABI format
+MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, bool alpha_neg, int prec, int L,
+                             uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
+{
+    const bool neg = to_magnitude(fix, stride, Lc);
+    round_store(fix, stride, Lc, e0, neg != alpha_neg, prec, L, sign_out, exp_out, limbs_out);
+}
+
+// NEXT-2: RNE(C0 + (-1)^alpha_neg V 2^e0), one rounding of the exact sum.  V = fix[0..Lc)
+// (two's complement); the sum is formed in sign-magnitude in R = fix[Lc..Lc+Lw) over a window
+// of 64 Lw >= 64 (Lc + L + 3) bits below the larger operand's top; bits of the smaller operand
+// below the window collapse into a sticky LSB (>= 2 guard bits below the rounding position).
+// C0 (N, L limbs, LSB weight 2^(exp - 64 L)) may alias the output element (read first).
+MPC_DEV void accumulate_store(uint64_t *fix, int stride, int Lc, int Lw, int64_t e0, bool alpha_neg,
+                              uint8_t c0s, int64_t c0e, const uint64_t *c0l, int prec, int L,
+                              uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
+{
+    const bool sV = to_magnitude(fix, stride, Lc) != alpha_neg;
+    int bV = 0;
+    for (int l = Lc - 1; l >= 0; l--) {
+        const uint64_t v = fix[(int64_t)l * stride];
+        if (v) { bV = 64 * l + 64 - __clzll((long long)v); break; }
+    }
+    const bool cz = __ldg(c0l + L - 1) == 0;
+    if (cz) { round_store(fix, stride, Lc, e0, sV, prec, L, sign_out, exp_out, limbs_out); return; }
+    const bool sC = c0s != 0;
+    const int64_t E1 = c0e - 64 * (int64_t)L;
+    if (bV == 0) {                                    // C0 is already a prec-bit value
+        uint64_t tmp[64];
+        for (int l = 0; l < L; l++) tmp[l] = __ldg(c0l + l);
+        *sign_out = sC ? 1 : 0; *exp_out = c0e;
+        for (int l = 0; l < L; l++) limbs_out[l] = tmp[l];
+        return;
+    }
+    const int64_t topV = e0 + bV, topC = c0e;
+    const int64_t top = topV > topC ? topV : topC;
+    int64_t WB = e0 < E1 ? e0 : E1;
+    if (WB < top - 64 * (int64_t)Lw + 2) WB = top - 64 * (int64_t)Lw + 2;
+    const FixView V{fix, stride, Lc};
+    uint64_t cN[64];
+    for (int l = 0; l < L; l++) cN[l] = __ldg(c0l + l);
+    auto nbits = [&](int64_t pos) -> uint64_t {      // 64 bits of N from bit pos
+        if (pos <= -64) return 0;
+        if (pos < 0) return cN[0] << (-pos);
+        const int64_t li = pos >> 6;
+        const int bo = (int)(pos & 63);
+        const uint64_t lo = li < L ? cN[li] : 0ull;
+        if (!bo) return lo;
+        const uint64_t hi = li + 1 < L ? cN[li + 1] : 0ull;
+        return (lo >> bo) | (hi << (64 - bo));
+    };
+    auto below = [&](auto get, int nl, int64_t cut) -> bool {   // any bit below position cut
+        if (cut <= 0) return false;
+        const int64_t full = cut >> 6;
+        for (int64_t l = 0; l < full && l < nl; l++) if (get(l)) return true;
+        if (full < nl && (cut & 63) && (get(full) & ((1ull << (cut & 63)) - 1))) return true;
+        return false;
+    };
+    const bool stV = below([&](int64_t l) { return V.at(l); }, Lc, WB - e0);
+    const bool stC = below([&](int64_t l) { return l < L ? cN[l] : 0ull; }, L, WB - E1);
+    uint64_t *R = fix + (int64_t)Lc * stride;
+    // compare |X| and |Y| (aligned) from the top when subtracting
+    const bool sub = sV != sC;
+    bool xbig = true;
+    if (sub) {
+        int cmp = 0;
+        for (int l = Lw - 1; l >= 0 && !cmp; l--) {
+            uint64_t x = V.bits64(WB - e0 + 64 * (int64_t)l), y = nbits(WB - E1 + 64 * (int64_t)l);
+            if (l == 0) { x |= stV; y |= stC; }
+            cmp = x > y ? 1 : (x < y ? -1 : 0);
+        }
+        if (cmp == 0) { *sign_out = 0; *exp_out = 0; for (int l = 0; l < L; l++) limbs_out[l] = 0; return; }
+        xbig = cmp > 0;
+    }
+    uint64_t c = 0;
+    for (int l = 0; l < Lw; l++) {
+        uint64_t x = V.bits64(WB - e0 + 64 * (int64_t)l), y = nbits(WB - E1 + 64 * (int64_t)l);
+        if (l == 0) { x |= stV; y |= stC; }
+        uint64_t r;
+        if (!sub) { r = x + y + c; c = (r < x || (c && r == x)) ? 1 : 0; }
+        else {
+            const uint64_t a = xbig ? x : y, bb = xbig ? y : x;
+            r = a - bb - c; c = (a < bb || (c && a == bb)) ? 1 : 0;
+        }
+        R[(int64_t)l * stride] = r;
+    }
+    const bool sR = sub ? (xbig ? sV : sC) : sV;
+    round_store(R, stride, Lw, WB, sR, prec, L, sign_out, exp_out, limbs_out);
+}
+
 // The partial planes are streamed by a producer warp with cp.async.bulk: for each slot (in
 // the order r = s+1..2, job, chunk) the contiguous strip partials[slot][i][j0 .. j0+T) lands in
 // a RING-deep shared-memory ring, so ~RING KB per block are in flight regardless of the
@@ -487,13 +584,15 @@ MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, int 
 constexpr int kFoldRing = 4;           // entries
 constexpr int kFoldPer = 8;            // slots per entry (one 8 KB bulk copy at T = 256)
 
-template <int kFoldT>
+template <int kFoldT, bool BETA>
 __global__ void __launch_bounds__(kFoldT + 32)
 fold_normalize_kernel(const FoldParams F)
 {
     extern __shared__ __align__(128) uint8_t fsm_raw[];
     const int s = F.s;
-    const int Lc = s / 8 + 3;
+    const int Lc0 = s / 8 + 3;                       // fixed-point limbs
+    const int Lw = BETA ? Lc0 + F.L + 3 : 0;         // NEXT-2 sum window
+    const int Lc = Lc0 + Lw;                         // limbs per part in shared memory
     int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                       // [RING][PER][T]
     uint64_t *fix = reinterpret_cast<uint64_t *>(fsm_raw + kFoldRing * kFoldPer * kFoldT * 4);  // [2][Lc][T]
     int32_t *slots = reinterpret_cast<int32_t *>(fix + 2 * (int64_t)Lc * kFoldT);  // [job][r][base,cnt]
@@ -569,40 +668,52 @@ fold_normalize_kernel(const FoldParams F)
         }
     }
     if (j >= F.n) return;
-    // the final carry at bit 8s, sign-extended to Lc limbs
+    // the final carry at bit 8s, sign-extended to Lc0 limbs
     const int l0 = s >> 3, o = 8 * (s & 7);
     {
         const uint64_t c = (uint64_t)c0, sx = c0 < 0 ? ~0ull : 0ull;
         fix0[(int64_t)l0 * kFoldT] = cur0 | (c << o);
         fix0[(int64_t)(l0 + 1) * kFoldT] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
-        for (int l = l0 + 2; l < Lc; l++) fix0[(int64_t)l * kFoldT] = sx;
+        for (int l = l0 + 2; l < Lc0; l++) fix0[(int64_t)l * kFoldT] = sx;
     }
     {
         const uint64_t c = (uint64_t)c1, sx = c1 < 0 ? ~0ull : 0ull;
         fix1[(int64_t)l0 * kFoldT] = cur1 | (c << o);
         fix1[(int64_t)(l0 + 1) * kFoldT] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
-        for (int l = l0 + 2; l < Lc; l++) fix1[(int64_t)l * kFoldT] = sx;
+        for (int l = l0 + 2; l < Lc0; l++) fix1[(int64_t)l * kFoldT] = sx;
     }
     const int64_t e0 = F.eA[i] + F.eB[j] + 6 - 8 * (int64_t)(s + 1);
     const int64_t oi = i * F.Cre.ld + j;
-    normalize_store(fix0, kFoldT, Lc, e0, F.prec, F.L, F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
     const int64_t oj = i * F.Cim.ld + j;
-    normalize_store(fix1, kFoldT, Lc, e0, F.prec, F.L, F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
+    if (BETA) {
+        const int64_t ci = i * F.C0re.ld + j, cj = i * F.C0im.ld + j;
+        const uint8_t s0 = F.C0re.sign[ci], s1 = F.C0im.sign[cj];       // read before the (aliasing) write
+        const int64_t x0 = F.C0re.exp[ci], x1 = F.C0im.exp[cj];
+        accumulate_store(fix0, kFoldT, Lc0, Lw, e0, F.alpha_neg, s0, x0, F.C0re.limbs + ci * F.L, F.prec, F.L,
+                         F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
+        accumulate_store(fix1, kFoldT, Lc0, Lw, e0, F.alpha_neg, s1, x1, F.C0im.limbs + cj * F.L, F.prec, F.L,
+                         F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
+    } else {
+        normalize_store(fix0, kFoldT, Lc0, e0, F.alpha_neg, F.prec, F.L, F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
+        normalize_store(fix1, kFoldT, Lc0, e0, F.alpha_neg, F.prec, F.L, F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
+    }
 }
 
-size_t fold_smem(int s, int T) {
-    const int Lc = s / 8 + 3;
+size_t fold_smem(int s, int T, int L, bool beta) {
+    const int Lc0 = s / 8 + 3;
+    const int Lc = Lc0 + (beta ? Lc0 + L + 3 : 0);
     return (size_t)kFoldRing * kFoldPer * T * 4 + (size_t)2 * Lc * T * 8 + (size_t)kMaxJobs * (s + 2) * 2 * 4 + 16 +
            (size_t)2 * kFoldRing * 8 + 16;
 }
 
-template <int T>
+template <int T, bool BETA>
 static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
-    const size_t sm = fold_smem(F.s, T);
-    cudaError_t e = cudaFuncSetAttribute(fold_normalize_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const size_t sm = fold_smem(F.s, T, F.L, BETA);
+    if (sm > 227 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(fold_normalize_kernel<T, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     dim3 grid(kRowBlk, (unsigned)(((F.n + T - 1) / T) * ((F.m + kRowBlk - 1) / kRowBlk)));
-    fold_normalize_kernel<T><<<grid, T + 32, sm, st>>>(F);
+    fold_normalize_kernel<T, BETA><<<grid, T + 32, sm, st>>>(F);
     return cudaGetLastError();
 }
 
@@ -610,9 +721,12 @@ cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
 {
     if (F.m == 0 || F.n == 0) return cudaSuccess;
     if (F.s > kMaxSlices) return cudaErrorInvalidValue;
-    if (fold_smem(F.s, 256) <= 112 * 1024) return fold_launch_t<256>(F, st);     // 2 blocks / SM
-    if (fold_smem(F.s, 256) <= 220 * 1024) return fold_launch_t<256>(F, st);
-    return fold_launch_t<64>(F, st);                                              // s up to 1024
+    if (F.beta) {
+        if (fold_smem(F.s, 128, F.L, true) <= 220 * 1024) return fold_launch_t<128, true>(F, st);
+        return fold_launch_t<32, true>(F, st);                                    // s up to 1024
+    }
+    if (fold_smem(F.s, 256, F.L, false) <= 220 * 1024) return fold_launch_t<256, false>(F, st);
+    return fold_launch_t<64, false>(F, st);                                       // s up to 1024
 }
 
 __global__ void zero_output_kernel(DMatOut C, int64_t m, int64_t n, int L) {

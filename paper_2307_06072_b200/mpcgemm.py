@@ -43,7 +43,8 @@ class CMatC(ctypes.Structure):
 class OptsC(ctypes.Structure):
     _fields_ = [("stream", ctypes.c_void_p), ("slices", ctypes.c_int32), ("validate", ctypes.c_int32),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-                ("timing", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("timing", ctypes.c_int32), ("beta", ctypes.c_int32), ("alpha_neg", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class ReportC(ctypes.Structure):
@@ -181,15 +182,17 @@ def _stream_ptr(stream):
 
 # ------------------------------------------------------------------ the calls (names = ABI)
 def mpcgemm_ex(A: DevCMat, B: DevCMat, C: DevCMat, prec: int, method="3M", slices: int = 0,
-               validate: int = 0, stream=None, workspace=None, timing: int = 0) -> dict:
-    """C := A B on the device (stream-ordered).  Returns the report as a dict."""
+               validate: int = 0, stream=None, workspace=None, timing: int = 0, beta: int = 0,
+               alpha_neg: int = 0) -> dict:
+    """C := beta C + (-1)^alpha_neg A B on the device (stream-ordered).  Returns the report."""
     m, k = A.shape
     k2, n = B.shape
     if k != k2 or C.shape != (m, n):
         raise MpcgemmError(-1, f"shape mismatch A {A.shape} B {B.shape} C {C.shape}")
     opts = OptsC(_stream_ptr(stream), slices, validate,
                  workspace.data_ptr() if workspace is not None else None,
-                 workspace.numel() * workspace.element_size() if workspace is not None else 0, timing, 0)
+                 workspace.numel() * workspace.element_size() if workspace is not None else 0, timing, beta,
+                 alpha_neg, 0)
     rep = ReportC()
     a, b, c = A.c(), B.c(), C.c()
     rc = lib().mpcgemm_ex(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), METHODS[method],
@@ -212,7 +215,8 @@ def _host_rmat(R) -> RMatC:
     return RMatC(R.sign.ctypes.data, R.exp.ctypes.data, R.limbs.ctypes.data, R.sign.shape[1])
 
 
-def mpcgemm_host(A, B, prec: int, method="3M", slices: int = 0, C=None, timing: int = 0):
+def mpcgemm_host(A, B, prec: int, method="3M", slices: int = 0, C=None, timing: int = 0, beta: int = 0,
+                 alpha_neg: int = 0):
     """End-to-end call on host numpy buffers (mpgen.CMat); returns (C, report)."""
     from mpgen import empty_cmat
     m, k = A.shape
@@ -221,7 +225,7 @@ def mpcgemm_host(A, B, prec: int, method="3M", slices: int = 0, C=None, timing: 
     a = CMatC(_host_rmat(A.re), _host_rmat(A.im))
     b = CMatC(_host_rmat(B.re), _host_rmat(B.im))
     c = CMatC(_host_rmat(C.re), _host_rmat(C.im))
-    opts = OptsC(None, slices, 0, None, 0, timing, 0)
+    opts = OptsC(None, slices, 0, None, 0, timing, beta, alpha_neg, 0)
     rep = ReportC()
     rc = lib().mpcgemm_host(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), METHODS[method],
                             ctypes.byref(opts), ctypes.byref(rep))
@@ -233,7 +237,7 @@ def mpcgemm_rho_bounds(A: DevCMat, B: DevCMat, prec: int, full: int = 0, stream=
     m, k = A.shape
     n = B.shape[1]
     out = (ctypes.c_int64 * 3)()
-    opts = OptsC(_stream_ptr(stream), 0, 0, None, 0, 0, 0)
+    opts = OptsC(_stream_ptr(stream), 0, 0, None, 0, 0, 0, 0, 0)
     a, b = A.c(), B.c()
     _check(lib().mpcgemm_rho_bounds(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), full, ctypes.byref(opts), out))
     return tuple(int(v) for v in out)

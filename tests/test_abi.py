@@ -55,7 +55,7 @@ def test_library_is_sm100a_with_tensor_core_code(P):
 def test_struct_layout_matches_header(P):
     M = P.mpcgemm
     assert ctypes.sizeof(M.RMatC) == 32 and ctypes.sizeof(M.CMatC) == 64
-    assert ctypes.sizeof(M.OptsC) == 40
+    assert ctypes.sizeof(M.OptsC) == 48
     assert M.ReportC.ms_fold.offset + 4 == ctypes.sizeof(M.ReportC) or ctypes.sizeof(M.ReportC) % 8 == 0
 
 

@@ -283,3 +283,46 @@ def test_large_forced_slices(method):
     si, sj = sample_idx(m, n, 30, seed=5)
     Rs = oracle.ozaki(A, B, prec, method, 420, samples=(si, sj))
     assert sampled_equal(C, Rs, si, sj) is None
+
+
+# ------------------------------------------------------------------ NEXT-2: C := C0 +- A B
+def _c0_variants(m, n, prec, A, B, method):
+    out = {"near": oracle.exact(A, B, prec, method)}                 # heavy cancellation
+    for kind, shift, zf in (("random", 0, 0.1), ("tiny", -400, 0.0), ("huge", 300, 0.0)):
+        C0 = mpgen.random_cmat(55, 9, m, n, prec, 4, zero_frac=zf)
+        for R in (C0.re, C0.im):
+            nz = R.limbs[..., -1] != 0
+            R.exp[nz] += shift
+        out[kind] = C0
+    return out
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+@pytest.mark.parametrize("alpha_neg", [0, 1])
+def test_accumulate_in_place_bitexact(method, alpha_neg):
+    """mpcgemm_ex(beta=1): C := C + (-1)^alpha_neg A B in place, one rounding, bit-exact vs the
+    oracle for every entry (incl. near-total cancellation and far-apart exponents)."""
+    m, n, k, prec = 70, 300, 90, 192
+    A = mpgen.random_cmat(61, 1, m, k, prec, 5, zero_frac=0.05)
+    B = mpgen.random_cmat(61, 2, k, n, prec, 5, zero_frac=0.05)
+    s = oracle.auto_slices(A, B, prec, method)[0]
+    for kind, C0 in _c0_variants(m, n, prec, A, B, method).items():
+        dA, dB, dC = P.to_device(A), P.to_device(B), P.to_device(C0)
+        rep = P.mpcgemm_ex(dA, dB, dC, prec, method, beta=1, alpha_neg=alpha_neg)
+        torch.cuda.synchronize()
+        C = P.to_host(dC)
+        assert rep["slices"] == s
+        R = oracle.ozaki_acc(A, B, C0, prec, method, s, beta=1, alpha_neg=alpha_neg)
+        assert same_bits(C, R), (kind, first_mismatch(C, R))
+
+
+def test_accumulate_host_entry_and_beta0():
+    m, n, k, prec = 33, 40, 25, 128
+    A = mpgen.random_cmat(62, 1, m, k, prec, 2)
+    B = mpgen.random_cmat(62, 2, k, n, prec, 2)
+    C0 = mpgen.random_cmat(62, 3, m, n, prec, 2)
+    s = oracle.auto_slices(A, B, prec, "3M")[0]
+    C, _ = P.mpcgemm_host(A, B, prec, "3M", C=C0.copy(), beta=1, alpha_neg=1)
+    assert same_bits(C, oracle.ozaki_acc(A, B, C0, prec, "3M", s, beta=1, alpha_neg=1))
+    C, _ = P.mpcgemm_host(A, B, prec, "3M", alpha_neg=1)                       # beta = 0: -A B
+    assert same_bits(C, oracle.ozaki_acc(A, B, C0, prec, "3M", s, beta=0, alpha_neg=1))

@@ -214,3 +214,68 @@ def test_zero_lines_and_transpose_3m():
     assert same_bits(oracle.ozaki(B.T(), A.T(), prec, "3M", s), C.T())
     # 4M via Eq. 5 with T2 subtracted exactly: also symmetric
     assert same_bits(oracle.ozaki(B.T(), A.T(), prec, "4M", s), oracle.ozaki(A, B, prec, "4M", s).T())
+
+
+# ------------------------------------------------------------------ NEXT-2: C := C0 +- A B
+from harness import entry_equal, entry_of_rne  # noqa: E402
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+@pytest.mark.parametrize("alpha_neg", [0, 1])
+def test_accumulate_single_rounding(method, alpha_neg):
+    """Accumulating GEMM (the LU update A22 - L21 U12): the result is ONE
+    RNE of the exact sum C0 +- P, where P is the unrounded Algorithm-2 value (obtained here by
+    asking the Ozaki oracle for an exact-width output) -- checked with Fractions."""
+    prec = 128
+    A, B = rand_small(501 + alpha_neg, 4, 7, 5, prec, 6, zero_frac=0.05)
+    s = oracle.auto_slices(A, B, prec, method)[0]
+    Pexact = oracle.ozaki(A, B, 8 * s + 200, method, s)            # W-bit fixed point: exact at this width
+    for c0kind in ("near", "random", "tiny", "huge", "zero"):
+        if c0kind == "near":                                       # heavy cancellation
+            C0 = oracle.exact(A, B, prec, method)
+        else:
+            spread = {"random": 4, "tiny": 0, "huge": 0, "zero": 0}[c0kind]
+            C0 = mpgen.random_cmat(77, 9, 4, 5, prec, spread, zero_frac=0.1 if c0kind == "random" else 0.0)
+            for R in (C0.re, C0.im):
+                nz = R.limbs[..., -1] != 0
+                if c0kind == "tiny":
+                    R.exp[nz] -= 400
+                if c0kind == "huge":
+                    R.exp[nz] += 300
+                if c0kind == "zero":
+                    R.sign[:] = 0; R.exp[:] = 0; R.limbs[:] = 0
+        C = oracle.ozaki_acc(A, B, C0, prec, method, s, beta=1, alpha_neg=alpha_neg)
+        sg = -1 if alpha_neg else 1
+        for i in range(4):
+            for j in range(5):
+                for part in ("re", "im"):
+                    want = to_fraction(getattr(C0, part), i, j) + sg * to_fraction(getattr(Pexact, part), i, j)
+                    assert entry_equal(getattr(C, part), i, j, entry_of_rne(want, prec, getattr(C, part).L)), (c0kind, i, j)
+
+
+def test_accumulate_beta0_and_integer_closure():
+    import random as _r
+    rnd = _r.Random(9)
+    m, k, n = 5, 6, 4
+    mk = lambda r, c: [[rnd.randint(-8, 8) for _ in range(c)] for _ in range(r)]
+    A = mpgen.CMat(mpgen.from_ints(mk(m, k), 128), mpgen.from_ints(mk(m, k), 128))
+    B = mpgen.CMat(mpgen.from_ints(mk(k, n), 128), mpgen.from_ints(mk(k, n), 128))
+    c0r, c0i = mk(m, n), mk(m, n)
+    C0 = mpgen.CMat(mpgen.from_ints(c0r, 128), mpgen.from_ints(c0i, 128))
+    s = oracle.auto_slices(A, B, 128, "3M")[0]
+    C = oracle.ozaki_acc(A, B, C0, 128, "3M", s, beta=1, alpha_neg=1)          # C0 - A B, exact here
+    for i in range(m):
+        for j in range(n):
+            ar = [to_fraction(A.re, i, q) for q in range(k)]
+            ai = [to_fraction(A.im, i, q) for q in range(k)]
+            br = [to_fraction(B.re, q, j) for q in range(k)]
+            bi = [to_fraction(B.im, q, j) for q in range(k)]
+            re = sum(ar[q] * br[q] - ai[q] * bi[q] for q in range(k))
+            im = sum(ar[q] * bi[q] + ai[q] * br[q] for q in range(k))
+            assert to_fraction(C.re, i, j) == c0r[i][j] - re and to_fraction(C.im, i, j) == c0i[i][j] - im
+    Cn = oracle.ozaki_acc(A, B, C0, 128, "4M", s, beta=0, alpha_neg=1)          # -A B
+    Cp = oracle.ozaki(A, B, 128, "4M", s)
+    for part in ("re", "im"):
+        for i in range(m):
+            for j in range(n):
+                assert to_fraction(getattr(Cn, part), i, j) == -to_fraction(getattr(Cp, part), i, j)
