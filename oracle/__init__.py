@@ -56,6 +56,14 @@ def lib():
             L.orc_cgemm_ozaki.restype = ctypes.c_int
             L.orc_cgemm_ozaki_acc.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, P, P, i32, i32, i32, i64, vp, vp, i32]
             L.orc_cgemm_ozaki_acc.restype = ctypes.c_int
+            L.orc_cgemm_ozaki_bits.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, i32, i64, vp, vp, i32]
+            L.orc_cgemm_ozaki_bits.restype = ctypes.c_int
+            L.orc_split_bits.argtypes = [ctypes.c_int, i64, i64, P, P, i32, i32, i32, vp]
+            L.orc_split_bits.restype = ctypes.c_int
+            L.orc_fp64_slice_bits.argtypes = [i64]
+            L.orc_fp64_slice_bits.restype = ctypes.c_int32
+            L.orc_slices_for_bits.argtypes = [i32, i32, i64, i64, i64, i64, i32]
+            L.orc_slices_for_bits.restype = ctypes.c_int32
             L.orc_exponents.argtypes = [i64, i64, i64, P, P, P, P, vp, vp, vp, vp]
             L.orc_split.argtypes = [ctypes.c_int, i64, i64, P, P, i32, i32, vp]
             L.orc_split.restype = ctypes.c_int
@@ -147,6 +155,48 @@ def ozaki_acc(A: CMat, B: CMat, C0: CMat, prec_out: int, method="3M", s: int | N
     if samples is not None:
         C = C.cols(0, ns)
     return C
+
+
+def fp64_slice_bits(k: int) -> int:
+    """b = 53 - ceil((53 + ceil(log2 k)) / 2): the paper's binary64 slice width."""
+    return int(lib().orc_fp64_slice_bits(k))
+
+
+def ozaki_bits(A: CMat, B: CMat, prec_out: int, method="3M", s: int = 1, bits: int = 8, samples=None,
+               nthreads: int = 0) -> CMat:
+    """The same method with balanced radix-2^bits slices (NEXT-1: bits = fp64_slice_bits(k))."""
+    fn = lib().orc_cgemm_ozaki_bits
+    m, k = A.shape
+    n = B.shape[1]
+    if samples is None:
+        Cre, Cim = empty_rmat(m, n, prec_out), empty_rmat(m, n, prec_out)
+        ns, si, sj = -1, None, None
+    else:
+        si = np.ascontiguousarray(np.asarray(samples[0], dtype=np.int64))
+        sj = np.ascontiguousarray(np.asarray(samples[1], dtype=np.int64))
+        ns = len(si)
+        Cre, Cim = empty_rmat(1, max(ns, 1), prec_out), empty_rmat(1, max(ns, 1), prec_out)
+    args = [_rm(A.re), _rm(A.im), _rm(B.re), _rm(B.im), _rm(Cre), _rm(Cim)]
+    rc = fn(m, n, k, *[_ptr(a) for a in args], prec_out, _form(method), s, bits, ns,
+            si.ctypes.data if si is not None else None, sj.ctypes.data if sj is not None else None, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle returned {rc}")
+    C = CMat(Cre, Cim)
+    return C.cols(0, ns) if samples is not None else C
+
+
+def split_bits(P: CMat, side: int, s: int, bits: int, nparts: int) -> np.ndarray:
+    rows, cols = P.shape
+    lines, k = (rows, cols) if side == 0 else (cols, rows)
+    dig = np.zeros((nparts, s, lines, k), np.int32)
+    rc = lib().orc_split_bits(side, lines, k, _ptr(_rm(P.re)), _ptr(_rm(P.im)), s, bits, nparts, dig.ctypes.data)
+    if rc:
+        raise RuntimeError(f"orc_split_bits returned {rc}")
+    return dig
+
+
+def slices_for_bits(prec: int, method, k: int, minT: int, minT1: int, maxD2: int, bits: int) -> int:
+    return int(lib().orc_slices_for_bits(prec, _form(method), k, minT, minT1, maxD2, bits))
 
 
 def exponents(A: CMat, B: CMat):

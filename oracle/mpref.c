@@ -401,24 +401,32 @@ static void add_tc(uint64_t *r, const uint64_t *a, const uint64_t *b, int n) {
     for (int i = 0; i < n; i++) { u128 t = (u128)a[i] + b[i] + c; r[i] = (uint64_t)t; c = (uint64_t)(t >> 64); }
 }
 
-/* the unique balanced radix-256 digits (digit set [-128,127]) of the two's complement
- * integer X: X = sum_{alpha=1..s} d[alpha-1] 256^(s-alpha).  Slice A_alpha of Algorithm 2
- * is d[alpha-1] * 2^(e + 3 - 8 alpha).  Returns 0 on success, -1 if X
- * does not fit s digits. */
-static int balanced_digits(const uint64_t *X, int nx, int s, int8_t *d) {
-    int c = 0;
+/* the unique balanced radix-2^b digits (digit set [-2^(b-1), 2^(b-1)-1]) of the two's
+ * complement integer X: X = sum_{alpha=1..s} d[alpha-1] 2^(b(s-alpha)).  Slice A_alpha of
+ * Algorithm 2 is d[alpha-1] * 2^(e + 3 - b alpha) (b = 8: the INT8 carrier;
+ * b = 53 - ceil((53 + ceil(log2 k))/2): the paper's binary64 carrier).  Returns 0 on
+ * success, -1 if X does not fit s digits. */
+static uint64_t bits_at(const uint64_t *X, int nx, int64_t pos, int b) {   /* b <= 32 */
+    int64_t li = pos >> 6; int bo = (int)(pos & 63);
+    uint64_t lo = li < nx ? X[li] : (X[nx - 1] >> 63 ? ~0ull : 0ull);
+    uint64_t hi = li + 1 < nx ? X[li + 1] : (X[nx - 1] >> 63 ? ~0ull : 0ull);
+    uint64_t v = bo ? ((lo >> bo) | (hi << (64 - bo))) : lo;
+    return v & ((1ull << b) - 1);
+}
+static int balanced_digits(const uint64_t *X, int nx, int s, int b, int32_t *d) {
+    int64_t c = 0;
+    const int64_t half = 1ll << (b - 1), full = 1ll << b;
     for (int t = 0; t < s; t++) {
-        int byte = (int)((X[t / 8] >> (8 * (t % 8))) & 0xFF);
-        int v = byte + c;
-        int dig = v >= 128 ? v - 256 : v;
-        c = v >= 128;
-        d[s - 1 - t] = (int8_t)dig;
+        int64_t v = (int64_t)bits_at(X, nx, (int64_t)b * t, b) + c;
+        int64_t dig = v >= half ? v - full : v;
+        c = v >= half;
+        d[s - 1 - t] = (int32_t)dig;
     }
-    /* the bytes above must be the sign extension cancelled by the final carry */
+    /* the bits above must be the sign extension cancelled by the final carry */
     int neg = (int)(X[nx - 1] >> 63);
-    for (int t = s; t < 8 * nx; t++) {
-        int byte = (int)((X[t / 8] >> (8 * (t % 8))) & 0xFF);
-        if (byte != (neg ? 0xFF : 0)) return -1;
+    for (int64_t pos = (int64_t)b * s; pos < 64 * (int64_t)nx; pos++) {
+        int bit = (int)((X[pos >> 6] >> (pos & 63)) & 1);
+        if (bit != neg) return -1;
     }
     return (neg ? (c == 1) : (c == 0)) ? 0 : -1;
 }
@@ -426,11 +434,11 @@ static int balanced_digits(const uint64_t *X, int nx, int s, int8_t *d) {
 /* digit planes of one line (row i of A, or column j of B), parts 0 = Re, 1 = Im,
  * 2 = Re + Im (exact fixed-point sum, reading Z11).  dig[part][alpha][q] for q < len. */
 static int line_digits(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64_t idx, int64_t len,
-                       int64_t e, int s, int nparts, int8_t *dig) {
-    int64_t W = 8 * (int64_t)s - 3;
-    int nx = (8 * s + 64) / 64 + 1;
+                       int64_t e, int s, int b, int nparts, int32_t *dig) {
+    int64_t W = (int64_t)b * s - 3;
+    int nx = (int)(((int64_t)b * s + 64) / 64 + 1);
     uint64_t X[3][nx];
-    int8_t d[s];
+    int32_t d[s];
     for (int64_t q = 0; q < len; q++) {
         for (int p = 0; p < 2; p++) {
             const orc_rmat *M = p ? Pim : Pre;
@@ -439,7 +447,7 @@ static int line_digits(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64
         }
         add_tc(X[2], X[0], X[1], nx);
         for (int p = 0; p < nparts; p++) {
-            if (balanced_digits(X[p], nx, s, d)) return -1;
+            if (balanced_digits(X[p], nx, s, b, d)) return -1;
             for (int a = 0; a < s; a++) dig[((int64_t)p * s + a) * len + q] = d[a];
         }
     }
@@ -448,18 +456,18 @@ static int line_digits(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64
 
 /* Algorithm 2's product for one output element and one (A part, B part):
  * C = sum_{alpha=1..d} sum_{beta=1..d-alpha+1} (A_alpha B_beta)_ij,
- * accumulated exactly (Z7) as the integer  sum (dA_alpha . dB_beta) 256^(s+1-alpha-beta)
- * into the two's complement accumulator acc (na limbs, weight 2^(eA+eB+6-8(s+1))). */
-static void ozaki_pair(const int8_t *da, const int8_t *db, int64_t k, int s, uint64_t *acc, int na, int neg) {
+ * accumulated exactly (Z7) as the integer  sum (dA_alpha . dB_beta) 2^(b(s+1-alpha-beta))
+ * into the two's complement accumulator acc (na limbs, weight 2^(eA+eB+6-b(s+1))). */
+static void ozaki_pair(const int32_t *da, const int32_t *db, int64_t k, int s, int b, uint64_t *acc, int na, int neg) {
     for (int alpha = 1; alpha <= s; alpha++) {
-        const int8_t *xa = da + (int64_t)(alpha - 1) * k;
+        const int32_t *xa = da + (int64_t)(alpha - 1) * k;
         for (int beta = 1; beta <= s - alpha + 1; beta++) {
-            const int8_t *yb = db + (int64_t)(beta - 1) * k;
+            const int32_t *yb = db + (int64_t)(beta - 1) * k;
             int64_t dot = 0;                                   /* C_alpha,beta := A_alpha B_beta */
             for (int64_t q = 0; q < k; q++) dot += (int64_t)xa[q] * (int64_t)yb[q];
             if (!dot) continue;
             uint64_t mag = (uint64_t)(dot < 0 ? -dot : dot);
-            addsh(acc, na, &mag, 1, 8 * (int64_t)(s + 1 - alpha - beta), neg ^ (dot < 0));
+            addsh(acc, na, &mag, 1, (int64_t)b * (s + 1 - alpha - beta), neg ^ (dot < 0));
         }
     }
 }
@@ -471,7 +479,7 @@ static int ozaki_core(int64_t m, int64_t n, int64_t k,
                       const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
                       orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
                       int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads,
-                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg);
+                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg, int32_t bits);
 
 int orc_cgemm_ozaki(int64_t m, int64_t n, int64_t k,
                     const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
@@ -479,7 +487,7 @@ int orc_cgemm_ozaki(int64_t m, int64_t n, int64_t k,
                     int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
 {
     return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s, nsamp, si, sj, nthreads,
-                      NULL, NULL, 0, 0);
+                      NULL, NULL, 0, 0, 8);
 }
 
 int orc_cgemm_ozaki_acc(int64_t m, int64_t n, int64_t k,
@@ -489,14 +497,32 @@ int orc_cgemm_ozaki_acc(int64_t m, int64_t n, int64_t k,
                         int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
 {
     return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s, nsamp, si, sj, nthreads,
-                      Cre0, Cim0, beta, alpha_neg);
+                      Cre0, Cim0, beta, alpha_neg, 8);
+}
+
+/* the same method with b-bit digits (NEXT-1: b = the paper's binary64 slice width) */
+int orc_cgemm_ozaki_bits(int64_t m, int64_t n, int64_t k,
+                         const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                         orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s, int32_t bits,
+                         int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
+{
+    if (bits < 2 || bits > 30) return -1;
+    return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s, nsamp, si, sj, nthreads,
+                      NULL, NULL, 0, 0, bits);
+}
+
+/* b = S - ceil((S + ceil(log2 k)) / 2), S = 53: the slice width of Algorithm 2's tau (P:161,
+ * reading Z2: ceil(log2 l)); every k-term sum of two b-bit balanced digits is exact in binary64 */
+int32_t orc_fp64_slice_bits(int64_t k) {
+    int lk = 0; while ((1ll << lk) < k) lk++;
+    return 53 - (53 + lk + 1) / 2;
 }
 
 static int ozaki_core(int64_t m, int64_t n, int64_t k,
                       const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
                       orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
                       int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads,
-                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg)
+                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg, int32_t bits)
 {
     if (m < 0 || n < 0 || k < 0 || (form != 3 && form != 4) || s < 1 || prec_out < 2) return -1;
     int64_t total = nsamp < 0 ? m * n : nsamp;
@@ -504,11 +530,12 @@ static int ozaki_core(int64_t m, int64_t n, int64_t k,
     int nparts = form == 3 ? 3 : 2;
     int err = 0;
     int cnt = 2; while ((1LL << cnt) < 4 * k + 1) cnt++;
-    int na = (8 * s + 14 + cnt + 64) / 64 + 2;
+    const int b = bits;
+    int na = (int)(((int64_t)b * s + 2 * b + cnt + 64) / 64 + 2);
     #pragma omp parallel num_threads(nt)
     {
-        int8_t *da = (int8_t *)malloc((size_t)nparts * s * (k ? k : 1));
-        int8_t *db = (int8_t *)malloc((size_t)nparts * s * (k ? k : 1));
+        int32_t *da = (int32_t *)malloc(sizeof(int32_t) * (size_t)nparts * s * (k ? k : 1));
+        int32_t *db = (int32_t *)malloc(sizeof(int32_t) * (size_t)nparts * s * (k ? k : 1));
         uint64_t *acc[3];
         for (int q = 0; q < 3; q++) acc[q] = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)na);
         #pragma omp for schedule(dynamic, 1)
@@ -520,24 +547,24 @@ static int ozaki_core(int64_t m, int64_t n, int64_t k,
             int64_t eA, eB;
             line_exponent(Are, Aim, 0, i, k, &eA);
             line_exponent(Bre, Bim, 1, j, k, &eB);
-            if (line_digits(Are, Aim, 0, i, k, eA, s, nparts, da) ||
-                line_digits(Bre, Bim, 1, j, k, eB, s, nparts, db)) { err = -2; continue; }
+            if (line_digits(Are, Aim, 0, i, k, eA, s, b, nparts, da) ||
+                line_digits(Bre, Bim, 1, j, k, eB, s, b, nparts, db)) { err = -2; continue; }
             const int64_t pl = (int64_t)s * k;
             for (int q = 0; q < 3; q++) memset(acc[q], 0, sizeof(uint64_t) * (size_t)na);
             if (form == 4) {
                 /* Eq. 5: Re = ReA ReB - ImA ImB ; Im = ReA ImB + ImA ReB  (each by Alg. 2) */
-                ozaki_pair(da, db, k, s, acc[0], na, 0);
-                ozaki_pair(da + pl, db + pl, k, s, acc[0], na, 1);
-                ozaki_pair(da, db + pl, k, s, acc[1], na, 0);
-                ozaki_pair(da + pl, db, k, s, acc[1], na, 0);
+                ozaki_pair(da, db, k, s, b, acc[0], na, 0);
+                ozaki_pair(da + pl, db + pl, k, s, b, acc[0], na, 1);
+                ozaki_pair(da, db + pl, k, s, b, acc[1], na, 0);
+                ozaki_pair(da + pl, db, k, s, b, acc[1], na, 0);
             } else {
                 /* Eq. 6: T1 = ReA ReB, T2 = ImA ImB, T3 = (ReA+ImA)(ReB+ImB) (each by Alg. 2);
                    Re = T1 - T2 ; Im = T3 - T1 - T2 */
-                ozaki_pair(da, db, k, s, acc[0], na, 0);                /* T1 */
-                ozaki_pair(da + pl, db + pl, k, s, acc[1], na, 0);      /* T2 */
-                ozaki_pair(da + 2 * pl, db + 2 * pl, k, s, acc[2], na, 0); /* T3 */
+                ozaki_pair(da, db, k, s, b, acc[0], na, 0);                /* T1 */
+                ozaki_pair(da + pl, db + pl, k, s, b, acc[1], na, 0);      /* T2 */
+                ozaki_pair(da + 2 * pl, db + 2 * pl, k, s, b, acc[2], na, 0); /* T3 */
             }
-            int64_t e0 = eA + eB + 6 - 8 * (int64_t)(s + 1);
+            int64_t e0 = eA + eB + 6 - (int64_t)b * (s + 1);
             xn re, im;
             if (form == 4) {
                 re = xn_from_acc(acc[0], na, e0);
@@ -580,20 +607,30 @@ int orc_exponents(int64_t m, int64_t n, int64_t k,
 /* digit planes (slices of Algorithm 2 under the readings) of A (side 0: dig[part][alpha][i][q],
  * q < k) or B (side 1: dig[part][alpha][j][q], i.e. column j of B as a line).  nparts = 2
  * (Re, Im) or 3 (Re, Im, Re+Im). */
-int orc_split(int side, int64_t rows, int64_t k, const orc_rmat *Pre, const orc_rmat *Pim,
-              int32_t s, int32_t nparts, int8_t *dig)
+int orc_split_bits(int side, int64_t rows, int64_t k, const orc_rmat *Pre, const orc_rmat *Pim,
+                   int32_t s, int32_t bits, int32_t nparts, int32_t *dig)
 {
-    int8_t *tmp = (int8_t *)malloc((size_t)nparts * s * (k ? k : 1));
+    int32_t *tmp = (int32_t *)malloc(sizeof(int32_t) * (size_t)nparts * s * (k ? k : 1));
     int rc = 0;
     for (int64_t r = 0; r < rows && !rc; r++) {
         int64_t e;
         line_exponent(Pre, Pim, side, r, k, &e);
-        if (line_digits(Pre, Pim, side, r, k, e, s, nparts, tmp)) { rc = -2; break; }
+        if (line_digits(Pre, Pim, side, r, k, e, s, bits, nparts, tmp)) { rc = -2; break; }
         for (int p = 0; p < nparts; p++)
             for (int a = 0; a < s; a++)
-                memcpy(dig + (((int64_t)p * s + a) * rows + r) * k, tmp + ((int64_t)p * s + a) * k, (size_t)k);
+                memcpy(dig + (((int64_t)p * s + a) * rows + r) * k, tmp + ((int64_t)p * s + a) * k, sizeof(int32_t) * (size_t)k);
     }
     free(tmp);
+    return rc;
+}
+
+int orc_split(int side, int64_t rows, int64_t k, const orc_rmat *Pre, const orc_rmat *Pim,
+              int32_t s, int32_t nparts, int8_t *dig)
+{
+    int32_t *d32 = (int32_t *)malloc(sizeof(int32_t) * (size_t)nparts * s * (rows ? rows : 1) * (k ? k : 1));
+    int rc = orc_split_bits(side, rows, k, Pre, Pim, s, 8, nparts, d32);
+    for (int64_t q = 0; q < (int64_t)nparts * s * rows * k; q++) dig[q] = (int8_t)d32[q];
+    free(d32);
     return rc;
 }
 
@@ -705,7 +742,14 @@ int orc_rho_bounds(int64_t m, int64_t n, int64_t k,
  *                             log2((double)k) + 2.0 + (double)maxD2 )          [maxD2 >= 0]
  *   minT < 0 : log2rho = 0 (the product is identically zero)
  *   s = min{ s >= 1 : 8.0 s >= prec - 4.0 + log2(c_M s) + log2rho + 0.1 }, c_4M = 3, c_3M = 4 */
+int32_t orc_slices_for_bits(int32_t prec, int32_t form, int64_t k, int64_t minT, int64_t minT1, int64_t maxD2,
+                            int32_t bits);
 int32_t orc_slices_for(int32_t prec, int32_t form, int64_t k, int64_t minT, int64_t minT1, int64_t maxD2) {
+    return orc_slices_for_bits(prec, form, k, minT, minT1, maxD2, 8);
+}
+/* the rule with b-bit digits: min{ s : b s >= prec - 4 + log2(c_M s) + log2rho + 0.1 } */
+int32_t orc_slices_for_bits(int32_t prec, int32_t form, int64_t k, int64_t minT, int64_t minT1, int64_t maxD2,
+                            int32_t bits) {
     double c = form == 3 ? 4.0 : 3.0;
     double log2rho = 0.0;
     if (minT > 0) log2rho = log2((double)k) + 14.0 - log2((double)minT);
@@ -716,6 +760,6 @@ int32_t orc_slices_for(int32_t prec, int32_t form, int64_t k, int64_t minT, int6
         if (log2rho < -1e299) log2rho = 0.0;
     }
     for (int32_t s = 1; s < 1000000; s++)
-        if (8.0 * s >= (double)prec - 4.0 + log2(c * s) + log2rho + 0.1) return s;
+        if ((double)bits * s >= (double)prec - 4.0 + log2(c * s) + log2rho + 0.1) return s;
     return -1;
 }
