@@ -80,7 +80,10 @@ typedef struct {
                                  (in place) and the exact sum is rounded once (SURVEY NEXT-2:
                                  the LU trailing update A22 - L21 U12)      */
     int32_t  alpha_neg;       /* 1: alpha = -1, else alpha = +1                                 */
-    int32_t  reserved;
+    int32_t  carrier;         /* slice carrier: 0 = INT8 digits on tcgen05 (default);
+                                 1 = the paper's binary64 slices, b = 53 - ceil((53 +
+                                 ceil(log2 k)) / 2) bits, on FP64 DMMA (SURVEY
+                                 NEXT-1; beta / alpha_neg not supported there)                  */
 } mpcgemm_opts;
 
 typedef struct {
@@ -91,6 +94,7 @@ typedef struct {
     int64_t mma_instructions; /* tcgen05.mma count issued by the slice GEMM (K=32 each)         */
     int64_t work_units;       /* slice-GEMM work units (tile, diagonal, chunk, product)         */
     int32_t kernel_launches;  /* kernels this call launched (memsets/copies excluded)           */
+    int32_t slice_bits;       /* digit width b: 8 (INT8 carrier) or the binary64 slice width   */
     int32_t slicegemm_ctas;   /* grid of the slice-GEMM launch                                 */
     float   ms_linemax, ms_prepass, ms_split, ms_gemm, ms_fold;   /* opts->timing only         */
 } mpcgemm_report;

@@ -54,4 +54,13 @@ cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st);
 
 cudaError_t zero_output_launch(DMatOut C, int64_t m, int64_t n, int L, cudaStream_t st);
 
+// NEXT-1: binary64 slice carrier on FP64 DMMA (fp64path.cu)
+cudaError_t split_f64_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
+                             const int64_t *eline, int s, int b, int nparts, double *dig, cudaStream_t st);
+cudaError_t dmma_slicegemm_launch(const double *digA, const double *digB, int64_t m, int64_t n, int64_t kp, int s,
+                                  const int4 *units, int nunits, const JobDesc *jobs, int njobs, int64_t *partials,
+                                  cudaStream_t st);
+cudaError_t fold_f64_launch(const int64_t *partials, int64_t m, int64_t n, int s, int b, int method, int prec, int L,
+                            const int64_t *eA, const int64_t *eB, DMatOut Cre, DMatOut Cim, cudaStream_t st);
+
 }  // namespace mpc

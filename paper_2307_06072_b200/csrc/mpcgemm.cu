@@ -410,11 +410,81 @@ double rule_log2rho(int64_t k, int64_t minT, int64_t minT1, int64_t maxD2) {
     return log2rho;
 }
 
-int rule_slices(int32_t prec, int method, double log2rho) {
+// the slice rule for b-bit digits (b = 8: INT8 carrier)
+int rule_slices(int32_t prec, int method, double log2rho, int bits = 8) {
     const double c = method == 3 ? 4.0 : 3.0;
     for (int s = 1; s <= kMaxSlices; s++)
-        if (8.0 * s >= (double)prec - 4.0 + log2(c * s) + log2rho + 0.1) return s;
+        if ((double)bits * s >= (double)prec - 4.0 + log2(c * s) + log2rho + 0.1) return s;
     return MPCGEMM_ERR_SLICES;
+}
+
+// b = 53 - ceil((53 + ceil(log2 k)) / 2): the paper's binary64 slice width
+int fp64_slice_bits(int64_t k) {
+    int lk = 0;
+    while ((1ll << lk) < k) lk++;
+    return 53 - (53 + lk + 1) / 2;
+}
+
+struct F64Plan {
+    int4 *d_units = nullptr;
+    JobDesc *d_jobs = nullptr;
+    int nunits = 0;
+};
+std::map<std::tuple<int, int64_t, int64_t, int, int>, F64Plan> g_f64plans;
+
+// NEXT-1 path: binary64 digits on FP64 DMMA (fp64path.cu)
+int run_main_f64(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
+                 mpc_cmat *C, int method, int s, int b, cudaStream_t st, uint8_t *meta, uint8_t *big,
+                 mpcgemm_report *rep, StageEvents *E) {
+    const int L = (prec + 63) / 64;
+    int64_t *eA = (int64_t *)meta, *eB = eA + m;
+    const int parts = method == 3 ? 3 : 2;
+    const int64_t kp = (int64_t)align_up((size_t)k, 16);
+    double *digA = (double *)big;
+    double *digB = (double *)((uint8_t *)digA + align_up((size_t)parts * s * m * kp * 8, 256));
+    int64_t *partials = (int64_t *)((uint8_t *)digB + align_up((size_t)parts * s * n * kp * 8, 256));
+    CK(split_f64_launch(dm(A->re), dm(A->im), 0, m, k, kp, L, eA, s, b, parts, digA, st));
+    CK(split_f64_launch(dm(B->re), dm(B->im), 1, n, k, kp, L, eB, s, b, parts, digB, st));
+    if (E) CK(cudaEventRecord(E->ev[3], st));
+    auto key = std::make_tuple(dev, m, n, s, method);
+    auto it = g_f64plans.find(key);
+    if (it == g_f64plans.end()) {
+        Plan P;
+        method_jobs(method, P);
+        std::vector<int4> units;
+        const int tm = (int)((m + 63) / 64), tn = (int)((n + 63) / 64);
+        for (int r = s + 1; r >= 2; r--)                   // longest diagonals first
+            for (int q = 0; q < P.njobs; q++)
+                for (int a = 0; a < tm; a++)
+                    for (int c = 0; c < tn; c++) units.push_back(make_int4(q, a, c, r));
+        F64Plan F;
+        F.nunits = (int)units.size();
+        if (cudaMalloc(&F.d_units, sizeof(int4) * units.size()) != cudaSuccess ||
+            cudaMalloc(&F.d_jobs, sizeof(JobDesc) * kMaxJobs) != cudaSuccess)
+            return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc f64 plan");
+        CK(cudaMemcpy(F.d_units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(F.d_jobs, P.jobs, sizeof(JobDesc) * kMaxJobs, cudaMemcpyHostToDevice));
+        it = g_f64plans.emplace(key, F).first;
+    }
+    CK(dmma_slicegemm_launch(digA, digB, m, n, kp, s, it->second.d_units, it->second.nunits, it->second.d_jobs,
+                             3, partials, st));
+    if (E) CK(cudaEventRecord(E->ev[4], st));
+    CK(fold_f64_launch(partials, m, n, s, b, method, prec, L, eA, eB, dmo(C->re), dmo(C->im), st));
+    if (E) CK(cudaEventRecord(E->ev[5], st));
+    if (rep) {
+        rep->kernel_launches += 4;
+        rep->work_units = it->second.nunits;
+        rep->slicegemm_ctas = it->second.nunits;
+        rep->mma_instructions = 0;
+    }
+    return 0;
+}
+
+size_t f64_main_bytes(int64_t m, int64_t n, int64_t k, int s, int method) {
+    const int parts = method == 3 ? 3 : 2;
+    const int64_t kp = (int64_t)align_up((size_t)std::max<int64_t>(k, 1), 16);
+    return align_up((size_t)parts * s * m * kp * 8, 256) + align_up((size_t)parts * s * n * kp * 8, 256) +
+           align_up((size_t)3 * (s + 2) * m * n * 8, 256);
 }
 
 // the device hot path with a known workspace
@@ -471,7 +541,11 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     const int validate = opts ? opts->validate : 0;
     const int beta = opts ? (opts->beta != 0) : 0;
     const int alpha_neg = opts ? (opts->alpha_neg != 0) : 0;
+    const int carrier = opts ? opts->carrier : 0;
     const int simt = env_int("MPCGEMM_SLICEGEMM_SIMT", 0);
+    if (carrier != 0 && carrier != 1) return fail(MPCGEMM_ERR_ARG, "carrier must be 0 (INT8) or 1 (FP64)");
+    if (carrier == 1 && (beta || alpha_neg)) return fail(MPCGEMM_ERR_ARG, "beta / alpha_neg need the INT8 carrier");
+    const int bits = carrier == 1 ? fp64_slice_bits(k) : 8;
     if (forced < 0 || forced > kMaxSlices) return fail(MPCGEMM_ERR_SLICES, "forced slices outside [1, 1024]");
     if (rep) { memset(rep, 0, sizeof(*rep)); rep->minT = rep->minT1 = rep->maxD2 = -1; }
     const int L = (prec + 63) / 64;
@@ -512,8 +586,27 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, pb)) return rc;
         launches += 4 + (pb[0] == 0 ? 1 : 0);         // planes x2, T GEMM, min [, max-plus]
         log2rho = rule_log2rho(k, pb[0], pb[1], pb[2]);
-        s = rule_slices(prec, method, log2rho);
+        s = rule_slices(prec, method, log2rho, bits);
         if (s < 0) return fail(MPCGEMM_ERR_SLICES, "slice rule needs s > 1024");
+    }
+    if (carrier == 1) {
+        uint8_t *big;
+        if (int rc = grow(&dc.ws, &dc.ws_bytes, f64_main_bytes(m, n, k, s, method))) return rc;
+        big = (uint8_t *)dc.ws;
+        if (E) CK(cudaEventRecord(E->ev[2], st));
+        if (rep) rep->kernel_launches = launches;
+        if (int rc = run_main_f64(dev, m, n, k, prec, A, B, C, method, s, bits, st, meta, big, rep, E)) return rc;
+        if (rep) {
+            rep->slices = s; rep->slice_bits = bits; rep->certified = 1; rep->minT = pb[0]; rep->minT1 = pb[1];
+            rep->maxD2 = pb[2]; rep->log2_rho_hat = log2rho;
+        }
+        if (E) {
+            CK(cudaEventSynchronize(E->ev[5]));
+            float t[5];
+            for (int q = 0; q < 5; q++) CK(cudaEventElapsedTime(&t[q], E->ev[q], E->ev[q + 1]));
+            if (rep) { rep->ms_linemax = t[0]; rep->ms_prepass = t[1]; rep->ms_split = t[2]; rep->ms_gemm = t[3]; rep->ms_fold = t[4]; }
+        }
+        return 0;
     }
     Layout Lm = layout_for(m, n, k, s, method, main_geometry(dev, m, n, k, s, method).maxkb);
     uint8_t *big;
@@ -529,8 +622,8 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     if (int rc = run_main(dev, m, n, k, prec, A, B, C, method, s, st, meta, big, Lm, simt, rep, E, beta, alpha_neg))
         return rc;
     if (rep) {
-        rep->slices = s; rep->certified = 1; rep->minT = pb[0]; rep->minT1 = pb[1]; rep->maxD2 = pb[2];
-        rep->log2_rho_hat = log2rho;
+        rep->slices = s; rep->slice_bits = 8; rep->certified = 1; rep->minT = pb[0]; rep->minT1 = pb[1];
+        rep->maxD2 = pb[2]; rep->log2_rho_hat = log2rho;
     }
     if (E) {
         CK(cudaEventSynchronize(E->ev[5]));

@@ -44,14 +44,14 @@ class OptsC(ctypes.Structure):
     _fields_ = [("stream", ctypes.c_void_p), ("slices", ctypes.c_int32), ("validate", ctypes.c_int32),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("timing", ctypes.c_int32), ("beta", ctypes.c_int32), ("alpha_neg", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("carrier", ctypes.c_int32)]
 
 
 class ReportC(ctypes.Structure):
     _fields_ = [("slices", ctypes.c_int32), ("certified", ctypes.c_int32), ("minT", ctypes.c_int64),
                 ("minT1", ctypes.c_int64), ("maxD2", ctypes.c_int64), ("log2_rho_hat", ctypes.c_double),
                 ("mma_instructions", ctypes.c_int64), ("work_units", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int32), ("slicegemm_ctas", ctypes.c_int32),
+                ("kernel_launches", ctypes.c_int32), ("slice_bits", ctypes.c_int32), ("slicegemm_ctas", ctypes.c_int32),
                 ("ms_linemax", ctypes.c_float), ("ms_prepass", ctypes.c_float), ("ms_split", ctypes.c_float),
                 ("ms_gemm", ctypes.c_float), ("ms_fold", ctypes.c_float)]
 
@@ -183,7 +183,7 @@ def _stream_ptr(stream):
 # ------------------------------------------------------------------ the calls (names = ABI)
 def mpcgemm_ex(A: DevCMat, B: DevCMat, C: DevCMat, prec: int, method="3M", slices: int = 0,
                validate: int = 0, stream=None, workspace=None, timing: int = 0, beta: int = 0,
-               alpha_neg: int = 0) -> dict:
+               alpha_neg: int = 0, carrier: int = 0) -> dict:
     """C := beta C + (-1)^alpha_neg A B on the device (stream-ordered).  Returns the report."""
     m, k = A.shape
     k2, n = B.shape
@@ -192,7 +192,7 @@ def mpcgemm_ex(A: DevCMat, B: DevCMat, C: DevCMat, prec: int, method="3M", slice
     opts = OptsC(_stream_ptr(stream), slices, validate,
                  workspace.data_ptr() if workspace is not None else None,
                  workspace.numel() * workspace.element_size() if workspace is not None else 0, timing, beta,
-                 alpha_neg, 0)
+                 alpha_neg, carrier)
     rep = ReportC()
     a, b, c = A.c(), B.c(), C.c()
     rc = lib().mpcgemm_ex(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), METHODS[method],
@@ -201,11 +201,12 @@ def mpcgemm_ex(A: DevCMat, B: DevCMat, C: DevCMat, prec: int, method="3M", slice
     return {f: getattr(rep, f) for f, _ in ReportC._fields_} | {"status": rc}
 
 
-def gemm(A: DevCMat, B: DevCMat, prec: int | None = None, method="3M", slices: int = 0, stream=None):
+def gemm(A: DevCMat, B: DevCMat, prec: int | None = None, method="3M", slices: int = 0, stream=None,
+         carrier: int = 0):
     """Allocating convenience wrapper: returns (C, report)."""
     prec = A.prec if prec is None else prec
     C = empty_device(A.shape[0], B.shape[1], prec, device=A.re.sign.device)
-    rep = mpcgemm_ex(A, B, C, prec, method, slices, stream=stream)
+    rep = mpcgemm_ex(A, B, C, prec, method, slices, stream=stream, carrier=carrier)
     return C, rep
 
 

@@ -326,3 +326,28 @@ def test_accumulate_host_entry_and_beta0():
     assert same_bits(C, oracle.ozaki_acc(A, B, C0, prec, "3M", s, beta=1, alpha_neg=1))
     C, _ = P.mpcgemm_host(A, B, prec, "3M", alpha_neg=1)                       # beta = 0: -A B
     assert same_bits(C, oracle.ozaki_acc(A, B, C0, prec, "3M", s, beta=0, alpha_neg=1))
+
+
+# ------------------------------------------------------------------ NEXT-1: binary64 carrier on DMMA
+@pytest.mark.parametrize("method", ["3M", "4M"])
+@pytest.mark.parametrize("m,n,k,prec,spread,d", [(70, 90, 100, 256, 4, 0), (130, 65, 257, 512, 0, 0),
+                                                 (40, 50, 1024, 256, 0, 13), (33, 17, 64, 128, 8, 9)])
+def test_fp64_carrier_bitexact(method, m, n, k, prec, spread, d):
+    """carrier = 1: b-bit binary64 slices multiplied on FP64 DMMA, bit-exact vs the oracle's
+    Algorithm 2 with the paper's slice width for the same d (auto rule when d = 0)."""
+    A = mpgen.random_cmat(k + d, 1, m, k, prec, spread, zero_frac=0.05)
+    B = mpgen.random_cmat(k + d, 2, k, n, prec, spread, zero_frac=0.05)
+    b = oracle.fp64_slice_bits(k)
+    dA, dB = P.to_device(A), P.to_device(B)
+    dC, rep = P.gemm(dA, dB, prec, method, slices=d, carrier=1)
+    torch.cuda.synchronize()
+    C = P.to_host(dC)
+    assert rep["slice_bits"] == b
+    if d == 0:
+        assert rep["slices"] == oracle.slices_for_bits(prec, method, k, *oracle.rho_bounds(A, B), b)
+    si, sj = sample_idx(m, n, 60, seed=k)
+    Rs = oracle.ozaki_bits(A, B, prec, method, rep["slices"], b, samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
+    if d == 0:
+        Xs = oracle.exact(A, B, prec + 64, method, samples=(si, sj))
+        assert max_err_log2(A, B, C, Xs, samples=(si, sj), ref_is_sampled=True) <= -(prec - BOUND[method])
