@@ -253,8 +253,10 @@ def main():
         "gpu_launches": int(sum(r["kernel_launches"] for r in reps)),
         "clocks": clk,
     }
-    if rank == 0 and world == 1 and not args.no_e2e:
-        line["e2e"] = e2e_measure(P, A, B, prec, args)
+    if not args.no_e2e:
+        e2e = e2e_measure(P, A, B, prec, args, world, dev)       # every rank; max over ranks
+        if rank == 0:
+            line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, desc = cpu_oracle_sample(A, B, prec, args.method, s, target_s=args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
@@ -264,9 +266,12 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_measure(P, A, B, prec, args):
-    """Same metric through the C ABI on HOST buffers (pinned), H2D + D2H inside the timed call."""
+def e2e_measure(P, A, B, prec, args, world=1, dev=None):
+    """Same metric through the C ABI on HOST buffers (pinned), H2D + D2H inside the timed call.
+    Each rank times its own rows (wall clock around the blocking call); value = all ranks'
+    CMACs / the max over ranks of the median time."""
     import torch
+    import torch.distributed as dist
 
     def pinned(R):
         out = []
@@ -283,18 +288,50 @@ def e2e_measure(P, A, B, prec, args):
     m, k = A.shape
     n = B.shape[1]
     hC = mpgen.CMat(pinned(mpgen.empty_rmat(m, n, prec)), pinned(mpgen.empty_rmat(m, n, prec)))
-    P.mpcgemm_host(hA, hB, prec, args.method, C=hC)          # warm-up (staging allocation)
+    if world == 1:
+        def run():
+            P.mpcgemm_host(hA, hB, prec, args.method, C=hC)
+    else:
+        # N > 1: the Python public API -- pinned host -> device copies, dist protocol (pre-pass
+        # all-reduce + mpcgemm_ex on this rank's rows), device -> pinned host copy of C
+        from paper_2307_06072_b200 import dist as pdist
+        dA, dB = P.to_device(A, dev), P.to_device(B, dev)
+        dC = P.empty_device(m, n, prec, dev)
+        srcs = [(getattr(dX, p_), getattr(hX, p_)) for dX, hX in ((dA, hA), (dB, hB)) for p_ in ("re", "im")]
+
+        def run():
+            for dR, hR in srcs:
+                for f in ("sign", "exp"):
+                    getattr(dR, f).copy_(torch.from_numpy(getattr(hR, f)), non_blocking=True)
+                dR.limbs.copy_(torch.from_numpy(hR.limbs.view(np.int64)), non_blocking=True)
+            kk = B.shape[0]
+            s_, _ = pdist.common_slices(lambda full: P.mpcgemm_rho_bounds(dA, dB, prec, full), P.mpcgemm_slices_for,
+                                        prec, args.method, kk, device=dev)
+            P.mpcgemm_ex(dA, dB, dC, prec, args.method, slices=s_)
+            for dR, hR in ((dC.re, hC.re), (dC.im, hC.im)):
+                torch.from_numpy(hR.sign).copy_(dR.sign, non_blocking=True)
+                torch.from_numpy(hR.exp).copy_(dR.exp, non_blocking=True)
+                torch.from_numpy(hR.limbs.view(np.int64)).copy_(dR.limbs, non_blocking=True)
+            torch.cuda.synchronize()
+    run()                                                        # warm-up (staging allocation)
     ts = []
     for _ in range(max(2, min(args.steps, 3))):
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        P.mpcgemm_host(hA, hB, prec, args.method, C=hC)
+        run()
         ts.append(time.perf_counter() - t0)
     t = statistics.median(ts)
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
     ent = lambda R: R.sign.nbytes + R.exp.nbytes + R.limbs.nbytes
-    return {"value": m * n * k / t, "unit": UNIT, "h2d_bytes_per_step": ent(A.re) + ent(A.im) + ent(B.re) + ent(B.im),
+    return {"value": world * m * n * k / t, "unit": UNIT, "h2d_bytes_per_step": ent(A.re) + ent(A.im) + ent(B.re) + ent(B.im),
             "d2h_bytes_per_step": 2 * (m * n * (9 + 8 * ((prec + 63) // 64))), "ms_per_step": 1e3 * t,
-            "api": "mpcgemm_host (C ABI, pinned host buffers)"}
+            "api": "mpcgemm_host (C ABI, pinned host buffers)" if world == 1 else
+                   "pinned host copies + dist protocol + mpcgemm_ex (Python public API)"}
 
 
 if __name__ == "__main__":
