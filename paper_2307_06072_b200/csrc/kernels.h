@@ -48,7 +48,10 @@ struct FoldParams {
     DMatOut Cre, Cim;
     int32_t beta, alpha_neg;     // NEXT-2: C = beta C0 + (-1)^alpha_neg A B (one rounding)
     DMat C0re, C0im;             // may alias Cre / Cim
+    uint64_t *fix;               // fixed-point scratch, fold_scratch_words(m, ldF, s, L, beta) words
+    int64_t ldF;                 // scratch row pitch (even, >= n)
 };
+size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta);
 // a-5 + a-6: exact fold (chunk sums, Eq. 5/6 combination, carry) and RNE normalization
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st);
 

@@ -325,7 +325,7 @@ int64_t count_slots(int64_t k, int s, int method, int maxkb) {
     return n;
 }
 
-Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb) {
+Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb, int prec = 64, bool beta = false) {
     Layout Lo;
     Lo.kp = align_up((size_t)std::max<int64_t>(k, 1), 16);
     Lo.nstrips = (std::max<int64_t>(n, 1) + kStrip - 1) / kStrip;
@@ -339,7 +339,8 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb)
         const int parts = method == 3 ? 3 : 2;
         const int64_t nslots = count_slots(k, s, method, maxkb);
         Lo.main = align_up((size_t)parts * s * m * Lo.kp, 256) + align_up((size_t)parts * s * n * Lo.kp, 256) +
-                  align_up((size_t)nslots * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256);
+                  align_up((size_t)nslots * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256) +
+                  align_up(fold_scratch_words(m, (n + 1) & ~1ll, s, (prec + 63) / 64, beta) * 8, 256);
     }
     return Lo;
 }
@@ -523,6 +524,9 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     F.s = s; F.method = method; F.prec = prec; F.L = L; F.slotinfo = plan->d_slotinfo;
     F.eA = eA; F.eB = eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
     F.beta = beta; F.alpha_neg = alpha_neg; F.C0re = dm(C->re); F.C0im = dm(C->im);
+    F.ldF = (n + 1) & ~1ll;
+    F.fix = (uint64_t *)((uint8_t *)partials +
+                         align_up((size_t)plan->nslots * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
     CK(fold_normalize_launch(F, st));
     if (E) CK(cudaEventRecord(E->ev[5], st));
     if (rep) {
@@ -608,7 +612,7 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         }
         return 0;
     }
-    Layout Lm = layout_for(m, n, k, s, method, main_geometry(dev, m, n, k, s, method).maxkb);
+    Layout Lm = layout_for(m, n, k, s, method, main_geometry(dev, m, n, k, s, method).maxkb, prec, beta != 0);
     uint8_t *big;
     if (opts && opts->workspace) {
         if (opts->workspace_bytes < Lm.main) return fail(MPCGEMM_ERR_NOMEM, "caller workspace too small");
@@ -683,7 +687,7 @@ size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec, mpc
     (void)prec;
     int dev = 0;
     cudaGetDevice(&dev);
-    Layout Lo = layout_for(m, n, k, slices, (int)method, main_geometry(dev, m, n, k, slices, (int)method).maxkb);
+    Layout Lo = layout_for(m, n, k, slices, (int)method, main_geometry(dev, m, n, k, slices, (int)method).maxkb, prec, true);
     return std::max(Lo.main, Lo.pre);
 }
 

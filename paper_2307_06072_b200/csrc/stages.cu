@@ -406,7 +406,7 @@ cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t nstrips,
 // final carry sign-extended at bit 8s.  normalize_store rounds it once (RNE) to prec bits.
 struct FixView {
     const uint64_t *base;   // fix[0][thread]
-    int stride;             // threads per block
+    int64_t stride;         // distance between consecutive limbs
     int n;                  // limbs
     MPC_DEV uint64_t at(int64_t l) const { return (l >= 0 && l < n) ? base[l * stride] : 0ull; }
     MPC_DEV uint64_t bits64(int64_t pos) const {
@@ -422,7 +422,7 @@ struct FixView {
 
 // RNE of a magnitude buf[0..n) (column of stride `stride`, LSB weight 2^e_lsb) to prec bits,
 // stored in the ABI element format with sign `neg`.
-MPC_DEV void round_store(const uint64_t *buf, int stride, int n, int64_t e_lsb, bool neg, int prec, int L,
+MPC_DEV void round_store(const uint64_t *buf, int64_t stride, int n, int64_t e_lsb, bool neg, int prec, int L,
                          uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
 {
     int b = 0;
@@ -474,7 +474,7 @@ MPC_DEV void round_store(const uint64_t *buf, int stride, int n, int64_t e_lsb, 
 }
 
 // two's complement fix[0..Lc) -> magnitude in place; returns the sign
-MPC_DEV bool to_magnitude(uint64_t *fix, int stride, int Lc) {
+MPC_DEV bool to_magnitude(uint64_t *fix, int64_t stride, int Lc) {
     const bool neg = (int64_t)fix[(int64_t)(Lc - 1) * stride] < 0;
     if (neg) {
         uint64_t c = 1;
@@ -488,7 +488,7 @@ MPC_DEV bool to_magnitude(uint64_t *fix, int stride, int Lc) {
 }
 
 // fix (two's complement, LSB weight 2^e0) -> RNE((-1)^alpha_neg fix 2^e0) in the ABI format
-MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, bool alpha_neg, int prec, int L,
+MPC_DEV void normalize_store(uint64_t *fix, int64_t stride, int Lc, int64_t e0, bool alpha_neg, int prec, int L,
                              uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
 {
     const bool neg = to_magnitude(fix, stride, Lc);
@@ -500,10 +500,11 @@ MPC_DEV void normalize_store(uint64_t *fix, int stride, int Lc, int64_t e0, bool
 // of 64 Lw >= 64 (Lc + L + 3) bits below the larger operand's top; bits of the smaller operand
 // below the window collapse into a sticky LSB (>= 2 guard bits below the rounding position).
 // C0 (N, L limbs, LSB weight 2^(exp - 64 L)) may alias the output element (read first).
-MPC_DEV void accumulate_store(uint64_t *fix, int stride, int Lc, int Lw, int64_t e0, bool alpha_neg,
+MPC_DEV void accumulate_store(uint64_t *fix, int unused, int Lc, int Lw, int64_t e0, bool alpha_neg,
                               uint8_t c0s, int64_t c0e, const uint64_t *c0l, int prec, int L,
-                              uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
+                              uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out, int64_t stride, uint64_t *R)
 {
+    (void)unused;
     const bool sV = to_magnitude(fix, stride, Lc) != alpha_neg;
     int bV = 0;
     for (int l = Lc - 1; l >= 0; l--) {
@@ -547,7 +548,6 @@ MPC_DEV void accumulate_store(uint64_t *fix, int stride, int Lc, int Lw, int64_t
     };
     const bool stV = below([&](int64_t l) { return V.at(l); }, Lc, WB - e0);
     const bool stC = below([&](int64_t l) { return l < L ? cN[l] : 0ull; }, L, WB - E1);
-    uint64_t *R = fix + (int64_t)Lc * stride;
     // compare |X| and |Y| (aligned) from the top when subtracting
     const bool sub = sV != sC;
     bool xbig = true;
@@ -578,155 +578,186 @@ MPC_DEV void accumulate_store(uint64_t *fix, int stride, int Lc, int Lw, int64_t
 }
 
 // The partial planes are streamed by a producer warp with cp.async.bulk: for each slot (in
-// the order r = s+1..2, job, chunk) the contiguous strip partials[slot][i][j0 .. j0+T) lands in
-// a RING-deep shared-memory ring, so ~RING KB per block are in flight regardless of the
-// consumers' registers.  T consumer threads (one output j each) run the carry chains.
+// the fold's consumption order r = s+1..2, job, chunk) the strip partials[slot][i][j0 .. j0+COLS)
+// lands in a shared-memory ring (PER slots per entry, RING entries), so ~RING*PER*COLS*4 bytes
+// per block are in flight regardless of the consumers' registers.  COLS/2 consumer threads (two
+// adjacent outputs each) walk a flat per-slot schedule (job of the slot, last slot of r) and run
+// the carry chains; the fixed-point numbers live in shared memory, fix[part][limb][column].
 constexpr int kFoldRing = 4;           // entries
-constexpr int kFoldPer = 8;            // slots per entry (one 8 KB bulk copy at T = 256)
+constexpr int kFoldPer = 8;            // slots per entry
+constexpr int kFoldEPT = 2;            // outputs per consumer thread
 
-template <int kFoldT, bool BETA>
-__global__ void __launch_bounds__(kFoldT + 32)
+template <int COLS, bool BETA>
+__global__ void __launch_bounds__(COLS / kFoldEPT + 32)
 fold_normalize_kernel(const FoldParams F)
 {
+    constexpr int NCONS = COLS / kFoldEPT;            // consumer threads
     extern __shared__ __align__(128) uint8_t fsm_raw[];
     const int s = F.s;
-    const int Lc0 = s / 8 + 3;                       // fixed-point limbs
-    const int Lw = BETA ? Lc0 + F.L + 3 : 0;         // NEXT-2 sum window
-    const int Lc = Lc0 + Lw;                         // limbs per part in shared memory
-    int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                       // [RING][PER][T]
-    uint64_t *fix = reinterpret_cast<uint64_t *>(fsm_raw + kFoldRing * kFoldPer * kFoldT * 4);  // [2][Lc][T]
-    int32_t *slots = reinterpret_cast<int32_t *>(fix + 2 * (int64_t)Lc * kFoldT);  // [job][r][base,cnt]
-    uint64_t *full = reinterpret_cast<uint64_t *>(slots + kMaxJobs * (s + 2) * 2 + 2);
-    full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(full) + 7) & ~uintptr_t(7));
+    const int Lc0 = s / 8 + 3;                        // fixed-point limbs
+    const int Lw = BETA ? Lc0 + F.L + 3 : 0;          // NEXT-2 sum window
+    const int nslots = (int)F.nslots;
+    int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                                   // [RING][PER][COLS]
+    uint8_t *sched = reinterpret_cast<uint8_t *>(fsm_raw + kFoldRing * kFoldPer * COLS * 4); // [nslots]
+    uint64_t *full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(sched + nslots) + 15) & ~uintptr_t(15));
     uint64_t *empty = full + kFoldRing;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int nsi = kMaxJobs * (s + 2) * 2;
-    for (int q = tid; q < nsi; q += blockDim.x) slots[q] = F.slotinfo[q];
+    // flat schedule: slot (r, q, c) -> q | 0x80 on the last slot of diagonal r
+    for (int x = tid; x < kMaxJobs * (s + 2); x += blockDim.x) {
+        const int q = x / (s + 2), r = x % (s + 2);
+        if (r < 2) continue;
+        const int base = F.slotinfo[(q * (s + 2) + r) * 2], cnt = F.slotinfo[(q * (s + 2) + r) * 2 + 1];
+        for (int c = 0; c < cnt; c++) sched[base + c] = (uint8_t)(q | ((q == kMaxJobs - 1 && c == cnt - 1) ? 0x80 : 0));
+    }
     if (tid == 0) {
-        for (int e = 0; e < kFoldRing; e++) { mbar_init(&full[e], 1); mbar_init(&empty[e], kFoldT / 32); }
+        for (int e = 0; e < kFoldRing; e++) { mbar_init(&full[e], 1); mbar_init(&empty[e], NCONS / 32); }
         fence_barrier_init();
     }
     __syncthreads();
-    // block (x, y): row i = (y / nsub) * 128 + x, columns j0 = (y % nsub) * T, so the 128 blocks
-    // of one (row block, strip) are adjacent in launch order
-    const int64_t nsub = (F.n + kFoldT - 1) / kFoldT;
+    // block (x, y): row i = (y / nsub) * 128 + x, columns j0 = (y % nsub) * COLS, so the 128
+    // blocks of one (row block, strip) are adjacent in launch order
+    const int64_t nsub = (F.n + COLS - 1) / COLS;
     const int64_t i = (int64_t)(blockIdx.y / nsub) * kRowBlk + blockIdx.x;
-    const int64_t j0 = (int64_t)(blockIdx.y % nsub) * kFoldT;   // kFoldT divides the 256-column strip
+    const int64_t j0 = (int64_t)(blockIdx.y % nsub) * COLS;      // COLS divides the 256-column strip
     if (i >= F.m) return;
-    if (warp == kFoldT / 32) {
-        // ---------------- producer warp: streams this (row, strip)'s slots 0..nslots-1 (the
-        // consumption order) into the ring, kFoldPer slots per entry, one expect_tx per entry
+    if (warp == NCONS / 32) {
+        // ---------------- producer warp
         if (lane == 0) {
             const int32_t *region = F.partials + part_off(i, j0, 0, F.nslots, F.nstrips);   // slot 0
             int e = 0; uint32_t ph = 0;
-            for (int64_t sl = 0; sl < F.nslots; sl += kFoldPer) {
-                const int cnt = (int)(F.nslots - sl < kFoldPer ? F.nslots - sl : kFoldPer);
+            for (int sl = 0; sl < nslots; sl += kFoldPer) {
+                const int cnt = nslots - sl < kFoldPer ? nslots - sl : kFoldPer;
                 mbar_wait(&empty[e], ph ^ 1);
-                mbar_arrive_expect_tx(&full[e], (uint32_t)(cnt * kFoldT * 4));
-                for (int f = 0; f < cnt; f++)                   // slot blocks are kTileElems apart
-                    bulk_load(ring + (e * kFoldPer + f) * kFoldT, region + (sl + f) * kTileElems, kFoldT * 4, &full[e]);
+                mbar_arrive_expect_tx(&full[e], (uint32_t)(cnt * COLS * 4));
+                for (int f = 0; f < cnt; f++)                // slot blocks are kTileElems apart
+                    bulk_load(ring + (e * kFoldPer + f) * COLS, region + (int64_t)(sl + f) * kTileElems, COLS * 4, &full[e]);
                 if (++e == kFoldRing) { e = 0; ph ^= 1; }
             }
         }
         return;
     }
-    // ---------------- consumers: one output element j per thread
-    const int64_t j = j0 + tid;
-    uint64_t cur0 = 0, cur1 = 0;
-    int64_t c0 = 0, c1 = 0;
+    // ---------------- consumers: outputs j0 + 2 tid, j0 + 2 tid + 1.  The fixed-point limbs go
+    // to the global scratch fix[part][limb][m*ldF] (column = element), read back by the rounding.
+    const int col = kFoldEPT * tid;
+    const int64_t jj = j0 + col;                      // first of the two elements
+    const int64_t lstride = F.m * F.ldF;              // limb stride in the scratch
+    uint64_t *fixg = F.fix + i * F.ldF + jj;
+    int64_t t0[2] = {0, 0}, t1[2] = {0, 0}, t2[2] = {0, 0};
+    int64_t cr[2][2] = {{0, 0}, {0, 0}};              // [part][element] carries
+    uint64_t cur[2][2] = {{0, 0}, {0, 0}};
     int e = 0, fill = 0; uint32_t ph = 0;
-    uint64_t *fix0 = fix + tid, *fix1 = fix + (int64_t)Lc * kFoldT + tid;
-    for (int r = s + 1; r >= 2; r--) {
-        int64_t t[kMaxJobs];
+    int b = 0;                                        // byte index = s + 1 - r
+    const bool live = jj < F.n;                       // (jj + 1 < n too: ldF is even and n is padded)
+    for (int sl = 0; sl < nslots; sl++) {
+        if (fill == 0) mbar_wait(&full[e], ph);
+        const int sc = sched[sl];
+        const int2 v = *reinterpret_cast<const int2 *>(ring + (e * kFoldPer + fill) * COLS + col);
+        const int q = sc & 3;
+        if (q == 0) { t0[0] += v.x; t0[1] += v.y; }
+        else if (q == 1) { t1[0] += v.x; t1[1] += v.y; }
+        else { t2[0] += v.x; t2[1] += v.y; }
+        if (++fill == kFoldPer) {
+            fill = 0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[e]);
+            if (++e == kFoldRing) { e = 0; ph ^= 1; }
+        }
+        if (sc & 0x80) {                              // diagonal r complete: combine and carry
+            const int sh = 8 * (b & 7);
 #pragma unroll
-        for (int q = 0; q < kMaxJobs; q++) {
-            const int cnt = slots[(q * (s + 2) + r) * 2 + 1];
-            int64_t v = 0;
-            for (int c = 0; c < cnt; c++) {
-                if (fill == 0) mbar_wait(&full[e], ph);
-                v += ring[(e * kFoldPer + fill) * kFoldT + tid];
-                if (++fill == kFoldPer) {
-                    fill = 0;
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[e]);
-                    if (++e == kFoldRing) { e = 0; ph ^= 1; }
-                }
+            for (int x = 0; x < 2; x++) {
+                int64_t d0, d1;
+                if (F.method == 3) { d0 = t0[x] - t1[x]; d1 = t2[x] - t0[x] - t1[x]; }   // Eq. 6
+                else               { d0 = t0[x] - t1[x]; d1 = t2[x]; }                   // Eq. 5
+                cr[0][x] += d0; cur[0][x] |= (uint64_t)(cr[0][x] & 0xFF) << sh; cr[0][x] >>= 8;
+                cr[1][x] += d1; cur[1][x] |= (uint64_t)(cr[1][x] & 0xFF) << sh; cr[1][x] >>= 8;
+                t0[x] = t1[x] = t2[x] = 0;
             }
-            t[q] = v;
-        }
-        int64_t d0, d1;
-        if (F.method == 3) { d0 = t[0] - t[1]; d1 = t[2] - t[0] - t[1]; }   // Eq. 6
-        else               { d0 = t[0] - t[1]; d1 = t[2]; }                 // Eq. 5
-        const int b = s + 1 - r;                                            // byte index
-        const int sh = 8 * (b & 7);
-        c0 += d0; cur0 |= (uint64_t)(c0 & 0xFF) << sh; c0 >>= 8;            // arithmetic shift
-        c1 += d1; cur1 |= (uint64_t)(c1 & 0xFF) << sh; c1 >>= 8;
-        if ((b & 7) == 7) {
-            fix0[(int64_t)(b >> 3) * kFoldT] = cur0; fix1[(int64_t)(b >> 3) * kFoldT] = cur1;
-            cur0 = 0; cur1 = 0;
+            if ((b & 7) == 7) {
+                if (live) {
+#pragma unroll
+                    for (int p = 0; p < 2; p++)
+                        *reinterpret_cast<ulonglong2 *>(fixg + ((int64_t)p * Lc0 + (b >> 3)) * lstride) =
+                            make_ulonglong2(cur[p][0], cur[p][1]);
+                }
+                cur[0][0] = cur[0][1] = cur[1][0] = cur[1][1] = 0;
+            }
+            b++;
         }
     }
-    if (j >= F.n) return;
-    // the final carry at bit 8s, sign-extended to Lc0 limbs
+    if (!live) return;
+    // the final carries at bit 8s, sign-extended to Lc0 limbs
     const int l0 = s >> 3, o = 8 * (s & 7);
-    {
-        const uint64_t c = (uint64_t)c0, sx = c0 < 0 ? ~0ull : 0ull;
-        fix0[(int64_t)l0 * kFoldT] = cur0 | (c << o);
-        fix0[(int64_t)(l0 + 1) * kFoldT] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
-        for (int l = l0 + 2; l < Lc0; l++) fix0[(int64_t)l * kFoldT] = sx;
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        uint64_t w[2][2];
+#pragma unroll
+        for (int x = 0; x < 2; x++) {
+            const uint64_t c = (uint64_t)cr[p][x], sx = cr[p][x] < 0 ? ~0ull : 0ull;
+            w[x][0] = cur[p][x] | (c << o);
+            w[x][1] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
+        }
+        uint64_t *fx = fixg + (int64_t)p * Lc0 * lstride;
+        *reinterpret_cast<ulonglong2 *>(fx + (int64_t)l0 * lstride) = make_ulonglong2(w[0][0], w[1][0]);
+        *reinterpret_cast<ulonglong2 *>(fx + (int64_t)(l0 + 1) * lstride) = make_ulonglong2(w[0][1], w[1][1]);
+        for (int l = l0 + 2; l < Lc0; l++)
+            *reinterpret_cast<ulonglong2 *>(fx + (int64_t)l * lstride) =
+                make_ulonglong2(cr[p][0] < 0 ? ~0ull : 0ull, cr[p][1] < 0 ? ~0ull : 0ull);
     }
-    {
-        const uint64_t c = (uint64_t)c1, sx = c1 < 0 ? ~0ull : 0ull;
-        fix1[(int64_t)l0 * kFoldT] = cur1 | (c << o);
-        fix1[(int64_t)(l0 + 1) * kFoldT] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
-        for (int l = l0 + 2; l < Lc0; l++) fix1[(int64_t)l * kFoldT] = sx;
-    }
-    const int64_t e0 = F.eA[i] + F.eB[j] + 6 - 8 * (int64_t)(s + 1);
-    const int64_t oi = i * F.Cre.ld + j;
-    const int64_t oj = i * F.Cim.ld + j;
-    if (BETA) {
-        const int64_t ci = i * F.C0re.ld + j, cj = i * F.C0im.ld + j;
-        const uint8_t s0 = F.C0re.sign[ci], s1 = F.C0im.sign[cj];       // read before the (aliasing) write
-        const int64_t x0 = F.C0re.exp[ci], x1 = F.C0im.exp[cj];
-        accumulate_store(fix0, kFoldT, Lc0, Lw, e0, F.alpha_neg, s0, x0, F.C0re.limbs + ci * F.L, F.prec, F.L,
-                         F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
-        accumulate_store(fix1, kFoldT, Lc0, Lw, e0, F.alpha_neg, s1, x1, F.C0im.limbs + cj * F.L, F.prec, F.L,
-                         F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
-    } else {
-        normalize_store(fix0, kFoldT, Lc0, e0, F.alpha_neg, F.prec, F.L, F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
-        normalize_store(fix1, kFoldT, Lc0, e0, F.alpha_neg, F.prec, F.L, F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
+#pragma unroll 1
+    for (int x = 0; x < 2; x++) {
+        const int64_t j = jj + x;
+        if (j >= F.n) break;
+        uint64_t *f0 = fixg + x, *f1 = fixg + x + (int64_t)(Lc0 + Lw) * lstride;   // parts: [0, Lc0+Lw), [Lc0+Lw, ..)
+        if (BETA) f1 = fixg + x + (int64_t)Lc0 * lstride;
+        const int64_t e0 = F.eA[i] + F.eB[j] + 6 - 8 * (int64_t)(s + 1);
+        const int64_t oi = i * F.Cre.ld + j;
+        const int64_t oj = i * F.Cim.ld + j;
+        if (BETA) {
+            uint64_t *R0 = F.fix + 2 * (int64_t)Lc0 * lstride + i * F.ldF + j;          // sum windows
+            const int64_t ci = i * F.C0re.ld + j, cj = i * F.C0im.ld + j;
+            const uint8_t s0 = F.C0re.sign[ci], s1 = F.C0im.sign[cj];   // read before the (aliasing) write
+            const int64_t x0 = F.C0re.exp[ci], x1 = F.C0im.exp[cj];
+            accumulate_store(f0, (int)0, Lc0, Lw, e0, F.alpha_neg, s0, x0, F.C0re.limbs + ci * F.L, F.prec, F.L,
+                             F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L, lstride, R0);
+            accumulate_store(f1, (int)0, Lc0, Lw, e0, F.alpha_neg, s1, x1, F.C0im.limbs + cj * F.L, F.prec, F.L,
+                             F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L, lstride, R0);
+        } else {
+            normalize_store(f0, lstride, Lc0, e0, F.alpha_neg, F.prec, F.L, F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
+            normalize_store(fixg + x + (int64_t)Lc0 * lstride, lstride, Lc0, e0, F.alpha_neg, F.prec, F.L,
+                            F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
+        }
     }
 }
 
-size_t fold_smem(int s, int T, int L, bool beta) {
-    const int Lc0 = s / 8 + 3;
-    const int Lc = Lc0 + (beta ? Lc0 + L + 3 : 0);
-    return (size_t)kFoldRing * kFoldPer * T * 4 + (size_t)2 * Lc * T * 8 + (size_t)kMaxJobs * (s + 2) * 2 * 4 + 16 +
-           (size_t)2 * kFoldRing * 8 + 16;
+size_t fold_smem(int s, int cols, int64_t nslots) {
+    (void)s;
+    return (size_t)kFoldRing * kFoldPer * cols * 4 + (size_t)nslots + 32 + (size_t)2 * kFoldRing * 8 + 16;
 }
 
-template <int T, bool BETA>
+template <int COLS, bool BETA>
 static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
-    const size_t sm = fold_smem(F.s, T, F.L, BETA);
-    if (sm > 227 * 1024) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(fold_normalize_kernel<T, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const size_t sm = fold_smem(F.s, COLS, F.nslots);
+    cudaError_t e = cudaFuncSetAttribute(fold_normalize_kernel<COLS, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    dim3 grid(kRowBlk, (unsigned)(((F.n + T - 1) / T) * ((F.m + kRowBlk - 1) / kRowBlk)));
-    fold_normalize_kernel<T, BETA><<<grid, T + 32, sm, st>>>(F);
+    dim3 grid(kRowBlk, (unsigned)(((F.n + COLS - 1) / COLS) * ((F.m + kRowBlk - 1) / kRowBlk)));
+    fold_normalize_kernel<COLS, BETA><<<grid, COLS / kFoldEPT + 32, sm, st>>>(F);
     return cudaGetLastError();
 }
 
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
 {
     if (F.m == 0 || F.n == 0) return cudaSuccess;
-    if (F.s > kMaxSlices) return cudaErrorInvalidValue;
-    if (F.beta) {
-        if (fold_smem(F.s, 128, F.L, true) <= 220 * 1024) return fold_launch_t<128, true>(F, st);
-        return fold_launch_t<32, true>(F, st);                                    // s up to 1024
-    }
-    if (fold_smem(F.s, 256, F.L, false) <= 220 * 1024) return fold_launch_t<256, false>(F, st);
-    return fold_launch_t<64, false>(F, st);                                       // s up to 1024
+    if (F.s > kMaxSlices || (F.ldF & 1)) return cudaErrorInvalidValue;
+    if (F.beta) return fold_launch_t<256, true>(F, st);
+    return fold_launch_t<256, false>(F, st);
+}
+
+// fixed-point scratch size (uint64 words) for the fold
+size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta) {
+    const int Lc0 = s / 8 + 3;
+    return (size_t)m * ldF * (2 * Lc0 + (beta ? Lc0 + L + 3 : 0));
 }
 
 __global__ void zero_output_kernel(DMatOut C, int64_t m, int64_t n, int L) {
