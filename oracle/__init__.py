@@ -56,6 +56,8 @@ def lib():
             L.orc_cgemm_ozaki.restype = ctypes.c_int
             L.orc_cgemm_ozaki_acc.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, P, P, i32, i32, i32, i64, vp, vp, i32]
             L.orc_cgemm_ozaki_acc.restype = ctypes.c_int
+            L.orc_cgemm_ozaki_rows.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, vp, i64, vp, vp, i32]
+            L.orc_cgemm_ozaki_rows.restype = ctypes.c_int
             L.orc_cgemm_ozaki_bits.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, i32, i64, vp, vp, i32]
             L.orc_cgemm_ozaki_bits.restype = ctypes.c_int
             L.orc_split_bits.argtypes = [ctypes.c_int, i64, i64, P, P, i32, i32, i32, vp]
@@ -124,6 +126,31 @@ def ozaki(A: CMat, B: CMat, prec_out: int, method="3M", s: int | None = None, sa
     if s is None:
         s, _ = auto_slices(A, B, A.prec, method)
     return _run(lib().orc_cgemm_ozaki, A, B, prec_out, method, s, samples, nthreads)
+
+
+def ozaki_rows(A: CMat, B: CMat, prec_out: int, method="3M", s_max: int = 1, srow=None, samples=None,
+               nthreads: int = 0) -> CMat:
+    """NEXT-4: Algorithm 2 with a per-row triangle d = srow[i] over the top srow[i] digits of
+    the s_max-digit expansions (orc_cgemm_ozaki_rows)."""
+    srow = np.ascontiguousarray(np.asarray(srow, dtype=np.int32))
+    assert srow.shape == (A.shape[0],)
+
+    def fn(m, n, k, a0, a1, b0, b1, c0, c1, prec, form, s, ns, si, sj, nt):
+        return lib().orc_cgemm_ozaki_rows(m, n, k, a0, a1, b0, b1, c0, c1, prec, form, s, srow.ctypes.data,
+                                          ns, si, sj, nt)
+    return _run(fn, A, B, prec_out, method, s_max, samples, nthreads)
+
+
+def block_slices(A: CMat, B: CMat, prec: int, method, block: int = 256, nthreads: int = 0):
+    """NEXT-4: the certified slice rule applied to each block of `block` rows of A (its own
+    rho-hat pre-pass over those rows and all of B).  Returns (list of s per block, ok)."""
+    m = A.shape[0]
+    out, ok = [], True
+    for r0 in range(0, m, block):
+        s, c = auto_slices(A.rows(r0, min(m, r0 + block)), B, prec, method, nthreads)
+        out.append(s)
+        ok = ok and c
+    return out, ok
 
 
 def ozaki_acc(A: CMat, B: CMat, C0: CMat, prec_out: int, method="3M", s: int | None = None, beta: int = 1,

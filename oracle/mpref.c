@@ -19,6 +19,7 @@
  *      representation (digit set [-128,127]), the triangle beta <= d-alpha+1
  *      (PAPER.md:174-177), exact accumulation (Z7) and one RNE rounding;
  *      complex forms by Eq. 5 (4M) / Eq. 6 (3M).
+ *      orc_cgemm_ozaki_rows: the same with a per-row d (NEXT-4).
  *  plus the slice-count rule:
  *      t_ik = floor(max(|ReA_ik|,|ImA_ik|) 2^(7-eA_i)), u_kj likewise, T = t u,
  *      log2rho = log2((double)k) + 14.0 - log2((double)minT),
@@ -459,6 +460,8 @@ static int line_digits(const orc_rmat *Pre, const orc_rmat *Pim, int side, int64
  * accumulated exactly (Z7) as the integer  sum (dA_alpha . dB_beta) 2^(b(s+1-alpha-beta))
  * into the two's complement accumulator acc (na limbs, weight 2^(eA+eB+6-b(s+1))). */
 static void ozaki_pair(const int32_t *da, const int32_t *db, int64_t k, int s, int b, uint64_t *acc, int na, int neg) {
+    /* s here is the triangle's d; the planes da/db may hold more digits (NEXT-4: the top s
+       digits of a longer expansion), only alpha, beta <= s are read */
     for (int alpha = 1; alpha <= s; alpha++) {
         const int32_t *xa = da + (int64_t)(alpha - 1) * k;
         for (int beta = 1; beta <= s - alpha + 1; beta++) {
@@ -479,7 +482,8 @@ static int ozaki_core(int64_t m, int64_t n, int64_t k,
                       const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
                       orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
                       int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads,
-                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg, int32_t bits);
+                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg, int32_t bits,
+                      const int32_t *srow);
 
 int orc_cgemm_ozaki(int64_t m, int64_t n, int64_t k,
                     const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
@@ -487,7 +491,7 @@ int orc_cgemm_ozaki(int64_t m, int64_t n, int64_t k,
                     int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
 {
     return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s, nsamp, si, sj, nthreads,
-                      NULL, NULL, 0, 0, 8);
+                      NULL, NULL, 0, 0, 8, NULL);
 }
 
 int orc_cgemm_ozaki_acc(int64_t m, int64_t n, int64_t k,
@@ -497,7 +501,7 @@ int orc_cgemm_ozaki_acc(int64_t m, int64_t n, int64_t k,
                         int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
 {
     return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s, nsamp, si, sj, nthreads,
-                      Cre0, Cim0, beta, alpha_neg, 8);
+                      Cre0, Cim0, beta, alpha_neg, 8, NULL);
 }
 
 /* the same method with b-bit digits (NEXT-1: b = the paper's binary64 slice width) */
@@ -508,7 +512,25 @@ int orc_cgemm_ozaki_bits(int64_t m, int64_t n, int64_t k,
 {
     if (bits < 2 || bits > 30) return -1;
     return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s, nsamp, si, sj, nthreads,
-                      NULL, NULL, 0, 0, bits);
+                      NULL, NULL, 0, 0, bits, NULL);
+}
+
+/* NEXT-4 (the paper's future work "set the optimal number of divisions",
+ * PAPER.md:360): a per-row triangle.  Digits are computed once with s_max slices (the split
+ * is unchanged); row i uses the TOP srow[i] <= s_max digits of every expansion it touches --
+ * its own row's and every column's of B -- and Algorithm 2's triangle with d = srow[i]
+ * (PAPER.md:173-177), value P 2^(eA_i + eB_j + 6 - 8(srow[i]+1)), one RNE.  The top t digits
+ * of a balanced expansion of X with s_max digits are the balanced digits of
+ * floor((X + H) / 256^(s_max-t)), H = sum_{u < s_max-t} 128 256^u (DESIGN.md NEXT-4). */
+int orc_cgemm_ozaki_rows(int64_t m, int64_t n, int64_t k,
+                         const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                         orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s_max,
+                         const int32_t *srow, int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
+{
+    if (!srow) return -1;
+    for (int64_t i = 0; i < m; i++) if (srow[i] < 1 || srow[i] > s_max) return -1;
+    return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s_max, nsamp, si, sj, nthreads,
+                      NULL, NULL, 0, 0, 8, srow);
 }
 
 /* b = S - ceil((S + ceil(log2 k)) / 2), S = 53: the slice width of Algorithm 2's tau (P:161,
@@ -522,7 +544,8 @@ static int ozaki_core(int64_t m, int64_t n, int64_t k,
                       const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
                       orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s,
                       int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads,
-                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg, int32_t bits)
+                      const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg, int32_t bits,
+                      const int32_t *srow)
 {
     if (m < 0 || n < 0 || k < 0 || (form != 3 && form != 4) || s < 1 || prec_out < 2) return -1;
     int64_t total = nsamp < 0 ? m * n : nsamp;
@@ -550,21 +573,22 @@ static int ozaki_core(int64_t m, int64_t n, int64_t k,
             if (line_digits(Are, Aim, 0, i, k, eA, s, b, nparts, da) ||
                 line_digits(Bre, Bim, 1, j, k, eB, s, b, nparts, db)) { err = -2; continue; }
             const int64_t pl = (int64_t)s * k;
+            const int d = srow ? srow[i] : s;             /* the triangle's d for this row */
             for (int q = 0; q < 3; q++) memset(acc[q], 0, sizeof(uint64_t) * (size_t)na);
             if (form == 4) {
                 /* Eq. 5: Re = ReA ReB - ImA ImB ; Im = ReA ImB + ImA ReB  (each by Alg. 2) */
-                ozaki_pair(da, db, k, s, b, acc[0], na, 0);
-                ozaki_pair(da + pl, db + pl, k, s, b, acc[0], na, 1);
-                ozaki_pair(da, db + pl, k, s, b, acc[1], na, 0);
-                ozaki_pair(da + pl, db, k, s, b, acc[1], na, 0);
+                ozaki_pair(da, db, k, d, b, acc[0], na, 0);
+                ozaki_pair(da + pl, db + pl, k, d, b, acc[0], na, 1);
+                ozaki_pair(da, db + pl, k, d, b, acc[1], na, 0);
+                ozaki_pair(da + pl, db, k, d, b, acc[1], na, 0);
             } else {
                 /* Eq. 6: T1 = ReA ReB, T2 = ImA ImB, T3 = (ReA+ImA)(ReB+ImB) (each by Alg. 2);
                    Re = T1 - T2 ; Im = T3 - T1 - T2 */
-                ozaki_pair(da, db, k, s, b, acc[0], na, 0);                /* T1 */
-                ozaki_pair(da + pl, db + pl, k, s, b, acc[1], na, 0);      /* T2 */
-                ozaki_pair(da + 2 * pl, db + 2 * pl, k, s, b, acc[2], na, 0); /* T3 */
+                ozaki_pair(da, db, k, d, b, acc[0], na, 0);                /* T1 */
+                ozaki_pair(da + pl, db + pl, k, d, b, acc[1], na, 0);      /* T2 */
+                ozaki_pair(da + 2 * pl, db + 2 * pl, k, d, b, acc[2], na, 0); /* T3 */
             }
-            int64_t e0 = eA + eB + 6 - (int64_t)b * (s + 1);
+            int64_t e0 = eA + eB + 6 - (int64_t)b * (d + 1);
             xn re, im;
             if (form == 4) {
                 re = xn_from_acc(acc[0], na, e0);
