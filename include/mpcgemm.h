@@ -84,6 +84,17 @@ typedef struct {
                                  1 = the paper's binary64 slices, b = 53 - ceil((53 +
                                  ceil(log2 k)) / 2) bits, on FP64 DMMA (SURVEY
                                  NEXT-1; beta / alpha_neg not supported there)                  */
+    int32_t  adaptive;        /* NEXT-4 ("set the optimal number of divisions"):
+                                 1 = a certified slice count per block of 256 rows of A / C.
+                                 Block b gets s_b = the slice rule applied to the pre-pass over
+                                 its rows (against all of B); the digits are split once with
+                                 s = max_b s_b and block b uses the TOP s_b digits of every
+                                 expansion with Algorithm 2's triangle d = s_b, value
+                                 P 2^(eA_i + eB_j + 6 - 8(s_b+1)).  Same error bound per block;
+                                 bit-identical to oracle orc_cgemm_ozaki_rows.  Ignored when
+                                 slices > 0; INT8 carrier only.  0 = one s for all rows.        */
+    int32_t *block_slices;    /* optional HOST output, ceil(m/256) entries: the s used by each
+                                 256-row block (all equal to s unless adaptive)               */
 } mpcgemm_opts;
 
 typedef struct {
@@ -97,6 +108,7 @@ typedef struct {
     int32_t slice_bits;       /* digit width b: 8 (INT8 carrier) or the binary64 slice width   */
     int32_t slicegemm_ctas;   /* grid of the slice-GEMM launch                                 */
     float   ms_linemax, ms_prepass, ms_split, ms_gemm, ms_fold;   /* opts->timing only         */
+    int32_t slices_min;       /* smallest per-block s (== slices unless opts->adaptive)        */
 } mpcgemm_report;
 
 /* C := A B (auto slice count).  Device pointers.  m, n, k >= 0 (empty: nothing written for

@@ -58,6 +58,9 @@ def lib():
             L.orc_cgemm_ozaki_acc.restype = ctypes.c_int
             L.orc_cgemm_ozaki_rows.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, vp, i64, vp, vp, i32]
             L.orc_cgemm_ozaki_rows.restype = ctypes.c_int
+            L.orc_cgemm_ozaki_acc_rows.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, P, P, i32, i32, i32, vp,
+                                                   i64, vp, vp, i32]
+            L.orc_cgemm_ozaki_acc_rows.restype = ctypes.c_int
             L.orc_cgemm_ozaki_bits.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, i32, i64, vp, vp, i32]
             L.orc_cgemm_ozaki_bits.restype = ctypes.c_int
             L.orc_split_bits.argtypes = [ctypes.c_int, i64, i64, P, P, i32, i32, i32, vp]
@@ -154,8 +157,9 @@ def block_slices(A: CMat, B: CMat, prec: int, method, block: int = 256, nthreads
 
 
 def ozaki_acc(A: CMat, B: CMat, C0: CMat, prec_out: int, method="3M", s: int | None = None, beta: int = 1,
-              alpha_neg: int = 0, samples=None, nthreads: int = 0) -> CMat:
-    """C = beta C0 + (-1)^alpha_neg (Algorithm-2 product), exact sum, one RNE (NEXT-2)."""
+              alpha_neg: int = 0, samples=None, nthreads: int = 0, srow=None) -> CMat:
+    """C = beta C0 + (-1)^alpha_neg (Algorithm-2 product), exact sum, one RNE (NEXT-2).
+    srow: NEXT-4 per-row triangle over the top srow[i] digits of s-digit expansions."""
     if s is None:
         s, _ = auto_slices(A, B, A.prec, method)
     m, k = A.shape
@@ -172,10 +176,17 @@ def ozaki_acc(A: CMat, B: CMat, C0: CMat, prec_out: int, method="3M", s: int | N
     a = [_rm(A.re), _rm(A.im), _rm(B.re), _rm(B.im)]
     c0 = [_rm(C0.re), _rm(C0.im)]
     out = [_rm(Cre), _rm(Cim)]
-    rc = lib().orc_cgemm_ozaki_acc(m, n, k, *[_ptr(x) for x in a], *[_ptr(x) for x in c0], beta, alpha_neg,
-                                   *[_ptr(x) for x in out], prec_out, _form(method), s, ns,
-                                   si.ctypes.data if si is not None else None,
-                                   sj.ctypes.data if sj is not None else None, nthreads)
+    sp = si.ctypes.data if si is not None else None
+    sq = sj.ctypes.data if sj is not None else None
+    if srow is None:
+        rc = lib().orc_cgemm_ozaki_acc(m, n, k, *[_ptr(x) for x in a], *[_ptr(x) for x in c0], beta, alpha_neg,
+                                       *[_ptr(x) for x in out], prec_out, _form(method), s, ns, sp, sq, nthreads)
+    else:
+        srow = np.ascontiguousarray(np.asarray(srow, dtype=np.int32))
+        assert srow.shape == (m,)
+        rc = lib().orc_cgemm_ozaki_acc_rows(m, n, k, *[_ptr(x) for x in a], *[_ptr(x) for x in c0], beta,
+                                            alpha_neg, *[_ptr(x) for x in out], prec_out, _form(method), s,
+                                            srow.ctypes.data, ns, sp, sq, nthreads)
     if rc:
         raise RuntimeError(f"oracle returned {rc}")
     C = CMat(Cre, Cim)

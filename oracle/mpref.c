@@ -533,6 +533,19 @@ int orc_cgemm_ozaki_rows(int64_t m, int64_t n, int64_t k,
                       NULL, NULL, 0, 0, 8, srow);
 }
 
+/* NEXT-2 + NEXT-4: C := beta C0 +- (per-row-triangle product), one RNE */
+int orc_cgemm_ozaki_acc_rows(int64_t m, int64_t n, int64_t k,
+                             const orc_rmat *Are, const orc_rmat *Aim, const orc_rmat *Bre, const orc_rmat *Bim,
+                             const orc_rmat *Cre0, const orc_rmat *Cim0, int32_t beta, int32_t alpha_neg,
+                             orc_rmat *Cre, orc_rmat *Cim, int32_t prec_out, int32_t form, int32_t s_max,
+                             const int32_t *srow, int64_t nsamp, const int64_t *si, const int64_t *sj, int32_t nthreads)
+{
+    if (!srow) return -1;
+    for (int64_t i = 0; i < m; i++) if (srow[i] < 1 || srow[i] > s_max) return -1;
+    return ozaki_core(m, n, k, Are, Aim, Bre, Bim, Cre, Cim, prec_out, form, s_max, nsamp, si, sj, nthreads,
+                      Cre0, Cim0, beta, alpha_neg, 8, srow);
+}
+
 /* b = S - ceil((S + ceil(log2 k)) / 2), S = 53: the slice width of Algorithm 2's tau (P:161,
  * reading Z2: ceil(log2 l)); every k-term sum of two b-bit balanced digits is exact in binary64 */
 int32_t orc_fp64_slice_bits(int64_t k) {

@@ -14,6 +14,10 @@ constexpr int kMaxPairs = 2;         // operand pairs concatenated into one job 
 // in k-blocks of 128: 1023 blocks = 130944 products.
 constexpr int kMaxKBlocksPerChunk = 1023;
 constexpr int kBK = 128;             // k-block: 128 int8 = one 128-byte swizzle row
+// NEXT-4 (per-block slice counts): the pre-pass reduces, and the adaptive mode chooses s, per
+// block of 256 rows of A / C (the CTA-pair tile height)
+constexpr int kSBlkShift = 8;
+constexpr int kSBlk = 1 << kSBlkShift;
 
 // Device view of one real MP matrix in the ABI format (include/mpcgemm.h).
 struct DMat {

@@ -31,7 +31,8 @@ cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, i
 cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
                                   const int64_t *eline, int8_t *t, int32_t *rel, cudaStream_t st);
 
-// a-2: stage 1 (out[0] = min T over nonzero line pairs) and stage 2 (minT_sup, minT1, maxD2)
+// a-2: stage 1 (out_min = min T over nonzero line pairs) and stage 2 (out_min, out_min1,
+// out_max2), each an array over the 256-row blocks of A (kSBlk)
 cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t nstrips,
                                   int64_t m, int64_t n, int64_t k, int64_t kp,
                                   const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA, const int32_t *relB,
@@ -48,6 +49,7 @@ struct FoldParams {
     DMatOut Cre, Cim;
     int32_t beta, alpha_neg;     // NEXT-2: C = beta C0 + (-1)^alpha_neg A B (one rounding)
     DMat C0re, C0im;             // may alias Cre / Cim
+    const int32_t *sblk;         // NEXT-4: slice count of each 256-row block (<= s), or nullptr
     uint64_t *fix;               // fixed-point scratch, fold_scratch_words(m, ldF, s, L, beta) words
     int64_t ldF;                 // scratch row pitch (even, >= n)
 };

@@ -79,9 +79,10 @@ StageEvents *stage_events(int dev) {
 // ---------------------------------------------------------------- plans (work lists)
 struct PlanKey {
     int64_t m, n, k; int s, method, BM, BN, grid, simt, maxkb, g2, order;
+    std::vector<int32_t> sblk;   // NEXT-4: per-256-row-block slice counts (empty: s everywhere)
     bool operator<(const PlanKey &o) const {
-        return std::tie(m, n, k, s, method, BM, BN, grid, simt, maxkb, g2, order) <
-               std::tie(o.m, o.n, o.k, o.s, o.method, o.BM, o.BN, o.grid, o.simt, o.maxkb, o.g2, o.order);
+        return std::tie(m, n, k, s, method, BM, BN, grid, simt, maxkb, g2, order, sblk) <
+               std::tie(o.m, o.n, o.k, o.s, o.method, o.BM, o.BN, o.grid, o.simt, o.maxkb, o.g2, o.order, o.sblk);
     }
 };
 struct Plan {
@@ -169,6 +170,11 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
         }
     auto base = [&](int q, int r) { return slotinfo[(q * (s + 2) + r) * 2]; };
     std::vector<WorkUnit> units;
+    // NEXT-4: a row tile of block b takes the segments whose first diagonal r <= sblk[b] + 1
+    // (a pair (r, r+1) with r = sblk[b] + 1 also computes D_{r+1}, which the fold skips)
+    auto in_tri = [&](int64_t tm, int r) {
+        return key.sblk.empty() || r <= key.sblk[(size_t)((tm * key.BM) >> kSBlkShift)] + 1;
+    };
     for (const Segment &sg : segs) {
         const int q = sg.q, r = sg.r;
         const int64_t np = P.jobs[q].npairs;
@@ -177,6 +183,7 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
                 const int32_t a = (int32_t)(c * KB / sg.nch), b = (int32_t)((c + 1) * KB / sg.nch);
                 for (int64_t tm = 0; tm < tiles_m; tm++)
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
+                        if (!in_tri(tm, r)) continue;
                         units.push_back({q | (2 << 8), (int32_t)tm, (int32_t)tn, r, a, b,
                                          base(q, r) + (int32_t)c, base(q, r + 1) + (int32_t)c});
                         P.mma += np * (b - a) * (2 * r - 1) * (kBK / 32);
@@ -188,6 +195,7 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
                 const int32_t a = (int32_t)(c * G / sg.nch), b = (int32_t)((c + 1) * G / sg.nch);
                 for (int64_t tm = 0; tm < tiles_m; tm++)
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
+                        if (!in_tri(tm, r)) continue;
                         units.push_back({q | (1 << 8), (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
                         P.mma += (int64_t)(b - a) * (kBK / 32);
                     }
@@ -277,6 +285,40 @@ int check_args(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A,
 DMat dm(const mpc_rmat &M) { return DMat{M.sign, M.exp, M.limbs, M.ld}; }
 DMatOut dmo(const mpc_rmat &M) { return DMatOut{M.sign, M.exp, M.limbs, M.ld}; }
 
+int64_t nblocks(int64_t m) { return (m + kSBlk - 1) / kSBlk; }
+
+// the small per-call metadata area: eA[m], eB[n], nzA[m], nzB[n], then the flags region:
+// validate error flag, the pre-pass results per 256-row block, the per-block slice counts
+struct MetaView {
+    int64_t *eA, *eB;
+    uint8_t *nzA, *nzB;
+    uint32_t *errflag;
+    unsigned long long *omin, *omin1;
+    long long *omax2;
+    int32_t *sblk;
+};
+size_t meta_flags_off(int64_t m, int64_t n) { return align_up(8 * (m + n) + (m + n) + 64, 256); }
+size_t meta_bytes(int64_t m, int64_t n) { return meta_flags_off(m, n) + align_up(64 + 28 * (size_t)nblocks(m) + 64, 256); }
+MetaView meta_view(uint8_t *meta, int64_t m, int64_t n) {
+    MetaView v;
+    v.eA = (int64_t *)meta; v.eB = v.eA + m;
+    v.nzA = (uint8_t *)(v.eB + n); v.nzB = v.nzA + m;
+    uint8_t *flags = meta + meta_flags_off(m, n);
+    v.errflag = (uint32_t *)flags;
+    v.omin = (unsigned long long *)(flags + 64);
+    v.omin1 = v.omin + nblocks(m);
+    v.omax2 = (long long *)(v.omin1 + nblocks(m));
+    v.sblk = (int32_t *)(v.omax2 + nblocks(m));
+    return v;
+}
+
+// per-block pre-pass integers (minT, minT1, maxD2) of the 256-row blocks of A, and the global
+// reduction (the rule's input for one common s)
+struct Bounds {
+    std::vector<int64_t> minT, minT1, maxD2;
+    int64_t g[3] = {-1, -1, -1};
+};
+
 // workspace layout of one call
 struct Layout {
     size_t meta;      // eA, eB, nz, flags, prepass outputs
@@ -329,7 +371,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb,
     Layout Lo;
     Lo.kp = align_up((size_t)std::max<int64_t>(k, 1), 16);
     Lo.nstrips = (std::max<int64_t>(n, 1) + kStrip - 1) / kStrip;
-    Lo.meta = align_up(8 * (m + n) + (m + n) + 64, 256) + 256;
+    Lo.meta = meta_bytes(m, n);
     const int64_t KB = (k + kBK - 1) / kBK;
     const int64_t nslotsT = (KB + exact_cap() - 1) / exact_cap();
     Lo.pre = align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256) +
@@ -345,24 +387,22 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb,
     return Lo;
 }
 
-// prepass on device pointers; fills out[3] (synchronizes the stream)
+// prepass on device pointers (synchronizes the stream).  Stage 1 gives each block's minT; if
+// any block has minT == 0 (or full), stage 2 gives every block's (minT1, maxD2).  Blocks
+// without a nonzero line pair keep -1.  B->g is the reduction over blocks (the global pre-pass).
 int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
-                int full, cudaStream_t st, uint8_t *meta, uint8_t *pre, const Layout &Lo, int simt, int64_t out[3]) {
+                int full, cudaStream_t st, uint8_t *meta, uint8_t *pre, const Layout &Lo, int simt, Bounds *out) {
     const int L = (prec + 63) / 64;
-    int64_t *eA = (int64_t *)meta, *eB = eA + m;
-    uint8_t *nzA = (uint8_t *)(eB + n), *nzB = nzA + m;
-    uint8_t *flags = meta + align_up(8 * (m + n) + (m + n) + 64, 256);
-    unsigned long long *omin = (unsigned long long *)flags;
-    unsigned long long *omin1 = omin + 1;
-    long long *omax2 = (long long *)(omin + 2);
+    const MetaView mv = meta_view(meta, m, n);
+    const int64_t nb = nblocks(m);
     int8_t *tA = (int8_t *)pre, *tB = tA + m * Lo.kp;
     int32_t *relA = (int32_t *)(pre + align_up((size_t)(m + n) * Lo.kp, 256)), *relB = relA + m * Lo.kp;
     int32_t *T = (int32_t *)(pre + align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256));
-    CK(prepass_planes_launch(dm(A->re), dm(A->im), 0, m, k, Lo.kp, L, eA, tA, relA, st));
-    CK(prepass_planes_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, tB, relB, st));
+    CK(prepass_planes_launch(dm(A->re), dm(A->im), 0, m, k, Lo.kp, L, mv.eA, tA, relA, st));
+    CK(prepass_planes_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, mv.eB, tB, relB, st));
     const int BN = tile_bn(n);
     const int grid = sm_count(dev);
-    PlanKey key{m, n, k, 1, 0, 128, BN, grid, simt, (int)kMaxKBlocksPerChunk, 0, 0};
+    PlanKey key{m, n, k, 1, 0, 128, BN, grid, simt, (int)kMaxKBlocksPerChunk, 0, 0, {}};
     Plan *plan;
     if (int rc = build_plan(dev, key, &plan)) return rc;
     SliceGemmLaunch SL;
@@ -375,27 +415,42 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     SL.digA = tA; SL.digB = tB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
     SL.grid = plan->grid; SL.BM = 128; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits; SL.units_flat = plan->d_units;
     CK(slicegemm_launch(SL, st));
-    unsigned long long init[3] = {~0ull, ~0ull, (unsigned long long)-1ll};
-    CK(cudaMemcpyAsync(omin, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, nzA, nzB, relA, relB, 1,
-                             omin, omin1, omax2, st));
-    unsigned long long h[3];
-    CK(cudaMemcpyAsync(h, omin, sizeof(h), cudaMemcpyDeviceToHost, st));
+    std::vector<unsigned long long> init(3 * nb), h(3 * nb);
+    for (int64_t b = 0; b < nb; b++) { init[b] = ~0ull; init[nb + b] = ~0ull; init[2 * nb + b] = (unsigned long long)-1ll; }
+    CK(cudaMemcpyAsync(mv.omin, init.data(), 8 * 3 * nb, cudaMemcpyHostToDevice, st));
+    CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 1,
+                             mv.omin, mv.omin1, mv.omax2, st));
+    CK(cudaMemcpyAsync(h.data(), mv.omin, 8 * nb, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const int64_t minraw = h[0] == ~0ull ? -1 : (int64_t)h[0];
-    if (minraw > 0 && !full) { out[0] = minraw; out[1] = minraw; out[2] = -1; return 0; }
-    if (minraw < 0) { out[0] = -1; out[1] = -1; out[2] = -1; return 0; }
-    CK(cudaMemcpyAsync(omin, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, nzA, nzB, relA, relB, 2,
-                             omin, omin1, omax2, st));
-    CK(cudaMemcpyAsync(h, omin, sizeof(h), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    const int64_t mn = h[0] == ~0ull ? -1 : (int64_t)h[0];
-    const int64_t mn1 = h[1] == ~0ull ? -1 : (int64_t)h[1];
-    const int64_t mx2 = (int64_t)h[2];
-    if (full) { out[0] = mn; out[1] = mn1; out[2] = mx2; }
-    else if (mn != 0) { out[0] = mn; out[1] = mn; out[2] = -1; }
-    else { out[0] = mn; out[1] = mn1; out[2] = mx2; }
+    out->minT.assign(nb, -1); out->minT1.assign(nb, -1); out->maxD2.assign(nb, -1);
+    bool any0 = false;
+    for (int64_t b = 0; b < nb; b++) {
+        out->minT[b] = h[b] == ~0ull ? -1 : (int64_t)h[b];
+        out->minT1[b] = out->minT[b];
+        any0 = any0 || out->minT[b] == 0;
+    }
+    if (any0 || full) {
+        CK(cudaMemcpyAsync(mv.omin, init.data(), 8 * 3 * nb, cudaMemcpyHostToDevice, st));
+        CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 2,
+                                 mv.omin, mv.omin1, mv.omax2, st));
+        CK(cudaMemcpyAsync(h.data(), mv.omin, 8 * 3 * nb, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t b = 0; b < nb; b++) {
+            out->minT[b] = h[b] == ~0ull ? -1 : (int64_t)h[b];
+            out->minT1[b] = h[nb + b] == ~0ull ? -1 : (int64_t)h[nb + b];
+            out->maxD2[b] = (int64_t)h[2 * nb + b];
+        }
+    }
+    // global: MIN minT; if it is 0 (or full) MIN minT1 and MAX maxD2, else (minT, minT, -1)
+    int64_t g0 = -1, g1 = -1, g2 = -1;
+    for (int64_t b = 0; b < nb; b++) {
+        if (out->minT[b] >= 0 && (g0 < 0 || out->minT[b] < g0)) g0 = out->minT[b];
+        if (out->minT1[b] >= 0 && (g1 < 0 || out->minT1[b] < g1)) g1 = out->minT1[b];
+        if (out->maxD2[b] > g2) g2 = out->maxD2[b];
+    }
+    if (g0 < 0) { out->g[0] = out->g[1] = out->g[2] = -1; }
+    else if (g0 > 0 && !full) { out->g[0] = g0; out->g[1] = g0; out->g[2] = -1; }
+    else { out->g[0] = g0; out->g[1] = g1; out->g[2] = g2; }
     return 0;
 }
 
@@ -491,9 +546,11 @@ size_t f64_main_bytes(int64_t m, int64_t n, int64_t k, int s, int method) {
 // the device hot path with a known workspace
 int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
              mpc_cmat *C, int method, int s, cudaStream_t st, uint8_t *meta, uint8_t *big, const Layout &Lo,
-             int simt, mpcgemm_report *rep, StageEvents *E, int beta, int alpha_neg) {
+             int simt, mpcgemm_report *rep, StageEvents *E, int beta, int alpha_neg,
+             const std::vector<int32_t> &sblk) {
     const int L = (prec + 63) / 64;
-    int64_t *eA = (int64_t *)meta, *eB = eA + m;
+    const MetaView mv = meta_view(meta, m, n);
+    int64_t *eA = mv.eA, *eB = mv.eB;
     const int parts = method == 3 ? 3 : 2;
     int8_t *digA = (int8_t *)big;
     int8_t *digB = digA + align_up((size_t)parts * s * m * Lo.kp, 256);
@@ -504,7 +561,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     const Geometry geo = main_geometry(dev, m, n, k, s, method);
     const int BN = geo.BN;
     PlanKey key{m, n, k, s, method, geo.BM, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0,
-                env_int("MPCGEMM_ORDER", 1)};
+                env_int("MPCGEMM_ORDER", 1), sblk};
     Plan *plan;
     if (int rc = build_plan(dev, key, &plan)) return rc;
     SliceGemmLaunch SL;
@@ -525,6 +582,11 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     F.eA = eA; F.eB = eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
     F.beta = beta; F.alpha_neg = alpha_neg; F.C0re = dm(C->re); F.C0im = dm(C->im);
     F.ldF = (n + 1) & ~1ll;
+    F.sblk = nullptr;
+    if (!sblk.empty()) {                               // NEXT-4: per-block triangles
+        CK(cudaMemcpyAsync(mv.sblk, sblk.data(), 4 * sblk.size(), cudaMemcpyHostToDevice, st));
+        F.sblk = mv.sblk;
+    }
     F.fix = (uint64_t *)((uint8_t *)partials +
                          align_up((size_t)plan->nslots * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
     CK(fold_normalize_launch(F, st));
@@ -546,7 +608,9 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     const int beta = opts ? (opts->beta != 0) : 0;
     const int alpha_neg = opts ? (opts->alpha_neg != 0) : 0;
     const int carrier = opts ? opts->carrier : 0;
+    const int adaptive = opts ? (opts->adaptive != 0) : 0;
     const int simt = env_int("MPCGEMM_SLICEGEMM_SIMT", 0);
+    if (adaptive && carrier == 1) return fail(MPCGEMM_ERR_ARG, "adaptive slices need the INT8 carrier");
     if (carrier != 0 && carrier != 1) return fail(MPCGEMM_ERR_ARG, "carrier must be 0 (INT8) or 1 (FP64)");
     if (carrier == 1 && (beta || alpha_neg)) return fail(MPCGEMM_ERR_ARG, "beta / alpha_neg need the INT8 carrier");
     const int bits = carrier == 1 ? fp64_slice_bits(k) : 8;
@@ -567,9 +631,10 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     Layout Lo = layout_for(m, n, k, 0, method, kMaxKBlocksPerChunk);
     if (int rc = grow(&dc.meta, &dc.meta_bytes, Lo.meta)) return rc;
     uint8_t *meta = (uint8_t *)dc.meta;
-    int64_t *eA = (int64_t *)meta, *eB = eA + m;
-    uint8_t *nzA = (uint8_t *)(eB + n), *nzB = nzA + m;
-    uint32_t *errflag = (uint32_t *)(meta + align_up(8 * (m + n) + (m + n) + 64, 256) + 64);
+    const MetaView mv = meta_view(meta, m, n);
+    int64_t *eA = mv.eA, *eB = mv.eB;
+    uint8_t *nzA = mv.nzA, *nzB = mv.nzB;
+    uint32_t *errflag = mv.errflag;
     if (validate) CK(cudaMemsetAsync(errflag, 0, 4, st));
     CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, eA, nzA, errflag, validate, st));
     CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, eB, nzB, errflag, validate, st));
@@ -585,13 +650,31 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     int s = forced;
     int64_t pb[3] = {-1, -1, -1};
     double log2rho = 0.0;
+    std::vector<int32_t> sblk;                         // NEXT-4 per-block slice counts
     if (!s) {
         if (int rc = grow(&dc.ws, &dc.ws_bytes, Lo.pre)) return rc;
-        if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, pb)) return rc;
+        Bounds bd;
+        if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, &bd)) return rc;
+        for (int q = 0; q < 3; q++) pb[q] = bd.g[q];
         launches += 4 + (pb[0] == 0 ? 1 : 0);         // planes x2, T GEMM, min [, max-plus]
         log2rho = rule_log2rho(k, pb[0], pb[1], pb[2]);
         s = rule_slices(prec, method, log2rho, bits);
         if (s < 0) return fail(MPCGEMM_ERR_SLICES, "slice rule needs s > 1024");
+        if (adaptive) {
+            // each 256-row block's own certified s (its rows against all of B); s = the max
+            int smin = s;
+            sblk.resize(bd.minT.size());
+            for (size_t b = 0; b < sblk.size(); b++) {
+                const int sb = rule_slices(prec, method, rule_log2rho(k, bd.minT[b], bd.minT1[b], bd.maxD2[b]), 8);
+                if (sb < 0) return fail(MPCGEMM_ERR_SLICES, "slice rule needs s > 1024");
+                sblk[b] = sb;
+                smin = std::min(smin, sb);
+            }
+            if (smin == s) sblk.clear();               // uniform: the plain path, bit-identical
+        }
+    }
+    if (opts && opts->block_slices) {
+        for (int64_t b = 0; b < nblocks(m); b++) opts->block_slices[b] = sblk.empty() ? s : sblk[(size_t)b];
     }
     if (carrier == 1) {
         uint8_t *big;
@@ -623,11 +706,13 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     }
     if (E) CK(cudaEventRecord(E->ev[2], st));
     if (rep) rep->kernel_launches = launches;
-    if (int rc = run_main(dev, m, n, k, prec, A, B, C, method, s, st, meta, big, Lm, simt, rep, E, beta, alpha_neg))
+    if (int rc = run_main(dev, m, n, k, prec, A, B, C, method, s, st, meta, big, Lm, simt, rep, E, beta, alpha_neg,
+                          sblk))
         return rc;
     if (rep) {
         rep->slices = s; rep->slice_bits = 8; rep->certified = 1; rep->minT = pb[0]; rep->minT1 = pb[1];
         rep->maxD2 = pb[2]; rep->log2_rho_hat = log2rho;
+        rep->slices_min = sblk.empty() ? s : *std::min_element(sblk.begin(), sblk.end());
     }
     if (E) {
         CK(cudaEventSynchronize(E->ev[5]));
@@ -671,12 +756,15 @@ int mpcgemm_rho_bounds(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_
     if (int rc = grow(&dc.meta, &dc.meta_bytes, Lo.meta)) return rc;
     if (int rc = grow(&dc.ws, &dc.ws_bytes, Lo.pre)) return rc;
     uint8_t *meta = (uint8_t *)dc.meta;
-    int64_t *eA = (int64_t *)meta, *eB = eA + m;
-    uint8_t *nzA = (uint8_t *)(eB + n), *nzB = nzA + m;
-    CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, eA, nzA, nullptr, 0, st));
-    CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, eB, nzB, nullptr, 0, st));
-    return run_prepass(dev, m, n, k, prec, A, B, full, st, meta, (uint8_t *)dc.ws, Lo,
-                       env_int("MPCGEMM_SLICEGEMM_SIMT", 0), out);
+    const MetaView mv = meta_view(meta, m, n);
+    CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, mv.eA, mv.nzA, nullptr, 0, st));
+    CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, mv.eB, mv.nzB, nullptr, 0, st));
+    Bounds bd;
+    if (int rc = run_prepass(dev, m, n, k, prec, A, B, full, st, meta, (uint8_t *)dc.ws, Lo,
+                             env_int("MPCGEMM_SLICEGEMM_SIMT", 0), &bd))
+        return rc;
+    for (int q = 0; q < 3; q++) out[q] = bd.g[q];
+    return 0;
 }
 
 int mpcgemm_slices_for(int32_t prec, mpcgemm_method method, int64_t k, int64_t minT, int64_t minT1, int64_t maxD2) {

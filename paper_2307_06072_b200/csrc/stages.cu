@@ -303,24 +303,35 @@ MPC_DEV int64_t sum_T(const int32_t *T, int nslots, int64_t nstrips, int64_t i, 
     return v;
 }
 
-// stage 1: min over nonzero line pairs of T_ij
+// stage 1: min over nonzero line pairs of T_ij, per 256-row block (out_min[i >> 8]; the
+// global value is the min over blocks, NEXT-4 uses each block's own)
 __global__ void prepass_min_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
                                    const uint8_t *nzA, const uint8_t *nzB, unsigned long long *out_min)
 {
-    unsigned long long best = ULLONG_MAX;
     const int64_t total = m * n;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = t / n, j = t - i * n;
-        if (!nzA[i] || !nzB[j]) continue;
-        const unsigned long long v = (unsigned long long)sum_T(T, nslots, nstrips, i, j);
-        best = v < best ? v : best;
-    }
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    // every warp iteration covers 32 consecutive (i, j); reduce per warp when they share a block
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < total; t0 += step) {
+        const int64_t t = t0 + (threadIdx.x & 31);
+        unsigned long long v = ULLONG_MAX;
+        int64_t blk = -1;
+        if (t < total) {
+            const int64_t i = t / n, j = t - i * n;
+            blk = i >> kSBlkShift;
+            if (nzA[i] && nzB[j]) v = (unsigned long long)sum_T(T, nslots, nstrips, i, j);
+        }
+        const int64_t b0 = __shfl_sync(0xffffffffu, blk, 0);
+        if (__all_sync(0xffffffffu, blk == b0 || blk < 0)) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
-        best = y < best ? y : best;
+            for (int o = 16; o; o >>= 1) {
+                unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+                v = y < v ? y : v;
+            }
+            if ((threadIdx.x & 31) == 0 && v != ULLONG_MAX) atomicMin(out_min + b0, v);
+        } else if (v != ULLONG_MAX) {
+            atomicMin(out_min + blk, v);
+        }
     }
-    if ((threadIdx.x & 31) == 0 && best != ULLONG_MAX) atomicMin(out_min, best);
 }
 
 // stage 2: exact max-plus exponent bound and the per-pair bound choice
@@ -371,10 +382,11 @@ prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m,
         y = __shfl_xor_sync(0xffffffffu, lmin1, o); lmin1 = y < lmin1 ? y : lmin1;
         long long z = __shfl_xor_sync(0xffffffffu, lmax2, o); lmax2 = z > lmax2 ? z : lmax2;
     }
-    if (tx == 0) {
-        if (lmin != ULLONG_MAX) atomicMin(out_min, lmin);
-        if (lmin1 != ULLONG_MAX) atomicMin(out_min1, lmin1);
-        if (lmax2 >= 0) atomicMax(out_max2, lmax2);
+    if (tx == 0) {                                    // a 32-row tile lies in one 256-row block
+        const int64_t b = i0 >> kSBlkShift;
+        if (lmin != ULLONG_MAX) atomicMin(out_min + b, lmin);
+        if (lmin1 != ULLONG_MAX) atomicMin(out_min1 + b, lmin1);
+        if (lmax2 >= 0) atomicMax(out_max2 + b, lmax2);
     }
 }
 
@@ -621,12 +633,16 @@ fold_normalize_kernel(const FoldParams F)
     const int64_t i = (int64_t)(blockIdx.y / nsub) * kRowBlk + blockIdx.x;
     const int64_t j0 = (int64_t)(blockIdx.y % nsub) * COLS;      // COLS divides the 256-column strip
     if (i >= F.m) return;
+    // NEXT-4: this row's triangle d = sr <= s; its diagonals r = sr+1 .. 2 are the slots from
+    // the first slot of (job 0, r = sr+1) on (slots of larger r are not read)
+    const int sr = F.sblk ? F.sblk[i >> kSBlkShift] : s;
+    const int sl0 = sr == s ? 0 : F.slotinfo[(sr + 1) * 2];
     if (warp == NCONS / 32) {
         // ---------------- producer warp
         if (lane == 0) {
             const int32_t *region = F.partials + part_off(i, j0, 0, F.nslots, F.nstrips);   // slot 0
             int e = 0; uint32_t ph = 0;
-            for (int sl = 0; sl < nslots; sl += kFoldPer) {
+            for (int sl = sl0; sl < nslots; sl += kFoldPer) {
                 const int cnt = nslots - sl < kFoldPer ? nslots - sl : kFoldPer;
                 mbar_wait(&empty[e], ph ^ 1);
                 mbar_arrive_expect_tx(&full[e], (uint32_t)(cnt * COLS * 4));
@@ -649,7 +665,7 @@ fold_normalize_kernel(const FoldParams F)
     int e = 0, fill = 0; uint32_t ph = 0;
     int b = 0;                                        // byte index = s + 1 - r
     const bool live = jj < F.n;                       // (jj + 1 < n too: ldF is even and n is padded)
-    for (int sl = 0; sl < nslots; sl++) {
+    for (int sl = sl0; sl < nslots; sl++) {
         if (fill == 0) mbar_wait(&full[e], ph);
         const int sc = sched[sl];
         const int2 v = *reinterpret_cast<const int2 *>(ring + (e * kFoldPer + fill) * COLS + col);
@@ -687,8 +703,8 @@ fold_normalize_kernel(const FoldParams F)
         }
     }
     if (!live) return;
-    // the final carries at bit 8s, sign-extended to Lc0 limbs
-    const int l0 = s >> 3, o = 8 * (s & 7);
+    // the final carries at bit 8 sr, sign-extended to Lc0 limbs
+    const int l0 = sr >> 3, o = 8 * (sr & 7);
 #pragma unroll
     for (int p = 0; p < 2; p++) {
         uint64_t w[2][2];
@@ -711,7 +727,7 @@ fold_normalize_kernel(const FoldParams F)
         if (j >= F.n) break;
         uint64_t *f0 = fixg + x, *f1 = fixg + x + (int64_t)(Lc0 + Lw) * lstride;   // parts: [0, Lc0+Lw), [Lc0+Lw, ..)
         if (BETA) f1 = fixg + x + (int64_t)Lc0 * lstride;
-        const int64_t e0 = F.eA[i] + F.eB[j] + 6 - 8 * (int64_t)(s + 1);
+        const int64_t e0 = F.eA[i] + F.eB[j] + 6 - 8 * (int64_t)(sr + 1);
         const int64_t oi = i * F.Cre.ld + j;
         const int64_t oj = i * F.Cim.ld + j;
         if (BETA) {

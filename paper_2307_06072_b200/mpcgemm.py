@@ -44,7 +44,8 @@ class OptsC(ctypes.Structure):
     _fields_ = [("stream", ctypes.c_void_p), ("slices", ctypes.c_int32), ("validate", ctypes.c_int32),
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("timing", ctypes.c_int32), ("beta", ctypes.c_int32), ("alpha_neg", ctypes.c_int32),
-                ("carrier", ctypes.c_int32)]
+                ("carrier", ctypes.c_int32), ("adaptive", ctypes.c_int32),
+                ("block_slices", ctypes.c_void_p)]
 
 
 class ReportC(ctypes.Structure):
@@ -53,7 +54,7 @@ class ReportC(ctypes.Structure):
                 ("mma_instructions", ctypes.c_int64), ("work_units", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int32), ("slice_bits", ctypes.c_int32), ("slicegemm_ctas", ctypes.c_int32),
                 ("ms_linemax", ctypes.c_float), ("ms_prepass", ctypes.c_float), ("ms_split", ctypes.c_float),
-                ("ms_gemm", ctypes.c_float), ("ms_fold", ctypes.c_float)]
+                ("ms_gemm", ctypes.c_float), ("ms_fold", ctypes.c_float), ("slices_min", ctypes.c_int32)]
 
 
 def lib():
@@ -183,30 +184,34 @@ def _stream_ptr(stream):
 # ------------------------------------------------------------------ the calls (names = ABI)
 def mpcgemm_ex(A: DevCMat, B: DevCMat, C: DevCMat, prec: int, method="3M", slices: int = 0,
                validate: int = 0, stream=None, workspace=None, timing: int = 0, beta: int = 0,
-               alpha_neg: int = 0, carrier: int = 0) -> dict:
-    """C := beta C + (-1)^alpha_neg A B on the device (stream-ordered).  Returns the report."""
+               alpha_neg: int = 0, carrier: int = 0, adaptive: int = 0) -> dict:
+    """C := beta C + (-1)^alpha_neg A B on the device (stream-ordered).  Returns the report
+    (plus "block_slices": the s of each 256-row block)."""
     m, k = A.shape
     k2, n = B.shape
     if k != k2 or C.shape != (m, n):
         raise MpcgemmError(-1, f"shape mismatch A {A.shape} B {B.shape} C {C.shape}")
+    nblk = max(1, (m + 255) // 256)
+    bs = (ctypes.c_int32 * nblk)()
     opts = OptsC(_stream_ptr(stream), slices, validate,
                  workspace.data_ptr() if workspace is not None else None,
                  workspace.numel() * workspace.element_size() if workspace is not None else 0, timing, beta,
-                 alpha_neg, carrier)
+                 alpha_neg, carrier, adaptive, ctypes.cast(bs, ctypes.c_void_p))
     rep = ReportC()
     a, b, c = A.c(), B.c(), C.c()
     rc = lib().mpcgemm_ex(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), METHODS[method],
                           ctypes.byref(opts), ctypes.byref(rep))
     _check(rc)
-    return {f: getattr(rep, f) for f, _ in ReportC._fields_} | {"status": rc}
+    return {f: getattr(rep, f) for f, _ in ReportC._fields_} | {"status": rc,
+                                                                "block_slices": list(bs)[: (m + 255) // 256]}
 
 
 def gemm(A: DevCMat, B: DevCMat, prec: int | None = None, method="3M", slices: int = 0, stream=None,
-         carrier: int = 0):
+         carrier: int = 0, adaptive: int = 0):
     """Allocating convenience wrapper: returns (C, report)."""
     prec = A.prec if prec is None else prec
     C = empty_device(A.shape[0], B.shape[1], prec, device=A.re.sign.device)
-    rep = mpcgemm_ex(A, B, C, prec, method, slices, stream=stream, carrier=carrier)
+    rep = mpcgemm_ex(A, B, C, prec, method, slices, stream=stream, carrier=carrier, adaptive=adaptive)
     return C, rep
 
 
@@ -217,7 +222,7 @@ def _host_rmat(R) -> RMatC:
 
 
 def mpcgemm_host(A, B, prec: int, method="3M", slices: int = 0, C=None, timing: int = 0, beta: int = 0,
-                 alpha_neg: int = 0):
+                 alpha_neg: int = 0, adaptive: int = 0):
     """End-to-end call on host numpy buffers (mpgen.CMat); returns (C, report)."""
     from mpgen import empty_cmat
     m, k = A.shape
@@ -226,7 +231,7 @@ def mpcgemm_host(A, B, prec: int, method="3M", slices: int = 0, C=None, timing: 
     a = CMatC(_host_rmat(A.re), _host_rmat(A.im))
     b = CMatC(_host_rmat(B.re), _host_rmat(B.im))
     c = CMatC(_host_rmat(C.re), _host_rmat(C.im))
-    opts = OptsC(None, slices, 0, None, 0, timing, beta, alpha_neg, 0)
+    opts = OptsC(None, slices, 0, None, 0, timing, beta, alpha_neg, 0, adaptive, None)
     rep = ReportC()
     rc = lib().mpcgemm_host(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), METHODS[method],
                             ctypes.byref(opts), ctypes.byref(rep))
@@ -238,7 +243,7 @@ def mpcgemm_rho_bounds(A: DevCMat, B: DevCMat, prec: int, full: int = 0, stream=
     m, k = A.shape
     n = B.shape[1]
     out = (ctypes.c_int64 * 3)()
-    opts = OptsC(_stream_ptr(stream), 0, 0, None, 0, 0, 0, 0, 0)
+    opts = OptsC(_stream_ptr(stream), 0, 0, None, 0, 0, 0, 0, 0, 0, None)
     a, b = A.c(), B.c()
     _check(lib().mpcgemm_rho_bounds(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), full, ctypes.byref(opts), out))
     return tuple(int(v) for v in out)

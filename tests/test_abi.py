@@ -52,11 +52,32 @@ def test_library_is_sm100a_with_tensor_core_code(P):
     assert "libtorch" not in deps and "python" not in deps
 
 
-def test_struct_layout_matches_header(P):
+def _c_layout(struct, fields):
+    """sizeof and offsetof of a header struct, from a C program compiled against the header."""
+    import subprocess
+    import tempfile
+    inc = os.path.join(ROOT, "include")
+    body = "".join(f'printf("%zu\\n", offsetof({struct}, {f}));' for f in fields)
+    src = (f'#include <stdio.h>\n#include <stddef.h>\n#include "mpcgemm.h"\n'
+           f'int main(void) {{ printf("%zu\\n", sizeof({struct})); {body} return 0; }}\n')
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = os.path.join(d, "l.c"), os.path.join(d, "l")
+        open(c, "w").write(src)
+        subprocess.check_call(["gcc", "-I", inc, "-o", exe, c])
+        vals = [int(x) for x in subprocess.check_output([exe]).split()]
+    return vals[0], vals[1:]
+
+
+@pytest.mark.parametrize("name", ["RMatC", "CMatC", "OptsC", "ReportC"])
+def test_struct_layout_matches_header(P, name):
+    """The binding's ctypes structs have the header's size and field offsets."""
     M = P.mpcgemm
-    assert ctypes.sizeof(M.RMatC) == 32 and ctypes.sizeof(M.CMatC) == 64
-    assert ctypes.sizeof(M.OptsC) == 48
-    assert M.ReportC.ms_fold.offset + 4 == ctypes.sizeof(M.ReportC) or ctypes.sizeof(M.ReportC) % 8 == 0
+    cls = getattr(M, name)
+    cname = {"RMatC": "mpc_rmat", "CMatC": "mpc_cmat", "OptsC": "mpcgemm_opts", "ReportC": "mpcgemm_report"}[name]
+    fields = [f for f, _ in cls._fields_]
+    size, offs = _c_layout(cname, fields)
+    assert ctypes.sizeof(cls) == size
+    assert [getattr(cls, f).offset for f in fields] == offs
 
 
 def test_version_and_strerror(P):
