@@ -61,6 +61,12 @@ def lib():
             L.orc_cgemm_ozaki_acc_rows.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, P, P, i32, i32, i32, vp,
                                                    i64, vp, vp, i32]
             L.orc_cgemm_ozaki_acc_rows.restype = ctypes.c_int
+            L.orc_cscalar.argtypes = [i32, i64, i32, P, P, P, P, P, P, P, P, vp]
+            L.orc_cscalar.restype = ctypes.c_int
+            L.orc_clu_factor.argtypes = [i64, P, P, i32, i32, i32, vp, i32, vp]
+            L.orc_clu_factor.restype = ctypes.c_int
+            L.orc_clu_solve.argtypes = [i64, P, P, vp, P, P, i64, i32]
+            L.orc_clu_solve.restype = ctypes.c_int
             L.orc_cgemm_ozaki_bits.argtypes = [i64, i64, i64, P, P, P, P, P, P, i32, i32, i32, i32, i64, vp, vp, i32]
             L.orc_cgemm_ozaki_bits.restype = ctypes.c_int
             L.orc_split_bits.argtypes = [ctypes.c_int, i64, i64, P, P, i32, i32, i32, vp]
@@ -284,3 +290,53 @@ def slices_for(prec: int, method, k: int, minT: int, minT1: int | None = None, m
 
 def auto_slices(A: CMat, B: CMat, prec: int, method, nthreads: int = 0):
     return slices_for(prec, method, A.shape[1], *rho_bounds(A, B, nthreads))
+
+
+# ------------------------------------------------------------------ NEXT-3: complex LU
+def cscalar(op: str, X: CMat, Y: CMat | None = None, A: CMat | None = None, prec: int | None = None):
+    """Elementwise MPC-style scalar ops on 1 x cnt matrices (orc_cscalar): "mul" = cmul(X, Y),
+    "fms" = A - X Y, "recip" = 1 / X (each part one RNE to prec); "key" -> list of pivot keys
+    (e, v)."""
+    prec = X.prec if prec is None else prec
+    cnt = X.shape[1]
+    Y = X if Y is None else Y
+    A = X if A is None else A
+    O = CMat(empty_rmat(1, cnt, prec), empty_rmat(1, cnt, prec))
+    kv = np.zeros(2 * max(cnt, 1), np.int64)
+    opn = {"mul": 0, "fms": 1, "recip": 2, "key": 3}[op]
+    args = [_rm(A.re), _rm(A.im), _rm(X.re), _rm(X.im), _rm(Y.re), _rm(Y.im), _rm(O.re), _rm(O.im)]
+    rc = lib().orc_cscalar(opn, cnt, prec, *[_ptr(a) for a in args], kv.ctypes.data)
+    if rc:
+        raise RuntimeError(f"orc_cscalar returned {rc}")
+    if op == "key":
+        return [(int(kv[2 * t]), float(kv[2 * t + 1:2 * t + 2].view(np.float64)[0])) for t in range(cnt)]
+    return O
+
+
+def lu_factor(A: CMat, K: int, method="3M", prec: int | None = None, nthreads: int = 0):
+    """Blocked right-looking complex LU with partial pivoting and Ozaki GEMM trailing updates
+    (orc_clu_factor).  Returns (LU, ipiv, info, smax); A is not modified."""
+    prec = A.prec if prec is None else prec
+    n = A.shape[0]
+    assert A.shape == (n, n)
+    F = A.copy()
+    ipiv = np.zeros(max(n, 1), np.int64)
+    smax = ctypes.c_int32(0)
+    info = lib().orc_clu_factor(n, _ptr(_rm(F.re)), _ptr(_rm(F.im)), prec, K, _form(method), ipiv.ctypes.data,
+                                nthreads, ctypes.addressof(smax))
+    if info < 0:
+        raise RuntimeError(f"orc_clu_factor returned {info}")
+    return F, ipiv[:n], info, smax.value
+
+
+def lu_solve(F: CMat, ipiv, B: CMat, prec: int | None = None) -> CMat:
+    """Eq. 7 solve with the factors of lu_factor (orc_clu_solve); returns X (B untouched)."""
+    prec = F.prec if prec is None else prec
+    n = F.shape[0]
+    X = B.copy()
+    ip = np.ascontiguousarray(np.asarray(ipiv, dtype=np.int64))
+    rc = lib().orc_clu_solve(n, _ptr(_rm(F.re)), _ptr(_rm(F.im)), ip.ctypes.data, _ptr(_rm(X.re)), _ptr(_rm(X.im)),
+                             X.shape[1], prec)
+    if rc:
+        raise RuntimeError(f"orc_clu_solve returned {rc}")
+    return X

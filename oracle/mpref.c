@@ -800,3 +800,293 @@ int32_t orc_slices_for_bits(int32_t prec, int32_t form, int64_t k, int64_t minT,
         if ((double)bits * s >= (double)prec - 4.0 + log2(c * s) + log2rho + 0.1) return s;
     return -1;
 }
+
+/* ================================================================== NEXT-3: complex LU
+ * The paper's second workload (Eq. 7, Fig. 3): blocked right-looking complex
+ * LU with partial pivoting whose trailing update A22 := A22 - L21 U12 is an Ozaki complex GEMM
+ * ("For fast LU decomposition, L21 U12 must be fast in xGEMM"), plus the forward
+ * and backward substitutions of Eq. 7.  Scalar operations are MPC-style: each real part of a
+ * complex result is the exact value rounded ONCE to prec (RNE; reading Z8):
+ *   cmul(x, y)    = ( RNE(xr yr - xi yi), RNE(xr yi + xi yr) )
+ *   cfms(a, x, y) = ( RNE(ar - (xr yr - xi yi)), RNE(ai - (xr yi + xi yr)) )      a - x y
+ *   crecip(z)     = ( RNE(zr / (zr^2 + zi^2)), RNE(-zi / (zr^2 + zi^2)) )
+ * The column scaling multiplies by the rounded reciprocal of the pivot (as LAPACK's xGETF2
+ * scales by 1 / A(j,j)), and the back substitution x_c = cmul(y_c, crecip(u_cc)).
+ * Pivot (max |re| + |im|): key(z) = (e, v), e = max exponent of the nonzero
+ * parts, v = t(re) + t(im) in binary64 (round to nearest), t(x) = (top 53 bits of |x|,
+ * truncated) * 2^(exp(x) - e) as a binary64 (0 if exp(x) - e < -1000); keys compare by (e, v)
+ * after normalising v into [0.5, 1) (v >= 1: e + 1, v / 2).  First maximum wins. */
+
+static xn xn_mul(const xn *a, const xn *b) {
+    xn r = {0, 0, 0, NULL, 1};
+    if (!a->n || !b->n) { r.own = 0; return r; }
+    r.m = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(a->n + b->n));
+    mulmag(r.m, a->m, a->n, b->m, b->n);
+    r.n = a->n + b->n;
+    r.e = a->e + b->e;
+    r.neg = a->neg ^ b->neg;
+    return r;
+}
+
+/* RNE(a / b) to prec bits (b != 0): q = floor(Na 2^sh / Nb) with >= prec + 2 bits by plain
+ * shift-and-subtract long division, then RNE of 2 q + (remainder != 0) */
+static void xn_div_store(const xn *a, const xn *b, int prec, uint8_t *sign, int64_t *exp, uint64_t *limbs, int Lout) {
+    if (!a->n) { xn z = {0, 0, 0, NULL, 0}; xn_store(&z, prec, sign, exp, limbs, Lout); return; }
+    int ba = bitlen_limbs(a->m, a->n), bb = bitlen_limbs(b->m, b->n);
+    int64_t sh = (int64_t)prec + 2 + bb - ba;            /* Na 2^sh >= 2^(prec+1) Nb */
+    if (sh < 0) sh = 0;
+    int nn = (int)((ba + sh) / 64) + 2, nd = b->n + 1;
+    uint64_t *num = (uint64_t *)calloc((size_t)nn, 8), *q = (uint64_t *)calloc((size_t)nn + 1, 8);
+    uint64_t *rem = (uint64_t *)calloc((size_t)nd + 1, 8);
+    shl_limbs(num, nn, a->m, a->n, sh);
+    for (int64_t pos = 64 * (int64_t)nn - 1; pos >= 0; pos--) {
+        uint64_t c = (uint64_t)getbit(num, nn, pos);        /* rem = 2 rem + bit */
+        for (int i = 0; i <= nd; i++) { uint64_t t = rem[i] >> 63; rem[i] = (rem[i] << 1) | c; c = t; }
+        int ge = 1;                                          /* rem >= Nb ? */
+        for (int i = nd; i >= 0; i--) {
+            uint64_t d = i < b->n ? b->m[i] : 0;
+            if (rem[i] != d) { ge = rem[i] > d; break; }
+        }
+        if (ge) {
+            uint64_t br = 0;
+            for (int i = 0; i <= nd; i++) {
+                uint64_t d = i < b->n ? b->m[i] : 0;
+                u128 t = (u128)rem[i] - d - br;
+                rem[i] = (uint64_t)t; br = (t >> 64) ? 1 : 0;
+            }
+            q[pos >> 6] |= 1ull << (pos & 63);
+        }
+    }
+    int sticky = !is_zero_limbs(rem, nd + 1);
+    xn r; r.own = 1; r.n = nn + 1; r.m = (uint64_t *)calloc((size_t)nn + 1, 8);
+    shl_limbs(r.m, nn + 1, q, nn, 1);
+    r.m[0] |= (uint64_t)sticky;
+    r.e = a->e - b->e - sh - 1;
+    r.neg = a->neg ^ b->neg;
+    xn_store(&r, prec, sign, exp, limbs, Lout);
+    xn_free(&r); free(num); free(q); free(rem);
+}
+
+static xn xn_of(const uint8_t *s, const int64_t *e, const uint64_t *l, int L) {
+    xn v; v.m = (uint64_t *)l; v.n = is_zero_limbs(l, L) ? 0 : L; v.neg = v.n ? (*s != 0) : 0;
+    v.e = *e - 64 * (int64_t)L; v.own = 0;
+    return v;
+}
+
+typedef struct { uint8_t *s; int64_t *e; uint64_t *l; } orc_el;     /* one real element */
+static orc_el el_at(orc_rmat *M, int64_t r, int64_t c) {
+    int64_t idx = r * M->ld + c;
+    orc_el x = {M->sign + idx, M->exp + idx, M->limbs + idx * M->L};
+    return x;
+}
+static xn xn_el(orc_el x, int L) { return xn_of(x.s, x.e, x.l, L); }
+
+/* (or, oi) := a - x y  (a may be NULL: := x y) , each part one RNE */
+static void c_fms(int L, int prec, const xn *ar, const xn *ai, const xn *xr, const xn *xi,
+                  const xn *yr, const xn *yi, orc_el or_, orc_el oi) {
+    xn p1 = xn_mul(xr, yr), p2 = xn_mul(xi, yi), p3 = xn_mul(xr, yi), p4 = xn_mul(xi, yr);
+    xn re = xn_add(&p1, &p2, 1), im = xn_add(&p3, &p4, 0);
+    if (ar) {
+        xn r2 = xn_add(ar, &re, 1), i2 = xn_add(ai, &im, 1);
+        xn_free(&re); xn_free(&im); re = r2; im = i2;
+    }
+    xn_store(&re, prec, or_.s, or_.e, or_.l, L);
+    xn_store(&im, prec, oi.s, oi.e, oi.l, L);
+    xn_free(&p1); xn_free(&p2); xn_free(&p3); xn_free(&p4); xn_free(&re); xn_free(&im);
+}
+
+static void c_recip(int L, int prec, const xn *zr, const xn *zi, orc_el or_, orc_el oi) {
+    xn a = xn_mul(zr, zr), b = xn_mul(zi, zi);
+    xn d = xn_add(&a, &b, 0);
+    xn nzi = *zi; nzi.neg = nzi.n ? !nzi.neg : 0;
+    xn_div_store(zr, &d, prec, or_.s, or_.e, or_.l, L);
+    xn_div_store(&nzi, &d, prec, oi.s, oi.e, oi.l, L);
+    xn_free(&a); xn_free(&b); xn_free(&d);
+}
+
+/* top 53 bits of |x| (truncated) as a binary64 scaled by 2^(exp - e) */
+static double key_part(const xn *x, int64_t e) {
+    if (!x->n) return 0.0;
+    int b = bitlen_limbs(x->m, x->n);
+    int64_t ex = x->e + b;                       /* MPFR exponent */
+    if (ex - e < -1000) return 0.0;
+    uint64_t t;
+    shr_limbs(&t, 1, x->m, x->n, b - 53);
+    return ldexp((double)t, (int)(ex - e - 53));
+}
+static void pivot_key(const xn *re, const xn *im, int64_t *e, double *v) {
+    int any = 0; int64_t best = 0;
+    const xn *p[2] = {re, im};
+    for (int q = 0; q < 2; q++) {
+        if (!p[q]->n) continue;
+        int64_t ex = p[q]->e + bitlen_limbs(p[q]->m, p[q]->n);
+        if (!any || ex > best) best = ex;
+        any = 1;
+    }
+    if (!any) { *e = INT64_MIN; *v = 0.0; return; }
+    volatile double a = key_part(re, best), b = key_part(im, best);
+    double s = a + b;
+    if (s >= 1.0) { s = s * 0.5; best += 1; }
+    *e = best; *v = s;
+}
+
+/* elementwise scalar ops for the pins: op 0 = cmul(x, y), 1 = cfms(a, x, y), 2 = crecip(x),
+ * 3 = pivot key (written to kv[2*i] = e, kv[2*i+1] = v bits).  All matrices 1 x cnt. */
+int orc_cscalar(int32_t op, int64_t cnt, int32_t prec, const orc_rmat *Ar, const orc_rmat *Ai,
+                const orc_rmat *Xr, const orc_rmat *Xi, const orc_rmat *Yr, const orc_rmat *Yi,
+                orc_rmat *Or, orc_rmat *Oi, int64_t *kv)
+{
+    int L = Xr->L;
+    for (int64_t t = 0; t < cnt; t++) {
+        xn xr = entry_of(Xr, 0, t), xi = entry_of(Xi, 0, t);
+        if (op == 3) {
+            double v; pivot_key(&xr, &xi, &kv[2 * t], &v);
+            memcpy(&kv[2 * t + 1], &v, 8);
+            continue;
+        }
+        orc_el o1 = el_at(Or, 0, t), o2 = el_at(Oi, 0, t);
+        if (op == 2) { if (!xr.n && !xi.n) return -1; c_recip(L, prec, &xr, &xi, o1, o2); continue; }
+        xn yr = entry_of(Yr, 0, t), yi = entry_of(Yi, 0, t);
+        if (op == 0) c_fms(L, prec, NULL, NULL, &xr, &xi, &yr, &yi, o1, o2);
+        else { xn ar = entry_of(Ar, 0, t), ai = entry_of(Ai, 0, t); c_fms(L, prec, &ar, &ai, &xr, &xi, &yr, &yi, o1, o2); }
+    }
+    return 0;
+}
+
+static orc_rmat view(const orc_rmat *M, int64_t r, int64_t c) {
+    orc_rmat v = *M;
+    int64_t idx = r * M->ld + c;
+    v.sign = M->sign + idx; v.exp = M->exp + idx; v.limbs = M->limbs + idx * M->L;
+    return v;
+}
+
+static void swap_rows(orc_rmat *M, int64_t r1, int64_t r2, int64_t ncols) {
+    int L = M->L;
+    for (int64_t c = 0; c < ncols; c++) {
+        orc_el a = el_at(M, r1, c), b = el_at(M, r2, c);
+        uint8_t ts = *a.s; *a.s = *b.s; *b.s = ts;
+        int64_t te = *a.e; *a.e = *b.e; *b.e = te;
+        for (int l = 0; l < L; l++) { uint64_t x = a.l[l]; a.l[l] = b.l[l]; b.l[l] = x; }
+    }
+}
+
+/* In place: L (unit lower, strictly below the diagonal) and U (upper) with P A = L U;
+ * ipiv[c] = the row swapped with row c at step c.  For each panel j0 = 0, K, 2K, ... of width
+ * w = min(K, n - j0) (Fig. 3):
+ *   (a) for c in [j0, j0+w): pivot p = argmax_{r >= c} key(A_rc); swap rows c, p (all
+ *       columns); r = crecip(A_cc); A_rc := cmul(A_rc, r) for r > c; A_rt := cfms(A_rt, A_rc,
+ *       A_ct) for r > c, c < t < j0+w                               (panel, LAPACK xGETF2)
+ *   (b) for c in [j0, j0+w), r in (c, j0+w), t >= j0+w: A_rt := cfms(A_rt, A_rc, A_ct)
+ *                                                                    (U12 := L11^-1 A12)
+ *   (c) A22 := A22 - L21 U12 by orc_cgemm_ozaki_acc (form, certified s of this product, one
+ *       rounding per element)
+ * Returns 0, or c + 1 for the first zero pivot (the factorization continues), < 0 on error.
+ * smax (optional) receives the largest slice count used by the updates. */
+int orc_clu_factor(int64_t n, orc_rmat *Ar, orc_rmat *Ai, int32_t prec, int32_t K, int32_t form,
+                   int64_t *ipiv, int32_t nthreads, int32_t *smax)
+{
+    if (n < 0 || K < 1 || (form != 3 && form != 4)) return -1;
+    const int L = Ar->L;
+    int info = 0;
+    if (smax) *smax = 0;
+    for (int64_t j0 = 0; j0 < n; j0 += K) {
+        const int64_t w = (n - j0 < K) ? n - j0 : K;
+        for (int64_t c = j0; c < j0 + w; c++) {
+            int64_t p = c, be = INT64_MIN; double bv = 0.0;
+            for (int64_t r = c; r < n; r++) {
+                xn zr = xn_el(el_at(Ar, r, c), L), zi = xn_el(el_at(Ai, r, c), L);
+                int64_t e; double v;
+                pivot_key(&zr, &zi, &e, &v);
+                if (e > be || (e == be && v > bv)) { be = e; bv = v; p = r; }
+            }
+            ipiv[c] = p;
+            if (p != c) { swap_rows(Ar, c, p, n); swap_rows(Ai, c, p, n); }
+            xn pr = xn_el(el_at(Ar, c, c), L), pi = xn_el(el_at(Ai, c, c), L);
+            if (!pr.n && !pi.n) { if (!info) info = (int)(c + 1); continue; }
+            uint8_t rs[2]; int64_t re_[2]; uint64_t rl[2][64];
+            orc_el o1 = {&rs[0], &re_[0], rl[0]}, o2 = {&rs[1], &re_[1], rl[1]};
+            c_recip(L, prec, &pr, &pi, o1, o2);
+            xn rr = xn_el(o1, L), ri = xn_el(o2, L);
+            for (int64_t r = c + 1; r < n; r++) {
+                xn ar = xn_el(el_at(Ar, r, c), L), ai = xn_el(el_at(Ai, r, c), L);
+                c_fms(L, prec, NULL, NULL, &ar, &ai, &rr, &ri, el_at(Ar, r, c), el_at(Ai, r, c));
+            }
+            #pragma omp parallel for num_threads(nthreads_of(nthreads)) schedule(static)
+            for (int64_t r = c + 1; r < n; r++) {
+                xn lr = xn_el(el_at(Ar, r, c), L), li = xn_el(el_at(Ai, r, c), L);
+                for (int64_t t = c + 1; t < j0 + w; t++) {
+                    xn ur = xn_el(el_at(Ar, c, t), L), ui = xn_el(el_at(Ai, c, t), L);
+                    xn ar = xn_el(el_at(Ar, r, t), L), ai = xn_el(el_at(Ai, r, t), L);
+                    c_fms(L, prec, &ar, &ai, &lr, &li, &ur, &ui, el_at(Ar, r, t), el_at(Ai, r, t));
+                }
+            }
+        }
+        if (j0 + w >= n) break;
+        for (int64_t c = j0; c < j0 + w; c++) {
+            #pragma omp parallel for num_threads(nthreads_of(nthreads)) schedule(static)
+            for (int64_t t = j0 + w; t < n; t++) {
+                xn ur = xn_el(el_at(Ar, c, t), L), ui = xn_el(el_at(Ai, c, t), L);
+                for (int64_t r = c + 1; r < j0 + w; r++) {
+                    xn lr = xn_el(el_at(Ar, r, c), L), li = xn_el(el_at(Ai, r, c), L);
+                    xn ar = xn_el(el_at(Ar, r, t), L), ai = xn_el(el_at(Ai, r, t), L);
+                    c_fms(L, prec, &ar, &ai, &lr, &li, &ur, &ui, el_at(Ar, r, t), el_at(Ai, r, t));
+                }
+            }
+        }
+        const int64_t m2 = n - j0 - w;
+        orc_rmat L21r = view(Ar, j0 + w, j0), L21i = view(Ai, j0 + w, j0);
+        orc_rmat U12r = view(Ar, j0, j0 + w), U12i = view(Ai, j0, j0 + w);
+        orc_rmat A22r = view(Ar, j0 + w, j0 + w), A22i = view(Ai, j0 + w, j0 + w);
+        int64_t rb[3];
+        if (orc_rho_bounds(m2, m2, w, &L21r, &L21i, &U12r, &U12i, rb, nthreads, 0)) return -2;
+        int32_t s = orc_slices_for(prec, form, w, rb[0], rb[1], rb[2]);
+        if (s < 1) return -3;
+        if (smax && s > *smax) *smax = s;
+        if (ozaki_core(m2, m2, w, &L21r, &L21i, &U12r, &U12i, &A22r, &A22i, prec, form, s, -1, NULL, NULL,
+                       nthreads, &A22r, &A22i, 1, 1, 8, NULL))
+            return -4;
+    }
+    return info;
+}
+
+/* Eq. 7 with the factors of orc_clu_factor: B (n x nrhs) := A^-1 B.  Row swaps ipiv[c] in
+ * order; forward substitution B_r := cfms(B_r, L_rc, B_c) (r > c, c ascending); backward
+ * B_c := cmul(B_c, crecip(U_cc)), then B_r := cfms(B_r, U_rc, B_c) (r < c, c descending). */
+int orc_clu_solve(int64_t n, const orc_rmat *LUr, const orc_rmat *LUi, const int64_t *ipiv,
+                  orc_rmat *Br, orc_rmat *Bi, int64_t nrhs, int32_t prec)
+{
+    const int L = LUr->L;
+    orc_rmat *Mr = (orc_rmat *)LUr, *Mi = (orc_rmat *)LUi;
+    for (int64_t c = 0; c < n; c++)
+        if (ipiv[c] != c) { swap_rows(Br, c, ipiv[c], nrhs); swap_rows(Bi, c, ipiv[c], nrhs); }
+    for (int64_t c = 0; c < n; c++)
+        for (int64_t r = c + 1; r < n; r++) {
+            xn lr = xn_el(el_at(Mr, r, c), L), li = xn_el(el_at(Mi, r, c), L);
+            for (int64_t q = 0; q < nrhs; q++) {
+                xn yr = xn_el(el_at(Br, c, q), L), yi = xn_el(el_at(Bi, c, q), L);
+                xn ar = xn_el(el_at(Br, r, q), L), ai = xn_el(el_at(Bi, r, q), L);
+                c_fms(L, prec, &ar, &ai, &lr, &li, &yr, &yi, el_at(Br, r, q), el_at(Bi, r, q));
+            }
+        }
+    for (int64_t c = n - 1; c >= 0; c--) {
+        xn ur = xn_el(el_at(Mr, c, c), L), ui = xn_el(el_at(Mi, c, c), L);
+        if (!ur.n && !ui.n) return -1;
+        uint8_t rs[2]; int64_t re_[2]; uint64_t rl[2][64];
+        orc_el o1 = {&rs[0], &re_[0], rl[0]}, o2 = {&rs[1], &re_[1], rl[1]};
+        c_recip(L, prec, &ur, &ui, o1, o2);
+        xn rr = xn_el(o1, L), ri = xn_el(o2, L);
+        for (int64_t q = 0; q < nrhs; q++) {
+            xn yr = xn_el(el_at(Br, c, q), L), yi = xn_el(el_at(Bi, c, q), L);
+            c_fms(L, prec, NULL, NULL, &yr, &yi, &rr, &ri, el_at(Br, c, q), el_at(Bi, c, q));
+        }
+        for (int64_t r = 0; r < c; r++) {
+            xn lr = xn_el(el_at(Mr, r, c), L), li = xn_el(el_at(Mi, r, c), L);
+            for (int64_t q = 0; q < nrhs; q++) {
+                xn yr = xn_el(el_at(Br, c, q), L), yi = xn_el(el_at(Bi, c, q), L);
+                xn ar = xn_el(el_at(Br, r, q), L), ai = xn_el(el_at(Bi, r, q), L);
+                c_fms(L, prec, &ar, &ai, &lr, &li, &yr, &yi, el_at(Br, r, q), el_at(Bi, r, q));
+            }
+        }
+    }
+    return 0;
+}
