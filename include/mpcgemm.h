@@ -151,6 +151,50 @@ int mpcgemm_slices_for(int32_t prec, mpcgemm_method method, int64_t k,
 size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec,
                               mpcgemm_method method, int32_t slices);
 
+/* ------------------------------------------------------------------ NEXT-3: complex LU
+ * The paper's second workload (Eq. 7, Fig. 3).  All pointers DEVICE; A is
+ * n x n (ld >= n), factored in place: P A = L U with L unit lower (strictly below the
+ * diagonal) and U upper; ipiv[c] (int64) = the row swapped with row c at step c.  For each
+ * panel j0 = 0, K, 2K, ... of width w = min(K, n - j0):
+ *   (a) c = j0 .. j0+w-1: pivot p = first argmax_{r >= c} key(A_rc) (key: |re| + |im| as
+ *       (max exponent, binary64 sum of the top-53-bit parts) -- DESIGN.md NEXT-3); swap rows c
+ *       and p over all n columns; A_rc := cmul(A_rc, crecip(A_cc)) for r > c; A_rt :=
+ *       cfms(A_rt, A_rc, A_ct) for r > c, c < t < j0 + w        (LAPACK xGETF2 on the panel)
+ *   (b) A_rt := cfms(A_rt, A_rc, A_ct) for c in the panel, c < r < j0 + w, t >= j0 + w
+ *                                                                 (U12 := L11^-1 A12)
+ *   (c) A22 := A22 - L21 U12 by mpcgemm_ex (method, certified auto s, beta = 1, alpha_neg = 1:
+ *       one rounding per element; opts->adaptive passes through)
+ * Scalar ops, each real part the exact value rounded once (RNE) to prec:
+ *   cmul(x, y) = RNE(x y);  cfms(a, x, y) = RNE(a - x y);  crecip(z) = RNE(conj(z) / |z|^2).
+ * Bit-identical to oracle orc_clu_factor.  K = 1 is column-wise LU with rank-1 Ozaki updates;
+ * K >= n is unblocked (no GEMM).  2 <= prec <= 1024.  A zero pivot does not stop the
+ * factorization; rep->info = c + 1 for the first one (0: nonsingular).  opts: stream,
+ * timing (per-phase times; synchronizes), adaptive.  Synchronizes the stream (info readback). */
+typedef struct {
+    int32_t info;             /* 0, or c + 1 of the first zero pivot                           */
+    int32_t gemm_calls;       /* trailing updates through the Ozaki GEMM                       */
+    int32_t slices_max;       /* largest slice count of the updates                            */
+    int32_t kernel_launches;  /* kernels launched (panel + trsm + GEMM)                        */
+    float   ms_panel, ms_trsm, ms_gemm;   /* opts->timing only                                  */
+} mpclu_report;
+
+int mpclu_factor(int64_t n, int32_t prec, mpc_cmat *A, int64_t *ipiv, int32_t K, mpcgemm_method method,
+                 const mpcgemm_opts *opts, mpclu_report *rep);
+
+/* Eq. 7: B (n x nrhs, ld >= nrhs, DEVICE) := A^-1 B with the factors of mpclu_factor: the row
+ * swaps ipiv[0..n) in order; forward B_r := cfms(B_r, L_rc, B_c) (r > c, c ascending);
+ * backward B_c := cmul(B_c, crecip(U_cc)), then B_r := cfms(B_r, U_rc, B_c) (r < c, c
+ * descending).  One CTA; stream-ordered.  A zero U_cc gives a zero B_c. */
+int mpclu_solve(int64_t n, int64_t nrhs, int32_t prec, const mpc_cmat *LU, const int64_t *ipiv, mpc_cmat *B,
+                const mpcgemm_opts *opts);
+
+/* Elementwise device MP scalar operations on 1 x cnt DEVICE matrices (used by the tests to
+ * check the LU's arithmetic against the oracle): op 0: O = cmul(X, Y); 1: O = cfms(A, X, Y);
+ * 2: O = crecip(X) (X != 0); 3: kv[2t] = key exponent, kv[2t+1] = key value (binary64 bits).
+ * stream: cudaStream_t (NULL: legacy default stream). */
+int mpc_scalar(int32_t op, int64_t cnt, int32_t prec, const mpc_cmat *A, const mpc_cmat *X, const mpc_cmat *Y,
+               mpc_cmat *O, int64_t *kv, void *stream);
+
 const char *mpcgemm_strerror(int code);
 const char *mpcgemm_last_error(void);   /* thread-local detail of the last error              */
 void mpcgemm_release(void);              /* frees the cached workspace of the current device   */

@@ -5,8 +5,10 @@ is the thin Python binding (mpcgemm.py) and the multi-GPU driver (dist.py).
 """
 from .mpcgemm import (DevCMat, DevRMat, MpcgemmError, empty_device, gemm, lib, mpcgemm_ex, mpcgemm_host,
                       mpcgemm_release, mpcgemm_rho_bounds, mpcgemm_slices_for, mpcgemm_strerror,
-                      mpcgemm_version, mpcgemm_workspace_size, to_device, to_host)
+                      mpcgemm_version, mpcgemm_workspace_size, mpc_scalar, mpclu_factor, mpclu_solve, to_device,
+                      to_host)
 
 __all__ = ["DevCMat", "DevRMat", "MpcgemmError", "empty_device", "gemm", "lib", "mpcgemm_ex", "mpcgemm_host",
            "mpcgemm_release", "mpcgemm_rho_bounds", "mpcgemm_slices_for", "mpcgemm_strerror",
-           "mpcgemm_version", "mpcgemm_workspace_size", "to_device", "to_host"]
+           "mpcgemm_version", "mpcgemm_workspace_size", "mpc_scalar", "mpclu_factor", "mpclu_solve", "to_device",
+           "to_host"]

@@ -68,4 +68,19 @@ cudaError_t dmma_slicegemm_launch(const double *digA, const double *digB, int64_
 cudaError_t fold_f64_launch(const int64_t *partials, int64_t m, int64_t n, int s, int b, int method, int prec, int L,
                             const int64_t *eA, const int64_t *eB, DMatOut Cre, DMatOut Cim, cudaStream_t st);
 
+// NEXT-3: complex LU (lu.cu).  L = limbs per element (1..16).
+struct LuScratch { uint8_t *sign; int64_t *exp; uint64_t *limbs; };   // 2 elements (1 / pivot)
+cudaError_t lu_pivot_launch(int L, DMatOut re, DMatOut im, int64_t n, int64_t c, int64_t *ipiv, cudaStream_t st);
+cudaError_t lu_swap_launch(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t c, const int64_t *ipiv, cudaStream_t st);
+cudaError_t lu_recip_launch(int L, DMatOut re, DMatOut im, int64_t c, int prec, LuScratch s, int32_t *info,
+                            cudaStream_t st);
+cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec, LuScratch s,
+                            cudaStream_t st);
+cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0, int64_t t1, int64_t c,
+                             int prec, cudaStream_t st);
+cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const int64_t *ipiv, DMatOut bre, DMatOut bim,
+                            int64_t nrhs, int prec, LuScratch s, cudaStream_t st);
+cudaError_t mp_scalar_launch(int L, int op, int64_t cnt, int prec, DMatOut Ar, DMatOut Ai, DMatOut Xr, DMatOut Xi,
+                             DMatOut Yr, DMatOut Yi, DMatOut Or, DMatOut Oi, int64_t *kv, cudaStream_t st);
+
 }  // namespace mpc

@@ -1,0 +1,258 @@
+// lu.cu -- NEXT-3: the kernels of the blocked right-looking complex LU with partial pivoting
+// (Fig. 3) and of the Eq. 7 solve.  The trailing update A22 -= L21 U12 is
+// the Ozaki GEMM of this library (mpcgemm.cu, accumulate mode); these kernels do the panel
+// (xGETF2: pivot search, row swap, reciprocal, column scaling, rank-1 updates), U12 := L11^-1
+// A12 and the substitutions, every scalar operation MPC-style (mpscalar.cuh).
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+#include "kernels.h"
+#include "mpscalar.cuh"
+
+namespace mpc {
+
+using namespace mps;
+
+struct El {                 // pointers to one real element
+    uint8_t *s; int64_t *e; uint64_t *l;
+};
+MPC_DEV El el(int L, const DMatOut &M, int64_t r, int64_t c) {
+    const int64_t i = r * M.ld + c;
+    return El{M.sign + i, M.exp + i, M.limbs + i * L};
+}
+MPC_DEV Num ld(int L, const El &x) { return load(L, x.s, x.e, x.l); }
+
+// ---------------------------------------------------------------- pivot search (one CTA)
+__global__ void __launch_bounds__(1024) lu_pivot_kernel(int L, DMatOut re, DMatOut im, int64_t n, int64_t c, int64_t *ipiv)
+{
+    __shared__ int64_t se[1024], sr[1024];
+    __shared__ double sv[1024];
+    Key best; best.e = INT64_MIN; best.v = 0.0;
+    int64_t br = c;
+    for (int64_t r = c + threadIdx.x; r < n; r += blockDim.x) {
+        const El a = el(L, re, r, c), b = el(L, im, r, c);
+        const Key k = pivot_key(a.s, a.e, a.l, b.s, b.e, b.l, L);
+        if (key_greater(k, best)) { best = k; br = r; }      // rows ascending: first max kept
+    }
+    se[threadIdx.x] = best.e; sv[threadIdx.x] = best.v; sr[threadIdx.x] = br;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            const int o = threadIdx.x + w;
+            const Key a{se[threadIdx.x], sv[threadIdx.x]}, b{se[o], sv[o]};
+            if (key_greater(b, a) || (!key_greater(a, b) && sr[o] < sr[threadIdx.x])) {
+                se[threadIdx.x] = b.e; sv[threadIdx.x] = b.v; sr[threadIdx.x] = sr[o];
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ipiv[c] = sr[0];
+}
+
+// ---------------------------------------------------------------- row swap (all columns)
+__global__ void lu_swap_kernel(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t c, const int64_t *ipiv)
+{
+    const int64_t p = ipiv[c];
+    if (p == c) return;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncols; t += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int part = 0; part < 2; part++) {
+            const DMatOut &M = part ? im : re;
+            El a = el(L, M, c, t), b = el(L, M, p, t);
+            const uint8_t ts = *a.s; *a.s = *b.s; *b.s = ts;
+            const int64_t te = *a.e; *a.e = *b.e; *b.e = te;
+#pragma unroll
+            for (int q = 0; q < L; q++) { const uint64_t x = a.l[q]; a.l[q] = b.l[q]; b.l[q] = x; }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- reciprocal of the pivot
+// scratch: sign[2], exp[2], limbs[2][L] (re, im of 1 / A_cc); *info = c + 1 on the first zero
+__global__ void lu_recip_kernel(int L, DMatOut re, DMatOut im, int64_t c, int prec, uint8_t *rs, int64_t *rexp,
+                                uint64_t *rl, int32_t *info)
+{
+    if (threadIdx.x || blockIdx.x) return;
+    const Num zr = ld(L, el(L, re, c, c)), zi = ld(L, el(L, im, c, c));
+    if (zr.zero && zi.zero) {
+        if (info && *info == 0) *info = (int32_t)(c + 1);
+        rs[0] = rs[1] = 0; rexp[0] = rexp[1] = 0;
+        for (int q = 0; q < 2 * L; q++) rl[q] = 0;
+        return;
+    }
+    crecip(L, zr, zi, prec, rs, rexp, rl, rs + 1, rexp + 1, rl + L);
+}
+
+// ---------------------------------------------------------------- column scaling
+__global__ void lu_scale_kernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec,
+                                const uint8_t *rs, const int64_t *rexp, const uint64_t *rl)
+{
+    const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= r1) return;
+    const Num yr = load(L, rs, rexp, rl), yi = load(L, rs + 1, rexp + 1, rl + L);
+    const El a = el(L, re, r, c), b = el(L, im, r, c);
+    const Num xr = ld(L, a), xi = ld(L, b);
+    cfms(L, nullptr, nullptr, xr, xi, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+}
+
+// ---------------------------------------------------------------- rank-1 update
+// A_rt := cfms(A_rt, A_rc, A_ct) for r in [r0, r1), t in [t0, t1)
+__global__ void __launch_bounds__(128) lu_update_kernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0,
+                                                        int64_t t1, int64_t c, int prec)
+{
+    const int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= t1) return;
+    const Num ur = ld(L, el(L, re, c, t)), ui = ld(L, el(L, im, c, t));
+    for (int64_t r = r0 + blockIdx.y; r < r1; r += gridDim.y) {
+        const Num lr = ld(L, el(L, re, r, c)), li = ld(L, el(L, im, r, c));
+        const El a = el(L, re, r, t), b = el(L, im, r, t);
+        const Num ar = ld(L, a), ai = ld(L, b);
+        cfms(L, &ar, &ai, lr, li, ur, ui, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+    }
+}
+
+// ---------------------------------------------------------------- Eq. 7 solve (one CTA)
+// B (n x nrhs) := U^-1 L^-1 P B, with the factors of the LU above
+__global__ void __launch_bounds__(256) lu_solve_kernel(int L, DMatOut fre, DMatOut fim, int64_t n, const int64_t *ipiv,
+                                                       DMatOut bre, DMatOut bim, int64_t nrhs, int prec,
+                                                       uint8_t *rs, int64_t *rexp, uint64_t *rl)
+{
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int64_t q = tid; q < nrhs; q += nt)                 // row swaps, in order
+        for (int64_t c = 0; c < n; c++) {
+            const int64_t p = ipiv[c];
+            if (p == c) continue;
+            for (int part = 0; part < 2; part++) {
+                const DMatOut &M = part ? bim : bre;
+                El a = el(L, M, c, q), b = el(L, M, p, q);
+                const uint8_t ts = *a.s; *a.s = *b.s; *b.s = ts;
+                const int64_t te = *a.e; *a.e = *b.e; *b.e = te;
+                for (int w = 0; w < L; w++) { const uint64_t x = a.l[w]; a.l[w] = b.l[w]; b.l[w] = x; }
+            }
+        }
+    __syncthreads();
+    for (int64_t c = 0; c < n; c++) {                         // forward: unit lower L
+        const int64_t cnt = (n - c - 1) * nrhs;
+        for (int64_t x = tid; x < cnt; x += nt) {
+            const int64_t r = c + 1 + x / nrhs, q = x % nrhs;
+            const Num lr = ld(L, el(L, fre, r, c)), li = ld(L, el(L, fim, r, c));
+            const Num yr = ld(L, el(L, bre, c, q)), yi = ld(L, el(L, bim, c, q));
+            const El a = el(L, bre, r, q), b = el(L, bim, r, q);
+            const Num ar = ld(L, a), ai = ld(L, b);
+            cfms(L, &ar, &ai, lr, li, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+        }
+        __syncthreads();
+    }
+    for (int64_t c = n - 1; c >= 0; c--) {                    // backward: U
+        if (tid == 0) {
+            const Num zr = ld(L, el(L, fre, c, c)), zi = ld(L, el(L, fim, c, c));
+            if (zr.zero && zi.zero) { rs[0] = rs[1] = 0; rexp[0] = rexp[1] = 0; for (int w = 0; w < 2 * L; w++) rl[w] = 0; }
+            else crecip(L, zr, zi, prec, rs, rexp, rl, rs + 1, rexp + 1, rl + L);
+        }
+        __syncthreads();
+        for (int64_t q = tid; q < nrhs; q += nt) {
+            const Num yr = load(L, rs, rexp, rl), yi = load(L, rs + 1, rexp + 1, rl + L);
+            const El a = el(L, bre, c, q), b = el(L, bim, c, q);
+            const Num xr = ld(L, a), xi = ld(L, b);
+            cfms(L, nullptr, nullptr, xr, xi, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+        }
+        __syncthreads();
+        const int64_t cnt = c * nrhs;
+        for (int64_t x = tid; x < cnt; x += nt) {
+            const int64_t r = x / nrhs, q = x % nrhs;
+            const Num ur = ld(L, el(L, fre, r, c)), ui = ld(L, el(L, fim, r, c));
+            const Num yr = ld(L, el(L, bre, c, q)), yi = ld(L, el(L, bim, c, q));
+            const El a = el(L, bre, r, q), b = el(L, bim, r, q);
+            const Num ar = ld(L, a), ai = ld(L, b);
+            cfms(L, &ar, &ai, ur, ui, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- elementwise (tests)
+// op 0: O = X Y ; 1: O = A - X Y ; 2: O = 1 / X ; 3: key of X -> kv[2t] = e, kv[2t+1] = v bits
+__global__ void mp_scalar_kernel(int L, int op, int64_t cnt, int prec, DMatOut Ar, DMatOut Ai, DMatOut Xr, DMatOut Xi,
+                                 DMatOut Yr, DMatOut Yi, DMatOut Or, DMatOut Oi, int64_t *kv)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    const El xr = el(L, Xr, 0, t), xi = el(L, Xi, 0, t);
+    if (op == 3) {
+        const Key k = pivot_key(xr.s, xr.e, xr.l, xi.s, xi.e, xi.l, L);
+        kv[2 * t] = k.e;
+        kv[2 * t + 1] = __double_as_longlong(k.v);
+        return;
+    }
+    const El o1 = el(L, Or, 0, t), o2 = el(L, Oi, 0, t);
+    const Num x1 = ld(L, xr), x2 = ld(L, xi);
+    if (op == 2) { crecip(L, x1, x2, prec, o1.s, o1.e, o1.l, o2.s, o2.e, o2.l); return; }
+    const Num y1 = ld(L, el(L, Yr, 0, t)), y2 = ld(L, el(L, Yi, 0, t));
+    if (op == 0) { cfms(L, nullptr, nullptr, x1, x2, y1, y2, prec, o1.s, o1.e, o1.l, o2.s, o2.e, o2.l); return; }
+    const Num a1 = ld(L, el(L, Ar, 0, t)), a2 = ld(L, el(L, Ai, 0, t));
+    cfms(L, &a1, &a2, x1, x2, y1, y2, prec, o1.s, o1.e, o1.l, o2.s, o2.e, o2.l);
+}
+
+// ---------------------------------------------------------------- launchers (L dispatch)
+cudaError_t lu_pivot_launch(int L, DMatOut re, DMatOut im, int64_t n, int64_t c, int64_t *ipiv, cudaStream_t st) {
+    if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    lu_pivot_kernel<<<1, 1024, 0, st>>>(L, re, im, n, c, ipiv);
+    return cudaGetLastError();
+}
+
+cudaError_t lu_swap_launch(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t c, const int64_t *ipiv, cudaStream_t st) {
+    const unsigned g = (unsigned)((ncols + 255) / 256);
+    if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    lu_swap_kernel<<<g, 256, 0, st>>>(L, re, im, ncols, c, ipiv);
+    return cudaGetLastError();
+}
+
+cudaError_t lu_recip_launch(int L, DMatOut re, DMatOut im, int64_t c, int prec, LuScratch s, int32_t *info,
+                            cudaStream_t st) {
+    if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    lu_recip_kernel<<<1, 32, 0, st>>>(L, re, im, c, prec, s.sign, s.exp, s.limbs, info);
+    return cudaGetLastError();
+}
+
+cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec, LuScratch s,
+                            cudaStream_t st) {
+    if (r1 <= r0) return cudaSuccess;
+    const unsigned g = (unsigned)((r1 - r0 + 127) / 128);
+    if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    lu_scale_kernel<<<g, 128, 0, st>>>(L, re, im, r0, r1, c, prec, s.sign, s.exp, s.limbs);
+    return cudaGetLastError();
+}
+
+cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0, int64_t t1, int64_t c,
+                             int prec, cudaStream_t st) {
+    if (r1 <= r0 || t1 <= t0) return cudaSuccess;
+    const int64_t rows = r1 - r0;
+    const int64_t gx = (t1 - t0 + 127) / 128;
+    int64_t gy = rows;
+    const int64_t want = 148 * 16;                            // ~16 CTAs of 128 threads per SM
+    if (gx * gy > want) gy = (want + gx - 1) / gx;
+    if (gy < 1) gy = 1;
+    if (gy > 65535) gy = 65535;
+    dim3 grid((unsigned)gx, (unsigned)gy);
+    if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    lu_update_kernel<<<grid, 128, 0, st>>>(L, re, im, r0, r1, t0, t1, c, prec);
+    return cudaGetLastError();
+}
+
+cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const int64_t *ipiv, DMatOut bre, DMatOut bim,
+                            int64_t nrhs, int prec, LuScratch s, cudaStream_t st) {
+    if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    lu_solve_kernel<<<1, 256, 0, st>>>(L, fre, fim, n, ipiv, bre, bim, nrhs, prec, s.sign, s.exp, s.limbs);
+    return cudaGetLastError();
+}
+
+cudaError_t mp_scalar_launch(int L, int op, int64_t cnt, int prec, DMatOut Ar, DMatOut Ai, DMatOut Xr, DMatOut Xi,
+                             DMatOut Yr, DMatOut Yi, DMatOut Or, DMatOut Oi, int64_t *kv, cudaStream_t st) {
+    if (cnt <= 0) return cudaSuccess;
+    const unsigned g = (unsigned)((cnt + 127) / 128);
+    if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    mp_scalar_kernel<<<g, 128, 0, st>>>(L, op, cnt, prec, Ar, Ai, Xr, Xi, Yr, Yi, Or, Oi, kv);
+    return cudaGetLastError();
+}
+
+}  // namespace mpc

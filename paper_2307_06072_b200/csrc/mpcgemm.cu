@@ -46,6 +46,7 @@ struct DevCache {
     void *ws = nullptr; size_t ws_bytes = 0;
     void *meta = nullptr; size_t meta_bytes = 0;
     void *stage = nullptr; size_t stage_bytes = 0;   // mpcgemm_host device staging
+    void *lu = nullptr; size_t lu_bytes = 0;         // NEXT-3 LU scratch (1 / pivot, info)
 };
 std::mutex g_mu;
 std::map<int, DevCache> g_cache;
@@ -255,7 +256,7 @@ size_t mat_span(const mpc_rmat &M, int64_t rows, int64_t cols, int L, int which)
 }
 
 int check_args(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
-               const mpc_cmat *C, int method) {
+               const mpc_cmat *C, int method, bool check_alias = true) {
     if (!A || !B || !C) return fail(MPCGEMM_ERR_ARG, "null matrix descriptor");
     if (m < 0 || n < 0 || k < 0) return fail(MPCGEMM_ERR_ARG, "negative dimension");
     if (method != MPCGEMM_3M && method != MPCGEMM_4M) return fail(MPCGEMM_ERR_ARG, "method must be 3 or 4");
@@ -270,6 +271,7 @@ int check_args(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A,
         if (mats[q]->ld < cols[q]) return fail(MPCGEMM_ERR_ARG, "ld < cols");
     }
     const int L = (prec + 63) / 64;
+    if (!check_alias) return 0;
     for (int c = 4; c < 6; c++)
         for (int q = 0; q < 4; q++)
             for (int w = 0; w < 3; w++)
@@ -599,9 +601,12 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     return 0;
 }
 
+// check_alias = false: the LU's in-place trailing update, whose A22 / L21 / U12 views of one
+// matrix interleave in memory but are element-disjoint (the split reads L21, U12 before the
+// fold writes A22, in stream order)
 int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
-              int method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
-    if (int rc = check_args(m, n, k, prec, A, B, C, method)) return rc;
+              int method, const mpcgemm_opts *opts, mpcgemm_report *rep, bool check_alias = true) {
+    if (int rc = check_args(m, n, k, prec, A, B, C, method, check_alias)) return rc;
     cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
     const int forced = opts ? opts->slices : 0;
     const int validate = opts ? opts->validate : 0;
@@ -719,6 +724,98 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         float t[5];
         for (int q = 0; q < 5; q++) CK(cudaEventElapsedTime(&t[q], E->ev[q], E->ev[q + 1]));
         if (rep) { rep->ms_linemax = t[0]; rep->ms_prepass = t[1]; rep->ms_split = t[2]; rep->ms_gemm = t[3]; rep->ms_fold = t[4]; }
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------- NEXT-3: complex LU
+mpc_rmat sub_view(const mpc_rmat &M, int64_t r, int64_t c, int L) {
+    mpc_rmat v = M;
+    const int64_t i = r * M.ld + c;
+    v.sign = M.sign + i; v.exp = M.exp + i; v.limbs = M.limbs + i * L;
+    return v;
+}
+
+int lu_scratch(int dev, int L, LuScratch *s, int32_t **info) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    DevCache &dc = g_cache[dev];
+    if (int rc = grow(&dc.lu, &dc.lu_bytes, 256 + 16 * 2 * (size_t)L + 64)) return rc;
+    uint8_t *b = (uint8_t *)dc.lu;
+    s->exp = (int64_t *)b; s->limbs = (uint64_t *)(b + 64); s->sign = b + 64 + 16 * 2 * (size_t)L;
+    *info = (int32_t *)(b + 64 + 16 * 2 * (size_t)L + 16);
+    return 0;
+}
+
+struct PhaseTimer {                                     // opts->timing: per-phase CUDA events
+    cudaEvent_t a = nullptr, b = nullptr; cudaStream_t st; bool on;
+    PhaseTimer(bool on_, cudaStream_t s) : st(s), on(on_) {
+        if (on) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, st); }
+    }
+    ~PhaseTimer() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
+    void lap(float *acc) {
+        if (!on) return;
+        float ms = 0.f;
+        cudaEventRecord(b, st); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
+        *acc += ms; std::swap(a, b);
+    }
+};
+
+int lu_impl(int64_t n, int32_t prec, mpc_cmat *A, int64_t *ipiv, int32_t K, int method, const mpcgemm_opts *opts,
+            mpclu_report *rep) {
+    if (rep) memset(rep, 0, sizeof(*rep));
+    if (!A || !ipiv || n < 0 || K < 1) return fail(MPCGEMM_ERR_ARG, "mpclu_factor: bad argument");
+    if (method != MPCGEMM_3M && method != MPCGEMM_4M) return fail(MPCGEMM_ERR_ARG, "method must be 3 or 4");
+    if (prec < 2 || prec > 1024) return fail(MPCGEMM_ERR_PREC, "mpclu_factor: prec outside [2, 1024]");
+    if (n == 0) return 0;
+    if (A->re.ld < n || A->im.ld < n || !A->re.sign || !A->im.sign) return fail(MPCGEMM_ERR_ARG, "mpclu_factor: bad matrix");
+    const int L = (prec + 63) / 64;
+    cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    LuScratch sc; int32_t *info;
+    if (int rc = lu_scratch(dev, L, &sc, &info)) return rc;
+    CK(cudaMemsetAsync(info, 0, 4, st));
+    const DMatOut re = dmo(A->re), im = dmo(A->im);
+    PhaseTimer T(opts && opts->timing, st);
+    float tp = 0.f, tt = 0.f, tg = 0.f;
+    int launches = 0, calls = 0, smax = 0;
+    for (int64_t j0 = 0; j0 < n; j0 += K) {
+        const int64_t w = std::min<int64_t>(K, n - j0);
+        for (int64_t c = j0; c < j0 + w; c++) {               // (a) panel, xGETF2
+            CK(lu_pivot_launch(L, re, im, n, c, ipiv, st));
+            CK(lu_swap_launch(L, re, im, n, c, ipiv, st));
+            CK(lu_recip_launch(L, re, im, c, prec, sc, info, st));
+            CK(lu_scale_launch(L, re, im, c + 1, n, c, prec, sc, st));
+            CK(lu_update_launch(L, re, im, c + 1, n, c + 1, j0 + w, c, prec, st));
+            launches += 5;
+        }
+        T.lap(&tp);
+        if (j0 + w >= n) break;
+        for (int64_t c = j0; c < j0 + w - 1; c++) {           // (b) U12 := L11^-1 A12
+            CK(lu_update_launch(L, re, im, c + 1, j0 + w, j0 + w, n, c, prec, st));
+            launches++;
+        }
+        T.lap(&tt);
+        const int64_t m2 = n - j0 - w;                        // (c) A22 -= L21 U12 (Ozaki)
+        mpc_cmat L21{sub_view(A->re, j0 + w, j0, L), sub_view(A->im, j0 + w, j0, L)};
+        mpc_cmat U12{sub_view(A->re, j0, j0 + w, L), sub_view(A->im, j0, j0 + w, L)};
+        mpc_cmat A22{sub_view(A->re, j0 + w, j0 + w, L), sub_view(A->im, j0 + w, j0 + w, L)};
+        mpcgemm_opts o;
+        memset(&o, 0, sizeof(o));
+        o.stream = (void *)st; o.beta = 1; o.alpha_neg = 1; o.adaptive = opts ? opts->adaptive : 0;
+        mpcgemm_report gr;
+        if (int rc = gemm_impl(m2, m2, w, prec, &L21, &U12, &A22, method, &o, &gr, false)) { if (rc < 0) return rc; }
+        smax = std::max(smax, gr.slices);
+        launches += gr.kernel_launches;
+        calls++;
+        T.lap(&tg);
+    }
+    int32_t h = 0;
+    CK(cudaMemcpyAsync(&h, info, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (rep) {
+        rep->info = h; rep->gemm_calls = calls; rep->slices_max = smax; rep->kernel_launches = launches;
+        rep->ms_panel = tp; rep->ms_trsm = tt; rep->ms_gemm = tg;
     }
     return 0;
 }
@@ -868,7 +965,7 @@ void mpcgemm_release(void) {
     cudaDeviceSynchronize();
     auto it = g_cache.find(dev);
     if (it != g_cache.end()) {
-        cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage);
+        cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage); cudaFree(it->second.lu);
         g_cache.erase(it);
     }
     for (auto p = g_plans.begin(); p != g_plans.end();) {
@@ -877,6 +974,41 @@ void mpcgemm_release(void) {
             p = g_plans.erase(p);
         } else ++p;
     }
+}
+
+int mpclu_factor(int64_t n, int32_t prec, mpc_cmat *A, int64_t *ipiv, int32_t K, mpcgemm_method method,
+                 const mpcgemm_opts *opts, mpclu_report *rep) {
+    return lu_impl(n, prec, A, ipiv, K, (int)method, opts, rep);
+}
+
+int mpclu_solve(int64_t n, int64_t nrhs, int32_t prec, const mpc_cmat *LU, const int64_t *ipiv, mpc_cmat *B,
+                const mpcgemm_opts *opts) {
+    if (!LU || !ipiv || !B || n < 0 || nrhs < 0) return fail(MPCGEMM_ERR_ARG, "mpclu_solve: bad argument");
+    if (prec < 2 || prec > 1024) return fail(MPCGEMM_ERR_PREC, "mpclu_solve: prec outside [2, 1024]");
+    if (n == 0 || nrhs == 0) return 0;
+    if (LU->re.ld < n || LU->im.ld < n || B->re.ld < nrhs || B->im.ld < nrhs) return fail(MPCGEMM_ERR_ARG, "mpclu_solve: ld");
+    const int L = (prec + 63) / 64;
+    cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    LuScratch sc; int32_t *info;
+    if (int rc = lu_scratch(dev, L, &sc, &info)) return rc;
+    CK(lu_solve_launch(L, dmo(LU->re), dmo(LU->im), n, ipiv, dmo(B->re), dmo(B->im), nrhs, prec, sc, st));
+    return 0;
+}
+
+int mpc_scalar(int32_t op, int64_t cnt, int32_t prec, const mpc_cmat *A, const mpc_cmat *X, const mpc_cmat *Y,
+               mpc_cmat *O, int64_t *kv, void *stream) {
+    if (op < 0 || op > 3 || cnt < 0 || !X) return fail(MPCGEMM_ERR_ARG, "mpc_scalar: bad argument");
+    if (prec < 2 || prec > 1024) return fail(MPCGEMM_ERR_PREC, "mpc_scalar: prec outside [2, 1024]");
+    if ((op == 3 && !kv) || (op != 3 && !O) || ((op == 0 || op == 1) && !Y) || (op == 1 && !A))
+        return fail(MPCGEMM_ERR_ARG, "mpc_scalar: missing operand");
+    const int L = (prec + 63) / 64;
+    const mpc_cmat *a = A ? A : X, *y = Y ? Y : X;
+    const mpc_cmat *o = O ? O : X;
+    CK(mp_scalar_launch(L, op, cnt, prec, dmo(a->re), dmo(a->im), dmo(X->re), dmo(X->im), dmo(y->re), dmo(y->im),
+                        dmo(o->re), dmo(o->im), kv, (cudaStream_t)stream));
+    return 0;
 }
 
 int mpcgemm_version(void) { return 100; }

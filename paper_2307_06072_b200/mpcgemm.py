@@ -23,7 +23,7 @@ ERRORS = {0: "OK", -1: "ERR_ARG", -2: "ERR_PREC", -3: "ERR_EXP_RANGE", -4: "ERR_
           -5: "ERR_ALIAS", -6: "ERR_NOMEM", -7: "ERR_CUDA", -8: "ERR_SLICES"}
 SYMBOLS = ["mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_rho_bounds", "mpcgemm_slices_for",
            "mpcgemm_workspace_size", "mpcgemm_strerror", "mpcgemm_last_error", "mpcgemm_release",
-           "mpcgemm_version"]
+           "mpcgemm_version", "mpclu_factor", "mpclu_solve", "mpc_scalar"]
 
 
 class MpcgemmError(RuntimeError):
@@ -57,6 +57,12 @@ class ReportC(ctypes.Structure):
                 ("ms_gemm", ctypes.c_float), ("ms_fold", ctypes.c_float), ("slices_min", ctypes.c_int32)]
 
 
+class LuReportC(ctypes.Structure):
+    _fields_ = [("info", ctypes.c_int32), ("gemm_calls", ctypes.c_int32), ("slices_max", ctypes.c_int32),
+                ("kernel_launches", ctypes.c_int32), ("ms_panel", ctypes.c_float), ("ms_trsm", ctypes.c_float),
+                ("ms_gemm", ctypes.c_float)]
+
+
 def lib():
     """Load libmpcgemm.so (built by __graft_entry__.build()); raises if absent."""
     global _lib
@@ -78,7 +84,11 @@ def lib():
             L.mpcgemm_strerror.restype = ctypes.c_char_p
             L.mpcgemm_last_error.restype = ctypes.c_char_p
             L.mpcgemm_release.restype = None
-            for name in ("mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_rho_bounds", "mpcgemm_slices_for", "mpcgemm_version"):
+            L.mpclu_factor.argtypes = [i64, i32, PC, vp, i32, ctypes.c_int, ctypes.POINTER(OptsC), ctypes.POINTER(LuReportC)]
+            L.mpclu_solve.argtypes = [i64, i64, i32, PC, vp, PC, ctypes.POINTER(OptsC)]
+            L.mpc_scalar.argtypes = [i32, i64, i32, PC, PC, PC, PC, vp, vp]
+            for name in ("mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_rho_bounds", "mpcgemm_slices_for", "mpcgemm_version",
+                         "mpclu_factor", "mpclu_solve", "mpc_scalar"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -267,3 +277,55 @@ def mpcgemm_version() -> int:
 
 def mpcgemm_strerror(code: int) -> str:
     return lib().mpcgemm_strerror(code).decode()
+
+
+# ------------------------------------------------------------------ NEXT-3: complex LU
+def mpclu_factor(A: DevCMat, K: int, method="3M", prec: int | None = None, stream=None, timing: int = 0,
+                 adaptive: int = 0, ipiv=None):
+    """In-place blocked complex LU of the n x n device matrix A (mpclu_factor).  Returns
+    (ipiv torch int64 tensor, report dict)."""
+    torch = _torch()
+    prec = A.prec if prec is None else prec
+    n = A.shape[0]
+    if A.shape != (n, n):
+        raise MpcgemmError(-1, f"A must be square, got {A.shape}")
+    if ipiv is None:
+        ipiv = torch.empty(max(n, 1), dtype=torch.int64, device=A.re.sign.device)
+    opts = OptsC(_stream_ptr(stream), 0, 0, None, 0, timing, 0, 0, 0, adaptive, None)
+    rep = LuReportC()
+    a = A.c()
+    _check(lib().mpclu_factor(n, prec, ctypes.byref(a), ipiv.data_ptr(), K, METHODS[method], ctypes.byref(opts),
+                              ctypes.byref(rep)))
+    return ipiv[:n], {f: getattr(rep, f) for f, _ in LuReportC._fields_}
+
+
+def mpclu_solve(F: DevCMat, ipiv, B: DevCMat, prec: int | None = None, stream=None):
+    """B := A^-1 B in place with the factors of mpclu_factor (Eq. 7)."""
+    prec = F.prec if prec is None else prec
+    n = F.shape[0]
+    if B.shape[0] != n:
+        raise MpcgemmError(-1, f"B has {B.shape[0]} rows, LU is {n} x {n}")
+    opts = OptsC(_stream_ptr(stream), 0, 0, None, 0, 0, 0, 0, 0, 0, None)
+    f, b = F.c(), B.c()
+    _check(lib().mpclu_solve(n, B.shape[1], prec, ctypes.byref(f), ipiv.data_ptr(), ctypes.byref(b), ctypes.byref(opts)))
+
+
+def mpc_scalar(op: str, X: DevCMat, Y: DevCMat | None = None, A: DevCMat | None = None, prec: int | None = None,
+               stream=None):
+    """Elementwise device MP scalar ops on 1 x cnt matrices: "mul", "fms" (A - X Y), "recip",
+    "key" (returns a torch int64 [cnt, 2] tensor of (e, v bits))."""
+    torch = _torch()
+    prec = X.prec if prec is None else prec
+    cnt = X.shape[1]
+    opn = {"mul": 0, "fms": 1, "recip": 2, "key": 3}[op]
+    dev = X.re.sign.device
+    O = empty_device(1, cnt, prec, device=dev) if op != "key" else None
+    kv = torch.zeros((max(cnt, 1), 2), dtype=torch.int64, device=dev) if op == "key" else None
+    x = X.c()
+    y = Y.c() if Y is not None else None
+    a = A.c() if A is not None else None
+    o = O.c() if O is not None else None
+    _check(lib().mpc_scalar(opn, cnt, prec, ctypes.byref(a) if a else None, ctypes.byref(x),
+                            ctypes.byref(y) if y else None, ctypes.byref(o) if o else None,
+                            kv.data_ptr() if kv is not None else None, _stream_ptr(stream)))
+    return kv[:cnt] if op == "key" else O
