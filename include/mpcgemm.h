@@ -184,7 +184,8 @@ int mpclu_factor(int64_t n, int32_t prec, mpc_cmat *A, int64_t *ipiv, int32_t K,
 /* Eq. 7: B (n x nrhs, ld >= nrhs, DEVICE) := A^-1 B with the factors of mpclu_factor: the row
  * swaps ipiv[0..n) in order; forward B_r := cfms(B_r, L_rc, B_c) (r > c, c ascending);
  * backward B_c := cmul(B_c, crecip(U_cc)), then B_r := cfms(B_r, U_rc, B_c) (r < c, c
- * descending).  One CTA; stream-ordered.  A zero U_cc gives a zero B_c. */
+ * descending).  2 n + 3 launches (one per substitution step, the reciprocals 1/U_cc all at
+ * once first); stream-ordered.  A zero U_cc gives a zero solution row (no error). */
 int mpclu_solve(int64_t n, int64_t nrhs, int32_t prec, const mpc_cmat *LU, const int64_t *ipiv, mpc_cmat *B,
                 const mpcgemm_opts *opts);
 

@@ -111,62 +111,90 @@ __global__ void __launch_bounds__(128) lu_update_kernel(int L, DMatOut re, DMatO
     }
 }
 
-// ---------------------------------------------------------------- Eq. 7 solve (one CTA)
-// B (n x nrhs) := U^-1 L^-1 P B, with the factors of the LU above
-__global__ void __launch_bounds__(256) lu_solve_kernel(int L, DMatOut fre, DMatOut fim, int64_t n, const int64_t *ipiv,
-                                                       DMatOut bre, DMatOut bim, int64_t nrhs, int prec,
-                                                       uint8_t *rs, int64_t *rexp, uint64_t *rl)
+// ---------------------------------------------------------------- Eq. 7 solve
+// B (n x nrhs) := U^-1 L^-1 P B with the factors above, one launch per substitution step:
+//   all reciprocals 1 / U_cc at once (they do not depend on B); the row swaps in order;
+//   forward  c = 0..n-2:  B_rq := cfms(B_rq, L_rc, B_cq)                     (r > c)
+//   backward c = n-1..0:  x = cmul(B_cq, 1/U_cc); X_cq := x; B_rq := cfms(B_rq, U_rc, x) (r < c)
+//   (every thread of step c recomputes x from the unchanged B_cq; X holds the solution rows,
+//   copied back to B at the end)
+__global__ void lu_recip_all_kernel(int L, DMatOut fre, DMatOut fim, int64_t n, int prec, DMatOut rre, DMatOut rim)
 {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int64_t q = tid; q < nrhs; q += nt)                 // row swaps, in order
-        for (int64_t c = 0; c < n; c++) {
-            const int64_t p = ipiv[c];
-            if (p == c) continue;
-            for (int part = 0; part < 2; part++) {
-                const DMatOut &M = part ? bim : bre;
-                El a = el(L, M, c, q), b = el(L, M, p, q);
-                const uint8_t ts = *a.s; *a.s = *b.s; *b.s = ts;
-                const int64_t te = *a.e; *a.e = *b.e; *b.e = te;
-                for (int w = 0; w < L; w++) { const uint64_t x = a.l[w]; a.l[w] = b.l[w]; b.l[w] = x; }
-            }
-        }
-    __syncthreads();
-    for (int64_t c = 0; c < n; c++) {                         // forward: unit lower L
-        const int64_t cnt = (n - c - 1) * nrhs;
-        for (int64_t x = tid; x < cnt; x += nt) {
-            const int64_t r = c + 1 + x / nrhs, q = x % nrhs;
-            const Num lr = ld(L, el(L, fre, r, c)), li = ld(L, el(L, fim, r, c));
-            const Num yr = ld(L, el(L, bre, c, q)), yi = ld(L, el(L, bim, c, q));
-            const El a = el(L, bre, r, q), b = el(L, bim, r, q);
-            const Num ar = ld(L, a), ai = ld(L, b);
-            cfms(L, &ar, &ai, lr, li, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
-        }
-        __syncthreads();
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    const Num zr = ld(L, el(L, fre, c, c)), zi = ld(L, el(L, fim, c, c));
+    const El o1 = el(L, rre, 0, c), o2 = el(L, rim, 0, c);
+    if (zr.zero && zi.zero) {
+        *o1.s = *o2.s = 0; *o1.e = *o2.e = 0;
+        for (int q = 0; q < L; q++) o1.l[q] = o2.l[q] = 0;
+        return;
     }
-    for (int64_t c = n - 1; c >= 0; c--) {                    // backward: U
-        if (tid == 0) {
-            const Num zr = ld(L, el(L, fre, c, c)), zi = ld(L, el(L, fim, c, c));
-            if (zr.zero && zi.zero) { rs[0] = rs[1] = 0; rexp[0] = rexp[1] = 0; for (int w = 0; w < 2 * L; w++) rl[w] = 0; }
-            else crecip(L, zr, zi, prec, rs, rexp, rl, rs + 1, rexp + 1, rl + L);
+    crecip(L, zr, zi, prec, o1.s, o1.e, o1.l, o2.s, o2.e, o2.l);
+}
+
+__global__ void lu_bswap_kernel(int L, DMatOut bre, DMatOut bim, int64_t n, int64_t nrhs, const int64_t *ipiv)
+{
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nrhs) return;
+    for (int64_t c = 0; c < n; c++) {
+        const int64_t p = ipiv[c];
+        if (p == c) continue;
+        for (int part = 0; part < 2; part++) {
+            const DMatOut &M = part ? bim : bre;
+            El a = el(L, M, c, q), b = el(L, M, p, q);
+            const uint8_t ts = *a.s; *a.s = *b.s; *b.s = ts;
+            const int64_t te = *a.e; *a.e = *b.e; *b.e = te;
+            for (int w = 0; w < L; w++) { const uint64_t x = a.l[w]; a.l[w] = b.l[w]; b.l[w] = x; }
         }
-        __syncthreads();
-        for (int64_t q = tid; q < nrhs; q += nt) {
-            const Num yr = load(L, rs, rexp, rl), yi = load(L, rs + 1, rexp + 1, rl + L);
-            const El a = el(L, bre, c, q), b = el(L, bim, c, q);
-            const Num xr = ld(L, a), xi = ld(L, b);
-            cfms(L, nullptr, nullptr, xr, xi, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
-        }
-        __syncthreads();
-        const int64_t cnt = c * nrhs;
-        for (int64_t x = tid; x < cnt; x += nt) {
-            const int64_t r = x / nrhs, q = x % nrhs;
-            const Num ur = ld(L, el(L, fre, r, c)), ui = ld(L, el(L, fim, r, c));
-            const Num yr = ld(L, el(L, bre, c, q)), yi = ld(L, el(L, bim, c, q));
-            const El a = el(L, bre, r, q), b = el(L, bim, r, q);
-            const Num ar = ld(L, a), ai = ld(L, b);
-            cfms(L, &ar, &ai, ur, ui, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
-        }
-        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(128) lu_fwd_kernel(int L, DMatOut fre, DMatOut fim, DMatOut bre, DMatOut bim,
+                                                     int64_t c, int64_t n, int64_t nrhs, int prec)
+{
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= (n - c - 1) * nrhs) return;
+    const int64_t r = c + 1 + x / nrhs, q = x % nrhs;
+    const Num lr = ld(L, el(L, fre, r, c)), li = ld(L, el(L, fim, r, c));
+    const Num yr = ld(L, el(L, bre, c, q)), yi = ld(L, el(L, bim, c, q));
+    const El a = el(L, bre, r, q), b = el(L, bim, r, q);
+    const Num ar = ld(L, a), ai = ld(L, b);
+    cfms(L, &ar, &ai, lr, li, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+}
+
+__global__ void __launch_bounds__(128) lu_bwd_kernel(int L, DMatOut fre, DMatOut fim, DMatOut bre, DMatOut bim,
+                                                     DMatOut xre, DMatOut xim, DMatOut rre, DMatOut rim,
+                                                     int64_t c, int64_t nrhs, int prec)
+{
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= (c + 1) * nrhs) return;
+    const int64_t r = x / nrhs, q = x % nrhs;
+    const Num yr = ld(L, el(L, bre, c, q)), yi = ld(L, el(L, bim, c, q));
+    const Num wr = ld(L, el(L, rre, 0, c)), wi = ld(L, el(L, rim, 0, c));
+    uint8_t s2[2]; int64_t e2[2]; uint64_t l2[2][kLMax];
+    cfms(L, nullptr, nullptr, yr, yi, wr, wi, prec, &s2[0], &e2[0], l2[0], &s2[1], &e2[1], l2[1]);
+    if (r == c) {
+        const El o1 = el(L, xre, c, q), o2 = el(L, xim, c, q);
+        *o1.s = s2[0]; *o1.e = e2[0]; *o2.s = s2[1]; *o2.e = e2[1];
+        for (int w = 0; w < L; w++) { o1.l[w] = l2[0][w]; o2.l[w] = l2[1][w]; }
+        return;
+    }
+    const Num vr = load(L, &s2[0], &e2[0], l2[0]), vi = load(L, &s2[1], &e2[1], l2[1]);
+    const Num ur = ld(L, el(L, fre, r, c)), ui = ld(L, el(L, fim, r, c));
+    const El a = el(L, bre, r, q), b = el(L, bim, r, q);
+    const Num ar = ld(L, a), ai = ld(L, b);
+    cfms(L, &ar, &ai, ur, ui, vr, vi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+}
+
+__global__ void lu_copy_kernel(int L, DMatOut xre, DMatOut xim, DMatOut bre, DMatOut bim, int64_t n, int64_t nrhs)
+{
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n * nrhs) return;
+    const int64_t r = x / nrhs, q = x % nrhs;
+    for (int part = 0; part < 2; part++) {
+        const El s_ = el(L, part ? xim : xre, r, q), d = el(L, part ? bim : bre, r, q);
+        *d.s = *s_.s; *d.e = *s_.e;
+        for (int w = 0; w < L; w++) d.l[w] = s_.l[w];
     }
 }
 
@@ -240,9 +268,16 @@ cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t 
 }
 
 cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const int64_t *ipiv, DMatOut bre, DMatOut bim,
-                            int64_t nrhs, int prec, LuScratch s, cudaStream_t st) {
+                            int64_t nrhs, int prec, SolveScratch s, cudaStream_t st) {
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    lu_solve_kernel<<<1, 256, 0, st>>>(L, fre, fim, n, ipiv, bre, bim, nrhs, prec, s.sign, s.exp, s.limbs);
+    lu_recip_all_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(L, fre, fim, n, prec, s.rre, s.rim);
+    lu_bswap_kernel<<<(unsigned)((nrhs + 127) / 128), 128, 0, st>>>(L, bre, bim, n, nrhs, ipiv);
+    for (int64_t c = 0; c + 1 < n; c++)
+        lu_fwd_kernel<<<(unsigned)(((n - c - 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, c, n, nrhs, prec);
+    for (int64_t c = n - 1; c >= 0; c--)
+        lu_bwd_kernel<<<(unsigned)(((c + 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, s.xre, s.xim,
+                                                                             s.rre, s.rim, c, nrhs, prec);
+    lu_copy_kernel<<<(unsigned)((n * nrhs + 127) / 128), 128, 0, st>>>(L, s.xre, s.xim, bre, bim, n, nrhs);
     return cudaGetLastError();
 }
 

@@ -47,6 +47,7 @@ struct DevCache {
     void *meta = nullptr; size_t meta_bytes = 0;
     void *stage = nullptr; size_t stage_bytes = 0;   // mpcgemm_host device staging
     void *lu = nullptr; size_t lu_bytes = 0;         // NEXT-3 LU scratch (1 / pivot, info)
+    void *solve = nullptr; size_t solve_bytes = 0;   // NEXT-3 solve scratch (1 / U_cc, X)
 };
 std::mutex g_mu;
 std::map<int, DevCache> g_cache;
@@ -966,6 +967,7 @@ void mpcgemm_release(void) {
     auto it = g_cache.find(dev);
     if (it != g_cache.end()) {
         cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage); cudaFree(it->second.lu);
+        cudaFree(it->second.solve);
         g_cache.erase(it);
     }
     for (auto p = g_plans.begin(); p != g_plans.end();) {
@@ -991,8 +993,26 @@ int mpclu_solve(int64_t n, int64_t nrhs, int32_t prec, const mpc_cmat *LU, const
     cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    LuScratch sc; int32_t *info;
-    if (int rc = lu_scratch(dev, L, &sc, &info)) return rc;
+    // scratch: 1 x n reciprocals and the n x nrhs solution, both parts (ABI element format)
+    const size_t ents = (size_t)n + (size_t)n * nrhs;
+    uint8_t *base;
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        DevCache &dc = g_cache[dev];
+        if (int rc = grow(&dc.solve, &dc.solve_bytes, 2 * ents * (9 + 8 * (size_t)L) + 4096)) return rc;
+        base = (uint8_t *)dc.solve;
+    }
+    auto carve = [&](size_t cnt, int64_t ldm) {
+        DMatOut M;
+        M.limbs = (uint64_t *)base; base += align_up(cnt * 8 * L, 256);
+        M.exp = (int64_t *)base; base += align_up(cnt * 8, 256);
+        M.sign = base; base += align_up(cnt, 256);
+        M.ld = ldm;
+        return M;
+    };
+    SolveScratch sc;
+    sc.rre = carve(n, n); sc.rim = carve(n, n);
+    sc.xre = carve((size_t)n * nrhs, nrhs); sc.xim = carve((size_t)n * nrhs, nrhs);
     CK(lu_solve_launch(L, dmo(LU->re), dmo(LU->im), n, ipiv, dmo(B->re), dmo(B->im), nrhs, prec, sc, st));
     return 0;
 }
