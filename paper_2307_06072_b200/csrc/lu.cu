@@ -20,7 +20,8 @@ MPC_DEV El el(int L, const DMatOut &M, int64_t r, int64_t c) {
     const int64_t i = r * M.ld + c;
     return El{M.sign + i, M.exp + i, M.limbs + i * L};
 }
-MPC_DEV Num ld(int L, const El &x) { return load(L, x.s, x.e, x.l); }
+template <int C>
+MPC_DEV Num<C> ld(int L, const El &x) { return load<C>(L, x.s, x.e, x.l); }
 
 // ---------------------------------------------------------------- pivot search (one CTA)
 __global__ void __launch_bounds__(1024) lu_pivot_kernel(int L, DMatOut re, DMatOut im, int64_t n, int64_t c, int64_t *ipiv)
@@ -67,47 +68,71 @@ __global__ void lu_swap_kernel(int L, DMatOut re, DMatOut im, int64_t ncols, int
     }
 }
 
+// Every MP-arithmetic kernel below gives the two real parts of a complex result to the two
+// lanes of a lane pair (part = lane & 1): each lane computes one exactly rounded part
+// (cfms_part / crecip_part), halving the per-element latency chain.
+
 // ---------------------------------------------------------------- reciprocal of the pivot
 // scratch: sign[2], exp[2], limbs[2][L] (re, im of 1 / A_cc); *info = c + 1 on the first zero
+template <int C>
 __global__ void lu_recip_kernel(int L, DMatOut re, DMatOut im, int64_t c, int prec, uint8_t *rs, int64_t *rexp,
                                 uint64_t *rl, int32_t *info)
 {
-    if (threadIdx.x || blockIdx.x) return;
-    const Num zr = ld(L, el(L, re, c, c)), zi = ld(L, el(L, im, c, c));
+    const int part = threadIdx.x;
+    if (part > 1 || blockIdx.x) return;
+    const Num<C> zr = ld<C>(L, el(L, re, c, c)), zi = ld<C>(L, el(L, im, c, c));
     if (zr.zero && zi.zero) {
-        if (info && *info == 0) *info = (int32_t)(c + 1);
-        rs[0] = rs[1] = 0; rexp[0] = rexp[1] = 0;
-        for (int q = 0; q < 2 * L; q++) rl[q] = 0;
+        if (part == 0 && info && *info == 0) *info = (int32_t)(c + 1);
+        rs[part] = 0; rexp[part] = 0;
+        for (int q = 0; q < L; q++) rl[part * L + q] = 0;
         return;
     }
-    crecip(L, zr, zi, prec, rs, rexp, rl, rs + 1, rexp + 1, rl + L);
+    crecip_part<C>(L, part, zr, zi, prec, rs + part, rexp + part, rl + part * L);
+}
+
+// store one computed part (after both lanes of the pair have read their inputs)
+MPC_DEV void put_part(const El &o, uint8_t s_, int64_t e_, const uint64_t *l_, int L) {
+    *o.s = s_; *o.e = e_;
+    for (int q = 0; q < L; q++) o.l[q] = l_[q];
 }
 
 // ---------------------------------------------------------------- column scaling
-__global__ void lu_scale_kernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec,
-                                const uint8_t *rs, const int64_t *rexp, const uint64_t *rl)
+// A_rc := cmul(A_rc, 1 / A_cc) for r in [r0, r1)   (in place: the pair syncs before storing)
+template <int C>
+__global__ void __launch_bounds__(128) lu_scale_kernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c,
+                                                       int prec, const uint8_t *rs, const int64_t *rexp,
+                                                       const uint64_t *rl)
 {
-    const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= r1) return;
-    const Num yr = load(L, rs, rexp, rl), yi = load(L, rs + 1, rexp + 1, rl + L);
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int part = (int)(g & 1);
+    const int64_t r = r0 + (g >> 1);
+    if (r >= r1) return;                               // both lanes of a pair leave together
+    const Num<C> yr = load<C>(L, rs, rexp, rl), yi = load<C>(L, rs + 1, rexp + 1, rl + L);
     const El a = el(L, re, r, c), b = el(L, im, r, c);
-    const Num xr = ld(L, a), xi = ld(L, b);
-    cfms(L, nullptr, nullptr, xr, xi, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+    const Num<C> xr = ld<C>(L, a), xi = ld<C>(L, b);
+    uint8_t so; int64_t eo; uint64_t lo[C];
+    cfms_part<C>(L, part, nullptr, xr, xi, yr, yi, prec, &so, &eo, lo);
+    __syncwarp(3u << (threadIdx.x & 30));
+    put_part(part ? b : a, so, eo, lo, L);
 }
 
 // ---------------------------------------------------------------- rank-1 update
-// A_rt := cfms(A_rt, A_rc, A_ct) for r in [r0, r1), t in [t0, t1)
+// A_rt := cfms(A_rt, A_rc, A_ct) for r in [r0, r1), t in [t0, t1)  (lane pairs: the two parts)
+template <int C>
 __global__ void __launch_bounds__(128) lu_update_kernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0,
                                                         int64_t t1, int64_t c, int prec)
 {
-    const int64_t t = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int part = (int)(g & 1);
+    const int64_t t = t0 + (g >> 1);
     if (t >= t1) return;
-    const Num ur = ld(L, el(L, re, c, t)), ui = ld(L, el(L, im, c, t));
+    const Num<C> ur = ld<C>(L, el(L, re, c, t)), ui = ld<C>(L, el(L, im, c, t));
+    const DMatOut &T = part ? im : re;
     for (int64_t r = r0 + blockIdx.y; r < r1; r += gridDim.y) {
-        const Num lr = ld(L, el(L, re, r, c)), li = ld(L, el(L, im, r, c));
-        const El a = el(L, re, r, t), b = el(L, im, r, t);
-        const Num ar = ld(L, a), ai = ld(L, b);
-        cfms(L, &ar, &ai, lr, li, ur, ui, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+        const Num<C> lr = ld<C>(L, el(L, re, r, c)), li = ld<C>(L, el(L, im, r, c));
+        const El a = el(L, T, r, t);
+        const Num<C> av = ld<C>(L, a);
+        cfms_part<C>(L, part, &av, lr, li, ur, ui, prec, a.s, a.e, a.l);
     }
 }
 
@@ -118,18 +143,21 @@ __global__ void __launch_bounds__(128) lu_update_kernel(int L, DMatOut re, DMatO
 //   backward c = n-1..0:  x = cmul(B_cq, 1/U_cc); X_cq := x; B_rq := cfms(B_rq, U_rc, x) (r < c)
 //   (every thread of step c recomputes x from the unchanged B_cq; X holds the solution rows,
 //   copied back to B at the end)
+template <int C>
 __global__ void lu_recip_all_kernel(int L, DMatOut fre, DMatOut fim, int64_t n, int prec, DMatOut rre, DMatOut rim)
 {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int part = (int)(g & 1);
+    const int64_t c = g >> 1;
     if (c >= n) return;
-    const Num zr = ld(L, el(L, fre, c, c)), zi = ld(L, el(L, fim, c, c));
-    const El o1 = el(L, rre, 0, c), o2 = el(L, rim, 0, c);
+    const Num<C> zr = ld<C>(L, el(L, fre, c, c)), zi = ld<C>(L, el(L, fim, c, c));
+    const El o = el(L, part ? rim : rre, 0, c);
     if (zr.zero && zi.zero) {
-        *o1.s = *o2.s = 0; *o1.e = *o2.e = 0;
-        for (int q = 0; q < L; q++) o1.l[q] = o2.l[q] = 0;
+        *o.s = 0; *o.e = 0;
+        for (int q = 0; q < L; q++) o.l[q] = 0;
         return;
     }
-    crecip(L, zr, zi, prec, o1.s, o1.e, o1.l, o2.s, o2.e, o2.l);
+    crecip_part<C>(L, part, zr, zi, prec, o.s, o.e, o.l);
 }
 
 __global__ void lu_bswap_kernel(int L, DMatOut bre, DMatOut bim, int64_t n, int64_t nrhs, const int64_t *ipiv)
@@ -149,41 +177,57 @@ __global__ void lu_bswap_kernel(int L, DMatOut bre, DMatOut bim, int64_t n, int6
     }
 }
 
+template <int C>
 __global__ void __launch_bounds__(128) lu_fwd_kernel(int L, DMatOut fre, DMatOut fim, DMatOut bre, DMatOut bim,
                                                      int64_t c, int64_t n, int64_t nrhs, int prec)
 {
-    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int part = (int)(g & 1);
+    const int64_t x = g >> 1;
     if (x >= (n - c - 1) * nrhs) return;
     const int64_t r = c + 1 + x / nrhs, q = x % nrhs;
-    const Num lr = ld(L, el(L, fre, r, c)), li = ld(L, el(L, fim, r, c));
-    const Num yr = ld(L, el(L, bre, c, q)), yi = ld(L, el(L, bim, c, q));
-    const El a = el(L, bre, r, q), b = el(L, bim, r, q);
-    const Num ar = ld(L, a), ai = ld(L, b);
-    cfms(L, &ar, &ai, lr, li, yr, yi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+    const Num<C> lr = ld<C>(L, el(L, fre, r, c)), li = ld<C>(L, el(L, fim, r, c));
+    const Num<C> yr = ld<C>(L, el(L, bre, c, q)), yi = ld<C>(L, el(L, bim, c, q));
+    const El a = el(L, part ? bim : bre, r, q);
+    const Num<C> av = ld<C>(L, a);
+    cfms_part<C>(L, part, &av, lr, li, yr, yi, prec, a.s, a.e, a.l);
 }
 
+// x = cmul(B_cq, 1/U_cc): each lane of the pair computes one part and they swap parts by shuffle
+template <int C>
 __global__ void __launch_bounds__(128) lu_bwd_kernel(int L, DMatOut fre, DMatOut fim, DMatOut bre, DMatOut bim,
                                                      DMatOut xre, DMatOut xim, DMatOut rre, DMatOut rim,
                                                      int64_t c, int64_t nrhs, int prec)
 {
-    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= (c + 1) * nrhs) return;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int part = (int)(g & 1);
+    const int64_t x = g >> 1;
+    if (x >= (c + 1) * nrhs) return;                   // pairs leave together
+    const unsigned pm = 3u << (threadIdx.x & 30);
     const int64_t r = x / nrhs, q = x % nrhs;
-    const Num yr = ld(L, el(L, bre, c, q)), yi = ld(L, el(L, bim, c, q));
-    const Num wr = ld(L, el(L, rre, 0, c)), wi = ld(L, el(L, rim, 0, c));
-    uint8_t s2[2]; int64_t e2[2]; uint64_t l2[2][kLMax];
-    cfms(L, nullptr, nullptr, yr, yi, wr, wi, prec, &s2[0], &e2[0], l2[0], &s2[1], &e2[1], l2[1]);
+    const Num<C> yr = ld<C>(L, el(L, bre, c, q)), yi = ld<C>(L, el(L, bim, c, q));
+    const Num<C> wr = ld<C>(L, el(L, rre, 0, c)), wi = ld<C>(L, el(L, rim, 0, c));
+    uint8_t s2[2]; int64_t e2[2]; uint64_t l2[2][C];
+    cfms_part<C>(L, part, nullptr, yr, yi, wr, wi, prec, &s2[part], &e2[part], l2[part]);
+    // exchange: the other part arrives from the partner lane
+    const int o = part ^ 1;
+    s2[o] = (uint8_t)__shfl_xor_sync(pm, (int)s2[part], 1);
+    e2[o] = __shfl_xor_sync(pm, e2[part], 1);
+#pragma unroll
+    for (int w = 0; w < C; w++) {
+        const uint64_t mine = w < L ? l2[part][w] : 0ull;
+        const uint64_t other = __shfl_xor_sync(pm, mine, 1);
+        if (w < L) l2[o][w] = other;
+    }
     if (r == c) {
-        const El o1 = el(L, xre, c, q), o2 = el(L, xim, c, q);
-        *o1.s = s2[0]; *o1.e = e2[0]; *o2.s = s2[1]; *o2.e = e2[1];
-        for (int w = 0; w < L; w++) { o1.l[w] = l2[0][w]; o2.l[w] = l2[1][w]; }
+        put_part(el(L, part ? xim : xre, c, q), s2[part], e2[part], l2[part], L);
         return;
     }
-    const Num vr = load(L, &s2[0], &e2[0], l2[0]), vi = load(L, &s2[1], &e2[1], l2[1]);
-    const Num ur = ld(L, el(L, fre, r, c)), ui = ld(L, el(L, fim, r, c));
-    const El a = el(L, bre, r, q), b = el(L, bim, r, q);
-    const Num ar = ld(L, a), ai = ld(L, b);
-    cfms(L, &ar, &ai, ur, ui, vr, vi, prec, a.s, a.e, a.l, b.s, b.e, b.l);
+    const Num<C> vr = load<C>(L, &s2[0], &e2[0], l2[0]), vi = load<C>(L, &s2[1], &e2[1], l2[1]);
+    const Num<C> ur = ld<C>(L, el(L, fre, r, c)), ui = ld<C>(L, el(L, fim, r, c));
+    const El a = el(L, part ? bim : bre, r, q);
+    const Num<C> av = ld<C>(L, a);
+    cfms_part<C>(L, part, &av, ur, ui, vr, vi, prec, a.s, a.e, a.l);
 }
 
 __global__ void lu_copy_kernel(int L, DMatOut xre, DMatOut xim, DMatOut bre, DMatOut bim, int64_t n, int64_t nrhs)
@@ -200,28 +244,40 @@ __global__ void lu_copy_kernel(int L, DMatOut xre, DMatOut xim, DMatOut bre, DMa
 
 // ---------------------------------------------------------------- elementwise (tests)
 // op 0: O = X Y ; 1: O = A - X Y ; 2: O = 1 / X ; 3: key of X -> kv[2t] = e, kv[2t+1] = v bits
+template <int C>
 __global__ void mp_scalar_kernel(int L, int op, int64_t cnt, int prec, DMatOut Ar, DMatOut Ai, DMatOut Xr, DMatOut Xi,
                                  DMatOut Yr, DMatOut Yi, DMatOut Or, DMatOut Oi, int64_t *kv)
 {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int part = (int)(g & 1);
+    const int64_t t = g >> 1;
     if (t >= cnt) return;
     const El xr = el(L, Xr, 0, t), xi = el(L, Xi, 0, t);
     if (op == 3) {
+        if (part) return;
         const Key k = pivot_key(xr.s, xr.e, xr.l, xi.s, xi.e, xi.l, L);
         kv[2 * t] = k.e;
         kv[2 * t + 1] = __double_as_longlong(k.v);
         return;
     }
-    const El o1 = el(L, Or, 0, t), o2 = el(L, Oi, 0, t);
-    const Num x1 = ld(L, xr), x2 = ld(L, xi);
-    if (op == 2) { crecip(L, x1, x2, prec, o1.s, o1.e, o1.l, o2.s, o2.e, o2.l); return; }
-    const Num y1 = ld(L, el(L, Yr, 0, t)), y2 = ld(L, el(L, Yi, 0, t));
-    if (op == 0) { cfms(L, nullptr, nullptr, x1, x2, y1, y2, prec, o1.s, o1.e, o1.l, o2.s, o2.e, o2.l); return; }
-    const Num a1 = ld(L, el(L, Ar, 0, t)), a2 = ld(L, el(L, Ai, 0, t));
-    cfms(L, &a1, &a2, x1, x2, y1, y2, prec, o1.s, o1.e, o1.l, o2.s, o2.e, o2.l);
+    const El o = el(L, part ? Oi : Or, 0, t);
+    const Num<C> x1 = ld<C>(L, xr), x2 = ld<C>(L, xi);
+    if (op == 2) { crecip_part<C>(L, part, x1, x2, prec, o.s, o.e, o.l); return; }
+    const Num<C> y1 = ld<C>(L, el(L, Yr, 0, t)), y2 = ld<C>(L, el(L, Yi, 0, t));
+    if (op == 0) { cfms_part<C>(L, part, nullptr, x1, x2, y1, y2, prec, o.s, o.e, o.l); return; }
+    const Num<C> av = ld<C>(L, el(L, part ? Ai : Ar, 0, t));
+    cfms_part<C>(L, part, &av, x1, x2, y1, y2, prec, o.s, o.e, o.l);
 }
 
 // ---------------------------------------------------------------- launchers (L dispatch)
+// capacity instantiation for L limbs: 4, 8 or 16
+#define MPC_DISPATCH_C(L, KERNEL_CALL)                        \
+    do {                                                      \
+        if ((L) <= 4) { constexpr int C = 4; KERNEL_CALL; }   \
+        else if ((L) <= 8) { constexpr int C = 8; KERNEL_CALL; } \
+        else { constexpr int C = 16; KERNEL_CALL; }           \
+    } while (0)
+
 cudaError_t lu_pivot_launch(int L, DMatOut re, DMatOut im, int64_t n, int64_t c, int64_t *ipiv, cudaStream_t st) {
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
     lu_pivot_kernel<<<1, 1024, 0, st>>>(L, re, im, n, c, ipiv);
@@ -238,16 +294,16 @@ cudaError_t lu_swap_launch(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t
 cudaError_t lu_recip_launch(int L, DMatOut re, DMatOut im, int64_t c, int prec, LuScratch s, int32_t *info,
                             cudaStream_t st) {
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    lu_recip_kernel<<<1, 32, 0, st>>>(L, re, im, c, prec, s.sign, s.exp, s.limbs, info);
+    MPC_DISPATCH_C(L, (lu_recip_kernel<C><<<1, 2, 0, st>>>(L, re, im, c, prec, s.sign, s.exp, s.limbs, info)));
     return cudaGetLastError();
 }
 
 cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec, LuScratch s,
                             cudaStream_t st) {
     if (r1 <= r0) return cudaSuccess;
-    const unsigned g = (unsigned)((r1 - r0 + 127) / 128);
+    const unsigned g = (unsigned)((2 * (r1 - r0) + 127) / 128);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    lu_scale_kernel<<<g, 128, 0, st>>>(L, re, im, r0, r1, c, prec, s.sign, s.exp, s.limbs);
+    MPC_DISPATCH_C(L, (lu_scale_kernel<C><<<g, 128, 0, st>>>(L, re, im, r0, r1, c, prec, s.sign, s.exp, s.limbs)));
     return cudaGetLastError();
 }
 
@@ -255,7 +311,7 @@ cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t 
                              int prec, cudaStream_t st) {
     if (r1 <= r0 || t1 <= t0) return cudaSuccess;
     const int64_t rows = r1 - r0;
-    const int64_t gx = (t1 - t0 + 127) / 128;
+    const int64_t gx = (2 * (t1 - t0) + 127) / 128;
     int64_t gy = rows;
     const int64_t want = 148 * 16;                            // ~16 CTAs of 128 threads per SM
     if (gx * gy > want) gy = (want + gx - 1) / gx;
@@ -263,20 +319,20 @@ cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t 
     if (gy > 65535) gy = 65535;
     dim3 grid((unsigned)gx, (unsigned)gy);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    lu_update_kernel<<<grid, 128, 0, st>>>(L, re, im, r0, r1, t0, t1, c, prec);
+    MPC_DISPATCH_C(L, (lu_update_kernel<C><<<grid, 128, 0, st>>>(L, re, im, r0, r1, t0, t1, c, prec)));
     return cudaGetLastError();
 }
 
 cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const int64_t *ipiv, DMatOut bre, DMatOut bim,
                             int64_t nrhs, int prec, SolveScratch s, cudaStream_t st) {
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    lu_recip_all_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(L, fre, fim, n, prec, s.rre, s.rim);
+    MPC_DISPATCH_C(L, (lu_recip_all_kernel<C><<<(unsigned)((2 * n + 127) / 128), 128, 0, st>>>(L, fre, fim, n, prec, s.rre, s.rim)));
     lu_bswap_kernel<<<(unsigned)((nrhs + 127) / 128), 128, 0, st>>>(L, bre, bim, n, nrhs, ipiv);
     for (int64_t c = 0; c + 1 < n; c++)
-        lu_fwd_kernel<<<(unsigned)(((n - c - 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, c, n, nrhs, prec);
+        MPC_DISPATCH_C(L, (lu_fwd_kernel<C><<<(unsigned)((2 * (n - c - 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, c, n, nrhs, prec)));
     for (int64_t c = n - 1; c >= 0; c--)
-        lu_bwd_kernel<<<(unsigned)(((c + 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, s.xre, s.xim,
-                                                                             s.rre, s.rim, c, nrhs, prec);
+        MPC_DISPATCH_C(L, (lu_bwd_kernel<C><<<(unsigned)((2 * (c + 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, s.xre, s.xim,
+                                                                             s.rre, s.rim, c, nrhs, prec)));
     lu_copy_kernel<<<(unsigned)((n * nrhs + 127) / 128), 128, 0, st>>>(L, s.xre, s.xim, bre, bim, n, nrhs);
     return cudaGetLastError();
 }
@@ -284,9 +340,9 @@ cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const in
 cudaError_t mp_scalar_launch(int L, int op, int64_t cnt, int prec, DMatOut Ar, DMatOut Ai, DMatOut Xr, DMatOut Xi,
                              DMatOut Yr, DMatOut Yi, DMatOut Or, DMatOut Oi, int64_t *kv, cudaStream_t st) {
     if (cnt <= 0) return cudaSuccess;
-    const unsigned g = (unsigned)((cnt + 127) / 128);
+    const unsigned g = (unsigned)((2 * cnt + 127) / 128);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    mp_scalar_kernel<<<g, 128, 0, st>>>(L, op, cnt, prec, Ar, Ai, Xr, Xi, Yr, Yi, Or, Oi, kv);
+    MPC_DISPATCH_C(L, (mp_scalar_kernel<C><<<g, 128, 0, st>>>(L, op, cnt, prec, Ar, Ai, Xr, Xi, Yr, Yi, Or, Oi, kv)));
     return cudaGetLastError();
 }
 

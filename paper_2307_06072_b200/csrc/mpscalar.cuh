@@ -189,63 +189,109 @@ MPC_DEV void sum_round(Term *t, int cnt, int prec, int L, uint64_t *buf, int nw_
 
 constexpr int kLMax = 16;                        // prec <= 1024 for the LU path
 
-// one real MP element in local memory (L <= kLMax limbs used)
+// Capacity-templated element: L <= C limbs used.  The kernels are instantiated for C = 4, 8
+// and 16 (lu.cu) so that operands and product accumulators stay in registers (static indices
+// under unrolled loops guarded by q < L) and the per-thread stack stays small.
+template <int C>
 struct Num {
-    uint64_t m[kLMax];
+    uint64_t m[C];
     int64_t e;        // weight of m[0]'s bit 0: exp - 64 L
     bool neg, zero;
 };
 
-MPC_DEV Num load(int L, const uint8_t *s, const int64_t *e, const uint64_t *l) {
-    Num x;
+template <int C>
+MPC_DEV Num<C> load(int L, const uint8_t *s, const int64_t *e, const uint64_t *l) {
+    Num<C> x;
     bool nz = false;
-    for (int q = 0; q < L; q++) { x.m[q] = l[q]; nz = nz || x.m[q]; }
+#pragma unroll
+    for (int q = 0; q < C; q++) { x.m[q] = q < L ? l[q] : 0ull; nz = nz || x.m[q]; }
     x.zero = !nz;
     x.neg = nz && *s;
     x.e = *e - 64 * (int64_t)L;
     return x;
 }
 
-MPC_DEV Term term_of(int L, const Num &x, bool flip) {
-    if (x.zero) { Term t; t.m = x.m; t.n = L; t.lsb = 0; t.top = INT64_MIN; t.neg = false; return t; }
-    return make_term(x.m, L, x.e, x.neg != flip);
+// p[0..2L) = a b (product scanning: a 192-bit column accumulator in registers, one store per
+// limb of p)
+MPC_DEV void mul_ps(uint64_t *p, const uint64_t *a, const uint64_t *b, int L) {
+    uint64_t acc0 = 0, acc1 = 0, acc2 = 0;
+    for (int k = 0; k < 2 * L - 1; k++) {
+        const int i0 = k - (L - 1) > 0 ? k - (L - 1) : 0, i1 = k < L - 1 ? k : L - 1;
+        for (int i = i0; i <= i1; i++) {
+            const uint64_t x = a[i], y = b[k - i];
+            const uint64_t lo = x * y, hi = __umul64hi(x, y);
+            acc0 += lo;
+            const uint64_t h = hi + (acc0 < lo);          // hi <= 2^64 - 2: no overflow
+            acc1 += h;
+            acc2 += acc1 < h;
+        }
+        p[k] = acc0;
+        acc0 = acc1; acc1 = acc2; acc2 = 0;
+    }
+    p[2 * L - 1] = acc0;
 }
 
-// product term x y into p[0..2L)
-MPC_DEV Term prod_term(int L, const Num &x, const Num &y, bool flip, uint64_t *p) {
+template <int C>
+MPC_DEV Term prod_term(int L, const Num<C> &x, const Num<C> &y, bool flip, uint64_t *p) {
     Term t;
     if (x.zero || y.zero) { t.m = p; t.n = 2 * L; t.lsb = 0; t.top = INT64_MIN; t.neg = false; return t; }
-    mulmag(p, x.m, L, y.m, L);
+    mul_ps(p, x.m, y.m, L);
     return make_term(p, 2 * L, x.e + y.e, (x.neg != y.neg) != flip);
 }
 
-constexpr int kNW = 9 * kLMax + 6;               // sum_round scratch limbs
+template <int C>
+MPC_DEV Term term_of(int L, const Num<C> &x, uint64_t *pa) {
+#pragma unroll
+    for (int q = 0; q < C; q++) if (q < L) pa[q] = x.m[q];
+    if (x.zero) { Term t; t.m = pa; t.n = L; t.lsb = 0; t.top = INT64_MIN; t.neg = false; return t; }
+    return make_term(pa, L, x.e, x.neg);
+}
+
+template <int C> struct NW { static constexpr int v = 9 * C + 6; };   // sum_round scratch limbs
+
+// one part of a - x y (a == nullptr: x y):  part 0 = re: ar - xr yr + xi yi ;
+// part 1 = im: ai - xr yi - xi yr.  The kernels give each part its own thread.
+template <int C>
+MPC_DEV void cfms_part(int L, int part, const Num<C> *a, const Num<C> &xr, const Num<C> &xi,
+                       const Num<C> &yr, const Num<C> &yi, int prec, uint8_t *so, int64_t *eo, uint64_t *lo)
+{
+    uint64_t p1[2 * C], p2[2 * C], pa[C], buf[NW<C>::v];
+    Term t[3];
+    const bool sub = a != nullptr;
+    if (part == 0) { t[0] = prod_term<C>(L, xr, yr, sub, p1); t[1] = prod_term<C>(L, xi, yi, !sub, p2); }
+    else           { t[0] = prod_term<C>(L, xr, yi, sub, p1); t[1] = prod_term<C>(L, xi, yr, sub, p2); }
+    int cnt = 2;
+    if (sub) t[cnt++] = term_of<C>(L, *a, pa);
+    sum_round(t, cnt, prec, L, buf, NW<C>::v, so, eo, lo);
+}
 
 // (out_re, out_im) = a - x y   (a == nullptr: x y)
-MPC_DEV void cfms(int L, const Num *ar, const Num *ai, const Num &xr, const Num &xi,
-                  const Num &yr, const Num &yi, int prec,
+template <int C>
+MPC_DEV void cfms(int L, const Num<C> *ar, const Num<C> *ai, const Num<C> &xr, const Num<C> &xi,
+                  const Num<C> &yr, const Num<C> &yi, int prec,
                   uint8_t *s_re, int64_t *e_re, uint64_t *l_re, uint8_t *s_im, int64_t *e_im, uint64_t *l_im)
 {
-    uint64_t p1[2 * kLMax], p2[2 * kLMax], buf[kNW];
+    uint64_t p1[2 * C], p2[2 * C], pa[C], buf[NW<C>::v];
     Term t[3];
     const bool sub = ar != nullptr;              // a - (x y): the products enter negated
     // real part: ar - xr yr + xi yi
-    t[0] = prod_term(L, xr, yr, sub, p1);
-    t[1] = prod_term(L, xi, yi, !sub, p2);
+    t[0] = prod_term<C>(L, xr, yr, sub, p1);
+    t[1] = prod_term<C>(L, xi, yi, !sub, p2);
     int cnt = 2;
-    if (sub) t[cnt++] = term_of(L, *ar, false);
-    uint8_t s0; int64_t e0; uint64_t r0[kLMax];
-    sum_round(t, cnt, prec, L, buf, kNW, &s0, &e0, r0);
+    if (sub) t[cnt++] = term_of<C>(L, *ar, pa);
+    uint8_t s0; int64_t e0; uint64_t r0[C];
+    sum_round(t, cnt, prec, L, buf, NW<C>::v, &s0, &e0, r0);
     // imaginary part: ai - xr yi - xi yr
-    t[0] = prod_term(L, xr, yi, sub, p1);
-    t[1] = prod_term(L, xi, yr, sub, p2);
+    t[0] = prod_term<C>(L, xr, yi, sub, p1);
+    t[1] = prod_term<C>(L, xi, yr, sub, p2);
     cnt = 2;
-    if (sub) t[cnt++] = term_of(L, *ai, false);
-    uint8_t s1; int64_t e1; uint64_t r1[kLMax];
-    sum_round(t, cnt, prec, L, buf, kNW, &s1, &e1, r1);
+    if (sub) t[cnt++] = term_of<C>(L, *ai, pa);
+    uint8_t s1; int64_t e1; uint64_t r1[C];
+    sum_round(t, cnt, prec, L, buf, NW<C>::v, &s1, &e1, r1);
     *s_re = s0; *e_re = e0;
     *s_im = s1; *e_im = e1;
-    for (int q = 0; q < L; q++) { l_re[q] = r0[q]; l_im[q] = r1[q]; }
+#pragma unroll
+    for (int q = 0; q < C; q++) if (q < L) { l_re[q] = r0[q]; l_im[q] = r1[q]; }
 }
 
 // ---------------------------------------------------------------- division (reciprocal)
@@ -297,13 +343,12 @@ MPC_DEV bool divmod32(uint32_t *u, int m, const uint32_t *vin, int n, uint32_t *
 // RNE(num / D) to prec bits.  num = (-1)^nneg nm[0..nn) 2^ne ; D = dm[0..dn) 2^de (> 0), or, if
 // drop_tail, D = dm 2^de + delta with 0 < delta below the rounding reach (see crecip).
 // Scratch sizes: digits of (prec + 4 + 64 dn) + 64 bits.
-constexpr int kDMax = 5 * kLMax + 2;                         // D limbs
-constexpr int kUMax = 2 * (kLMax + 2) + 2 * kDMax + 4;       // dividend 32-bit digits
-
+template <int C>
 MPC_DEV void div_round(int L, const uint64_t *nm, int nn, int64_t ne, bool nneg, const uint64_t *dm, int dn, int64_t de,
                        bool drop_tail, int prec, uint8_t *so, int64_t *eo, uint64_t *lo)
 {
-    constexpr int DMAX = kDMax, UMAX = kUMax;
+    constexpr int DMAX = 5 * C + 2;                          // D limbs
+    constexpr int UMAX = 2 * (C + 2) + 2 * DMAX + 4;         // dividend 32-bit digits
     const int bn = bitlen(nm, nn);
     if (!bn) { *so = 0; *eo = 0; for (int l = 0; l < L; l++) lo[l] = 0; return; }
     const int bd = bitlen(dm, dn);
@@ -346,16 +391,19 @@ MPC_DEV void div_round(int L, const uint64_t *nm, int nn, int64_t ne, bool nneg,
     round_store(r, rn, ne - de - sh - 1, nneg, prec, L, so, eo, lo);
 }
 
-// (re, im) = 1 / (zr + i zi), z != 0
-MPC_DEV void crecip(int L, const Num &zr, const Num &zi, int prec,
-                    uint8_t *s_re, int64_t *e_re, uint64_t *l_re, uint8_t *s_im, int64_t *e_im, uint64_t *l_im)
+// one part of 1 / (zr + i zi) (part 0: zr / D, part 1: -zi / D), z != 0
+template <int C>
+MPC_DEV void crecip_part(int L, int part, const Num<C> &zr, const Num<C> &zi, int prec,
+                         uint8_t *so, int64_t *eo, uint64_t *lo)
 {
+    const Num<C> &num = part ? zi : zr;
+    if (num.zero) { *so = 0; *eo = 0; for (int q = 0; q < L; q++) lo[q] = 0; return; }
     const int DMAX = 5 * L + 2;
-    uint64_t sr[2 * kLMax], si[2 * kLMax], D[kDMax];
+    uint64_t sr[2 * C], si[2 * C], D[5 * C + 2], na[C];
     const bool hr = !zr.zero, hi = !zi.zero;
     int64_t tr = INT64_MIN, ti = INT64_MIN;
-    if (hr) { mulmag(sr, zr.m, L, zr.m, L); tr = 2 * zr.e + bitlen(sr, 2 * L); }
-    if (hi) { mulmag(si, zi.m, L, zi.m, L); ti = 2 * zi.e + bitlen(si, 2 * L); }
+    if (hr) { mul_ps(sr, zr.m, zr.m, L); tr = 2 * zr.e + bitlen(sr, 2 * L); }
+    if (hi) { mul_ps(si, zi.m, zi.m, L); ti = 2 * zi.e + bitlen(si, 2 * L); }
     // the larger square b, the smaller s
     const bool rb = tr >= ti;
     const uint64_t *Sb = rb ? sr : si, *Ss = rb ? si : sr;
@@ -366,7 +414,6 @@ MPC_DEV void crecip(int L, const Num &zr, const Num &zi, int prec,
     int64_t de;
     if (Ts == INT64_MIN) {                                   // one part is zero: D = Sb exactly
         for (int q = 0; q < 2 * L; q++) D[q] = Sb[q];
-        for (int q = 2 * L; q < DMAX; q++) D[q] = 0;
         dn = 2 * L; de = Eb;
     } else if (Tb - Ts > (int64_t)prec + 128 * L + 4) {      // Ss below the quotient's reach
         for (int q = 0; q < 2 * L; q++) D[q] = Sb[q];
@@ -379,10 +426,17 @@ MPC_DEV void crecip(int L, const Num &zr, const Num &zi, int prec,
         addsh(D, dn, Sb, 2 * L, Eb - de, false);
         addsh(D, dn, Ss, 2 * L, Es - de, false);
     }
-    if (hr) div_round(L, zr.m, L, zr.e, zr.neg, D, dn, de, drop, prec, s_re, e_re, l_re);
-    else { *s_re = 0; *e_re = 0; for (int q = 0; q < L; q++) l_re[q] = 0; }
-    if (hi) div_round(L, zi.m, L, zi.e, !zi.neg, D, dn, de, drop, prec, s_im, e_im, l_im);
-    else { *s_im = 0; *e_im = 0; for (int q = 0; q < L; q++) l_im[q] = 0; }
+    for (int q = 0; q < L; q++) na[q] = num.m[q];
+    div_round<C>(L, na, L, num.e, part ? !num.neg : num.neg, D, dn, de, drop, prec, so, eo, lo);
+}
+
+// (re, im) = 1 / (zr + i zi), z != 0
+template <int C>
+MPC_DEV void crecip(int L, const Num<C> &zr, const Num<C> &zi, int prec,
+                    uint8_t *s_re, int64_t *e_re, uint64_t *l_re, uint8_t *s_im, int64_t *e_im, uint64_t *l_im)
+{
+    crecip_part<C>(L, 0, zr, zi, prec, s_re, e_re, l_re);
+    crecip_part<C>(L, 1, zr, zi, prec, s_im, e_im, l_im);
 }
 
 // ---------------------------------------------------------------- pivot key
