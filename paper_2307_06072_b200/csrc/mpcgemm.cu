@@ -14,6 +14,7 @@
 #include <queue>
 #include <string>
 #include <tuple>
+#include <functional>
 #include <vector>
 
 #include "../../include/mpcgemm.h"
@@ -48,6 +49,8 @@ struct DevCache {
     void *stage = nullptr; size_t stage_bytes = 0;   // mpcgemm_host device staging
     void *lu = nullptr; size_t lu_bytes = 0;         // NEXT-3 LU scratch (1 / pivot, info)
     void *solve = nullptr; size_t solve_bytes = 0;   // NEXT-3 solve scratch (1 / U_cc, X)
+    cudaStream_t copy_stream = nullptr;              // mpcgemm_host: D2H of finished row groups
+    cudaEvent_t group_event = nullptr;
 };
 std::mutex g_mu;
 std::map<int, DevCache> g_cache;
@@ -546,67 +549,93 @@ size_t f64_main_bytes(int64_t m, int64_t n, int64_t k, int s, int method) {
            align_up((size_t)3 * (s + 2) * m * n * 8, 256);
 }
 
-// the device hot path with a known workspace
+mpc_cmat rows_of(const mpc_cmat &M, int64_t r0, int L) {
+    mpc_cmat v = M;
+    for (mpc_rmat *R : {&v.re, &v.im}) {
+        const int64_t o = r0 * R->ld;
+        R->sign += o; R->exp += o; R->limbs += o * L;
+    }
+    return v;
+}
+
+// row groups of the e2e path: the hook runs after group [r0, r1) of C is final (stream order)
+using GroupHook = std::function<int(int64_t, int64_t)>;
+
+// the device hot path with a known workspace.  group_rows > 0 (a multiple of 256): the rows of
+// A / C are processed in groups of that many rows (split A_g, slice GEMM, fold), B split once;
+// Lo must then be the layout of one group.
 int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
              mpc_cmat *C, int method, int s, cudaStream_t st, uint8_t *meta, uint8_t *big, const Layout &Lo,
              int simt, mpcgemm_report *rep, StageEvents *E, int beta, int alpha_neg,
-             const std::vector<int32_t> &sblk) {
+             const std::vector<int32_t> &sblk, int64_t group_rows = 0, const GroupHook *hook = nullptr) {
     const int L = (prec + 63) / 64;
     const MetaView mv = meta_view(meta, m, n);
     int64_t *eA = mv.eA, *eB = mv.eB;
     const int parts = method == 3 ? 3 : 2;
+    const int64_t mg = group_rows > 0 ? std::min(m, group_rows) : m;
     int8_t *digA = (int8_t *)big;
-    int8_t *digB = digA + align_up((size_t)parts * s * m * Lo.kp, 256);
+    int8_t *digB = digA + align_up((size_t)parts * s * mg * Lo.kp, 256);
     int32_t *partials = (int32_t *)((uint8_t *)digB + align_up((size_t)parts * s * n * Lo.kp, 256));
-    CK(split_launch(dm(A->re), dm(A->im), 0, m, k, Lo.kp, L, eA, s, parts, digA, st));
+    uint64_t *fix = (uint64_t *)((uint8_t *)partials);  // set below per plan
     CK(split_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, s, parts, digB, st));
-    if (E) CK(cudaEventRecord(E->ev[3], st));
-    const Geometry geo = main_geometry(dev, m, n, k, s, method);
-    const int BN = geo.BN;
-    PlanKey key{m, n, k, s, method, geo.BM, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0,
-                env_int("MPCGEMM_ORDER", 1), sblk};
-    Plan *plan;
-    if (int rc = build_plan(dev, key, &plan)) return rc;
-    SliceGemmLaunch SL;
-    memset(&SL, 0, sizeof(SL));
-    SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
-    SL.P.partials = partials; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
-    SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = s; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
-    SL.P.partsA = SL.P.partsB = parts;
-    for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
-    SL.digA = digA; SL.digB = digB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
-    SL.grid = plan->grid; SL.BM = geo.BM; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits;
-    SL.units_flat = plan->d_units;
-    CK(slicegemm_launch(SL, st));
-    if (E) CK(cudaEventRecord(E->ev[4], st));
-    FoldParams F;
-    F.partials = partials; F.nslots = plan->nslots; F.nstrips = Lo.nstrips; F.m = m; F.n = n;
-    F.s = s; F.method = method; F.prec = prec; F.L = L; F.slotinfo = plan->d_slotinfo;
-    F.eA = eA; F.eB = eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
-    F.beta = beta; F.alpha_neg = alpha_neg; F.C0re = dm(C->re); F.C0im = dm(C->im);
-    F.ldF = (n + 1) & ~1ll;
-    F.sblk = nullptr;
-    if (!sblk.empty()) {                               // NEXT-4: per-block triangles
-        CK(cudaMemcpyAsync(mv.sblk, sblk.data(), 4 * sblk.size(), cudaMemcpyHostToDevice, st));
-        F.sblk = mv.sblk;
+    if (!sblk.empty()) CK(cudaMemcpyAsync(mv.sblk, sblk.data(), 4 * sblk.size(), cudaMemcpyHostToDevice, st));
+    int launches = 1;
+    for (int64_t r0 = 0; r0 < m; r0 += mg) {
+        const int64_t mr = std::min(mg, m - r0);
+        const mpc_cmat Ag = rows_of(*A, r0, L);
+        const mpc_cmat Cg = rows_of(*C, r0, L);
+        CK(split_launch(dm(Ag.re), dm(Ag.im), 0, mr, k, Lo.kp, L, eA + r0, s, parts, digA, st));
+        if (E && r0 == 0) CK(cudaEventRecord(E->ev[3], st));
+        const Geometry geo = main_geometry(dev, mr, n, k, s, method);
+        const int BN = geo.BN;
+        std::vector<int32_t> sb;
+        if (!sblk.empty()) sb.assign(sblk.begin() + (r0 >> kSBlkShift), sblk.begin() + ((r0 + mr + kSBlk - 1) >> kSBlkShift));
+        PlanKey key{mr, n, k, s, method, geo.BM, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0,
+                    env_int("MPCGEMM_ORDER", 1), sb};
+        Plan *plan;
+        if (int rc = build_plan(dev, key, &plan)) return rc;
+        SliceGemmLaunch SL;
+        memset(&SL, 0, sizeof(SL));
+        SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
+        SL.P.partials = partials; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
+        SL.P.m = (int32_t)mr; SL.P.n = (int32_t)n; SL.P.s = s; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
+        SL.P.partsA = SL.P.partsB = parts;
+        for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
+        SL.digA = digA; SL.digB = digB; SL.rowsA = mr; SL.rowsB = n; SL.kp = Lo.kp;
+        SL.grid = plan->grid; SL.BM = geo.BM; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits;
+        SL.units_flat = plan->d_units;
+        CK(slicegemm_launch(SL, st));
+        if (E && r0 + mr >= m) CK(cudaEventRecord(E->ev[4], st));
+        FoldParams F;
+        F.partials = partials; F.nslots = plan->nslots; F.nstrips = Lo.nstrips; F.m = mr; F.n = n;
+        F.s = s; F.method = method; F.prec = prec; F.L = L; F.slotinfo = plan->d_slotinfo;
+        F.eA = eA + r0; F.eB = eB; F.Cre = dmo(Cg.re); F.Cim = dmo(Cg.im);
+        F.beta = beta; F.alpha_neg = alpha_neg; F.C0re = dm(Cg.re); F.C0im = dm(Cg.im);
+        F.ldF = (n + 1) & ~1ll;
+        F.sblk = sblk.empty() ? nullptr : mv.sblk + (r0 >> kSBlkShift);    // NEXT-4: per-block triangles
+        fix = (uint64_t *)((uint8_t *)partials +
+                           align_up((size_t)plan->nslots * ((mr + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
+        F.fix = fix;
+        CK(fold_normalize_launch(F, st));
+        launches += 3;                                 // split A_g, slice GEMM, fold
+        if (rep) {
+            rep->mma_instructions += plan->mma; rep->work_units += plan->nunits;
+            rep->slicegemm_ctas = simt ? plan->nunits : plan->grid;
+        }
+        if (hook) if (int rc = (*hook)(r0, r0 + mr)) return rc;
     }
-    F.fix = (uint64_t *)((uint8_t *)partials +
-                         align_up((size_t)plan->nslots * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
-    CK(fold_normalize_launch(F, st));
     if (E) CK(cudaEventRecord(E->ev[5], st));
-    if (rep) {
-        rep->mma_instructions = plan->mma; rep->work_units = plan->nunits;
-        rep->kernel_launches += 4;                     // split x2, slice GEMM, fold
-        rep->slicegemm_ctas = simt ? plan->nunits : plan->grid;
-    }
+    if (rep) rep->kernel_launches += launches;
     return 0;
 }
 
 // check_alias = false: the LU's in-place trailing update, whose A22 / L21 / U12 views of one
 // matrix interleave in memory but are element-disjoint (the split reads L21, U12 before the
 // fold writes A22, in stream order)
+// group_rows / hook: the e2e path's row groups (run_main)
 int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
-              int method, const mpcgemm_opts *opts, mpcgemm_report *rep, bool check_alias = true) {
+              int method, const mpcgemm_opts *opts, mpcgemm_report *rep, bool check_alias = true,
+              int64_t group_rows = 0, const GroupHook *hook = nullptr) {
     if (int rc = check_args(m, n, k, prec, A, B, C, method, check_alias)) return rc;
     cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
     const int forced = opts ? opts->slices : 0;
@@ -701,7 +730,16 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         }
         return 0;
     }
-    Layout Lm = layout_for(m, n, k, s, method, main_geometry(dev, m, n, k, s, method).maxkb, prec, beta != 0);
+    if (group_rows >= m) group_rows = 0;
+    const int64_t mg = group_rows > 0 ? group_rows : m;
+    Layout Lm = layout_for(mg, n, k, s, method, main_geometry(dev, mg, n, k, s, method).maxkb, prec, beta != 0);
+    if (group_rows > 0 && m % mg) {                   // the ragged last group may need more slots
+        const int64_t ml = m % mg;
+        const int parts = method == 3 ? 3 : 2;
+        Layout Ll = layout_for(ml, n, k, s, method, main_geometry(dev, ml, n, k, s, method).maxkb, prec, beta != 0);
+        const size_t extra = align_up((size_t)parts * s * mg * Lm.kp, 256) - align_up((size_t)parts * s * ml * Lm.kp, 256);
+        Lm.main = std::max(Lm.main, Ll.main + extra);
+    }
     uint8_t *big;
     if (opts && opts->workspace) {
         if (opts->workspace_bytes < Lm.main) return fail(MPCGEMM_ERR_NOMEM, "caller workspace too small");
@@ -713,7 +751,7 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     if (E) CK(cudaEventRecord(E->ev[2], st));
     if (rep) rep->kernel_launches = launches;
     if (int rc = run_main(dev, m, n, k, prec, A, B, C, method, s, st, meta, big, Lm, simt, rep, E, beta, alpha_neg,
-                          sblk))
+                          sblk, group_rows, hook))
         return rc;
     if (rep) {
         rep->slices = s; rep->slice_bits = 8; rep->certified = 1; rep->minT = pb[0]; rep->minT1 = pb[1];
@@ -877,6 +915,9 @@ size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec, mpc
     return std::max(Lo.main, Lo.pre);
 }
 
+// e2e entry: H2D of A, B (and C0), the hot path in row groups, and the D2H of each finished
+// group of C on a second stream while the next group computes (MPCGEMM_HOST_GROUP rows per
+// group, a multiple of 256; default 512 when m >= 1024; 0 = one group)
 int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
                  mpcgemm_method method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
     if (int rc = check_args(m, n, k, prec, A, B, C, (int)method)) return rc;
@@ -894,11 +935,18 @@ int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *
     int dev = 0;
     CK(cudaGetDevice(&dev));
     uint8_t *base;
+    cudaStream_t cs;                                   // D2H copy stream
+    cudaEvent_t ev;
     {
         std::lock_guard<std::mutex> lock(g_mu);
         DevCache &dc = g_cache[dev];
         if (int rc = grow(&dc.stage, &dc.stage_bytes, total)) return rc;
         base = (uint8_t *)dc.stage;
+        if (!dc.copy_stream) {
+            CK(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&dc.group_event, cudaEventDisableTiming));
+        }
+        cs = dc.copy_stream; ev = dc.group_event;
     }
     mpc_rmat dmats[6];
     for (int q = 0; q < 6; q++) {
@@ -927,18 +975,34 @@ int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *
         }
     }
     mpc_cmat dA{dmats[0], dmats[1]}, dB{dmats[2], dmats[3]}, dC{dmats[4], dmats[5]};
-    int rc = gemm_impl(m, n, k, prec, &dA, &dB, &dC, (int)method, opts, rep);
-    if (rc < 0) return rc;
     mpc_rmat *outs[2] = {&C->re, &C->im};
-    for (int q = 0; q < 2; q++) {
-        const mpc_rmat &D = dmats[4 + q];
-        mpc_rmat &H = *outs[q];
-        if (m == 0 || n == 0) continue;
-        CK(cudaMemcpy2DAsync(H.sign, H.ld, D.sign, n, n, m, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpy2DAsync(H.exp, H.ld * 8, D.exp, n * 8, n * 8, m, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpy2DAsync(H.limbs, H.ld * 8 * L, D.limbs, n * 8 * L, n * 8 * L, m, cudaMemcpyDeviceToHost, st));
+    // D2H of C rows [r0, r1) on the copy stream once the compute stream has finished them
+    GroupHook d2h = [&](int64_t r0, int64_t r1) -> int {
+        if (n == 0 || r1 <= r0) return 0;
+        CK(cudaEventRecord(ev, st));
+        CK(cudaStreamWaitEvent(cs, ev, 0));
+        for (int q = 0; q < 2; q++) {
+            const mpc_rmat &D = dmats[4 + q];
+            mpc_rmat &H = *outs[q];
+            const int64_t nr = r1 - r0;
+            CK(cudaMemcpy2DAsync(H.sign + r0 * H.ld, H.ld, D.sign + r0 * n, n, n, nr, cudaMemcpyDeviceToHost, cs));
+            CK(cudaMemcpy2DAsync(H.exp + r0 * H.ld, H.ld * 8, D.exp + r0 * n, n * 8, n * 8, nr, cudaMemcpyDeviceToHost, cs));
+            CK(cudaMemcpy2DAsync(H.limbs + r0 * H.ld * L, H.ld * 8 * L, D.limbs + r0 * n * L, n * 8 * L, n * 8 * L, nr,
+                                 cudaMemcpyDeviceToHost, cs));
+        }
+        return 0;
+    };
+    int64_t group = env_int("MPCGEMM_HOST_GROUP", m >= 1024 ? 512 : 0);
+    if (group > 0) group = std::max<int64_t>(kSBlk, group / kSBlk * kSBlk);
+    const bool grouped = group > 0 && group < m && !(opts && opts->carrier == 1);
+    int rc = gemm_impl(m, n, k, prec, &dA, &dB, &dC, (int)method, opts, rep, true, grouped ? group : 0,
+                       grouped ? &d2h : nullptr);
+    if (rc < 0) { cudaStreamSynchronize(cs); return rc; }
+    if (!grouped) {
+        if (int r2 = d2h(0, m)) return r2;
     }
     CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(cs));
     return rc;
 }
 

@@ -213,6 +213,31 @@ def test_host_entry_matches_device():
         assert r1["slices"] == r2["slices"] and same_bits(C1, C2)
 
 
+@pytest.mark.parametrize("group", [256, 512])
+def test_host_entry_row_groups(monkeypatch, group):
+    """mpcgemm_host in row groups (D2H of finished groups overlapping the next group's compute):
+    bitwise the one-call device result, incl. a ragged last group, adaptive blocks and beta = 1."""
+    monkeypatch.setenv("MPCGEMM_HOST_GROUP", str(group))
+    prec = 192
+    A = mpgen.random_cmat(32, 1, 700, 70, prec, 3)
+    A2 = mpgen.random_cmat(32, 4, 700, 70, prec, 30, zero_frac=0.2)
+    A.re.exp[300:] = A2.re.exp[300:]; A.re.limbs[300:] = A2.re.limbs[300:]; A.re.sign[300:] = A2.re.sign[300:]
+    B = mpgen.random_cmat(32, 2, 70, 300, prec, 3)
+    C0 = mpgen.random_cmat(32, 3, 700, 300, prec, 1)
+    for method in ("3M", "4M"):
+        C1, r1 = run_gpu(A, B, prec, method)
+        C2, r2 = P.mpcgemm_host(A, B, prec, method)
+        assert r1["slices"] == r2["slices"] and same_bits(C1, C2), first_mismatch(C1, C2)
+        dA, dB = P.to_device(A), P.to_device(B)
+        dC, ra = P.gemm(dA, dB, prec, method, adaptive=1)
+        Ca, rb = P.mpcgemm_host(A, B, prec, method, adaptive=1)
+        assert same_bits(P.to_host(dC), Ca)
+        dC0 = P.to_device(C0)
+        P.mpcgemm_ex(dA, dB, dC0, prec, method, beta=1, alpha_neg=1)
+        Cb, _ = P.mpcgemm_host(A, B, prec, method, C=C0.copy(), beta=1, alpha_neg=1)
+        assert same_bits(P.to_host(dC0), Cb)
+
+
 def test_validate_and_errors():
     prec = 128
     A = mpgen.random_cmat(41, 1, 8, 8, prec)
