@@ -40,6 +40,8 @@ struct DMatOut {
 //  G = 2: anti-diagonals r and r+1 together over the k-blocks kb in [a, b) of every pair and
 //         every p, into planes slot0 (D_r) and slot1 (D_{r+1}); each A_p / B_q tile is
 //         loaded once and feeds both diagonals.
+//  G = 3: anti-diagonal r alone over the k-blocks kb in [a, b) of every pair (a pair segment
+//         cut at r = s_b + 1 by a NEXT-4 per-block slice count), into slot0.
 struct WorkUnit {
     int32_t job_g, tm, tn, r, a, b, slot0, slot1;
 };

@@ -175,8 +175,8 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
         }
     auto base = [&](int q, int r) { return slotinfo[(q * (s + 2) + r) * 2]; };
     std::vector<WorkUnit> units;
-    // NEXT-4: a row tile of block b takes the segments whose first diagonal r <= sblk[b] + 1
-    // (a pair (r, r+1) with r = sblk[b] + 1 also computes D_{r+1}, which the fold skips)
+    // NEXT-4: a row tile of block b takes the segments whose first diagonal r <= sblk[b] + 1; a
+    // pair (r, r+1) with r = sblk[b] + 1 becomes a G = 3 unit computing D_r alone
     auto in_tri = [&](int64_t tm, int r) {
         return key.sblk.empty() || r <= key.sblk[(size_t)((tm * key.BM) >> kSBlkShift)] + 1;
     };
@@ -189,6 +189,11 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
                 for (int64_t tm = 0; tm < tiles_m; tm++)
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
                         if (!in_tri(tm, r)) continue;
+                        if (!in_tri(tm, r + 1)) {              // block's last diagonal is r: D_r alone
+                            units.push_back({q | (3 << 8), (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
+                            P.mma += np * (b - a) * (r - 1) * (kBK / 32);
+                            continue;
+                        }
                         units.push_back({q | (2 << 8), (int32_t)tm, (int32_t)tn, r, a, b,
                                          base(q, r) + (int32_t)c, base(q, r + 1) + (int32_t)c});
                         P.mma += np * (b - a) * (2 * r - 1) * (kBK / 32);
@@ -208,7 +213,9 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
         }
     }
     auto work = [&](const WorkUnit &w) -> int64_t {
-        return unit_G(w) == 2 ? (int64_t)P.jobs[unit_job(w)].npairs * (w.b - w.a) * (2 * w.r - 1) : (int64_t)(w.b - w.a);
+        const int64_t np = P.jobs[unit_job(w)].npairs;
+        return unit_G(w) == 2 ? np * (w.b - w.a) * (2 * w.r - 1)
+             : unit_G(w) == 3 ? np * (w.b - w.a) * (w.r - 1) : (int64_t)(w.b - w.a);
     };
     if (key.order == 1) {
         // job-major, then longest first: co-running units are neighbouring diagonal pairs of

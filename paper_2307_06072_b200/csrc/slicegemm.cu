@@ -105,6 +105,11 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                         for (int kb = w.a; kb < w.b; kb++)
                             for (int p = 1; p <= w.r; p++)          // A_p, B_{r+1-p}
                                 load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), kb, w.tm, w.tn);
+                } else if (unit_G(w) == 3) {                        // D_r alone over kb in [a, b)
+                    for (int pr = 0; pr < J.npairs; pr++)
+                        for (int kb = w.a; kb < w.b; kb++)
+                            for (int p = 1; p < w.r; p++)           // A_p, B_{r-p}
+                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1), kb, w.tm, w.tn);
                 } else {
                     const int per_pair = (w.r - 1) * KB;
                     for (int g = w.a; g < w.b; g++) {
@@ -163,7 +168,8 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
                             }
                 } else {
-                    for (int g = w.a; g < w.b; g++) {
+                    const int nsteps = unit_G(w) == 3 ? J.npairs * (w.b - w.a) * (w.r - 1) : w.b - w.a;
+                    for (int g = 0; g < nsteps; g++) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
@@ -171,7 +177,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; kk++)
                             mma_i8(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                   (g > w.a || kk > 0) ? 1u : 0u);
+                                   (g > 0 || kk > 0) ? 1u : 0u);
                         mma_commit(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -198,7 +204,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             mbar_wait(tfull, tphase);
             tc_fence_after();
             const int row = w.tm * kBM + q * 32 + lane;
-            for (int acc = 0; acc < unit_G(w); acc++) {
+            for (int acc = 0; acc < (unit_G(w) == 2 ? 2 : 1); acc++) {
                 const int64_t slot = acc ? w.slot1 : w.slot0;
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; c++) {
@@ -320,6 +326,11 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         for (int kb = w.a; kb < w.b; kb++)
                             for (int p = 1; p <= w.r; p++)          // A_p, B_{r+1-p}
                                 load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), kb, w.tm, w.tn);
+                } else if (unit_G(w) == 3) {                        // D_r alone over kb in [a, b)
+                    for (int pr = 0; pr < J.npairs; pr++)
+                        for (int kb = w.a; kb < w.b; kb++)
+                            for (int p = 1; p < w.r; p++)           // A_p, B_{r-p}
+                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1), kb, w.tm, w.tn);
                 } else {
                     const int per_pair = (w.r - 1) * KB;
                     for (int g = w.a; g < w.b; g++) {
@@ -378,7 +389,8 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
                             }
                 } else {
-                    for (int g = w.a; g < w.b; g++) {
+                    const int nsteps = unit_G(w) == 3 ? J.npairs * (w.b - w.a) * (w.r - 1) : w.b - w.a;
+                    for (int g = 0; g < nsteps; g++) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
@@ -386,7 +398,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; kk++)
                             mma_i8_2sm(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                       (g > w.a || kk > 0) ? 1u : 0u);
+                                       (g > 0 || kk > 0) ? 1u : 0u);
                         mma_commit_2sm(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -416,7 +428,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             mbar_wait(tfull, tphase);
             tc_fence_after();
             const int row = w.tm * 256 + (int)rank * 128 + q * 32 + lane;
-            for (int acc = 0; acc < unit_G(w); acc++) {
+            for (int acc = 0; acc < (unit_G(w) == 2 ? 2 : 1); acc++) {
                 const int64_t slot = acc ? w.slot1 : w.slot0;
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; c++) {
@@ -467,7 +479,7 @@ slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict_
     int32_t acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
     // enumerate (accumulator, A plane, B plane, kb) exactly as the tensor-core kernel pairs them
     const int npairs = J.npairs;
-    const int nsteps = G == 2 ? npairs * (w.b - w.a) * w.r * 2 : (w.b - w.a);
+    const int nsteps = G == 2 ? npairs * (w.b - w.a) * w.r * 2 : G == 3 ? npairs * (w.b - w.a) * (w.r - 1) : (w.b - w.a);
     for (int t = 0; t < nsteps; t++) {
         int which, planeA, planeB, kb;
         if (G == 2) {
@@ -481,6 +493,12 @@ slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict_
                 if (p >= w.r) continue;
                 which = 0; planeA = J.pa[pr] * P.s + p - 1; planeB = J.pb[pr] * P.s + (w.r - 1 - p);
             }
+        } else if (G == 3) {                          // (pair, kb, p) with p = 1..r-1: D_r only
+            int x = t;
+            const int p = x % (w.r - 1) + 1; x /= (w.r - 1);
+            kb = w.a + x % (w.b - w.a); x /= (w.b - w.a);
+            const int pr = x;
+            which = 0; planeA = J.pa[pr] * P.s + p - 1; planeB = J.pb[pr] * P.s + (w.r - p - 1);
         } else {
             const int g = w.a + t;
             const int per_pair = (w.r - 1) * P.KB;
@@ -510,7 +528,7 @@ slicegemm_simt_kernel(const int8_t *__restrict__ digA, const int8_t *__restrict_
             acc[which][e] = v;
         }
     }
-    for (int a = 0; a < G; a++)
+    for (int a = 0; a < (G == 2 ? 2 : 1); a++)
         for (int e = 0; e < 4; e++) {
             const int64_t row = row0 + ty * 4 + e, col = col0 + tx;
             const int slot = a ? w.slot1 : w.slot0;

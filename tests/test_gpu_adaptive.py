@@ -101,3 +101,34 @@ def test_adaptive_accumulate_bitexact():
                               samples=(si[sel] - r0, sj[sel]), srow=srow[r0:r1])
         bad = sampled_equal(C.rows(r0, r1), Rs, si[sel] - r0, sj[sel])
         assert bad is None, (b, bad)
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_adaptive_simt_crosscheck_and_cut_pairs(method, monkeypatch):
+    """Blocks whose last diagonal s_b + 1 opens a diagonal pair run G = 3 units (D_r alone):
+    the tensor-core kernels equal the dp4a cross-check kernel and the oracle, and the MMA count
+    drops by exactly the skipped diagonals."""
+    prec, k = 128, 200
+    found = None
+    for seed in range(40):                              # blocks with an odd s_b < s_max
+        A = mixed_rows(seed, k, prec, (0, 40), (256, 40), zero_frac=0.3)
+        B = mpgen.random_cmat(seed, 7, k, 260, prec, 1)
+        sb, ok = oracle.block_slices(A, B, prec, method, block=256)
+        if ok and min(sb) < max(sb) and min(sb) % 2 == 1:
+            found = (A, B, sb)
+            break
+    assert found, "no seed with an odd smaller block slice count"
+    A, B, sb = found
+    dA, dB = P.to_device(A), P.to_device(B)
+    C1, r1 = P.gemm(dA, dB, prec, method, adaptive=1)
+    C0, r0 = P.gemm(dA, dB, prec, method, adaptive=0)
+    monkeypatch.setenv("MPCGEMM_SLICEGEMM_SIMT", "1")
+    C2, r2 = P.gemm(dA, dB, prec, method, adaptive=1)
+    torch.cuda.synchronize()
+    assert r1["block_slices"] == sb and same_bits(P.to_host(C1), P.to_host(C2))
+    assert r1["mma_instructions"] < r0["mma_instructions"]
+    m, n = A.shape[0], B.shape[1]
+    si, sj = samples_for(m, n, 150, seed=9)
+    srow = [sb[i // 256] for i in range(m)]
+    Rs = oracle.ozaki_rows(A, B, prec, method, max(sb), srow, samples=(si, sj))
+    assert sampled_equal(P.to_host(C1), Rs, si, sj) is None

@@ -1,7 +1,8 @@
 """Sweep of the BASELINE configs (1-5) x {3M, 4M} on one GPU: device time per call (CUDA events,
 median of K after W warm-ups), CMAC/s, slice count, slice-GEMM INT8 TOP/s and its fraction of
 the peak used by bench.py, per-stage ms.  Config 5 = the sum over its 15 LU-update GEMMs.
-Writes one JSON document to stdout.  (Evidence for profiles/, not the driver's bench line.)"""
+Writes one JSON document to stdout.  (Evidence for profiles/, not the driver's bench line.)
+ADAPTIVE=1: NEXT-4 per-256-row-block slice counts (opts.adaptive); CONFIGS=1,2,..: subset."""
 import json
 import os
 import statistics
@@ -16,15 +17,18 @@ import mpgen  # noqa: E402
 import paper_2307_06072_b200 as P  # noqa: E402
 
 
+ADAPTIVE = int(os.environ.get("ADAPTIVE", "0"))
+
+
 def time_call(dA, dB, dC, prec, method, steps, warmup):
     for _ in range(warmup):
-        P.mpcgemm_ex(dA, dB, dC, prec, method)
+        P.mpcgemm_ex(dA, dB, dC, prec, method, adaptive=ADAPTIVE)
     torch.cuda.synchronize()
     ts, reps = [], []
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        reps.append(P.mpcgemm_ex(dA, dB, dC, prec, method, timing=1))
+        reps.append(P.mpcgemm_ex(dA, dB, dC, prec, method, timing=1, adaptive=ADAPTIVE))
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -34,8 +38,9 @@ def time_call(dA, dB, dC, prec, method, steps, warmup):
 def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     peak = 2.0 * peaks["bf16_tflops_sustained"]
-    out = {"peak_int8_tops": peak, "configs": []}
-    for cfg in (1, 2, 3, 4, 5):
+    out = {"peak_int8_tops": peak, "adaptive": ADAPTIVE, "configs": []}
+    cfgs = [int(c) for c in os.environ.get("CONFIGS", "1,2,3,4,5").split(",")]
+    for cfg in cfgs:
         for method in ("3M", "4M"):
             R = 3 if method == "3M" else 4
             if cfg <= 4:
@@ -50,7 +55,7 @@ def main():
                 ops = 2.0 * R * s * (s + 1) / 2 * cm
                 gms = statistics.median(r["ms_gemm"] for r in reps)
                 out["configs"].append({"config": cfg, "method": method, "prec": c["prec"], "shape": [c["m"], c["n"], c["k"]],
-                                       "slices": s, "ms": ms, "cmac_per_s": cm / (ms / 1e3),
+                                       "slices": s, "block_slices": reps[-1]["block_slices"], "ms": ms, "cmac_per_s": cm / (ms / 1e3),
                                        "gemm_ms": gms, "gemm_tops": ops / (gms / 1e3) / 1e12,
                                        "gemm_frac": ops / (gms / 1e3) / 1e12 / peak,
                                        "stages_ms": {f: statistics.median(r[f] for r in reps) for f in
@@ -65,7 +70,7 @@ def main():
                     dC = P.empty_device(mm, nn, mpgen.LU_PREC)
                     ms, reps = time_call(dA, dB, dC, mpgen.LU_PREC, method, 3, 2)
                     s = reps[-1]["slices"]
-                    ss.append(s)
+                    ss.append(reps[-1]["block_slices"] if ADAPTIVE else s)
                     tot_ms += ms
                     tot_cm += mm * nn * kk
                     tot_ops += 2.0 * R * s * (s + 1) / 2 * mm * nn * kk
@@ -76,7 +81,7 @@ def main():
                                        "gemm_frac": tot_ops / (tot_g / 1e3) / 1e12 / peak})
             torch.cuda.empty_cache()
     by = {(c["config"], c["method"]): c for c in out["configs"]}
-    out["ratio_3m_over_4m_time"] = {cfg: by[(cfg, "3M")]["ms"] / by[(cfg, "4M")]["ms"] for cfg in (1, 2, 3, 4, 5)}
+    out["ratio_3m_over_4m_time"] = {cfg: by[(cfg, "3M")]["ms"] / by[(cfg, "4M")]["ms"] for cfg in cfgs}
     print(json.dumps(out, indent=1))
 
 
