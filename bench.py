@@ -140,6 +140,28 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def hbm_kernels(args, reps, m, n, k, prec, s, pk, src):
+    """Achieved HBM bandwidth of the bandwidth-bound steps from their live stage times (CUDA
+    events on the launching stream) and ALGORITHMIC bytes:
+      split (a-3, A and B): read 2 (m k + k n)(9 + 8 L), write parts s (m + n) kp
+      fold + normalize (a-5/a-6): read 4 nslots per output element, write 2 (9 + 8 L) per element"""
+    L = (prec + 63) // 64
+    parts = 3 if args.method == "3M" else 2
+    kp = (k + 15) // 16 * 16
+    ent = 9 + 8 * L
+    split_b = 2 * (m * k + k * n) * ent + parts * s * (m + n) * kp
+    nslots = reps[-1].get("partial_slots", 0)
+    fold_b = m * n * (4 * nslots + 2 * ent)
+    peak = pk["hbm_gbs"]
+    out = []
+    for name, b, f in (("split_kernel x2 (a-3)", split_b, "ms_split"), ("fold_normalize_kernel (a-5/a-6)", fold_b, "ms_fold")):
+        ms = statistics.mean(r[f] for r in reps)
+        gbs = b / (ms / 1e3) / 1e9
+        out.append({"kernel": name, "bytes": b, "ms": round(ms, 3), "achieved": round(gbs, 1), "peak": peak,
+                    "unit": "GB/s", "frac": round(gbs / peak, 3), "peak_source": f"{src}: hbm_gbs"})
+    return out
+
+
 def workload_config(args, s):
     c = mpgen.CONFIGS[args.config]
     return {"workload": f"BASELINE config {args.config}: " + c["desc"], "method": args.method, "m_per_rank": c["m"],
@@ -250,6 +272,7 @@ def main():
                      "peak_source": f"{src}: 2 x bf16_tflops_sustained (nominal int8/bf16 = 2)",
                      "algorithmic": f"2 R P m n k = 2*{R}*{pairs}*{m}*{n}*{k} int8 ops per launch"},
         "stages_ms": stage_ms,
+        "hbm_kernels": hbm_kernels(args, reps, m, n, k, prec, s, pk, src),
         "gpu_launches": int(sum(r["kernel_launches"] for r in reps)),
         "clocks": clk,
     }

@@ -109,6 +109,7 @@ typedef struct {
     int32_t slicegemm_ctas;   /* grid of the slice-GEMM launch                                 */
     float   ms_linemax, ms_prepass, ms_split, ms_gemm, ms_fold;   /* opts->timing only         */
     int32_t slices_min;       /* smallest per-block s (== slices unless opts->adaptive)        */
+    int32_t partial_slots;    /* int32 partial planes per output element read by the fold       */
 } mpcgemm_report;
 
 /* C := A B (auto slice count).  Device pointers.  m, n, k >= 0 (empty: nothing written for

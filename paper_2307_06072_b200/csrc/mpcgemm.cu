@@ -627,6 +627,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         launches += 3;                                 // split A_g, slice GEMM, fold
         if (rep) {
             rep->mma_instructions += plan->mma; rep->work_units += plan->nunits;
+            rep->partial_slots = (int32_t)plan->nslots;
             rep->slicegemm_ctas = simt ? plan->nunits : plan->grid;
         }
         if (hook) if (int rc = (*hook)(r0, r0 + mr)) return rc;

@@ -54,7 +54,8 @@ class ReportC(ctypes.Structure):
                 ("mma_instructions", ctypes.c_int64), ("work_units", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int32), ("slice_bits", ctypes.c_int32), ("slicegemm_ctas", ctypes.c_int32),
                 ("ms_linemax", ctypes.c_float), ("ms_prepass", ctypes.c_float), ("ms_split", ctypes.c_float),
-                ("ms_gemm", ctypes.c_float), ("ms_fold", ctypes.c_float), ("slices_min", ctypes.c_int32)]
+                ("ms_gemm", ctypes.c_float), ("ms_fold", ctypes.c_float), ("slices_min", ctypes.c_int32),
+                ("partial_slots", ctypes.c_int32)]
 
 
 class LuReportC(ctypes.Structure):
