@@ -148,7 +148,10 @@ int mpcgemm_rho_bounds(int64_t m, int64_t n, int64_t k, int32_t prec,
 int mpcgemm_slices_for(int32_t prec, mpcgemm_method method, int64_t k,
                        int64_t minT, int64_t minT1, int64_t maxD2);
 
-/* Device workspace bytes for one call with s slices. */
+/* Device workspace bytes for one call with s slices.  A smaller caller workspace (or less free
+ * device memory, or the MPCGEMM_WS_LIMIT environment variable, bytes) makes the call run in row
+ * groups of 256 * 2^j rows (B split once; bit-identical result); ERR_NOMEM only when one
+ * 256-row group does not fit. */
 size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec,
                               mpcgemm_method method, int32_t slices);
 

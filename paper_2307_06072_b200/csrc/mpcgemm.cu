@@ -738,16 +738,37 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         }
         return 0;
     }
+    // workspace of row groups of mg rows (the ragged last group may need more slots)
+    auto grouped_layout = [&](int64_t mg) {
+        Layout Lg = layout_for(mg, n, k, s, method, main_geometry(dev, mg, n, k, s, method).maxkb, prec, beta != 0);
+        if (mg < m && m % mg) {
+            const int64_t ml = m % mg;
+            const int parts = method == 3 ? 3 : 2;
+            Layout Ll = layout_for(ml, n, k, s, method, main_geometry(dev, ml, n, k, s, method).maxkb, prec, beta != 0);
+            const size_t extra = align_up((size_t)parts * s * mg * Lg.kp, 256) - align_up((size_t)parts * s * ml * Lg.kp, 256);
+            Lg.main = std::max(Lg.main, Ll.main + extra);
+        }
+        return Lg;
+    };
     if (group_rows >= m) group_rows = 0;
-    const int64_t mg = group_rows > 0 ? group_rows : m;
-    Layout Lm = layout_for(mg, n, k, s, method, main_geometry(dev, mg, n, k, s, method).maxkb, prec, beta != 0);
-    if (group_rows > 0 && m % mg) {                   // the ragged last group may need more slots
-        const int64_t ml = m % mg;
-        const int parts = method == 3 ? 3 : 2;
-        Layout Ll = layout_for(ml, n, k, s, method, main_geometry(dev, ml, n, k, s, method).maxkb, prec, beta != 0);
-        const size_t extra = align_up((size_t)parts * s * mg * Lm.kp, 256) - align_up((size_t)parts * s * ml * Lm.kp, 256);
-        Lm.main = std::max(Lm.main, Ll.main + extra);
+    // memory bound: when one call's workspace does not fit (the caller's workspace, or free
+    // device memory minus 1 GiB, or MPCGEMM_WS_LIMIT bytes), run row groups of 256 * 2^j rows
+    size_t budget;
+    if (opts && opts->workspace) budget = opts->workspace_bytes;
+    else {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        budget = fr + dc.ws_bytes > ((size_t)1 << 30) ? fr + dc.ws_bytes - ((size_t)1 << 30) : 0;
     }
+    if (const char *lim = getenv("MPCGEMM_WS_LIMIT")) if (*lim) budget = std::min(budget, (size_t)strtoull(lim, nullptr, 10));
+    if (grouped_layout(group_rows > 0 ? group_rows : m).main > budget) {
+        int64_t g = (std::min(group_rows > 0 ? group_rows : m, m) + kSBlk - 1) / kSBlk * kSBlk;
+        while (g > kSBlk && grouped_layout(std::min(g, m)).main > budget) g = std::max<int64_t>(kSBlk, g / 2 / kSBlk * kSBlk);
+        if (grouped_layout(std::min(g, m)).main > budget) return fail(MPCGEMM_ERR_NOMEM, "workspace for 256-row groups exceeds the budget");
+        group_rows = g < m ? g : 0;
+    }
+    const int64_t mg = group_rows > 0 ? group_rows : m;
+    Layout Lm = grouped_layout(mg);
     uint8_t *big;
     if (opts && opts->workspace) {
         if (opts->workspace_bytes < Lm.main) return fail(MPCGEMM_ERR_NOMEM, "caller workspace too small");

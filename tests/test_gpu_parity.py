@@ -238,6 +238,23 @@ def test_host_entry_row_groups(monkeypatch, group):
         assert same_bits(P.to_host(dC0), Cb)
 
 
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_workspace_limit_row_groups(monkeypatch, method):
+    """A workspace budget below one call's need runs row groups (256 * 2^j rows): bitwise equal."""
+    prec = 128
+    A = mpgen.random_cmat(33, 1, 900, 130, prec, 2)
+    B = mpgen.random_cmat(33, 2, 130, 300, prec, 2)
+    C1, r1 = run_gpu(A, B, prec, method)
+    need = P.mpcgemm_workspace_size(900, 300, 130, prec, method, r1["slices"])
+    monkeypatch.setenv("MPCGEMM_WS_LIMIT", str(need // 3))
+    C2, r2 = run_gpu(A, B, prec, method)
+    assert r2["kernel_launches"] > r1["kernel_launches"]          # more than one group ran
+    assert same_bits(C1, C2), first_mismatch(C1, C2)
+    monkeypatch.setenv("MPCGEMM_WS_LIMIT", "1000")
+    with pytest.raises(P.MpcgemmError):
+        run_gpu(A, B, prec, method)
+
+
 def test_validate_and_errors():
     prec = 128
     A = mpgen.random_cmat(41, 1, 8, 8, prec)
