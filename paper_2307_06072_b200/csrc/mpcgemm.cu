@@ -754,14 +754,16 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     // memory bound: when one call's workspace does not fit (the caller's workspace, or free
     // device memory minus 1 GiB, or MPCGEMM_WS_LIMIT bytes), run row groups of 256 * 2^j rows
     size_t budget;
+    const size_t want = grouped_layout(group_rows > 0 ? group_rows : m).main;
     if (opts && opts->workspace) budget = opts->workspace_bytes;
-    else {
+    else if (want <= dc.ws_bytes) budget = dc.ws_bytes;          // fits the cached workspace
+    else {                                                       // (cudaMemGetInfo costs ~ms)
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
         budget = fr + dc.ws_bytes > ((size_t)1 << 30) ? fr + dc.ws_bytes - ((size_t)1 << 30) : 0;
     }
     if (const char *lim = getenv("MPCGEMM_WS_LIMIT")) if (*lim) budget = std::min(budget, (size_t)strtoull(lim, nullptr, 10));
-    if (grouped_layout(group_rows > 0 ? group_rows : m).main > budget) {
+    if (want > budget) {
         int64_t g = (std::min(group_rows > 0 ? group_rows : m, m) + kSBlk - 1) / kSBlk * kSBlk;
         while (g > kSBlk && grouped_layout(std::min(g, m)).main > budget) g = std::max<int64_t>(kSBlk, g / 2 / kSBlk * kSBlk);
         if (grouped_layout(std::min(g, m)).main > budget) return fail(MPCGEMM_ERR_NOMEM, "workspace for 256-row groups exceeds the budget");
