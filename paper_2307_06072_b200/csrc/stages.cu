@@ -740,9 +740,19 @@ fold_normalize_kernel(const FoldParams F)
             accumulate_store(f1, (int)0, Lc0, Lw, e0, F.alpha_neg, s1, x1, F.C0im.limbs + cj * F.L, F.prec, F.L,
                              F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L, lstride, R0);
         } else {
-            normalize_store(f0, lstride, Lc0, e0, F.alpha_neg, F.prec, F.L, F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L);
-            normalize_store(fixg + x + (int64_t)Lc0 * lstride, lstride, Lc0, e0, F.alpha_neg, F.prec, F.L,
-                            F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L);
+            // copy each part's limbs to a thread-local array with independent (batched) loads,
+            // then magnitude + RNE on the L1-resident copy (the scratch reads were a dependent
+            // chain of global loads -- profiles/ncu_hbm_r1o.md)
+            uint64_t loc[kMaxSlices / 8 + 3];
+#pragma unroll 1
+            for (int p = 0; p < 2; p++) {
+                const uint64_t *src = fixg + x + (int64_t)p * Lc0 * lstride;
+#pragma unroll 8
+                for (int l = 0; l < Lc0; l++) loc[l] = src[(int64_t)l * lstride];
+                const DMatOut &Co = p ? F.Cim : F.Cre;
+                const int64_t oo = p ? oj : oi;
+                normalize_store(loc, 1, Lc0, e0, F.alpha_neg, F.prec, F.L, Co.sign + oo, Co.exp + oo, Co.limbs + oo * F.L);
+            }
         }
     }
 }
