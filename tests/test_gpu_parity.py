@@ -327,6 +327,35 @@ def test_large_forced_slices(method):
     assert sampled_equal(C, Rs, si, sj) is None
 
 
+@pytest.mark.parametrize("method", ["3M", "4M"])
+@pytest.mark.parametrize("prec,k,spread", [(2048, 12, 3), (4096, 5, 1), (1000, 9, 40)])
+def test_high_precision_bitexact(method, prec, k, spread):
+    """prec up to the ABI's 4096 bits (L = 64 limbs, s ~ 515): auto s, sampled bit-exact, within bound."""
+    m, n = 23, 37
+    A = mpgen.random_cmat(prec + k, 1, m, k, prec, spread)
+    B = mpgen.random_cmat(prec + k, 2, k, n, prec, spread)
+    C, rep = run_gpu(A, B, prec, method)
+    assert rep["slices"] == oracle.auto_slices(A, B, prec, method)[0]
+    si, sj = sample_idx(m, n, 25, seed=prec)
+    Rs = oracle.ozaki(A, B, prec, method, rep["slices"], samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
+    Xs = oracle.exact(A, B, prec + 64, method, samples=(si, sj))
+    assert max_err_log2(A, B, C, Xs, samples=(si, sj), ref_is_sampled=True) <= -(prec - BOUND[method])
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_long_k_exactness_chunks(method):
+    """k = 20000 (157 k-blocks): every diagonal past r ~ 7 is cut into INT32-exact chunks (<= 1023
+    k-blocks per accumulator); sampled bit-exact and within bound."""
+    m, n, k, prec = 33, 45, 20000, 128
+    A = mpgen.random_cmat(20, 1, m, k, prec, 2)
+    B = mpgen.random_cmat(20, 2, k, n, prec, 2)
+    C, rep = run_gpu(A, B, prec, method)
+    si, sj = sample_idx(m, n, 12, seed=20)
+    Rs = oracle.ozaki(A, B, prec, method, rep["slices"], samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
+
+
 # ------------------------------------------------------------------ NEXT-2: C := C0 +- A B
 def _c0_variants(m, n, prec, A, B, method):
     out = {"near": oracle.exact(A, B, prec, method)}                 # heavy cancellation
