@@ -51,6 +51,23 @@ struct DevCache {
     void *solve = nullptr; size_t solve_bytes = 0;   // NEXT-3 solve scratch (1 / U_cc, X)
     cudaStream_t copy_stream = nullptr;              // mpcgemm_host: D2H of finished row groups
     cudaEvent_t group_event = nullptr;
+    cudaEvent_t done = nullptr;                      // completion of the last call's device work
+};
+
+// The cached workspace / scratch of a device is shared by every call, whatever its stream:
+// each call's device work is ordered after the previous call's (an event wait on the new
+// stream; a no-op on the same stream), so calls on different streams cannot overlap on it.
+// Construct with g_mu held; the destructor records this call's completion (g_mu still held).
+struct StreamOrder {
+    DevCache &dc;
+    cudaStream_t st;
+    StreamOrder(DevCache &d, cudaStream_t s) : dc(d), st(s) {
+        if (dc.done) cudaStreamWaitEvent(st, dc.done, 0);
+    }
+    ~StreamOrder() {
+        if (!dc.done) cudaEventCreateWithFlags(&dc.done, cudaEventDisableTiming);
+        cudaEventRecord(dc.done, st);
+    }
 };
 std::mutex g_mu;
 std::map<int, DevCache> g_cache;
@@ -669,6 +686,7 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(g_mu);
     DevCache &dc = g_cache[dev];
+    StreamOrder order(dc, st);
     StageEvents *E = (opts && opts->timing) ? stage_events(dev) : nullptr;
     if (E) CK(cudaEventRecord(E->ev[0], st));
     Layout Lo = layout_for(m, n, k, 0, method, kMaxKBlocksPerChunk);
@@ -806,6 +824,25 @@ mpc_rmat sub_view(const mpc_rmat &M, int64_t r, int64_t c, int L) {
     return v;
 }
 
+// LU factor / solve: one at a time per process (they share the device's LU scratch), and their
+// device work ordered after the previous call's like every other call (StreamOrder); g_mu is
+// taken only briefly here because the LU's own GEMM updates take it.
+std::mutex g_lu_mu;
+struct LuOrder {
+    int dev; cudaStream_t st;
+    LuOrder(int d, cudaStream_t s) : dev(d), st(s) {
+        std::lock_guard<std::mutex> lock(g_mu);
+        DevCache &dc = g_cache[dev];
+        if (dc.done) cudaStreamWaitEvent(st, dc.done, 0);
+    }
+    ~LuOrder() {
+        std::lock_guard<std::mutex> lock(g_mu);
+        DevCache &dc = g_cache[dev];
+        if (!dc.done) cudaEventCreateWithFlags(&dc.done, cudaEventDisableTiming);
+        cudaEventRecord(dc.done, st);
+    }
+};
+
 int lu_scratch(int dev, int L, LuScratch *s, int32_t **info) {
     std::lock_guard<std::mutex> lock(g_mu);
     DevCache &dc = g_cache[dev];
@@ -842,6 +879,8 @@ int lu_impl(int64_t n, int32_t prec, mpc_cmat *A, int64_t *ipiv, int32_t K, int 
     cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
     int dev = 0;
     CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lulock(g_lu_mu);
+    LuOrder order(dev, st);
     LuScratch sc; int32_t *info;
     if (int rc = lu_scratch(dev, L, &sc, &info)) return rc;
     CK(cudaMemsetAsync(info, 0, 4, st));
@@ -919,6 +958,7 @@ int mpcgemm_rho_bounds(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_
     CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(g_mu);
     DevCache &dc = g_cache[dev];
+    StreamOrder order(dc, st);
     Layout Lo = layout_for(m, n, k, 0, MPCGEMM_3M, kMaxKBlocksPerChunk);
     if (int rc = grow(&dc.meta, &dc.meta_bytes, Lo.meta)) return rc;
     if (int rc = grow(&dc.ws, &dc.ws_bytes, Lo.pre)) return rc;
@@ -949,9 +989,12 @@ size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec, mpc
 // e2e entry: H2D of A, B (and C0), the hot path in row groups, and the D2H of each finished
 // group of C on a second stream while the next group computes (MPCGEMM_HOST_GROUP rows per
 // group, a multiple of 256; default 512 when m >= 1024; 0 = one group)
+std::mutex g_host_mu;                                  // one host-buffer call at a time (staging)
+
 int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
                  mpcgemm_method method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
     if (int rc = check_args(m, n, k, prec, A, B, C, (int)method)) return rc;
+    std::lock_guard<std::mutex> hostlock(g_host_mu);
     const int L = (prec + 63) / 64;
     cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
     const mpc_rmat *in[4] = {&A->re, &A->im, &B->re, &B->im};
@@ -1061,6 +1104,7 @@ void mpcgemm_release(void) {
     cudaDeviceSynchronize();
     auto it = g_cache.find(dev);
     if (it != g_cache.end()) {
+        if (it->second.done) cudaEventDestroy(it->second.done);
         cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage); cudaFree(it->second.lu);
         cudaFree(it->second.solve);
         g_cache.erase(it);
@@ -1088,6 +1132,8 @@ int mpclu_solve(int64_t n, int64_t nrhs, int32_t prec, const mpc_cmat *LU, const
     cudaStream_t st = opts ? (cudaStream_t)opts->stream : nullptr;
     int dev = 0;
     CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lulock(g_lu_mu);
+    LuOrder order(dev, st);
     // scratch: 1 x n reciprocals and the n x nrhs solution, both parts (ABI element format)
     const size_t ents = (size_t)n + (size_t)n * nrhs;
     uint8_t *base;

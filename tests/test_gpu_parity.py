@@ -255,6 +255,27 @@ def test_workspace_limit_row_groups(monkeypatch, method):
         run_gpu(A, B, prec, method)
 
 
+def test_concurrent_streams_share_workspace_safely():
+    """Calls on different streams without host synchronisation: each call's device work is
+    ordered after the previous call's (the device workspace is shared), so both results are
+    the single-call results bitwise."""
+    prec = 256
+    A1, B1 = mpgen.random_cmat(41, 1, 300, 200, prec, 4), mpgen.random_cmat(41, 2, 200, 260, prec, 4)
+    A2, B2 = mpgen.random_cmat(42, 1, 420, 150, prec, 9), mpgen.random_cmat(42, 2, 150, 310, prec, 9)
+    R1, _ = run_gpu(A1, B1, prec, "3M")
+    R2, _ = run_gpu(A2, B2, prec, "4M")
+    dA1, dB1, dA2, dB2 = P.to_device(A1), P.to_device(B1), P.to_device(A2), P.to_device(B2)
+    dC1, dC2 = P.empty_device(300, 260, prec), P.empty_device(420, 310, prec)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        P.mpcgemm_ex(dA1, dB1, dC1, prec, "3M", stream=s1)
+        P.mpcgemm_ex(dA2, dB2, dC2, prec, "4M", stream=s2)
+        ipiv, _ = P.mpclu_factor(P.to_device(mpgen.random_cmat(43, 1, 40, 40, 128)), 8, "3M", stream=s1)
+    torch.cuda.synchronize()
+    assert same_bits(P.to_host(dC1), R1) and same_bits(P.to_host(dC2), R2)
+
+
 def test_validate_and_errors():
     prec = 128
     A = mpgen.random_cmat(41, 1, 8, 8, prec)
