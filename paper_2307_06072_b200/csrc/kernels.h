@@ -51,8 +51,9 @@ struct FoldParams {
     DMat C0re, C0im;             // may alias Cre / Cim
     const int32_t *sblk;         // NEXT-4: slice count of each 256-row block (<= s), or nullptr
     uint64_t *fix;               // fixed-point scratch, fold_scratch_words(m, ldF, s, L, beta) words
-    int64_t ldF;                 // scratch row pitch (even, >= n)
+    int64_t ldF;                 // scratch row pitch (a multiple of kFoldLdAlign, >= n)
 };
+constexpr int kFoldLdAlign = 2;  // fold outputs per consumer thread
 size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta);
 // a-5 + a-6: exact fold (chunk sums, Eq. 5/6 combination, carry) and RNE normalization
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st);

@@ -412,7 +412,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb,
         const int64_t nslots = count_slots(k, s, method, maxkb);
         Lo.main = align_up((size_t)parts * s * m * Lo.kp, 256) + align_up((size_t)parts * s * n * Lo.kp, 256) +
                   align_up((size_t)nslots * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256) +
-                  align_up(fold_scratch_words(m, (n + 1) & ~1ll, s, (prec + 63) / 64, beta) * 8, 256);
+                  align_up(fold_scratch_words(m, (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign, s, (prec + 63) / 64, beta) * 8, 256);
     }
     return Lo;
 }
@@ -635,7 +635,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         F.s = s; F.method = method; F.prec = prec; F.L = L; F.slotinfo = plan->d_slotinfo;
         F.eA = eA + r0; F.eB = eB; F.Cre = dmo(Cg.re); F.Cim = dmo(Cg.im);
         F.beta = beta; F.alpha_neg = alpha_neg; F.C0re = dm(Cg.re); F.C0im = dm(Cg.im);
-        F.ldF = (n + 1) & ~1ll;
+        F.ldF = (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign;
         F.sblk = sblk.empty() ? nullptr : mv.sblk + (r0 >> kSBlkShift);    // NEXT-4: per-block triangles
         fix = (uint64_t *)((uint8_t *)partials +
                            align_up((size_t)plan->nslots * ((mr + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));

@@ -597,13 +597,18 @@ MPC_DEV void accumulate_store(uint64_t *fix, int unused, int Lc, int Lw, int64_t
 // the carry chains; the fixed-point numbers live in shared memory, fix[part][limb][column].
 constexpr int kFoldRing = 4;           // entries
 constexpr int kFoldPer = 8;            // slots per entry
-constexpr int kFoldEPT = 2;            // outputs per consumer thread
+constexpr int kFoldEPT = 2;            // outputs per consumer thread (4 was tried: slower, profiles/README.md)
+static_assert(kFoldEPT == kFoldLdAlign, "scratch pitch alignment");
 
-template <int COLS, bool BETA>
-__global__ void __launch_bounds__(COLS / kFoldEPT + 32)
+template <int V> struct IntVec;
+template <> struct IntVec<2> { using T = int2; MPC_DEV static void get(const T &v, int32_t (&o)[2]) { o[0] = v.x; o[1] = v.y; } };
+template <> struct IntVec<4> { using T = int4; MPC_DEV static void get(const T &v, int32_t (&o)[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; } };
+
+template <int COLS, bool BETA, int EPT = kFoldEPT>
+__global__ void __launch_bounds__(COLS / EPT + 32)
 fold_normalize_kernel(const FoldParams F)
 {
-    constexpr int NCONS = COLS / kFoldEPT;            // consumer threads
+    constexpr int NCONS = COLS / EPT;                 // consumer threads
     extern __shared__ __align__(128) uint8_t fsm_raw[];
     const int s = F.s;
     const int Lc0 = s / 8 + 3;                        // fixed-point limbs
@@ -653,26 +658,36 @@ fold_normalize_kernel(const FoldParams F)
         }
         return;
     }
-    // ---------------- consumers: outputs j0 + 2 tid, j0 + 2 tid + 1.  The fixed-point limbs go
-    // to the global scratch fix[part][limb][m*ldF] (column = element), read back by the rounding.
-    const int col = kFoldEPT * tid;
-    const int64_t jj = j0 + col;                      // first of the two elements
+    // ---------------- consumers: outputs j0 + EPT tid .. + EPT-1.  The fixed-point limbs go to
+    // the global scratch fix[part][limb][m*ldF] (column = element), read back by the rounding.
+    const int col = EPT * tid;
+    const int64_t jj = j0 + col;                      // first of the EPT elements
     const int64_t lstride = F.m * F.ldF;              // limb stride in the scratch
     uint64_t *fixg = F.fix + i * F.ldF + jj;
-    int64_t t0[2] = {0, 0}, t1[2] = {0, 0}, t2[2] = {0, 0};
-    int64_t cr[2][2] = {{0, 0}, {0, 0}};              // [part][element] carries
-    uint64_t cur[2][2] = {{0, 0}, {0, 0}};
+    int64_t t0[EPT], t1[EPT], t2[EPT];
+    int64_t cr[2][EPT];                               // [part][element] carries
+    uint64_t cur[2][EPT];
+#pragma unroll
+    for (int x = 0; x < EPT; x++) { t0[x] = t1[x] = t2[x] = 0; cr[0][x] = cr[1][x] = 0; cur[0][x] = cur[1][x] = 0; }
     int e = 0, fill = 0; uint32_t ph = 0;
     int b = 0;                                        // byte index = s + 1 - r
-    const bool live = jj < F.n;                       // (jj + 1 < n too: ldF is even and n is padded)
+    const bool live = jj < F.n;                       // (the rest of the EPT too: ldF is a multiple of EPT)
     for (int sl = sl0; sl < nslots; sl++) {
         if (fill == 0) mbar_wait(&full[e], ph);
         const int sc = sched[sl];
-        const int2 v = *reinterpret_cast<const int2 *>(ring + (e * kFoldPer + fill) * COLS + col);
+        int32_t v[EPT];
+        IntVec<EPT>::get(*reinterpret_cast<const typename IntVec<EPT>::T *>(ring + (e * kFoldPer + fill) * COLS + col), v);
         const int q = sc & 3;
-        if (q == 0) { t0[0] += v.x; t0[1] += v.y; }
-        else if (q == 1) { t1[0] += v.x; t1[1] += v.y; }
-        else { t2[0] += v.x; t2[1] += v.y; }
+        if (q == 0) {
+#pragma unroll
+            for (int x = 0; x < EPT; x++) t0[x] += v[x];
+        } else if (q == 1) {
+#pragma unroll
+            for (int x = 0; x < EPT; x++) t1[x] += v[x];
+        } else {
+#pragma unroll
+            for (int x = 0; x < EPT; x++) t2[x] += v[x];
+        }
         if (++fill == kFoldPer) {
             fill = 0;
             __syncwarp();
@@ -682,7 +697,7 @@ fold_normalize_kernel(const FoldParams F)
         if (sc & 0x80) {                              // diagonal r complete: combine and carry
             const int sh = 8 * (b & 7);
 #pragma unroll
-            for (int x = 0; x < 2; x++) {
+            for (int x = 0; x < EPT; x++) {
                 int64_t d0, d1;
                 if (F.method == 3) { d0 = t0[x] - t1[x]; d1 = t2[x] - t0[x] - t1[x]; }   // Eq. 6
                 else               { d0 = t0[x] - t1[x]; d1 = t2[x]; }                   // Eq. 5
@@ -694,10 +709,13 @@ fold_normalize_kernel(const FoldParams F)
                 if (live) {
 #pragma unroll
                     for (int p = 0; p < 2; p++)
-                        *reinterpret_cast<ulonglong2 *>(fixg + ((int64_t)p * Lc0 + (b >> 3)) * lstride) =
-                            make_ulonglong2(cur[p][0], cur[p][1]);
+#pragma unroll
+                        for (int x = 0; x < EPT; x += 2)
+                            *reinterpret_cast<ulonglong2 *>(fixg + ((int64_t)p * Lc0 + (b >> 3)) * lstride + x) =
+                                make_ulonglong2(cur[p][x], cur[p][x + 1]);
                 }
-                cur[0][0] = cur[0][1] = cur[1][0] = cur[1][1] = 0;
+#pragma unroll
+                for (int x = 0; x < EPT; x++) cur[0][x] = cur[1][x] = 0;
             }
             b++;
         }
@@ -707,22 +725,27 @@ fold_normalize_kernel(const FoldParams F)
     const int l0 = sr >> 3, o = 8 * (sr & 7);
 #pragma unroll
     for (int p = 0; p < 2; p++) {
-        uint64_t w[2][2];
+        uint64_t w[EPT][2];
 #pragma unroll
-        for (int x = 0; x < 2; x++) {
+        for (int x = 0; x < EPT; x++) {
             const uint64_t c = (uint64_t)cr[p][x], sx = cr[p][x] < 0 ? ~0ull : 0ull;
             w[x][0] = cur[p][x] | (c << o);
             w[x][1] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
         }
         uint64_t *fx = fixg + (int64_t)p * Lc0 * lstride;
-        *reinterpret_cast<ulonglong2 *>(fx + (int64_t)l0 * lstride) = make_ulonglong2(w[0][0], w[1][0]);
-        *reinterpret_cast<ulonglong2 *>(fx + (int64_t)(l0 + 1) * lstride) = make_ulonglong2(w[0][1], w[1][1]);
+#pragma unroll
+        for (int x = 0; x < EPT; x += 2) {
+            *reinterpret_cast<ulonglong2 *>(fx + (int64_t)l0 * lstride + x) = make_ulonglong2(w[x][0], w[x + 1][0]);
+            *reinterpret_cast<ulonglong2 *>(fx + (int64_t)(l0 + 1) * lstride + x) = make_ulonglong2(w[x][1], w[x + 1][1]);
+        }
         for (int l = l0 + 2; l < Lc0; l++)
-            *reinterpret_cast<ulonglong2 *>(fx + (int64_t)l * lstride) =
-                make_ulonglong2(cr[p][0] < 0 ? ~0ull : 0ull, cr[p][1] < 0 ? ~0ull : 0ull);
+#pragma unroll
+            for (int x = 0; x < EPT; x += 2)
+                *reinterpret_cast<ulonglong2 *>(fx + (int64_t)l * lstride + x) =
+                    make_ulonglong2(cr[p][x] < 0 ? ~0ull : 0ull, cr[p][x + 1] < 0 ? ~0ull : 0ull);
     }
 #pragma unroll 1
-    for (int x = 0; x < 2; x++) {
+    for (int x = 0; x < EPT; x++) {
         const int64_t j = jj + x;
         if (j >= F.n) break;
         uint64_t *f0 = fixg + x, *f1 = fixg + x + (int64_t)(Lc0 + Lw) * lstride;   // parts: [0, Lc0+Lw), [Lc0+Lw, ..)
@@ -775,7 +798,7 @@ static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
 {
     if (F.m == 0 || F.n == 0) return cudaSuccess;
-    if (F.s > kMaxSlices || (F.ldF & 1)) return cudaErrorInvalidValue;
+    if (F.s > kMaxSlices || (F.ldF % kFoldEPT)) return cudaErrorInvalidValue;
     if (F.beta) return fold_launch_t<256, true>(F, st);
     return fold_launch_t<256, false>(F, st);
 }
