@@ -434,9 +434,21 @@ struct FixView {
 
 // RNE of a magnitude buf[0..n) (column of stride `stride`, LSB weight 2^e_lsb) to prec bits,
 // stored in the ABI element format with sign `neg`.
+// an output element's L limbs written as whole 16-byte vectors (one element's limbs are
+// contiguous; limb-by-limb 8-byte stores from a warp left sectors half written in L2 and cost
+// read-modify-write DRAM traffic)
+MPC_DEV void store_limbs(uint64_t *dst, const uint64_t *v, int L) {
+    if (!(L & 1) && !(reinterpret_cast<uintptr_t>(dst) & 15)) {
+        for (int l = 0; l < L; l += 2) *reinterpret_cast<ulonglong2 *>(dst + l) = make_ulonglong2(v[l], v[l + 1]);
+    } else {
+        for (int l = 0; l < L; l++) dst[l] = v[l];
+    }
+}
+
 MPC_DEV void round_store(const uint64_t *buf, int64_t stride, int n, int64_t e_lsb, bool neg, int prec, int L,
                          uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
 {
+    uint64_t ov[kMaxSlices / 8 + 8];                  // >= L (prec <= 4096)
     int b = 0;
     for (int l = n - 1; l >= 0; l--) {
         const uint64_t v = buf[(int64_t)l * stride];
@@ -444,7 +456,8 @@ MPC_DEV void round_store(const uint64_t *buf, int64_t stride, int n, int64_t e_l
     }
     if (b == 0) {
         *sign_out = 0; *exp_out = 0;
-        for (int l = 0; l < L; l++) limbs_out[l] = 0;
+        for (int l = 0; l < L; l++) ov[l] = 0;
+        store_limbs(limbs_out, ov, L);
         return;
     }
     const FixView F{buf, stride, n};
@@ -467,8 +480,9 @@ MPC_DEV void round_store(const uint64_t *buf, int64_t stride, int n, int64_t e_l
         bool allones = (w0 | ((1ull << drop) - 1)) == ~0ull;
         for (int l = 1; l < L && allones; l++) allones = F.bits64(base + 64 * l) == ~0ull;
         if (allones) {
-            for (int l = 0; l < L - 1; l++) limbs_out[l] = 0;
-            limbs_out[L - 1] = 1ull << 63;
+            for (int l = 0; l < L - 1; l++) ov[l] = 0;
+            ov[L - 1] = 1ull << 63;
+            store_limbs(limbs_out, ov, L);
             *sign_out = neg ? 1 : 0;
             *exp_out = E + 1;
             return;
@@ -479,8 +493,9 @@ MPC_DEV void round_store(const uint64_t *buf, int64_t stride, int n, int64_t e_l
         uint64_t w = l == 0 ? w0 : F.bits64(base + 64 * l);
         const uint64_t x = w + c;
         c = (x < w) ? 1ull : 0ull;
-        limbs_out[l] = x;
+        ov[l] = x;
     }
+    store_limbs(limbs_out, ov, L);
     *sign_out = neg ? 1 : 0;
     *exp_out = E;
 }
@@ -615,18 +630,15 @@ fold_normalize_kernel(const FoldParams F)
     const int Lw = BETA ? Lc0 + F.L + 3 : 0;          // NEXT-2 sum window
     const int nslots = (int)F.nslots;
     int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                                   // [RING][PER][COLS]
-    uint8_t *sched = reinterpret_cast<uint8_t *>(fsm_raw + kFoldRing * kFoldPer * COLS * 4); // [nslots]
-    uint64_t *full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(sched + nslots) + 15) & ~uintptr_t(15));
+    uint8_t *cntq = reinterpret_cast<uint8_t *>(fsm_raw + kFoldRing * kFoldPer * COLS * 4);  // [job][s+2] chunk counts
+    const int ntab = nslots > kMaxJobs * (s + 2) ? nslots : kMaxJobs * (s + 2);
+    uint64_t *full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(cntq + ntab) + 15) & ~uintptr_t(15));
     uint64_t *empty = full + kFoldRing;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    // flat schedule: slot (r, q, c) -> q | 0x80 on the last slot of diagonal r
-    for (int x = tid; x < kMaxJobs * (s + 2); x += blockDim.x) {
-        const int q = x / (s + 2), r = x % (s + 2);
-        if (r < 2) continue;
-        const int base = F.slotinfo[(q * (s + 2) + r) * 2], cnt = F.slotinfo[(q * (s + 2) + r) * 2 + 1];
-        for (int c = 0; c < cnt; c++) sched[base + c] = (uint8_t)(q | ((q == kMaxJobs - 1 && c == cnt - 1) ? 0x80 : 0));
-    }
+    // chunk count of every (job, diagonal): the slots come in the order r = s+1..2, job, chunk
+    for (int x = tid; x < kMaxJobs * (s + 2); x += blockDim.x)
+        cntq[x] = (uint8_t)((x % (s + 2)) < 2 ? 0 : F.slotinfo[x * 2 + 1]);
     if (tid == 0) {
         for (int e = 0; e < kFoldRing; e++) { mbar_init(&full[e], 1); mbar_init(&empty[e], NCONS / 32); }
         fence_barrier_init();
@@ -670,41 +682,73 @@ fold_normalize_kernel(const FoldParams F)
 #pragma unroll
     for (int x = 0; x < EPT; x++) { t0[x] = t1[x] = t2[x] = 0; cr[0][x] = cr[1][x] = 0; cur[0][x] = cur[1][x] = 0; }
     int e = 0, fill = 0; uint32_t ph = 0;
-    int b = 0;                                        // byte index = s + 1 - r
     const bool live = jj < F.n;                       // (the rest of the EPT too: ldF is a multiple of EPT)
-    for (int sl = sl0; sl < nslots; sl++) {
+    // next slot's strip from the ring (consumer side of the producer's bulk copies)
+    auto next = [&](int32_t (&v)[EPT]) {
         if (fill == 0) mbar_wait(&full[e], ph);
-        const int sc = sched[sl];
-        int32_t v[EPT];
         IntVec<EPT>::get(*reinterpret_cast<const typename IntVec<EPT>::T *>(ring + (e * kFoldPer + fill) * COLS + col), v);
-        const int q = sc & 3;
-        if (q == 0) {
-#pragma unroll
-            for (int x = 0; x < EPT; x++) t0[x] += v[x];
-        } else if (q == 1) {
-#pragma unroll
-            for (int x = 0; x < EPT; x++) t1[x] += v[x];
-        } else {
-#pragma unroll
-            for (int x = 0; x < EPT; x++) t2[x] += v[x];
-        }
         if (++fill == kFoldPer) {
             fill = 0;
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[e]);
             if (++e == kFoldRing) { e = 0; ph ^= 1; }
         }
-        if (sc & 0x80) {                              // diagonal r complete: combine and carry
-            const int sh = 8 * (b & 7);
+    };
+    // diagonals r = sr+1 .. 2 (byte b = sr + 1 - r of the fixed-point number), two at a time:
+    //   acc = carry + D_b + 256 D_{b+1};  emit 16 bits at bit 8 b;  carry = acc >> 16
+    int64_t pend[2][EPT];
+    int b = 0;
+    for (int r = sr + 1; r >= 2; r--, b++) {
 #pragma unroll
-            for (int x = 0; x < EPT; x++) {
-                int64_t d0, d1;
-                if (F.method == 3) { d0 = t0[x] - t1[x]; d1 = t2[x] - t0[x] - t1[x]; }   // Eq. 6
-                else               { d0 = t0[x] - t1[x]; d1 = t2[x]; }                   // Eq. 5
-                cr[0][x] += d0; cur[0][x] |= (uint64_t)(cr[0][x] & 0xFF) << sh; cr[0][x] >>= 8;
-                cr[1][x] += d1; cur[1][x] |= (uint64_t)(cr[1][x] & 0xFF) << sh; cr[1][x] >>= 8;
-                t0[x] = t1[x] = t2[x] = 0;
-            }
+        for (int x = 0; x < EPT; x++) t0[x] = t1[x] = t2[x] = 0;
+        int32_t v[EPT];
+        for (int c = cntq[r]; c > 0; c--) {
+            next(v);
+#pragma unroll
+            for (int x = 0; x < EPT; x++) t0[x] += v[x];
+        }
+        for (int c = cntq[(s + 2) + r]; c > 0; c--) {
+            next(v);
+#pragma unroll
+            for (int x = 0; x < EPT; x++) t1[x] += v[x];
+        }
+        for (int c = cntq[2 * (s + 2) + r]; c > 0; c--) {
+            next(v);
+#pragma unroll
+            for (int x = 0; x < EPT; x++) t2[x] += v[x];
+        }
+        int64_t d[2][EPT];
+#pragma unroll
+        for (int x = 0; x < EPT; x++) {
+            if (F.method == 3) { d[0][x] = t0[x] - t1[x]; d[1][x] = t2[x] - t0[x] - t1[x]; }   // Eq. 6
+            else               { d[0][x] = t0[x] - t1[x]; d[1][x] = t2[x]; }                   // Eq. 5
+        }
+        if (!(b & 1) && r > 2) {                      // first of a pair: keep it
+#pragma unroll
+            for (int x = 0; x < EPT; x++) { pend[0][x] = d[0][x]; pend[1][x] = d[1][x]; }
+            continue;
+        }
+        const int sh = 8 * (b & 7);                  // bit offset of this diagonal's byte in cur
+        if (b & 1) {                                  // pair (b-1, b): 16 bits at bit 8 (b-1)
+#pragma unroll
+            for (int p = 0; p < 2; p++)
+#pragma unroll
+                for (int x = 0; x < EPT; x++) {
+                    const int64_t acc = cr[p][x] + pend[p][x] + d[p][x] * 256;
+                    cur[p][x] |= (uint64_t)(acc & 0xFFFF) << (sh - 8);
+                    cr[p][x] = acc >> 16;
+                }
+        } else {                                      // unpaired last diagonal (r = 2, b even)
+#pragma unroll
+            for (int p = 0; p < 2; p++)
+#pragma unroll
+                for (int x = 0; x < EPT; x++) {
+                    const int64_t acc = cr[p][x] + d[p][x];
+                    cur[p][x] |= (uint64_t)(acc & 0xFF) << sh;
+                    cr[p][x] = acc >> 8;
+                }
+        }
+        if ((b & 7) == 7 || r == 2) {                 // a 64-bit limb complete (or the last one)
             if ((b & 7) == 7) {
                 if (live) {
 #pragma unroll
@@ -717,7 +761,6 @@ fold_normalize_kernel(const FoldParams F)
 #pragma unroll
                 for (int x = 0; x < EPT; x++) cur[0][x] = cur[1][x] = 0;
             }
-            b++;
         }
     }
     if (!live) return;
@@ -781,8 +824,8 @@ fold_normalize_kernel(const FoldParams F)
 }
 
 size_t fold_smem(int s, int cols, int64_t nslots) {
-    (void)s;
-    return (size_t)kFoldRing * kFoldPer * cols * 4 + (size_t)nslots + 32 + (size_t)2 * kFoldRing * 8 + 16;
+    const size_t ntab = (size_t)std::max<int64_t>(nslots, (int64_t)kMaxJobs * (s + 2));
+    return (size_t)kFoldRing * kFoldPer * cols * 4 + ntab + 32 + (size_t)2 * kFoldRing * 8 + 16;
 }
 
 template <int COLS, bool BETA>
