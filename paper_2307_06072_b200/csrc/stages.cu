@@ -620,7 +620,7 @@ template <> struct IntVec<2> { using T = int2; MPC_DEV static void get(const T &
 template <> struct IntVec<4> { using T = int4; MPC_DEV static void get(const T &v, int32_t (&o)[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; } };
 
 template <int COLS, bool BETA, int EPT = kFoldEPT>
-__global__ void __launch_bounds__(COLS / EPT + 32)
+__global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : 6)
 fold_normalize_kernel(const FoldParams F)
 {
     constexpr int NCONS = COLS / EPT;                 // consumer threads
