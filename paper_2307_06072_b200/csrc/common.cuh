@@ -46,7 +46,11 @@ struct WorkUnit {
     int32_t job_g, tm, tn, r, a, b, slot0, slot1;
 };
 __host__ __device__ __forceinline__ int unit_job(const WorkUnit &w) { return w.job_g & 0xFF; }
-__host__ __device__ __forceinline__ int unit_G(const WorkUnit &w) { return w.job_g >> 8; }
+__host__ __device__ __forceinline__ int unit_G(const WorkUnit &w) { return (w.job_g >> 8) & 0xFF; }
+// serpentine k order: units of alternate diagonal pairs walk their k-blocks downward, so a group
+// starts on the k-blocks the previous group (the neighbouring diagonals) read last -- still in L2
+__host__ __device__ __forceinline__ bool unit_rev(const WorkUnit &w) { return (w.job_g >> 16) & 1; }
+__host__ __device__ __forceinline__ int unit_kb(const WorkUnit &w, int i) { return unit_rev(w) ? w.b - 1 - i : w.a + i; }
 
 struct JobDesc {
     int32_t npairs;

@@ -197,6 +197,7 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
     auto in_tri = [&](int64_t tm, int r) {
         return key.sblk.empty() || r <= key.sblk[(size_t)((tm * key.BM) >> kSBlkShift)] + 1;
     };
+    const bool serp = env_int("MPCGEMM_SERPENTINE", 1) != 0;
     for (const Segment &sg : segs) {
         const int q = sg.q, r = sg.r;
         const int64_t np = P.jobs[q].npairs;
@@ -206,12 +207,13 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
                 for (int64_t tm = 0; tm < tiles_m; tm++)
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
                         if (!in_tri(tm, r)) continue;
+                        const int32_t rev = serp && ((r >> 1) & 1) ? (1 << 16) : 0;
                         if (!in_tri(tm, r + 1)) {              // block's last diagonal is r: D_r alone
-                            units.push_back({q | (3 << 8), (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
+                            units.push_back({q | (3 << 8) | rev, (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
                             P.mma += np * (b - a) * (r - 1) * (kBK / 32);
                             continue;
                         }
-                        units.push_back({q | (2 << 8), (int32_t)tm, (int32_t)tn, r, a, b,
+                        units.push_back({q | (2 << 8) | rev, (int32_t)tm, (int32_t)tn, r, a, b,
                                          base(q, r) + (int32_t)c, base(q, r + 1) + (int32_t)c});
                         P.mma += np * (b - a) * (2 * r - 1) * (kBK / 32);
                     }

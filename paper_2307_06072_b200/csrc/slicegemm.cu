@@ -102,14 +102,14 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 const JobDesc &J = P.jobs[unit_job(w)];
                 if (unit_G(w) == 2) {
                     for (int pr = 0; pr < J.npairs; pr++)
-                        for (int kb = w.a; kb < w.b; kb++)
+                        for (int i = 0; i < w.b - w.a; i++)
                             for (int p = 1; p <= w.r; p++)          // A_p, B_{r+1-p}
-                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), kb, w.tm, w.tn);
+                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), unit_kb(w, i), w.tm, w.tn);
                 } else if (unit_G(w) == 3) {                        // D_r alone over kb in [a, b)
                     for (int pr = 0; pr < J.npairs; pr++)
-                        for (int kb = w.a; kb < w.b; kb++)
+                        for (int i = 0; i < w.b - w.a; i++)
                             for (int p = 1; p < w.r; p++)           // A_p, B_{r-p}
-                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1), kb, w.tm, w.tn);
+                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1), unit_kb(w, i), w.tm, w.tn);
                 } else {
                     const int per_pair = (w.r - 1) * KB;
                     for (int g = w.a; g < w.b; g++) {
@@ -144,13 +144,13 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 if (unit_G(w) == 2) {
                     int prev = 0;
                     for (int pr = 0; pr < J.npairs; pr++)
-                        for (int kb = w.a; kb < w.b; kb++)
+                        for (int i = 0; i < w.b - w.a; i++)
                             for (int p = 1; p <= w.r; p++) {
                                 mbar_wait(&full[stage], phase);
                                 tc_fence_after();
                                 const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                                 const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                                const bool first = (pr == 0 && kb == w.a);
+                                const bool first = (pr == 0 && i == 0);
 #pragma unroll
                                 for (int kk = 0; kk < kBK / 32; kk++)   // D_{r+1} += A_p B_{r+1-p}
                                     mma_i8(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
@@ -323,14 +323,14 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 const JobDesc &J = P.jobs[unit_job(w)];
                 if (unit_G(w) == 2) {
                     for (int pr = 0; pr < J.npairs; pr++)
-                        for (int kb = w.a; kb < w.b; kb++)
+                        for (int i = 0; i < w.b - w.a; i++)
                             for (int p = 1; p <= w.r; p++)          // A_p, B_{r+1-p}
-                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), kb, w.tm, w.tn);
+                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), unit_kb(w, i), w.tm, w.tn);
                 } else if (unit_G(w) == 3) {                        // D_r alone over kb in [a, b)
                     for (int pr = 0; pr < J.npairs; pr++)
-                        for (int kb = w.a; kb < w.b; kb++)
+                        for (int i = 0; i < w.b - w.a; i++)
                             for (int p = 1; p < w.r; p++)           // A_p, B_{r-p}
-                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1), kb, w.tm, w.tn);
+                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1), unit_kb(w, i), w.tm, w.tn);
                 } else {
                     const int per_pair = (w.r - 1) * KB;
                     for (int g = w.a; g < w.b; g++) {
@@ -365,13 +365,13 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 if (unit_G(w) == 2) {
                     int prev = 0;
                     for (int pr = 0; pr < J.npairs; pr++)
-                        for (int kb = w.a; kb < w.b; kb++)
+                        for (int i = 0; i < w.b - w.a; i++)
                             for (int p = 1; p <= w.r; p++) {
                                 mbar_wait(&full[stage], phase);
                                 tc_fence_after();
                                 const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                                 const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                                const bool first = (pr == 0 && kb == w.a);
+                                const bool first = (pr == 0 && i == 0);
 #pragma unroll
                                 for (int kk = 0; kk < kBK / 32; kk++)   // D_{r+1} += A_p B_{r+1-p}
                                     mma_i8_2sm(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
