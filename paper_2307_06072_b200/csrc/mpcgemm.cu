@@ -173,6 +173,13 @@ bool g2_enabled() { return env_int("MPCGEMM_G2", 1) != 0; }
 int build_plan(int dev, const PlanKey &key, Plan **out) {
     auto it = g_plans.find({dev, key});
     if (it != g_plans.end()) { *out = &it->second; return 0; }
+    if (g_plans.size() >= 512) {                       // bound the cache (many shapes, e.g. LU updates)
+        cudaDeviceSynchronize();                       // queued kernels may still read a plan's units
+        for (auto &kv : g_plans) {
+            cudaFree(kv.second.d_units); cudaFree(kv.second.d_counter); cudaFree(kv.second.d_slotinfo);
+        }
+        g_plans.clear();
+    }
     Plan P;
     method_jobs(key.method, P);
     const int s = key.s;
