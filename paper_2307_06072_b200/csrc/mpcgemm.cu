@@ -454,9 +454,9 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     SL.digA = tA; SL.digB = tB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
     SL.grid = plan->grid; SL.BM = 128; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits; SL.units_flat = plan->d_units;
     CK(slicegemm_launch(SL, st));
-    std::vector<unsigned long long> init(3 * nb), h(3 * nb);
-    for (int64_t b = 0; b < nb; b++) { init[b] = ~0ull; init[nb + b] = ~0ull; init[2 * nb + b] = (unsigned long long)-1ll; }
-    CK(cudaMemcpyAsync(mv.omin, init.data(), 8 * 3 * nb, cudaMemcpyHostToDevice, st));
+    std::vector<unsigned long long> h(3 * nb);
+    // minima start at ~0, the max-plus maximum at -1: all bytes 0xFF (no pageable host copy)
+    CK(cudaMemsetAsync(mv.omin, 0xFF, 8 * 3 * nb, st));
     CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 1,
                              mv.omin, mv.omin1, mv.omax2, st));
     CK(cudaMemcpyAsync(h.data(), mv.omin, 8 * nb, cudaMemcpyDeviceToHost, st));
@@ -469,7 +469,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
         any0 = any0 || out->minT[b] == 0;
     }
     if (any0 || full) {
-        CK(cudaMemcpyAsync(mv.omin, init.data(), 8 * 3 * nb, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(mv.omin, 0xFF, 8 * 3 * nb, st));
         CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 2,
                                  mv.omin, mv.omin1, mv.omax2, st));
         CK(cudaMemcpyAsync(h.data(), mv.omin, 8 * 3 * nb, cudaMemcpyDeviceToHost, st));
