@@ -27,6 +27,10 @@ cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, 
 cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
                          const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st);
 
+// 3-D TMA map over ABI limbs (implemented in slicegemm.cu; map = CUtensorMap*, 64-byte aligned)
+int encode_limb_map(void *map, const uint64_t *base, int L, uint64_t d1, uint64_t d2, uint64_t stride1,
+                    uint64_t stride2, int b1, int b2);
+
 // a-2: pre-pass planes: t[lines][kp] int8 and relative entry exponents rel[lines][kp] int32
 cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
                                   const int64_t *eline, int8_t *t, int32_t *rel, cudaStream_t st);

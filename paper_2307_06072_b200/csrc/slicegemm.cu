@@ -550,6 +550,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
+// 3-D map over the uint64 limbs of ABI entries for the staged split (stages.cu): dims {L, d1, d2},
+// strides (bytes) of dims 1, 2; box {L, b1, b2}; the swizzle matches the 8L-byte rows (L = 16: 128B,
+// 8: 64B, 4: 32B, 2: none).  Returns 0 on success.
+int encode_limb_map(void *map, const uint64_t *base, int L, uint64_t d1, uint64_t d2, uint64_t stride1,
+                    uint64_t stride2, int b1, int b2) {
+    auto enc = get_encode();
+    if (!enc) return -1;
+    CUtensorMapSwizzle sw = L == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : L == 8 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : L == 4 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+    cuuint64_t dims[3] = {(cuuint64_t)L, (cuuint64_t)d1, (cuuint64_t)d2};
+    cuuint64_t strides[2] = {(cuuint64_t)stride1, (cuuint64_t)stride2};
+    cuuint32_t box[3] = {(cuuint32_t)L, (cuuint32_t)b1, (cuuint32_t)b2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(reinterpret_cast<CUtensorMap *>(map), CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t *>(base),
+                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 // 3-D map over digit planes int8 [planes][rows][kp] with box {128, box_rows, 1}, 128B swizzle
 static int make_plane_map(CUtensorMap *map, const int8_t *base, int64_t planes, int64_t rows, int64_t kp, int box_rows) {
     auto enc = get_encode();

@@ -5,6 +5,8 @@
 //   a-5/a-6 fold_normalize  exact fold of the slice products with the Eq. 5/6
 //                        combination, carry propagation and one RNE rounding
 #include <climits>
+#include <cstdlib>
+#include <cuda.h>
 #include "common.cuh"
 #include "kernels.h"
 
@@ -227,10 +229,168 @@ split_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, i
     }
 }
 
+// TMA-staged split (L in {2, 4, 8, 16}): a CTA takes kSplitT consecutive k of one line; one thread
+// issues two 3-D TMA loads (Re, Im) of the 256 entries' limbs into shared memory -- coalesced,
+// vectorised, every DRAM sector read once; the rows land swizzled (the swizzle span = one 8L-byte
+// entry row) so that the per-word reads of consecutive entries by consecutive lanes spread over
+// the banks -- while each thread loads its entry's exponent and sign.  Thread t then streams the
+// words of entry k0 + t (same word arithmetic as split_kernel) and writes one byte per digit
+// plane: a warp writes 32 consecutive bytes (one sector) of a plane row per store.
+constexpr int kSplitT = 128;           // k per CTA = threads per CTA
+
+template <int L>
+__global__ void __launch_bounds__(kSplitT)
+split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant__ CUtensorMap mim, DMat re, DMat im,
+                 int side, int64_t lines, int64_t k, int64_t kp, const int64_t *__restrict__ eline, int s, int nparts,
+                 int8_t *__restrict__ dig)
+{
+    extern __shared__ uint8_t tsm_raw[];
+    uint8_t *tile = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int ROW = 8 * L;                        // bytes per entry row
+    constexpr int SWM = L == 16 ? 7 : L == 8 ? 3 : L == 4 ? 1 : 0;   // 16-byte chunk XOR mask
+    // digit staging, double-buffered: [2][3 parts][8 planes][kSplitT bytes]
+    uint8_t *stage = tile + 2 * kSplitT * ROW;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(stage + 2 * 3 * 8 * kSplitT);
+    const int tid = threadIdx.x;
+    const int64_t line = blockIdx.y;
+    const int64_t k0 = (int64_t)blockIdx.x * kSplitT;
+    if (tid == 0) { mbar_init(bar, 1); fence_barrier_init(); }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_arrive_expect_tx(bar, 2u * kSplitT * ROW);
+        if (side == 0) {                              // dims {L, k, rows}: coords (0, k0, line)
+            tma_load_3d(tile, &mre, bar, 0, (int)k0, (int)line);
+            tma_load_3d(tile + kSplitT * ROW, &mim, bar, 0, (int)k0, (int)line);
+        } else {                                      // dims {L, n, k}: coords (0, line, k0)
+            tma_load_3d(tile, &mre, bar, 0, (int)line, (int)k0);
+            tma_load_3d(tile + kSplitT * ROW, &mim, bar, 0, (int)line, (int)k0);
+        }
+    }
+    const int64_t kk = k0 + tid;
+    const bool valid = kk < k;
+    int64_t ex[2] = {0, 0};
+    bool neg[2] = {false, false};
+    if (valid) {
+#pragma unroll
+        for (int p = 0; p < 2; p++) {
+            const DMat &M = p ? im : re;
+            const int64_t idx = side == 0 ? line * M.ld + kk : kk * M.ld + line;
+            ex[p] = __ldg(M.exp + idx);
+            neg[p] = __ldg(M.sign + idx) != 0;
+        }
+    }
+    const int64_t e = eline[line];
+    const int64_t W = 8 * (int64_t)s - 3;
+    mbar_wait(bar, 0);
+    // limb l of this thread's entry in part p (swizzled shared-memory address)
+    auto limb = [&](int p, int64_t l) -> uint64_t {
+        if (l < 0 || l >= L) return 0ull;
+        const uint32_t o = (uint32_t)(tid * ROW + 8 * l);
+        const uint32_t so = o ^ (((o >> 7) & SWM) << 4);
+        return *reinterpret_cast<const uint64_t *>(tile + (size_t)p * kSplitT * ROW + so);
+    };
+    int64_t li[2]; int bo[2]; uint64_t lo[2], nc[2] = {1, 1};
+    bool zero[2];
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        zero[p] = !valid || limb(p, L - 1) == 0;
+        const int64_t pos0 = 64 * (int64_t)L - W + e - ex[p];
+        li[p] = pos0 >= 0 ? (pos0 >> 6) : -((-pos0 + 63) >> 6);
+        bo[p] = (int)(pos0 - (li[p] << 6));
+        lo[p] = zero[p] ? 0ull : limb(p, li[p]);
+        neg[p] = neg[p] && !zero[p];
+    }
+    uint64_t csum = 0, ch[3] = {0, 0, 0};
+    const int64_t plane = lines * kp;
+    const int64_t rowlen = min((int64_t)kSplitT, kp - k0);          // bytes of this CTA's plane rows
+    const int nwords = (s + 7) / 8;
+    for (int w = 0; w < nwords; w++) {
+        uint8_t *stg = stage + (w & 1) * (3 * 8 * kSplitT);
+        uint64_t y[3];
+#pragma unroll
+        for (int p = 0; p < 2; p++) {
+            const uint64_t hi = zero[p] ? 0ull : limb(p, li[p] + 1);
+            uint64_t x = bo[p] ? ((lo[p] >> bo[p]) | (hi << (64 - bo[p]))) : lo[p];
+            lo[p] = hi; li[p]++;
+            if (neg[p]) { const uint64_t t = ~x + nc[p]; nc[p] = (nc[p] && t == 0) ? 1ull : 0ull; x = t; }
+            y[p] = x;
+        }
+        {   // 3M: Re + Im (two's complement, with carry)
+            const uint64_t t = y[0] + y[1];
+            const uint64_t c1 = t < y[0];
+            y[2] = t + csum;
+            csum = c1 | (y[2] < t);
+        }
+#pragma unroll
+        for (int p = 0; p < 3; p++) {                 // + H with carry, XOR 0x80 per byte -> staging
+            if (p >= nparts) break;
+            const uint64_t t = y[p] + kH;
+            const uint64_t c1 = t < y[p];
+            const uint64_t z = t + ch[p];
+            ch[p] = c1 | (z < t);
+            const uint64_t d = z ^ kH;
+#pragma unroll
+            for (int bt = 0; bt < 8; bt++) stg[(p * 8 + bt) * kSplitT + tid] = (uint8_t)(d >> (8 * bt));
+        }
+        __syncthreads();
+        // plane rows of this word: (part p, byte bt) -> plane s-1-(8w+bt), 16-byte vector stores
+        const int nb = min(8, s - 8 * w);
+        const int vec_per_row = (int)((rowlen + 15) / 16);
+        for (int q = tid; q < nparts * 8 * vec_per_row; q += kSplitT) {
+            const int row = q / vec_per_row, v = q - row * vec_per_row;
+            const int p = row >> 3, bt = row & 7;
+            if (bt >= nb) continue;
+            int8_t *o = dig + ((int64_t)p * s + (s - 1 - 8 * w - bt)) * plane + line * kp + k0 + 16 * v;
+            const uint4 val = *reinterpret_cast<const uint4 *>(stg + (p * 8 + bt) * kSplitT + 16 * v);
+            if (16 * v + 16 <= rowlen) *reinterpret_cast<uint4 *>(o) = val;
+            else {
+                const uint8_t *vb = reinterpret_cast<const uint8_t *>(&val);
+                for (int x = 0; 16 * v + x < rowlen; x++) o[x] = (int8_t)vb[x];
+            }
+        }
+        // (the other staging buffer is written next; the one stored here is rewritten only after
+        //  the next word's __syncthreads)
+    }
+}
+
+template <int L>
+static cudaError_t split_tma_launch_t(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp,
+                                      const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st)
+{
+    alignas(64) uint8_t mre[128], mim[128];           // CUtensorMap storage
+    for (int p = 0; p < 2; p++) {
+        const DMat &M = p ? im : re;
+        int rc;
+        if (side == 0)      // A (lines x k): dims {L, k, lines}
+            rc = encode_limb_map(p ? mim : mre, M.limbs, L, (uint64_t)k, (uint64_t)lines, 8ull * L, 8ull * L * M.ld, kSplitT, 1);
+        else                // B (k x lines): dims {L, lines, k}
+            rc = encode_limb_map(p ? mim : mre, M.limbs, L, (uint64_t)lines, (uint64_t)k, 8ull * L, 8ull * L * M.ld, 1, kSplitT);
+        if (rc) return cudaErrorInvalidValue;
+    }
+    const size_t sm = 1024 + 2 * (size_t)kSplitT * 8 * L + 2 * 3 * 8 * kSplitT + 64;
+    cudaError_t e = cudaFuncSetAttribute(split_tma_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((kp + kSplitT - 1) / kSplitT), (unsigned)lines);
+    split_tma_kernel<L><<<grid, kSplitT, sm, st>>>(*reinterpret_cast<const CUtensorMap *>(mre),
+                                                   *reinterpret_cast<const CUtensorMap *>(mim), re, im, side, lines, k, kp,
+                                                   eline, s, nparts, dig);
+    return cudaGetLastError();
+}
+
 cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
                          const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st)
 {
     if (lines == 0 || kp == 0) return cudaSuccess;
+    const bool tma_ok = lines < 65536 && getenv("MPCGEMM_SPLIT_V1") == nullptr &&
+                        !(reinterpret_cast<uintptr_t>(re.limbs) & 15) && !(reinterpret_cast<uintptr_t>(im.limbs) & 15);
+    if (tma_ok) {
+        cudaError_t e = cudaErrorNotSupported;
+        if (L == 16) e = split_tma_launch_t<16>(re, im, side, lines, k, kp, eline, s, nparts, dig, st);
+        else if (L == 8) e = split_tma_launch_t<8>(re, im, side, lines, k, kp, eline, s, nparts, dig, st);
+        else if (L == 4) e = split_tma_launch_t<4>(re, im, side, lines, k, kp, eline, s, nparts, dig, st);
+        else if (L == 2) e = split_tma_launch_t<2>(re, im, side, lines, k, kp, eline, s, nparts, dig, st);
+        if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
+    }
     const int64_t threads = (kp + kSplitVec - 1) / kSplitVec;
     dim3 grid((unsigned)((threads + 127) / 128), (unsigned)(lines < 65535 ? lines : 65535));
     split_kernel<<<grid, 128, 0, st>>>(re, im, side, lines, k, kp, L, eline, s, nparts, dig);
