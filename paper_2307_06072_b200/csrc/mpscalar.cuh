@@ -265,35 +265,6 @@ MPC_DEV void cfms_part(int L, int part, const Num<C> *a, const Num<C> &xr, const
     sum_round(t, cnt, prec, L, buf, NW<C>::v, so, eo, lo);
 }
 
-// (out_re, out_im) = a - x y   (a == nullptr: x y)
-template <int C>
-MPC_DEV void cfms(int L, const Num<C> *ar, const Num<C> *ai, const Num<C> &xr, const Num<C> &xi,
-                  const Num<C> &yr, const Num<C> &yi, int prec,
-                  uint8_t *s_re, int64_t *e_re, uint64_t *l_re, uint8_t *s_im, int64_t *e_im, uint64_t *l_im)
-{
-    uint64_t p1[2 * C], p2[2 * C], pa[C], buf[NW<C>::v];
-    Term t[3];
-    const bool sub = ar != nullptr;              // a - (x y): the products enter negated
-    // real part: ar - xr yr + xi yi
-    t[0] = prod_term<C>(L, xr, yr, sub, p1);
-    t[1] = prod_term<C>(L, xi, yi, !sub, p2);
-    int cnt = 2;
-    if (sub) t[cnt++] = term_of<C>(L, *ar, pa);
-    uint8_t s0; int64_t e0; uint64_t r0[C];
-    sum_round(t, cnt, prec, L, buf, NW<C>::v, &s0, &e0, r0);
-    // imaginary part: ai - xr yi - xi yr
-    t[0] = prod_term<C>(L, xr, yi, sub, p1);
-    t[1] = prod_term<C>(L, xi, yr, sub, p2);
-    cnt = 2;
-    if (sub) t[cnt++] = term_of<C>(L, *ai, pa);
-    uint8_t s1; int64_t e1; uint64_t r1[C];
-    sum_round(t, cnt, prec, L, buf, NW<C>::v, &s1, &e1, r1);
-    *s_re = s0; *e_re = e0;
-    *s_im = s1; *e_im = e1;
-#pragma unroll
-    for (int q = 0; q < C; q++) if (q < L) { l_re[q] = r0[q]; l_im[q] = r1[q]; }
-}
-
 // ---------------------------------------------------------------- division (reciprocal)
 // Knuth's algorithm D on 32-bit digits: q = floor(u / v), returns remainder != 0.
 // u: m + n digits (u[m+n] scratch digit appended by the caller), v: n digits, v[n-1] != 0.
@@ -428,15 +399,6 @@ MPC_DEV void crecip_part(int L, int part, const Num<C> &zr, const Num<C> &zi, in
     }
     for (int q = 0; q < L; q++) na[q] = num.m[q];
     div_round<C>(L, na, L, num.e, part ? !num.neg : num.neg, D, dn, de, drop, prec, so, eo, lo);
-}
-
-// (re, im) = 1 / (zr + i zi), z != 0
-template <int C>
-MPC_DEV void crecip(int L, const Num<C> &zr, const Num<C> &zi, int prec,
-                    uint8_t *s_re, int64_t *e_re, uint64_t *l_re, uint8_t *s_im, int64_t *e_im, uint64_t *l_im)
-{
-    crecip_part<C>(L, 0, zr, zi, prec, s_re, e_re, l_re);
-    crecip_part<C>(L, 1, zr, zi, prec, s_im, e_im, l_im);
 }
 
 // ---------------------------------------------------------------- pivot key
