@@ -790,15 +790,14 @@ fold_normalize_kernel(const FoldParams F)
     const int Lw = BETA ? Lc0 + F.L + 3 : 0;          // NEXT-2 sum window
     const int nslots = (int)F.nslots;
     int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                                   // [RING][PER][COLS]
-    uint8_t *cntq = reinterpret_cast<uint8_t *>(fsm_raw + kFoldRing * kFoldPer * COLS * 4);  // [job][s+2] chunk counts
-    const int ntab = nslots > kMaxJobs * (s + 2) ? nslots : kMaxJobs * (s + 2);
-    uint64_t *full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(cntq + ntab) + 15) & ~uintptr_t(15));
+    uint16_t *cntq = reinterpret_cast<uint16_t *>(fsm_raw + kFoldRing * kFoldPer * COLS * 4);  // [job][s+2] chunk counts
+    uint64_t *full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(cntq + kMaxJobs * (s + 2)) + 15) & ~uintptr_t(15));
     uint64_t *empty = full + kFoldRing;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     // chunk count of every (job, diagonal): the slots come in the order r = s+1..2, job, chunk
     for (int x = tid; x < kMaxJobs * (s + 2); x += blockDim.x)
-        cntq[x] = (uint8_t)((x % (s + 2)) < 2 ? 0 : F.slotinfo[x * 2 + 1]);
+        cntq[x] = (uint16_t)((x % (s + 2)) < 2 ? 0 : F.slotinfo[x * 2 + 1]);
     if (tid == 0) {
         for (int e = 0; e < kFoldRing; e++) { mbar_init(&full[e], 1); mbar_init(&empty[e], NCONS / 32); }
         fence_barrier_init();
@@ -984,8 +983,8 @@ fold_normalize_kernel(const FoldParams F)
 }
 
 size_t fold_smem(int s, int cols, int64_t nslots) {
-    const size_t ntab = (size_t)std::max<int64_t>(nslots, (int64_t)kMaxJobs * (s + 2));
-    return (size_t)kFoldRing * kFoldPer * cols * 4 + ntab + 32 + (size_t)2 * kFoldRing * 8 + 16;
+    (void)nslots;
+    return (size_t)kFoldRing * kFoldPer * cols * 4 + 2 * (size_t)kMaxJobs * (s + 2) + 32 + (size_t)2 * kFoldRing * 8 + 16;
 }
 
 template <int COLS, bool BETA>

@@ -377,6 +377,17 @@ def test_long_k_exactness_chunks(method):
     assert sampled_equal(C, Rs, si, sj) is None
 
 
+def test_very_long_k_many_chunks():
+    """k = 800000 (6250 k-blocks): the longest diagonals are cut into > 255 exactness chunks each."""
+    m, n, k, prec = 2, 3, 800000, 320
+    A = mpgen.random_cmat(21, 1, m, k, prec, 1)
+    B = mpgen.random_cmat(21, 2, k, n, prec, 1)
+    C, rep = run_gpu(A, B, prec, "3M")
+    si, sj = np.array([0, 1]), np.array([2, 0])
+    Rs = oracle.ozaki(A, B, prec, "3M", rep["slices"], samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
+
+
 # ------------------------------------------------------------------ NEXT-2: C := C0 +- A B
 def _c0_variants(m, n, prec, A, B, method):
     out = {"near": oracle.exact(A, B, prec, method)}                 # heavy cancellation
