@@ -187,6 +187,8 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
     const int64_t tiles_m = (key.m + key.BM - 1) / key.BM, tiles_n = (key.n + key.BN - 1) / key.BN;
     std::vector<int32_t> slotinfo((size_t)kMaxJobs * (s + 2) * 2, 0);
     const std::vector<Segment> segs = diag_segments(P, KB, s, key.method, key.maxkb, key.g2);
+    for (const Segment &sg : segs)                     // the fold's chunk-count table is 16-bit
+        if (sg.nch > 65535) return fail(MPCGEMM_ERR_ARG, "k too large: more than 65535 exactness chunks per diagonal");
     // slot numbers follow the fold's consumption order: r = s+1 .. 2, job, chunk
     for (const Segment &sg : segs)
         for (int d = 0; d < sg.G; d++) slotinfo[(sg.q * (s + 2) + sg.r + d) * 2 + 1] = (int32_t)sg.nch;
