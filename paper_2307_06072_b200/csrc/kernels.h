@@ -83,7 +83,11 @@ cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r
                             cudaStream_t st);
 cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0, int64_t t1, int64_t c,
                              int prec, cudaStream_t st);
-struct SolveScratch { DMatOut rre, rim; /* 1 x n: 1 / U_cc */ DMatOut xre, xim; /* n x nrhs: solution rows */ };
+struct SolveScratch {
+    DMatOut rre, rim;            // 1 x n: 1 / U_cc
+    DMatOut xre, xim;            // n x nrhs: the permuted right-hand sides, then the solution rows
+    int64_t *perm;               // n: the row permutation P
+};
 cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const int64_t *ipiv, DMatOut bre, DMatOut bim,
                             int64_t nrhs, int prec, SolveScratch s, cudaStream_t st);
 cudaError_t mp_scalar_launch(int L, int op, int64_t cnt, int prec, DMatOut Ar, DMatOut Ai, DMatOut Xr, DMatOut Xi,

@@ -51,19 +51,27 @@ __global__ void __launch_bounds__(1024) lu_pivot_kernel(int L, DMatOut re, DMatO
 }
 
 // ---------------------------------------------------------------- row swap (all columns)
+// one thread per (column, part, limb): every word of the two rows moves independently (a
+// per-element loop over the limbs was a chain of dependent load/store pairs, ~8 us per column)
 __global__ void lu_swap_kernel(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t c, const int64_t *ipiv)
 {
     const int64_t p = ipiv[c];
     if (p == c) return;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ncols; t += (int64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-        for (int part = 0; part < 2; part++) {
-            const DMatOut &M = part ? im : re;
-            El a = el(L, M, c, t), b = el(L, M, p, t);
-            const uint8_t ts = *a.s; *a.s = *b.s; *b.s = ts;
-            const int64_t te = *a.e; *a.e = *b.e; *b.e = te;
-#pragma unroll
-            for (int q = 0; q < L; q++) { const uint64_t x = a.l[q]; a.l[q] = b.l[q]; b.l[q] = x; }
+    const int64_t per = 2 * (int64_t)L;               // words per column (both parts)
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ncols * per; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = g / per;
+        const int w = (int)(g - t * per);
+        const int part = w >= L;
+        const int l = w - part * L;
+        const DMatOut &M = part ? im : re;
+        uint64_t *a = M.limbs + (c * M.ld + t) * L + l, *b = M.limbs + (p * M.ld + t) * L + l;
+        const uint64_t x = *a, y = *b;
+        *a = y; *b = x;
+        if (l == 0) {
+            const int64_t ia = c * M.ld + t, ib = p * M.ld + t;
+            const uint8_t sa = M.sign[ia], sb = M.sign[ib];
+            const int64_t ea = M.exp[ia], eb = M.exp[ib];
+            M.sign[ia] = sb; M.sign[ib] = sa; M.exp[ia] = eb; M.exp[ib] = ea;
         }
     }
 }
@@ -160,20 +168,34 @@ __global__ void lu_recip_all_kernel(int L, DMatOut fre, DMatOut fim, int64_t n, 
     crecip_part<C>(L, part, zr, zi, prec, o.s, o.e, o.l);
 }
 
-__global__ void lu_bswap_kernel(int L, DMatOut bre, DMatOut bim, int64_t n, int64_t nrhs, const int64_t *ipiv)
+// the row swaps of P, composed into one permutation (one thread: integer work only), then
+// applied as a parallel gather B -> X and a parallel copy X -> B
+__global__ void lu_perm_kernel(int64_t n, const int64_t *ipiv, int64_t *perm)
 {
-    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nrhs) return;
+    if (threadIdx.x || blockIdx.x) return;
+    for (int64_t i = 0; i < n; i++) perm[i] = i;
     for (int64_t c = 0; c < n; c++) {
         const int64_t p = ipiv[c];
-        if (p == c) continue;
-        for (int part = 0; part < 2; part++) {
-            const DMatOut &M = part ? bim : bre;
-            El a = el(L, M, c, q), b = el(L, M, p, q);
-            const uint8_t ts = *a.s; *a.s = *b.s; *b.s = ts;
-            const int64_t te = *a.e; *a.e = *b.e; *b.e = te;
-            for (int w = 0; w < L; w++) { const uint64_t x = a.l[w]; a.l[w] = b.l[w]; b.l[w] = x; }
-        }
+        if (p != c) { const int64_t t = perm[c]; perm[c] = perm[p]; perm[p] = t; }
+    }
+}
+
+// X row r := B row perm[r] (one thread per word)
+__global__ void lu_gather_kernel(int L, DMatOut bre, DMatOut bim, DMatOut xre, DMatOut xim, int64_t n, int64_t nrhs,
+                                 const int64_t *perm)
+{
+    const int64_t per = 2 * (int64_t)L;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n * nrhs * per) return;
+    const int64_t e = g / per;
+    const int w = (int)(g - e * per);
+    const int part = w >= L, l = w - part * L;
+    const int64_t r = e / nrhs, q = e - r * nrhs, src = perm[r];
+    const DMatOut &Bm = part ? bim : bre, &Xm = part ? xim : xre;
+    Xm.limbs[(r * Xm.ld + q) * L + l] = Bm.limbs[(src * Bm.ld + q) * L + l];
+    if (l == 0) {
+        Xm.sign[r * Xm.ld + q] = Bm.sign[src * Bm.ld + q];
+        Xm.exp[r * Xm.ld + q] = Bm.exp[src * Bm.ld + q];
     }
 }
 
@@ -285,7 +307,7 @@ cudaError_t lu_pivot_launch(int L, DMatOut re, DMatOut im, int64_t n, int64_t c,
 }
 
 cudaError_t lu_swap_launch(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t c, const int64_t *ipiv, cudaStream_t st) {
-    const unsigned g = (unsigned)((ncols + 255) / 256);
+    const unsigned g = (unsigned)((ncols * 2 * L + 255) / 256);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
     lu_swap_kernel<<<g, 256, 0, st>>>(L, re, im, ncols, c, ipiv);
     return cudaGetLastError();
@@ -327,7 +349,9 @@ cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const in
                             int64_t nrhs, int prec, SolveScratch s, cudaStream_t st) {
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
     MPC_DISPATCH_C(L, (lu_recip_all_kernel<C><<<(unsigned)((2 * n + 127) / 128), 128, 0, st>>>(L, fre, fim, n, prec, s.rre, s.rim)));
-    lu_bswap_kernel<<<(unsigned)((nrhs + 127) / 128), 128, 0, st>>>(L, bre, bim, n, nrhs, ipiv);
+    lu_perm_kernel<<<1, 1, 0, st>>>(n, ipiv, s.perm);
+    lu_gather_kernel<<<(unsigned)((n * nrhs * 2 * L + 255) / 256), 256, 0, st>>>(L, bre, bim, s.xre, s.xim, n, nrhs, s.perm);
+    lu_copy_kernel<<<(unsigned)((n * nrhs + 127) / 128), 128, 0, st>>>(L, s.xre, s.xim, bre, bim, n, nrhs);
     for (int64_t c = 0; c + 1 < n; c++)
         MPC_DISPATCH_C(L, (lu_fwd_kernel<C><<<(unsigned)((2 * (n - c - 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, c, n, nrhs, prec)));
     for (int64_t c = n - 1; c >= 0; c--)

@@ -1151,7 +1151,7 @@ int mpclu_solve(int64_t n, int64_t nrhs, int32_t prec, const mpc_cmat *LU, const
     {
         std::lock_guard<std::mutex> lock(g_mu);
         DevCache &dc = g_cache[dev];
-        if (int rc = grow(&dc.solve, &dc.solve_bytes, 2 * ents * (9 + 8 * (size_t)L) + 4096)) return rc;
+        if (int rc = grow(&dc.solve, &dc.solve_bytes, 2 * ents * (9 + 8 * (size_t)L) + 8 * (size_t)n + 8192)) return rc;
         base = (uint8_t *)dc.solve;
     }
     auto carve = [&](size_t cnt, int64_t ldm) {
@@ -1165,6 +1165,7 @@ int mpclu_solve(int64_t n, int64_t nrhs, int32_t prec, const mpc_cmat *LU, const
     SolveScratch sc;
     sc.rre = carve(n, n); sc.rim = carve(n, n);
     sc.xre = carve((size_t)n * nrhs, nrhs); sc.xim = carve((size_t)n * nrhs, nrhs);
+    sc.perm = (int64_t *)base;
     CK(lu_solve_launch(L, dmo(LU->re), dmo(LU->im), n, ipiv, dmo(B->re), dmo(B->im), nrhs, prec, sc, st));
     return 0;
 }
