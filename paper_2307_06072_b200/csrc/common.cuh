@@ -51,6 +51,10 @@ __host__ __device__ __forceinline__ int unit_G(const WorkUnit &w) { return (w.jo
 // starts on the k-blocks the previous group (the neighbouring diagonals) read last -- still in L2
 __host__ __device__ __forceinline__ bool unit_rev(const WorkUnit &w) { return (w.job_g >> 16) & 1; }
 __host__ __device__ __forceinline__ int unit_kb(const WorkUnit &w, int i) { return unit_rev(w) ? w.b - 1 - i : w.a + i; }
+// p-blocking of a G >= 2 unit: its planes p = 1 .. np (np = r for G = 2, r - 1 for G = 3) are
+// walked in nblk blocks, each over all its k-blocks, so one k-block step touches pblk planes
+__host__ __device__ __forceinline__ int unit_nblk(int np, int pblk) { return pblk > 0 && np > pblk ? (np + pblk - 1) / pblk : 1; }
+__host__ __device__ __forceinline__ int unit_pfirst(int np, int nblk, int j) { return j * np / nblk + 1; }
 
 struct JobDesc {
     int32_t npairs;
@@ -82,6 +86,14 @@ struct GemmParams {
     int32_t s;                 // slices
     int32_t KB;                // k-blocks per digit plane row
     int32_t partsA, partsB;    // number of digit parts stored per side
+    int32_t dbg;               // power experiments only (MPCGEMM_DBG, results invalid when != 0):
+                               // bit 0: epilogue skips the partial-plane stores; bit 1: every TMA
+                               // load reads plane 0 / tile (0, 0) (L2-resident operands); bit 2: loads
+                               // cycle through 8 planes x 2 k-blocks x 2 tiles (~1 MB, varying data)
+    int32_t *hot;              // k-phase hints, one per (job, r, chunk) group (or null): the position
+                               // (pair, p-block, k-block) a running unit of the group last started;
+                               // a new unit of the group begins there (CTA-pair kernel, G >= 2)
+    int32_t pblk;              // p-block length of the CTA-pair kernel's G >= 2 units (0: one block)
     JobDesc jobs[kMaxJobs];
 };
 
@@ -138,6 +150,14 @@ MPC_DEV uint32_t mapa_rank(uint32_t local_addr, uint32_t rank) {
 }
 MPC_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+MPC_DEV int32_t ld_relaxed_s32(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+MPC_DEV void st_relaxed_s32(int32_t *p, int32_t v) {
+    asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 MPC_DEV void st_remote_u32(uint32_t cluster_addr, uint32_t v) {
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");

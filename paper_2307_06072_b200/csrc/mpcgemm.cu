@@ -261,11 +261,12 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
     P.nunits = (int)flat.size(); P.nslots = nslots; P.grid = grid;
     if (P.nunits) {
         if (cudaMalloc(&P.d_units, sizeof(WorkUnit) * flat.size()) != cudaSuccess ||
-            cudaMalloc(&P.d_counter, sizeof(int32_t)) != cudaSuccess ||
+            cudaMalloc(&P.d_counter, sizeof(int32_t) * (1 + (size_t)nslots)) != cudaSuccess ||
             cudaMalloc(&P.d_slotinfo, sizeof(int32_t) * slotinfo.size()) != cudaSuccess)
             return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc plan");
         CK(cudaMemcpy(P.d_units, flat.data(), sizeof(WorkUnit) * flat.size(), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(P.d_slotinfo, slotinfo.data(), sizeof(int32_t) * slotinfo.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemset(P.d_counter, 0, sizeof(int32_t) * (1 + (size_t)nslots)));   // counter + k-phase hints
     }
     auto res = g_plans.emplace(std::make_pair(dev, key), P);
     *out = &res.first->second;
@@ -635,6 +636,9 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         SL.P.partials = partials; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
         SL.P.m = (int32_t)mr; SL.P.n = (int32_t)n; SL.P.s = s; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
         SL.P.partsA = SL.P.partsB = parts;
+        SL.P.dbg = env_int("MPCGEMM_DBG", 0);
+        SL.P.hot = env_int("MPCGEMM_KPHASE", 1) ? plan->d_counter + 1 : nullptr;
+        SL.P.pblk = env_int("MPCGEMM_PBLK", 32);
         for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
         SL.digA = digA; SL.digB = digB; SL.rowsA = mr; SL.rowsB = n; SL.kp = Lo.kp;
         SL.grid = plan->grid; SL.BM = geo.BM; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits;

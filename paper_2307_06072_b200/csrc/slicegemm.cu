@@ -266,7 +266,8 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     uint64_t *qfull = tempty + 1;                     // both CTAs (leader producer arrives on both)
     uint64_t *qempty = qfull + Cfg::QN;               // leader's used: 10 arrivals
     int32_t *uq = reinterpret_cast<int32_t *>(qempty + Cfg::QN);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(uq + Cfg::QN);
+    int32_t *uqr = uq + Cfg::QN;                      // each unit's k-phase rotation (both producers)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(uqr + Cfg::QN);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -287,6 +288,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const uint32_t lead_qempty = mapa_rank(smem_u32(qempty), 0);
     const uint32_t lead_tempty = mapa_rank(smem_u32(tempty), 0);
     const uint32_t peer_uq = mapa_rank(smem_u32(uq), 1);
+    const uint32_t peer_uqr = mapa_rank(smem_u32(uqr), 1);
     const uint32_t peer_qfull = mapa_rank(smem_u32(qfull), 1);
     const int s = P.s, KB = P.KB;
 
@@ -298,39 +300,64 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             auto load = [&](int planeA, int planeB, int kb, int tm, int tn) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+                if (P.dbg & 2) { planeA = planeB = 0; kb = 0; tm = tn = 0; }
+                if (P.dbg & 4) { planeA &= 7; planeB &= 7; kb &= 1; tm &= 1; tn &= 1; }   // ~1 MB of varying operands
                 tma_load_3d_2sm(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, tm * 256 + (int)rank * 128, planeA);
                 tma_load_3d_2sm(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, tn * 256 + (int)rank * 128, planeB);
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             };
             for (;;) {
-                int u;
+                int u, rot = 0;
                 if (rank == 0) {
                     u = atomicAdd(P.counter, 1);
                     if (u >= P.nunits) u = -1;
+                    if (u >= 0 && P.hot) {
+                        // k-phase alignment: begin at the (pair, k-block) position the group's
+                        // running units are on, so the units sharing a digit-plane tile read it
+                        // within one k-block step of each other (an L2 hit) whatever their start
+                        const WorkUnit &wu = P.units[u];
+                        if (unit_G(wu) >= 2) {
+                            const int nkb = wu.b - wu.a;
+                            const int npos = P.jobs[unit_job(wu)].npairs * unit_nblk(unit_G(wu) == 2 ? wu.r : wu.r - 1, P.pblk) * nkb;
+                            const int h = ld_relaxed_s32(P.hot + wu.slot0);
+                            rot = (h > 0 && h < npos) ? h : 0;
+                        }
+                    }
                     mbar_wait_cluster(&qempty[qs], qph ^ 1);
                     *reinterpret_cast<volatile int32_t *>(&uq[qs]) = u;
+                    *reinterpret_cast<volatile int32_t *>(&uqr[qs]) = rot;
                     st_remote_u32(peer_uq + 4 * qs, (uint32_t)u);
+                    st_remote_u32(peer_uqr + 4 * qs, (uint32_t)rot);
                     mbar_arrive(&qfull[qs]);
                     mbar_arrive_remote(peer_qfull + 8 * qs);
                 } else {
                     mbar_wait_cluster(&qfull[qs], qph);
                     u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
+                    rot = *reinterpret_cast<volatile int32_t *>(&uqr[qs]);
                     mbar_arrive_remote(lead_qempty + 8 * qs);
                 }
                 if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
                 if (u < 0) break;
                 const WorkUnit w = P.units[u];
                 const JobDesc &J = P.jobs[unit_job(w)];
-                if (unit_G(w) == 2) {
-                    for (int pr = 0; pr < J.npairs; pr++)
-                        for (int i = 0; i < w.b - w.a; i++)
-                            for (int p = 1; p <= w.r; p++)          // A_p, B_{r+1-p}
-                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p), unit_kb(w, i), w.tm, w.tn);
-                } else if (unit_G(w) == 3) {                        // D_r alone over kb in [a, b)
-                    for (int pr = 0; pr < J.npairs; pr++)
-                        for (int i = 0; i < w.b - w.a; i++)
-                            for (int p = 1; p < w.r; p++)           // A_p, B_{r-p}
-                                load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1), unit_kb(w, i), w.tm, w.tn);
+                if (unit_G(w) >= 2) {
+                    // positions (pair, p-block, k-block), t = 0 .. npos - 1 taken from rot on; D_r and
+                    // D_{r+1} (G = 2: A_p, B_{r+1-p}) or D_r alone (G = 3: A_p, B_{r-p}).  A G = 2
+                    // block that starts at p0 > 1 first loads A_{p0-1} (D_r's partner of B_{r+1-p0})
+                    const int g2 = unit_G(w) == 2;
+                    const int np = g2 ? w.r : w.r - 1, nkb = w.b - w.a, nblk = unit_nblk(np, P.pblk);
+                    const int npos = J.npairs * nblk * nkb;
+                    int pos = rot;
+                    for (int t = 0; t < npos; t++) {
+                        const int pb = pos / nkb, pr = pb / nblk, blk = pb - pr * nblk;
+                        const int kb = unit_kb(w, pos - pb * nkb);
+                        const int p0 = unit_pfirst(np, nblk, blk), p1 = unit_pfirst(np, nblk, blk + 1) - 1;
+                        if (rank == 0 && P.hot) st_relaxed_s32(P.hot + w.slot0, pos);
+                        if (g2 && p0 > 1) load(J.pa[pr] * s + p0 - 2, J.pb[pr] * s + (w.r - p0), kb, w.tm, w.tn);
+                        for (int p = p0; p <= p1; p++)
+                            load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1 + g2), kb, w.tm, w.tn);
+                        if (++pos == npos) pos = 0;
+                    }
                 } else {
                     const int per_pair = (w.r - 1) * KB;
                     for (int g = w.a; g < w.b; g++) {
@@ -355,6 +382,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             for (;;) {
                 mbar_wait_cluster(&qfull[qs], qph);
                 const int u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
+                const int rot = *reinterpret_cast<volatile int32_t *>(&uqr[qs]);
                 mbar_arrive(&qempty[qs]);
                 if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
                 if (u < 0) break;
@@ -363,31 +391,45 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 mbar_wait_cluster(tempty, tphase ^ 1);
                 tc_fence_after();
                 if (unit_G(w) == 2) {
-                    int prev = 0;
-                    for (int pr = 0; pr < J.npairs; pr++)
-                        for (int i = 0; i < w.b - w.a; i++)
-                            for (int p = 1; p <= w.r; p++) {
-                                mbar_wait(&full[stage], phase);
-                                tc_fence_after();
-                                const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
-                                const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                                const bool first = (pr == 0 && i == 0);
+                    // the producer's stage sequence: per position a block p0..p1 (plus the A_{p0-1}
+                    // lead stage when p0 > 1); an accumulator's first MMA overwrites it
+                    const int nkb = w.b - w.a, nblk = unit_nblk(w.r, P.pblk), npos = J.npairs * nblk * nkb;
+                    uint32_t acc0 = 0, acc1 = 0;
+                    int pos = rot;
+                    for (int t = 0; t < npos; t++) {
+                        const int blk = (pos / nkb) % nblk;
+                        const int p0 = unit_pfirst(w.r, nblk, blk), p1 = unit_pfirst(w.r, nblk, blk + 1) - 1;
+                        int prev = -1;
+                        if (p0 > 1) {                                   // lead stage: A_{p0-1}
+                            mbar_wait(&full[stage], phase);
+                            prev = stage;
+                            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        }
+                        for (int p = p0; p <= p1; p++) {
+                            mbar_wait(&full[stage], phase);
+                            tc_fence_after();
+                            const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+                            const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
 #pragma unroll
-                                for (int kk = 0; kk < kBK / 32; kk++)   // D_{r+1} += A_p B_{r+1-p}
-                                    mma_i8_2sm(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                               (first && p == 1 && kk == 0) ? 0u : 1u);
-                                if (p >= 2) {                           // D_r += A_{p-1} B_{r+1-p}
-                                    const uint32_t ap = smem_u32(sA + prev * Cfg::A_BYTES);
-#pragma unroll
-                                    for (int kk = 0; kk < kBK / 32; kk++)
-                                        mma_i8_2sm(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                                   (first && p == 2 && kk == 0) ? 0u : 1u);
-                                    mma_commit_2sm(&empty[prev]);
-                                }
-                                if (p == w.r) mma_commit_2sm(&empty[stage]);
-                                prev = stage;
-                                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                            for (int kk = 0; kk < kBK / 32; kk++) {     // D_{r+1} += A_p B_{r+1-p}
+                                mma_i8_2sm(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc, acc1);
+                                acc1 = 1u;
                             }
+                            if (prev >= 0) {                            // D_r += A_{p-1} B_{r+1-p}
+                                const uint32_t ap = smem_u32(sA + prev * Cfg::A_BYTES);
+#pragma unroll
+                                for (int kk = 0; kk < kBK / 32; kk++) {
+                                    mma_i8_2sm(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc, acc0);
+                                    acc0 = 1u;
+                                }
+                                mma_commit_2sm(&empty[prev]);
+                            }
+                            if (p == p1) mma_commit_2sm(&empty[stage]);
+                            prev = stage;
+                            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        }
+                        if (++pos == npos) pos = 0;
+                    }
                 } else {
                     const int nsteps = unit_G(w) == 3 ? J.npairs * (w.b - w.a) * (w.r - 1) : w.b - w.a;
                     for (int g = 0; g < nsteps; g++) {
@@ -427,7 +469,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             const WorkUnit w = P.units[u];
             mbar_wait(tfull, tphase);
             tc_fence_after();
-            const int row = w.tm * 256 + (int)rank * 128 + q * 32 + lane;
+            const int row = (P.dbg & 1) ? P.m : w.tm * 256 + (int)rank * 128 + q * 32 + lane;
             for (int acc = 0; acc < (unit_G(w) == 2 ? 2 : 1); acc++) {
                 const int64_t slot = acc ? w.slot1 : w.slot0;
 #pragma unroll 1
