@@ -346,16 +346,39 @@ def e2e_measure(P, A, B, prec, args, world=1, dev=None):
         t0 = time.perf_counter()
         run()
         ts.append(time.perf_counter() - t0)
-    t = statistics.median(ts)
+    t_block = statistics.median(ts)
+    t = t_block
+    pipelined = None
+    if world == 1:
+        # a stream of K products through the queued entry: step i+1's H2D overlaps step i's slice
+        # GEMM and step i's D2H the next step's compute; every step still copies its inputs in
+        # and its C out inside the timed region (wall clock from the first call to the wait)
+        hC2 = mpgen.CMat(pinned(mpgen.empty_rmat(m, n, prec)), pinned(mpgen.empty_rmat(m, n, prec)))
+        outs = (hC, hC2)
+        K = max(3, args.steps)
+        for i in range(2):                                       # warm-up: both staging sets
+            P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i])
+        P.mpcgemm_host_wait()
+        t0 = time.perf_counter()
+        for i in range(K):
+            P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i & 1])
+        P.mpcgemm_host_wait()
+        t = (time.perf_counter() - t0) / K
+        pipelined = K
     if world > 1:
         tt = torch.tensor([t], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
     ent = lambda R: R.sign.nbytes + R.exp.nbytes + R.limbs.nbytes
-    return {"value": world * m * n * k / t, "unit": UNIT, "h2d_bytes_per_step": ent(A.re) + ent(A.im) + ent(B.re) + ent(B.im),
-            "d2h_bytes_per_step": 2 * (m * n * (9 + 8 * ((prec + 63) // 64))), "ms_per_step": 1e3 * t,
-            "api": "mpcgemm_host (C ABI, pinned host buffers)" if world == 1 else
-                   "pinned host copies + dist protocol + mpcgemm_ex (Python public API)"}
+    out = {"value": world * m * n * k / t, "unit": UNIT, "h2d_bytes_per_step": ent(A.re) + ent(A.im) + ent(B.re) + ent(B.im),
+           "d2h_bytes_per_step": 2 * (m * n * (9 + 8 * ((prec + 63) // 64))), "ms_per_step": 1e3 * t,
+           "api": "pinned host copies + dist protocol + mpcgemm_ex (Python public API)"}
+    if pipelined:
+        out["api"] = (f"mpcgemm_host_async x {pipelined} steps + mpcgemm_host_wait (C ABI, pinned host buffers; "
+                      "step i+1's H2D overlaps step i's compute)")
+        out["blocking_ms_per_step"] = 1e3 * t_block
+        out["blocking_api"] = "mpcgemm_host (one blocking call: H2D, compute, D2H)"
+    return out
 
 
 if __name__ == "__main__":

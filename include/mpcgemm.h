@@ -129,6 +129,22 @@ int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec,
                  const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C, mpcgemm_method method,
                  const mpcgemm_opts *opts, mpcgemm_report *rep);
 
+/* Pipelined form of mpcgemm_host for a stream of independent products: same arguments and
+ * result, but returns once the call's device work is queued (it blocks only for its own
+ * slice-count pre-pass).  The H2D of the inputs runs on a library copy stream into one of two
+ * device staging sets, so call i+1's copies overlap call i's slice GEMM, and C's D2H overlaps
+ * the next call's compute.  The host buffers A, B, C must stay valid and unmodified until
+ * mpcgemm_host_wait() returns; the report is filled at return (opts->timing makes the call
+ * synchronize per stage).  Errors detected while queuing are returned by the call (after
+ * draining its queued work); asynchronous device faults by mpcgemm_host_wait(). */
+int mpcgemm_host_async(int64_t m, int64_t n, int64_t k, int32_t prec,
+                       const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C, mpcgemm_method method,
+                       const mpcgemm_opts *opts, mpcgemm_report *rep);
+
+/* Blocks until every mpcgemm_host_async call issued on this device has finished (C on the
+ * host).  0 or MPCGEMM_ERR_CUDA. */
+int mpcgemm_host_wait(void);
+
 /* The rho-hat pre-pass on this process's A rows:
  *   out[0] = minT  = min_ij T_ij, T = t u (INT8 GEMM), over nonzero rows/columns with
  *                    (|A||B|)_ij != 0  (-1: no such pair)

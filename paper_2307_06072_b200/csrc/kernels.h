@@ -37,6 +37,9 @@ cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int
 
 // a-2: stage 1 (out_min = min T over nonzero line pairs) and stage 2 (out_min, out_min1,
 // out_max2), each an array over the 256-row blocks of A (kSBlk)
+// small device -> host results (pre-pass integers, flags) written by SM stores into mapped
+// pinned host memory: no copy engine, so they never queue behind a bulk D2H on another stream
+cudaError_t readback_launch(void *dst_mapped, const void *src, size_t bytes, cudaStream_t st);
 cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t nstrips,
                                   int64_t m, int64_t n, int64_t k, int64_t kp,
                                   const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA, const int32_t *relB,

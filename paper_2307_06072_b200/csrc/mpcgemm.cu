@@ -46,7 +46,13 @@ int env_int(const char *name, int dflt);
 struct DevCache {
     void *ws = nullptr; size_t ws_bytes = 0;
     void *meta = nullptr; size_t meta_bytes = 0;
-    void *stage = nullptr; size_t stage_bytes = 0;   // mpcgemm_host device staging
+    void *stage[2] = {}; size_t stage_bytes[2] = {}; // mpcgemm_host device staging, two sets:
+                                                     // an async call fills one while the
+                                                     // previous call computes from the other
+    int stage_next = 0;
+    cudaStream_t h2d_stream = nullptr;               // mpcgemm_host: H2D of the inputs
+    cudaEvent_t stage_in[2] = {}, stage_free[2] = {};
+    void *rb = nullptr; size_t rb_bytes = 0;         // mapped pinned host memory for readback()
     void *lu = nullptr; size_t lu_bytes = 0;         // NEXT-3 LU scratch (1 / pivot, info)
     void *solve = nullptr; size_t solve_bytes = 0;   // NEXT-3 solve scratch (1 / U_cc, X)
     cudaStream_t copy_stream = nullptr;              // mpcgemm_host: D2H of finished row groups
@@ -79,6 +85,26 @@ int grow(void **p, size_t *have, size_t need) {
     cudaError_t e = cudaMalloc(p, sz);
     if (e != cudaSuccess) { *p = nullptr; cudaGetLastError(); return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc workspace", e); }
     *have = sz;
+    return 0;
+}
+
+// Stream-ordered read of a few device words to the host (caller holds g_mu): a kernel stores
+// them into mapped pinned memory, then the stream is synchronized.  Unlike a D2H memcpy it does
+// not wait for the copy engine, which may be busy with a queued call's bulk D2H of C.
+int readback(int dev, void *out, const void *src, size_t bytes, cudaStream_t st) {
+    DevCache &dc = g_cache[dev];
+    if (dc.rb_bytes < bytes) {
+        if (dc.rb) { cudaStreamSynchronize(st); cudaFreeHost(dc.rb); dc.rb = nullptr; dc.rb_bytes = 0; }
+        const size_t sz = align_up(std::max<size_t>(bytes, 4096), 4096);
+        cudaError_t e = cudaHostAlloc(&dc.rb, sz, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess) { dc.rb = nullptr; cudaGetLastError(); return fail(MPCGEMM_ERR_NOMEM, "cudaHostAlloc readback", e); }
+        dc.rb_bytes = sz;
+    }
+    void *dptr = nullptr;
+    CK(cudaHostGetDevicePointer(&dptr, dc.rb, 0));
+    CK(readback_launch(dptr, src, bytes, st));
+    CK(cudaStreamSynchronize(st));
+    memcpy(out, dc.rb, bytes);
     return 0;
 }
 
@@ -462,8 +488,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     CK(cudaMemsetAsync(mv.omin, 0xFF, 8 * 3 * nb, st));
     CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 1,
                              mv.omin, mv.omin1, mv.omax2, st));
-    CK(cudaMemcpyAsync(h.data(), mv.omin, 8 * nb, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    if (int rc = readback(dev, h.data(), mv.omin, 8 * nb, st)) return rc;
     out->minT.assign(nb, -1); out->minT1.assign(nb, -1); out->maxD2.assign(nb, -1);
     bool any0 = false;
     for (int64_t b = 0; b < nb; b++) {
@@ -475,8 +500,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
         CK(cudaMemsetAsync(mv.omin, 0xFF, 8 * 3 * nb, st));
         CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 2,
                                  mv.omin, mv.omin1, mv.omax2, st));
-        CK(cudaMemcpyAsync(h.data(), mv.omin, 8 * 3 * nb, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        if (int rc = readback(dev, h.data(), mv.omin, 8 * 3 * nb, st)) return rc;
         for (int64_t b = 0; b < nb; b++) {
             out->minT[b] = h[b] == ~0ull ? -1 : (int64_t)h[b];
             out->minT1[b] = h[nb + b] == ~0ull ? -1 : (int64_t)h[nb + b];
@@ -715,11 +739,10 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, eA, nzA, errflag, validate, st));
     CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, eB, nzB, errflag, validate, st));
     if (E) CK(cudaEventRecord(E->ev[1], st));
-    int launches = 4;                                  // linemax + finalize, A and B
+    int launches = 4 + (validate ? 1 : 0);             // linemax + finalize, A and B [, flag readback]
     if (validate) {
         uint32_t h = 0;
-        CK(cudaMemcpyAsync(&h, errflag, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        if (int rc = readback(dev, &h, errflag, 4, st)) return rc;
         if (h & 2u) return fail(MPCGEMM_ERR_EXP_RANGE, "|exp| > 2^61");
         if (h & 1u) return fail(MPCGEMM_ERR_NOT_NORMALIZED, "mantissa not normalized");
     }
@@ -732,7 +755,7 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         Bounds bd;
         if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, &bd)) return rc;
         for (int q = 0; q < 3; q++) pb[q] = bd.g[q];
-        launches += 4 + (pb[0] == 0 ? 1 : 0);         // planes x2, T GEMM, min [, max-plus]
+        launches += 5 + (pb[0] == 0 ? 2 : 0);         // planes x2, T GEMM, min, readback [, max-plus, readback]
         log2rho = rule_log2rho(k, pb[0], pb[1], pb[2]);
         s = rule_slices(prec, method, log2rho, bits);
         if (s < 0) return fail(MPCGEMM_ERR_SLICES, "slice rule needs s > 1024");
@@ -1006,8 +1029,11 @@ size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec, mpc
 // group, a multiple of 256; default 512 when m >= 1024; 0 = one group)
 std::mutex g_host_mu;                                  // one host-buffer call at a time (staging)
 
-int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
-                 mpcgemm_method method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
+// e2e entry (sync: returns with C on the host; async: returns once the call's device work is
+// queued -- H2D on the h2d stream into staging set j, compute on st, D2H of finished row groups
+// on the copy stream -- and set j is released by an event when its D2H is done)
+int host_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
+              mpcgemm_method method, const mpcgemm_opts *opts, mpcgemm_report *rep, bool async) {
     if (int rc = check_args(m, n, k, prec, A, B, C, (int)method)) return rc;
     std::lock_guard<std::mutex> hostlock(g_host_mu);
     const int L = (prec + 63) / 64;
@@ -1024,18 +1050,26 @@ int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *
     int dev = 0;
     CK(cudaGetDevice(&dev));
     uint8_t *base;
-    cudaStream_t cs;                                   // D2H copy stream
-    cudaEvent_t ev;
+    cudaStream_t cs, hs;                               // D2H copy stream, H2D stream
+    cudaEvent_t ev, ev_in, ev_free;
     {
         std::lock_guard<std::mutex> lock(g_mu);
         DevCache &dc = g_cache[dev];
-        if (int rc = grow(&dc.stage, &dc.stage_bytes, total)) return rc;
-        base = (uint8_t *)dc.stage;
         if (!dc.copy_stream) {
             CK(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&dc.h2d_stream, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&dc.group_event, cudaEventDisableTiming));
+            for (int j = 0; j < 2; j++) {
+                CK(cudaEventCreateWithFlags(&dc.stage_in[j], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&dc.stage_free[j], cudaEventDisableTiming));
+            }
         }
-        cs = dc.copy_stream; ev = dc.group_event;
+        const int j = async ? dc.stage_next : 0;       // sync calls keep to set 0 (one set of memory)
+        if (async) dc.stage_next ^= 1;
+        if (int rc = grow(&dc.stage[j], &dc.stage_bytes[j], total)) return rc;   // grow syncs before a free
+        base = (uint8_t *)dc.stage[j];
+        cs = dc.copy_stream; hs = dc.h2d_stream; ev = dc.group_event;
+        ev_in = dc.stage_in[j]; ev_free = dc.stage_free[j];
     }
     mpc_rmat dmats[6];
     for (int q = 0; q < 6; q++) {
@@ -1044,25 +1078,29 @@ int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *
         dmats[q].limbs = (uint64_t *)(base + off[q][2]);
         dmats[q].ld = cols[q];
     }
+    // the H2D waits until the set's previous call has finished with it (its D2H included)
+    CK(cudaStreamWaitEvent(hs, ev_free, 0));
     for (int q = 0; q < 4; q++) {
         const mpc_rmat &H = *in[q];
         if (rows[q] == 0 || cols[q] == 0) continue;
-        CK(cudaMemcpy2DAsync(dmats[q].sign, cols[q], H.sign, H.ld, cols[q], rows[q], cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpy2DAsync(dmats[q].exp, cols[q] * 8, H.exp, H.ld * 8, cols[q] * 8, rows[q], cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpy2DAsync(dmats[q].sign, cols[q], H.sign, H.ld, cols[q], rows[q], cudaMemcpyHostToDevice, hs));
+        CK(cudaMemcpy2DAsync(dmats[q].exp, cols[q] * 8, H.exp, H.ld * 8, cols[q] * 8, rows[q], cudaMemcpyHostToDevice, hs));
         CK(cudaMemcpy2DAsync(dmats[q].limbs, cols[q] * 8 * L, H.limbs, H.ld * 8 * L, cols[q] * 8 * L, rows[q],
-                             cudaMemcpyHostToDevice, st));
+                             cudaMemcpyHostToDevice, hs));
     }
     if (opts && opts->beta) {                          // C is an input too
         const mpc_rmat *cin[2] = {&C->re, &C->im};
         for (int q = 0; q < 2; q++) {
             if (m == 0 || n == 0) continue;
             const mpc_rmat &H = *cin[q];
-            CK(cudaMemcpy2DAsync(dmats[4 + q].sign, n, H.sign, H.ld, n, m, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpy2DAsync(dmats[4 + q].exp, n * 8, H.exp, H.ld * 8, n * 8, m, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpy2DAsync(dmats[4 + q].sign, n, H.sign, H.ld, n, m, cudaMemcpyHostToDevice, hs));
+            CK(cudaMemcpy2DAsync(dmats[4 + q].exp, n * 8, H.exp, H.ld * 8, n * 8, m, cudaMemcpyHostToDevice, hs));
             CK(cudaMemcpy2DAsync(dmats[4 + q].limbs, n * 8 * L, H.limbs, H.ld * 8 * L, n * 8 * L, m,
-                                 cudaMemcpyHostToDevice, st));
+                                 cudaMemcpyHostToDevice, hs));
         }
     }
+    CK(cudaEventRecord(ev_in, hs));
+    CK(cudaStreamWaitEvent(st, ev_in, 0));
     mpc_cmat dA{dmats[0], dmats[1]}, dB{dmats[2], dmats[3]}, dC{dmats[4], dmats[5]};
     mpc_rmat *outs[2] = {&C->re, &C->im};
     // D2H of C rows [r0, r1) on the copy stream once the compute stream has finished them
@@ -1081,18 +1119,50 @@ int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *
         }
         return 0;
     };
-    int64_t group = env_int("MPCGEMM_HOST_GROUP", m >= 1024 ? 512 : 0);
+    // row groups let a blocking call's D2H overlap its own later groups (~7 ms of extra GEMM
+    // tails and B re-reads at config 4); a queued call's D2H overlaps the next call instead
+    int64_t group = env_int("MPCGEMM_HOST_GROUP", (!async && m >= 1024) ? 512 : 0);
     if (group > 0) group = std::max<int64_t>(kSBlk, group / kSBlk * kSBlk);
     const bool grouped = group > 0 && group < m && !(opts && opts->carrier == 1);
     int rc = gemm_impl(m, n, k, prec, &dA, &dB, &dC, (int)method, opts, rep, true, grouped ? group : 0,
                        grouped ? &d2h : nullptr);
-    if (rc < 0) { cudaStreamSynchronize(cs); return rc; }
-    if (!grouped) {
-        if (int r2 = d2h(0, m)) return r2;
+    if (rc >= 0 && !grouped) {
+        if (int r2 = d2h(0, m)) rc = r2;
     }
-    CK(cudaStreamSynchronize(st));
-    CK(cudaStreamSynchronize(cs));
+    // the set is free once everything queued for this call has run (compute and D2H)
+    CK(cudaEventRecord(ev, st));
+    CK(cudaStreamWaitEvent(cs, ev, 0));
+    CK(cudaEventRecord(ev_free, cs));
+    if (rc < 0 || !async) {
+        CK(cudaStreamSynchronize(st));
+        CK(cudaStreamSynchronize(cs));
+    }
     return rc;
+}
+
+int mpcgemm_host(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B, mpc_cmat *C,
+                 mpcgemm_method method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
+    return host_impl(m, n, k, prec, A, B, C, method, opts, rep, false);
+}
+
+int mpcgemm_host_async(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
+                       mpc_cmat *C, mpcgemm_method method, const mpcgemm_opts *opts, mpcgemm_report *rep) {
+    return host_impl(m, n, k, prec, A, B, C, method, opts, rep, true);
+}
+
+int mpcgemm_host_wait(void) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaEvent_t fr[2] = {};
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        auto it = g_cache.find(dev);
+        if (it == g_cache.end() || !it->second.copy_stream) return 0;
+        fr[0] = it->second.stage_free[0]; fr[1] = it->second.stage_free[1];
+    }
+    for (int j = 0; j < 2; j++) CK(cudaEventSynchronize(fr[j]));
+    CK(cudaGetLastError());
+    return 0;
 }
 
 const char *mpcgemm_strerror(int code) {
@@ -1120,8 +1190,10 @@ void mpcgemm_release(void) {
     auto it = g_cache.find(dev);
     if (it != g_cache.end()) {
         if (it->second.done) cudaEventDestroy(it->second.done);
-        cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage); cudaFree(it->second.lu);
+        cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage[0]); cudaFree(it->second.stage[1]);
+        cudaFree(it->second.lu);
         cudaFree(it->second.solve);
+        if (it->second.rb) cudaFreeHost(it->second.rb);
         g_cache.erase(it);
     }
     for (auto p = g_plans.begin(); p != g_plans.end();) {

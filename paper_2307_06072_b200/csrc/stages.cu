@@ -550,6 +550,19 @@ prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m,
     }
 }
 
+__global__ void readback_kernel(uint32_t *dst, const uint32_t *src, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t readback_launch(void *dst_mapped, const void *src, size_t bytes, cudaStream_t st) {
+    const int64_t n = (int64_t)(bytes / 4);            // callers pass multiples of 4 bytes
+    if (n == 0) return cudaSuccess;
+    readback_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 64), 256, 0, st>>>((uint32_t *)dst_mapped,
+                                                                                      (const uint32_t *)src, n);
+    return cudaGetLastError();
+}
+
 cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t nstrips,
                                   int64_t m, int64_t n, int64_t k, int64_t kp,
                                   const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA, const int32_t *relB,

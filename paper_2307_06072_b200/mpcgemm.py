@@ -21,7 +21,7 @@ _lib = None
 METHODS = {"3M": 3, "4M": 4, 3: 3, 4: 4}
 ERRORS = {0: "OK", -1: "ERR_ARG", -2: "ERR_PREC", -3: "ERR_EXP_RANGE", -4: "ERR_NOT_NORMALIZED",
           -5: "ERR_ALIAS", -6: "ERR_NOMEM", -7: "ERR_CUDA", -8: "ERR_SLICES"}
-SYMBOLS = ["mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_rho_bounds", "mpcgemm_slices_for",
+SYMBOLS = ["mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_host_async", "mpcgemm_host_wait", "mpcgemm_rho_bounds", "mpcgemm_slices_for",
            "mpcgemm_workspace_size", "mpcgemm_strerror", "mpcgemm_last_error", "mpcgemm_release",
            "mpcgemm_version", "mpclu_factor", "mpclu_solve", "mpc_scalar"]
 
@@ -77,6 +77,8 @@ def lib():
             L.mpcgemm.argtypes = [i64, i64, i64, i32, PC, PC, PC, ctypes.c_int]
             L.mpcgemm_ex.argtypes = [i64, i64, i64, i32, PC, PC, PC, ctypes.c_int, ctypes.POINTER(OptsC), ctypes.POINTER(ReportC)]
             L.mpcgemm_host.argtypes = L.mpcgemm_ex.argtypes
+            L.mpcgemm_host_async.argtypes = L.mpcgemm_ex.argtypes
+            L.mpcgemm_host_wait.argtypes = []
             L.mpcgemm_rho_bounds.argtypes = [i64, i64, i64, i32, PC, PC, i32, ctypes.POINTER(OptsC), ctypes.POINTER(ctypes.c_int64)]
             L.mpcgemm_slices_for.argtypes = [i32, ctypes.c_int, i64, i64, i64, i64]
             L.mpcgemm_workspace_size.argtypes = [i64, i64, i64, i32, ctypes.c_int, i32]
@@ -88,7 +90,7 @@ def lib():
             L.mpclu_factor.argtypes = [i64, i32, PC, vp, i32, ctypes.c_int, ctypes.POINTER(OptsC), ctypes.POINTER(LuReportC)]
             L.mpclu_solve.argtypes = [i64, i64, i32, PC, vp, PC, ctypes.POINTER(OptsC)]
             L.mpc_scalar.argtypes = [i32, i64, i32, PC, PC, PC, PC, vp, vp]
-            for name in ("mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_rho_bounds", "mpcgemm_slices_for", "mpcgemm_version",
+            for name in ("mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_host_async", "mpcgemm_host_wait", "mpcgemm_rho_bounds", "mpcgemm_slices_for", "mpcgemm_version",
                          "mpclu_factor", "mpclu_solve", "mpc_scalar"):
                 getattr(L, name).restype = ctypes.c_int
             _lib = L
@@ -248,6 +250,37 @@ def mpcgemm_host(A, B, prec: int, method="3M", slices: int = 0, C=None, timing: 
                             ctypes.byref(opts), ctypes.byref(rep))
     _check(rc)
     return C, {f: getattr(rep, f) for f, _ in ReportC._fields_} | {"status": rc}
+
+
+_pending = []     # host matrices of queued mpcgemm_host_async calls (kept alive until the wait)
+
+
+def mpcgemm_host_async(A, B, prec: int, method="3M", C=None, slices: int = 0, beta: int = 0, alpha_neg: int = 0,
+                       adaptive: int = 0):
+    """Queued end-to-end call (C ABI mpcgemm_host_async): returns (C, report) once the device work
+    is queued; C is valid on the host after mpcgemm_host_wait().  A, B, C must not be modified before."""
+    from mpgen import empty_cmat
+    m, k = A.shape
+    n = B.shape[1]
+    C = empty_cmat(m, n, prec) if C is None else C
+    a = CMatC(_host_rmat(A.re), _host_rmat(A.im))
+    b = CMatC(_host_rmat(B.re), _host_rmat(B.im))
+    c = CMatC(_host_rmat(C.re), _host_rmat(C.im))
+    opts = OptsC(None, slices, 0, None, 0, 0, beta, alpha_neg, 0, adaptive, None)
+    rep = ReportC()
+    _pending.append((A, B, C))
+    rc = lib().mpcgemm_host_async(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), METHODS[method],
+                                  ctypes.byref(opts), ctypes.byref(rep))
+    _check(rc)
+    return C, {f: getattr(rep, f) for f, _ in ReportC._fields_} | {"status": rc}
+
+
+def mpcgemm_host_wait():
+    """Blocks until every queued mpcgemm_host_async call has its C on the host."""
+    try:
+        _check(lib().mpcgemm_host_wait())
+    finally:
+        _pending.clear()
 
 
 def mpcgemm_rho_bounds(A: DevCMat, B: DevCMat, prec: int, full: int = 0, stream=None):

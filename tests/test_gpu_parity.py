@@ -128,6 +128,31 @@ def test_small_chunks_equal_default(monkeypatch):
     assert same_bits(C1, C2) and same_bits(C1, C3) and same_bits(C1, C4) and same_bits(C1, C5)
 
 
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_schedule_variants_bitexact(method, monkeypatch):
+    """The CTA-pair kernel's walk order is free (exact integer sums): p-blocks of 1..7 planes (lead
+    stages for D_r), k-phase hints on/off (units starting mid-walk, also from a previous call's
+    stale hints), serpentine off, many exactness chunks -- all bitwise equal, and equal to the oracle."""
+    m, n, k, prec = 300, 260, 900, 256
+    A = mpgen.random_cmat(21, 1, m, k, prec, 3)
+    B = mpgen.random_cmat(21, 2, k, n, prec, 3)
+    C0, rep = run_gpu(A, B, prec, method)
+    variants = [{"MPCGEMM_PBLK": "1"}, {"MPCGEMM_PBLK": "3"}, {"MPCGEMM_PBLK": "7", "MPCGEMM_MAXKB": "2"},
+                {"MPCGEMM_PBLK": "0", "MPCGEMM_KPHASE": "0"}, {"MPCGEMM_KPHASE": "0", "MPCGEMM_SERPENTINE": "0"},
+                {"MPCGEMM_PBLK": "5", "MPCGEMM_SERPENTINE": "0", "MPCGEMM_MAXKB": "3"}]
+    for v in variants:
+        for key in ("MPCGEMM_PBLK", "MPCGEMM_KPHASE", "MPCGEMM_SERPENTINE", "MPCGEMM_MAXKB"):
+            monkeypatch.delenv(key, raising=False)
+        for key, val in v.items():
+            monkeypatch.setenv(key, val)
+        for _ in range(2):
+            C1, _ = run_gpu(A, B, prec, method)
+            assert same_bits(C0, C1), (v, first_mismatch(C0, C1))
+    si, sj = sample_idx(m, n, 60, seed=5)
+    Rs = oracle.ozaki(A, B, prec, method, rep["slices"], samples=(si, sj))
+    assert sampled_equal(C0, Rs, si, sj) is None
+
+
 @pytest.mark.parametrize("spread,k", [(16, 12), (16, 3), (0, 64), (4, 40)])
 def test_prepass_matches_oracle(spread, k):
     """rho-hat pre-pass integers and the resulting s equal the oracle's (incl. the minT == 0
@@ -211,6 +236,36 @@ def test_host_entry_matches_device():
         C1, r1 = run_gpu(A, B, prec, method)
         C2, r2 = P.mpcgemm_host(A, B, prec, method)
         assert r1["slices"] == r2["slices"] and same_bits(C1, C2)
+
+
+@pytest.mark.parametrize("group", [0, 256])
+def test_host_async_pipeline(monkeypatch, group):
+    """mpcgemm_host_async: five products queued back to back (two staging sets in turn, row
+    groups or not, different shapes / precisions / methods, one with beta = 1) -- after
+    mpcgemm_host_wait every C equals the blocking mpcgemm_host result bitwise; an argument error
+    while calls are queued is reported and leaves the pipeline usable."""
+    monkeypatch.setenv("MPCGEMM_HOST_GROUP", str(group))
+    cases = [(300, 90, 200, 192, "3M", 0), (530, 70, 260, 256, "4M", 0), (257, 40, 300, 128, "3M", 1),
+             (600, 64, 129, 320, "4M", 0), (100, 33, 80, 64, "3M", 0)]
+    probs = []
+    for i, (m, k, n, prec, method, beta) in enumerate(cases):
+        A = mpgen.random_cmat(50 + i, 1, m, k, prec, 4)
+        B = mpgen.random_cmat(50 + i, 2, k, n, prec, 4)
+        C0 = mpgen.random_cmat(50 + i, 3, m, n, prec, 2)
+        ref, _ = P.mpcgemm_host(A, B, prec, method, C=C0.copy() if beta else None, beta=beta)
+        probs.append((A, B, C0, prec, method, beta, ref))
+    outs = []
+    for A, B, C0, prec, method, beta, _ in probs:
+        C, rep = P.mpcgemm_host_async(A, B, prec, method, C=C0.copy() if beta else None, beta=beta)
+        outs.append(C)
+    with pytest.raises(P.MpcgemmError):
+        P.mpcgemm_host_async(probs[0][0], probs[0][1], 5000, "3M")
+    P.mpcgemm_host_wait()
+    for (A, B, C0, prec, method, beta, ref), C in zip(probs, outs):
+        assert same_bits(ref, C), (prec, method, beta, first_mismatch(ref, C))
+    C, _ = P.mpcgemm_host_async(probs[1][0], probs[1][1], probs[1][3], probs[1][4])
+    P.mpcgemm_host_wait()
+    assert same_bits(probs[1][6], C)
 
 
 @pytest.mark.parametrize("group", [256, 512])
