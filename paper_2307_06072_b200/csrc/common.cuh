@@ -94,6 +94,8 @@ struct GemmParams {
                                // (pair, p-block, k-block) a running unit of the group last started;
                                // a new unit of the group begins there (CTA-pair kernel, G >= 2)
     int32_t pblk;              // p-block length of the CTA-pair kernel's G >= 2 units (0: one block)
+    int32_t kk_last;           // K = 32 MMA steps of the last k-block (1..3; 0: all 4): the zero
+                               // padding of k up to a multiple of 128 is not multiplied
     JobDesc jobs[kMaxJobs];
 };
 

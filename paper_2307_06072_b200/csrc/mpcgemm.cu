@@ -233,6 +233,9 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
         return key.sblk.empty() || r <= key.sblk[(size_t)((tm * key.BM) >> kSBlkShift)] + 1;
     };
     const bool serp = env_int("MPCGEMM_SERPENTINE", 1) != 0;
+    // K = 32 MMAs per k-block step: 4, except kk_last for the last (zero-padded) k-block
+    const int64_t kkl = ((key.k - 1) % kBK) / 32 + 1;
+    auto kk_sum = [&](int64_t a, int64_t b) { return (b - a) * (kBK / 32) - ((a <= KB - 1 && KB - 1 < b) ? kBK / 32 - kkl : 0); };
     for (const Segment &sg : segs) {
         const int q = sg.q, r = sg.r;
         const int64_t np = P.jobs[q].npairs;
@@ -245,12 +248,12 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
                         const int32_t rev = serp && ((r >> 1) & 1) ? (1 << 16) : 0;
                         if (!in_tri(tm, r + 1)) {              // block's last diagonal is r: D_r alone
                             units.push_back({q | (3 << 8) | rev, (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
-                            P.mma += np * (b - a) * (r - 1) * (kBK / 32);
+                            P.mma += np * kk_sum(a, b) * (r - 1);
                             continue;
                         }
                         units.push_back({q | (2 << 8) | rev, (int32_t)tm, (int32_t)tn, r, a, b,
                                          base(q, r) + (int32_t)c, base(q, r + 1) + (int32_t)c});
-                        P.mma += np * (b - a) * (2 * r - 1) * (kBK / 32);
+                        P.mma += np * kk_sum(a, b) * (2 * r - 1);
                     }
             }
         } else {
@@ -261,7 +264,7 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
                         if (!in_tri(tm, r)) continue;
                         units.push_back({q | (1 << 8), (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
-                        P.mma += (int64_t)(b - a) * (kBK / 32);
+                        P.mma += (int64_t)(b - a) * (kBK / 32) - (b / KB - a / KB) * (kBK / 32 - kkl);
                     }
             }
         }
@@ -478,6 +481,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
     SL.P.partials = T; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
     SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = 1; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
+    SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
     SL.P.partsA = SL.P.partsB = 1;
     for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
     SL.digA = tA; SL.digB = tB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
@@ -659,6 +663,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
         SL.P.partials = partials; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
         SL.P.m = (int32_t)mr; SL.P.n = (int32_t)n; SL.P.s = s; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
+        SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
         SL.P.partsA = SL.P.partsB = parts;
         SL.P.dbg = env_int("MPCGEMM_DBG", 0);
         SL.P.hot = env_int("MPCGEMM_KPHASE", 1) ? plan->d_counter + 1 : nullptr;

@@ -57,6 +57,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     uint64_t *qempty = qfull + Cfg::QN;
     int32_t *uq = reinterpret_cast<int32_t *>(qempty + Cfg::QN);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(uq + Cfg::QN);
+    uint8_t *skk = reinterpret_cast<uint8_t *>(tmem_slot + 1);   // per stage: MMA K-steps to issue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
@@ -85,6 +86,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             int qs = 0; uint32_t qph = 0;
             auto load = [&](int planeA, int planeB, int kb, int tm, int tn) {
                 mbar_wait(&empty[stage], phase ^ 1);
+                skk[stage] = (uint8_t)(kb == KB - 1 && P.kk_last ? P.kk_last : kBK / 32);   // before the arrive (release)
                 mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
                 tma_load_3d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, tm * kBM, planeA);
                 tma_load_3d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, tn * BN, planeB);
@@ -151,16 +153,19 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                                 const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                                 const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
                                 const bool first = (pr == 0 && i == 0);
+                                const int nkk = skk[stage];
 #pragma unroll
                                 for (int kk = 0; kk < kBK / 32; kk++)   // D_{r+1} += A_p B_{r+1-p}
-                                    mma_i8(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                           (first && p == 1 && kk == 0) ? 0u : 1u);
+                                    if (kk < nkk)
+                                        mma_i8(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                               (first && p == 1 && kk == 0) ? 0u : 1u);
                                 if (p >= 2) {                           // D_r += A_{p-1} B_{r+1-p}
                                     const uint32_t ap = smem_u32(sA + prev * Cfg::A_BYTES);
 #pragma unroll
                                     for (int kk = 0; kk < kBK / 32; kk++)
-                                        mma_i8(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                               (first && p == 2 && kk == 0) ? 0u : 1u);
+                                        if (kk < nkk)
+                                            mma_i8(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                                   (first && p == 2 && kk == 0) ? 0u : 1u);
                                     mma_commit(&empty[prev]);           // A_{p-1} no longer needed
                                 }
                                 if (p == w.r) mma_commit(&empty[stage]);   // A_r pairs only with B_1
@@ -174,10 +179,12 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+                        const int nkk = skk[stage];
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; kk++)
-                            mma_i8(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                   (g > 0 || kk > 0) ? 1u : 0u);
+                            if (kk < nkk)
+                                mma_i8(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                       (g > 0 || kk > 0) ? 1u : 0u);
                         mma_commit(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -268,6 +275,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     int32_t *uq = reinterpret_cast<int32_t *>(qempty + Cfg::QN);
     int32_t *uqr = uq + Cfg::QN;                      // each unit's k-phase rotation (both producers)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(uqr + Cfg::QN);
+    uint8_t *skk = reinterpret_cast<uint8_t *>(tmem_slot + 1);   // per stage: MMA K-steps to issue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -299,6 +307,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             int qs = 0; uint32_t qph = 0;
             auto load = [&](int planeA, int planeB, int kb, int tm, int tn) {
                 mbar_wait(&empty[stage], phase ^ 1);
+                skk[stage] = (uint8_t)(kb == KB - 1 && P.kk_last ? P.kk_last : kBK / 32);   // before the arrive (release)
                 if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
                 if (P.dbg & 2) { planeA = planeB = 0; kb = 0; tm = tn = 0; }
                 if (P.dbg & 4) { planeA &= 7; planeB &= 7; kb &= 1; tm &= 1; tn &= 1; }   // ~1 MB of varying operands
@@ -410,17 +419,22 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                             tc_fence_after();
                             const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                             const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+                            const int nkk = skk[stage];
 #pragma unroll
                             for (int kk = 0; kk < kBK / 32; kk++) {     // D_{r+1} += A_p B_{r+1-p}
-                                mma_i8_2sm(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc, acc1);
-                                acc1 = 1u;
+                                if (kk < nkk) {
+                                    mma_i8_2sm(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc, acc1);
+                                    acc1 = 1u;
+                                }
                             }
                             if (prev >= 0) {                            // D_r += A_{p-1} B_{r+1-p}
                                 const uint32_t ap = smem_u32(sA + prev * Cfg::A_BYTES);
 #pragma unroll
                                 for (int kk = 0; kk < kBK / 32; kk++) {
-                                    mma_i8_2sm(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc, acc0);
-                                    acc0 = 1u;
+                                    if (kk < nkk) {
+                                        mma_i8_2sm(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc, acc0);
+                                        acc0 = 1u;
+                                    }
                                 }
                                 mma_commit_2sm(&empty[prev]);
                             }
@@ -437,10 +451,12 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+                        const int nkk = skk[stage];
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; kk++)
-                            mma_i8_2sm(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                       (g > 0 || kk > 0) ? 1u : 0u);
+                            if (kk < nkk)
+                                mma_i8_2sm(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
+                                           (g > 0 || kk > 0) ? 1u : 0u);
                         mma_commit_2sm(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
