@@ -297,6 +297,7 @@ __global__ void mp_scalar_kernel(int L, int op, int64_t cnt, int prec, DMatOut A
     do {                                                      \
         if ((L) <= 4) { constexpr int C = 4; KERNEL_CALL; }   \
         else if ((L) <= 8) { constexpr int C = 8; KERNEL_CALL; } \
+        else if ((L) <= 12) { constexpr int C = 12; KERNEL_CALL; } \
         else { constexpr int C = 16; KERNEL_CALL; }           \
     } while (0)
 

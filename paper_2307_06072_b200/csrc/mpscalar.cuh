@@ -189,8 +189,8 @@ MPC_DEV void sum_round(Term *t, int cnt, int prec, int L, uint64_t *buf, int nw_
 
 constexpr int kLMax = 16;                        // prec <= 1024 for the LU path
 
-// Capacity-templated element: L <= C limbs used.  The kernels are instantiated for C = 4, 8
-// and 16 (lu.cu) so that operands and product accumulators stay in registers (static indices
+// Capacity-templated element: L <= C limbs used.  The kernels are instantiated for C = 4, 8,
+// 12 and 16 (lu.cu) so that operands and product accumulators stay in registers (static indices
 // under unrolled loops guarded by q < L) and the per-thread stack stays small.
 template <int C>
 struct Num {
@@ -249,20 +249,205 @@ MPC_DEV Term term_of(int L, const Num<C> &x, uint64_t *pa) {
 
 template <int C> struct NW { static constexpr int v = 9 * C + 6; };   // sum_round scratch limbs
 
+// ---------------------------------------------------------------- register fast path
+// For C <= 12 the (at most three) terms of cfms_part are summed exactly in a fixed window of
+// W = 2C + 3 limbs (top limb: headroom for the sign) whenever every nonzero term's lowest bit
+// lies inside it -- exponent gaps up to ~128 bits, the LU's usual case -- and the sum is
+// rounded there.  Every array index is static (runtime shifts go through a barrel shifter), so
+// the whole operation stays in registers; otherwise the general sum_round above decides.  Both
+// give the same bits: the window holds the exact sum, rounded like round_store.
+template <int N>
+MPC_DEV void shl_bits(uint64_t (&x)[N], int b) {            // x <<= b, 0 <= b < 64
+    if (!b) return;
+#pragma unroll
+    for (int i = N - 1; i > 0; i--) x[i] = (x[i] << b) | (x[i - 1] >> (64 - b));
+    x[0] <<= b;
+}
+template <int N>
+MPC_DEV void shl_limbs(uint64_t (&x)[N], int o) {           // x <<= 64 o, 0 <= o < 64
+#pragma unroll
+    for (int k = 1; k < N; k <<= 1)
+        if (o & k) {
+#pragma unroll
+            for (int i = N - 1; i >= 0; i--) x[i] = i >= k ? x[i - k] : 0ull;
+        }
+}
+template <int N>
+MPC_DEV void shr_bits(uint64_t (&x)[N], int b) {            // x >>= b, 0 <= b < 64
+    if (!b) return;
+#pragma unroll
+    for (int i = 0; i < N - 1; i++) x[i] = (x[i] >> b) | (x[i + 1] << (64 - b));
+    x[N - 1] >>= b;
+}
+template <int N>
+MPC_DEV void shr_limbs(uint64_t (&x)[N], int o) {           // x >>= 64 o, 0 <= o < 64
+#pragma unroll
+    for (int k = 1; k < N; k <<= 1)
+        if (o & k) {
+#pragma unroll
+            for (int i = 0; i < N; i++) x[i] = i + k < N ? x[i + k] : 0ull;
+        }
+}
+
+// p[0..2C) = a b (limbs beyond L are zero in a Num, so the C x C product is the L x L one)
+template <int C>
+MPC_DEV void mul_reg(uint64_t (&p)[2 * C], const uint64_t (&a)[C], const uint64_t (&b)[C]) {
+    uint64_t acc0 = 0, acc1 = 0, acc2 = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * C - 1; k++) {
+#pragma unroll
+        for (int i = 0; i < C; i++) {
+            const int j = k - i;
+            if (j >= 0 && j < C) {
+                const uint64_t x = a[i], y = b[j];
+                const uint64_t lo = x * y, hi = __umul64hi(x, y);
+                acc0 += lo;
+                const uint64_t h = hi + (acc0 < lo);
+                acc1 += h;
+                acc2 += acc1 < h;
+            }
+        }
+        p[k] = acc0;
+        acc0 = acc1; acc1 = acc2; acc2 = 0;
+    }
+    p[2 * C - 1] = acc0;
+}
+
+// acc (two's complement, W limbs) += (neg ? -1 : 1) * m[0..N) * 2^sh, 0 <= sh, no bit beyond W
+template <int W, int N>
+MPC_DEV void win_add(uint64_t (&acc)[W], const uint64_t (&m)[N], int64_t sh, bool neg) {
+    uint64_t t[W];
+#pragma unroll
+    for (int i = 0; i < W; i++) t[i] = i < N ? m[i] : 0ull;
+    shl_bits(t, (int)(sh & 63));
+    shl_limbs(t, (int)(sh >> 6));
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < W; i++) {
+        const uint64_t x = acc[i], v = t[i];
+        if (!neg) { const uint64_t u = x + v, u2 = u + c; c = (u < x) + (u2 < u); acc[i] = u2; }
+        else      { const uint64_t u = x - v, u2 = u - c; c = (x < v) + (u < c); acc[i] = u2; }
+    }
+}
+
+// RNE of the magnitude acc * 2^base to prec bits, sign neg (round_store's rule)
+template <int C, int W>
+MPC_DEV void mag_round(uint64_t (&acc)[W], int64_t base, bool neg, int prec, int L, uint8_t *so, int64_t *eo,
+                       uint64_t *lo) {
+    int B = 0;
+#pragma unroll
+    for (int i = 0; i < W; i++) if (acc[i]) B = 64 * i + 64 - __clzll((long long)acc[i]);
+    if (!B) {
+        *so = 0; *eo = 0;
+#pragma unroll
+        for (int l = 0; l < C; l++) if (l < L) lo[l] = 0;
+        return;
+    }
+    int64_t E = base + B;
+    const int rpos = B - prec - 1;
+    int rbit = 0;
+    bool sticky = false;
+    if (rpos >= 0) {
+        const int ri = rpos >> 6, rb = rpos & 63;
+#pragma unroll
+        for (int i = 0; i < W; i++) {
+            if (i == ri) { rbit = (int)((acc[i] >> rb) & 1); sticky = sticky || (acc[i] & ((1ull << rb) - 1)) != 0; }
+            if (i < ri) sticky = sticky || acc[i] != 0;
+        }
+    }
+    const int wb = B - 64 * L;                                // acc bits [wb, B) -> the L limbs
+    if (wb >= 0) { shr_bits(acc, wb & 63); shr_limbs(acc, wb >> 6); }
+    else         { shl_bits(acc, (-wb) & 63); shl_limbs(acc, (-wb) >> 6); }
+    const int drop = 64 * L - prec;
+    if (drop) acc[0] &= ~((1ull << drop) - 1);
+    const bool up = rpos >= 0 && rbit && (sticky || ((acc[0] >> drop) & 1));
+    uint64_t c = up ? (1ull << drop) : 0ull;
+#pragma unroll
+    for (int l = 0; l < C; l++)
+        if (l < L) { const uint64_t x = acc[l] + c; c = x < acc[l]; acc[l] = x; }
+    if (c) {                                                  // all kept bits were ones: 2^E
+#pragma unroll
+        for (int l = 0; l < C; l++) if (l < L) acc[l] = l == L - 1 ? 1ull << 63 : 0ull;
+        E += 1;
+    }
+    *so = neg ? 1 : 0;
+    *eo = E;
+#pragma unroll
+    for (int l = 0; l < C; l++) if (l < L) lo[l] = acc[l];
+}
+
+// RNE of the window's two's-complement value acc * 2^base to prec bits
+template <int C, int W>
+MPC_DEV void win_round(uint64_t (&acc)[W], int64_t base, int prec, int L, uint8_t *so, int64_t *eo, uint64_t *lo) {
+    const bool neg = (int64_t)acc[W - 1] < 0;
+    if (neg) {
+        uint64_t c = 1;
+#pragma unroll
+        for (int i = 0; i < W; i++) { const uint64_t x = ~acc[i] + c; c = c && x == 0; acc[i] = x; }
+    }
+    mag_round<C>(acc, base, neg, prec, L, so, eo, lo);
+}
+
+// the fast path of cfms_part; false: a term lies outside the window (the caller falls back)
+template <int C>
+MPC_DEV bool cfms_fast(int L, int part, const Num<C> *a, const Num<C> &xr, const Num<C> &xi,
+                       const Num<C> &yr, const Num<C> &yi, int prec, uint8_t *so, int64_t *eo, uint64_t *lo)
+{
+    constexpr int W = 2 * C + 3;
+    const bool sub = a != nullptr;
+    const Num<C> &v0 = part ? yi : yr, &v1 = part ? yr : yi;
+    const bool z0 = xr.zero || v0.zero, z1 = xi.zero || v1.zero, za = !sub || a->zero;
+    const int64_t e0 = xr.e + v0.e, e1 = xi.e + v1.e;
+    int64_t H = INT64_MIN;
+    if (!z0) H = e0 + 128 * L;
+    if (!z1 && e1 + 128 * L > H) H = e1 + 128 * L;
+    if (!za && a->e + 64 * L > H) H = a->e + 64 * L;
+    if (H == INT64_MIN) {                                     // every term is zero
+        *so = 0; *eo = 0;
+#pragma unroll
+        for (int l = 0; l < C; l++) if (l < L) lo[l] = 0;
+        return true;
+    }
+    const int64_t base = H - 64 * (W - 1);
+    if ((!z0 && e0 < base) || (!z1 && e1 < base) || (!za && a->e < base)) return false;
+    uint64_t acc[W];
+#pragma unroll
+    for (int i = 0; i < W; i++) acc[i] = 0;
+    uint64_t p[2 * C];
+    // part 0: a - xr yr + xi yi (cmul: xr yr - xi yi); part 1: a - xr yi - xi yr (cmul: +, +)
+    if (!z0) { mul_reg<C>(p, xr.m, v0.m); win_add(acc, p, e0 - base, (xr.neg != v0.neg) != sub); }
+    if (!z1) { mul_reg<C>(p, xi.m, v1.m); win_add(acc, p, e1 - base, (xi.neg != v1.neg) != (part == 0 ? !sub : sub)); }
+    if (!za) win_add(acc, a->m, a->e - base, a->neg);
+    win_round<C>(acc, base, prec, L, so, eo, lo);
+    return true;
+}
+
+// (operands by value: the fast path's caller keeps its copies in registers)
+template <int C>
+__device__ __noinline__ void cfms_general(int L, int part, bool sub, const Num<C> av, const Num<C> xr, const Num<C> xi,
+                                          const Num<C> yr, const Num<C> yi, int prec, uint8_t *so, int64_t *eo,
+                                          uint64_t *lo)
+{
+    uint64_t p1[2 * C], p2[2 * C], pa[C], buf[NW<C>::v];
+    Term t[3];
+    const Num<C> *a = &av;
+    if (part == 0) { t[0] = prod_term<C>(L, xr, yr, sub, p1); t[1] = prod_term<C>(L, xi, yi, !sub, p2); }
+    else           { t[0] = prod_term<C>(L, xr, yi, sub, p1); t[1] = prod_term<C>(L, xi, yr, sub, p2); }
+    int cnt = 2;
+    if (sub) t[cnt++] = term_of<C>(L, *a, pa);
+    sum_round(t, cnt, prec, L, buf, NW<C>::v, so, eo, lo);
+}
+
 // one part of a - x y (a == nullptr: x y):  part 0 = re: ar - xr yr + xi yi ;
 // part 1 = im: ai - xr yi - xi yr.  The kernels give each part its own thread.
 template <int C>
 MPC_DEV void cfms_part(int L, int part, const Num<C> *a, const Num<C> &xr, const Num<C> &xi,
                        const Num<C> &yr, const Num<C> &yi, int prec, uint8_t *so, int64_t *eo, uint64_t *lo)
 {
-    uint64_t p1[2 * C], p2[2 * C], pa[C], buf[NW<C>::v];
-    Term t[3];
-    const bool sub = a != nullptr;
-    if (part == 0) { t[0] = prod_term<C>(L, xr, yr, sub, p1); t[1] = prod_term<C>(L, xi, yi, !sub, p2); }
-    else           { t[0] = prod_term<C>(L, xr, yi, sub, p1); t[1] = prod_term<C>(L, xi, yr, sub, p2); }
-    int cnt = 2;
-    if (sub) t[cnt++] = term_of<C>(L, *a, pa);
-    sum_round(t, cnt, prec, L, buf, NW<C>::v, so, eo, lo);
+    if constexpr (C <= 12) {
+        if (cfms_fast<C>(L, part, a, xr, xi, yr, yi, prec, so, eo, lo)) return;
+    }
+    cfms_general<C>(L, part, a != nullptr, a ? *a : xr, xr, xi, yr, yi, prec, so, eo, lo);
 }
 
 // ---------------------------------------------------------------- division (reciprocal)
@@ -362,10 +547,110 @@ MPC_DEV void div_round(int L, const uint64_t *nm, int nn, int64_t ne, bool nneg,
     round_store(r, rn, ne - de - sh - 1, nneg, prec, L, so, eo, lo);
 }
 
+// Register fast path of crecip_part (C <= 8): D = zr^2 + zi^2 exactly in 2C + 2 limbs (square
+// exponents at most 120 bits apart, else false), normalised to its top bit; the numerator's
+// mantissa N placed so that U = N 2^(32 + 64 (2C + 2)); q = floor(U / D) by Knuth's algorithm
+// D on 32-bit digits with every index static (6C + 5 dividend digits, 4C + 4 divisor digits,
+// 2C + 2 quotient digits: q >= 2^(64C + 31) > 2^(prec + 1)); then RNE of 2q + (remainder != 0),
+// the same rounding input div_round builds.
+template <int C>
+MPC_DEV bool crecip_fast(int L, int part, const Num<C> &zr, const Num<C> &zi, int prec, uint8_t *so, int64_t *eo,
+                         uint64_t *lo)
+{
+    constexpr int ND = 2 * C + 2;                             // divisor limbs
+    constexpr int N = 2 * ND;                                 // divisor digits
+    constexpr int MU = 6 * C + 5;                             // dividend digits
+    constexpr int NQ = MU - N + 1;                            // quotient digits
+    const Num<C> &num = part ? zi : zr;
+    if (num.zero) { *so = 0; *eo = 0; for (int q = 0; q < L; q++) lo[q] = 0; return true; }
+    const bool hr = !zr.zero, hi = !zi.zero;
+    int64_t de;
+    uint64_t D[ND];
+#pragma unroll
+    for (int i = 0; i < ND; i++) D[i] = 0;
+    uint64_t sq[2 * C];
+    if (hr && hi) {
+        const int64_t gr = 2 * zr.e, gi = 2 * zi.e;
+        de = gr < gi ? gr : gi;
+        if ((gr > gi ? gr - gi : gi - gr) > 120) return false;
+        mul_reg<C>(sq, zr.m, zr.m); win_add(D, sq, gr - de, false);
+        mul_reg<C>(sq, zi.m, zi.m); win_add(D, sq, gi - de, false);
+    } else {
+        const Num<C> &z = hr ? zr : zi;
+        de = 2 * z.e;
+        mul_reg<C>(sq, z.m, z.m); win_add(D, sq, 0, false);
+    }
+    int bd = 0;
+#pragma unroll
+    for (int i = 0; i < ND; i++) if (D[i]) bd = 64 * i + 64 - __clzll((long long)D[i]);
+    const int sd = 64 * ND - bd;                              // normalise: top bit at 64 ND - 1
+    shl_bits(D, sd & 63);
+    shl_limbs(D, sd >> 6);
+    uint32_t v[N], u[MU + 1];
+#pragma unroll
+    for (int i = 0; i < N; i++) v[i] = (uint32_t)(D[i >> 1] >> (32 * (i & 1)));
+    // N's mantissa (top bit at bit 64 L - 1) moved to the top of C limbs, placed at digit 4C + 5
+    uint64_t nm[C];
+#pragma unroll
+    for (int i = 0; i < C; i++) nm[i] = num.m[i];
+    shl_limbs(nm, C - L);
+#pragma unroll
+    for (int i = 0; i <= MU; i++) {
+        const int k = i - (4 * C + 5);
+        u[i] = (k >= 0 && k < 2 * C) ? (uint32_t)(nm[k >> 1] >> (32 * (k & 1))) : 0u;
+    }
+    uint32_t q[NQ];
+#pragma unroll
+    for (int j = NQ - 1; j >= 0; j--) {
+        const uint64_t numr = ((uint64_t)u[j + N] << 32) | u[j + N - 1];
+        uint64_t qhat = numr / v[N - 1], rhat = numr % v[N - 1];
+        while (qhat >= (1ull << 32) || qhat * v[N - 2] > ((rhat << 32) | u[j + N - 2])) {
+            qhat--; rhat += v[N - 1];
+            if (rhat >= (1ull << 32)) break;
+        }
+        int64_t borrow = 0;
+        uint64_t carry = 0;
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            const uint64_t p = qhat * v[i] + carry;
+            carry = p >> 32;
+            const int64_t t = (int64_t)u[i + j] - (int64_t)(p & 0xFFFFFFFFull) - borrow;
+            u[i + j] = (uint32_t)t;
+            borrow = t < 0;
+        }
+        const int64_t t = (int64_t)u[j + N] - (int64_t)carry - borrow;
+        u[j + N] = (uint32_t)t;
+        if (t < 0) {                                          // qhat one too large: add back
+            qhat--;
+            uint64_t c = 0;
+#pragma unroll
+            for (int i = 0; i < N; i++) { const uint64_t s2 = (uint64_t)u[i + j] + v[i] + c; u[i + j] = (uint32_t)s2; c = s2 >> 32; }
+            u[j + N] += (uint32_t)c;
+        }
+        q[j] = (uint32_t)qhat;
+    }
+    bool rem = false;
+#pragma unroll
+    for (int i = 0; i < N; i++) rem = rem || u[i] != 0;
+    constexpr int RW = (NQ + 1) / 2 + 1;                      // 2 q + sticky
+    uint64_t r[RW];
+#pragma unroll
+    for (int i = 0; i < RW; i++) {
+        const uint64_t lo32 = 2 * i < NQ ? q[2 * i] : 0u, hi32 = 2 * i + 1 < NQ ? q[2 * i + 1] : 0u;
+        r[i] = lo32 | (hi32 << 32);
+    }
+    shl_bits(r, 1);
+    r[0] |= rem ? 1ull : 0ull;
+    // value = (U / D_norm) 2^(num.e - de - X), X = 64 (C - L) + 32 + 64 ND - sd
+    const int64_t X = 64 * (int64_t)(C - L) + 32 + 64 * (int64_t)ND - sd;
+    mag_round<C>(r, num.e - de - X - 1, part ? !num.neg : num.neg, prec, L, so, eo, lo);
+    return true;
+}
+
 // one part of 1 / (zr + i zi) (part 0: zr / D, part 1: -zi / D), z != 0
 template <int C>
-MPC_DEV void crecip_part(int L, int part, const Num<C> &zr, const Num<C> &zi, int prec,
-                         uint8_t *so, int64_t *eo, uint64_t *lo)
+__device__ __noinline__ void crecip_general(int L, int part, const Num<C> zr, const Num<C> zi, int prec,
+                                            uint8_t *so, int64_t *eo, uint64_t *lo)
 {
     const Num<C> &num = part ? zi : zr;
     if (num.zero) { *so = 0; *eo = 0; for (int q = 0; q < L; q++) lo[q] = 0; return; }
@@ -399,6 +684,16 @@ MPC_DEV void crecip_part(int L, int part, const Num<C> &zr, const Num<C> &zi, in
     }
     for (int q = 0; q < L; q++) na[q] = num.m[q];
     div_round<C>(L, na, L, num.e, part ? !num.neg : num.neg, D, dn, de, drop, prec, so, eo, lo);
+}
+
+template <int C>
+MPC_DEV void crecip_part(int L, int part, const Num<C> &zr, const Num<C> &zi, int prec,
+                         uint8_t *so, int64_t *eo, uint64_t *lo)
+{
+    if constexpr (C <= 8) {
+        if (crecip_fast<C>(L, part, zr, zi, prec, so, eo, lo)) return;
+    }
+    crecip_general<C>(L, part, zr, zi, prec, so, eo, lo);
 }
 
 // ---------------------------------------------------------------- pivot key
