@@ -77,6 +77,44 @@ def test_recip_gaps_bitexact():
         assert same_bits(G, R), (prec, first_mismatch(G, R))
 
 
+@pytest.mark.parametrize("prec", [256, 320, 512, 700])
+def test_fast_path_window_edges_bitexact(prec):
+    """The register fast paths' switches (DESIGN.md NEXT-3): fms/mul with term exponent gaps
+    around the 2C + 3-limb window edge (~128 bits), random full mantissas, deep cancellation
+    between the products; reciprocals with square-exponent gaps around 120 bits.  Bit-exact
+    against the oracle on both sides of every switch."""
+    import random
+    rng = random.Random(prec)
+    m = lambda: rng.getrandbits(prec) | (1 << (prec - 1))
+    fr = lambda e, sgn=1: Fraction(sgn * m()) * Fraction(2) ** (e - prec)
+    X, Y, A = [], [], []
+    for g in list(range(100, 150, 3)) + [60, 64, 126, 127, 128, 129, 130, 192, 200]:
+        for case in range(3):
+            xr, xi, yr, yi = fr(0), fr(-g // 2), fr(1, -1), fr(-(g - g // 2))
+            if case == 0:
+                a = (fr(g), fr(-g, -1))                       # a far above the products
+            elif case == 1:
+                a = (fr(-g), fr(-g - 5))                      # a far below the products
+            else:                                             # products cancel each other
+                xi, yi = xr, yr
+                a = (fr(-g), fr(3))
+            X.append((xr, xi)); Y.append((yr, yi)); A.append(a)
+    dX, dY, dA = (P.to_device(row_of(v, prec)) for v in (X, Y, A))
+    Xh, Yh, Ah = (row_of(v, prec) for v in (X, Y, A))
+    for op in ("mul", "fms"):
+        G = P.to_host(P.mpc_scalar(op, dX, dY, dA))
+        R = oracle.cscalar(op, Xh, Yh, Ah)
+        assert same_bits(G, R), (op, first_mismatch(G, R))
+    Z = []
+    for g in list(range(50, 70)) + [0, 1, 2, 30, 100]:          # square gaps 2 g around 120
+        Z.append((fr(0), fr(-g, -1)))
+        Z.append((fr(-g), fr(0)))
+    Zh = row_of(Z, prec)
+    G = P.to_host(P.mpc_scalar("recip", P.to_device(Zh)))
+    R = oracle.cscalar("recip", Zh)
+    assert same_bits(G, R), first_mismatch(G, R)
+
+
 def lu_gpu(A, K, method, adaptive=0):
     dA = P.to_device(A)
     ipiv, rep = P.mpclu_factor(dA, K, method, adaptive=adaptive)
