@@ -600,10 +600,18 @@ MPC_DEV bool crecip_fast(int L, int part, const Num<C> &zr, const Num<C> &zi, in
         u[i] = (k >= 0 && k < 2 * C) ? (uint32_t)(nm[k >> 1] >> (32 * (k & 1))) : 0u;
     }
     uint32_t q[NQ];
+    // qhat = floor(numr / v_top) from a binary64 estimate (|error| <= 2: numr < 2^64 carries 53
+    // bits, qhat < 2^33), corrected exactly -- no 64-bit integer division in the loop
+    const uint64_t vt = v[N - 1];
+    const double rv = 1.0 / (double)vt;
 #pragma unroll
     for (int j = NQ - 1; j >= 0; j--) {
         const uint64_t numr = ((uint64_t)u[j + N] << 32) | u[j + N - 1];
-        uint64_t qhat = numr / v[N - 1], rhat = numr % v[N - 1];
+        uint64_t qhat = (uint64_t)((double)numr * rv);
+        if (qhat) qhat -= 1;                                  // now qhat * vt <= numr (see below)
+        while (qhat * vt > numr) qhat--;
+        uint64_t rhat = numr - qhat * vt;
+        while (rhat >= vt) { qhat++; rhat -= vt; }
         while (qhat >= (1ull << 32) || qhat * v[N - 2] > ((rhat << 32) | u[j + N - 2])) {
             qhat--; rhat += v[N - 1];
             if (rhat >= (1ull << 32)) break;
@@ -690,8 +698,8 @@ template <int C>
 MPC_DEV void crecip_part(int L, int part, const Num<C> &zr, const Num<C> &zi, int prec,
                          uint8_t *so, int64_t *eo, uint64_t *lo)
 {
-    if constexpr (C <= 8) {
-        if (crecip_fast<C>(L, part, zr, zi, prec, so, eo, lo)) return;
+    if constexpr (C <= 8) {                              // (C = 12: the unrolled division's code
+        if (crecip_fast<C>(L, part, zr, zi, prec, so, eo, lo)) return;   // size made it slower)
     }
     crecip_general<C>(L, part, zr, zi, prec, so, eo, lo);
 }
