@@ -1,15 +1,24 @@
 #!/bin/bash
-# full GPU suite with the defaults (k-phase hints, p-blocks of 32), then serpentine / p-block A/B
+# unit order / shared k-phase hints A/B: parity under the variant, bench GEMM ms, DRAM bytes of the slice GEMM
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SERPENTINE=0 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -1
 run() {  # tag env...
   local tag=$1; shift
   env "$@" timeout 600 python bench.py --no-e2e --no-cpu > gpurun_out/kp_$tag.json 2>/dev/null
   python -c "import json; d=json.load(open('gpurun_out/kp_$tag.json')); print('$tag', round(d['ms_per_step'],1), d['stages_ms']['ms_gemm'], d['clocks']['sm_mhz'])"
 }
-run def
-run serp0 MPCGEMM_SERPENTINE=0
-run pb40 MPCGEMM_PBLK=40
-run def2
-run serp0b MPCGEMM_SERPENTINE=0
-run pb28 MPCGEMM_PBLK=28
+ncurun() {
+  local tag=$1; shift
+  env "$@" timeout 900 ncu --metrics dram__bytes_read.sum,lts__t_sector_hit_rate.pct,gpu__time_duration.sum \
+    -k regex:slicegemm_tc2 -c 1 --csv python bench.py --no-e2e --no-cpu --steps 1 --warmup 0 > gpurun_out/kp_ncu_$tag.csv 2>/dev/null
+  grep -E "dram__|hit_rate|duration" gpurun_out/kp_ncu_$tag.csv | awk -F'"' -v t=$tag '{print t, $(NF-5), $(NF-1)}'
+}
+run base
+run h1 MPCGEMM_HINTS=1
+run o2m2 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=2 MPCGEMM_SERPENTINE=0
+run o2m1 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=1 MPCGEMM_SERPENTINE=0
+run o2m4 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=4 MPCGEMM_SERPENTINE=0
+run base2
+ncurun h1 MPCGEMM_HINTS=1
+ncurun o2m2 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=2 MPCGEMM_SERPENTINE=0
+ncurun o2m1 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=1 MPCGEMM_SERPENTINE=0
