@@ -3,11 +3,14 @@
 // the Ozaki GEMM of this library (mpcgemm.cu, accumulate mode); these kernels do the panel
 // (xGETF2: pivot search, row swap, reciprocal, column scaling, rank-1 updates), U12 := L11^-1
 // A12 and the substitutions, every scalar operation MPC-style (mpscalar.cuh).
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "common.cuh"
 #include "kernels.h"
 #include "mpscalar.cuh"
+#include "mpwarp.cuh"
 
 namespace mpc {
 
@@ -122,6 +125,52 @@ __global__ void __launch_bounds__(128) lu_scale_kernel(int L, DMatOut re, DMatOu
     cfms_part<C>(L, part, nullptr, xr, xi, yr, yi, prec, &so, &eo, lo);
     __syncwarp(3u << (threadIdx.x & 30));
     put_part(part ? b : a, so, eo, lo, L);
+}
+
+// ---------------------------------------------------------------- warp-cooperative (L <= 12)
+// one warp per (element, part), one limb per lane (mpwarp.cuh)
+MPC_DEV mpw::WNum wld(int L, const DMatOut &M, int64_t r, int64_t c, int lane) {
+    const El x = el(L, M, r, c);
+    return mpw::wload(L, x.s, x.e, x.l, lane);
+}
+
+// A_rc := cmul(A_rc, 1 / A_cc), r in [r0, r1): 4 elements per 256-thread block; every warp has
+// its operands in registers (block barrier) before any warp stores (in place)
+__global__ void __launch_bounds__(256) lu_scale_wkernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c,
+                                                        int prec, const uint8_t *rs, const int64_t *rexp,
+                                                        const uint64_t *rl)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, part = warp & 1;
+    const int64_t r = r0 + (int64_t)blockIdx.x * 4 + (warp >> 1);
+    const bool on = r < r1;
+    mpw::WNum xr{}, xi{}, yr{}, yi{};
+    if (on) {
+        xr = wld(L, re, r, c, lane); xi = wld(L, im, r, c, lane);
+        yr = mpw::wload(L, rs, rexp, rl, lane); yi = mpw::wload(L, rs + 1, rexp + 1, rl + L, lane);
+    }
+    __syncthreads();
+    if (!on) return;
+    const El o = el(L, part ? im : re, r, c);
+    mpw::cfms_warp(L, part, false, xr, xr, xi, yr, yi, prec, o.s, o.e, o.l, lane);
+}
+
+// A_rt := cfms(A_rt, A_rc, A_ct), r in [r0, r1), t in [t0, t1): one warp per (r, t, part)
+__global__ void __launch_bounds__(256) lu_update_wkernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0,
+                                                         int64_t t1, int64_t c, int prec)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t nt = t1 - t0, total = (r1 - r0) * nt * 2;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int part = (int)(w & 1);
+        const int64_t e = w >> 1, r = r0 + e / nt, t = t0 + e % nt;
+        const mpw::WNum lr = wld(L, re, r, c, lane), li = wld(L, im, r, c, lane);
+        const mpw::WNum ur = wld(L, re, c, t, lane), ui = wld(L, im, c, t, lane);
+        const El a = el(L, part ? im : re, r, t);
+        const mpw::WNum av = mpw::wload(L, a.s, a.e, a.l, lane);
+        __syncwarp();
+        mpw::cfms_warp(L, part, true, av, lr, li, ur, ui, prec, a.s, a.e, a.l, lane);
+    }
 }
 
 // ---------------------------------------------------------------- rank-1 update
@@ -291,7 +340,86 @@ __global__ void mp_scalar_kernel(int L, int op, int64_t cnt, int prec, DMatOut A
     cfms_part<C>(L, part, &av, x1, x2, y1, y2, prec, o.s, o.e, o.l);
 }
 
+// Eq. 7 solve steps, warp-cooperative (L <= 12): forward B_rq := cfms(B_rq, L_rc, B_cq), one
+// warp per (r, q, part)
+__global__ void __launch_bounds__(256) lu_fwd_wkernel(int L, DMatOut fre, DMatOut fim, DMatOut bre, DMatOut bim,
+                                                      int64_t c, int64_t n, int64_t nrhs, int prec)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int part = (int)(w & 1);
+    const int64_t x = w >> 1;
+    if (x >= (n - c - 1) * nrhs) return;
+    const int64_t r = c + 1 + x / nrhs, q = x % nrhs;
+    const mpw::WNum lr = wld(L, fre, r, c, lane), li = wld(L, fim, r, c, lane);
+    const mpw::WNum yr = wld(L, bre, c, q, lane), yi = wld(L, bim, c, q, lane);
+    const El a = el(L, part ? bim : bre, r, q);
+    const mpw::WNum av = mpw::wload(L, a.s, a.e, a.l, lane);
+    __syncwarp();
+    mpw::cfms_warp(L, part, true, av, lr, li, yr, yi, prec, a.s, a.e, a.l, lane);
+}
+
+// backward: x = cmul(B_cq, 1/U_cc) -- the two warps of an element's pair compute one part each
+// into shared memory -- then B_rq := cfms(B_rq, U_rc, x) (r < c) or X_cq := x (r == c)
+__global__ void __launch_bounds__(256) lu_bwd_wkernel(int L, DMatOut fre, DMatOut fim, DMatOut bre, DMatOut bim,
+                                                      DMatOut xre, DMatOut xim, DMatOut rre, DMatOut rim,
+                                                      int64_t c, int64_t nrhs, int prec)
+{
+    __shared__ uint8_t ss[4][2];
+    __shared__ int64_t se[4][2];
+    __shared__ uint64_t sl[4][2][16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, part = warp & 1, slot = warp >> 1;
+    const int64_t x = (int64_t)blockIdx.x * 4 + slot;
+    const bool on = x < (c + 1) * nrhs;
+    const int64_t r = on ? x / nrhs : 0, q = on ? x % nrhs : 0;
+    if (on) {
+        const mpw::WNum yr = wld(L, bre, c, q, lane), yi = wld(L, bim, c, q, lane);
+        const mpw::WNum wr = wld(L, rre, 0, c, lane), wi = wld(L, rim, 0, c, lane);
+        mpw::cfms_warp(L, part, false, yr, yr, yi, wr, wi, prec, &ss[slot][part], &se[slot][part], sl[slot][part], lane);
+    }
+    __syncthreads();
+    if (!on) return;
+    if (r == c) {
+        const El o = el(L, part ? xim : xre, c, q);
+        if (lane < L) o.l[lane] = sl[slot][part][lane];
+        if (lane == 0) { *o.s = ss[slot][part]; *o.e = se[slot][part]; }
+        return;
+    }
+    const mpw::WNum vr = mpw::wload(L, &ss[slot][0], &se[slot][0], sl[slot][0], lane);
+    const mpw::WNum vi = mpw::wload(L, &ss[slot][1], &se[slot][1], sl[slot][1], lane);
+    const mpw::WNum ur = wld(L, fre, r, c, lane), ui = wld(L, fim, r, c, lane);
+    const El a = el(L, part ? bim : bre, r, q);
+    const mpw::WNum av = mpw::wload(L, a.s, a.e, a.l, lane);
+    __syncwarp();
+    mpw::cfms_warp(L, part, true, av, ur, ui, vr, vi, prec, a.s, a.e, a.l, lane);
+}
+
+// op 0 / 1 of mp_scalar_kernel, warp-cooperative (L <= 12)
+__global__ void __launch_bounds__(256) mp_scalar_wkernel(int L, int op, int64_t cnt, int prec, DMatOut Ar, DMatOut Ai,
+                                                         DMatOut Xr, DMatOut Xi, DMatOut Yr, DMatOut Yi, DMatOut Or,
+                                                         DMatOut Oi)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int part = (int)(w & 1);
+    const int64_t t = w >> 1;
+    if (t >= cnt) return;
+    const mpw::WNum x1 = wld(L, Xr, 0, t, lane), x2 = wld(L, Xi, 0, t, lane);
+    const mpw::WNum y1 = wld(L, Yr, 0, t, lane), y2 = wld(L, Yi, 0, t, lane);
+    const mpw::WNum av = op == 1 ? wld(L, part ? Ai : Ar, 0, t, lane) : x1;
+    const El o = el(L, part ? Oi : Or, 0, t);
+    mpw::cfms_warp(L, part, op == 1, av, x1, x2, y1, y2, prec, o.s, o.e, o.l, lane);
+}
+
 // ---------------------------------------------------------------- launchers (L dispatch)
+// Warp kernels (L <= 12) run a launch when it has at most MPCGEMM_MPWARP_MAX elements (default
+// 1024; 0: never): a warp per element part issues ~32x the instructions of a thread per part,
+// so it pays only while the launch is latency-bound (few elements)
+static int64_t mpw_max() {
+    const char *e = getenv("MPCGEMM_MPWARP_MAX");
+    return e && *e ? atoll(e) : 1024;
+}
+
 // capacity instantiation for L limbs: 4, 8 or 16
 #define MPC_DISPATCH_C(L, KERNEL_CALL)                        \
     do {                                                      \
@@ -326,6 +454,10 @@ cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r
     if (r1 <= r0) return cudaSuccess;
     const unsigned g = (unsigned)((2 * (r1 - r0) + 127) / 128);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    if (L <= 12 && r1 - r0 <= mpw_max()) {
+        lu_scale_wkernel<<<(unsigned)((r1 - r0 + 3) / 4), 256, 0, st>>>(L, re, im, r0, r1, c, prec, s.sign, s.exp, s.limbs);
+        return cudaGetLastError();
+    }
     MPC_DISPATCH_C(L, (lu_scale_kernel<C><<<g, 128, 0, st>>>(L, re, im, r0, r1, c, prec, s.sign, s.exp, s.limbs)));
     return cudaGetLastError();
 }
@@ -333,6 +465,12 @@ cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r
 cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0, int64_t t1, int64_t c,
                              int prec, cudaStream_t st) {
     if (r1 <= r0 || t1 <= t0) return cudaSuccess;
+    if (L >= 1 && L <= 12 && (r1 - r0) * (t1 - t0) <= mpw_max()) {
+        const int64_t warps = (r1 - r0) * (t1 - t0) * 2;
+        const int64_t blocks = std::min<int64_t>((warps + 7) / 8, 148 * 64);
+        lu_update_wkernel<<<(unsigned)blocks, 256, 0, st>>>(L, re, im, r0, r1, t0, t1, c, prec);
+        return cudaGetLastError();
+    }
     const int64_t rows = r1 - r0;
     const int64_t gx = (2 * (t1 - t0) + 127) / 128;
     int64_t gy = rows;
@@ -353,11 +491,21 @@ cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const in
     lu_perm_kernel<<<1, 1, 0, st>>>(n, ipiv, s.perm);
     lu_gather_kernel<<<(unsigned)((n * nrhs * 2 * L + 255) / 256), 256, 0, st>>>(L, bre, bim, s.xre, s.xim, n, nrhs, s.perm);
     lu_copy_kernel<<<(unsigned)((n * nrhs + 127) / 128), 128, 0, st>>>(L, s.xre, s.xim, bre, bim, n, nrhs);
-    for (int64_t c = 0; c + 1 < n; c++)
-        MPC_DISPATCH_C(L, (lu_fwd_kernel<C><<<(unsigned)((2 * (n - c - 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, c, n, nrhs, prec)));
-    for (int64_t c = n - 1; c >= 0; c--)
-        MPC_DISPATCH_C(L, (lu_bwd_kernel<C><<<(unsigned)((2 * (c + 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, s.xre, s.xim,
-                                                                             s.rre, s.rim, c, nrhs, prec)));
+    const int64_t wmax = mpw_max();
+    for (int64_t c = 0; c + 1 < n; c++) {
+        if (L <= 12 && (n - c - 1) * nrhs <= wmax)
+            lu_fwd_wkernel<<<(unsigned)(((n - c - 1) * nrhs * 2 + 7) / 8), 256, 0, st>>>(L, fre, fim, bre, bim, c, n, nrhs, prec);
+        else
+            MPC_DISPATCH_C(L, (lu_fwd_kernel<C><<<(unsigned)((2 * (n - c - 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, c, n, nrhs, prec)));
+    }
+    for (int64_t c = n - 1; c >= 0; c--) {
+        if (L <= 12 && (c + 1) * nrhs <= wmax)
+            lu_bwd_wkernel<<<(unsigned)(((c + 1) * nrhs + 3) / 4), 256, 0, st>>>(L, fre, fim, bre, bim, s.xre, s.xim, s.rre, s.rim,
+                                                                                   c, nrhs, prec);
+        else
+            MPC_DISPATCH_C(L, (lu_bwd_kernel<C><<<(unsigned)((2 * (c + 1) * nrhs + 127) / 128), 128, 0, st>>>(L, fre, fim, bre, bim, s.xre, s.xim,
+                                                                                 s.rre, s.rim, c, nrhs, prec)));
+    }
     lu_copy_kernel<<<(unsigned)((n * nrhs + 127) / 128), 128, 0, st>>>(L, s.xre, s.xim, bre, bim, n, nrhs);
     return cudaGetLastError();
 }
@@ -367,6 +515,10 @@ cudaError_t mp_scalar_launch(int L, int op, int64_t cnt, int prec, DMatOut Ar, D
     if (cnt <= 0) return cudaSuccess;
     const unsigned g = (unsigned)((2 * cnt + 127) / 128);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    if ((op == 0 || op == 1) && L <= 12 && mpw_max() > 0) {
+        mp_scalar_wkernel<<<(unsigned)((2 * cnt + 7) / 8), 256, 0, st>>>(L, op, cnt, prec, Ar, Ai, Xr, Xi, Yr, Yi, Or, Oi);
+        return cudaGetLastError();
+    }
     MPC_DISPATCH_C(L, (mp_scalar_kernel<C><<<g, 128, 0, st>>>(L, op, cnt, prec, Ar, Ai, Xr, Xi, Yr, Yi, Or, Oi, kv)));
     return cudaGetLastError();
 }

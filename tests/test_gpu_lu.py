@@ -115,6 +115,26 @@ def test_fast_path_window_edges_bitexact(prec):
     assert same_bits(G, R), first_mismatch(G, R)
 
 
+@pytest.mark.parametrize("wmax", ["0", "100000"])
+def test_thread_and_warp_kernels_agree(monkeypatch, wmax):
+    """The LU's scalar kernels for L <= 12 exist twice -- a thread per element part and a warp per
+    element part (mpwarp.cuh), chosen by launch size (MPCGEMM_MPWARP_MAX): forcing either gives
+    the oracle's bits for the scalar ops and a small factorization."""
+    monkeypatch.setenv("MPCGEMM_MPWARP_MAX", wmax)
+    for prec, spread in ((256, 8), (512, 40), (200, 300), (768, 20), (700, 250)):
+        X, Y, A = scalar_inputs(prec, spread, 120, prec + 3 * spread)
+        dX, dY, dA = P.to_device(X), P.to_device(Y), P.to_device(A)
+        for op in ("mul", "fms"):
+            G = P.to_host(P.mpc_scalar(op, dX, dY, dA))
+            R = oracle.cscalar(op, X, Y, A)
+            assert same_bits(G, R), (wmax, op, first_mismatch(G, R))
+    A = mpgen.random_cmat(77, 51, 40, 40, 256, 2)
+    F, ipiv, rep, _ = lu_gpu(A, 8, "3M")
+    R, ipiv_r, info_r, _ = oracle.lu_factor(A, 8, "3M")
+    assert list(ipiv) == list(ipiv_r) and rep["info"] == info_r
+    assert same_bits(F, R), first_mismatch(F, R)
+
+
 def lu_gpu(A, K, method, adaptive=0):
     dA = P.to_device(A)
     ipiv, rep = P.mpclu_factor(dA, K, method, adaptive=adaptive)
