@@ -340,6 +340,21 @@ __global__ void mp_scalar_kernel(int L, int op, int64_t cnt, int prec, DMatOut A
     cfms_part<C>(L, part, &av, x1, x2, y1, y2, prec, o.s, o.e, o.l);
 }
 
+// 1 / A_cc into the scratch, one warp per part (L <= 8); *info = c + 1 on the first zero pivot
+__global__ void __launch_bounds__(64) lu_recip_wkernel(int L, DMatOut re, DMatOut im, int64_t c, int prec, uint8_t *rs,
+                                                       int64_t *rexp, uint64_t *rl, int32_t *info)
+{
+    const int lane = threadIdx.x & 31, part = threadIdx.x >> 5;
+    const mpw::WNum zr = wld(L, re, c, c, lane), zi = wld(L, im, c, c, lane);
+    if (zr.zero && zi.zero) {
+        if (part == 0 && lane == 0 && info && *info == 0) *info = (int32_t)(c + 1);
+        if (lane == 0) { rs[part] = 0; rexp[part] = 0; }
+        if (lane < L) rl[part * L + lane] = 0;
+        return;
+    }
+    mpw::crecip_warp(L, part, zr, zi, prec, rs + part, rexp + part, rl + part * L, lane);
+}
+
 // Eq. 7 solve steps, warp-cooperative (L <= 12): forward B_rq := cfms(B_rq, L_rc, B_cq), one
 // warp per (r, q, part)
 __global__ void __launch_bounds__(256) lu_fwd_wkernel(int L, DMatOut fre, DMatOut fim, DMatOut bre, DMatOut bim,
@@ -405,9 +420,18 @@ __global__ void __launch_bounds__(256) mp_scalar_wkernel(int L, int op, int64_t 
     const int64_t t = w >> 1;
     if (t >= cnt) return;
     const mpw::WNum x1 = wld(L, Xr, 0, t, lane), x2 = wld(L, Xi, 0, t, lane);
+    const El o = el(L, part ? Oi : Or, 0, t);
+    if (op == 2) {
+        if (x1.zero && x2.zero) {                      // (the tests pass nonzero z only)
+            if (lane < L) o.l[lane] = 0;
+            if (lane == 0) { *o.s = 0; *o.e = 0; }
+            return;
+        }
+        mpw::crecip_warp(L, part, x1, x2, prec, o.s, o.e, o.l, lane);
+        return;
+    }
     const mpw::WNum y1 = wld(L, Yr, 0, t, lane), y2 = wld(L, Yi, 0, t, lane);
     const mpw::WNum av = op == 1 ? wld(L, part ? Ai : Ar, 0, t, lane) : x1;
-    const El o = el(L, part ? Oi : Or, 0, t);
     mpw::cfms_warp(L, part, op == 1, av, x1, x2, y1, y2, prec, o.s, o.e, o.l, lane);
 }
 
@@ -445,6 +469,10 @@ cudaError_t lu_swap_launch(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t
 cudaError_t lu_recip_launch(int L, DMatOut re, DMatOut im, int64_t c, int prec, LuScratch s, int32_t *info,
                             cudaStream_t st) {
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    if (L <= 8 && mpw_max() > 0) {
+        lu_recip_wkernel<<<1, 64, 0, st>>>(L, re, im, c, prec, s.sign, s.exp, s.limbs, info);
+        return cudaGetLastError();
+    }
     MPC_DISPATCH_C(L, (lu_recip_kernel<C><<<1, 2, 0, st>>>(L, re, im, c, prec, s.sign, s.exp, s.limbs, info)));
     return cudaGetLastError();
 }
@@ -515,7 +543,7 @@ cudaError_t mp_scalar_launch(int L, int op, int64_t cnt, int prec, DMatOut Ar, D
     if (cnt <= 0) return cudaSuccess;
     const unsigned g = (unsigned)((2 * cnt + 127) / 128);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    if ((op == 0 || op == 1) && L <= 12 && mpw_max() > 0) {
+    if (((op == 0 || op == 1) && L <= 12 || op == 2 && L <= 8) && mpw_max() > 0) {
         mp_scalar_wkernel<<<(unsigned)((2 * cnt + 7) / 8), 256, 0, st>>>(L, op, cnt, prec, Ar, Ai, Xr, Xi, Yr, Yi, Or, Oi);
         return cudaGetLastError();
     }

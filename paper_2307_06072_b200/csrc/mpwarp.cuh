@@ -182,5 +182,129 @@ MPC_DEV void cfms_warp(int L, int part, bool sub, const WNum &a, const WNum &xr,
     if (lane == 0) { *so = (neg && nzv) ? 1 : 0; *eo = E; }
 }
 
+// ---------------------------------------------------------------- reciprocal (L <= 8)
+// 128 / 64 division helpers for Knuth's algorithm D in base 2^64 (d normalised: top bit set)
+MPC_DEV uint64_t invert_limb(uint64_t d) {             // floor((2^128 - 1) / d) - 2^64
+    uint64_t hi = ~d, lo = ~0ull, q = 0;               // (hi:lo) = 2^128 - 1 - d 2^64, hi < d
+    for (int i = 0; i < 64; i++) {                     // restoring long division, one bit a step
+        const bool top = hi >> 63;
+        hi = (hi << 1) | (lo >> 63);
+        lo <<= 1;
+        q <<= 1;
+        if (top || hi >= d) { hi -= d; q |= 1; }
+    }
+    return q;
+}
+// (u1:u0) / d with u1 < d: quotient and remainder (Moller and Granlund's 2-by-1 division)
+MPC_DEV uint64_t div_preinv(uint64_t u1, uint64_t u0, uint64_t d, uint64_t v, uint64_t *r_out) {
+    uint64_t q0 = v * u1, q1 = __umul64hi(v, u1);
+    const uint64_t t = q0 + u0;
+    q1 += u1 + (t < q0);
+    q0 = t;
+    q1 += 1;
+    uint64_t r = u0 - q1 * d;
+    if (r > q0) { q1 -= 1; r += d; }
+    if (r >= d) { q1 += 1; r -= d; }
+    *r_out = r;
+    return q1;
+}
+
+// one part of 1 / (zr + i zi): part 0 zr / D, part 1 -zi / D, D = zr^2 + zi^2 exactly (square
+// exponents <= 120 bits apart, else lane 0 runs the single-thread code on gathered operands).
+// Knuth's algorithm D in base 2^64 with the divisor normalised in ND = 2L + 2 lanes, the
+// numerator's mantissa placed at limb ND + 1 (quotient L + 2 limbs >= prec + 2 bits), each
+// quotient limb's multiply-subtract across the warp; then RNE of 2 q + (remainder != 0).
+MPC_DEV void crecip_warp(int L, int part, const WNum &zr, const WNum &zi, int prec, uint8_t *so, int64_t *eo,
+                         uint64_t *lo, int lane)
+{
+    const WNum &num = part ? zi : zr;
+    if (num.zero) {
+        if (lane < L) lo[lane] = 0;
+        if (lane == 0) { *so = 0; *eo = 0; }
+        return;
+    }
+    const bool hr = !zr.zero, hi = !zi.zero;
+    int64_t de;
+    uint64_t D;
+    if (hr && hi) {
+        const int64_t gr = 2 * zr.e, gi = 2 * zi.e;
+        if ((gr > gi ? gr - gi : gi - gr) > 120) {
+            mps::Num<8> n[2];
+            const WNum *src[2] = {&zr, &zi};
+            for (int q = 0; q < 2; q++) {
+                for (int l = 0; l < 8; l++) {
+                    const uint64_t v = __shfl_sync(kAll, src[q]->m, l);
+                    n[q].m[l] = l < L ? v : 0ull;
+                }
+                n[q].e = src[q]->e; n[q].neg = src[q]->neg; n[q].zero = src[q]->zero;
+            }
+            if (lane == 0) mps::crecip_part<8>(L, part, n[0], n[1], prec, so, eo, lo);
+            return;
+        }
+        de = gr < gi ? gr : gi;
+        const uint64_t sr = wshl(wmul(zr.m, zr.m, L, lane), gr - de, lane);
+        const uint64_t si = wshl(wmul(zi.m, zi.m, L, lane), gi - de, lane);
+        D = wadd(sr, si, false, lane);
+    } else {
+        const WNum &z = hr ? zr : zi;
+        de = 2 * z.e;
+        D = wmul(z.m, z.m, L, lane);
+    }
+    const int ND = 2 * L + 2;                           // divisor limbs
+    const unsigned nzd = __ballot_sync(kAll, D != 0);
+    const int hl = 31 - __clz(nzd);
+    const int bd = 64 * hl + 64 - __clzll((long long)__shfl_sync(kAll, D, hl));
+    const int sd = 64 * ND - bd;                        // normalise: top bit at 64 ND - 1
+    const uint64_t Dn = wshl(D, sd, lane);
+    const uint64_t vt = __shfl_sync(kAll, Dn, ND - 1), v2 = __shfl_sync(kAll, Dn, ND - 2);
+    const uint64_t vinv = invert_limb(vt);
+    // U = N 2^(64 (ND + 1)): limbs ND+1 .. ND+L, plus the zero top limb ND+L+1
+    uint64_t u = wshl(num.m, 64 * (int64_t)(ND + 1), lane);
+    uint64_t q = 0;
+    const int m = L + 1;                                // quotient limbs j = m .. 0
+    for (int j = m; j >= 0; j--) {
+        const uint64_t ut = __shfl_sync(kAll, u, j + ND), un = __shfl_sync(kAll, u, j + ND - 1);
+        const uint64_t u2 = __shfl_sync(kAll, u, j + ND - 2);
+        uint64_t qh, rh;
+        bool rover = false;
+        if (ut >= vt) {                                 // (ut == vt) qhat = 2^64 - 1
+            qh = ~0ull;
+            rh = un + vt;
+            rover = rh < un;
+        } else {
+            qh = div_preinv(ut, un, vt, vinv, &rh);
+        }
+        while (!rover) {                                // Knuth's test with the second limb
+            const uint64_t plo = qh * v2, phi = __umul64hi(qh, v2);
+            if (phi > rh || (phi == rh && plo > u2)) {
+                qh--;
+                const uint64_t r2 = rh + vt;
+                rover = r2 < rh;
+                rh = r2;
+            } else break;
+        }
+        // u -= qh Dn 2^(64 j)
+        const uint64_t plo = qh * Dn, phi = __umul64hi(qh, Dn);
+        const uint64_t hin = __shfl_up_sync(kAll, phi, 1);
+        const uint64_t qv = wadd(plo, lane >= 1 ? hin : 0ull, false, lane);   // qh Dn, ND + 1 limbs
+        const uint64_t t = wshl(qv, 64 * (int64_t)j, lane);
+        u = wsub(u, t, lane);
+        if ((int64_t)__shfl_sync(kAll, u, 31) < 0) {    // qhat one too large: add back
+            qh--;
+            u = wadd(u, wshl(Dn, 64 * (int64_t)j, lane), false, lane);
+        }
+        if (lane == j) q = qh;
+    }
+    const bool rem = __ballot_sync(kAll, u != 0) != 0;
+    uint64_t r = wshl(q, 1, lane);
+    if (lane == 0 && rem) r |= 1ull;
+    // value = (U / Dn) 2^(num.e - de - X), X = 64 (ND + 1) - sd
+    const int64_t X = 64 * (int64_t)(ND + 1) - sd;
+    int64_t E;
+    const uint64_t res = wround(r, num.e - de - X - 1, prec, L, lane, &E);
+    if (lane < L) lo[lane] = res;
+    if (lane == 0) { *so = (part ? !num.neg : num.neg) ? 1 : 0; *eo = E; }
+}
+
 }  // namespace mpw
 }  // namespace mpc
