@@ -1,7 +1,10 @@
 """Randomised GPU parity: 160 seeded combinations of shape (incl. 1 and ragged tile tails), precision
 (every limb count 1..16 and a few wide ones), exponent spread, zero fraction, method, slice count
 (auto / forced), adaptive blocks, accumulate mode and padded leading dimensions -- every sampled output
-bit-exact against the oracle (Algorithm 2 under the DESIGN.md readings)."""
+bit-exact against the oracle (Algorithm 2 under the DESIGN.md readings).  MPCGEMM_FUZZ_SEEDS=N
+runs N seeds (a longer sweep)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -36,7 +39,7 @@ def case(seed):
     return m, n, k, prec, spread, zf, method, forced, adaptive, beta, pad
 
 
-@pytest.mark.parametrize("seed", list(range(160)))
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("MPCGEMM_FUZZ_SEEDS", "160")))))
 def test_fuzz_bitexact(seed):
     m, n, k, prec, spread, zf, method, forced, adaptive, beta, pad = case(seed)
     A = mpgen.random_cmat(seed, 1, m, k, prec, spread, zero_frac=zf)
@@ -69,3 +72,39 @@ def test_fuzz_bitexact(seed):
         Rs = oracle.ozaki(A, B, prec, method, s, samples=(si, sj))
     bad = sampled_equal(C, Rs, si, sj)
     assert bad is None, (case(seed), bad)
+
+
+def case_large(seed):
+    rng = np.random.default_rng(5000 + seed)
+    m = int(rng.choice([257, 513, 700, 1100]))
+    n = int(rng.choice([129, 300, 640, 1024]))
+    k = int(rng.choice([128, 255, 600, 1300]))
+    prec = int(rng.choice([256, 320, 512, 768, 1024]))
+    spread = int(rng.choice([0, 2, 16]))
+    method = str(rng.choice(["3M", "4M"]))
+    beta = int(rng.integers(0, 2))
+    return m, n, k, prec, spread, method, beta
+
+
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("MPCGEMM_FUZZ_LARGE", "4")))))
+def test_fuzz_large_bitexact(seed):
+    """Larger shapes (many tiles, exactness chunks, p-blocks, k-phase hints, ragged k-blocks):
+    sampled outputs bit-exact against the oracle.  MPCGEMM_FUZZ_LARGE=N runs N seeds."""
+    m, n, k, prec, spread, method, beta = case_large(seed)
+    A = mpgen.random_cmat(seed, 11, m, k, prec, spread)
+    B = mpgen.random_cmat(seed, 12, k, n, prec, spread)
+    C0 = mpgen.random_cmat(seed, 13, m, n, prec, spread)
+    dA, dB = P.to_device(A), P.to_device(B)
+    dC = P.to_device(C0) if beta else P.empty_device(m, n, prec)
+    rep = P.mpcgemm_ex(dA, dB, dC, prec, method, beta=beta)
+    torch.cuda.synchronize()
+    C = P.to_host(dC)
+    rng = np.random.default_rng(seed)
+    si = np.concatenate([rng.integers(0, m, 24), [0, m - 1, 255, 256]])
+    sj = np.concatenate([rng.integers(0, n, 24), [n - 1, 0, 127, 128]])
+    if beta:
+        Rs = oracle.ozaki_acc(A, B, C0, prec, method, s=rep["slices"], beta=1, samples=(si, sj))
+    else:
+        Rs = oracle.ozaki(A, B, prec, method, rep["slices"], samples=(si, sj))
+    bad = sampled_equal(C, Rs, si, sj)
+    assert bad is None, (case_large(seed), bad)

@@ -212,3 +212,20 @@ def test_lu_solve_bitexact_and_eq7(n, K, prec, nrhs):
             di = float(to_fraction(Xg.im, k, q) - xv[k][q][1])
             err = max(err, math.hypot(dr, di) / abs(complex(float(xv[k][q][0]), float(xv[k][q][1]))))
     assert err <= 2.0 ** -(prec - 24)
+
+
+@pytest.mark.parametrize("seed", list(range(int(__import__("os").environ.get("MPCGEMM_FUZZ_LU", "6")))))
+def test_fuzz_lu_bitexact(seed):
+    """Random (n, K, prec, spread, method): factorization bit-exact against the oracle, both the
+    warp (small launches) and the thread (large launches) kernels in play.  MPCGEMM_FUZZ_LU=N."""
+    rng = np.random.default_rng(7000 + seed)
+    n = int(rng.choice([1, 3, 17, 40, 64, 90]))
+    K = int(rng.choice([1, 2, 8, 16, 33, 128]))
+    prec = int(rng.choice([64, 128, 200, 256, 512, 700] if n > 40 else [64, 128, 256, 512, 768, 1000]))
+    spread = int(rng.choice([0, 3, 30]))
+    method = str(rng.choice(["3M", "4M"]))
+    A = mpgen.random_cmat(seed, 60, n, n, prec, spread)
+    F, ipiv, rep, _ = lu_gpu(A, K, method)
+    R, ipiv_r, info_r, smax_r = oracle.lu_factor(A, K, method)
+    assert list(ipiv) == list(ipiv_r) and rep["info"] == info_r, (n, K, prec, spread, method)
+    assert same_bits(F, R), ((n, K, prec, spread, method), first_mismatch(F, R))
