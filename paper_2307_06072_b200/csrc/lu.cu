@@ -12,6 +12,11 @@
 #include "mpscalar.cuh"
 #include "mpwarp.cuh"
 
+// resident blocks per SM for the thread-per-part rank-1 update (large launches): capping it at
+// 128 registers doubles the threads in flight; measured best (3: 170, 6: 85 registers are slower)
+#ifndef MPC_UPD_MINB
+#define MPC_UPD_MINB 4
+#endif
 namespace mpc {
 
 using namespace mps;
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(256) lu_update_wkernel(int L, DMatOut re, DMat
 // ---------------------------------------------------------------- rank-1 update
 // A_rt := cfms(A_rt, A_rc, A_ct) for r in [r0, r1), t in [t0, t1)  (lane pairs: the two parts)
 template <int C>
-__global__ void __launch_bounds__(128) lu_update_kernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0,
+__global__ void __launch_bounds__(128, MPC_UPD_MINB) lu_update_kernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0,
                                                         int64_t t1, int64_t c, int prec)
 {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
