@@ -32,10 +32,16 @@ template <int C>
 MPC_DEV Num<C> ld(int L, const El &x) { return load<C>(L, x.s, x.e, x.l); }
 
 // ---------------------------------------------------------------- pivot search (one CTA)
+// the larger key, ties to the smaller row (the first maximum)
+MPC_DEV void key_max(int64_t &e, double &v, int64_t &r, int64_t e2, double v2, int64_t r2) {
+    const Key a{e, v}, b{e2, v2};
+    if (key_greater(b, a) || (!key_greater(a, b) && r2 < r)) { e = e2; v = v2; r = r2; }
+}
+
 __global__ void __launch_bounds__(1024) lu_pivot_kernel(int L, DMatOut re, DMatOut im, int64_t n, int64_t c, int64_t *ipiv)
 {
-    __shared__ int64_t se[1024], sr[1024];
-    __shared__ double sv[1024];
+    __shared__ int64_t se[32], sr[32];
+    __shared__ double sv[32];
     Key best; best.e = INT64_MIN; best.v = 0.0;
     int64_t br = c;
     for (int64_t r = c + threadIdx.x; r < n; r += blockDim.x) {
@@ -43,19 +49,20 @@ __global__ void __launch_bounds__(1024) lu_pivot_kernel(int L, DMatOut re, DMatO
         const Key k = pivot_key(a.s, a.e, a.l, b.s, b.e, b.l, L);
         if (key_greater(k, best)) { best = k; br = r; }      // rows ascending: first max kept
     }
-    se[threadIdx.x] = best.e; sv[threadIdx.x] = best.v; sr[threadIdx.x] = br;
+    int64_t e = best.e, r = br;
+    double v = best.v;
+    for (int o = 16; o > 0; o >>= 1)                        // warp, then across warps
+        key_max(e, v, r, __shfl_xor_sync(0xFFFFFFFFu, e, o), __shfl_xor_sync(0xFFFFFFFFu, v, o),
+                __shfl_xor_sync(0xFFFFFFFFu, r, o));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (lane == 0) { se[warp] = e; sv[warp] = v; sr[warp] = r; }
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) {
-            const int o = threadIdx.x + w;
-            const Key a{se[threadIdx.x], sv[threadIdx.x]}, b{se[o], sv[o]};
-            if (key_greater(b, a) || (!key_greater(a, b) && sr[o] < sr[threadIdx.x])) {
-                se[threadIdx.x] = b.e; sv[threadIdx.x] = b.v; sr[threadIdx.x] = sr[o];
-            }
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) ipiv[c] = sr[0];
+    if (warp) return;
+    e = lane < nw ? se[lane] : INT64_MIN; v = lane < nw ? sv[lane] : 0.0; r = lane < nw ? sr[lane] : n;
+    for (int o = 16; o > 0; o >>= 1)
+        key_max(e, v, r, __shfl_xor_sync(0xFFFFFFFFu, e, o), __shfl_xor_sync(0xFFFFFFFFu, v, o),
+                __shfl_xor_sync(0xFFFFFFFFu, r, o));
+    if (lane == 0) ipiv[c] = r;
 }
 
 // ---------------------------------------------------------------- row swap (all columns)
