@@ -352,7 +352,7 @@ __global__ void mp_scalar_kernel(int L, int op, int64_t cnt, int prec, DMatOut A
     cfms_part<C>(L, part, &av, x1, x2, y1, y2, prec, o.s, o.e, o.l);
 }
 
-// 1 / A_cc into the scratch, one warp per part (L <= 8); *info = c + 1 on the first zero pivot
+// 1 / A_cc into the scratch, one warp per part (L <= 12); *info = c + 1 on the first zero pivot
 __global__ void __launch_bounds__(64) lu_recip_wkernel(int L, DMatOut re, DMatOut im, int64_t c, int prec, uint8_t *rs,
                                                        int64_t *rexp, uint64_t *rl, int32_t *info)
 {
@@ -481,7 +481,7 @@ cudaError_t lu_swap_launch(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t
 cudaError_t lu_recip_launch(int L, DMatOut re, DMatOut im, int64_t c, int prec, LuScratch s, int32_t *info,
                             cudaStream_t st) {
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    if (L <= 8 && mpw_max() > 0) {
+    if (L <= 12 && mpw_max() > 0) {
         lu_recip_wkernel<<<1, 64, 0, st>>>(L, re, im, c, prec, s.sign, s.exp, s.limbs, info);
         return cudaGetLastError();
     }
@@ -555,7 +555,7 @@ cudaError_t mp_scalar_launch(int L, int op, int64_t cnt, int prec, DMatOut Ar, D
     if (cnt <= 0) return cudaSuccess;
     const unsigned g = (unsigned)((2 * cnt + 127) / 128);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    if (((op == 0 || op == 1) && L <= 12 || op == 2 && L <= 8) && mpw_max() > 0) {
+    if ((op == 0 || op == 1 || op == 2) && L <= 12 && mpw_max() > 0) {
         mp_scalar_wkernel<<<(unsigned)((2 * cnt + 7) / 8), 256, 0, st>>>(L, op, cnt, prec, Ar, Ai, Xr, Xi, Yr, Yi, Or, Oi);
         return cudaGetLastError();
     }

@@ -182,7 +182,7 @@ MPC_DEV void cfms_warp(int L, int part, bool sub, const WNum &a, const WNum &xr,
     if (lane == 0) { *so = (neg && nzv) ? 1 : 0; *eo = E; }
 }
 
-// ---------------------------------------------------------------- reciprocal (L <= 8)
+// ---------------------------------------------------------------- reciprocal (L <= 12)
 // 128 / 64 division helpers for Knuth's algorithm D in base 2^64 (d normalised: top bit set)
 MPC_DEV uint64_t invert_limb(uint64_t d) {             // floor((2^128 - 1) / d) - 2^64
     uint64_t hi = ~d, lo = ~0ull, q = 0;               // (hi:lo) = 2^128 - 1 - d 2^64, hi < d
@@ -213,7 +213,8 @@ MPC_DEV uint64_t div_preinv(uint64_t u1, uint64_t u0, uint64_t d, uint64_t v, ui
 // exponents <= 120 bits apart, else lane 0 runs the single-thread code on gathered operands).
 // Knuth's algorithm D in base 2^64 with the divisor normalised in ND = 2L + 2 lanes, the
 // numerator's mantissa placed at limb ND + 1 (quotient L + 2 limbs >= prec + 2 bits), each
-// quotient limb's multiply-subtract across the warp; then RNE of 2 q + (remainder != 0).
+// quotient limb's multiply-subtract across the warp on a sliding ND + 1-limb window of the
+// dividend; then RNE of 2 q + (remainder != 0).
 MPC_DEV void crecip_warp(int L, int part, const WNum &zr, const WNum &zi, int prec, uint8_t *so, int64_t *eo,
                          uint64_t *lo, int lane)
 {
@@ -229,16 +230,16 @@ MPC_DEV void crecip_warp(int L, int part, const WNum &zr, const WNum &zi, int pr
     if (hr && hi) {
         const int64_t gr = 2 * zr.e, gi = 2 * zi.e;
         if ((gr > gi ? gr - gi : gi - gr) > 120) {
-            mps::Num<8> n[2];
+            mps::Num<16> n[2];
             const WNum *src[2] = {&zr, &zi};
             for (int q = 0; q < 2; q++) {
-                for (int l = 0; l < 8; l++) {
+                for (int l = 0; l < 16; l++) {
                     const uint64_t v = __shfl_sync(kAll, src[q]->m, l);
                     n[q].m[l] = l < L ? v : 0ull;
                 }
                 n[q].e = src[q]->e; n[q].neg = src[q]->neg; n[q].zero = src[q]->zero;
             }
-            if (lane == 0) mps::crecip_part<8>(L, part, n[0], n[1], prec, so, eo, lo);
+            if (lane == 0) mps::crecip_part<16>(L, part, n[0], n[1], prec, so, eo, lo);
             return;
         }
         de = gr < gi ? gr : gi;
@@ -258,13 +259,15 @@ MPC_DEV void crecip_warp(int L, int part, const WNum &zr, const WNum &zi, int pr
     const uint64_t Dn = wshl(D, sd, lane);
     const uint64_t vt = __shfl_sync(kAll, Dn, ND - 1), v2 = __shfl_sync(kAll, Dn, ND - 2);
     const uint64_t vinv = invert_limb(vt);
-    // U = N 2^(64 (ND + 1)): limbs ND+1 .. ND+L, plus the zero top limb ND+L+1
-    uint64_t u = wshl(num.m, 64 * (int64_t)(ND + 1), lane);
-    uint64_t q = 0;
+    // U = N 2^(64 (ND + 1)): limbs ND+1 .. ND+L, plus the zero top limb ND+L+1.  Step j touches
+    // limbs j .. j+ND only, so the warp holds that window (lane l = limb j + l), moved down one
+    // limb per step (the limbs entering below are U's zeros): ND + 1 <= 27 lanes for L <= 12
     const int m = L + 1;                                // quotient limbs j = m .. 0
+    uint64_t u = wshl(num.m, 64 * (int64_t)(ND + 1 - m), lane);
+    uint64_t q = 0;
     for (int j = m; j >= 0; j--) {
-        const uint64_t ut = __shfl_sync(kAll, u, j + ND), un = __shfl_sync(kAll, u, j + ND - 1);
-        const uint64_t u2 = __shfl_sync(kAll, u, j + ND - 2);
+        const uint64_t ut = __shfl_sync(kAll, u, ND), un = __shfl_sync(kAll, u, ND - 1);
+        const uint64_t u2 = __shfl_sync(kAll, u, ND - 2);
         uint64_t qh, rh;
         bool rover = false;
         if (ut >= vt) {                                 // (ut == vt) qhat = 2^64 - 1
@@ -283,19 +286,22 @@ MPC_DEV void crecip_warp(int L, int part, const WNum &zr, const WNum &zi, int pr
                 rh = r2;
             } else break;
         }
-        // u -= qh Dn 2^(64 j)
+        // window -= qh Dn
         const uint64_t plo = qh * Dn, phi = __umul64hi(qh, Dn);
         const uint64_t hin = __shfl_up_sync(kAll, phi, 1);
         const uint64_t qv = wadd(plo, lane >= 1 ? hin : 0ull, false, lane);   // qh Dn, ND + 1 limbs
-        const uint64_t t = wshl(qv, 64 * (int64_t)j, lane);
-        u = wsub(u, t, lane);
+        u = wsub(u, qv, lane);
         if ((int64_t)__shfl_sync(kAll, u, 31) < 0) {    // qhat one too large: add back
             qh--;
-            u = wadd(u, wshl(Dn, 64 * (int64_t)j, lane), false, lane);
+            u = wadd(u, Dn, false, lane);
         }
         if (lane == j) q = qh;
+        if (j) {                                        // next window: limbs j-1 .. j-1+ND
+            const uint64_t d = __shfl_up_sync(kAll, u, 1);
+            u = lane ? d : 0ull;
+        }
     }
-    const bool rem = __ballot_sync(kAll, u != 0) != 0;
+    const bool rem = __ballot_sync(kAll, u != 0) != 0;  // the remainder: lanes 0 .. ND-1
     uint64_t r = wshl(q, 1, lane);
     if (lane == 0 && rem) r |= 1ull;
     // value = (U / Dn) 2^(num.e - de - X), X = 64 (ND + 1) - sd
