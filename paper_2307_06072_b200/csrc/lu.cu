@@ -449,11 +449,12 @@ __global__ void __launch_bounds__(256) mp_scalar_wkernel(int L, int op, int64_t 
 
 // ---------------------------------------------------------------- launchers (L dispatch)
 // Warp kernels (L <= 12) run a launch when it has at most MPCGEMM_MPWARP_MAX elements (default
-// 1024; 0: never): a warp per element part issues ~32x the instructions of a thread per part,
-// so it pays only while the launch is latency-bound (few elements)
-static int64_t mpw_max() {
+// 1024 for L <= 8, 4096 above, where the thread-per-part code is slower; 0: never): a warp per
+// element part issues ~32x the instructions of a thread per part, so it pays only while the
+// launch is latency-bound (few elements)
+static int64_t mpw_max(int L) {
     const char *e = getenv("MPCGEMM_MPWARP_MAX");
-    return e && *e ? atoll(e) : 1024;
+    return e && *e ? atoll(e) : (L > 8 ? 4096 : 1024);
 }
 
 // capacity instantiation for L limbs: 4, 8 or 16
@@ -481,7 +482,7 @@ cudaError_t lu_swap_launch(int L, DMatOut re, DMatOut im, int64_t ncols, int64_t
 cudaError_t lu_recip_launch(int L, DMatOut re, DMatOut im, int64_t c, int prec, LuScratch s, int32_t *info,
                             cudaStream_t st) {
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    if (L <= 12 && mpw_max() > 0) {
+    if (L <= 12 && mpw_max(L) > 0) {
         lu_recip_wkernel<<<1, 64, 0, st>>>(L, re, im, c, prec, s.sign, s.exp, s.limbs, info);
         return cudaGetLastError();
     }
@@ -494,7 +495,7 @@ cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r
     if (r1 <= r0) return cudaSuccess;
     const unsigned g = (unsigned)((2 * (r1 - r0) + 127) / 128);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    if (L <= 12 && r1 - r0 <= mpw_max()) {
+    if (L <= 12 && r1 - r0 <= mpw_max(L)) {
         lu_scale_wkernel<<<(unsigned)((r1 - r0 + 3) / 4), 256, 0, st>>>(L, re, im, r0, r1, c, prec, s.sign, s.exp, s.limbs);
         return cudaGetLastError();
     }
@@ -505,7 +506,7 @@ cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r
 cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0, int64_t t1, int64_t c,
                              int prec, cudaStream_t st) {
     if (r1 <= r0 || t1 <= t0) return cudaSuccess;
-    if (L >= 1 && L <= 12 && (r1 - r0) * (t1 - t0) <= mpw_max()) {
+    if (L >= 1 && L <= 12 && (r1 - r0) * (t1 - t0) <= mpw_max(L)) {
         const int64_t warps = (r1 - r0) * (t1 - t0) * 2;
         const int64_t blocks = std::min<int64_t>((warps + 7) / 8, 148 * 64);
         lu_update_wkernel<<<(unsigned)blocks, 256, 0, st>>>(L, re, im, r0, r1, t0, t1, c, prec);
@@ -531,7 +532,7 @@ cudaError_t lu_solve_launch(int L, DMatOut fre, DMatOut fim, int64_t n, const in
     lu_perm_kernel<<<1, 1, 0, st>>>(n, ipiv, s.perm);
     lu_gather_kernel<<<(unsigned)((n * nrhs * 2 * L + 255) / 256), 256, 0, st>>>(L, bre, bim, s.xre, s.xim, n, nrhs, s.perm);
     lu_copy_kernel<<<(unsigned)((n * nrhs + 127) / 128), 128, 0, st>>>(L, s.xre, s.xim, bre, bim, n, nrhs);
-    const int64_t wmax = mpw_max();
+    const int64_t wmax = mpw_max(L);
     for (int64_t c = 0; c + 1 < n; c++) {
         if (L <= 12 && (n - c - 1) * nrhs <= wmax)
             lu_fwd_wkernel<<<(unsigned)(((n - c - 1) * nrhs * 2 + 7) / 8), 256, 0, st>>>(L, fre, fim, bre, bim, c, n, nrhs, prec);
@@ -555,7 +556,7 @@ cudaError_t mp_scalar_launch(int L, int op, int64_t cnt, int prec, DMatOut Ar, D
     if (cnt <= 0) return cudaSuccess;
     const unsigned g = (unsigned)((2 * cnt + 127) / 128);
     if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
-    if ((op == 0 || op == 1 || op == 2) && L <= 12 && mpw_max() > 0) {
+    if ((op == 0 || op == 1 || op == 2) && L <= 12 && mpw_max(L) > 0) {
         mp_scalar_wkernel<<<(unsigned)((2 * cnt + 7) / 8), 256, 0, st>>>(L, op, cnt, prec, Ar, Ai, Xr, Xi, Yr, Yi, Or, Oi);
         return cudaGetLastError();
     }
