@@ -89,7 +89,8 @@ struct GemmParams {
     int32_t dbg;               // power experiments only (MPCGEMM_DBG, results invalid when != 0):
                                // bit 0: epilogue skips the partial-plane stores; bit 1: every TMA
                                // load reads plane 0 / tile (0, 0) (L2-resident operands); bit 2: loads
-                               // cycle through 8 planes x 2 k-blocks x 2 tiles (~1 MB, varying data)
+                               // cycle through 8 planes x 2 k-blocks x 2 tiles (~1 MB, varying data);
+                               // bit 3: after the first ring fill no loads at all (smem reused)
     int32_t *hot;              // k-phase hints, one per (job, r, chunk) group (or null): the position
                                // (pair, p-block, k-block) a running unit of the group last started;
                                // a new unit of the group begins there (CTA-pair kernel, G >= 2)

@@ -305,9 +305,16 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             // ---------------- (leader) scheduler + both CTAs' TMA producers
             int stage = 0; uint32_t phase = 0;
             int qs = 0; uint32_t qph = 0;
+            int nload = 0;
             auto load = [&](int planeA, int planeB, int kb, int tm, int tn) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 skk[stage] = (uint8_t)(kb == KB - 1 && P.kk_last ? P.kk_last : kBK / 32);   // before the arrive (release)
+                if ((P.dbg & 8) && nload >= STAGES) {          // experiment: no operand traffic at all
+                    if (rank == 0) mbar_arrive(&full[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    return;
+                }
+                nload++;
                 if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
                 if (P.dbg & 2) { planeA = planeB = 0; kb = 0; tm = tn = 0; }
                 if (P.dbg & 4) { planeA &= 7; planeB &= 7; kb &= 1; tm &= 1; tn &= 1; }   // ~1 MB of varying operands
