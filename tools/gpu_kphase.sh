@@ -1,7 +1,7 @@
 #!/bin/bash
-# unit order / shared k-phase hints A/B: parity under the variant, bench GEMM ms, DRAM bytes of the slice GEMM
+# k-phase hand-off A/B: parity, bench GEMM ms with MPCGEMM_HANDOFF=1/0, DRAM bytes of the slice GEMM
 mkdir -p gpurun_out
-MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SERPENTINE=0 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q -m gpu 2>&1 | tail -1
 run() {  # tag env...
   local tag=$1; shift
   env "$@" timeout 600 python bench.py --no-e2e --no-cpu > gpurun_out/kp_$tag.json 2>/dev/null
@@ -13,12 +13,9 @@ ncurun() {
     -k regex:slicegemm_tc2 -c 1 --csv python bench.py --no-e2e --no-cpu --steps 1 --warmup 0 > gpurun_out/kp_ncu_$tag.csv 2>/dev/null
   grep -E "dram__|hit_rate|duration" gpurun_out/kp_ncu_$tag.csv | awk -F'"' -v t=$tag '{print t, $(NF-5), $(NF-1)}'
 }
-run base
-run h1 MPCGEMM_HINTS=1
-run o2m2 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=2 MPCGEMM_SERPENTINE=0
-run o2m1 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=1 MPCGEMM_SERPENTINE=0
-run o2m4 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=4 MPCGEMM_SERPENTINE=0
-run base2
-ncurun h1 MPCGEMM_HINTS=1
-ncurun o2m2 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=2 MPCGEMM_SERPENTINE=0
-ncurun o2m1 MPCGEMM_HINTS=1 MPCGEMM_ORDER=2 MPCGEMM_SGM=1 MPCGEMM_SERPENTINE=0
+run h1 MPCGEMM_HANDOFF=1
+run h0 MPCGEMM_HANDOFF=0
+run h1b MPCGEMM_HANDOFF=1
+run h0b MPCGEMM_HANDOFF=0
+ncurun h1 MPCGEMM_HANDOFF=1
+ncurun h0 MPCGEMM_HANDOFF=0
