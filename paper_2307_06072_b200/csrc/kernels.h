@@ -84,6 +84,10 @@ cudaError_t lu_recip_launch(int L, DMatOut re, DMatOut im, int64_t c, int prec, 
                             cudaStream_t st);
 cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec, LuScratch s,
                             cudaStream_t st);
+// 1 / A_cc into s (and *info) and A_rc := cmul(A_rc, 1 / A_cc) for r in [r0, r1): one launch when
+// the warp kernels apply, else lu_recip_launch + lu_scale_launch
+cudaError_t lu_recip_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec,
+                                  LuScratch s, int32_t *info, int *nlaunch, cudaStream_t st);
 cudaError_t lu_update_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t t0, int64_t t1, int64_t c,
                              int prec, cudaStream_t st);
 struct SolveScratch {

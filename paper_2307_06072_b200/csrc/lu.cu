@@ -367,6 +367,42 @@ __global__ void __launch_bounds__(64) lu_recip_wkernel(int L, DMatOut re, DMatOu
     mpw::crecip_warp(L, part, zr, zi, prec, rs + part, rexp + part, rl + part * L, lane);
 }
 
+// recip + scale in one launch (L <= 12, few rows): warps 0 and 1 of every block compute the two
+// parts of 1 / A_cc into shared memory (block 0 also stores them and the zero-pivot flag), then
+// every warp scales its element part: A_rc := cmul(A_rc, 1 / A_cc), r in [r0, r1)
+__global__ void __launch_bounds__(256) lu_recip_scale_wkernel(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1,
+                                                              int64_t c, int prec, uint8_t *rs, int64_t *rexp,
+                                                              uint64_t *rl, int32_t *info)
+{
+    __shared__ uint8_t ss[2];
+    __shared__ int64_t se[2];
+    __shared__ uint64_t sl[2][16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, part = warp & 1;
+    if (warp < 2) {
+        const mpw::WNum zr = wld(L, re, c, c, lane), zi = wld(L, im, c, c, lane);
+        if (zr.zero && zi.zero) {
+            if (blockIdx.x == 0 && part == 0 && lane == 0 && info && *info == 0) *info = (int32_t)(c + 1);
+            if (lane == 0) { ss[part] = 0; se[part] = 0; }
+            if (lane < L) sl[part][lane] = 0;
+        } else {
+            mpw::crecip_warp(L, part, zr, zi, prec, &ss[part], &se[part], sl[part], lane);
+        }
+    }
+    const int64_t r = r0 + (int64_t)blockIdx.x * 4 + (warp >> 1);
+    const bool on = r < r1;
+    mpw::WNum xr{}, xi{};
+    if (on) { xr = wld(L, re, r, c, lane); xi = wld(L, im, r, c, lane); }
+    __syncthreads();                                  // recip in shared memory; operands in registers
+    if (blockIdx.x == 0 && warp < 2) {
+        if (lane < L) rl[part * L + lane] = sl[part][lane];
+        if (lane == 0) { rs[part] = ss[part]; rexp[part] = se[part]; }
+    }
+    if (!on) return;
+    const mpw::WNum yr = mpw::wload(L, &ss[0], &se[0], sl[0], lane), yi = mpw::wload(L, &ss[1], &se[1], sl[1], lane);
+    const El o = el(L, part ? im : re, r, c);
+    mpw::cfms_warp(L, part, false, xr, xr, xi, yr, yi, prec, o.s, o.e, o.l, lane);
+}
+
 // Eq. 7 solve steps, warp-cooperative (L <= 12): forward B_rq := cfms(B_rq, L_rc, B_cq), one
 // warp per (r, q, part)
 __global__ void __launch_bounds__(256) lu_fwd_wkernel(int L, DMatOut fre, DMatOut fim, DMatOut bre, DMatOut bim,
@@ -488,6 +524,21 @@ cudaError_t lu_recip_launch(int L, DMatOut re, DMatOut im, int64_t c, int prec, 
     }
     MPC_DISPATCH_C(L, (lu_recip_kernel<C><<<1, 2, 0, st>>>(L, re, im, c, prec, s.sign, s.exp, s.limbs, info)));
     return cudaGetLastError();
+}
+
+cudaError_t lu_recip_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec,
+                                  LuScratch s, int32_t *info, int *nlaunch, cudaStream_t st) {
+    if (L < 1 || L > mps::kLMax) return cudaErrorInvalidValue;
+    *nlaunch = 1;
+    if (L <= 12 && r1 > r0 && r1 - r0 <= mpw_max(L)) {
+        lu_recip_scale_wkernel<<<(unsigned)((r1 - r0 + 3) / 4), 256, 0, st>>>(L, re, im, r0, r1, c, prec, s.sign, s.exp,
+                                                                              s.limbs, info);
+        return cudaGetLastError();
+    }
+    cudaError_t e = lu_recip_launch(L, re, im, c, prec, s, info, st);
+    if (e != cudaSuccess) return e;
+    *nlaunch = r1 > r0 ? 2 : 1;
+    return lu_scale_launch(L, re, im, r0, r1, c, prec, s, st);
 }
 
 cudaError_t lu_scale_launch(int L, DMatOut re, DMatOut im, int64_t r0, int64_t r1, int64_t c, int prec, LuScratch s,

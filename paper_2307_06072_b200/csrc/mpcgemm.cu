@@ -936,10 +936,10 @@ int lu_impl(int64_t n, int32_t prec, mpc_cmat *A, int64_t *ipiv, int32_t K, int 
         for (int64_t c = j0; c < j0 + w; c++) {               // (a) panel, xGETF2
             CK(lu_pivot_launch(L, re, im, n, c, ipiv, st));
             CK(lu_swap_launch(L, re, im, n, c, ipiv, st));
-            CK(lu_recip_launch(L, re, im, c, prec, sc, info, st));
-            CK(lu_scale_launch(L, re, im, c + 1, n, c, prec, sc, st));
+            int nrs = 0;
+            CK(lu_recip_scale_launch(L, re, im, c + 1, n, c, prec, sc, info, &nrs, st));
             CK(lu_update_launch(L, re, im, c + 1, n, c + 1, j0 + w, c, prec, st));
-            launches += 5;
+            launches += 3 + nrs;
         }
         T.lap(&tp);
         if (j0 + w >= n) break;
