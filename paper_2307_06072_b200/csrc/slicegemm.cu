@@ -306,7 +306,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             int stage = 0; uint32_t phase = 0;
             int qs = 0; uint32_t qph = 0;
             int nload = 0;
-            auto load = [&](int planeA, int planeB, int kb, int tm, int tn) {
+            auto load = [&](int planeA, int planeB, int kb, int tm, int tn, bool a_only = false) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 skk[stage] = (uint8_t)(kb == KB - 1 && P.kk_last ? P.kk_last : kBK / 32);   // before the arrive (release)
                 if ((P.dbg & 8) && nload >= STAGES) {          // experiment: no operand traffic at all
@@ -315,11 +315,12 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     return;
                 }
                 nload++;
-                if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+                if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (a_only ? Cfg::A_BYTES : Cfg::STAGE_BYTES));
                 if (P.dbg & 2) { planeA = planeB = 0; kb = 0; tm = tn = 0; }
                 if (P.dbg & 4) { planeA &= 7; planeB &= 7; kb &= 1; tm &= 1; tn &= 1; }   // ~1 MB of varying operands
                 tma_load_3d_2sm(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, tm * 256 + (int)rank * 128, planeA);
-                tma_load_3d_2sm(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, tn * 256 + (int)rank * 128, planeB);
+                if (!a_only)                                  // (a p-block's lead stage needs only A)
+                    tma_load_3d_2sm(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, tn * 256 + (int)rank * 128, planeB);
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             };
             for (;;) {
@@ -369,7 +370,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         const int kb = unit_kb(w, pos - pb * nkb);
                         const int p0 = unit_pfirst(np, nblk, blk), p1 = unit_pfirst(np, nblk, blk + 1) - 1;
                         if (rank == 0 && P.hot) st_relaxed_s32(P.hot + w.slot0, pos);
-                        if (g2 && p0 > 1) load(J.pa[pr] * s + p0 - 2, J.pb[pr] * s + (w.r - p0), kb, w.tm, w.tn);
+                        if (g2 && p0 > 1) load(J.pa[pr] * s + p0 - 2, 0, kb, w.tm, w.tn, true);   // A_{p0-1} only
                         for (int p = p0; p <= p1; p++)
                             load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1 + g2), kb, w.tm, w.tn);
                         if (++pos == npos) pos = 0;
