@@ -5,7 +5,9 @@ Output row blocks of C are independent (eA_i is row-local), so A is row-partitio
 replicated on every rank.  The only data-dependent exchange is the slice count: every rank
 runs the rho-hat pre-pass on its rows and the ranks all-reduce its integers (MIN of minT;
 if that is 0, a second round of MIN minT1 / MAX maxD2), so all ranks use the same s and C is
-bitwise identical for any number of GPUs.  C row blocks can be all-gathered.
+bitwise identical for any number of GPUs.  A can be row-scattered from one rank
+(scatter_rows), B broadcast from one rank (broadcast_fields), and C row blocks all-gathered
+(gather_rows).
 """
 from __future__ import annotations
 
@@ -60,6 +62,37 @@ def gather_rows(local: torch.Tensor, m: int, device, group=None) -> torch.Tensor
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
     return torch.cat([parts[r][: row_range(m, r, world)[1] - row_range(m, r, world)[0]] for r in range(world)], 0)
+
+
+def broadcast_fields(fields: dict, src: int = 0, group=None) -> dict:
+    """B broadcast: every tensor of `fields` (e.g. one part's sign / exp / limbs, allocated with
+    the same shape on every rank) is overwritten in place by the source rank's copy."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        for t in fields.values():
+            dist.broadcast(t, src=src, group=group)
+    return fields
+
+
+def scatter_rows(full, m: int, rest: tuple, dtype, device, src: int = 0, group=None) -> torch.Tensor:
+    """Row shards: the source rank's [m, *rest] tensor `full` is cut into the row_range blocks and
+    each rank receives its own block (other ranks pass full=None)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world == 1:
+        return full
+    r0, r1 = row_range(m, rank, world)
+    maxr = row_range(m, 0, world)[1]
+    out = torch.empty((maxr,) + tuple(rest), dtype=dtype, device=device)
+    chunks = None
+    if rank == src:
+        chunks = []
+        for r in range(world):
+            a, b = row_range(m, r, world)
+            c = torch.zeros((maxr,) + tuple(rest), dtype=dtype, device=device)
+            c[: b - a] = full[a:b]
+            chunks.append(c)
+    dist.scatter(out, chunks, src=src, group=group)
+    return out[: r1 - r0]
 
 
 def orchestrate(bounds_fn, slices_fn, local_fn, prec: int, method, k: int, device="cpu", group=None):

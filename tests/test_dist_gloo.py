@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 
 import mpgen
 import oracle
-from paper_2307_06072_b200.dist import gather_rows, orchestrate, row_range
+from paper_2307_06072_b200.dist import broadcast_fields, gather_rows, orchestrate, row_range, scatter_rows
 
 
 def _free_port():
@@ -30,14 +30,41 @@ def _to_t(R):
             "limbs": torch.from_numpy(R.limbs.view(np.int64).copy())}
 
 
-def _worker(rank, world, port, case, outdir):
+def _from_t(fields, prec):
+    return mpgen.RMat(fields["sign"].numpy().copy(), fields["exp"].numpy().copy(),
+                      fields["limbs"].numpy().view(np.uint64).copy(), prec)
+
+
+def _distribute(A, B, m, n, k, prec, rank):
+    """Rank 0 alone holds A and B: A's rows are scattered, B broadcast (torch tensors)."""
+    L = (prec + 63) // 64
+    Al, Bl = {}, {}
+    for p in ("re", "im"):
+        src_a = _to_t(getattr(A, p)) if rank == 0 else None
+        Al[p] = {f: scatter_rows(src_a[f] if src_a else None, m, rest, dt, "cpu")
+                 for f, rest, dt in (("sign", (k,), torch.uint8), ("exp", (k,), torch.int64),
+                                     ("limbs", (k, L), torch.int64))}
+        fb = _to_t(getattr(B, p)) if rank == 0 else {"sign": torch.zeros((k, n), dtype=torch.uint8),
+                                                    "exp": torch.zeros((k, n), dtype=torch.int64),
+                                                    "limbs": torch.zeros((k, n, L), dtype=torch.int64)}
+        Bl[p] = broadcast_fields(fb)
+    return (mpgen.CMat(_from_t(Al["re"], prec), _from_t(Al["im"], prec)),
+            mpgen.CMat(_from_t(Bl["re"], prec), _from_t(Bl["im"], prec)))
+
+
+def _worker(rank, world, port, case, outdir, distribute=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     m, n, k, prec, spread, method = case
     A = mpgen.random_cmat(77, 1, m, k, prec, spread, zero_frac=0.1)
     B = mpgen.random_cmat(77, 2, k, n, prec, spread, zero_frac=0.1)
     r0, r1 = row_range(m, rank, world)
-    Al = A.rows(r0, r1)
+    if distribute:                                     # only rank 0's copies are used
+        if rank:
+            A = B = None
+        Al, B = _distribute(A, B, m, n, k, prec, rank)
+    else:
+        Al = A.rows(r0, r1)
     s, bounds, C = orchestrate(lambda full: oracle.rho_bounds(Al, B, full=full),
                                lambda *a: oracle.slices_for(*a)[0],
                                lambda s_: oracle.ozaki(Al, B, prec, method, s_),
@@ -58,13 +85,16 @@ def test_row_range_partition():
             assert max(b - a for a, b in rr) - min(b - a for a, b in rr) <= 1
 
 
+@pytest.mark.parametrize("distribute", [False, True])
 @pytest.mark.parametrize("case", [(7, 9, 11, 128, 4, "3M"),      # ragged rows
                                   (9, 6, 12, 256, 16, "4M"),     # minT == 0: second round
                                   (1, 5, 8, 128, 0, "3M")])      # one rank without rows
-def test_two_ranks_gloo(case):
+def test_two_ranks_gloo(case, distribute):
+    """distribute: A row-scattered and B broadcast from rank 0 instead of every
+    rank generating its own copies."""
     m, n, k, prec, spread, method = case
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(2, _free_port(), case, d), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, _free_port(), case, d, distribute), nprocs=2, join=True)
         z = np.load(os.path.join(d, "out.npz"))
         A = mpgen.random_cmat(77, 1, m, k, prec, spread, zero_frac=0.1)
         B = mpgen.random_cmat(77, 2, k, n, prec, spread, zero_frac=0.1)
