@@ -635,6 +635,15 @@ int encode_limb_map(void *map, const uint64_t *base, int L, uint64_t d1, uint64_
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// L2 promotion of the digit-plane loads (MPCGEMM_L2PROMO = 0/64/128/256): 128 B = one box row,
+// 148 GB DRAM reads per cfg4 launch vs 161 GB with 256 B (same time within noise)
+static CUtensorMapL2promotion l2_promotion() {
+    const char *e = getenv("MPCGEMM_L2PROMO");
+    const int v = e && *e ? atoi(e) : 128;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // 3-D map over digit planes int8 [planes][rows][kp] with box {128, box_rows, 1}, 128B swizzle
 static int make_plane_map(CUtensorMap *map, const int8_t *base, int64_t planes, int64_t rows, int64_t kp, int box_rows) {
     auto enc = get_encode();
@@ -644,7 +653,7 @@ static int make_plane_map(CUtensorMap *map, const int8_t *base, int64_t planes, 
     cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : -2;
 }

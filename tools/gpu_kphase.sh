@@ -1,8 +1,11 @@
 #!/bin/bash
-# A/B of the current tree vs MPCGEMM_PBLK=0 (no p-blocks, no lead stages): parity, bench GEMM ms
+# TMA L2 promotion A/B for the digit-plane maps (MPCGEMM_L2PROMO): bench GEMM ms and DRAM bytes
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py -x -q -m gpu 2>&1 | tail -1
-for T in a b a b; do
-  timeout 600 python bench.py --no-e2e --no-cpu > gpurun_out/kp_$T.json 2>/dev/null
-  python -c "import json; d=json.load(open('gpurun_out/kp_$T.json')); print('$T', round(d['ms_per_step'],1), d['stages_ms']['ms_gemm'], d['clocks']['sm_mhz'])"
+for V in 256 128 0 256 128 0; do
+  MPCGEMM_L2PROMO=$V timeout 600 python bench.py --no-e2e --no-cpu > gpurun_out/kp_$V.json 2>/dev/null
+  python -c "import json; d=json.load(open('gpurun_out/kp_$V.json')); print('promo=$V', round(d['ms_per_step'],1), d['stages_ms']['ms_gemm'], d['clocks']['sm_mhz'])"
+done
+for V in 128 0; do
+  MPCGEMM_L2PROMO=$V timeout 900 ncu --metrics dram__bytes_read.sum,gpu__time_duration.sum -k regex:slicegemm_tc2 -c 1 --csv \
+    python bench.py --no-e2e --no-cpu --steps 1 --warmup 0 2>/dev/null | grep -E "dram__" | awk -F'"' -v t=$V '{print "promo=" t, $(NF-5), $(NF-1)}'
 done
