@@ -26,6 +26,27 @@ namespace mpc {
 
 constexpr int kBM = 128;
 
+// The K = 32 MMAs of one stage into accumulator d: unpredicated for a full k-block (a per-MMA
+// predicate there cost ~6 % of the tensor pipe's issue rate), guarded for the last, partial one.
+// acc0: enable-input of the first MMA (0 overwrites the accumulator).
+template <bool PAIR>
+MPC_DEV void issue_kblock(uint32_t d, uint32_t a, uint32_t b, uint32_t idesc, uint32_t acc0, int n) {
+    if (n == kBK / 32) {
+#pragma unroll
+        for (int kk = 0; kk < kBK / 32; kk++) {
+            if constexpr (PAIR) mma_i8_2sm(d, make_sw128_desc(a + kk * 32), make_sw128_desc(b + kk * 32), idesc, kk ? 1u : acc0);
+            else                mma_i8(d, make_sw128_desc(a + kk * 32), make_sw128_desc(b + kk * 32), idesc, kk ? 1u : acc0);
+        }
+    } else {
+#pragma unroll
+        for (int kk = 0; kk < kBK / 32; kk++)
+            if (kk < n) {
+                if constexpr (PAIR) mma_i8_2sm(d, make_sw128_desc(a + kk * 32), make_sw128_desc(b + kk * 32), idesc, kk ? 1u : acc0);
+                else                mma_i8(d, make_sw128_desc(a + kk * 32), make_sw128_desc(b + kk * 32), idesc, kk ? 1u : acc0);
+            }
+    }
+}
+
 template <int BN, int STAGES>
 struct TcCfg {
     static constexpr int A_BYTES = kBM * kBK;
@@ -153,19 +174,11 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                                 const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                                 const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
                                 const bool first = (pr == 0 && i == 0);
-                                const int nkk = skk[stage];
-#pragma unroll
-                                for (int kk = 0; kk < kBK / 32; kk++)   // D_{r+1} += A_p B_{r+1-p}
-                                    if (kk < nkk)
-                                        mma_i8(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                               (first && p == 1 && kk == 0) ? 0u : 1u);
+                                const int nkk = (unit_kb(w, i) == KB - 1 && P.kk_last) ? P.kk_last : kBK / 32;
+                                issue_kblock<false>(d1, a0, b0, idesc, (first && p == 1) ? 0u : 1u, nkk);   // D_{r+1} += A_p B_{r+1-p}
                                 if (p >= 2) {                           // D_r += A_{p-1} B_{r+1-p}
-                                    const uint32_t ap = smem_u32(sA + prev * Cfg::A_BYTES);
-#pragma unroll
-                                    for (int kk = 0; kk < kBK / 32; kk++)
-                                        if (kk < nkk)
-                                            mma_i8(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                                   (first && p == 2 && kk == 0) ? 0u : 1u);
+                                    issue_kblock<false>(d0, smem_u32(sA + prev * Cfg::A_BYTES), b0, idesc,
+                                                        (first && p == 2) ? 0u : 1u, nkk);
                                     mma_commit(&empty[prev]);           // A_{p-1} no longer needed
                                 }
                                 if (p == w.r) mma_commit(&empty[stage]);   // A_r pairs only with B_1
@@ -179,12 +192,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                        const int nkk = skk[stage];
-#pragma unroll
-                        for (int kk = 0; kk < kBK / 32; kk++)
-                            if (kk < nkk)
-                                mma_i8(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                       (g > 0 || kk > 0) ? 1u : 0u);
+                        issue_kblock<false>(d0, a0, b0, idesc, g > 0 ? 1u : 0u, skk[stage]);
                         mma_commit(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -416,6 +424,9 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     for (int t = 0; t < npos; t++) {
                         const int blk = (pos / nkb) % nblk;
                         const int p0 = unit_pfirst(w.r, nblk, blk), p1 = unit_pfirst(w.r, nblk, blk + 1) - 1;
+                        // MMA K-steps of this position's k-block (from registers: a shared-memory
+                        // read here would sit between each stage's barrier and its first MMA)
+                        const int nkk = (unit_kb(w, pos % nkb) == KB - 1 && P.kk_last) ? P.kk_last : kBK / 32;
                         int prev = -1;
                         if (p0 > 1) {                                   // lead stage: A_{p0-1}
                             mbar_wait(&full[stage], phase);
@@ -427,23 +438,11 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                             tc_fence_after();
                             const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                             const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                            const int nkk = skk[stage];
-#pragma unroll
-                            for (int kk = 0; kk < kBK / 32; kk++) {     // D_{r+1} += A_p B_{r+1-p}
-                                if (kk < nkk) {
-                                    mma_i8_2sm(d1, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc, acc1);
-                                    acc1 = 1u;
-                                }
-                            }
+                            issue_kblock<true>(d1, a0, b0, idesc, acc1, nkk);   // D_{r+1} += A_p B_{r+1-p}
+                            acc1 = 1u;
                             if (prev >= 0) {                            // D_r += A_{p-1} B_{r+1-p}
-                                const uint32_t ap = smem_u32(sA + prev * Cfg::A_BYTES);
-#pragma unroll
-                                for (int kk = 0; kk < kBK / 32; kk++) {
-                                    if (kk < nkk) {
-                                        mma_i8_2sm(d0, make_sw128_desc(ap + kk * 32), make_sw128_desc(b0 + kk * 32), idesc, acc0);
-                                        acc0 = 1u;
-                                    }
-                                }
+                                issue_kblock<true>(d0, smem_u32(sA + prev * Cfg::A_BYTES), b0, idesc, acc0, nkk);
+                                acc0 = 1u;
                                 mma_commit_2sm(&empty[prev]);
                             }
                             if (p == p1) mma_commit_2sm(&empty[stage]);
@@ -459,12 +458,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                        const int nkk = skk[stage];
-#pragma unroll
-                        for (int kk = 0; kk < kBK / 32; kk++)
-                            if (kk < nkk)
-                                mma_i8_2sm(d0, make_sw128_desc(a0 + kk * 32), make_sw128_desc(b0 + kk * 32), idesc,
-                                           (g > 0 || kk > 0) ? 1u : 0u);
+                        issue_kblock<true>(d0, a0, b0, idesc, g > 0 ? 1u : 0u, skk[stage]);
                         mma_commit_2sm(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
