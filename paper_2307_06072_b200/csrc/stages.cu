@@ -335,6 +335,21 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
         __syncthreads();
         // plane rows of this word: (part p, byte bt) -> plane s-1-(8w+bt), 16-byte vector stores
         const int nb = min(8, s - 8 * w);
+        if (rowlen == kSplitT) {                       // full tile: 8 vectors per row, no divisions
+            constexpr int VPR = kSplitT / 16;
+#pragma unroll
+            for (int it = 0; it < (3 * 8 * VPR + kSplitT - 1) / kSplitT; it++) {
+                const int q = tid + it * kSplitT;
+                if (q >= nparts * 8 * VPR) break;
+                const int row = q / VPR, v = q % VPR;
+                const int p = row >> 3, bt = row & 7;
+                if (bt < nb) {
+                    int8_t *o = dig + ((int64_t)p * s + (s - 1 - 8 * w - bt)) * plane + line * kp + k0 + 16 * v;
+                    *reinterpret_cast<uint4 *>(o) = *reinterpret_cast<const uint4 *>(stg + (p * 8 + bt) * kSplitT + 16 * v);
+                }
+            }
+            continue;
+        }
         const int vec_per_row = (int)((rowlen + 15) / 16);
         for (int q = tid; q < nparts * 8 * vec_per_row; q += kSplitT) {
             const int row = q / vec_per_row, v = q - row * vec_per_row;
