@@ -804,8 +804,20 @@ constexpr int kFoldEPT = 2;            // outputs per consumer thread (4 was tri
 static_assert(kFoldEPT == kFoldLdAlign, "scratch pitch alignment");
 
 template <int V> struct IntVec;
-template <> struct IntVec<2> { using T = int2; MPC_DEV static void get(const T &v, int32_t (&o)[2]) { o[0] = v.x; o[1] = v.y; } };
-template <> struct IntVec<4> { using T = int4; MPC_DEV static void get(const T &v, int32_t (&o)[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; } };
+template <> struct IntVec<2> {
+    using T = int2;
+    MPC_DEV static void get(const T &v, int32_t (&o)[2]) { o[0] = v.x; o[1] = v.y; }
+    MPC_DEV static void get_shared(uint32_t a, int32_t (&o)[2]) {
+        asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(o[0]), "=r"(o[1]) : "r"(a) : "memory");
+    }
+};
+template <> struct IntVec<4> {
+    using T = int4;
+    MPC_DEV static void get(const T &v, int32_t (&o)[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+    MPC_DEV static void get_shared(uint32_t a, int32_t (&o)[4]) {
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "r"(a) : "memory");
+    }
+};
 
 template <int COLS, bool BETA, int EPT = kFoldEPT>
 __global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : 6)
@@ -871,14 +883,19 @@ fold_normalize_kernel(const FoldParams F)
     int e = 0, fill = 0; uint32_t ph = 0;
     const bool live = jj < F.n;                       // (the rest of the EPT too: ldF is a multiple of EPT)
     // next slot's strip from the ring (consumer side of the producer's bulk copies)
+    // the ring's slots are consecutive COLS-int32 rows: this thread's column advances by one row
+    // per slot (a shared-space address, no per-slot index arithmetic) and wraps with the ring
+    const uint32_t ring0 = smem_u32(ring) + (uint32_t)col * 4u;
+    uint32_t addr = ring0;
     auto next = [&](int32_t (&v)[EPT]) {
         if (fill == 0) mbar_wait(&full[e], ph);
-        IntVec<EPT>::get(*reinterpret_cast<const typename IntVec<EPT>::T *>(ring + (e * kFoldPer + fill) * COLS + col), v);
+        IntVec<EPT>::get_shared(addr, v);
+        addr += (uint32_t)COLS * 4u;
         if (++fill == kFoldPer) {
             fill = 0;
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[e]);
-            if (++e == kFoldRing) { e = 0; ph ^= 1; }
+            if (++e == kFoldRing) { e = 0; ph ^= 1; addr = ring0; }
         }
     };
     // diagonals r = sr+1 .. 2 (byte b = sr + 1 - r of the fixed-point number), two at a time:
