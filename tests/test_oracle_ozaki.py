@@ -279,3 +279,75 @@ def test_accumulate_beta0_and_integer_closure():
         for i in range(m):
             for j in range(n):
                 assert to_fraction(getattr(Cn, part), i, j) == -to_fraction(getattr(Cp, part), i, j)
+
+
+# ------------------------------------------------------------------ triangle extent
+def balanced_digits_int(X: int, s: int):
+    """The s balanced radix-256 digits of X (digit set [-128, 127]), top digit first, by
+    repeated division -- Python ints only, independent of oracle.split."""
+    d = []
+    for _ in range(s):
+        r = ((X + 128) % 256) - 128
+        d.append(r)
+        X = (X - r) // 256
+    assert X == 0, "X outside the s-digit range"
+    return d[::-1]
+
+
+def triangle_value(A, B, s, method, extent):
+    """Algorithm 2's product with the triangle alpha + beta <= extent, as a
+    Fraction per output element, written out from Fraction-derived digits:
+        P = sum_k sum_{alpha + beta <= extent} d^A_alpha d^B_beta 256^(s+1-alpha-beta),
+    value P 2^(eA_i + eB_j + 6 - 8(s+1)); Eq. 5 (4M) / Eq. 6 (3M) on the exact values."""
+    m, k = A.shape
+    n = B.shape[1]
+    W = 8 * s - 3
+    eA = [line_exp(A, 0, i) for i in range(m)]
+    eB = [line_exp(B, 1, j) for j in range(n)]
+    def digs(P, i, j, e):
+        xr = fixed_point(to_fraction(P.re, i, j), e, W)
+        xi = fixed_point(to_fraction(P.im, i, j), e, W)
+        return [balanced_digits_int(X, s) for X in (xr, xi, xr + xi)]
+    dA = [[digs(A, i, q, eA[i]) for q in range(k)] for i in range(m)]
+    dB = [[digs(B, q, j, eB[j]) for j in range(n)] for q in range(k)]
+    def P(i, j, pa, pb):
+        tot = 0
+        for q in range(k):
+            x, y = dA[i][q][pa], dB[q][j][pb]
+            for a in range(1, s + 1):
+                for b in range(1, s + 1):
+                    if a + b <= extent:
+                        tot += x[a - 1] * y[b - 1] * 256 ** (s + 1 - a - b)
+        return Fraction(tot) * Fraction(2) ** (eA[i] + eB[j] + 6 - 8 * (s + 1))
+    out = {}
+    for i in range(m):
+        for j in range(n):
+            t1, t2 = P(i, j, 0, 0), P(i, j, 1, 1)
+            if method == "4M":
+                out[i, j] = (t1 - t2, P(i, j, 0, 1) + P(i, j, 1, 0))
+            else:
+                out[i, j] = (t1 - t2, P(i, j, 2, 2) - t1 - t2)
+    return out
+
+
+@pytest.mark.parametrize("method", ["4M", "3M"])
+@pytest.mark.parametrize("s", [2, 3, 5])
+def test_triangle_extent_exact(method, s):
+    """Pins the loop bound beta <= d - alpha + 1 of Algorithm 2 from both
+    sides: with an output width that holds the product exactly, oracle.ozaki equals the
+    triangle alpha + beta <= s + 1 written out above, and differs from both the one-diagonal-
+    shorter (<= s) and one-diagonal-longer (<= s + 2) triangles -- full random mantissas make
+    every digit nonzero, so the alpha + beta = s + 2 and s + 1 pairs contribute."""
+    prec = 128
+    A, B = rand_small(700 + s, 3, 4, 3, prec, 2)
+    wide = 8 * s + 256                                         # exact: |P| < 2^(16 s + 8 + log2 k)
+    C = oracle.ozaki(A, B, wide, method, s)
+    want = triangle_value(A, B, s, method, s + 1)
+    longer = triangle_value(A, B, s, method, s + 2)
+    shorter = triangle_value(A, B, s, method, s)
+    diff_long = diff_short = 0
+    for (i, j), (re, im) in want.items():
+        assert to_fraction(C.re, i, j) == re and to_fraction(C.im, i, j) == im, (i, j)
+        diff_long += (longer[i, j][0] != re) + (longer[i, j][1] != im)
+        diff_short += (shorter[i, j][0] != re) + (shorter[i, j][1] != im)
+    assert diff_long == 2 * len(want) and diff_short == 2 * len(want)
