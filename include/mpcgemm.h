@@ -110,6 +110,12 @@ typedef struct {
     float   ms_linemax, ms_prepass, ms_split, ms_gemm, ms_fold;   /* opts->timing only         */
     int32_t slices_min;       /* smallest per-block s (== slices unless opts->adaptive)        */
     int32_t partial_slots;    /* int32 partial planes per output element read by the fold       */
+    int32_t tile_m, tile_n;   /* output tile of one slice-GEMM work unit (rows x columns)      */
+    int64_t mma_issued;       /* tcgen05.mma instructions (K = 32) counted ON THE DEVICE by the
+                                 issuing thread of every slice-GEMM CTA (pre-pass T GEMM
+                                 excluded); opts->timing only, else -1.  Closed form for a full
+                                 triangle: R P ceil(m/tile_m) ceil(n/tile_n) ceil(k/32),
+                                 R = 3 (3M) / 4 (4M), P = s (s+1) / 2                          */
 } mpcgemm_report;
 
 /* C := A B (auto slice count).  Device pointers.  m, n, k >= 0 (empty: nothing written for
@@ -164,7 +170,9 @@ int mpcgemm_rho_bounds(int64_t m, int64_t n, int64_t k, int32_t prec,
 int mpcgemm_slices_for(int32_t prec, mpcgemm_method method, int64_t k,
                        int64_t minT, int64_t minT1, int64_t maxD2);
 
-/* Device workspace bytes for one call with s slices.  A smaller caller workspace (or less free
+/* Device workspace bytes for one call with s slices (slices <= 0: the s the rule picks at
+ * minT = 1, the largest first-stage s for this prec and k -- an auto-s call whose inputs need
+ * the max-plus stage may pick more and then runs in row groups).  A smaller caller workspace (or less free
  * device memory, or the MPCGEMM_WS_LIMIT environment variable, bytes) makes the call run in row
  * groups of 256 * 2^j rows (B split once; bit-identical result); ERR_NOMEM only when one
  * 256-row group does not fit. */

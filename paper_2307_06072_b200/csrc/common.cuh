@@ -97,6 +97,7 @@ struct GemmParams {
     int32_t pblk;              // p-block length of the CTA-pair kernel's G >= 2 units (0: one block)
     int32_t kk_last;           // K = 32 MMA steps of the last k-block (1..3; 0: all 4): the zero
                                // padding of k up to a multiple of 128 is not multiplied
+    unsigned long long *mma_count;   // or null: tcgen05.mma instructions issued, added at CTA exit
     JobDesc jobs[kMaxJobs];
 };
 

@@ -239,8 +239,8 @@ fold_f64_kernel(const int64_t *__restrict__ partials, int64_t m, int64_t n, int 
                 const int64_t *__restrict__ eA, const int64_t *__restrict__ eB, DMatOut Cre, DMatOut Cim)
 {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t i = blockIdx.y;
     if (j >= n) return;
+    for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
     const int64_t plane = m * n, off = i * n + j;
     uint64_t fix[2][kF64Lmax];
     const int Lc = (int)(((int64_t)b * (s + 1) + 64) / 64 + 1);
@@ -279,6 +279,7 @@ fold_f64_kernel(const int64_t *__restrict__ partials, int64_t m, int64_t n, int 
         const int64_t o = i * outs[p]->ld + j;
         round_store_local(fix[p], Lc, e0, neg, prec, L, outs[p]->sign + o, outs[p]->exp + o, outs[p]->limbs + o * L);
     }
+    }                                                     // rows i (grid-stride over gridDim.y)
 }
 
 cudaError_t fold_f64_launch(const int64_t *partials, int64_t m, int64_t n, int s, int b, int method, int prec, int L,
@@ -286,7 +287,7 @@ cudaError_t fold_f64_launch(const int64_t *partials, int64_t m, int64_t n, int s
 {
     if (m == 0 || n == 0) return cudaSuccess;
     if ((int64_t)b * (s + 1) + 64 > 64 * (kF64Lmax - 2)) return cudaErrorInvalidValue;
-    dim3 grid((unsigned)((n + 127) / 128), (unsigned)m);
+    dim3 grid((unsigned)((n + 127) / 128), (unsigned)(m < 65535 ? m : 65535));
     fold_f64_kernel<<<grid, 128, 0, st>>>(partials, m, n, s, b, method, prec, L, eA, eB, Cre, Cim);
     return cudaGetLastError();
 }

@@ -58,6 +58,7 @@ struct DevCache {
     cudaStream_t copy_stream = nullptr;              // mpcgemm_host: D2H of finished row groups
     cudaEvent_t group_event = nullptr;
     cudaEvent_t done = nullptr;                      // completion of the last call's device work
+    unsigned long long *mma_dev = nullptr;           // device MMA counter (opts->timing calls)
 };
 
 // The cached workspace / scratch of a device is shared by every call, whatever its stream:
@@ -196,7 +197,7 @@ bool g2_enabled() { return env_int("MPCGEMM_G2", 1) != 0; }
 
 // Builds the unit list (segments x chunks x output tiles), each unit with its own partial
 // planes, and the slot table (job, r) -> (first plane, chunk count) used by the fold.
-int build_plan(int dev, const PlanKey &key, Plan **out) {
+int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
     auto it = g_plans.find({dev, key});
     if (it != g_plans.end()) { *out = &it->second; return 0; }
     if (g_plans.size() >= 512) {                       // bound the cache (many shapes, e.g. LU updates)
@@ -293,9 +294,12 @@ int build_plan(int dev, const PlanKey &key, Plan **out) {
             cudaMalloc(&P.d_counter, sizeof(int32_t) * (1 + (size_t)nslots)) != cudaSuccess ||
             cudaMalloc(&P.d_slotinfo, sizeof(int32_t) * slotinfo.size()) != cudaSuccess)
             return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc plan");
-        CK(cudaMemcpy(P.d_units, flat.data(), sizeof(WorkUnit) * flat.size(), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(P.d_slotinfo, slotinfo.data(), sizeof(int32_t) * slotinfo.size(), cudaMemcpyHostToDevice));
-        CK(cudaMemset(P.d_counter, 0, sizeof(int32_t) * (1 + (size_t)nslots)));   // counter + k-phase hints
+        // uploads ordered on the call's stream (a later call on another stream is ordered after
+        // this one by StreamOrder); a pageable-source cudaMemcpyAsync has staged the host data
+        // by the time it returns, so the host vectors may go
+        CK(cudaMemcpyAsync(P.d_units, flat.data(), sizeof(WorkUnit) * flat.size(), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(P.d_slotinfo, slotinfo.data(), sizeof(int32_t) * slotinfo.size(), cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(P.d_counter, 0, sizeof(int32_t) * (1 + (size_t)nslots), st));   // counter + k-phase hints
     }
     auto res = g_plans.emplace(std::make_pair(dev, key), P);
     *out = &res.first->second;
@@ -475,7 +479,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     const int grid = sm_count(dev);
     PlanKey key{m, n, k, 1, 0, 128, BN, grid, simt, (int)kMaxKBlocksPerChunk, 0, 0, {}};
     Plan *plan;
-    if (int rc = build_plan(dev, key, &plan)) return rc;
+    if (int rc = build_plan(dev, key, &plan, st)) return rc;
     SliceGemmLaunch SL;
     memset(&SL, 0, sizeof(SL));
     SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
@@ -588,8 +592,8 @@ int run_main_f64(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const m
         if (cudaMalloc(&F.d_units, sizeof(int4) * units.size()) != cudaSuccess ||
             cudaMalloc(&F.d_jobs, sizeof(JobDesc) * kMaxJobs) != cudaSuccess)
             return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc f64 plan");
-        CK(cudaMemcpy(F.d_units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(F.d_jobs, P.jobs, sizeof(JobDesc) * kMaxJobs, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(F.d_units, units.data(), sizeof(int4) * units.size(), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(F.d_jobs, P.jobs, sizeof(JobDesc) * kMaxJobs, cudaMemcpyHostToDevice, st));
         it = g_f64plans.emplace(key, F).first;
     }
     CK(dmma_slicegemm_launch(digA, digB, m, n, kp, s, it->second.d_units, it->second.nunits, it->second.d_jobs,
@@ -631,7 +635,8 @@ using GroupHook = std::function<int(int64_t, int64_t)>;
 int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
              mpc_cmat *C, int method, int s, cudaStream_t st, uint8_t *meta, uint8_t *big, const Layout &Lo,
              int simt, mpcgemm_report *rep, StageEvents *E, int beta, int alpha_neg,
-             const std::vector<int32_t> &sblk, int64_t group_rows = 0, const GroupHook *hook = nullptr) {
+             const std::vector<int32_t> &sblk, int64_t group_rows = 0, const GroupHook *hook = nullptr,
+             unsigned long long *mma_dev = nullptr) {
     const int L = (prec + 63) / 64;
     const MetaView mv = meta_view(meta, m, n);
     int64_t *eA = mv.eA, *eB = mv.eB;
@@ -657,7 +662,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         PlanKey key{mr, n, k, s, method, geo.BM, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0,
                     env_int("MPCGEMM_ORDER", 1), sb};
         Plan *plan;
-        if (int rc = build_plan(dev, key, &plan)) return rc;
+        if (int rc = build_plan(dev, key, &plan, st)) return rc;
         SliceGemmLaunch SL;
         memset(&SL, 0, sizeof(SL));
         SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
@@ -668,6 +673,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         SL.P.dbg = env_int("MPCGEMM_DBG", 0);
         SL.P.hot = env_int("MPCGEMM_KPHASE", 1) ? plan->d_counter + 1 : nullptr;
         SL.P.pblk = env_int("MPCGEMM_PBLK", 32);
+        SL.P.mma_count = mma_dev;
         for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
         SL.digA = digA; SL.digB = digB; SL.rowsA = mr; SL.rowsB = n; SL.kp = Lo.kp;
         SL.grid = plan->grid; SL.BM = geo.BM; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits;
@@ -690,6 +696,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
             rep->mma_instructions += plan->mma; rep->work_units += plan->nunits;
             rep->partial_slots = (int32_t)plan->nslots;
             rep->slicegemm_ctas = simt ? plan->nunits : plan->grid;
+            rep->tile_m = geo.BM; rep->tile_n = BN;
         }
         if (hook) if (int rc = (*hook)(r0, r0 + mr)) return rc;
     }
@@ -719,7 +726,7 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     if (carrier == 1 && (beta || alpha_neg)) return fail(MPCGEMM_ERR_ARG, "beta / alpha_neg need the INT8 carrier");
     const int bits = carrier == 1 ? fp64_slice_bits(k) : 8;
     if (forced < 0 || forced > kMaxSlices) return fail(MPCGEMM_ERR_SLICES, "forced slices outside [1, 1024]");
-    if (rep) { memset(rep, 0, sizeof(*rep)); rep->minT = rep->minT1 = rep->maxD2 = -1; }
+    if (rep) { memset(rep, 0, sizeof(*rep)); rep->minT = rep->minT1 = rep->maxD2 = -1; rep->mma_issued = -1; }
     const int L = (prec + 63) / 64;
     if (m == 0 || n == 0) return 0;
     if (k == 0) {                                      // A B = 0: C := beta C
@@ -842,8 +849,14 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     }
     if (E) CK(cudaEventRecord(E->ev[2], st));
     if (rep) rep->kernel_launches = launches;
+    unsigned long long *mma_dev = nullptr;             // device-side MMA count (timed calls)
+    if (E && rep) {
+        if (!dc.mma_dev) CK(cudaMalloc(&dc.mma_dev, sizeof(unsigned long long)));
+        mma_dev = dc.mma_dev;
+        CK(cudaMemsetAsync(mma_dev, 0, sizeof(unsigned long long), st));
+    }
     if (int rc = run_main(dev, m, n, k, prec, A, B, C, method, s, st, meta, big, Lm, simt, rep, E, beta, alpha_neg,
-                          sblk, group_rows, hook))
+                          sblk, group_rows, hook, mma_dev))
         return rc;
     if (rep) {
         rep->slices = s; rep->slice_bits = 8; rep->certified = 1; rep->minT = pb[0]; rep->minT1 = pb[1];
@@ -855,6 +868,11 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         float t[5];
         for (int q = 0; q < 5; q++) CK(cudaEventElapsedTime(&t[q], E->ev[q], E->ev[q + 1]));
         if (rep) { rep->ms_linemax = t[0]; rep->ms_prepass = t[1]; rep->ms_split = t[2]; rep->ms_gemm = t[3]; rep->ms_fold = t[4]; }
+        if (rep && mma_dev && !simt) {
+            unsigned long long h = 0;
+            if (int rc = readback(dev, &h, mma_dev, sizeof(h), st)) return rc;
+            rep->mma_issued = (int64_t)h;
+        }
     }
     return 0;
 }
@@ -1022,9 +1040,12 @@ int mpcgemm_slices_for(int32_t prec, mpcgemm_method method, int64_t k, int64_t m
 }
 
 size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec, mpcgemm_method method, int32_t slices) {
-    (void)prec;
     int dev = 0;
     cudaGetDevice(&dev);
+    if (slices <= 0) {                                 // auto: the s of the rule at minT = 1, the
+        slices = rule_slices(prec, (int)method, rule_log2rho(std::max<int64_t>(k, 1), 1, 1, -1));   // largest
+        if (slices < 0) slices = kMaxSlices;           // first-stage s (max-plus inputs may need more)
+    }
     Layout Lo = layout_for(m, n, k, slices, (int)method, main_geometry(dev, m, n, k, slices, (int)method).maxkb, prec, true);
     return std::max(Lo.main, Lo.pre);
 }
@@ -1198,6 +1219,7 @@ void mpcgemm_release(void) {
         cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage[0]); cudaFree(it->second.stage[1]);
         cudaFree(it->second.lu);
         cudaFree(it->second.solve);
+        cudaFree(it->second.mma_dev);
         if (it->second.rb) cudaFreeHost(it->second.rb);
         g_cache.erase(it);
     }

@@ -30,7 +30,8 @@ constexpr int kBM = 128;
 // predicate there cost ~6 % of the tensor pipe's issue rate), guarded for the last, partial one.
 // acc0: enable-input of the first MMA (0 overwrites the accumulator).
 template <bool PAIR>
-MPC_DEV void issue_kblock(uint32_t d, uint32_t a, uint32_t b, uint32_t idesc, uint32_t acc0, int n) {
+MPC_DEV void issue_kblock(uint32_t d, uint32_t a, uint32_t b, uint32_t idesc, uint32_t acc0, int n, uint64_t &cnt) {
+    cnt += (uint64_t)n;
     if (n == kBK / 32) {
 #pragma unroll
         for (int kk = 0; kk < kBK / 32; kk++) {
@@ -154,12 +155,13 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             int stage = 0; uint32_t phase = 0;
             uint32_t tphase = 0;
             int qs = 0; uint32_t qph = 0;
+            uint64_t nmma = 0;                                // MMA instructions issued (P.mma_count)
             for (;;) {
                 mbar_wait(&qfull[qs], qph);
                 const int u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
                 mbar_arrive(&qempty[qs]);
                 if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
-                if (u < 0) break;
+                if (u < 0) { if (P.mma_count) atomicAdd(P.mma_count, (unsigned long long)nmma); break; }
                 const WorkUnit w = P.units[u];
                 const JobDesc &J = P.jobs[unit_job(w)];
                 mbar_wait(tempty, tphase ^ 1);
@@ -175,10 +177,10 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                                 const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
                                 const bool first = (pr == 0 && i == 0);
                                 const int nkk = (unit_kb(w, i) == KB - 1 && P.kk_last) ? P.kk_last : kBK / 32;
-                                issue_kblock<false>(d1, a0, b0, idesc, (first && p == 1) ? 0u : 1u, nkk);   // D_{r+1} += A_p B_{r+1-p}
+                                issue_kblock<false>(d1, a0, b0, idesc, (first && p == 1) ? 0u : 1u, nkk, nmma);   // D_{r+1} += A_p B_{r+1-p}
                                 if (p >= 2) {                           // D_r += A_{p-1} B_{r+1-p}
                                     issue_kblock<false>(d0, smem_u32(sA + prev * Cfg::A_BYTES), b0, idesc,
-                                                        (first && p == 2) ? 0u : 1u, nkk);
+                                                        (first && p == 2) ? 0u : 1u, nkk, nmma);
                                     mma_commit(&empty[prev]);           // A_{p-1} no longer needed
                                 }
                                 if (p == w.r) mma_commit(&empty[stage]);   // A_r pairs only with B_1
@@ -192,7 +194,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                        issue_kblock<false>(d0, a0, b0, idesc, g > 0 ? 1u : 0u, skk[stage]);
+                        issue_kblock<false>(d0, a0, b0, idesc, g > 0 ? 1u : 0u, skk[stage], nmma);
                         mma_commit(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -404,13 +406,14 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             int stage = 0; uint32_t phase = 0;
             uint32_t tphase = 0;
             int qs = 0; uint32_t qph = 0;
+            uint64_t nmma = 0;                                // MMA instructions issued (P.mma_count)
             for (;;) {
                 mbar_wait_cluster(&qfull[qs], qph);
                 const int u = *reinterpret_cast<volatile int32_t *>(&uq[qs]);
                 const int rot = *reinterpret_cast<volatile int32_t *>(&uqr[qs]);
                 mbar_arrive(&qempty[qs]);
                 if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
-                if (u < 0) break;
+                if (u < 0) { if (P.mma_count) atomicAdd(P.mma_count, (unsigned long long)nmma); break; }
                 const WorkUnit w = P.units[u];
                 const JobDesc &J = P.jobs[unit_job(w)];
                 mbar_wait_cluster(tempty, tphase ^ 1);
@@ -438,10 +441,10 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                             tc_fence_after();
                             const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                             const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                            issue_kblock<true>(d1, a0, b0, idesc, acc1, nkk);   // D_{r+1} += A_p B_{r+1-p}
+                            issue_kblock<true>(d1, a0, b0, idesc, acc1, nkk, nmma);   // D_{r+1} += A_p B_{r+1-p}
                             acc1 = 1u;
                             if (prev >= 0) {                            // D_r += A_{p-1} B_{r+1-p}
-                                issue_kblock<true>(d0, smem_u32(sA + prev * Cfg::A_BYTES), b0, idesc, acc0, nkk);
+                                issue_kblock<true>(d0, smem_u32(sA + prev * Cfg::A_BYTES), b0, idesc, acc0, nkk, nmma);
                                 acc0 = 1u;
                                 mma_commit_2sm(&empty[prev]);
                             }
@@ -458,7 +461,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
-                        issue_kblock<true>(d0, a0, b0, idesc, g > 0 ? 1u : 0u, skk[stage]);
+                        issue_kblock<true>(d0, a0, b0, idesc, g > 0 ? 1u : 0u, skk[stage], nmma);
                         mma_commit_2sm(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }

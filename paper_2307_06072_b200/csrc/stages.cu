@@ -1058,16 +1058,17 @@ size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta) {
 
 __global__ void zero_output_kernel(DMatOut C, int64_t m, int64_t n, int L) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t i = blockIdx.y;
     if (j >= n) return;
-    const int64_t o = i * C.ld + j;
-    C.sign[o] = 0; C.exp[o] = 0;
-    for (int l = 0; l < L; l++) C.limbs[o * L + l] = 0;
+    for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
+        const int64_t o = i * C.ld + j;
+        C.sign[o] = 0; C.exp[o] = 0;
+        for (int l = 0; l < L; l++) C.limbs[o * L + l] = 0;
+    }
 }
 
 cudaError_t zero_output_launch(DMatOut C, int64_t m, int64_t n, int L, cudaStream_t st) {
     if (m == 0 || n == 0) return cudaSuccess;
-    dim3 grid((unsigned)((n + 127) / 128), (unsigned)m);
+    dim3 grid((unsigned)((n + 127) / 128), (unsigned)(m < 65535 ? m : 65535));
     zero_output_kernel<<<grid, 128, 0, st>>>(C, m, n, L);
     return cudaGetLastError();
 }

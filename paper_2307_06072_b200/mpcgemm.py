@@ -55,7 +55,8 @@ class ReportC(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int32), ("slice_bits", ctypes.c_int32), ("slicegemm_ctas", ctypes.c_int32),
                 ("ms_linemax", ctypes.c_float), ("ms_prepass", ctypes.c_float), ("ms_split", ctypes.c_float),
                 ("ms_gemm", ctypes.c_float), ("ms_fold", ctypes.c_float), ("slices_min", ctypes.c_int32),
-                ("partial_slots", ctypes.c_int32)]
+                ("partial_slots", ctypes.c_int32), ("tile_m", ctypes.c_int32), ("tile_n", ctypes.c_int32),
+                ("mma_issued", ctypes.c_int64)]
 
 
 class LuReportC(ctypes.Structure):
