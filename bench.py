@@ -3,14 +3,17 @@
 A step is one whole hot path (exponent scan, rho-hat pre-pass
 and slice rule, split, tcgen05 slice GEMMs, fold + normalize) over one batch of synthetic
 input: BASELINE config 4, complex 2048^3 at prec 1024 (the configuration the metric is
-quoted on at 1/2/4/8 GPUs), method 3M by default.  Multi-GPU (torchrun): every rank owns a
-2048-row block of a global A (weak scaling), B is replicated, s is agreed by an all-reduce of
-the pre-pass integers (paper_2307_06072_b200/dist.py); no data-path collective.
+quoted on at 1/2/4/8 GPUs), method 3M by default.  Multi-GPU (torchrun): STRONG scaling of the
+same 2048^3 product -- rank r owns rows row_range(2048, r, N) of A (pre-sharded), B lives on
+rank 0 and is broadcast by NCCL inside every step, s is agreed by an all-reduce of the pre-pass
+integers, and the C row blocks are all-gathered by NCCL inside every step
+(paper_2307_06072_b200/dist.py StrongGemm: broadcast / gather of neighbouring steps pipelined on
+a communication stream).  A weak-scaling run (2048 rows per rank) is an extra key.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--method 3M|4M] [--impl ours|reference]
 
-Prints ONE JSON line (rank 0).  value = total CMACs of all ranks / max-over-ranks device
-time of the K timed steps (CUDA events on the launching stream, barrier + synchronize on
+Prints ONE JSON line (rank 0).  value = the product's CMACs (m n k) / max-over-ranks device
+time per step of the K timed steps (CUDA events on the launching stream, barrier + synchronize on
 both sides).  Inputs are larger than L2 (2.3 GB per rank), so no flush is needed.
 """
 import argparse
@@ -132,7 +135,7 @@ def run_reference(args):
     value = args.steps * per_step * c["k"] / tot
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/u64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8/i32/u64",
             "data": "synthetic", "config": workload_config(args, s),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{per_step} sampled output elements per step (x k={c['k']} CMACs), Algorithm-2 oracle"},
@@ -162,11 +165,55 @@ def hbm_kernels(args, reps, m, n, k, prec, s, pk, src):
     return out
 
 
-def workload_config(args, s):
+def workload_config(args, s, world=1):
     c = mpgen.CONFIGS[args.config]
-    return {"workload": f"BASELINE config {args.config}: " + c["desc"], "method": args.method, "m_per_rank": c["m"],
+    rows = [r1 - r0 for r0, r1 in (row_range_(c["m"], r, world) for r in range(world))]
+    return {"workload": f"BASELINE config {args.config}: " + c["desc"], "method": args.method, "m": c["m"],
             "n": c["n"], "k": c["k"], "prec": c["prec"], "slices": s, "seed": 0,
-            "l2": "inputs larger than L2 (no flush needed)", "parallelism": f"rows x{args.gpus} (weak)"}
+            "l2": "inputs larger than L2 (no flush needed)",
+            "parallelism": (f"rows x{world} (strong: A pre-sharded, rows per rank {min(rows)}-{max(rows)}; B broadcast and "
+                            "C all-gathered by NCCL inside every step, pipelined on a communication stream)")
+            if world > 1 else "1 GPU"}
+
+
+def row_range_(m, rank, world):
+    base, rem = divmod(m, world)
+    r0 = rank * base + min(rank, rem)
+    return r0, r0 + base + (1 if rank < rem else 0)
+
+
+def inrun_ceilings():
+    """INT8 tensor ceilings measured in this run (after the timed region): back-to-back tcgen05.mma
+    kind::i8 on rotating random SMEM operands, 148 SMs (tools/mma_power, built by build()), and
+    cuBLASLt INT8 (torch._int_mm 8192^3, best of 10)."""
+    import torch
+    out = {}
+    exe = os.path.join(ROOT, "tools", "mma_power")
+    if os.path.exists(exe):
+        try:
+            r = subprocess.run([exe, "10000000"], capture_output=True, text=True, timeout=120)
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            out["tcgen05_mma_random_operands"] = {"tops": d["int8_tops"], "sm_ghz": d["avg_sm_ghz"],
+                                                  "seconds": d["seconds"]}
+        except Exception as e:  # noqa: BLE001
+            out["tcgen05_mma_random_operands"] = {"error": str(e)[:200]}
+    try:
+        N = 8192
+        a = torch.randint(-128, 127, (N, N), dtype=torch.int8, device="cuda")
+        b = torch.randint(-128, 127, (N, N), dtype=torch.int8, device="cuda").t().contiguous().t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); torch._int_mm(a, b); e1.record(); torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        out["cublaslt_int8_burst"] = {"tops": round(2.0 * N ** 3 / best / 1e12, 1)}
+        del a, b
+    except Exception as e:  # noqa: BLE001
+        out["cublaslt_int8_burst"] = {"error": str(e)[:200]}
+    return out
 
 
 def main():
@@ -179,6 +226,7 @@ def main():
     ap.add_argument("--method", default="3M", choices=["3M", "4M"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the 4M sub-record, in-run ceilings, weak run")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -198,87 +246,179 @@ def main():
     dev = torch.device("cuda", local)
     c = mpgen.CONFIGS[args.config]
     m, n, k, prec = c["m"], c["n"], c["k"], c["prec"]
-    # weak scaling: rank r owns rows [r m, (r+1) m) of a global (world m) x k matrix A
-    A, B = mpgen.config_inputs(args.config, seed=0, row0=rank * m, rows=m)
-    dA, dB = P.to_device(A, dev), P.to_device(B, dev)
-    dC = P.empty_device(m, n, prec, dev)
     stream = torch.cuda.current_stream(dev)
-
-    def step(timing=0):
-        if world > 1:
-            s, _ = pdist.common_slices(lambda full: P.mpcgemm_rho_bounds(dA, dB, prec, full, stream=stream),
-                                       P.mpcgemm_slices_for, prec, args.method, k, device=dev)
-            return P.mpcgemm_ex(dA, dB, dC, prec, args.method, slices=s, stream=stream, timing=timing)
-        return P.mpcgemm_ex(dA, dB, dC, prec, args.method, stream=stream, timing=timing)
-
-    for _ in range(args.warmup):
-        rep = step()
-    torch.cuda.synchronize()
+    extra = {}
     clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    if world > 1:
+
+    if world == 1:
+        A, B = mpgen.config_inputs(args.config, seed=0)
+        dA, dB = P.to_device(A, dev), P.to_device(B, dev)
+        dC = P.empty_device(m, n, prec, dev)
+
+        def step(timing=0, method=args.method):
+            return P.mpcgemm_ex(dA, dB, dC, prec, method, stream=stream, timing=timing)
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        clocks.start()
+        time.sleep(0.3)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = []
+        e0.record(stream)
+        for _ in range(args.steps):
+            reps.append(step(timing=1))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        clk = clocks.stop()
+        s = reps[-1]["slices"]
+        launches = int(sum(r["kernel_launches"] for r in reps))
+    else:
+        # strong scaling: rank r owns rows row_range(m, r, N) of the one global A (pre-sharded, from
+        # the same seeded generator); B lives on rank 0 and is broadcast inside every step
+        r0, r1 = pdist.row_range(m, rank, world)
+        A, B = mpgen.config_inputs(args.config, seed=0, row0=r0, rows=r1 - r0)
+        dA = P.to_device(A, dev)
+        Bsrc = None
+        if rank == 0:
+            Bsrc = pdist.packed_cmat(k, n, prec, dev)
+            pdist.copy_cmat(Bsrc[0], P.to_device(B, dev))
+        reps_all = []
+
+        def compute(Al, Bd, Cv, s_, timing=[1]):
+            return P.mpcgemm_ex(Al, Bd, Cv, prec, args.method, slices=s_, timing=timing[0])
+
+        SG = pdist.StrongGemm(m, n, k, prec, args.method, dev,
+                              lambda Al, Bd, full: P.mpcgemm_rho_bounds(Al, Bd, prec, full),
+                              P.mpcgemm_slices_for, compute)
+        SG.run(dA, Bsrc, args.warmup)
+        SG.finish()
+        clocks.start()
+        time.sleep(0.3)
         dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = []
-    e0.record(stream)
-    for _ in range(args.steps):
-        reps.append(step(timing=1))
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        reps = SG.run(dA, Bsrc, args.steps)
+        # the last step's gather is inside the timed region: the compute stream waits for it
+        stream.wait_stream(SG.comm)
+        e1.record(stream)
+        torch.cuda.synchronize()
         dist.barrier()
-    ms_local = e0.elapsed_time(e1) / args.steps
-    clk = clocks.stop()
-    ms = ms_local
-    if world > 1:
+        ms_local = e0.elapsed_time(e1) / args.steps
+        clk = clocks.stop()
+        parts = SG.finish()
         t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    s = reps[-1]["slices"]
-    cmacs = world * m * n * k
+        s = reps[-1]["slices"]
+        launches = int(sum(r["kernel_launches"] for r in reps))
+        extra["strong"] = {"compute_ms_per_step": round(parts["compute_ms"] / args.steps, 3),
+                           "bcast_ms_per_step": round(parts["bcast_ms"] / args.steps, 3),
+                           "gather_ms_per_step": round(parts["gather_ms"] / args.steps, 3),
+                           "rows_this_rank0": r1 - r0,
+                           "note": "per-stream device times (CUDA events); B broadcast / C all-gather of "
+                                   "neighbouring steps overlap compute, so they do not add up to ms_per_step"}
+    cmacs = m * n * k                                   # the whole product, all ranks together
     value = cmacs / (ms / 1e3)
 
     # roofline of the dominant kernel (the tcgen05 slice GEMM), timed live with CUDA events
     # on the launching stream inside the library (opts.timing) over the timed steps
     R = 3 if args.method == "3M" else 4
     pairs = s * (s + 1) // 2
-    ops = 2.0 * R * pairs * m * n * k                   # algorithmic INT8 ops per launch
-    gemm_ms = statistics.mean(r["ms_gemm"] for r in reps)
     pk, src = peaks()
     peak_int8 = 2.0 * pk["bf16_tflops_sustained"]       # measured bf16 sustained x nominal int8/bf16 = 2
-    achieved = ops / (gemm_ms / 1e3) / 1e12
-    stage_ms = {f: round(statistics.mean(r[f] for r in reps), 3) for f in
-                ("ms_linemax", "ms_prepass", "ms_split", "ms_gemm", "ms_fold")}
-    traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
-        if tr["config"] == args.config and tr["method"] == args.method and tr["slices"] == s:
-            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
-    except Exception:
-        traffic = None
+    stage_ms = {}
+    roof = None
+    if world == 1 or all("ms_gemm" in r for r in reps):
+        ops = 2.0 * R * pairs * A.shape[0] * n * k      # algorithmic INT8 ops per launch (this rank's rows)
+        gemm_ms = statistics.mean(r["ms_gemm"] for r in reps) if reps[-1].get("ms_gemm", 0) > 0 else None
+        if gemm_ms:
+            achieved = ops / (gemm_ms / 1e3) / 1e12
+            stage_ms = {f: round(statistics.mean(r[f] for r in reps), 3) for f in
+                        ("ms_linemax", "ms_prepass", "ms_split", "ms_gemm", "ms_fold")}
+            traffic = None
+            try:
+                tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+                if tr["config"] == args.config and tr["method"] == args.method and tr["slices"] == s and world == 1:
+                    traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+            except Exception:
+                traffic = None
+            roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak_int8, 1), "unit": "TOP/s",
+                    "frac": round(achieved / peak_int8, 4), "frac_vs_nominal_4500": round(achieved / 4500.0, 4),
+                    "traffic": traffic,
+                    "traffic_note": "ncu dram__bytes_read+write per launch (profiles/roofline_traffic.json); "
+                                    "the kernel is tensor-bound, its algorithmic operand bytes are the digit planes",
+                    "kernel": "slicegemm_tc2_kernel (tcgen05.mma.cta_group::2 kind::i8)",
+                    "peak_source": f"{src}: 2 x bf16_tflops_sustained (nominal int8/bf16 = 2)",
+                    "algorithmic": f"2 R P m n k = 2*{R}*{pairs}*{A.shape[0]}*{n}*{k} int8 ops per launch",
+                    "mma_instructions_per_launch": reps[-1].get("mma_issued")}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32/u64",
-        "data": "synthetic", "config": workload_config(args, s),
-        "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak_int8, 1), "unit": "TOP/s",
-                     "frac": round(achieved / peak_int8, 4), "frac_vs_nominal_4500": round(achieved / 4500.0, 4),
-                     "traffic": traffic,
-                     "traffic_note": "ncu dram__bytes_read+write per launch (profiles/roofline_traffic.json); "
-                                     "the kernel is tensor-bound, its algorithmic operand bytes are the digit planes",
-                     "kernel": "slicegemm_tc2_kernel (tcgen05.mma.cta_group::2 kind::i8)",
-                     "ceilings_tops": {"pure_mma_random_operands_sustained": 3704, "cublaslt_int8_sustained": 2412,
-                                       "cublaslt_int8_burst": 3081, "nominal": 4500},
-                     "peak_source": f"{src}: 2 x bf16_tflops_sustained (nominal int8/bf16 = 2)",
-                     "algorithmic": f"2 R P m n k = 2*{R}*{pairs}*{m}*{n}*{k} int8 ops per launch"},
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8/i32/u64",
+        "data": "synthetic", "config": workload_config(args, s, world),
+        "roofline": roof,
         "stages_ms": stage_ms,
-        "hbm_kernels": hbm_kernels(args, reps, m, n, k, prec, s, pk, src),
-        "gpu_launches": int(sum(r["kernel_launches"] for r in reps)),
+        "gpu_launches": launches,
         "clocks": clk,
     }
+    if world == 1 and stage_ms:
+        line["hbm_kernels"] = hbm_kernels(args, reps, m, n, k, prec, s, pk, src)
+    line.update(extra)
+    if world == 1 and not args.no_extra:
+        # the other method on the same workload (3M is 24-26 % faster than 4M)
+        other = "4M" if args.method == "3M" else "3M"
+        for _ in range(2):
+            step(method=other)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r2 = []
+        e0.record(stream)
+        for _ in range(max(2, min(args.steps, 4))):
+            r2.append(step(timing=1, method=other))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms2 = e0.elapsed_time(e1) / len(r2)
+        line[f"method_{other}"] = {"value": cmacs / (ms2 / 1e3), "unit": UNIT, "ms_per_step": ms2,
+                                   "ms_gemm": round(statistics.mean(r["ms_gemm"] for r in r2), 3),
+                                   "steps": len(r2), "slices": r2[-1]["slices"],
+                                   "time_ratio_3M_over_4M": round((ms if args.method == "3M" else ms2) /
+                                                                  (ms2 if args.method == "3M" else ms), 4)}
+        if roof:
+            ceil = inrun_ceilings()
+            roof["ceilings_in_run"] = ceil
+            mm = ceil.get("tcgen05_mma_random_operands", {}).get("tops")
+            if mm:
+                roof["frac_vs_in_run_mma_ceiling"] = round(roof["achieved"] / mm, 4)
+    if world > 1 and not args.no_extra:
+        # weak scaling (extra key): every rank its own 2048-row block of a (N x 2048)-row A, B local
+        Aw, Bw = mpgen.config_inputs(args.config, seed=0, row0=rank * m, rows=m)
+        dAw, dBw = P.to_device(Aw, dev), P.to_device(Bw, dev)
+        dCw = P.empty_device(m, n, prec, dev)
+
+        def wstep():
+            s_, _ = pdist.common_slices(lambda full: P.mpcgemm_rho_bounds(dAw, dBw, prec, full, stream=stream),
+                                        P.mpcgemm_slices_for, prec, args.method, k, device=dev)
+            return P.mpcgemm_ex(dAw, dBw, dCw, prec, args.method, slices=s_, stream=stream)
+        wstep()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            wstep()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        line["weak"] = {"value": world * m * n * k / (float(t.item()) / 1e3), "unit": UNIT,
+                        "ms_per_step": float(t.item()), "rows_per_rank": m, "scaling": "weak"}
+        del dAw, dBw, dCw
     if not args.no_e2e:
-        e2e = e2e_measure(P, A, B, prec, args, world, dev)       # every rank; max over ranks
+        e2e = e2e_measure(P, A, B, prec, args, world, dev,
+                          strong=(SG, dA, Bsrc) if world > 1 else None)   # every rank; max over ranks
         if rank == 0:
             line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -290,10 +430,14 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_measure(P, A, B, prec, args, world=1, dev=None):
-    """Same metric through the C ABI on HOST buffers (pinned), H2D + D2H inside the timed call.
-    Each rank times its own rows (wall clock around the blocking call); value = all ranks'
-    CMACs / the max over ranks of the median time."""
+def e2e_measure(P, A, B, prec, args, world=1, dev=None, strong=None):
+    """Same metric through the public API on HOST buffers (pinned), every step's H2D of its inputs
+    and D2H of its result inside the timed region.
+      N = 1: the C ABI's queued host entry (mpcgemm_host_async x K + mpcgemm_host_wait; step i+1's
+             H2D overlaps step i's compute), plus one blocking mpcgemm_host call;
+      N > 1: per step, H2D of this rank's A rows (and of B on rank 0), the strong-scaling product
+             (B broadcast, common s, this rank's rows, C all-gather) and the D2H of the gathered C
+             on rank 0; wall clock, max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -307,78 +451,83 @@ def e2e_measure(P, A, B, prec, args, world=1, dev=None):
             out.append(v)
         return mpgen.RMat(out[0], out[1], out[2], R.prec)
 
-    hA = mpgen.CMat(pinned(A.re), pinned(A.im))
-    hB = mpgen.CMat(pinned(B.re), pinned(B.im))
+    ent = lambda R: R.sign.nbytes + R.exp.nbytes + R.limbs.nbytes
     m, k = A.shape
     n = B.shape[1]
-    hC = mpgen.CMat(pinned(mpgen.empty_rmat(m, n, prec)), pinned(mpgen.empty_rmat(m, n, prec)))
-    if world == 1:
-        def run():
-            P.mpcgemm_host(hA, hB, prec, args.method, C=hC)
-    else:
-        # N > 1: the Python public API -- pinned host -> device copies, dist protocol (pre-pass
-        # all-reduce + mpcgemm_ex on this rank's rows), device -> pinned host copy of C
-        from paper_2307_06072_b200 import dist as pdist
-        dA, dB = P.to_device(A, dev), P.to_device(B, dev)
-        dC = P.empty_device(m, n, prec, dev)
-        srcs = [(getattr(dX, p_), getattr(hX, p_)) for dX, hX in ((dA, hA), (dB, hB)) for p_ in ("re", "im")]
+    if world > 1:
+        SG, dA, Bsrc = strong
+        rank = dist.get_rank()
+        hA = mpgen.CMat(pinned(A.re), pinned(A.im))
+        hB = mpgen.CMat(pinned(B.re), pinned(B.im)) if rank == 0 else None
+        mfull = SG.m
+        L = (prec + 63) // 64
+        hC = torch.empty(SG.Cfull[0].numel(), dtype=torch.uint8, pin_memory=True) if rank == 0 else None
+
+        def h2d(dX, hX):
+            for p_ in ("re", "im"):
+                dR, hR = getattr(dX, p_), getattr(hX, p_)
+                dR.sign.copy_(torch.from_numpy(hR.sign), non_blocking=True)
+                dR.exp.copy_(torch.from_numpy(hR.exp), non_blocking=True)
+                dR.limbs.copy_(torch.from_numpy(hR.limbs.view(np.int64)), non_blocking=True)
 
         def run():
-            for dR, hR in srcs:
-                for f in ("sign", "exp"):
-                    getattr(dR, f).copy_(torch.from_numpy(getattr(hR, f)), non_blocking=True)
-                dR.limbs.copy_(torch.from_numpy(hR.limbs.view(np.int64)), non_blocking=True)
-            kk = B.shape[0]
-            s_, _ = pdist.common_slices(lambda full: P.mpcgemm_rho_bounds(dA, dB, prec, full), P.mpcgemm_slices_for,
-                                        prec, args.method, kk, device=dev)
-            P.mpcgemm_ex(dA, dB, dC, prec, args.method, slices=s_)
-            for dR, hR in ((dC.re, hC.re), (dC.im, hC.im)):
-                torch.from_numpy(hR.sign).copy_(dR.sign, non_blocking=True)
-                torch.from_numpy(hR.exp).copy_(dR.exp, non_blocking=True)
-                torch.from_numpy(hR.limbs.view(np.int64)).copy_(dR.limbs, non_blocking=True)
+            h2d(dA, hA)
+            if rank == 0:
+                h2d(Bsrc[0], hB)
+            SG.run(dA, Bsrc, 1)
+            if rank == 0:
+                torch.cuda.current_stream().wait_stream(SG.comm)
+                hC.copy_(SG.Cfull[0], non_blocking=True)
             torch.cuda.synchronize()
-    run()                                                        # warm-up (staging allocation)
+        run()
+        ts = []
+        for _ in range(max(2, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            run()
+            ts.append(time.perf_counter() - t0)
+        SG.finish()
+        tt = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+        return {"value": mfull * n * k / t, "unit": UNIT,
+                "h2d_bytes_per_step": (ent(A.re) + ent(A.im)) * world + ent(B.re) + ent(B.im),
+                "d2h_bytes_per_step": 2 * mfull * n * (9 + 8 * L), "ms_per_step": 1e3 * t,
+                "api": "pinned host copies of each rank's A rows and rank 0's B + dist.StrongGemm (NCCL broadcast "
+                       "of B, pre-pass all-reduce, mpcgemm_ex, NCCL all-gather of C) + D2H of the gathered C on rank 0"}
+
+    hA = mpgen.CMat(pinned(A.re), pinned(A.im))
+    hB = mpgen.CMat(pinned(B.re), pinned(B.im))
+    hC = mpgen.CMat(pinned(mpgen.empty_rmat(m, n, prec)), pinned(mpgen.empty_rmat(m, n, prec)))
+    P.mpcgemm_host(hA, hB, prec, args.method, C=hC)               # warm-up (staging allocation)
     ts = []
     for _ in range(max(2, min(args.steps, 3))):
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
         t0 = time.perf_counter()
-        run()
+        P.mpcgemm_host(hA, hB, prec, args.method, C=hC)
         ts.append(time.perf_counter() - t0)
     t_block = statistics.median(ts)
-    t = t_block
-    pipelined = None
-    if world == 1:
-        # a stream of K products through the queued entry: step i+1's H2D overlaps step i's slice
-        # GEMM and step i's D2H the next step's compute; every step still copies its inputs in
-        # and its C out inside the timed region (wall clock from the first call to the wait)
-        hC2 = mpgen.CMat(pinned(mpgen.empty_rmat(m, n, prec)), pinned(mpgen.empty_rmat(m, n, prec)))
-        outs = (hC, hC2)
-        K = max(3, args.steps)
-        for i in range(2):                                       # warm-up: both staging sets
-            P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i])
-        P.mpcgemm_host_wait()
-        t0 = time.perf_counter()
-        for i in range(K):
-            P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i & 1])
-        P.mpcgemm_host_wait()
-        t = (time.perf_counter() - t0) / K
-        pipelined = K
-    if world > 1:
-        tt = torch.tensor([t], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
-    ent = lambda R: R.sign.nbytes + R.exp.nbytes + R.limbs.nbytes
-    out = {"value": world * m * n * k / t, "unit": UNIT, "h2d_bytes_per_step": ent(A.re) + ent(A.im) + ent(B.re) + ent(B.im),
-           "d2h_bytes_per_step": 2 * (m * n * (9 + 8 * ((prec + 63) // 64))), "ms_per_step": 1e3 * t,
-           "api": "pinned host copies + dist protocol + mpcgemm_ex (Python public API)"}
-    if pipelined:
-        out["api"] = (f"mpcgemm_host_async x {pipelined} steps + mpcgemm_host_wait (C ABI, pinned host buffers; "
-                      "step i+1's H2D overlaps step i's compute)")
-        out["blocking_ms_per_step"] = 1e3 * t_block
-        out["blocking_api"] = "mpcgemm_host (one blocking call: H2D, compute, D2H)"
-    return out
+    # a stream of K products through the queued entry: step i+1's H2D overlaps step i's slice
+    # GEMM and step i's D2H the next step's compute; every step still copies its inputs in and
+    # its C out inside the timed region (wall clock from the first call to the wait)
+    hC2 = mpgen.CMat(pinned(mpgen.empty_rmat(m, n, prec)), pinned(mpgen.empty_rmat(m, n, prec)))
+    outs = (hC, hC2)
+    K = max(3, args.steps)
+    for i in range(2):                                           # warm-up: both staging sets
+        P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i])
+    P.mpcgemm_host_wait()
+    t0 = time.perf_counter()
+    for i in range(K):
+        P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i & 1])
+    P.mpcgemm_host_wait()
+    t = (time.perf_counter() - t0) / K
+    return {"value": m * n * k / t, "unit": UNIT, "h2d_bytes_per_step": ent(A.re) + ent(A.im) + ent(B.re) + ent(B.im),
+            "d2h_bytes_per_step": 2 * (m * n * (9 + 8 * ((prec + 63) // 64))), "ms_per_step": 1e3 * t,
+            "api": (f"mpcgemm_host_async x {K} steps + mpcgemm_host_wait (C ABI, pinned host buffers; "
+                    "step i+1's H2D overlaps step i's compute)"),
+            "blocking_ms_per_step": 1e3 * t_block,
+            "blocking_api": "mpcgemm_host (one blocking call: H2D, compute, D2H)"}
 
 
 if __name__ == "__main__":

@@ -17,6 +17,8 @@
 #include <functional>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/mpcgemm.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -40,6 +42,12 @@ int fail(int code, const char *what, cudaError_t e = cudaSuccess) {
     } while (0)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// NVTX range per stage of the hot path (host-side launch sequence; visible in nsys / ncu --nvtx)
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 int env_int(const char *name, int dflt);
 
 // ---------------------------------------------------------------- workspace cache
@@ -646,14 +654,20 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     int8_t *digB = digA + align_up((size_t)parts * s * mg * Lo.kp, 256);
     int32_t *partials = (int32_t *)((uint8_t *)digB + align_up((size_t)parts * s * n * Lo.kp, 256));
     uint64_t *fix = (uint64_t *)((uint8_t *)partials);  // set below per plan
-    CK(split_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, s, parts, digB, st));
+    {
+        Nvtx r("mpcgemm.a3_split_B");
+        CK(split_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, s, parts, digB, st));
+    }
     if (!sblk.empty()) CK(cudaMemcpyAsync(mv.sblk, sblk.data(), 4 * sblk.size(), cudaMemcpyHostToDevice, st));
     int launches = 1;
     for (int64_t r0 = 0; r0 < m; r0 += mg) {
         const int64_t mr = std::min(mg, m - r0);
         const mpc_cmat Ag = rows_of(*A, r0, L);
         const mpc_cmat Cg = rows_of(*C, r0, L);
-        CK(split_launch(dm(Ag.re), dm(Ag.im), 0, mr, k, Lo.kp, L, eA + r0, s, parts, digA, st));
+        {
+            Nvtx r("mpcgemm.a3_split_A");
+            CK(split_launch(dm(Ag.re), dm(Ag.im), 0, mr, k, Lo.kp, L, eA + r0, s, parts, digA, st));
+        }
         if (E && r0 == 0) CK(cudaEventRecord(E->ev[3], st));
         const Geometry geo = main_geometry(dev, mr, n, k, s, method);
         const int BN = geo.BN;
@@ -678,7 +692,10 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         SL.digA = digA; SL.digB = digB; SL.rowsA = mr; SL.rowsB = n; SL.kp = Lo.kp;
         SL.grid = plan->grid; SL.BM = geo.BM; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits;
         SL.units_flat = plan->d_units;
-        CK(slicegemm_launch(SL, st));
+        {
+            Nvtx r("mpcgemm.a4_slicegemm");
+            CK(slicegemm_launch(SL, st));
+        }
         if (E && r0 + mr >= m) CK(cudaEventRecord(E->ev[4], st));
         FoldParams F;
         F.partials = partials; F.nslots = plan->nslots; F.nstrips = Lo.nstrips; F.m = mr; F.n = n;
@@ -690,7 +707,10 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         fix = (uint64_t *)((uint8_t *)partials +
                            align_up((size_t)plan->nslots * ((mr + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
         F.fix = fix;
-        CK(fold_normalize_launch(F, st));
+        {
+            Nvtx r("mpcgemm.a5a6_fold_normalize");
+            CK(fold_normalize_launch(F, st));
+        }
         launches += 3;                                 // split A_g, slice GEMM, fold
         if (rep) {
             rep->mma_instructions += plan->mma; rep->work_units += plan->nunits;
@@ -747,9 +767,13 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     int64_t *eA = mv.eA, *eB = mv.eB;
     uint8_t *nzA = mv.nzA, *nzB = mv.nzB;
     uint32_t *errflag = mv.errflag;
+    Nvtx range_call("mpcgemm");
     if (validate) CK(cudaMemsetAsync(errflag, 0, 4, st));
-    CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, eA, nzA, errflag, validate, st));
-    CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, eB, nzB, errflag, validate, st));
+    {
+        Nvtx r("mpcgemm.a1_linemax");
+        CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, eA, nzA, errflag, validate, st));
+        CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, eB, nzB, errflag, validate, st));
+    }
     if (E) CK(cudaEventRecord(E->ev[1], st));
     int launches = 4 + (validate ? 1 : 0);             // linemax + finalize, A and B [, flag readback]
     if (validate) {
@@ -765,6 +789,7 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     if (!s) {
         if (int rc = grow(&dc.ws, &dc.ws_bytes, Lo.pre)) return rc;
         Bounds bd;
+        Nvtx range_pre("mpcgemm.a2_prepass");
         if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, &bd)) return rc;
         for (int q = 0; q < 3; q++) pb[q] = bd.g[q];
         launches += 5 + (pb[0] == 0 ? 2 : 0);         // planes x2, T GEMM, min, readback [, max-plus, readback]

@@ -304,6 +304,20 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
     const int64_t plane = lines * kp;
     const int64_t rowlen = min((int64_t)kSplitT, kp - k0);          // bytes of this CTA's plane rows
     const int nwords = (s + 7) / 8;
+    // full tiles: thread q copies the fixed (part, byte, vector) rows q and q + 128 of the staging
+    // every word; their plane rows move down 8 planes per word (a constant pointer step)
+    constexpr int VPR = kSplitT / 16;
+    int8_t *optr[2]; int ostg[2]; int obt[2]; bool oon[2];
+#pragma unroll
+    for (int it = 0; it < 2; it++) {
+        const int q = tid + it * kSplitT, row = q / VPR, v = q % VPR;
+        const int p = row >> 3, bt = row & 7;
+        oon[it] = q < nparts * 8 * VPR;
+        obt[it] = bt;
+        ostg[it] = (p * 8 + bt) * kSplitT + 16 * v;
+        optr[it] = dig + ((int64_t)p * s + (s - 1 - bt)) * plane + line * kp + k0 + 16 * v;
+    }
+    const int64_t ostep = 8 * plane;
     for (int w = 0; w < nwords; w++) {
         uint8_t *stg = stage + (w & 1) * (3 * 8 * kSplitT);
         uint64_t y[3];
@@ -336,17 +350,11 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
         // plane rows of this word: (part p, byte bt) -> plane s-1-(8w+bt), 16-byte vector stores
         const int nb = min(8, s - 8 * w);
         if (rowlen == kSplitT) {                       // full tile: 8 vectors per row, no divisions
-            constexpr int VPR = kSplitT / 16;
 #pragma unroll
-            for (int it = 0; it < (3 * 8 * VPR + kSplitT - 1) / kSplitT; it++) {
-                const int q = tid + it * kSplitT;
-                if (q >= nparts * 8 * VPR) break;
-                const int row = q / VPR, v = q % VPR;
-                const int p = row >> 3, bt = row & 7;
-                if (bt < nb) {
-                    int8_t *o = dig + ((int64_t)p * s + (s - 1 - 8 * w - bt)) * plane + line * kp + k0 + 16 * v;
-                    *reinterpret_cast<uint4 *>(o) = *reinterpret_cast<const uint4 *>(stg + (p * 8 + bt) * kSplitT + 16 * v);
-                }
+            for (int it = 0; it < 2; it++) {
+                if (oon[it] && obt[it] < nb)
+                    *reinterpret_cast<uint4 *>(optr[it]) = *reinterpret_cast<const uint4 *>(stg + ostg[it]);
+                optr[it] -= ostep;
             }
             continue;
         }
@@ -636,7 +644,12 @@ MPC_DEV void store_limbs(uint64_t *dst, const uint64_t *v, int L) {
 MPC_DEV void round_store(const uint64_t *buf, int64_t stride, int n, int64_t e_lsb, bool neg, int prec, int L,
                          uint8_t *sign_out, int64_t *exp_out, uint64_t *limbs_out)
 {
-    uint64_t ov[kMaxSlices / 8 + 8];                  // >= L (prec <= 4096)
+    // output limbs go out in pairs as they are formed (16-byte stores when aligned; no local array)
+    const bool vec = !(L & 1) && !(reinterpret_cast<uintptr_t>(limbs_out) & 15);
+    auto put2 = [&](int l, uint64_t a, uint64_t b) {
+        if (vec) *reinterpret_cast<ulonglong2 *>(limbs_out + l) = make_ulonglong2(a, b);
+        else { limbs_out[l] = a; if (l + 1 < L) limbs_out[l + 1] = b; }
+    };
     int b = 0;
     for (int l = n - 1; l >= 0; l--) {
         const uint64_t v = buf[(int64_t)l * stride];
@@ -644,8 +657,7 @@ MPC_DEV void round_store(const uint64_t *buf, int64_t stride, int n, int64_t e_l
     }
     if (b == 0) {
         *sign_out = 0; *exp_out = 0;
-        for (int l = 0; l < L; l++) ov[l] = 0;
-        store_limbs(limbs_out, ov, L);
+        for (int l = 0; l < L; l += 2) put2(l, 0ull, 0ull);
         return;
     }
     const FixView F{buf, stride, n};
@@ -668,22 +680,26 @@ MPC_DEV void round_store(const uint64_t *buf, int64_t stride, int n, int64_t e_l
         bool allones = (w0 | ((1ull << drop) - 1)) == ~0ull;
         for (int l = 1; l < L && allones; l++) allones = F.bits64(base + 64 * l) == ~0ull;
         if (allones) {
-            for (int l = 0; l < L - 1; l++) ov[l] = 0;
-            ov[L - 1] = 1ull << 63;
-            store_limbs(limbs_out, ov, L);
+            for (int l = 0; l < L; l += 2) put2(l, 0ull, l + 1 == L - 1 ? (1ull << 63) : 0ull);
+            if (L & 1) limbs_out[L - 1] = 1ull << 63;
             *sign_out = neg ? 1 : 0;
             *exp_out = E + 1;
             return;
         }
     }
     uint64_t c = up ? (1ull << drop) : 0ull;
-    for (int l = 0; l < L; l++) {
-        uint64_t w = l == 0 ? w0 : F.bits64(base + 64 * l);
-        const uint64_t x = w + c;
-        c = (x < w) ? 1ull : 0ull;
-        ov[l] = x;
+    for (int l = 0; l < L; l += 2) {
+        const uint64_t wa = l == 0 ? w0 : F.bits64(base + 64 * l);
+        const uint64_t xa = wa + c;
+        c = (xa < wa) ? 1ull : 0ull;
+        uint64_t xb = 0;
+        if (l + 1 < L) {
+            const uint64_t wb = F.bits64(base + 64 * (l + 1));
+            xb = wb + c;
+            c = (xb < wb) ? 1ull : 0ull;
+        }
+        put2(l, xa, xb);
     }
-    store_limbs(limbs_out, ov, L);
     *sign_out = neg ? 1 : 0;
     *exp_out = E;
 }
@@ -804,6 +820,11 @@ constexpr int kFoldEPT = 2;            // outputs per consumer thread (4 was tri
 static_assert(kFoldEPT == kFoldLdAlign, "scratch pitch alignment");
 
 template <int V> struct IntVec;
+template <> struct IntVec<1> {
+    MPC_DEV static void get_shared(uint32_t a, int32_t (&o)[1]) {
+        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(o[0]) : "r"(a) : "memory");
+    }
+};
 template <> struct IntVec<2> {
     using T = int2;
     MPC_DEV static void get(const T &v, int32_t (&o)[2]) { o[0] = v.x; o[1] = v.y; }
@@ -819,8 +840,21 @@ template <> struct IntVec<4> {
     }
 };
 
-template <int COLS, bool BETA, int EPT = kFoldEPT>
-__global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : 6)
+// SFIX: the fixed-point limbs of the CTA's COLS outputs stay in shared memory, fix[part][limb][col]
+// (no global round trip); otherwise (NEXT-2 sums, or s too large for shared memory) they go to
+// the global scratch fix[part][limb][m*ldF]
+// the EPT adjacent elements' words of one limb (16-byte stores for pairs)
+template <int EPT>
+MPC_DEV void store_ept(uint64_t *dst, const uint64_t *v) {
+    if constexpr (EPT == 1) { *dst = v[0]; }
+    else {
+#pragma unroll
+        for (int x = 0; x < EPT; x += 2) *reinterpret_cast<ulonglong2 *>(dst + x) = make_ulonglong2(v[x], v[x + 1]);
+    }
+}
+
+template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRing>
+__global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : (SFIX ? 3 : 6))
 fold_normalize_kernel(const FoldParams F)
 {
     constexpr int NCONS = COLS / EPT;                 // consumer threads
@@ -830,24 +864,27 @@ fold_normalize_kernel(const FoldParams F)
     const int Lw = BETA ? Lc0 + F.L + 3 : 0;          // NEXT-2 sum window
     const int nslots = (int)F.nslots;
     int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                                   // [RING][PER][COLS]
-    uint16_t *cntq = reinterpret_cast<uint16_t *>(fsm_raw + kFoldRing * kFoldPer * COLS * 4);  // [job][s+2] chunk counts
+    uint16_t *cntq = reinterpret_cast<uint16_t *>(fsm_raw + RING * kFoldPer * COLS * 4);  // [job][s+2] chunk counts
     uint64_t *full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(cntq + kMaxJobs * (s + 2)) + 15) & ~uintptr_t(15));
-    uint64_t *empty = full + kFoldRing;
+    uint64_t *empty = full + RING;
+    uint64_t *fixs = empty + RING;               // SFIX: [2][Lc0][COLS] (16-byte aligned)
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     // chunk count of every (job, diagonal): the slots come in the order r = s+1..2, job, chunk
     for (int x = tid; x < kMaxJobs * (s + 2); x += blockDim.x)
         cntq[x] = (uint16_t)((x % (s + 2)) < 2 ? 0 : F.slotinfo[x * 2 + 1]);
     if (tid == 0) {
-        for (int e = 0; e < kFoldRing; e++) { mbar_init(&full[e], 1); mbar_init(&empty[e], NCONS / 32); }
+        for (int e = 0; e < RING; e++) { mbar_init(&full[e], 1); mbar_init(&empty[e], NCONS / 32); }
         fence_barrier_init();
     }
     __syncthreads();
     // block (x, y): row i = (y / nsub) * 128 + x, columns j0 = (y % nsub) * COLS, so the 128
     // blocks of one (row block, strip) are adjacent in launch order
+    // (a 1-D grid: block b = y * 128 + x)
     const int64_t nsub = (F.n + COLS - 1) / COLS;
-    const int64_t i = (int64_t)(blockIdx.y / nsub) * kRowBlk + blockIdx.x;
-    const int64_t j0 = (int64_t)(blockIdx.y % nsub) * COLS;      // COLS divides the 256-column strip
+    const int64_t bx = (int64_t)blockIdx.x & (kRowBlk - 1), by = (int64_t)blockIdx.x >> 7;
+    const int64_t i = (by / nsub) * kRowBlk + bx;
+    const int64_t j0 = (by % nsub) * COLS;            // COLS divides the 256-column strip
     if (i >= F.m) return;
     // NEXT-4: this row's triangle d = sr <= s; its diagonals r = sr+1 .. 2 are the slots from
     // the first slot of (job 0, r = sr+1) on (slots of larger r are not read)
@@ -864,7 +901,7 @@ fold_normalize_kernel(const FoldParams F)
                 mbar_arrive_expect_tx(&full[e], (uint32_t)(cnt * COLS * 4));
                 for (int f = 0; f < cnt; f++)                // slot blocks are kTileElems apart
                     bulk_load(ring + (e * kFoldPer + f) * COLS, region + (int64_t)(sl + f) * kTileElems, COLS * 4, &full[e]);
-                if (++e == kFoldRing) { e = 0; ph ^= 1; }
+                if (++e == RING) { e = 0; ph ^= 1; }
             }
         }
         return;
@@ -873,8 +910,8 @@ fold_normalize_kernel(const FoldParams F)
     // the global scratch fix[part][limb][m*ldF] (column = element), read back by the rounding.
     const int col = EPT * tid;
     const int64_t jj = j0 + col;                      // first of the EPT elements
-    const int64_t lstride = F.m * F.ldF;              // limb stride in the scratch
-    uint64_t *fixg = F.fix + i * F.ldF + jj;
+    const int64_t lstride = SFIX ? (int64_t)COLS : F.m * F.ldF;   // limb stride
+    uint64_t *fixg = SFIX ? fixs + col : F.fix + i * F.ldF + jj;
     int64_t t0[EPT], t1[EPT], t2[EPT];
     int64_t cr[2][EPT];                               // [part][element] carries
     uint64_t cur[2][EPT];
@@ -895,7 +932,7 @@ fold_normalize_kernel(const FoldParams F)
             fill = 0;
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[e]);
-            if (++e == kFoldRing) { e = 0; ph ^= 1; addr = ring0; }
+            if (++e == RING) { e = 0; ph ^= 1; addr = ring0; }
         }
     };
     // diagonals r = sr+1 .. 2 (byte b = sr + 1 - r of the fixed-point number), two at a time:
@@ -957,10 +994,7 @@ fold_normalize_kernel(const FoldParams F)
                 if (live) {
 #pragma unroll
                     for (int p = 0; p < 2; p++)
-#pragma unroll
-                        for (int x = 0; x < EPT; x += 2)
-                            *reinterpret_cast<ulonglong2 *>(fixg + ((int64_t)p * Lc0 + (b >> 3)) * lstride + x) =
-                                make_ulonglong2(cur[p][x], cur[p][x + 1]);
+                        store_ept<EPT>(fixg + ((int64_t)p * Lc0 + (b >> 3)) * lstride, cur[p]);
                 }
 #pragma unroll
                 for (int x = 0; x < EPT; x++) cur[0][x] = cur[1][x] = 0;
@@ -980,16 +1014,12 @@ fold_normalize_kernel(const FoldParams F)
             w[x][1] = o ? ((c >> (64 - o)) | (sx << o)) : sx;
         }
         uint64_t *fx = fixg + (int64_t)p * Lc0 * lstride;
+        uint64_t w0[EPT], w1[EPT], sx[EPT];
 #pragma unroll
-        for (int x = 0; x < EPT; x += 2) {
-            *reinterpret_cast<ulonglong2 *>(fx + (int64_t)l0 * lstride + x) = make_ulonglong2(w[x][0], w[x + 1][0]);
-            *reinterpret_cast<ulonglong2 *>(fx + (int64_t)(l0 + 1) * lstride + x) = make_ulonglong2(w[x][1], w[x + 1][1]);
-        }
-        for (int l = l0 + 2; l < Lc0; l++)
-#pragma unroll
-            for (int x = 0; x < EPT; x += 2)
-                *reinterpret_cast<ulonglong2 *>(fx + (int64_t)l * lstride + x) =
-                    make_ulonglong2(cr[p][x] < 0 ? ~0ull : 0ull, cr[p][x + 1] < 0 ? ~0ull : 0ull);
+        for (int x = 0; x < EPT; x++) { w0[x] = w[x][0]; w1[x] = w[x][1]; sx[x] = cr[p][x] < 0 ? ~0ull : 0ull; }
+        store_ept<EPT>(fx + (int64_t)l0 * lstride, w0);
+        store_ept<EPT>(fx + (int64_t)(l0 + 1) * lstride, w1);
+        for (int l = l0 + 2; l < Lc0; l++) store_ept<EPT>(fx + (int64_t)l * lstride, sx);
     }
 #pragma unroll 1
     for (int x = 0; x < EPT; x++) {
@@ -1009,6 +1039,14 @@ fold_normalize_kernel(const FoldParams F)
                              F.Cre.sign + oi, F.Cre.exp + oi, F.Cre.limbs + oi * F.L, lstride, R0);
             accumulate_store(f1, (int)0, Lc0, Lw, e0, F.alpha_neg, s1, x1, F.C0im.limbs + cj * F.L, F.prec, F.L,
                              F.Cim.sign + oj, F.Cim.exp + oj, F.Cim.limbs + oj * F.L, lstride, R0);
+        } else if (SFIX) {                            // limbs in shared memory: round in place
+#pragma unroll 1
+            for (int p = 0; p < 2; p++) {
+                const DMatOut &Co = p ? F.Cim : F.Cre;
+                const int64_t oo = p ? oj : oi;
+                normalize_store(fixg + x + (int64_t)p * Lc0 * lstride, lstride, Lc0, e0, F.alpha_neg, F.prec, F.L,
+                                Co.sign + oo, Co.exp + oo, Co.limbs + oo * F.L);
+            }
         } else {
             // copy each part's limbs to a thread-local array with independent (batched) loads,
             // then magnitude + RNE on the L1-resident copy (the scratch reads were a dependent
@@ -1027,18 +1065,30 @@ fold_normalize_kernel(const FoldParams F)
     }
 }
 
-size_t fold_smem(int s, int cols, int64_t nslots) {
-    (void)nslots;
-    return (size_t)kFoldRing * kFoldPer * cols * 4 + 2 * (size_t)kMaxJobs * (s + 2) + 32 + (size_t)2 * kFoldRing * 8 + 16;
+size_t fold_smem(int s, int cols, bool sfix, int ring = kFoldRing) {
+    const size_t base = (size_t)ring * kFoldPer * cols * 4 + 2 * (size_t)kMaxJobs * (s + 2) + 32 + (size_t)2 * ring * 8 + 16;
+    return base + (sfix ? (size_t)2 * (s / 8 + 3) * cols * 8 + 16 : 0);
 }
 
-template <int COLS, bool BETA>
+// shared-memory-limbs fold: 128 columns per CTA, one output per consumer thread, an 8-entry ring
+// (3 CTAs per SM: ~96 KB of partial strips in flight per SM) -- or, when the limbs do not fit,
+// the global scratch
+constexpr int kSfixCols = 128, kSfixRing = 8;
+static bool fold_sfix(int s, bool beta) {
+    // measured slower (fewer resident consumer threads: the fold is issue-bound), so off by default
+    if (beta || !getenv("MPCGEMM_FOLD_SFIX")) return false;
+    return fold_smem(s, kSfixCols, true, kSfixRing) <= 220 * 1024;
+}
+
+template <int COLS, bool BETA, bool SFIX, int EPT, int RING>
 static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
-    const size_t sm = fold_smem(F.s, COLS, F.nslots);
-    cudaError_t e = cudaFuncSetAttribute(fold_normalize_kernel<COLS, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const size_t sm = fold_smem(F.s, COLS, SFIX, RING);
+    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    dim3 grid(kRowBlk, (unsigned)(((F.n + COLS - 1) / COLS) * ((F.m + kRowBlk - 1) / kRowBlk)));
-    fold_normalize_kernel<COLS, BETA><<<grid, COLS / kFoldEPT + 32, sm, st>>>(F);
+    const int64_t blocks = (int64_t)kRowBlk * ((F.n + COLS - 1) / COLS) * ((F.m + kRowBlk - 1) / kRowBlk);
+    if (blocks > INT_MAX) return cudaErrorInvalidValue;
+    kern<<<(unsigned)blocks, COLS / EPT + 32, sm, st>>>(F);
     return cudaGetLastError();
 }
 
@@ -1046,12 +1096,14 @@ cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
 {
     if (F.m == 0 || F.n == 0) return cudaSuccess;
     if (F.s > kMaxSlices || (F.ldF % kFoldEPT)) return cudaErrorInvalidValue;
-    if (F.beta) return fold_launch_t<256, true>(F, st);
-    return fold_launch_t<256, false>(F, st);
+    if (F.beta) return fold_launch_t<256, true, false, kFoldEPT, kFoldRing>(F, st);
+    if (fold_sfix(F.s, false)) return fold_launch_t<kSfixCols, false, true, 1, kSfixRing>(F, st);
+    return fold_launch_t<256, false, false, kFoldEPT, kFoldRing>(F, st);
 }
 
-// fixed-point scratch size (uint64 words) for the fold
+// fixed-point scratch size (uint64 words) for the fold (0 when the limbs stay in shared memory)
 size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta) {
+    if (fold_sfix(s, beta)) return 0;
     const int Lc0 = s / 8 + 3;
     return (size_t)m * ldF * (2 * Lc0 + (beta ? Lc0 + L + 3 : 0));
 }

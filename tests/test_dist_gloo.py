@@ -106,3 +106,60 @@ def test_two_ranks_gloo(case, distribute):
             assert np.array_equal(z[f"{p}_sign"], Rp.sign)
             assert np.array_equal(z[f"{p}_exp"], Rp.exp)
             assert np.array_equal(z[f"{p}_limbs"].view(np.uint64), Rp.limbs)
+
+
+# ------------------------------------------------------------------ strong scaling (dist.StrongGemm)
+def _strong_worker(rank, world, port, case, outdir, steps):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2307_06072_b200 as P
+    from paper_2307_06072_b200.dist import StrongGemm, copy_cmat, packed_cmat
+    m, n, k, prec, spread, method = case
+    r0, r1 = row_range(m, rank, world)
+    A = mpgen.random_cmat(78, 1, m, k, prec, spread, zero_frac=0.1).rows(r0, r1)    # pre-sharded rows
+    Bsrc = None
+    if rank == 0:                                      # B lives on rank 0 only
+        Bsrc = packed_cmat(k, n, prec, "cpu")
+        copy_cmat(Bsrc[0], P.to_device(mpgen.random_cmat(78, 2, k, n, prec, spread, zero_frac=0.1), "cpu"))
+
+    def compute(Al, Bd, Cv, s_):                       # the per-rank stand-in: the oracle
+        C = oracle.ozaki(P.to_host(Al), P.to_host(Bd), prec, method, s_)
+        for p in ("re", "im"):
+            R, D = getattr(C, p), getattr(Cv, p)
+            D.sign.copy_(torch.from_numpy(R.sign)); D.exp.copy_(torch.from_numpy(R.exp))
+            D.limbs.copy_(torch.from_numpy(R.limbs.view(np.int64)))
+        return {"slices": s_}
+
+    SG = StrongGemm(m, n, k, prec, method, "cpu",
+                    lambda Al, Bd, full: oracle.rho_bounds(P.to_host(Al), P.to_host(Bd), full=full),
+                    lambda *a: oracle.slices_for(*a)[0], compute)
+    reps = SG.run(P.to_device(A, "cpu"), Bsrc, steps)
+    SG.finish()
+    full = SG.full_c(steps - 1)
+    if rank == 0:
+        np.savez(os.path.join(outdir, "out.npz"), s=reps[-1]["slices"], nsteps=len(reps),
+                 **{f"{p}_{f}": full[p][f].numpy() for p in ("re", "im") for f in ("sign", "exp", "limbs")})
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", [(7, 9, 11, 128, 4, "3M"),      # ragged rows
+                                  (9, 6, 12, 256, 16, "4M"),     # minT == 0: second all-reduce round
+                                  (1, 5, 8, 128, 0, "3M")])      # one rank without rows
+def test_strong_gemm_two_ranks(case):
+    """dist.StrongGemm (the bench's N > 1 path) at world size 2 on gloo: A pre-sharded, B only on
+    rank 0 and broadcast inside each of 3 pipelined products (double buffers reused), the pre-pass
+    all-reduce, C row blocks all-gathered; the gathered C equals one process's oracle on all rows."""
+    m, n, k, prec, spread, method = case
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_strong_worker, args=(2, _free_port(), case, d, 3), nprocs=2, join=True)
+        z = np.load(os.path.join(d, "out.npz"))
+        A = mpgen.random_cmat(78, 1, m, k, prec, spread, zero_frac=0.1)
+        B = mpgen.random_cmat(78, 2, k, n, prec, spread, zero_frac=0.1)
+        s_ref, _ = oracle.auto_slices(A, B, prec, method)
+        assert int(z["s"]) == s_ref and int(z["nsteps"]) == 3
+        R = oracle.ozaki(A, B, prec, method, s_ref)
+        for p in ("re", "im"):
+            Rp = getattr(R, p)
+            assert np.array_equal(z[f"{p}_sign"], Rp.sign)
+            assert np.array_equal(z[f"{p}_exp"], Rp.exp)
+            assert np.array_equal(z[f"{p}_limbs"].view(np.uint64), Rp.limbs)

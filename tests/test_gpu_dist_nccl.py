@@ -55,3 +55,40 @@ def test_dist_gemm_nccl_world1(method):
         assert np.array_equal(full[p]["sign"].cpu().numpy(), R.sign)
         assert np.array_equal(full[p]["exp"].cpu().numpy(), R.exp)
         assert np.array_equal(full[p]["limbs"].cpu().numpy().view(np.uint64), R.limbs)
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+def test_strong_gemm_nccl_world1(method):
+    """dist.StrongGemm -- the bench's strong-scaling path: packed B broadcast from rank 0, the
+    pre-pass all-reduce, the C ABI on this rank's rows, C all-gather, pipelined over a
+    communication stream with double buffers -- through real NCCL collectives (world size 1),
+    4 products: the gathered C equals the plain single call bitwise."""
+    prec = 256
+    m, n, k = 300, 270, 160
+    A = mpgen.random_cmat(13, 1, m, k, prec, 4, zero_frac=0.05)
+    B = mpgen.random_cmat(13, 2, k, n, prec, 4, zero_frac=0.05)
+    dA, dB = P.to_device(A), P.to_device(B)
+    C0, r0 = P.gemm(dA, dB, prec, method)
+    torch.cuda.synchronize()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        Bsrc = pdist.packed_cmat(k, n, prec, "cuda")
+        pdist.copy_cmat(Bsrc[0], dB)
+        SG = pdist.StrongGemm(m, n, k, prec, method, "cuda",
+                              lambda Al, Bd, full: P.mpcgemm_rho_bounds(Al, Bd, prec, full),
+                              P.mpcgemm_slices_for,
+                              lambda Al, Bd, Cv, s_: P.mpcgemm_ex(Al, Bd, Cv, prec, method, slices=s_))
+        reps = SG.run(dA, Bsrc, 4)
+        parts = SG.finish()
+        full = SG.full_c(3)
+    finally:
+        dist.destroy_process_group()
+    assert all(r["slices"] == r0["slices"] for r in reps)
+    assert parts["compute_ms"] > 0
+    H0 = P.to_host(C0)
+    for p in ("re", "im"):
+        R = getattr(H0, p)
+        assert np.array_equal(full[p]["sign"].cpu().numpy(), R.sign)
+        assert np.array_equal(full[p]["exp"].cpu().numpy(), R.exp)
+        assert np.array_equal(full[p]["limbs"].cpu().numpy().view(np.uint64), R.limbs)
