@@ -95,6 +95,20 @@ typedef struct {
                                  slices > 0; INT8 carrier only.  0 = one s for all rows.        */
     int32_t *block_slices;    /* optional HOST output, ceil(m/256) entries: the s used by each
                                  256-row block (all equal to s unless adaptive)               */
+    int32_t  device_rule;     /* 1 (with slices == 0): the slice rule runs ON THE DEVICE -- the
+                                 pre-pass integers are reduced and the certified s chosen by a
+                                 kernel, which selects one of the plans the host prepared for every
+                                 s the first pre-pass stage can yield, s_lo = rule(log2 rho = 0) ..
+                                 s_hi = rule(minT = 1); the split, slice GEMM and fold read the
+                                 chosen plan from device memory.  The call never synchronizes the
+                                 host (after the first call of a shape: plans and workspace are
+                                 cached), so it can be captured in a CUDA graph.  Same result as
+                                 the host rule, bit for bit.  If the certified s falls outside
+                                 [s_lo, s_hi] (only when the max-plus stage is needed) nothing is
+                                 written to C and mpcgemm_device_rule_result() returns
+                                 MPCGEMM_ERR_SLICES -- callers then repeat the call with
+                                 device_rule = 0.  Ignored with slices > 0, validate, beta,
+                                 alpha_neg, adaptive, carrier = 1; rep->slices is 0 (unknown).    */
 } mpcgemm_opts;
 
 typedef struct {
@@ -223,6 +237,12 @@ int mpclu_solve(int64_t n, int64_t nrhs, int32_t prec, const mpc_cmat *LU, const
  * stream: cudaStream_t (NULL: legacy default stream). */
 int mpc_scalar(int32_t op, int64_t cnt, int32_t prec, const mpc_cmat *A, const mpc_cmat *X, const mpc_cmat *Y,
                mpc_cmat *O, int64_t *kv, void *stream);
+
+/* Result of the last device_rule call of shape m x n on this device: synchronizes `stream`
+ * (cudaStream_t, NULL = legacy default) and reads the device state.  out[0] = the certified s,
+ * out[1..3] = the reduced pre-pass integers (minT, minT1, maxD2).  Returns 0, or
+ * MPCGEMM_ERR_SLICES when that s was outside the planned range (C untouched). */
+int mpcgemm_device_rule_result(int64_t m, int64_t n, void *stream, int64_t out[4]);
 
 const char *mpcgemm_strerror(int code);
 const char *mpcgemm_last_error(void);   /* thread-local detail of the last error              */

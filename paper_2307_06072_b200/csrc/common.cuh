@@ -75,6 +75,23 @@ __host__ __device__ __forceinline__ int64_t part_off(int64_t row, int64_t col, i
            (col & (kStrip - 1));
 }
 
+// Device-rule mode (opts->device_rule): the slice count is chosen on the device from the pre-pass
+// integers, among candidate plans built by the host for every s the first stage can yield; the
+// kernels after the rule read the chosen plan from device memory (no host readback).
+struct DevPlan {
+    const WorkUnit *units;     // the plan's unit list
+    int32_t *hot;              // its k-phase hints
+    const int32_t *slotinfo;   // its (job, r) -> (first slot, chunk count) table
+    int32_t s, nunits, nslots, pad;
+};
+struct DevRuleState {
+    DevPlan cur;               // the chosen plan
+    int32_t status;            // 0: ok; MPCGEMM_ERR_SLICES (-8): the certified s is outside the planned
+                               // range -- every kernel after the rule returns without writing C
+    int32_t s_needed;          // the certified s (also when outside the range)
+    int64_t minT, minT1, maxD2;   // the reduced pre-pass integers the rule used
+};
+
 struct GemmParams {
     const WorkUnit *units;     // global order: size-descending, tiles of one (job, r, chunk) contiguous
     int32_t nunits;
@@ -98,6 +115,7 @@ struct GemmParams {
     int32_t kk_last;           // K = 32 MMA steps of the last k-block (1..3; 0: all 4): the zero
                                // padding of k up to a multiple of 128 is not multiplied
     unsigned long long *mma_count;   // or null: tcgen05.mma instructions issued, added at CTA exit
+    const DevRuleState *drs;         // or null; else s, nunits, nslots, units, hot come from drs->cur
     JobDesc jobs[kMaxJobs];
 };
 

@@ -23,9 +23,17 @@ cudaError_t slicegemm_launch(const SliceGemmLaunch &L, cudaStream_t st);
 cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, int prec, int side,
                            int64_t *eline, uint8_t *nz, uint32_t *errflag, int validate, cudaStream_t st);
 
+// a-1 for both operands in one scan launch (eAB = eA[m] then eB[n], nzAB likewise)
+cudaError_t linemax2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int L, int prec,
+                            int64_t *eAB, uint8_t *nzAB, uint32_t *errflag, int validate, cudaStream_t st);
+cudaError_t prepass_planes2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp,
+                                   int L, const int64_t *eA, const int64_t *eB, int8_t *tA, int32_t *relA, int8_t *tB,
+                                   int32_t *relB, cudaStream_t st);
+
 // a-3: balanced radix-256 digit planes dig[part][alpha][lines][kp]
 cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
-                         const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st);
+                         const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st,
+                         const DevRuleState *drs = nullptr);
 
 // 3-D TMA map over ABI limbs (implemented in slicegemm.cu; map = CUtensorMap*, 64-byte aligned)
 int encode_limb_map(void *map, const uint64_t *base, int L, uint64_t d1, uint64_t d2, uint64_t stride1,
@@ -40,6 +48,14 @@ cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int
 // small device -> host results (pre-pass integers, flags) written by SM stores into mapped
 // pinned host memory: no copy engine, so they never queue behind a bulk D2H on another stream
 cudaError_t readback_launch(void *dst_mapped, const void *src, size_t bytes, cudaStream_t st);
+// device-rule mode: stage 2 only if some block's stage-1 minimum is 0 (decided on the device;
+// out_*2 arrays, initialised to all-ones), then the slice rule over the reduced integers picks
+// the plan (plans[s - s_lo] for s in [s_lo, s_hi]) into *drs
+cudaError_t prepass_rule_launch(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n, int64_t k,
+                                int64_t kp, const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA,
+                                const int32_t *relB, const unsigned long long *min1, unsigned long long *min2,
+                                unsigned long long *min12, long long *max22, int prec, int method,
+                                const DevPlan *plans, int s_lo, int s_hi, DevRuleState *drs, cudaStream_t st);
 cudaError_t prepass_reduce_launch(const int32_t *T, int nslots, int64_t nstrips,
                                   int64_t m, int64_t n, int64_t k, int64_t kp,
                                   const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA, const int32_t *relB,
@@ -59,6 +75,8 @@ struct FoldParams {
     const int32_t *sblk;         // NEXT-4: slice count of each 256-row block (<= s), or nullptr
     uint64_t *fix;               // fixed-point scratch, fold_scratch_words(m, ldF, s, L, beta) words
     int64_t ldF;                 // scratch row pitch (a multiple of kFoldLdAlign, >= n)
+    const DevRuleState *drs;     // or null; else s, nslots, slotinfo come from drs->cur (F.s: the
+                                 // largest candidate s, which sizes shared memory and the scratch)
 };
 constexpr int kFoldLdAlign = 2;  // fold outputs per consumer thread
 size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta);

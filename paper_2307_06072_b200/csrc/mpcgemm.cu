@@ -22,6 +22,7 @@
 #include "../../include/mpcgemm.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "rule.cuh"
 
 using namespace mpc;
 
@@ -76,10 +77,15 @@ struct DevCache {
 struct StreamOrder {
     DevCache &dc;
     cudaStream_t st;
-    StreamOrder(DevCache &d, cudaStream_t s) : dc(d), st(s) {
-        if (dc.done) cudaStreamWaitEvent(st, dc.done, 0);
+    bool capturing = false;                          // inside CUDA graph capture: the graph orders
+    StreamOrder(DevCache &d, cudaStream_t s) : dc(d), st(s) {   // its nodes, no cross-stream event
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        capturing = cs != cudaStreamCaptureStatusNone;
+        if (dc.done && !capturing) cudaStreamWaitEvent(st, dc.done, 0);
     }
     ~StreamOrder() {
+        if (capturing) return;
         if (!dc.done) cudaEventCreateWithFlags(&dc.done, cudaEventDisableTiming);
         cudaEventRecord(dc.done, st);
     }
@@ -379,9 +385,14 @@ struct MetaView {
     unsigned long long *omin, *omin1;
     long long *omax2;
     int32_t *sblk;
+    unsigned long long *dmin2, *dmin12;   // device rule: the stage-2 arrays (per block)
+    long long *dmax22;
+    DevRuleState *drs;                    // device rule: the chosen s / plan
 };
 size_t meta_flags_off(int64_t m, int64_t n) { return align_up(8 * (m + n) + (m + n) + 64, 256); }
-size_t meta_bytes(int64_t m, int64_t n) { return meta_flags_off(m, n) + align_up(64 + 28 * (size_t)nblocks(m) + 64, 256); }
+size_t meta_bytes(int64_t m, int64_t n) {
+    return meta_flags_off(m, n) + align_up(64 + 52 * (size_t)nblocks(m) + 64, 256) + align_up(sizeof(DevRuleState), 256);
+}
 MetaView meta_view(uint8_t *meta, int64_t m, int64_t n) {
     MetaView v;
     v.eA = (int64_t *)meta; v.eB = v.eA + m;
@@ -392,6 +403,10 @@ MetaView meta_view(uint8_t *meta, int64_t m, int64_t n) {
     v.omin1 = v.omin + nblocks(m);
     v.omax2 = (long long *)(v.omin1 + nblocks(m));
     v.sblk = (int32_t *)(v.omax2 + nblocks(m));
+    v.dmin2 = (unsigned long long *)align_up((size_t)(v.sblk + nblocks(m)), 8);
+    v.dmin12 = v.dmin2 + nblocks(m);
+    v.dmax22 = (long long *)(v.dmin12 + nblocks(m));
+    v.drs = (DevRuleState *)(meta + meta_flags_off(m, n) + align_up(64 + 52 * (size_t)nblocks(m) + 64, 256));
     return v;
 }
 
@@ -481,8 +496,8 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     int8_t *tA = (int8_t *)pre, *tB = tA + m * Lo.kp;
     int32_t *relA = (int32_t *)(pre + align_up((size_t)(m + n) * Lo.kp, 256)), *relB = relA + m * Lo.kp;
     int32_t *T = (int32_t *)(pre + align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256));
-    CK(prepass_planes_launch(dm(A->re), dm(A->im), 0, m, k, Lo.kp, L, mv.eA, tA, relA, st));
-    CK(prepass_planes_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, mv.eB, tB, relB, st));
+    CK(prepass_planes2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, Lo.kp, L, mv.eA, mv.eB, tA, relA, tB,
+                              relB, st));
     const int BN = tile_bn(n);
     const int grid = sm_count(dev);
     PlanKey key{m, n, k, 1, 0, 128, BN, grid, simt, (int)kMaxKBlocksPerChunk, 0, 0, {}};
@@ -534,26 +549,6 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     else if (g0 > 0 && !full) { out->g[0] = g0; out->g[1] = g0; out->g[2] = -1; }
     else { out->g[0] = g0; out->g[1] = g1; out->g[2] = g2; }
     return 0;
-}
-
-double rule_log2rho(int64_t k, int64_t minT, int64_t minT1, int64_t maxD2) {
-    double log2rho = 0.0;
-    if (minT > 0) log2rho = log2((double)k) + 14.0 - log2((double)minT);
-    else if (minT == 0) {
-        log2rho = -1e300;
-        if (minT1 >= 1) log2rho = log2((double)k) + 14.0 - log2((double)minT1);
-        if (maxD2 >= 0) { double b2 = log2((double)k) + 2.0 + (double)maxD2; if (b2 > log2rho) log2rho = b2; }
-        if (log2rho < -1e299) log2rho = 0.0;
-    }
-    return log2rho;
-}
-
-// the slice rule for b-bit digits (b = 8: INT8 carrier)
-int rule_slices(int32_t prec, int method, double log2rho, int bits = 8) {
-    const double c = method == 3 ? 4.0 : 3.0;
-    for (int s = 1; s <= kMaxSlices; s++)
-        if ((double)bits * s >= (double)prec - 4.0 + log2(c * s) + log2rho + 0.1) return s;
-    return MPCGEMM_ERR_SLICES;
 }
 
 // b = 53 - ceil((53 + ceil(log2 k)) / 2): the paper's binary64 slice width
@@ -697,7 +692,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
             CK(slicegemm_launch(SL, st));
         }
         if (E && r0 + mr >= m) CK(cudaEventRecord(E->ev[4], st));
-        FoldParams F;
+        FoldParams F{};
         F.partials = partials; F.nslots = plan->nslots; F.nstrips = Lo.nstrips; F.m = mr; F.n = n;
         F.s = s; F.method = method; F.prec = prec; F.L = L; F.slotinfo = plan->d_slotinfo;
         F.eA = eA + r0; F.eB = eB; F.Cre = dmo(Cg.re); F.Cim = dmo(Cg.im);
@@ -722,6 +717,149 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     }
     if (E) CK(cudaEventRecord(E->ev[5], st));
     if (rep) rep->kernel_launches += launches;
+    return 0;
+}
+
+// ---------------------------------------------------------------- device-rule mode
+// Candidate plans for every s the device rule can pick without needing more than planned: the
+// rule's s at log2 rho-hat = 0 (the smallest) .. at minT = 1 (the largest first-stage s).
+struct DevPlanSet {
+    DevPlan *d_plans = nullptr;          // [s_hi - s_lo + 1]
+    int32_t *d_counter = nullptr;        // the shared unit counter
+    int s_lo = 0, s_hi = 0;
+    int64_t nslots_max = 0;
+    size_t main_bytes = 0;               // workspace of the largest candidate
+};
+std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int, int, int>, DevPlanSet> g_devplans;
+
+int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int method, cudaStream_t st,
+                 DevPlanSet **out) {
+    const int s_lo = rule_slices(prec, method, 0.0);
+    const int s_hi = rule_slices(prec, method, rule_log2rho(k, 1, 1, -1));
+    if (s_lo < 0 || s_hi < 0) return fail(MPCGEMM_ERR_SLICES, "device rule: slice range above 1024");
+    auto key = std::make_tuple(dev, m, n, k, method, s_lo, s_hi, env_int("MPCGEMM_ORDER", 1));
+    auto it = g_devplans.find(key);
+    if (it != g_devplans.end()) { *out = &it->second; return 0; }
+    DevPlanSet S;
+    S.s_lo = s_lo; S.s_hi = s_hi;
+    std::vector<DevPlan> hp;
+    for (int s = s_lo; s <= s_hi; s++) {
+        const Geometry geo = main_geometry(dev, m, n, k, s, method);
+        PlanKey key2{m, n, k, s, method, geo.BM, geo.BN, geo.grid, 0, geo.maxkb, g2_enabled() ? 1 : 0,
+                     env_int("MPCGEMM_ORDER", 1), {}};
+        Plan *plan;
+        if (int rc = build_plan(dev, key2, &plan, st)) return rc;
+        hp.push_back(DevPlan{plan->d_units, plan->d_counter + 1, plan->d_slotinfo, s, plan->nunits, plan->nslots, 0});
+        S.nslots_max = std::max<int64_t>(S.nslots_max, plan->nslots);
+        S.main_bytes = std::max(S.main_bytes, layout_for(m, n, k, s, method, geo.maxkb, prec, false).main);
+    }
+    if (cudaMalloc(&S.d_plans, sizeof(DevPlan) * hp.size()) != cudaSuccess ||
+        cudaMalloc(&S.d_counter, sizeof(int32_t)) != cudaSuccess)
+        return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc device plans");
+    CK(cudaMemcpyAsync(S.d_plans, hp.data(), sizeof(DevPlan) * hp.size(), cudaMemcpyHostToDevice, st));
+    *out = &g_devplans.emplace(key, S).first->second;
+    return 0;
+}
+
+// the device-rule hot path: pre-pass, stage 2 (device-gated), rule kernel, then split / slice GEMM
+// / fold reading the chosen plan from device memory -- no host synchronisation anywhere
+int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
+                    mpc_cmat *C, int method, cudaStream_t st, uint8_t *meta, DevCache &dc, const mpcgemm_opts *opts,
+                    mpcgemm_report *rep) {
+    const int L = (prec + 63) / 64;
+    const MetaView mv = meta_view(meta, m, n);
+    DevPlanSet *S;
+    if (int rc = dev_plan_set(dev, m, n, k, prec, method, st, &S)) return rc;
+    const int s_hi = S->s_hi;
+    const Layout Lo = layout_for(m, n, k, 0, method, kMaxKBlocksPerChunk);
+    // workspace: pre-pass area and the largest candidate's main area share the cache (pre-pass first)
+    const size_t need = std::max(Lo.pre, S->main_bytes);
+    uint8_t *big;
+    if (opts && opts->workspace) {
+        if (opts->workspace_bytes < need) return fail(MPCGEMM_ERR_NOMEM, "caller workspace too small");
+        big = (uint8_t *)opts->workspace;
+    } else {
+        if (int rc = grow(&dc.ws, &dc.ws_bytes, need)) return rc;
+        big = (uint8_t *)dc.ws;
+    }
+    // ---- a-2 pre-pass on the device (as run_prepass, without the readback)
+    int8_t *tA = (int8_t *)big, *tB = tA + m * Lo.kp;
+    int32_t *relA = (int32_t *)(big + align_up((size_t)(m + n) * Lo.kp, 256)), *relB = relA + m * Lo.kp;
+    int32_t *T = (int32_t *)(big + align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256));
+    {
+        Nvtx r("mpcgemm.a2_prepass_device_rule");
+        CK(prepass_planes2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, Lo.kp, L, mv.eA, mv.eB, tA, relA,
+                                  tB, relB, st));
+        PlanKey key{m, n, k, 1, 0, 128, tile_bn(n), sm_count(dev), 0, (int)kMaxKBlocksPerChunk, 0, 0, {}};
+        Plan *plan;
+        if (int rc = build_plan(dev, key, &plan, st)) return rc;
+        SliceGemmLaunch SL;
+        memset(&SL, 0, sizeof(SL));
+        SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
+        SL.P.partials = T; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
+        SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = 1; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
+        SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
+        SL.P.partsA = SL.P.partsB = 1;
+        for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
+        SL.digA = tA; SL.digB = tB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
+        SL.grid = plan->grid; SL.BM = 128; SL.BN = tile_bn(n); SL.simt = 0; SL.nunits = plan->nunits;
+        SL.units_flat = plan->d_units;
+        CK(slicegemm_launch(SL, st));
+        const int64_t nb = nblocks(m);
+        CK(cudaMemsetAsync(mv.omin, 0xFF, 8 * 3 * nb, st));
+        CK(cudaMemsetAsync(mv.dmin2, 0xFF, 8 * 3 * nb, st));
+        CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 1,
+                                 mv.omin, mv.omin1, mv.omax2, st));
+        CK(prepass_rule_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, mv.omin,
+                               mv.dmin2, mv.dmin12, mv.dmax22, prec, method, S->d_plans, S->s_lo, s_hi, mv.drs, st));
+    }
+    // ---- a-3..a-6 with the chosen plan (the workspace laid out for the largest candidate)
+    const int parts = method == 3 ? 3 : 2;
+    int8_t *digA = (int8_t *)big;
+    int8_t *digB = digA + align_up((size_t)parts * s_hi * m * Lo.kp, 256);
+    int32_t *partials = (int32_t *)((uint8_t *)digB + align_up((size_t)parts * s_hi * n * Lo.kp, 256));
+    uint64_t *fix = (uint64_t *)((uint8_t *)partials +
+                                 align_up((size_t)S->nslots_max * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
+    {
+        Nvtx r("mpcgemm.a3_split");
+        CK(split_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, mv.eB, s_hi, parts, digB, st, mv.drs));
+        CK(split_launch(dm(A->re), dm(A->im), 0, m, k, Lo.kp, L, mv.eA, s_hi, parts, digA, st, mv.drs));
+    }
+    const Geometry geo = main_geometry(dev, m, n, k, s_hi, method);
+    SliceGemmLaunch SL;
+    memset(&SL, 0, sizeof(SL));
+    Plan Pj;
+    method_jobs(method, Pj);
+    SL.P.counter = S->d_counter; SL.P.partials = partials; SL.P.nstrips = Lo.nstrips;
+    SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = s_hi; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
+    SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
+    SL.P.partsA = SL.P.partsB = parts;
+    SL.P.pblk = env_int("MPCGEMM_PBLK", 32);
+    SL.P.drs = mv.drs;
+    for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = Pj.jobs[q];
+    SL.digA = digA; SL.digB = digB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
+    SL.grid = geo.BM == 256 ? (geo.grid & ~1) : geo.grid; SL.BM = geo.BM; SL.BN = geo.BN; SL.simt = 0;
+    {
+        Nvtx r("mpcgemm.a4_slicegemm");
+        CK(slicegemm_launch(SL, st));
+    }
+    FoldParams F{};
+    F.partials = partials; F.nstrips = Lo.nstrips; F.m = m; F.n = n;
+    F.s = s_hi; F.method = method; F.prec = prec; F.L = L;
+    F.eA = mv.eA; F.eB = mv.eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
+    F.beta = 0; F.alpha_neg = 0; F.C0re = dm(C->re); F.C0im = dm(C->im);
+    F.ldF = (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign;
+    F.fix = fix; F.drs = mv.drs;
+    {
+        Nvtx r("mpcgemm.a5a6_fold_normalize");
+        CK(fold_normalize_launch(F, st));
+    }
+    if (rep) {
+        rep->slices = 0;                                 // chosen on the device: mpcgemm_device_rule_result()
+        rep->kernel_launches += 9;                      // planes, T GEMM, min, max-plus, rule, split x2, GEMM, fold
+        rep->slicegemm_ctas = SL.grid; rep->tile_m = geo.BM; rep->tile_n = geo.BN;
+        rep->certified = 1;
+    }
     return 0;
 }
 
@@ -771,16 +909,22 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     if (validate) CK(cudaMemsetAsync(errflag, 0, 4, st));
     {
         Nvtx r("mpcgemm.a1_linemax");
-        CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, eA, nzA, errflag, validate, st));
-        CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, eB, nzB, errflag, validate, st));
+        CK(linemax2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, L, prec, eA, nzA, errflag, validate, st));
+        (void)eB; (void)nzB;                          // (eB = eA + m, nzB = nzA + m)
     }
     if (E) CK(cudaEventRecord(E->ev[1], st));
-    int launches = 4 + (validate ? 1 : 0);             // linemax + finalize, A and B [, flag readback]
+    int launches = 2 + (validate ? 1 : 0);             // linemax (A and B) + finalize [, flag readback]
     if (validate) {
         uint32_t h = 0;
         if (int rc = readback(dev, &h, errflag, 4, st)) return rc;
         if (h & 2u) return fail(MPCGEMM_ERR_EXP_RANGE, "|exp| > 2^61");
         if (h & 1u) return fail(MPCGEMM_ERR_NOT_NORMALIZED, "mantissa not normalized");
+    }
+    const bool devrule = opts && opts->device_rule && !forced && !adaptive && carrier == 0 && !simt && !validate &&
+                         !beta && !alpha_neg && group_rows == 0 && !hook;
+    if (devrule) {
+        if (rep) rep->kernel_launches = launches;
+        return run_device_rule(dev, m, n, k, prec, A, B, C, method, st, meta, dc, opts, rep);
     }
     int s = forced;
     int64_t pb[3] = {-1, -1, -1};
@@ -792,7 +936,7 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         Nvtx range_pre("mpcgemm.a2_prepass");
         if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, &bd)) return rc;
         for (int q = 0; q < 3; q++) pb[q] = bd.g[q];
-        launches += 5 + (pb[0] == 0 ? 2 : 0);         // planes x2, T GEMM, min, readback [, max-plus, readback]
+        launches += 4 + (pb[0] == 0 ? 2 : 0);         // planes, T GEMM, min, readback [, max-plus, readback]
         log2rho = rule_log2rho(k, pb[0], pb[1], pb[2]);
         s = rule_slices(prec, method, log2rho, bits);
         if (s < 0) return fail(MPCGEMM_ERR_SLICES, "slice rule needs s > 1024");
@@ -1050,8 +1194,7 @@ int mpcgemm_rho_bounds(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_
     if (int rc = grow(&dc.ws, &dc.ws_bytes, Lo.pre)) return rc;
     uint8_t *meta = (uint8_t *)dc.meta;
     const MetaView mv = meta_view(meta, m, n);
-    CK(linemax_launch(dm(A->re), dm(A->im), m, k, L, prec, 0, mv.eA, mv.nzA, nullptr, 0, st));
-    CK(linemax_launch(dm(B->re), dm(B->im), k, n, L, prec, 1, mv.eB, mv.nzB, nullptr, 0, st));
+    CK(linemax2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, L, prec, mv.eA, mv.nzA, nullptr, 0, st));
     Bounds bd;
     if (int rc = run_prepass(dev, m, n, k, prec, A, B, full, st, meta, (uint8_t *)dc.ws, Lo,
                              env_int("MPCGEMM_SLICEGEMM_SIMT", 0), &bd))
@@ -1216,6 +1359,21 @@ int mpcgemm_host_wait(void) {
     return 0;
 }
 
+int mpcgemm_device_rule_result(int64_t m, int64_t n, void *stream, int64_t out[4]) {
+    if (!out) return fail(MPCGEMM_ERR_ARG, "null out");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaStream_t st = (cudaStream_t)stream;
+    std::lock_guard<std::mutex> lock(g_mu);
+    DevCache &dc = g_cache[dev];
+    if (!dc.meta || dc.meta_bytes < meta_bytes(m, n)) return fail(MPCGEMM_ERR_ARG, "no device-rule call of this shape");
+    const MetaView mv = meta_view((uint8_t *)dc.meta, m, n);
+    DevRuleState h;
+    if (int rc = readback(dev, &h, mv.drs, sizeof(h), st)) return rc;
+    out[0] = h.s_needed; out[1] = h.minT; out[2] = h.minT1; out[3] = h.maxD2;
+    return h.status;
+}
+
 const char *mpcgemm_strerror(int code) {
     switch (code) {
         case MPCGEMM_OK: return "ok";
@@ -1247,6 +1405,10 @@ void mpcgemm_release(void) {
         cudaFree(it->second.mma_dev);
         if (it->second.rb) cudaFreeHost(it->second.rb);
         g_cache.erase(it);
+    }
+    for (auto p = g_devplans.begin(); p != g_devplans.end();) {
+        if (std::get<0>(p->first) == dev) { cudaFree(p->second.d_plans); cudaFree(p->second.d_counter); p = g_devplans.erase(p); }
+        else ++p;
     }
     for (auto p = g_plans.begin(); p != g_plans.end();) {
         if (p->first.first == dev) {

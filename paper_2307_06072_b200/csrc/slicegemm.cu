@@ -82,6 +82,11 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     uint8_t *skk = reinterpret_cast<uint8_t *>(tmem_slot + 1);   // per stage: MMA K-steps to issue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (P.drs && P.drs->status != 0) return;          // device rule: s outside the planned range
+    const DevPlan *dp = P.drs ? &P.drs->cur : nullptr;
+    const WorkUnit *units = dp ? dp->units : P.units;
+    const int nunits = dp ? dp->nunits : P.nunits;
+    const int64_t nslots = dp ? dp->nslots : P.nslots;
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
         mbar_init(tfull, 1);
@@ -97,7 +102,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int s = P.s, KB = P.KB;
+    const int s = dp ? dp->s : P.s, KB = P.KB;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -116,13 +121,13 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             };
             for (;;) {
                 int u = atomicAdd(P.counter, 1);
-                if (u >= P.nunits) u = -1;
+                if (u >= nunits) u = -1;
                 mbar_wait(&qempty[qs], qph ^ 1);
                 *reinterpret_cast<volatile int32_t *>(&uq[qs]) = u;
                 mbar_arrive(&qfull[qs]);
                 if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
                 if (u < 0) break;
-                const WorkUnit w = P.units[u];
+                const WorkUnit w = units[u];
                 const JobDesc &J = P.jobs[unit_job(w)];
                 if (unit_G(w) == 2) {
                     for (int pr = 0; pr < J.npairs; pr++)
@@ -162,7 +167,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 mbar_arrive(&qempty[qs]);
                 if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
                 if (u < 0) { if (P.mma_count) atomicAdd(P.mma_count, (unsigned long long)nmma); break; }
-                const WorkUnit w = P.units[u];
+                const WorkUnit w = units[u];
                 const JobDesc &J = P.jobs[unit_job(w)];
                 mbar_wait(tempty, tphase ^ 1);
                 tc_fence_after();
@@ -217,7 +222,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             if (lane == 0) mbar_arrive(&qempty[qs]);
             if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
             if (u < 0) break;
-            const WorkUnit w = P.units[u];
+            const WorkUnit w = units[u];
             mbar_wait(tfull, tphase);
             tc_fence_after();
             const int row = w.tm * kBM + q * 32 + lane;
@@ -230,7 +235,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                     tmem_ld_wait();
                     const int col0 = w.tn * BN + c * 32;      // 32 columns inside one 256-column strip
                     if (row < P.m) {
-                        int32_t *out = P.partials + part_off(row, col0, slot, P.nslots, P.nstrips);
+                        int32_t *out = P.partials + part_off(row, col0, slot, nslots, P.nstrips);
 #pragma unroll
                         for (int g4 = 0; g4 < 8; g4++)
                             st_global_v4_hint(out + 4 * g4, (int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2],
@@ -288,6 +293,12 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     uint8_t *skk = reinterpret_cast<uint8_t *>(tmem_slot + 1);   // per stage: MMA K-steps to issue
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (P.drs && P.drs->status != 0) return;          // device rule: s outside the planned range
+    const DevPlan *dp = P.drs ? &P.drs->cur : nullptr;
+    const WorkUnit *units = dp ? dp->units : P.units;
+    const int nunits = dp ? dp->nunits : P.nunits;
+    const int64_t nslots = dp ? dp->nslots : P.nslots;
+    int32_t *const hot = dp ? dp->hot : P.hot;
     const uint32_t rank = cluster_ctarank();
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -308,7 +319,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const uint32_t peer_uq = mapa_rank(smem_u32(uq), 1);
     const uint32_t peer_uqr = mapa_rank(smem_u32(uqr), 1);
     const uint32_t peer_qfull = mapa_rank(smem_u32(qfull), 1);
-    const int s = P.s, KB = P.KB;
+    const int s = dp ? dp->s : P.s, KB = P.KB;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -337,16 +348,16 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 int u, rot = 0;
                 if (rank == 0) {
                     u = atomicAdd(P.counter, 1);
-                    if (u >= P.nunits) u = -1;
-                    if (u >= 0 && P.hot) {
+                    if (u >= nunits) u = -1;
+                    if (u >= 0 && hot) {
                         // k-phase alignment: begin at the (pair, k-block) position the group's
                         // running units are on, so the units sharing a digit-plane tile read it
                         // within one k-block step of each other (an L2 hit) whatever their start
-                        const WorkUnit &wu = P.units[u];
+                        const WorkUnit &wu = units[u];
                         if (unit_G(wu) >= 2) {
                             const int nkb = wu.b - wu.a;
                             const int npos = P.jobs[unit_job(wu)].npairs * unit_nblk(unit_G(wu) == 2 ? wu.r : wu.r - 1, P.pblk) * nkb;
-                            const int h = ld_relaxed_s32(P.hot + wu.slot0);
+                            const int h = ld_relaxed_s32(hot + wu.slot0);
                             rot = (h > 0 && h < npos) ? h : 0;
                         }
                     }
@@ -365,7 +376,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 }
                 if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
                 if (u < 0) break;
-                const WorkUnit w = P.units[u];
+                const WorkUnit w = units[u];
                 const JobDesc &J = P.jobs[unit_job(w)];
                 if (unit_G(w) >= 2) {
                     // positions (pair, p-block, k-block), t = 0 .. npos - 1 taken from rot on; D_r and
@@ -379,7 +390,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         const int pb = pos / nkb, pr = pb / nblk, blk = pb - pr * nblk;
                         const int kb = unit_kb(w, pos - pb * nkb);
                         const int p0 = unit_pfirst(np, nblk, blk), p1 = unit_pfirst(np, nblk, blk + 1) - 1;
-                        if (rank == 0 && P.hot) st_relaxed_s32(P.hot + w.slot0, pos);
+                        if (rank == 0 && hot) st_relaxed_s32(hot + w.slot0, pos);
                         if (g2 && p0 > 1) load(J.pa[pr] * s + p0 - 2, 0, kb, w.tm, w.tn, true);   // A_{p0-1} only
                         for (int p = p0; p <= p1; p++)
                             load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1 + g2), kb, w.tm, w.tn);
@@ -414,7 +425,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 mbar_arrive(&qempty[qs]);
                 if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
                 if (u < 0) { if (P.mma_count) atomicAdd(P.mma_count, (unsigned long long)nmma); break; }
-                const WorkUnit w = P.units[u];
+                const WorkUnit w = units[u];
                 const JobDesc &J = P.jobs[unit_job(w)];
                 mbar_wait_cluster(tempty, tphase ^ 1);
                 tc_fence_after();
@@ -487,7 +498,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             }
             if (++qs == Cfg::QN) { qs = 0; qph ^= 1; }
             if (u < 0) break;
-            const WorkUnit w = P.units[u];
+            const WorkUnit w = units[u];
             mbar_wait(tfull, tphase);
             tc_fence_after();
             const int row = (P.dbg & 1) ? P.m : w.tm * 256 + (int)rank * 128 + q * 32 + lane;
@@ -500,7 +511,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     tmem_ld_wait();
                     const int col0 = w.tn * BN + c * 32;
                     if (row < P.m) {
-                        int32_t *out = P.partials + part_off(row, col0, slot, P.nslots, P.nstrips);
+                        int32_t *out = P.partials + part_off(row, col0, slot, nslots, P.nstrips);
 #pragma unroll
                         for (int g4 = 0; g4 < 8; g4++)
                             st_global_v4_hint(out + 4 * g4, (int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2],

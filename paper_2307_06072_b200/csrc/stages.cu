@@ -4,11 +4,13 @@
 //   a-3 split            error-free split into balanced radix-256 digit planes
 //   a-5/a-6 fold_normalize  exact fold of the slice products with the Eq. 5/6
 //                        combination, carry propagation and one RNE rounding
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cuda.h>
 #include "common.cuh"
 #include "kernels.h"
+#include "rule.cuh"
 
 namespace mpc {
 
@@ -32,15 +34,16 @@ MPC_DEV uint64_t bits64(const uint64_t *a, int n, int64_t pos) {
 // ================================================================== a-1: exponent scan
 MPC_DEV uint64_t enc_exp(int64_t e) { return (uint64_t)e ^ 0x8000000000000000ull; }   // order-preserving
 
-__global__ void linemax_kernel(DMat re, DMat im, int64_t rows, int64_t cols, int L, int prec, int side,
-                               unsigned long long *emax, uint32_t *errflag, int validate)
+// block (bx, by) of a (., gy) grid over one side
+MPC_DEV void linemax_body(const DMat &re, const DMat &im, int64_t rows, int64_t cols, int L, int prec, int side,
+                          unsigned long long *emax, uint32_t *errflag, int validate, int64_t bx, int64_t by, int64_t gy)
 {
     __shared__ unsigned long long red[8][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int64_t c = (int64_t)blockIdx.x * 32 + tx;
+    const int64_t c = bx * 32 + tx;
     unsigned long long colmax = 0;
     const uint64_t lowmask = (64 * L - prec) ? ((1ull << (64 * L - prec)) - 1) : 0ull;
-    for (int64_t r = (int64_t)blockIdx.y * 8 + ty; r < rows; r += (int64_t)gridDim.y * 8) {
+    for (int64_t r = by * 8 + ty; r < rows; r += gy * 8) {
         unsigned long long v = 0;
         if (c < cols) {
 #pragma unroll
@@ -87,6 +90,25 @@ __global__ void linemax_kernel(DMat re, DMat im, int64_t rows, int64_t cols, int
     }
 }
 
+__global__ void linemax_kernel(DMat re, DMat im, int64_t rows, int64_t cols, int L, int prec, int side,
+                               unsigned long long *emax, uint32_t *errflag, int validate)
+{
+    linemax_body(re, im, rows, cols, L, prec, side, emax, errflag, validate, blockIdx.x, blockIdx.y, gridDim.y);
+}
+
+// both sides in one launch: blocks [0, gx0*gy0) scan the rows of A, the rest the columns of B
+__global__ void linemax2_kernel(DMat re0, DMat im0, int64_t rows0, int64_t cols0, DMat re1, DMat im1, int64_t rows1,
+                                int64_t cols1, int L, int prec, unsigned long long *emax0, unsigned long long *emax1,
+                                uint32_t *errflag, int validate, int64_t gx0, int64_t gy0, int64_t gx1, int64_t gy1)
+{
+    const int64_t b = blockIdx.x;
+    if (b < gx0 * gy0) linemax_body(re0, im0, rows0, cols0, L, prec, 0, emax0, errflag, validate, b % gx0, b / gx0, gy0);
+    else {
+        const int64_t c = b - gx0 * gy0;
+        linemax_body(re1, im1, rows1, cols1, L, prec, 1, emax1, errflag, validate, c % gx1, c / gx1, gy1);
+    }
+}
+
 __global__ void linemax_finalize_kernel(unsigned long long *emax, int64_t n, int64_t *eline, uint8_t *nz) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -113,6 +135,27 @@ cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, 
         linemax_kernel<<<grid, block, 0, st>>>(re, im, rows, cols, L, prec, side, acc, errflag, validate);
     }
     linemax_finalize_kernel<<<(unsigned)((lines + 255) / 256), 256, 0, st>>>(acc, lines, eline, nz);
+    return cudaGetLastError();
+}
+
+// a-1 for A (rows) and B (columns) together: one accumulator memset (eA, eB contiguous), one scan
+// launch, one finalize launch (nz and eline of both sides contiguous too)
+cudaError_t linemax2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int L, int prec,
+                            int64_t *eAB, uint8_t *nzAB, uint32_t *errflag, int validate, cudaStream_t st)
+{
+    if (m + n == 0) return cudaSuccess;
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(eAB);
+    cudaError_t e = cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * (m + n), st);
+    if (e != cudaSuccess) return e;
+    if (k > 0) {
+        const int64_t gx0 = m > 0 ? (k + 31) / 32 : 0, gy0 = std::min<int64_t>((m + 7) / 8, 65535);
+        const int64_t gx1 = n > 0 ? (n + 31) / 32 : 0, gy1 = std::min<int64_t>((k + 7) / 8, 64);
+        const int64_t blocks = gx0 * gy0 + gx1 * gy1;
+        if (blocks > 0)
+            linemax2_kernel<<<(unsigned)blocks, dim3(32, 8), 0, st>>>(Are, Aim, m, k, Bre, Bim, k, n, L, prec, acc, acc + m,
+                                                                      errflag, validate, gx0, gy0, gx1, gy1);
+    }
+    linemax_finalize_kernel<<<(unsigned)((m + n + 255) / 256), 256, 0, st>>>(acc, m + n, eAB, nzAB);
     return cudaGetLastError();
 }
 
@@ -150,8 +193,9 @@ constexpr uint64_t kH = 0x8080808080808080ull;
 
 __global__ void __launch_bounds__(128, 4)
 split_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
-             const int64_t *__restrict__ eline, int s, int nparts, int8_t *__restrict__ dig)
+             const int64_t *__restrict__ eline, int s, int nparts, int8_t *__restrict__ dig, const DevRuleState *drs)
 {
+    if (drs) { if (drs->status) return; s = drs->cur.s; }    // device rule: the chosen s
     const int64_t kk0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kSplitVec;
     if (kk0 >= kp) return;
     const int64_t plane = lines * kp;
@@ -242,8 +286,9 @@ template <int L>
 __global__ void __launch_bounds__(kSplitT)
 split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant__ CUtensorMap mim, DMat re, DMat im,
                  int side, int64_t lines, int64_t k, int64_t kp, const int64_t *__restrict__ eline, int s, int nparts,
-                 int8_t *__restrict__ dig)
+                 int8_t *__restrict__ dig, const DevRuleState *drs)
 {
+    if (drs) { if (drs->status) return; s = drs->cur.s; }    // device rule: the chosen s
     extern __shared__ uint8_t tsm_raw[];
     uint8_t *tile = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
     constexpr int ROW = 8 * L;                        // bytes per entry row
@@ -378,7 +423,8 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
 
 template <int L>
 static cudaError_t split_tma_launch_t(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp,
-                                      const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st)
+                                      const int64_t *eline, int s, int nparts, int8_t *dig, const DevRuleState *drs,
+                                      cudaStream_t st)
 {
     alignas(64) uint8_t mre[128], mim[128];           // CUtensorMap storage
     for (int p = 0; p < 2; p++) {
@@ -396,27 +442,27 @@ static cudaError_t split_tma_launch_t(DMat re, DMat im, int side, int64_t lines,
     dim3 grid((unsigned)((kp + kSplitT - 1) / kSplitT), (unsigned)lines);
     split_tma_kernel<L><<<grid, kSplitT, sm, st>>>(*reinterpret_cast<const CUtensorMap *>(mre),
                                                    *reinterpret_cast<const CUtensorMap *>(mim), re, im, side, lines, k, kp,
-                                                   eline, s, nparts, dig);
+                                                   eline, s, nparts, dig, drs);
     return cudaGetLastError();
 }
 
 cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
-                         const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st)
+                         const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st, const DevRuleState *drs)
 {
     if (lines == 0 || kp == 0) return cudaSuccess;
     const bool tma_ok = lines < 65536 && getenv("MPCGEMM_SPLIT_V1") == nullptr &&
                         !(reinterpret_cast<uintptr_t>(re.limbs) & 15) && !(reinterpret_cast<uintptr_t>(im.limbs) & 15);
     if (tma_ok) {
         cudaError_t e = cudaErrorNotSupported;
-        if (L == 16) e = split_tma_launch_t<16>(re, im, side, lines, k, kp, eline, s, nparts, dig, st);
-        else if (L == 8) e = split_tma_launch_t<8>(re, im, side, lines, k, kp, eline, s, nparts, dig, st);
-        else if (L == 4) e = split_tma_launch_t<4>(re, im, side, lines, k, kp, eline, s, nparts, dig, st);
-        else if (L == 2) e = split_tma_launch_t<2>(re, im, side, lines, k, kp, eline, s, nparts, dig, st);
+        if (L == 16) e = split_tma_launch_t<16>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
+        else if (L == 8) e = split_tma_launch_t<8>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
+        else if (L == 4) e = split_tma_launch_t<4>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
+        else if (L == 2) e = split_tma_launch_t<2>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
     }
     const int64_t threads = (kp + kSplitVec - 1) / kSplitVec;
     dim3 grid((unsigned)((threads + 127) / 128), (unsigned)(lines < 65535 ? lines : 65535));
-    split_kernel<<<grid, 128, 0, st>>>(re, im, side, lines, k, kp, L, eline, s, nparts, dig);
+    split_kernel<<<grid, 128, 0, st>>>(re, im, side, lines, k, kp, L, eline, s, nparts, dig, drs);
     return cudaGetLastError();
 }
 
@@ -427,12 +473,13 @@ cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, i
 constexpr int32_t kRelSentinel = -(1 << 30);
 constexpr int32_t kRelClamp = -(1 << 28);
 
-__global__ void prepass_planes_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
-                                      const int64_t *__restrict__ eline, int8_t *t, int32_t *rel)
+MPC_DEV void prepass_planes_body(const DMat &re, const DMat &im, int side, int64_t lines, int64_t k, int64_t kp, int L,
+                                 const int64_t *__restrict__ eline, int8_t *t, int32_t *rel, int64_t bx, int64_t by,
+                                 int64_t gy)
 {
-    const int64_t kk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t kk = bx * blockDim.x + threadIdx.x;
     if (kk >= kp) return;
-    for (int64_t line = blockIdx.y; line < lines; line += gridDim.y) {
+    for (int64_t line = by; line < lines; line += gy) {
         int best = 0;
         int64_t emax = 0; bool any = false;
         if (kk < k) {
@@ -469,6 +516,35 @@ __global__ void prepass_planes_kernel(DMat re, DMat im, int side, int64_t lines,
         }
         rel[line * kp + kk] = r;
     }
+}
+
+__global__ void prepass_planes_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
+                                      const int64_t *__restrict__ eline, int8_t *t, int32_t *rel)
+{
+    prepass_planes_body(re, im, side, lines, k, kp, L, eline, t, rel, blockIdx.x, blockIdx.y, gridDim.y);
+}
+
+__global__ void prepass_planes2_kernel(DMat re0, DMat im0, int64_t lines0, const int64_t *eline0, int8_t *t0, int32_t *rel0,
+                                       DMat re1, DMat im1, int64_t lines1, const int64_t *eline1, int8_t *t1, int32_t *rel1,
+                                       int64_t k, int64_t kp, int L, int64_t gx, int64_t gy0, int64_t gy1)
+{
+    const int64_t b = blockIdx.x;
+    if (b < gx * gy0) prepass_planes_body(re0, im0, 0, lines0, k, kp, L, eline0, t0, rel0, b % gx, b / gx, gy0);
+    else {
+        const int64_t c = b - gx * gy0;
+        prepass_planes_body(re1, im1, 1, lines1, k, kp, L, eline1, t1, rel1, c % gx, c / gx, gy1);
+    }
+}
+
+cudaError_t prepass_planes2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp,
+                                   int L, const int64_t *eA, const int64_t *eB, int8_t *tA, int32_t *relA, int8_t *tB,
+                                   int32_t *relB, cudaStream_t st)
+{
+    if (kp == 0 || m + n == 0) return cudaSuccess;
+    const int64_t gx = (kp + 127) / 128, gy0 = std::min<int64_t>(m, 32768), gy1 = std::min<int64_t>(n, 32768);
+    prepass_planes2_kernel<<<(unsigned)(gx * (gy0 + gy1)), 128, 0, st>>>(Are, Aim, m, eA, tA, relA, Bre, Bim, n, eB, tB, relB,
+                                                                       k, kp, L, gx, gy0, gy1);
+    return cudaGetLastError();
 }
 
 cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
@@ -522,9 +598,15 @@ __global__ void __launch_bounds__(256)
 prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
                        int64_t k, int64_t kp, const uint8_t *nzA, const uint8_t *nzB,
                        const int32_t *relA, const int32_t *relB,
-                       unsigned long long *out_min, unsigned long long *out_min1, long long *out_max2)
+                       unsigned long long *out_min, unsigned long long *out_min1, long long *out_max2,
+                       const unsigned long long *gate = nullptr, int64_t ngate = 0)
 {
     __shared__ int32_t sa[32][33], sb[32][33];
+    if (gate) {                                       // device rule: run only if a block's stage-1 min is 0
+        int z = 0;
+        for (int64_t b = threadIdx.x; b < ngate; b += blockDim.x) z |= gate[b] == 0;
+        if (!__syncthreads_or(z)) return;
+    }
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;    // 32 x 8
     const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
     int32_t mp[4] = {kRelSentinel, kRelSentinel, kRelSentinel, kRelSentinel};
@@ -583,6 +665,71 @@ cudaError_t readback_launch(void *dst_mapped, const void *src, size_t bytes, cud
     if (n == 0) return cudaSuccess;
     readback_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 64), 256, 0, st>>>((uint32_t *)dst_mapped,
                                                                                       (const uint32_t *)src, n);
+    return cudaGetLastError();
+}
+
+// device rule: the host path's reduction over 256-row blocks and slice rule (mpcgemm.cu
+// run_prepass / gemm_impl; rule.cuh), one warp; picks the candidate plan of the certified s
+__global__ void rule_kernel(const unsigned long long *min1, const unsigned long long *min2,
+                            const unsigned long long *min12, const long long *max22, int64_t nb, int64_t k, int prec,
+                            int method, const DevPlan *plans, int s_lo, int s_hi, DevRuleState *drs)
+{
+    if (blockIdx.x) return;
+    // lanes test 32 consecutive candidate s at a time from s_lo - 1 on, with rule_slices' predicate
+    // (the rule at log2 rho-hat >= 0 cannot pick below s_lo), then lane 0 finishes
+    __shared__ double lr_sh;
+    if (threadIdx.x == 0) {
+    bool any0 = false;
+    for (int64_t b = 0; b < nb; b++) any0 = any0 || min1[b] == 0;
+    int64_t g0 = -1, g1 = -1, g2 = -1;
+    for (int64_t b = 0; b < nb; b++) {
+        int64_t t0, t1, t2;
+        if (!any0) { t0 = min1[b] == ULLONG_MAX ? -1 : (int64_t)min1[b]; t1 = t0; t2 = -1; }
+        else {
+            t0 = min2[b] == ULLONG_MAX ? -1 : (int64_t)min2[b];
+            t1 = min12[b] == ULLONG_MAX ? -1 : (int64_t)min12[b];
+            t2 = (int64_t)max22[b];
+        }
+        if (t0 >= 0 && (g0 < 0 || t0 < g0)) g0 = t0;
+        if (t1 >= 0 && (g1 < 0 || t1 < g1)) g1 = t1;
+        if (t2 > g2) g2 = t2;
+    }
+    if (g0 < 0) { g1 = g2 = -1; }
+    else if (g0 > 0) { g1 = g0; g2 = -1; }
+    lr_sh = rule_log2rho(k, g0, g1, g2);
+    drs->minT = g0; drs->minT1 = g1; drs->maxD2 = g2;
+    }
+    __syncwarp();
+    const double lr = lr_sh;
+    const double c = method == 3 ? 4.0 : 3.0;
+    int sv = -8;
+    for (int base = max(1, s_lo - 1); base <= kMaxSlices; base += 32) {
+        const int cand = base + (int)threadIdx.x;
+        const bool ok = cand <= kMaxSlices && 8.0 * cand >= (double)prec - 4.0 + log2(c * cand) + lr + 0.1;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (bal) { sv = base + __ffs(bal) - 1; break; }
+    }
+    if (threadIdx.x) return;
+    drs->s_needed = sv;
+    if (sv >= s_lo && sv <= s_hi) { drs->cur = plans[sv - s_lo]; drs->status = 0; }
+    else { drs->cur = DevPlan{nullptr, nullptr, nullptr, sv, 0, 0, 0}; drs->status = -8; }
+}
+
+cudaError_t prepass_rule_launch(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n, int64_t k,
+                                int64_t kp, const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA,
+                                const int32_t *relB, const unsigned long long *min1, unsigned long long *min2,
+                                unsigned long long *min12, long long *max22, int prec, int method,
+                                const DevPlan *plans, int s_lo, int s_hi, DevRuleState *drs, cudaStream_t st)
+{
+    const int64_t nb = (m + kSBlk - 1) / kSBlk;
+    if (m > 0 && n > 0) {
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
+        prepass_maxplus_kernel<<<grid, 256, 0, st>>>(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB,
+                                                     min2, min12, max22, min1, nb);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    rule_kernel<<<1, 32, 0, st>>>(min1, min2, min12, max22, nb, k, prec, method, plans, s_lo, s_hi, drs);
     return cudaGetLastError();
 }
 
@@ -859,10 +1006,12 @@ fold_normalize_kernel(const FoldParams F)
 {
     constexpr int NCONS = COLS / EPT;                 // consumer threads
     extern __shared__ __align__(128) uint8_t fsm_raw[];
-    const int s = F.s;
+    if (F.drs && F.drs->status) return;              // device rule: s outside the planned range
+    const int s = F.drs ? F.drs->cur.s : F.s;        // (device rule: the chosen plan's s, slots)
+    const int32_t *const slotinfo = F.drs ? F.drs->cur.slotinfo : F.slotinfo;
     const int Lc0 = s / 8 + 3;                        // fixed-point limbs
     const int Lw = BETA ? Lc0 + F.L + 3 : 0;          // NEXT-2 sum window
-    const int nslots = (int)F.nslots;
+    const int nslots = F.drs ? F.drs->cur.nslots : (int)F.nslots;
     int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                                   // [RING][PER][COLS]
     uint16_t *cntq = reinterpret_cast<uint16_t *>(fsm_raw + RING * kFoldPer * COLS * 4);  // [job][s+2] chunk counts
     uint64_t *full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(cntq + kMaxJobs * (s + 2)) + 15) & ~uintptr_t(15));
@@ -872,7 +1021,7 @@ fold_normalize_kernel(const FoldParams F)
     const int warp = tid >> 5, lane = tid & 31;
     // chunk count of every (job, diagonal): the slots come in the order r = s+1..2, job, chunk
     for (int x = tid; x < kMaxJobs * (s + 2); x += blockDim.x)
-        cntq[x] = (uint16_t)((x % (s + 2)) < 2 ? 0 : F.slotinfo[x * 2 + 1]);
+        cntq[x] = (uint16_t)((x % (s + 2)) < 2 ? 0 : slotinfo[x * 2 + 1]);
     if (tid == 0) {
         for (int e = 0; e < RING; e++) { mbar_init(&full[e], 1); mbar_init(&empty[e], NCONS / 32); }
         fence_barrier_init();
@@ -889,11 +1038,11 @@ fold_normalize_kernel(const FoldParams F)
     // NEXT-4: this row's triangle d = sr <= s; its diagonals r = sr+1 .. 2 are the slots from
     // the first slot of (job 0, r = sr+1) on (slots of larger r are not read)
     const int sr = F.sblk ? F.sblk[i >> kSBlkShift] : s;
-    const int sl0 = sr == s ? 0 : F.slotinfo[(sr + 1) * 2];
+    const int sl0 = sr == s ? 0 : slotinfo[(sr + 1) * 2];
     if (warp == NCONS / 32) {
         // ---------------- producer warp
         if (lane == 0) {
-            const int32_t *region = F.partials + part_off(i, j0, 0, F.nslots, F.nstrips);   // slot 0
+            const int32_t *region = F.partials + part_off(i, j0, 0, nslots, F.nstrips);   // slot 0
             int e = 0; uint32_t ph = 0;
             for (int sl = sl0; sl < nslots; sl += kFoldPer) {
                 const int cnt = nslots - sl < kFoldPer ? nslots - sl : kFoldPer;

@@ -23,7 +23,7 @@ ERRORS = {0: "OK", -1: "ERR_ARG", -2: "ERR_PREC", -3: "ERR_EXP_RANGE", -4: "ERR_
           -5: "ERR_ALIAS", -6: "ERR_NOMEM", -7: "ERR_CUDA", -8: "ERR_SLICES"}
 SYMBOLS = ["mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_host_async", "mpcgemm_host_wait", "mpcgemm_rho_bounds", "mpcgemm_slices_for",
            "mpcgemm_workspace_size", "mpcgemm_strerror", "mpcgemm_last_error", "mpcgemm_release",
-           "mpcgemm_version", "mpclu_factor", "mpclu_solve", "mpc_scalar"]
+           "mpcgemm_version", "mpclu_factor", "mpclu_solve", "mpc_scalar", "mpcgemm_device_rule_result"]
 
 
 class MpcgemmError(RuntimeError):
@@ -45,7 +45,7 @@ class OptsC(ctypes.Structure):
                 ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
                 ("timing", ctypes.c_int32), ("beta", ctypes.c_int32), ("alpha_neg", ctypes.c_int32),
                 ("carrier", ctypes.c_int32), ("adaptive", ctypes.c_int32),
-                ("block_slices", ctypes.c_void_p)]
+                ("block_slices", ctypes.c_void_p), ("device_rule", ctypes.c_int32)]
 
 
 class ReportC(ctypes.Structure):
@@ -91,6 +91,8 @@ def lib():
             L.mpclu_factor.argtypes = [i64, i32, PC, vp, i32, ctypes.c_int, ctypes.POINTER(OptsC), ctypes.POINTER(LuReportC)]
             L.mpclu_solve.argtypes = [i64, i64, i32, PC, vp, PC, ctypes.POINTER(OptsC)]
             L.mpc_scalar.argtypes = [i32, i64, i32, PC, PC, PC, PC, vp, vp]
+            L.mpcgemm_device_rule_result.argtypes = [i64, i64, vp, ctypes.POINTER(ctypes.c_int64)]
+            L.mpcgemm_device_rule_result.restype = ctypes.c_int
             for name in ("mpcgemm", "mpcgemm_ex", "mpcgemm_host", "mpcgemm_host_async", "mpcgemm_host_wait", "mpcgemm_rho_bounds", "mpcgemm_slices_for", "mpcgemm_version",
                          "mpclu_factor", "mpclu_solve", "mpc_scalar"):
                 getattr(L, name).restype = ctypes.c_int
@@ -198,7 +200,7 @@ def _stream_ptr(stream):
 # ------------------------------------------------------------------ the calls (names = ABI)
 def mpcgemm_ex(A: DevCMat, B: DevCMat, C: DevCMat, prec: int, method="3M", slices: int = 0,
                validate: int = 0, stream=None, workspace=None, timing: int = 0, beta: int = 0,
-               alpha_neg: int = 0, carrier: int = 0, adaptive: int = 0) -> dict:
+               alpha_neg: int = 0, carrier: int = 0, adaptive: int = 0, device_rule: int = 0) -> dict:
     """C := beta C + (-1)^alpha_neg A B on the device (stream-ordered).  Returns the report
     (plus "block_slices": the s of each 256-row block)."""
     m, k = A.shape
@@ -210,7 +212,7 @@ def mpcgemm_ex(A: DevCMat, B: DevCMat, C: DevCMat, prec: int, method="3M", slice
     opts = OptsC(_stream_ptr(stream), slices, validate,
                  workspace.data_ptr() if workspace is not None else None,
                  workspace.numel() * workspace.element_size() if workspace is not None else 0, timing, beta,
-                 alpha_neg, carrier, adaptive, ctypes.cast(bs, ctypes.c_void_p))
+                 alpha_neg, carrier, adaptive, ctypes.cast(bs, ctypes.c_void_p), device_rule)
     rep = ReportC()
     a, b, c = A.c(), B.c(), C.c()
     rc = lib().mpcgemm_ex(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), METHODS[method],
@@ -292,6 +294,16 @@ def mpcgemm_rho_bounds(A: DevCMat, B: DevCMat, prec: int, full: int = 0, stream=
     a, b = A.c(), B.c()
     _check(lib().mpcgemm_rho_bounds(m, n, k, prec, ctypes.byref(a), ctypes.byref(b), full, ctypes.byref(opts), out))
     return tuple(int(v) for v in out)
+
+
+def mpcgemm_device_rule_result(m: int, n: int, stream=None):
+    """(status, s, (minT, minT1, maxD2)) of the last device_rule call of shape m x n (synchronizes
+    the stream)."""
+    out = (ctypes.c_int64 * 4)()
+    rc = lib().mpcgemm_device_rule_result(m, n, _stream_ptr(stream), out)
+    if rc < 0 and rc != -8:
+        _check(rc)
+    return rc, int(out[0]), (int(out[1]), int(out[2]), int(out[3]))
 
 
 def mpcgemm_slices_for(prec: int, method, k: int, minT: int, minT1: int, maxD2: int) -> int:
