@@ -185,6 +185,10 @@ class StrongGemm:
         self.r0, self.r1 = row_range(m, self.rank, self.world)
         self.maxr = row_range(m, 0, self.world)[1]
         self.bounds_fn, self.slices_fn, self.compute_fn = bounds_fn, slices_fn, compute_fn
+        # the pre-pass all-reduce on its own communicator: on the bulk one it would queue behind the
+        # next product's B broadcast (one NCCL stream per communicator runs its collectives in order)
+        self.small = (dist.new_group(ranks=list(range(self.world)))
+                      if dist.is_initialized() and self.world > 1 and group is None else group)
         self.gpu = self.device.type == "cuda"
         self.B = [packed_cmat(k, n, prec, self.device) for _ in range(2)] if self.rank != src else None
         self.C = [packed_cmat(self.maxr, n, prec, self.device) for _ in range(2)]
@@ -261,7 +265,7 @@ class StrongGemm:
                 t0 = self._ev()
                 t0.record(cs)
             s, bounds = common_slices(lambda full: self.bounds_fn(A_local, Bj, full), self.slices_fn, self.prec,
-                                      self.method, self.k, device=self.device, group=self.group)
+                                      self.method, self.k, device=self.device, group=self.small)
             rep = self.compute_fn(A_local, Bj, Cv, s) if rows > 0 else {"slices": s}
             rep["bounds"] = bounds
             reps.append(rep)
