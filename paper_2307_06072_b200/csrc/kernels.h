@@ -35,6 +35,10 @@ cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, i
                          const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st,
                          const DevRuleState *drs = nullptr);
 
+// 3-D TMA map over the fold's int32 partial planes (slicegemm.cu): box = one row's 256-column strip
+// of 8 consecutive slots
+int encode_partials_map(void *map, const int32_t *base, int64_t gslots);
+
 // 3-D TMA map over ABI limbs (implemented in slicegemm.cu; map = CUtensorMap*, 64-byte aligned)
 int encode_limb_map(void *map, const uint64_t *base, int L, uint64_t d1, uint64_t d2, uint64_t stride1,
                     uint64_t stride2, int b1, int b2);

@@ -643,6 +643,22 @@ int encode_limb_map(void *map, const uint64_t *base, int L, uint64_t d1, uint64_
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// 3-D map over the int32 partial planes for the fold's producer: dims {256 columns of a strip,
+// 128 rows of a row block, global slot g = (rowblk * nstrips + strip) * nslots + slot}, box
+// {256, 1, 8}: one TMA load brings one row's strip for 8 consecutive slots.  Returns 0 on success.
+int encode_partials_map(void *map, const int32_t *base, int64_t gslots) {
+    auto enc = get_encode();
+    if (!enc) return -1;
+    cuuint64_t dims[3] = {(cuuint64_t)kStrip, (cuuint64_t)kRowBlk, (cuuint64_t)gslots};
+    cuuint64_t strides[2] = {(cuuint64_t)kStrip * 4, (cuuint64_t)kTileElems * 4};
+    cuuint32_t box[3] = {(cuuint32_t)kStrip, 1, 8};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(reinterpret_cast<CUtensorMap *>(map), CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<int32_t *>(base),
+                     dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 // L2 promotion of the digit-plane loads (MPCGEMM_L2PROMO = 0/64/128/256): 128 B = one box row,
 // 148 GB DRAM reads per cfg4 launch vs 161 GB with 256 B (same time within noise)
 static CUtensorMapL2promotion l2_promotion() {

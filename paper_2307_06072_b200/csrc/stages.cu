@@ -1000,9 +1000,12 @@ MPC_DEV void store_ept(uint64_t *dst, const uint64_t *v) {
     }
 }
 
-template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRing>
+// TMAP: the producer fetches each ring entry (8 slots of one row's strip) with ONE 3-D TMA load
+// (encode_partials_map) instead of 8 bulk copies -- the producer's instructions were a third of
+// the kernel's; a short last entry over-reads into the next slots (never consumed)
+template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRing, bool TMAP = false>
 __global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : (SFIX ? 3 : 6))
-fold_normalize_kernel(const FoldParams F)
+fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pmap)
 {
     constexpr int NCONS = COLS / EPT;                 // consumer threads
     extern __shared__ __align__(128) uint8_t fsm_raw[];
@@ -1041,7 +1044,18 @@ fold_normalize_kernel(const FoldParams F)
     const int sl0 = sr == s ? 0 : slotinfo[(sr + 1) * 2];
     if (warp == NCONS / 32) {
         // ---------------- producer warp
-        if (lane == 0) {
+        if (lane == 0 && TMAP) {
+            static_assert(!TMAP || COLS == kStrip, "TMA entries are whole strips");
+            const int g0 = (int)((((i >> 7) * F.nstrips + (j0 >> 8)) * nslots));   // global slot of slot 0
+            const int row = (int)(i & (kRowBlk - 1));
+            int e = 0; uint32_t ph = 0;
+            for (int sl = sl0; sl < nslots; sl += kFoldPer) {
+                mbar_wait(&empty[e], ph ^ 1);
+                mbar_arrive_expect_tx(&full[e], (uint32_t)(kFoldPer * COLS * 4));
+                tma_load_3d(ring + e * kFoldPer * COLS, &pmap, &full[e], 0, row, g0 + sl);
+                if (++e == RING) { e = 0; ph ^= 1; }
+            }
+        } else if (lane == 0) {
             const int32_t *region = F.partials + part_off(i, j0, 0, nslots, F.nstrips);   // slot 0
             int e = 0; uint32_t ph = 0;
             for (int sl = sl0; sl < nslots; sl += kFoldPer) {
@@ -1084,71 +1098,75 @@ fold_normalize_kernel(const FoldParams F)
             if (++e == RING) { e = 0; ph ^= 1; addr = ring0; }
         }
     };
-    // diagonals r = sr+1 .. 2 (byte b = sr + 1 - r of the fixed-point number), two at a time:
+    // diagonals r = sr+1 .. 2 (byte b = sr + 1 - r of the fixed-point number), two per iteration:
     //   acc = carry + D_b + 256 D_{b+1};  emit 16 bits at bit 8 b;  carry = acc >> 16
-    int64_t pend[2][EPT];
-    int b = 0;
-    for (int r = sr + 1; r >= 2; r--, b++) {
+    // D_r: the chunk sums of the jobs' partials combined by Eq. 6 (3M) or Eq. 5 (4M)
+    auto diag = [&](int r, int64_t (&d)[2][EPT]) {
+        int64_t u0[EPT], u1[EPT], u2[EPT];
 #pragma unroll
-        for (int x = 0; x < EPT; x++) t0[x] = t1[x] = t2[x] = 0;
+        for (int x = 0; x < EPT; x++) u0[x] = u1[x] = u2[x] = 0;
         int32_t v[EPT];
         for (int c = cntq[r]; c > 0; c--) {
             next(v);
 #pragma unroll
-            for (int x = 0; x < EPT; x++) t0[x] += v[x];
+            for (int x = 0; x < EPT; x++) u0[x] += v[x];
         }
         for (int c = cntq[(s + 2) + r]; c > 0; c--) {
             next(v);
 #pragma unroll
-            for (int x = 0; x < EPT; x++) t1[x] += v[x];
+            for (int x = 0; x < EPT; x++) u1[x] += v[x];
         }
         for (int c = cntq[2 * (s + 2) + r]; c > 0; c--) {
             next(v);
 #pragma unroll
-            for (int x = 0; x < EPT; x++) t2[x] += v[x];
+            for (int x = 0; x < EPT; x++) u2[x] += v[x];
         }
-        int64_t d[2][EPT];
 #pragma unroll
         for (int x = 0; x < EPT; x++) {
-            if (F.method == 3) { d[0][x] = t0[x] - t1[x]; d[1][x] = t2[x] - t0[x] - t1[x]; }   // Eq. 6
-            else               { d[0][x] = t0[x] - t1[x]; d[1][x] = t2[x]; }                   // Eq. 5
+            if (F.method == 3) { d[0][x] = u0[x] - u1[x]; d[1][x] = u2[x] - u0[x] - u1[x]; }   // Eq. 6
+            else               { d[0][x] = u0[x] - u1[x]; d[1][x] = u2[x]; }                   // Eq. 5
         }
-        if (!(b & 1) && r > 2) {                      // first of a pair: keep it
+    };
+    // limb pointers advance by one limb stride per completed 64-bit limb (no index arithmetic)
+    uint64_t *lp0 = fixg, *lp1 = fixg + (int64_t)Lc0 * lstride;
+    int b = 0, r = sr + 1;
+    for (; r >= 3; r -= 2, b += 2) {
+        int64_t d[2][EPT];
+        diag(r, d);
 #pragma unroll
-            for (int x = 0; x < EPT; x++) { pend[0][x] = d[0][x]; pend[1][x] = d[1][x]; }
-            continue;
-        }
-        const int sh = 8 * (b & 7);                  // bit offset of this diagonal's byte in cur
-        if (b & 1) {                                  // pair (b-1, b): 16 bits at bit 8 (b-1)
+        for (int p = 0; p < 2; p++)
 #pragma unroll
-            for (int p = 0; p < 2; p++)
+            for (int x = 0; x < EPT; x++) cr[p][x] += d[p][x];                  // carry + D_b
+        diag(r - 1, d);
+        const int sh = 8 * (b & 7);
 #pragma unroll
-                for (int x = 0; x < EPT; x++) {
-                    const int64_t acc = cr[p][x] + pend[p][x] + d[p][x] * 256;
-                    cur[p][x] |= (uint64_t)(acc & 0xFFFF) << (sh - 8);
-                    cr[p][x] = acc >> 16;
-                }
-        } else {                                      // unpaired last diagonal (r = 2, b even)
+        for (int p = 0; p < 2; p++)
 #pragma unroll
-            for (int p = 0; p < 2; p++)
-#pragma unroll
-                for (int x = 0; x < EPT; x++) {
-                    const int64_t acc = cr[p][x] + d[p][x];
-                    cur[p][x] |= (uint64_t)(acc & 0xFF) << sh;
-                    cr[p][x] = acc >> 8;
-                }
-        }
-        if ((b & 7) == 7 || r == 2) {                 // a 64-bit limb complete (or the last one)
-            if ((b & 7) == 7) {
-                if (live) {
-#pragma unroll
-                    for (int p = 0; p < 2; p++)
-                        store_ept<EPT>(fixg + ((int64_t)p * Lc0 + (b >> 3)) * lstride, cur[p]);
-                }
-#pragma unroll
-                for (int x = 0; x < EPT; x++) cur[0][x] = cur[1][x] = 0;
+            for (int x = 0; x < EPT; x++) {
+                const int64_t acc = cr[p][x] + d[p][x] * 256;
+                cur[p][x] |= (uint64_t)(acc & 0xFFFF) << sh;
+                cr[p][x] = acc >> 16;
             }
+        if ((b & 7) == 6) {                           // a 64-bit limb complete
+            if (live) { store_ept<EPT>(lp0, cur[0]); store_ept<EPT>(lp1, cur[1]); }
+            lp0 += lstride; lp1 += lstride;
+#pragma unroll
+            for (int x = 0; x < EPT; x++) cur[0][x] = cur[1][x] = 0;
         }
+    }
+    if (r == 2) {                                     // odd number of diagonals: the last one alone
+        int64_t d0[2][EPT];
+        diag(2, d0);
+        const int sh = 8 * (b & 7);
+#pragma unroll
+        for (int p = 0; p < 2; p++)
+#pragma unroll
+            for (int x = 0; x < EPT; x++) {
+                const int64_t acc = cr[p][x] + d0[p][x];
+                cur[p][x] |= (uint64_t)(acc & 0xFF) << sh;
+                cr[p][x] = acc >> 8;
+            }
+        b++;
     }
     if (!live) return;
     // the final carries at bit 8 sr, sign-extended to Lc0 limbs
@@ -1229,15 +1247,22 @@ static bool fold_sfix(int s, bool beta) {
     return fold_smem(s, kSfixCols, true, kSfixRing) <= 220 * 1024;
 }
 
-template <int COLS, bool BETA, bool SFIX, int EPT, int RING>
+template <int COLS, bool BETA, bool SFIX, int EPT, int RING, bool TMAP = false>
 static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
     const size_t sm = fold_smem(F.s, COLS, SFIX, RING);
-    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING>;
+    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING, TMAP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (int64_t)kRowBlk * ((F.n + COLS - 1) / COLS) * ((F.m + kRowBlk - 1) / kRowBlk);
     if (blocks > INT_MAX) return cudaErrorInvalidValue;
-    kern<<<(unsigned)blocks, COLS / EPT + 32, sm, st>>>(F);
+    alignas(64) uint8_t map[128] = {};
+    if (TMAP) {
+        // the partial planes of all (row block, strip) pairs: nslots is the launch's (the device
+        // rule's plans have at most F.nslots slots and share the layout's base)
+        const int64_t gslots = ((F.m + kRowBlk - 1) / kRowBlk) * F.nstrips * F.nslots;
+        if (encode_partials_map(map, F.partials, gslots)) return cudaErrorInvalidValue;
+    }
+    kern<<<(unsigned)blocks, COLS / EPT + 32, sm, st>>>(F, *reinterpret_cast<const CUtensorMap *>(map));
     return cudaGetLastError();
 }
 
@@ -1245,9 +1270,13 @@ cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
 {
     if (F.m == 0 || F.n == 0) return cudaSuccess;
     if (F.s > kMaxSlices || (F.ldF % kFoldEPT)) return cudaErrorInvalidValue;
-    if (F.beta) return fold_launch_t<256, true, false, kFoldEPT, kFoldRing>(F, st);
+    // TMA entries need the slot count known on the host (the device rule picks it on the device)
+    const bool tmap = !F.drs && !getenv("MPCGEMM_FOLD_BULK");
+    if (F.beta) return tmap ? fold_launch_t<256, true, false, kFoldEPT, kFoldRing, true>(F, st)
+                            : fold_launch_t<256, true, false, kFoldEPT, kFoldRing>(F, st);
     if (fold_sfix(F.s, false)) return fold_launch_t<kSfixCols, false, true, 1, kSfixRing>(F, st);
-    return fold_launch_t<256, false, false, kFoldEPT, kFoldRing>(F, st);
+    return tmap ? fold_launch_t<256, false, false, kFoldEPT, kFoldRing, true>(F, st)
+                : fold_launch_t<256, false, false, kFoldEPT, kFoldRing>(F, st);
 }
 
 // fixed-point scratch size (uint64 words) for the fold (0 when the limbs stay in shared memory)
