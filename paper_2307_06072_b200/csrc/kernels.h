@@ -82,7 +82,7 @@ struct FoldParams {
     const DevRuleState *drs;     // or null; else s, nslots, slotinfo come from drs->cur (F.s: the
                                  // largest candidate s, which sizes shared memory and the scratch)
 };
-constexpr int kFoldLdAlign = 2;  // fold outputs per consumer thread
+constexpr int kFoldLdAlign = 4;  // scratch pitch: a multiple of every fold variant's outputs per thread
 size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta);
 // a-5 + a-6: exact fold (chunk sums, Eq. 5/6 combination, carry) and RNE normalization
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st);

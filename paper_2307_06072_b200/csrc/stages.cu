@@ -963,8 +963,8 @@ MPC_DEV void accumulate_store(uint64_t *fix, int unused, int Lc, int Lw, int64_t
 // the carry chains; the fixed-point numbers live in shared memory, fix[part][limb][column].
 constexpr int kFoldRing = 4;           // entries
 constexpr int kFoldPer = 8;            // slots per entry
-constexpr int kFoldEPT = 2;            // outputs per consumer thread (4 was tried: slower, profiles/README.md)
-static_assert(kFoldEPT == kFoldLdAlign, "scratch pitch alignment");
+constexpr int kFoldEPT = 2;            // outputs per consumer thread (4: fewer instructions but slower, profiles/README.md)
+static_assert(kFoldLdAlign % 4 == 0, "scratch pitch alignment");
 
 template <int V> struct IntVec;
 template <> struct IntVec<1> {
