@@ -282,7 +282,7 @@ split_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, i
 // plane: a warp writes 32 consecutive bytes (one sector) of a plane row per store.
 constexpr int kSplitT = 128;           // k per CTA = threads per CTA
 
-template <int L>
+template <int L, bool WS = true>
 __global__ void __launch_bounds__(kSplitT)
 split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant__ CUtensorMap mim, DMat re, DMat im,
                  int side, int64_t lines, int64_t k, int64_t kp, const int64_t *__restrict__ eline, int s, int nparts,
@@ -328,11 +328,15 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
     const int64_t W = 8 * (int64_t)s - 3;
     mbar_wait(bar, 0);
     // limb l of this thread's entry in part p (swizzled shared-memory address)
+    // (the swizzle's XOR operand (o >> 7) & SWM is constant per thread: the entry row tid * ROW has
+    //  zero low bits wherever the XOR acts)
+    const uint32_t xm = (uint32_t)((((tid * ROW) >> 7) & SWM) << 4);
+    const uint32_t myrow = smem_u32(tile) + (uint32_t)(tid * ROW);      // shared-space address
     auto limb = [&](int p, int64_t l) -> uint64_t {
-        if (l < 0 || l >= L) return 0ull;
-        const uint32_t o = (uint32_t)(tid * ROW + 8 * l);
-        const uint32_t so = o ^ (((o >> 7) & SWM) << 4);
-        return *reinterpret_cast<const uint64_t *>(tile + (size_t)p * kSplitT * ROW + so);
+        if ((uint64_t)l >= (uint64_t)L) return 0ull;
+        uint64_t v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(myrow + (uint32_t)(p * kSplitT * ROW) + ((uint32_t)(8 * l) ^ xm)));
+        return v;
     };
     int64_t li[2]; int bo[2]; uint64_t lo[2], nc[2] = {1, 1};
     bool zero[2];
@@ -363,6 +367,15 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
         optr[it] = dig + ((int64_t)p * s + (s - 1 - bt)) * plane + line * kp + k0 + 16 * v;
     }
     const int64_t ostep = 8 * plane;
+    // WS: thread q handles the (part, quad) items q and q + 128 inside this CTA's row length
+    int8_t *qptr[2]; int qoff[2]; bool qon[2];
+#pragma unroll
+    for (int it = 0; it < 2; it++) {
+        const int q = tid + it * kSplitT, p = q / (kSplitT / 4), c = q % (kSplitT / 4);
+        qon[it] = p < nparts && 4 * c < rowlen;
+        qoff[it] = (p * kSplitT + 4 * c) * 8;
+        qptr[it] = dig + ((int64_t)p * s + (s - 1)) * plane + line * kp + k0 + 4 * c;
+    }
     for (int w = 0; w < nwords; w++) {
         uint8_t *stg = stage + (w & 1) * (3 * 8 * kSplitT);
         uint64_t y[3];
@@ -388,12 +401,42 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
             const uint64_t z = t + ch[p];
             ch[p] = c1 | (z < t);
             const uint64_t d = z ^ kH;
+            if constexpr (WS) {                          // [part][entry] words
+                asm volatile("st.shared.u64 [%0], %1;" :: "r"(smem_u32(stg) + (uint32_t)((p * kSplitT + tid) * 8)), "l"(d) : "memory");
+            } else {
 #pragma unroll
-            for (int bt = 0; bt < 8; bt++) stg[(p * 8 + bt) * kSplitT + tid] = (uint8_t)(d >> (8 * bt));
+                for (int bt = 0; bt < 8; bt++) stg[(p * 8 + bt) * kSplitT + tid] = (uint8_t)(d >> (8 * bt));
+            }
         }
         __syncthreads();
-        // plane rows of this word: (part p, byte bt) -> plane s-1-(8w+bt), 16-byte vector stores
         const int nb = min(8, s - 8 * w);
+        if constexpr (WS) {
+            // item (part p, quad c): the words of entries 4c .. 4c+3; for each of the 8 planes a
+            // byte-permute gathers their byte bt into one 32-bit word; a warp's store is one whole
+            // 128-byte plane row segment
+#pragma unroll
+            for (int it = 0; it < 2; it++) {
+                if (!qon[it]) continue;
+                uint4 w01, w23;
+                const uint32_t qa = smem_u32(stg) + (uint32_t)qoff[it];
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w01.x), "=r"(w01.y), "=r"(w01.z), "=r"(w01.w) : "r"(qa) : "memory");
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w23.x), "=r"(w23.y), "=r"(w23.z), "=r"(w23.w) : "r"(qa + 16) : "memory");
+                int8_t *o = qptr[it];
+#pragma unroll
+                for (int bt = 0; bt < 8; bt++, o -= plane) {
+                    if (bt < nb) {
+                        const uint32_t sel = (uint32_t)((bt & 3) | (((bt & 3) + 4) << 4));
+                        const uint32_t x0 = bt < 4 ? w01.x : w01.y, x1 = bt < 4 ? w01.z : w01.w;
+                        const uint32_t x2 = bt < 4 ? w23.x : w23.y, x3 = bt < 4 ? w23.z : w23.w;
+                        const uint32_t v = __byte_perm(__byte_perm(x0, x1, sel), __byte_perm(x2, x3, sel), 0x5410);
+                        *reinterpret_cast<uint32_t *>(o) = v;
+                    }
+                }
+                qptr[it] -= ostep;
+            }
+            continue;
+        }
+        // plane rows of this word: (part p, byte bt) -> plane s-1-(8w+bt), 16-byte vector stores
         if (rowlen == kSplitT) {                       // full tile: 8 vectors per row, no divisions
 #pragma unroll
             for (int it = 0; it < 2; it++) {
@@ -426,6 +469,7 @@ static cudaError_t split_tma_launch_t(DMat re, DMat im, int side, int64_t lines,
                                       const int64_t *eline, int s, int nparts, int8_t *dig, const DevRuleState *drs,
                                       cudaStream_t st)
 {
+    static const bool bytestg = getenv("MPCGEMM_SPLIT_BYTESTG") != nullptr;   // round-1 byte staging
     alignas(64) uint8_t mre[128], mim[128];           // CUtensorMap storage
     for (int p = 0; p < 2; p++) {
         const DMat &M = p ? im : re;
@@ -437,12 +481,12 @@ static cudaError_t split_tma_launch_t(DMat re, DMat im, int side, int64_t lines,
         if (rc) return cudaErrorInvalidValue;
     }
     const size_t sm = 1024 + 2 * (size_t)kSplitT * 8 * L + 2 * 3 * 8 * kSplitT + 64;
-    cudaError_t e = cudaFuncSetAttribute(split_tma_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    auto kern = bytestg ? split_tma_kernel<L, false> : split_tma_kernel<L, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((kp + kSplitT - 1) / kSplitT), (unsigned)lines);
-    split_tma_kernel<L><<<grid, kSplitT, sm, st>>>(*reinterpret_cast<const CUtensorMap *>(mre),
-                                                   *reinterpret_cast<const CUtensorMap *>(mim), re, im, side, lines, k, kp,
-                                                   eline, s, nparts, dig, drs);
+    kern<<<grid, kSplitT, sm, st>>>(*reinterpret_cast<const CUtensorMap *>(mre), *reinterpret_cast<const CUtensorMap *>(mim),
+                                    re, im, side, lines, k, kp, eline, s, nparts, dig, drs);
     return cudaGetLastError();
 }
 
