@@ -285,7 +285,6 @@ def main():
         if rank == 0:
             Bsrc = pdist.packed_cmat(k, n, prec, dev)
             pdist.copy_cmat(Bsrc[0], P.to_device(B, dev))
-        reps_all = []
 
         def compute(Al, Bd, Cv, s_, timing=[1]):
             return P.mpcgemm_ex(Al, Bd, Cv, prec, args.method, slices=s_, timing=timing[0])

@@ -524,3 +524,30 @@ def test_stage_variants_bitexact(env, method, monkeypatch):
     C1, r1 = run_gpu(A, B, prec, method)
     assert r0["slices"] == r1["slices"]
     assert same_bits(C0, C1), first_mismatch(C0, C1)
+
+
+@pytest.mark.parametrize("carrier", [0, 1])
+def test_tall_shapes_beyond_grid_y(carrier):
+    """m = 70000 > 65535 rows: every launch that once put m in gridDim.y (the fold, the zero-fill for
+    k = 0, the binary64 fold) now loops or flattens -- sampled bit-exact vs the oracle."""
+    m, n, k, prec = 70000, 3, 2, 64
+    A = mpgen.random_cmat(23, 1, m, k, prec, 3)
+    B = mpgen.random_cmat(23, 2, k, n, prec, 3)
+    dA, dB = P.to_device(A), P.to_device(B)
+    dC, rep = P.gemm(dA, dB, prec, "3M", carrier=carrier)
+    torch.cuda.synchronize()
+    C = P.to_host(dC)
+    rng = np.random.default_rng(3)
+    si = np.concatenate([rng.integers(0, m, 40), [0, 65535, 65536, m - 1]])
+    sj = np.concatenate([rng.integers(0, n, 40), [0, 1, 2, n - 1]])
+    if carrier:
+        Rs = oracle.ozaki_bits(A, B, prec, "3M", rep["slices"], bits=rep["slice_bits"], samples=(si, sj))
+    else:
+        Rs = oracle.ozaki(A, B, prec, "3M", rep["slices"], samples=(si, sj))
+    assert sampled_equal(C, Rs, si, sj) is None
+    A0 = mpgen.random_cmat(23, 3, m, 0, prec)
+    B0 = mpgen.random_cmat(23, 4, 0, n, prec)
+    dC0, _ = P.gemm(P.to_device(A0), P.to_device(B0), prec, "4M")     # k = 0: C = 0 on every row
+    torch.cuda.synchronize()
+    C0 = P.to_host(dC0)
+    assert not C0.re.limbs.any() and not C0.im.limbs.any() and not C0.re.exp.any()
