@@ -502,6 +502,12 @@ cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, i
         else if (L == 8) e = split_tma_launch_t<8>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
         else if (L == 4) e = split_tma_launch_t<4>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
         else if (L == 2) e = split_tma_launch_t<2>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
+        // other even L: unswizzled tiles (8L-byte rows; the bank conflicts of the per-entry limb
+        // reads cost far less than the per-thread-streams kernel's L2 re-fetches)
+        else if (L == 12) e = split_tma_launch_t<12>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
+        else if (L == 6) e = split_tma_launch_t<6>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
+        else if (L == 10) e = split_tma_launch_t<10>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
+        else if (L == 14) e = split_tma_launch_t<14>(re, im, side, lines, k, kp, eline, s, nparts, dig, drs, st);
         if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
     }
     const int64_t threads = (kp + kSplitVec - 1) / kSplitVec;
