@@ -37,7 +37,7 @@ cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, i
 
 // 3-D TMA map over the fold's int32 partial planes (slicegemm.cu): box = one row's 256-column strip
 // of 8 consecutive slots
-int encode_partials_map(void *map, const int32_t *base, int64_t gslots);
+int encode_partials_map(void *map, const int32_t *base, int64_t gslots, int slots_per_box);
 
 // 3-D TMA map over ABI limbs (implemented in slicegemm.cu; map = CUtensorMap*, 64-byte aligned)
 int encode_limb_map(void *map, const uint64_t *base, int L, uint64_t d1, uint64_t d2, uint64_t stride1,
@@ -81,6 +81,7 @@ struct FoldParams {
     int64_t ldF;                 // scratch row pitch (a multiple of kFoldLdAlign, >= n)
     const DevRuleState *drs;     // or null; else s, nslots, slotinfo come from drs->cur (F.s: the
                                  // largest candidate s, which sizes shared memory and the scratch)
+    int32_t uni1;                // every (job, diagonal) of the plan has exactly one chunk
 };
 constexpr int kFoldLdAlign = 4;  // scratch pitch: a multiple of every fold variant's outputs per thread
 size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta);

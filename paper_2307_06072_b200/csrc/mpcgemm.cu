@@ -153,6 +153,7 @@ struct Plan {
     int32_t *d_counter = nullptr;
     int32_t *d_slotinfo = nullptr;
     int nunits = 0, nslots = 0, grid = 0;
+    bool uni1 = false;             // every (job, diagonal) has exactly one chunk (3 slots per diagonal)
     int64_t mma = 0;
     JobDesc jobs[kMaxJobs];
     int njobs = 0, partsA = 0, partsB = 0;
@@ -241,6 +242,9 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
             nslots += slotinfo[(q * (s + 2) + r) * 2 + 1];
         }
     auto base = [&](int q, int r) { return slotinfo[(q * (s + 2) + r) * 2]; };
+    P.uni1 = P.njobs == 3;
+    for (int r = 2; r <= rtop; r++)
+        for (int q = 0; q < P.njobs; q++) P.uni1 = P.uni1 && slotinfo[(q * (s + 2) + r) * 2 + 1] == 1;
     std::vector<WorkUnit> units;
     // NEXT-4: a row tile of block b takes the segments whose first diagonal r <= sblk[b] + 1; a
     // pair (r, r+1) with r = sblk[b] + 1 becomes a G = 3 unit computing D_r alone
@@ -699,6 +703,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         F.beta = beta; F.alpha_neg = alpha_neg; F.C0re = dm(Cg.re); F.C0im = dm(Cg.im);
         F.ldF = (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign;
         F.sblk = sblk.empty() ? nullptr : mv.sblk + (r0 >> kSBlkShift);    // NEXT-4: per-block triangles
+        F.uni1 = plan->uni1 ? 1 : 0;
         fix = (uint64_t *)((uint8_t *)partials +
                            align_up((size_t)plan->nslots * ((mr + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
         F.fix = fix;
@@ -728,6 +733,7 @@ struct DevPlanSet {
     int32_t *d_counter = nullptr;        // the shared unit counter
     int s_lo = 0, s_hi = 0;
     int64_t nslots_max = 0;
+    bool uni1 = true;                    // every candidate has one chunk per (job, diagonal)
     size_t main_bytes = 0;               // workspace of the largest candidate
 };
 std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int, int, int>, DevPlanSet> g_devplans;
@@ -751,6 +757,7 @@ int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int met
         if (int rc = build_plan(dev, key2, &plan, st)) return rc;
         hp.push_back(DevPlan{plan->d_units, plan->d_counter + 1, plan->d_slotinfo, s, plan->nunits, plan->nslots, 0});
         S.nslots_max = std::max<int64_t>(S.nslots_max, plan->nslots);
+        S.uni1 = S.uni1 && plan->uni1;
         S.main_bytes = std::max(S.main_bytes, layout_for(m, n, k, s, method, geo.maxkb, prec, false).main);
     }
     if (cudaMalloc(&S.d_plans, sizeof(DevPlan) * hp.size()) != cudaSuccess ||
@@ -849,7 +856,7 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     F.eA = mv.eA; F.eB = mv.eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
     F.beta = 0; F.alpha_neg = 0; F.C0re = dm(C->re); F.C0im = dm(C->im);
     F.ldF = (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign;
-    F.fix = fix; F.drs = mv.drs;
+    F.fix = fix; F.drs = mv.drs; F.nslots = S->nslots_max; F.uni1 = S->uni1 ? 1 : 0;
     {
         Nvtx r("mpcgemm.a5a6_fold_normalize");
         CK(fold_normalize_launch(F, st));

@@ -645,13 +645,14 @@ int encode_limb_map(void *map, const uint64_t *base, int L, uint64_t d1, uint64_
 
 // 3-D map over the int32 partial planes for the fold's producer: dims {256 columns of a strip,
 // 128 rows of a row block, global slot g = (rowblk * nstrips + strip) * nslots + slot}, box
-// {256, 1, 8}: one TMA load brings one row's strip for 8 consecutive slots.  Returns 0 on success.
-int encode_partials_map(void *map, const int32_t *base, int64_t gslots) {
+// {256, 1, slots_per_box}: one TMA load brings one row's strip for that many consecutive slots.
+// Returns 0 on success.
+int encode_partials_map(void *map, const int32_t *base, int64_t gslots, int slots_per_box) {
     auto enc = get_encode();
     if (!enc) return -1;
     cuuint64_t dims[3] = {(cuuint64_t)kStrip, (cuuint64_t)kRowBlk, (cuuint64_t)gslots};
     cuuint64_t strides[2] = {(cuuint64_t)kStrip * 4, (cuuint64_t)kTileElems * 4};
-    cuuint32_t box[3] = {(cuuint32_t)kStrip, 1, 8};
+    cuuint32_t box[3] = {(cuuint32_t)kStrip, 1, (cuuint32_t)slots_per_box};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(reinterpret_cast<CUtensorMap *>(map), CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<int32_t *>(base),
                      dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -1053,10 +1053,14 @@ MPC_DEV void store_ept(uint64_t *dst, const uint64_t *v) {
 // TMAP: the producer fetches each ring entry (8 slots of one row's strip) with ONE 3-D TMA load
 // (encode_partials_map) instead of 8 bulk copies -- the producer's instructions were a third of
 // the kernel's; a short last entry over-reads into the next slots (never consumed)
-template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRing, bool TMAP = false>
+// UNI1 (with TMAP): every (job, diagonal) has exactly one chunk (3 slots per diagonal, in job
+// order), so a ring entry is one PAIR of diagonals (6 slots, one TMA load) and the consumers read
+// it at fixed offsets: one wait and one release per pair, no per-slot bookkeeping
+template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRing, bool TMAP = false, bool UNI1 = false>
 __global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : (SFIX ? 3 : 6))
 fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pmap)
 {
+    constexpr int PER = UNI1 ? 6 : kFoldPer;          // slots per ring entry
     constexpr int NCONS = COLS / EPT;                 // consumer threads
     extern __shared__ __align__(128) uint8_t fsm_raw[];
     if (F.drs && F.drs->status) return;              // device rule: s outside the planned range
@@ -1066,7 +1070,7 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
     const int Lw = BETA ? Lc0 + F.L + 3 : 0;          // NEXT-2 sum window
     const int nslots = F.drs ? F.drs->cur.nslots : (int)F.nslots;
     int32_t *ring = reinterpret_cast<int32_t *>(fsm_raw);                                   // [RING][PER][COLS]
-    uint16_t *cntq = reinterpret_cast<uint16_t *>(fsm_raw + RING * kFoldPer * COLS * 4);  // [job][s+2] chunk counts
+    uint16_t *cntq = reinterpret_cast<uint16_t *>(fsm_raw + RING * PER * COLS * 4);  // [job][s+2] chunk counts
     uint64_t *full = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(cntq + kMaxJobs * (s + 2)) + 15) & ~uintptr_t(15));
     uint64_t *empty = full + RING;
     uint64_t *fixs = empty + RING;               // SFIX: [2][Lc0][COLS] (16-byte aligned)
@@ -1099,21 +1103,21 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
             const int g0 = (int)((((i >> 7) * F.nstrips + (j0 >> 8)) * nslots));   // global slot of slot 0
             const int row = (int)(i & (kRowBlk - 1));
             int e = 0; uint32_t ph = 0;
-            for (int sl = sl0; sl < nslots; sl += kFoldPer) {
+            for (int sl = sl0; sl < nslots; sl += PER) {
                 mbar_wait(&empty[e], ph ^ 1);
-                mbar_arrive_expect_tx(&full[e], (uint32_t)(kFoldPer * COLS * 4));
-                tma_load_3d(ring + e * kFoldPer * COLS, &pmap, &full[e], 0, row, g0 + sl);
+                mbar_arrive_expect_tx(&full[e], (uint32_t)(PER * COLS * 4));
+                tma_load_3d(ring + e * PER * COLS, &pmap, &full[e], 0, row, g0 + sl);
                 if (++e == RING) { e = 0; ph ^= 1; }
             }
         } else if (lane == 0) {
             const int32_t *region = F.partials + part_off(i, j0, 0, nslots, F.nstrips);   // slot 0
             int e = 0; uint32_t ph = 0;
-            for (int sl = sl0; sl < nslots; sl += kFoldPer) {
-                const int cnt = nslots - sl < kFoldPer ? nslots - sl : kFoldPer;
+            for (int sl = sl0; sl < nslots; sl += PER) {
+                const int cnt = nslots - sl < PER ? nslots - sl : PER;
                 mbar_wait(&empty[e], ph ^ 1);
                 mbar_arrive_expect_tx(&full[e], (uint32_t)(cnt * COLS * 4));
                 for (int f = 0; f < cnt; f++)                // slot blocks are kTileElems apart
-                    bulk_load(ring + (e * kFoldPer + f) * COLS, region + (int64_t)(sl + f) * kTileElems, COLS * 4, &full[e]);
+                    bulk_load(ring + (e * PER + f) * COLS, region + (int64_t)(sl + f) * kTileElems, COLS * 4, &full[e]);
                 if (++e == RING) { e = 0; ph ^= 1; }
             }
         }
@@ -1141,7 +1145,7 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
         if (fill == 0) mbar_wait(&full[e], ph);
         IntVec<EPT>::get_shared(addr, v);
         addr += (uint32_t)COLS * 4u;
-        if (++fill == kFoldPer) {
+        if (++fill == PER) {
             fill = 0;
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[e]);
@@ -1156,6 +1160,15 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
 #pragma unroll
         for (int x = 0; x < EPT; x++) u0[x] = u1[x] = u2[x] = 0;
         int32_t v[EPT];
+        if constexpr (UNI1) {                         // the entry is resident: three fixed slots
+            int32_t w1[EPT], w2[EPT];
+            IntVec<EPT>::get_shared(addr, v);
+            IntVec<EPT>::get_shared(addr + (uint32_t)COLS * 4u, w1);
+            IntVec<EPT>::get_shared(addr + (uint32_t)COLS * 8u, w2);
+            addr += (uint32_t)COLS * 12u;
+#pragma unroll
+            for (int x = 0; x < EPT; x++) { u0[x] = v[x]; u1[x] = w1[x]; u2[x] = w2[x]; }
+        } else {
         for (int c = cntq[r]; c > 0; c--) {
             next(v);
 #pragma unroll
@@ -1171,6 +1184,7 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
 #pragma unroll
             for (int x = 0; x < EPT; x++) u2[x] += v[x];
         }
+        }
 #pragma unroll
         for (int x = 0; x < EPT; x++) {
             if (F.method == 3) { d[0][x] = u0[x] - u1[x]; d[1][x] = u2[x] - u0[x] - u1[x]; }   // Eq. 6
@@ -1180,14 +1194,27 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
     // limb pointers advance by one limb stride per completed 64-bit limb (no index arithmetic)
     uint64_t *lp0 = fixg, *lp1 = fixg + (int64_t)Lc0 * lstride;
     int b = 0, r = sr + 1;
+    // UNI1: wait for / release one ring entry (a pair of diagonals)
+    auto entry_begin = [&]() {
+        if constexpr (UNI1) { mbar_wait(&full[e], ph); addr = ring0 + (uint32_t)(e * PER * COLS * 4); }
+    };
+    auto entry_end = [&]() {
+        if constexpr (UNI1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[e]);
+            if (++e == RING) { e = 0; ph ^= 1; }
+        }
+    };
     for (; r >= 3; r -= 2, b += 2) {
         int64_t d[2][EPT];
+        entry_begin();
         diag(r, d);
 #pragma unroll
         for (int p = 0; p < 2; p++)
 #pragma unroll
             for (int x = 0; x < EPT; x++) cr[p][x] += d[p][x];                  // carry + D_b
         diag(r - 1, d);
+        entry_end();
         const int sh = 8 * (b & 7);
 #pragma unroll
         for (int p = 0; p < 2; p++)
@@ -1206,7 +1233,9 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
     }
     if (r == 2) {                                     // odd number of diagonals: the last one alone
         int64_t d0[2][EPT];
+        entry_begin();
         diag(2, d0);
+        entry_end();
         const int sh = 8 * (b & 7);
 #pragma unroll
         for (int p = 0; p < 2; p++)
@@ -1282,8 +1311,8 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
     }
 }
 
-size_t fold_smem(int s, int cols, bool sfix, int ring = kFoldRing) {
-    const size_t base = (size_t)ring * kFoldPer * cols * 4 + 2 * (size_t)kMaxJobs * (s + 2) + 32 + (size_t)2 * ring * 8 + 16;
+size_t fold_smem(int s, int cols, bool sfix, int ring = kFoldRing, int per = kFoldPer) {
+    const size_t base = (size_t)ring * per * cols * 4 + 2 * (size_t)kMaxJobs * (s + 2) + 32 + (size_t)2 * ring * 8 + 16;
     return base + (sfix ? (size_t)2 * (s / 8 + 3) * cols * 8 + 16 : 0);
 }
 
@@ -1297,10 +1326,10 @@ static bool fold_sfix(int s, bool beta) {
     return fold_smem(s, kSfixCols, true, kSfixRing) <= 220 * 1024;
 }
 
-template <int COLS, bool BETA, bool SFIX, int EPT, int RING, bool TMAP = false>
+template <int COLS, bool BETA, bool SFIX, int EPT, int RING, bool TMAP = false, bool UNI1 = false>
 static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
-    const size_t sm = fold_smem(F.s, COLS, SFIX, RING);
-    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING, TMAP>;
+    const size_t sm = fold_smem(F.s, COLS, SFIX, RING, UNI1 ? 6 : kFoldPer);
+    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING, TMAP, UNI1>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (int64_t)kRowBlk * ((F.n + COLS - 1) / COLS) * ((F.m + kRowBlk - 1) / kRowBlk);
@@ -1310,7 +1339,7 @@ static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
         // the partial planes of all (row block, strip) pairs: nslots is the launch's (the device
         // rule's plans have at most F.nslots slots and share the layout's base)
         const int64_t gslots = ((F.m + kRowBlk - 1) / kRowBlk) * F.nstrips * F.nslots;
-        if (encode_partials_map(map, F.partials, gslots)) return cudaErrorInvalidValue;
+        if (encode_partials_map(map, F.partials, gslots, UNI1 ? 6 : kFoldPer)) return cudaErrorInvalidValue;
     }
     kern<<<(unsigned)blocks, COLS / EPT + 32, sm, st>>>(F, *reinterpret_cast<const CUtensorMap *>(map));
     return cudaGetLastError();
@@ -1320,12 +1349,15 @@ cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
 {
     if (F.m == 0 || F.n == 0) return cudaSuccess;
     if (F.s > kMaxSlices || (F.ldF % kFoldEPT)) return cudaErrorInvalidValue;
-    // TMA entries need the slot count known on the host (the device rule picks it on the device)
-    const bool tmap = !F.drs && !getenv("MPCGEMM_FOLD_BULK");
-    if (F.beta) return tmap ? fold_launch_t<256, true, false, kFoldEPT, kFoldRing, true>(F, st)
+    // (device rule: F.nslots is the largest candidate's slot count, so the map covers the chosen plan)
+    const bool tmap = !getenv("MPCGEMM_FOLD_BULK");
+    const bool uni1 = tmap && F.uni1 && !getenv("MPCGEMM_FOLD_NOUNI1");
+    if (F.beta) return uni1 ? fold_launch_t<256, true, false, kFoldEPT, 5, true, true>(F, st)
+                     : tmap ? fold_launch_t<256, true, false, kFoldEPT, kFoldRing, true>(F, st)
                             : fold_launch_t<256, true, false, kFoldEPT, kFoldRing>(F, st);
     if (fold_sfix(F.s, false)) return fold_launch_t<kSfixCols, false, true, 1, kSfixRing>(F, st);
-    return tmap ? fold_launch_t<256, false, false, kFoldEPT, kFoldRing, true>(F, st)
+    return uni1 ? fold_launch_t<256, false, false, kFoldEPT, 5, true, true>(F, st)
+         : tmap ? fold_launch_t<256, false, false, kFoldEPT, kFoldRing, true>(F, st)
                 : fold_launch_t<256, false, false, kFoldEPT, kFoldRing>(F, st);
 }
 

@@ -511,17 +511,24 @@ def test_fp64_carrier_bitexact(method, m, n, k, prec, spread, d):
         assert max_err_log2(A, B, C, Xs, samples=(si, sj), ref_is_sampled=True) <= -(prec - BOUND[method])
 
 
-@pytest.mark.parametrize("env", ["MPCGEMM_FOLD_BULK", "MPCGEMM_FOLD_SFIX", "MPCGEMM_SPLIT_V1"])
+@pytest.mark.parametrize("env", ["MPCGEMM_FOLD_BULK", "MPCGEMM_FOLD_SFIX", "MPCGEMM_SPLIT_V1", "MPCGEMM_FOLD_NOUNI1",
+                                 "MPCGEMM_SPLIT_BYTESTG"])
 @pytest.mark.parametrize("method", ["3M", "4M"])
 def test_stage_variants_bitexact(env, method, monkeypatch):
-    """The fold's bulk-copy producer and shared-memory-limbs variant and the non-TMA split give the
-    default path's bits (the same exact integers, one rounding), at a ragged shape with chunks."""
-    m, n, k, prec = 200, 300, 700, 256
+    """The fold's bulk-copy producer, shared-memory-limbs and generic (non pair-entry) variants and the
+    non-TMA / byte-staged splits give the default path's bits (the same exact integers, one rounding),
+    at a ragged shape with exactness chunks and at one where every diagonal has one chunk."""
+    for (m, n, k, prec) in ((200, 300, 700, 256), (130, 270, 200, 384)):
+        _stage_variant_case(env, method, monkeypatch, m, n, k, prec)
+
+
+def _stage_variant_case(env, method, monkeypatch, m, n, k, prec):
     A = mpgen.random_cmat(17, 1, m, k, prec, 6, zero_frac=0.05)
     B = mpgen.random_cmat(17, 2, k, n, prec, 6, zero_frac=0.05)
     C0, r0 = run_gpu(A, B, prec, method)
     monkeypatch.setenv(env, "1")
     C1, r1 = run_gpu(A, B, prec, method)
+    monkeypatch.delenv(env)
     assert r0["slices"] == r1["slices"]
     assert same_bits(C0, C1), first_mismatch(C0, C1)
 
