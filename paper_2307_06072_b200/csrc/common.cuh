@@ -218,6 +218,10 @@ MPC_DEV void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// orders this thread's generic-proxy shared-memory accesses before later async-proxy accesses
+// (TMA / bulk copies) -- e.g. before releasing a ring slot that a TMA load will overwrite
+MPC_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // L2 cache policies (createpolicy) and a 16-byte store carrying one
 MPC_DEV uint64_t l2_policy_evict_first() {
     uint64_t p;

@@ -691,8 +691,8 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         SL.digA = digA; SL.digB = digB; SL.rowsA = mr; SL.rowsB = n; SL.kp = Lo.kp;
         SL.grid = plan->grid; SL.BM = geo.BM; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits;
         SL.units_flat = plan->d_units;
-        {
-            Nvtx r("mpcgemm.a4_slicegemm");
+        if (!(SL.P.dbg & 16)) {                        // (MPCGEMM_DBG bit 4: fold the previous call's
+            Nvtx r("mpcgemm.a4_slicegemm");            //  partials again -- a race detector for the fold)
             CK(slicegemm_launch(SL, st));
         }
         if (E && r0 + mr >= m) CK(cudaEventRecord(E->ev[4], st));

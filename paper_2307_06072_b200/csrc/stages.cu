@@ -1141,14 +1141,22 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
     // per slot (a shared-space address, no per-slot index arithmetic) and wraps with the ring
     const uint32_t ring0 = smem_u32(ring) + (uint32_t)col * 4u;
     uint32_t addr = ring0;
+    // Releasing a ring entry: the producer's next write into it is an ASYNC-proxy write (TMA / bulk
+    // copy), which the mbarrier hand-off alone does not order after this warp's generic-proxy shared
+    // loads (the last of which may still be in flight): each lane fences the proxies first.  Without
+    // the fence ~5-10 % of config-4 folds corrupted a few outputs (tools/determinism.py, MPCGEMM_DBG=16).
+    auto release = [&]() {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[e]);
+    };
     auto next = [&](int32_t (&v)[EPT]) {
         if (fill == 0) mbar_wait(&full[e], ph);
         IntVec<EPT>::get_shared(addr, v);
         addr += (uint32_t)COLS * 4u;
         if (++fill == PER) {
             fill = 0;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[e]);
+            release();
             if (++e == RING) { e = 0; ph ^= 1; addr = ring0; }
         }
     };
@@ -1200,8 +1208,7 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
     };
     auto entry_end = [&]() {
         if constexpr (UNI1) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[e]);
+            release();
             if (++e == RING) { e = 0; ph ^= 1; }
         }
     };
