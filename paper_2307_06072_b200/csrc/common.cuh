@@ -116,6 +116,7 @@ struct GemmParams {
                                // padding of k up to a multiple of 128 is not multiplied
     unsigned long long *mma_count;   // or null: tcgen05.mma instructions issued, added at CTA exit
     const DevRuleState *drs;         // or null; else s, nunits, nslots, units, hot come from drs->cur
+    int32_t halfn;                   // CTA-pair kernel: N = 128 MMAs on a last tile column of <= 128 columns
     JobDesc jobs[kMaxJobs];
 };
 

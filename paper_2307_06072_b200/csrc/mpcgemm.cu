@@ -687,6 +687,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         SL.P.hot = env_int("MPCGEMM_KPHASE", 1) ? plan->d_counter + 1 : nullptr;
         SL.P.pblk = env_int("MPCGEMM_PBLK", 32);
         SL.P.mma_count = mma_dev;
+        SL.P.halfn = env_int("MPCGEMM_HALFN", 1);
         for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
         SL.digA = digA; SL.digB = digB; SL.rowsA = mr; SL.rowsB = n; SL.kp = Lo.kp;
         SL.grid = plan->grid; SL.BM = geo.BM; SL.BN = BN; SL.simt = simt; SL.nunits = plan->nunits;
@@ -843,6 +844,7 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     SL.P.partsA = SL.P.partsB = parts;
     SL.P.pblk = env_int("MPCGEMM_PBLK", 32);
     SL.P.drs = mv.drs;
+    SL.P.halfn = env_int("MPCGEMM_HALFN", 1);
     for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = Pj.jobs[q];
     SL.digA = digA; SL.digB = digB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
     SL.grid = geo.BM == 256 ? (geo.grid & ~1) : geo.grid; SL.BM = geo.BM; SL.BN = geo.BN; SL.simt = 0;

@@ -299,6 +299,9 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const int nunits = dp ? dp->nunits : P.nunits;
     const int64_t nslots = dp ? dp->nslots : P.nslots;
     int32_t *const hot = dp ? dp->hot : P.hot;
+    // a tile column with at most 128 valid columns (n mod 256 in (0, 128]): N = 128 MMAs (each CTA
+    // supplies 64 B rows), half the epilogue -- instead of multiplying 128 zero-padded columns
+    auto half_n = [&](int tn) { return P.halfn && P.n - tn * 256 <= 128; };
     const uint32_t rank = cluster_ctarank();
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < STAGES; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -341,7 +344,8 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 if (P.dbg & 4) { planeA &= 7; planeB &= 7; kb &= 1; tm &= 1; tn &= 1; }   // ~1 MB of varying operands
                 tma_load_3d_2sm(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, tm * 256 + (int)rank * 128, planeA);
                 if (!a_only)                                  // (a p-block's lead stage needs only A)
-                    tma_load_3d_2sm(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, tn * 256 + (int)rank * 128, planeB);
+                    tma_load_3d_2sm(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK,
+                                    tn * 256 + (int)rank * (half_n(tn) ? 64 : 128), planeB);
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             };
             for (;;) {
@@ -412,7 +416,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             // ---------------- MMA issuer (leader CTA only)
-            constexpr uint32_t idesc = make_idesc_i8(256, BN);
+            constexpr uint32_t idesc_full = make_idesc_i8(256, BN), idesc_half = make_idesc_i8(256, BN / 2);
             const uint32_t d0 = tmem_base, d1 = tmem_base + (uint32_t)BN;
             int stage = 0; uint32_t phase = 0;
             uint32_t tphase = 0;
@@ -427,6 +431,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 if (u < 0) { if (P.mma_count) atomicAdd(P.mma_count, (unsigned long long)nmma); break; }
                 const WorkUnit w = units[u];
                 const JobDesc &J = P.jobs[unit_job(w)];
+                const uint32_t idesc = half_n(w.tn) ? idesc_half : idesc_full;   // ragged last tile column: N = 128
                 mbar_wait_cluster(tempty, tphase ^ 1);
                 tc_fence_after();
                 if (unit_G(w) == 2) {
@@ -505,7 +510,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             for (int acc = 0; acc < (unit_G(w) == 2 ? 2 : 1); acc++) {
                 const int64_t slot = acc ? w.slot1 : w.slot0;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; c++) {
+                for (int c = 0; c < (half_n(w.tn) ? BN / 64 : BN / 32); c++) {
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
                     tmem_ld_wait();
