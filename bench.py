@@ -240,6 +240,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        # NCCL's kernels (96 registers x its threads) cannot become resident next to a slice-GEMM CTA,
+        # so the pipelined B broadcast / C all-gather overlap the GEMM only on SMs the GEMM leaves
+        # free: 8 channels on 8 reserved SMs (unmeasured on > 1 GPU here; both are overridable)
+        os.environ.setdefault("NCCL_MAX_NCHANNELS", "8")
+        os.environ.setdefault("MPCGEMM_RESERVE_SMS", "8")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -318,6 +324,8 @@ def main():
                            "bcast_ms_per_step": round(parts["bcast_ms"] / args.steps, 3),
                            "gather_ms_per_step": round(parts["gather_ms"] / args.steps, 3),
                            "rows_this_rank0": r1 - r0,
+                           "reserved_sms": int(os.environ.get("MPCGEMM_RESERVE_SMS", "0")),
+                           "nccl_max_nchannels": os.environ.get("NCCL_MAX_NCHANNELS"),
                            "note": "per-stream device times (CUDA events); B broadcast / C all-gather of "
                                    "neighbouring steps overlap compute, so they do not add up to ms_per_step"}
     cmacs = m * n * k                                   # the whole product, all ranks together

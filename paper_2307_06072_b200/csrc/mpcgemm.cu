@@ -455,7 +455,10 @@ Geometry main_geometry(int dev, int64_t m, int64_t n, int64_t k, int s, int meth
     g.BN = env_int("MPCGEMM_BN", tile_bn(n));
     if (g.BN != 128 && g.BN != 256) g.BN = tile_bn(n);
     g.BM = (g.BN == 256 && env_int("MPCGEMM_CTA2", 1)) ? 256 : 128;   // CTA pairs for wide tiles
-    g.grid = sm_count(dev);
+    // MPCGEMM_RESERVE_SMS: SMs left free of the persistent slice GEMM (multi-GPU: NCCL's kernels
+    // cannot become resident next to a slice-GEMM CTA -- registers -- so the B broadcast / C gather
+    // of neighbouring products overlap the GEMM only on reserved SMs)
+    g.grid = std::max(2, sm_count(dev) - std::max(0, env_int("MPCGEMM_RESERVE_SMS", 0)));
     g.maxkb = (int)chunk_kb(m, n, k, s, method, g.BM, g.BN, g.grid);
     return g;
 }

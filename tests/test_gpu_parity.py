@@ -512,7 +512,7 @@ def test_fp64_carrier_bitexact(method, m, n, k, prec, spread, d):
 
 
 @pytest.mark.parametrize("env", ["MPCGEMM_FOLD_BULK", "MPCGEMM_FOLD_SFIX", "MPCGEMM_SPLIT_V1", "MPCGEMM_FOLD_NOUNI1",
-                                 "MPCGEMM_SPLIT_BYTESTG"])
+                                 "MPCGEMM_SPLIT_BYTESTG", "MPCGEMM_RESERVE_SMS", "MPCGEMM_HALFN=0"])
 @pytest.mark.parametrize("method", ["3M", "4M"])
 def test_stage_variants_bitexact(env, method, monkeypatch):
     """The fold's bulk-copy producer, shared-memory-limbs and generic (non pair-entry) variants and the
@@ -526,9 +526,10 @@ def _stage_variant_case(env, method, monkeypatch, m, n, k, prec):
     A = mpgen.random_cmat(17, 1, m, k, prec, 6, zero_frac=0.05)
     B = mpgen.random_cmat(17, 2, k, n, prec, 6, zero_frac=0.05)
     C0, r0 = run_gpu(A, B, prec, method)
-    monkeypatch.setenv(env, "1")
+    name, _, val = env.partition("=")
+    monkeypatch.setenv(name, val or "1")
     C1, r1 = run_gpu(A, B, prec, method)
-    monkeypatch.delenv(env)
+    monkeypatch.delenv(name)
     assert r0["slices"] == r1["slices"]
     assert same_bits(C0, C1), first_mismatch(C0, C1)
 
