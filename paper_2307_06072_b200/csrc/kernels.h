@@ -35,6 +35,11 @@ cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, i
                          const int64_t *eline, int s, int nparts, int8_t *dig, cudaStream_t st,
                          const DevRuleState *drs = nullptr);
 
+// a-3 for both operands (B then A) in one launch where the TMA split applies
+cudaError_t split2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp, int L,
+                          const int64_t *eA, const int64_t *eB, int s, int nparts, int8_t *digA, int8_t *digB,
+                          cudaStream_t st, const DevRuleState *drs = nullptr, int *nlaunch = nullptr);
+
 // 3-D TMA map over the fold's int32 partial planes (slicegemm.cu): box = one row's 256-column strip
 // of 8 consecutive slots
 int encode_partials_map(void *map, const int32_t *base, int64_t gslots, int slots_per_box);

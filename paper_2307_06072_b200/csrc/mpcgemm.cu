@@ -656,17 +656,21 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
     int8_t *digB = digA + align_up((size_t)parts * s * mg * Lo.kp, 256);
     int32_t *partials = (int32_t *)((uint8_t *)digB + align_up((size_t)parts * s * n * Lo.kp, 256));
     uint64_t *fix = (uint64_t *)((uint8_t *)partials);  // set below per plan
+    const bool one_group = mg >= m;                   // B and A split by one launch
+    int nsplit = 1;
     {
-        Nvtx r("mpcgemm.a3_split_B");
-        CK(split_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, s, parts, digB, st));
+        Nvtx r(one_group ? "mpcgemm.a3_split" : "mpcgemm.a3_split_B");
+        if (one_group) CK(split2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, Lo.kp, L, eA, eB, s, parts,
+                                        digA, digB, st, nullptr, &nsplit));
+        else CK(split_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, eB, s, parts, digB, st));
     }
     if (!sblk.empty()) CK(cudaMemcpyAsync(mv.sblk, sblk.data(), 4 * sblk.size(), cudaMemcpyHostToDevice, st));
-    int launches = 1;
+    int launches = one_group ? nsplit - 1 : 1;         // (+ 3 per group below: split A, GEMM, fold)
     for (int64_t r0 = 0; r0 < m; r0 += mg) {
         const int64_t mr = std::min(mg, m - r0);
         const mpc_cmat Ag = rows_of(*A, r0, L);
         const mpc_cmat Cg = rows_of(*C, r0, L);
-        {
+        if (!one_group) {
             Nvtx r("mpcgemm.a3_split_A");
             CK(split_launch(dm(Ag.re), dm(Ag.im), 0, mr, k, Lo.kp, L, eA + r0, s, parts, digA, st));
         }
@@ -831,10 +835,11 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     int32_t *partials = (int32_t *)((uint8_t *)digB + align_up((size_t)parts * s_hi * n * Lo.kp, 256));
     uint64_t *fix = (uint64_t *)((uint8_t *)partials +
                                  align_up((size_t)S->nslots_max * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
+    int nsplit = 1;
     {
         Nvtx r("mpcgemm.a3_split");
-        CK(split_launch(dm(B->re), dm(B->im), 1, n, k, Lo.kp, L, mv.eB, s_hi, parts, digB, st, mv.drs));
-        CK(split_launch(dm(A->re), dm(A->im), 0, m, k, Lo.kp, L, mv.eA, s_hi, parts, digA, st, mv.drs));
+        CK(split2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, Lo.kp, L, mv.eA, mv.eB, s_hi, parts, digA,
+                         digB, st, mv.drs, &nsplit));
     }
     const Geometry geo = main_geometry(dev, m, n, k, s_hi, method);
     SliceGemmLaunch SL;
@@ -868,7 +873,7 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     }
     if (rep) {
         rep->slices = 0;                                 // chosen on the device: mpcgemm_device_rule_result()
-        rep->kernel_launches += 9;                      // planes, T GEMM, min, max-plus, rule, split x2, GEMM, fold
+        rep->kernel_launches += 7 + nsplit;             // planes, T GEMM, min, max-plus, rule, split, GEMM, fold
         rep->slicegemm_ctas = SL.grid; rep->tile_m = geo.BM; rep->tile_n = geo.BN;
         rep->certified = 1;
     }

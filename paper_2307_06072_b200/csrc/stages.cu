@@ -282,13 +282,14 @@ split_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, i
 // plane: a warp writes 32 consecutive bytes (one sector) of a plane row per store.
 constexpr int kSplitT = 128;           // k per CTA = threads per CTA
 
-template <int L, bool WS = true>
-__global__ void __launch_bounds__(kSplitT)
-split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant__ CUtensorMap mim, DMat re, DMat im,
-                 int side, int64_t lines, int64_t k, int64_t kp, const int64_t *__restrict__ eline, int s, int nparts,
-                 int8_t *__restrict__ dig, const DevRuleState *drs)
+// one CTA: kSplitT consecutive k of line `line` (k0 = first k); mre / mim: the tensor maps of the
+// side's Re / Im limbs (kernel parameters)
+template <int L, bool WS>
+MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, const DMat &re, const DMat &im,
+                            int side, int64_t lines, int64_t k, int64_t kp, const int64_t *__restrict__ eline, int s,
+                            int nparts, int8_t *__restrict__ dig, int64_t line, int64_t k0)
 {
-    if (drs) { if (drs->status) return; s = drs->cur.s; }    // device rule: the chosen s
+    const CUtensorMap &mre = *mre_p, &mim = *mim_p;
     extern __shared__ uint8_t tsm_raw[];
     uint8_t *tile = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
     constexpr int ROW = 8 * L;                        // bytes per entry row
@@ -297,8 +298,6 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
     uint8_t *stage = tile + 2 * kSplitT * ROW;
     uint64_t *bar = reinterpret_cast<uint64_t *>(stage + 2 * 3 * 8 * kSplitT);
     const int tid = threadIdx.x;
-    const int64_t line = blockIdx.y;
-    const int64_t k0 = (int64_t)blockIdx.x * kSplitT;
     if (tid == 0) { mbar_init(bar, 1); fence_barrier_init(); }
     __syncthreads();
     if (tid == 0) {
@@ -464,6 +463,32 @@ split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant_
     }
 }
 
+template <int L, bool WS = true>
+__global__ void __launch_bounds__(kSplitT)
+split_tma_kernel(const __grid_constant__ CUtensorMap mre, const __grid_constant__ CUtensorMap mim, DMat re, DMat im,
+                 int side, int64_t lines, int64_t k, int64_t kp, const int64_t *__restrict__ eline, int s, int nparts,
+                 int8_t *__restrict__ dig, const DevRuleState *drs)
+{
+    if (drs) { if (drs->status) return; s = drs->cur.s; }    // device rule: the chosen s
+    split_tma_body<L, WS>(&mre, &mim, re, im, side, lines, k, kp, eline, s, nparts, dig, blockIdx.y,
+                          (int64_t)blockIdx.x * kSplitT);
+}
+
+// both operands in one launch: block rows [0, n) split the columns of B, [n, n + m) the rows of A
+template <int L>
+__global__ void __launch_bounds__(kSplitT)
+split2_tma_kernel(const __grid_constant__ CUtensorMap mAre, const __grid_constant__ CUtensorMap mAim,
+                  const __grid_constant__ CUtensorMap mBre, const __grid_constant__ CUtensorMap mBim, DMat Are, DMat Aim,
+                  DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp, const int64_t *__restrict__ eA,
+                  const int64_t *__restrict__ eB, int s, int nparts, int8_t *__restrict__ digA, int8_t *__restrict__ digB,
+                  const DevRuleState *drs)
+{
+    if (drs) { if (drs->status) return; s = drs->cur.s; }
+    const int64_t y = blockIdx.y, k0 = (int64_t)blockIdx.x * kSplitT;
+    if (y < n) split_tma_body<L, true>(&mBre, &mBim, Bre, Bim, 1, n, k, kp, eB, s, nparts, digB, y, k0);
+    else       split_tma_body<L, true>(&mAre, &mAim, Are, Aim, 0, m, k, kp, eA, s, nparts, digA, y - n, k0);
+}
+
 template <int L>
 static cudaError_t split_tma_launch_t(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp,
                                       const int64_t *eline, int s, int nparts, int8_t *dig, const DevRuleState *drs,
@@ -488,6 +513,58 @@ static cudaError_t split_tma_launch_t(DMat re, DMat im, int side, int64_t lines,
     kern<<<grid, kSplitT, sm, st>>>(*reinterpret_cast<const CUtensorMap *>(mre), *reinterpret_cast<const CUtensorMap *>(mim),
                                     re, im, side, lines, k, kp, eline, s, nparts, dig, drs);
     return cudaGetLastError();
+}
+
+template <int L>
+static cudaError_t split2_launch_t(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp,
+                                   const int64_t *eA, const int64_t *eB, int s, int nparts, int8_t *digA, int8_t *digB,
+                                   const DevRuleState *drs, cudaStream_t st)
+{
+    alignas(64) uint8_t maps[4][128];                 // A re, A im, B re, B im
+    const DMat *M[4] = {&Are, &Aim, &Bre, &Bim};
+    for (int q = 0; q < 4; q++) {
+        const int rc = q < 2 ? encode_limb_map(maps[q], M[q]->limbs, L, (uint64_t)k, (uint64_t)m, 8ull * L, 8ull * L * M[q]->ld, kSplitT, 1)
+                             : encode_limb_map(maps[q], M[q]->limbs, L, (uint64_t)n, (uint64_t)k, 8ull * L, 8ull * L * M[q]->ld, 1, kSplitT);
+        if (rc) return cudaErrorInvalidValue;
+    }
+    const size_t sm = 1024 + 2 * (size_t)kSplitT * 8 * L + 2 * 3 * 8 * kSplitT + 64;
+    cudaError_t e = cudaFuncSetAttribute(split2_tma_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((kp + kSplitT - 1) / kSplitT), (unsigned)(m + n));
+    auto cm = [&](int q) { return *reinterpret_cast<const CUtensorMap *>(maps[q]); };
+    split2_tma_kernel<L><<<grid, kSplitT, sm, st>>>(cm(0), cm(1), cm(2), cm(3), Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s,
+                                                   nparts, digA, digB, drs);
+    return cudaGetLastError();
+}
+
+// a-3 for B and A in one launch when the TMA path applies (else two split_launch calls)
+cudaError_t split2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp, int L,
+                          const int64_t *eA, const int64_t *eB, int s, int nparts, int8_t *digA, int8_t *digB,
+                          cudaStream_t st, const DevRuleState *drs, int *nlaunch)
+{
+    if (nlaunch) *nlaunch = 1;
+    const bool aligned = !(reinterpret_cast<uintptr_t>(Are.limbs) & 15) && !(reinterpret_cast<uintptr_t>(Aim.limbs) & 15) &&
+                         !(reinterpret_cast<uintptr_t>(Bre.limbs) & 15) && !(reinterpret_cast<uintptr_t>(Bim.limbs) & 15);
+    if (m > 0 && n > 0 && kp > 0 && m + n < 65536 && aligned && !getenv("MPCGEMM_SPLIT_V1") &&
+        !getenv("MPCGEMM_SPLIT_BYTESTG")) {
+        cudaError_t e = cudaErrorNotSupported;
+        switch (L) {
+            case 16: e = split2_launch_t<16>(Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s, nparts, digA, digB, drs, st); break;
+            case 14: e = split2_launch_t<14>(Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s, nparts, digA, digB, drs, st); break;
+            case 12: e = split2_launch_t<12>(Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s, nparts, digA, digB, drs, st); break;
+            case 10: e = split2_launch_t<10>(Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s, nparts, digA, digB, drs, st); break;
+            case 8:  e = split2_launch_t<8>(Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s, nparts, digA, digB, drs, st); break;
+            case 6:  e = split2_launch_t<6>(Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s, nparts, digA, digB, drs, st); break;
+            case 4:  e = split2_launch_t<4>(Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s, nparts, digA, digB, drs, st); break;
+            case 2:  e = split2_launch_t<2>(Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s, nparts, digA, digB, drs, st); break;
+            default: break;
+        }
+        if (e != cudaErrorNotSupported && e != cudaErrorInvalidValue) return e;
+    }
+    if (nlaunch) *nlaunch = 2;
+    cudaError_t e = split_launch(Bre, Bim, 1, n, k, kp, L, eB, s, nparts, digB, st, drs);
+    if (e != cudaSuccess) return e;
+    return split_launch(Are, Aim, 0, m, k, kp, L, eA, s, nparts, digA, st, drs);
 }
 
 cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
