@@ -431,14 +431,15 @@ struct Layout {
 
 int tile_bn(int64_t n) { return n > 128 ? 256 : 128; }
 
-// Load-balance target for the MMA k-blocks of one unit: at least ~4 units per CTA.  (The
+// Load-balance target for the MMA k-blocks of one unit: about one unit per CTA (MPCGEMM_BALANCE
+// units per CTA; 4 was 21 % slower at config 2: more, shorter units each pay an accumulator drain).  (The
 // INT32 exactness cap is separate: exact_cap().)
 int64_t chunk_kb(int64_t m, int64_t n, int64_t k, int s, int method, int BM, int BN, int grid) {
     const int64_t KB = (k + kBK - 1) / kBK;
     const int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN) * (BM / 128);   // in 128-row CTA tiles
     const int64_t npairs_total = method == 0 ? 1 : (method == 3 ? 3 : 4);
     const int64_t work = npairs_total * KB * (int64_t)s * (s + 1) / 2 * tiles;   // k-blocks
-    int64_t target = work / (4 * (int64_t)grid);
+    int64_t target = work / (std::max(1, env_int("MPCGEMM_BALANCE", 1)) * (int64_t)grid);
     return std::max<int64_t>(8, std::min<int64_t>(target, 1 << 30));
 }
 
@@ -450,7 +451,10 @@ int64_t exact_cap() {
 
 struct Geometry { int BM, BN, grid, maxkb; };
 
-Geometry main_geometry(int dev, int64_t m, int64_t n, int64_t k, int s, int method) {
+// m_balance (> 0): the row count whose work sets the chunk target -- row groups use the whole
+// call's, so every group has the whole call's slot table (and a group's workspace scales with its
+// rows)
+Geometry main_geometry(int dev, int64_t m, int64_t n, int64_t k, int s, int method, int64_t m_balance = 0) {
     Geometry g;
     g.BN = env_int("MPCGEMM_BN", tile_bn(n));
     if (g.BN != 128 && g.BN != 256) g.BN = tile_bn(n);
@@ -459,7 +463,7 @@ Geometry main_geometry(int dev, int64_t m, int64_t n, int64_t k, int s, int meth
     // cannot become resident next to a slice-GEMM CTA -- registers -- so the B broadcast / C gather
     // of neighbouring products overlap the GEMM only on reserved SMs)
     g.grid = std::max(2, sm_count(dev) - std::max(0, env_int("MPCGEMM_RESERVE_SMS", 0)));
-    g.maxkb = (int)chunk_kb(m, n, k, s, method, g.BM, g.BN, g.grid);
+    g.maxkb = (int)chunk_kb(m_balance > 0 ? m_balance : m, n, k, s, method, g.BM, g.BN, g.grid);
     return g;
 }
 
@@ -675,7 +679,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
             CK(split_launch(dm(Ag.re), dm(Ag.im), 0, mr, k, Lo.kp, L, eA + r0, s, parts, digA, st));
         }
         if (E && r0 == 0) CK(cudaEventRecord(E->ev[3], st));
-        const Geometry geo = main_geometry(dev, mr, n, k, s, method);
+        const Geometry geo = main_geometry(dev, mr, n, k, s, method, m);
         const int BN = geo.BN;
         std::vector<int32_t> sb;
         if (!sblk.empty()) sb.assign(sblk.begin() + (r0 >> kSBlkShift), sblk.begin() + ((r0 + mr + kSBlk - 1) >> kSBlkShift));
@@ -994,11 +998,11 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     }
     // workspace of row groups of mg rows (the ragged last group may need more slots)
     auto grouped_layout = [&](int64_t mg) {
-        Layout Lg = layout_for(mg, n, k, s, method, main_geometry(dev, mg, n, k, s, method).maxkb, prec, beta != 0);
+        Layout Lg = layout_for(mg, n, k, s, method, main_geometry(dev, mg, n, k, s, method, m).maxkb, prec, beta != 0);
         if (mg < m && m % mg) {
             const int64_t ml = m % mg;
             const int parts = method == 3 ? 3 : 2;
-            Layout Ll = layout_for(ml, n, k, s, method, main_geometry(dev, ml, n, k, s, method).maxkb, prec, beta != 0);
+            Layout Ll = layout_for(ml, n, k, s, method, main_geometry(dev, ml, n, k, s, method, m).maxkb, prec, beta != 0);
             const size_t extra = align_up((size_t)parts * s * mg * Lg.kp, 256) - align_up((size_t)parts * s * ml * Lg.kp, 256);
             Lg.main = std::max(Lg.main, Ll.main + extra);
         }
