@@ -199,7 +199,10 @@ std::vector<Segment> diag_segments(const Plan &P, int64_t KB, int s, int method,
                 r += 2;
             } else {
                 const int64_t G = np * (r - 1) * KB;
-                const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(cap, target));
+                // with pairs, a single diagonal (the odd top one) has about half a pair unit's work:
+                // cut it only for exactness, so its slots match the other diagonals' (the fold's
+                // pair-entry mode needs one chunk per diagonal wherever exactness allows)
+                const int64_t chunk = std::max<int64_t>(1, g2 ? cap : std::min<int64_t>(cap, target));
                 segs.push_back({q, r, 1, (G + chunk - 1) / chunk});
                 r += 1;
             }
