@@ -55,6 +55,20 @@ __host__ __device__ __forceinline__ int unit_kb(const WorkUnit &w, int i) { retu
 // walked in nblk blocks, each over all its k-blocks, so one k-block step touches pblk planes
 __host__ __device__ __forceinline__ int unit_nblk(int np, int pblk) { return pblk > 0 && np > pblk ? (np + pblk - 1) / pblk : 1; }
 __host__ __device__ __forceinline__ int unit_pfirst(int np, int nblk, int j) { return j * np / nblk + 1; }
+// job-wide k-phase mode (GemmParams.kmode == 2): the hint of a G >= 2 unit is shared by every
+// unit of its (job, k-block chunk) class (id in job_g bits 17..30), and its p-blocks start at
+// absolute plane numbers 1, pblk + 1, 2 pblk + 1, ... (the last block takes the remainder), so
+// co-running units of neighbouring diagonal pairs walk the same A_p tiles at the same time
+__host__ __device__ __forceinline__ int unit_hint(const WorkUnit &w) { return (w.job_g >> 17) & 0x3FFF; }
+constexpr int kHintNB = 1024;   // p-block stride of a class-wide position (pair, p-block, k-block)
+__host__ __device__ __forceinline__ int unit_nblk_m(int np, int pblk, int kmode) {
+    if (kmode != 2) return unit_nblk(np, pblk);
+    return pblk > 0 && np > pblk ? (np + pblk / 2) / pblk : 1;
+}
+__host__ __device__ __forceinline__ int unit_pfirst_m(int np, int nblk, int j, int pblk, int kmode) {
+    if (kmode != 2) return unit_pfirst(np, nblk, j);
+    return j >= nblk ? np + 1 : j * pblk + 1;
+}
 
 struct JobDesc {
     int32_t npairs;
@@ -112,6 +126,8 @@ struct GemmParams {
                                // (pair, p-block, k-block) a running unit of the group last started;
                                // a new unit of the group begins there (CTA-pair kernel, G >= 2)
     int32_t pblk;              // p-block length of the CTA-pair kernel's G >= 2 units (0: one block)
+    int32_t kmode;             // k-phase hint mode: 1 one hint per (job, r, chunk) group; 2 one per
+                               // (job, chunk) class with absolute p-blocks (unit_hint)
     int32_t kk_last;           // K = 32 MMA steps of the last k-block (1..3; 0: all 4): the zero
                                // padding of k up to a multiple of 128 is not multiplied
     unsigned long long *mma_count;   // or null: tcgen05.mma instructions issued, added at CTA exit

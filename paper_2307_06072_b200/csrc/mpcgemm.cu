@@ -254,7 +254,15 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
     auto in_tri = [&](int64_t tm, int r) {
         return key.sblk.empty() || r <= key.sblk[(size_t)((tm * key.BM) >> kSBlkShift)] + 1;
     };
-    const bool serp = env_int("MPCGEMM_SERPENTINE", 1) != 0;
+    // k-phase mode 2 (job-wide hints): a class id per (job, k-block chunk) in job_g bits 17..30;
+    // every unit of a class walks its k-blocks upward (no serpentine), so positions agree
+    const int kmode = env_int("MPCGEMM_KPHASE", 2);
+    const bool serp = kmode != 2 && env_int("MPCGEMM_SERPENTINE", 1) != 0;
+    std::map<std::tuple<int, int, int>, int32_t> hint_ids;
+    auto hint = [&](int q, int32_t a, int32_t b) -> int32_t {
+        auto it = hint_ids.emplace(std::make_tuple(q, (int)a, (int)b), (int32_t)hint_ids.size()).first;
+        return (it->second & 0x3FFF) << 17;
+    };
     // K = 32 MMAs per k-block step: 4, except kk_last for the last (zero-padded) k-block
     const int64_t kkl = ((key.k - 1) % kBK) / 32 + 1;
     auto kk_sum = [&](int64_t a, int64_t b) { return (b - a) * (kBK / 32) - ((a <= KB - 1 && KB - 1 < b) ? kBK / 32 - kkl : 0); };
@@ -269,11 +277,11 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
                         if (!in_tri(tm, r)) continue;
                         const int32_t rev = serp && ((r >> 1) & 1) ? (1 << 16) : 0;
                         if (!in_tri(tm, r + 1)) {              // block's last diagonal is r: D_r alone
-                            units.push_back({q | (3 << 8) | rev, (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
+                            units.push_back({q | (3 << 8) | rev | hint(q, a, b), (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
                             P.mma += np * kk_sum(a, b) * (r - 1);
                             continue;
                         }
-                        units.push_back({q | (2 << 8) | rev, (int32_t)tm, (int32_t)tn, r, a, b,
+                        units.push_back({q | (2 << 8) | rev | hint(q, a, b), (int32_t)tm, (int32_t)tn, r, a, b,
                                          base(q, r) + (int32_t)c, base(q, r + 1) + (int32_t)c});
                         P.mma += np * kk_sum(a, b) * (2 * r - 1);
                     }
@@ -296,7 +304,29 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
         return unit_G(w) == 2 ? np * (w.b - w.a) * (2 * w.r - 1)
              : unit_G(w) == 3 ? np * (w.b - w.a) * (w.r - 1) : (int64_t)(w.b - w.a);
     };
-    if (key.order == 1) {
+    if (key.order == 2) {
+        // job-major; within a job the units of one k-block chunk class (a, b) together -- classes
+        // by their smallest unit, largest first, so the job still ends on its smallest units --
+        // then longest first: co-running groups are neighbouring diagonal pairs on the SAME
+        // k-blocks (with the class-wide k-phase hint they read the same A_p tiles and B planes
+        // two steps apart), instead of alternating between the chunks of a multi-chunk diagonal
+        std::map<int, int64_t> cmin;                   // class id (G >= 2) -> smallest unit work
+        auto cls = [&](const WorkUnit &w) { return unit_G(w) >= 2 ? unit_hint(w) : -1 - unit_job(w); };
+        for (const WorkUnit &w : units) {
+            auto it = cmin.find(cls(w));
+            if (it == cmin.end()) cmin[cls(w)] = work(w); else it->second = std::min(it->second, work(w));
+        }
+        std::stable_sort(units.begin(), units.end(), [&](const WorkUnit &a, const WorkUnit &b) {
+            if (unit_job(a) != unit_job(b)) return unit_job(a) < unit_job(b);
+            const int ca = cls(a), cb = cls(b);
+            if (ca != cb) {
+                const int64_t ma = cmin[ca], mb = cmin[cb];
+                if (ma != mb) return ma > mb;
+                return ca < cb;
+            }
+            return work(a) > work(b);
+        });
+    } else if (key.order == 1) {
         // job-major, then longest first: co-running units are neighbouring diagonal pairs of
         // one job and read mostly the same digit planes; the tail is the last job's smallest
         std::stable_sort(units.begin(), units.end(), [&](const WorkUnit &a, const WorkUnit &b) {
@@ -687,7 +717,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         std::vector<int32_t> sb;
         if (!sblk.empty()) sb.assign(sblk.begin() + (r0 >> kSBlkShift), sblk.begin() + ((r0 + mr + kSBlk - 1) >> kSBlkShift));
         PlanKey key{mr, n, k, s, method, geo.BM, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0,
-                    env_int("MPCGEMM_ORDER", 1), sb};
+                    env_int("MPCGEMM_ORDER", 2), sb};
         Plan *plan;
         if (int rc = build_plan(dev, key, &plan, st)) return rc;
         SliceGemmLaunch SL;
@@ -698,8 +728,9 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
         SL.P.partsA = SL.P.partsB = parts;
         SL.P.dbg = env_int("MPCGEMM_DBG", 0);
-        SL.P.hot = env_int("MPCGEMM_KPHASE", 1) ? plan->d_counter + 1 : nullptr;
-        SL.P.pblk = env_int("MPCGEMM_PBLK", 32);
+        SL.P.hot = env_int("MPCGEMM_KPHASE", 2) ? plan->d_counter + 1 : nullptr;
+        SL.P.pblk = env_int("MPCGEMM_PBLK", 64);
+        SL.P.kmode = env_int("MPCGEMM_KPHASE", 2);
         SL.P.mma_count = mma_dev;
         SL.P.halfn = env_int("MPCGEMM_HALFN", 1);
         for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
@@ -758,7 +789,7 @@ int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int met
     const int s_lo = rule_slices(prec, method, 0.0);
     const int s_hi = rule_slices(prec, method, rule_log2rho(k, 1, 1, -1));
     if (s_lo < 0 || s_hi < 0) return fail(MPCGEMM_ERR_SLICES, "device rule: slice range above 1024");
-    auto key = std::make_tuple(dev, m, n, k, method, s_lo, s_hi, env_int("MPCGEMM_ORDER", 1));
+    auto key = std::make_tuple(dev, m, n, k, method, s_lo, s_hi, env_int("MPCGEMM_ORDER", 2));
     auto it = g_devplans.find(key);
     if (it != g_devplans.end()) { *out = &it->second; return 0; }
     DevPlanSet S;
@@ -767,7 +798,7 @@ int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int met
     for (int s = s_lo; s <= s_hi; s++) {
         const Geometry geo = main_geometry(dev, m, n, k, s, method);
         PlanKey key2{m, n, k, s, method, geo.BM, geo.BN, geo.grid, 0, geo.maxkb, g2_enabled() ? 1 : 0,
-                     env_int("MPCGEMM_ORDER", 1), {}};
+                     env_int("MPCGEMM_ORDER", 2), {}};
         Plan *plan;
         if (int rc = build_plan(dev, key2, &plan, st)) return rc;
         hp.push_back(DevPlan{plan->d_units, plan->d_counter + 1, plan->d_slotinfo, s, plan->nunits, plan->nslots, 0});
@@ -857,7 +888,8 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = s_hi; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
     SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
     SL.P.partsA = SL.P.partsB = parts;
-    SL.P.pblk = env_int("MPCGEMM_PBLK", 32);
+    SL.P.pblk = env_int("MPCGEMM_PBLK", 64);
+    SL.P.kmode = env_int("MPCGEMM_KPHASE", 2);
     SL.P.drs = mv.drs;
     SL.P.halfn = env_int("MPCGEMM_HALFN", 1);
     for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = Pj.jobs[q];

@@ -359,10 +359,17 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         // within one k-block step of each other (an L2 hit) whatever their start
                         const WorkUnit &wu = units[u];
                         if (unit_G(wu) >= 2) {
-                            const int nkb = wu.b - wu.a;
-                            const int npos = P.jobs[unit_job(wu)].npairs * unit_nblk(unit_G(wu) == 2 ? wu.r : wu.r - 1, P.pblk) * nkb;
-                            const int h = ld_relaxed_s32(hot + wu.slot0);
-                            rot = (h > 0 && h < npos) ? h : 0;
+                            const int nkb = wu.b - wu.a, npairs = P.jobs[unit_job(wu)].npairs;
+                            const int nblk = unit_nblk_m(unit_G(wu) == 2 ? wu.r : wu.r - 1, P.pblk, P.kmode);
+                            const int npos = npairs * nblk * nkb;
+                            if (P.kmode == 2) {               // class-wide position -> this unit's
+                                const int h = ld_relaxed_s32(hot + unit_hint(wu));
+                                const int hk = h % nkb, hb = (h / nkb) % kHintNB, hp = h / (nkb * kHintNB);
+                                rot = (h > 0 && hp < npairs && hb < nblk) ? (hp * nblk + hb) * nkb + hk : 0;
+                            } else {
+                                const int h = ld_relaxed_s32(hot + wu.slot0);
+                                rot = (h > 0 && h < npos) ? h : 0;
+                            }
                         }
                     }
                     mbar_wait_cluster(&qempty[qs], qph ^ 1);
@@ -387,14 +394,18 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                     // D_{r+1} (G = 2: A_p, B_{r+1-p}) or D_r alone (G = 3: A_p, B_{r-p}).  A G = 2
                     // block that starts at p0 > 1 first loads A_{p0-1} (D_r's partner of B_{r+1-p0})
                     const int g2 = unit_G(w) == 2;
-                    const int np = g2 ? w.r : w.r - 1, nkb = w.b - w.a, nblk = unit_nblk(np, P.pblk);
+                    const int np = g2 ? w.r : w.r - 1, nkb = w.b - w.a, nblk = unit_nblk_m(np, P.pblk, P.kmode);
                     const int npos = J.npairs * nblk * nkb;
                     int pos = rot;
                     for (int t = 0; t < npos; t++) {
                         const int pb = pos / nkb, pr = pb / nblk, blk = pb - pr * nblk;
                         const int kb = unit_kb(w, pos - pb * nkb);
-                        const int p0 = unit_pfirst(np, nblk, blk), p1 = unit_pfirst(np, nblk, blk + 1) - 1;
-                        if (rank == 0 && hot) st_relaxed_s32(hot + w.slot0, pos);
+                        const int p0 = unit_pfirst_m(np, nblk, blk, P.pblk, P.kmode);
+                        const int p1 = unit_pfirst_m(np, nblk, blk + 1, P.pblk, P.kmode) - 1;
+                        if (rank == 0 && hot) {
+                            if (P.kmode == 2) st_relaxed_s32(hot + unit_hint(w), (pr * kHintNB + blk) * nkb + (pos - pb * nkb));
+                            else st_relaxed_s32(hot + w.slot0, pos);
+                        }
                         if (g2 && p0 > 1) load(J.pa[pr] * s + p0 - 2, 0, kb, w.tm, w.tn, true);   // A_{p0-1} only
                         for (int p = p0; p <= p1; p++)
                             load(J.pa[pr] * s + p - 1, J.pb[pr] * s + (w.r - p - 1 + g2), kb, w.tm, w.tn);
@@ -437,12 +448,13 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                 if (unit_G(w) == 2) {
                     // the producer's stage sequence: per position a block p0..p1 (plus the A_{p0-1}
                     // lead stage when p0 > 1); an accumulator's first MMA overwrites it
-                    const int nkb = w.b - w.a, nblk = unit_nblk(w.r, P.pblk), npos = J.npairs * nblk * nkb;
+                    const int nkb = w.b - w.a, nblk = unit_nblk_m(w.r, P.pblk, P.kmode), npos = J.npairs * nblk * nkb;
                     uint32_t acc0 = 0, acc1 = 0;
                     int pos = rot;
                     for (int t = 0; t < npos; t++) {
                         const int blk = (pos / nkb) % nblk;
-                        const int p0 = unit_pfirst(w.r, nblk, blk), p1 = unit_pfirst(w.r, nblk, blk + 1) - 1;
+                        const int p0 = unit_pfirst_m(w.r, nblk, blk, P.pblk, P.kmode);
+                        const int p1 = unit_pfirst_m(w.r, nblk, blk + 1, P.pblk, P.kmode) - 1;
                         // MMA K-steps of this position's k-block (from registers: a shared-memory
                         // read here would sit between each stage's barrier and its first MMA)
                         const int nkk = (unit_kb(w, pos % nkb) == KB - 1 && P.kk_last) ? P.kk_last : kBK / 32;

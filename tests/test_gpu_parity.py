@@ -131,17 +131,21 @@ def test_small_chunks_equal_default(monkeypatch):
 @pytest.mark.parametrize("method", ["3M", "4M"])
 def test_schedule_variants_bitexact(method, monkeypatch):
     """The CTA-pair kernel's walk order is free (exact integer sums): p-blocks of 1..7 planes (lead
-    stages for D_r), k-phase hints on/off (units starting mid-walk, also from a previous call's
-    stale hints), serpentine off, many exactness chunks -- all bitwise equal, and equal to the oracle."""
+    stages for D_r; even and absolute-aligned splits), k-phase hints off / per group / class-wide
+    (units starting mid-walk, also from a previous call's stale hints), serpentine off, the three
+    unit orders, many exactness chunks -- all bitwise equal, and equal to the oracle."""
     m, n, k, prec = 300, 260, 900, 256
     A = mpgen.random_cmat(21, 1, m, k, prec, 3)
     B = mpgen.random_cmat(21, 2, k, n, prec, 3)
     C0, rep = run_gpu(A, B, prec, method)
     variants = [{"MPCGEMM_PBLK": "1"}, {"MPCGEMM_PBLK": "3"}, {"MPCGEMM_PBLK": "7", "MPCGEMM_MAXKB": "2"},
                 {"MPCGEMM_PBLK": "0", "MPCGEMM_KPHASE": "0"}, {"MPCGEMM_KPHASE": "0", "MPCGEMM_SERPENTINE": "0"},
-                {"MPCGEMM_PBLK": "5", "MPCGEMM_SERPENTINE": "0", "MPCGEMM_MAXKB": "3"}]
+                {"MPCGEMM_PBLK": "5", "MPCGEMM_SERPENTINE": "0", "MPCGEMM_MAXKB": "3"},
+                {"MPCGEMM_KPHASE": "1", "MPCGEMM_PBLK": "32"}, {"MPCGEMM_KPHASE": "1", "MPCGEMM_ORDER": "1"},
+                {"MPCGEMM_KPHASE": "2", "MPCGEMM_PBLK": "3", "MPCGEMM_MAXKB": "2"},
+                {"MPCGEMM_KPHASE": "2", "MPCGEMM_PBLK": "2", "MPCGEMM_ORDER": "0"}]
     for v in variants:
-        for key in ("MPCGEMM_PBLK", "MPCGEMM_KPHASE", "MPCGEMM_SERPENTINE", "MPCGEMM_MAXKB"):
+        for key in ("MPCGEMM_PBLK", "MPCGEMM_KPHASE", "MPCGEMM_SERPENTINE", "MPCGEMM_MAXKB", "MPCGEMM_ORDER"):
             monkeypatch.delenv(key, raising=False)
         for key, val in v.items():
             monkeypatch.setenv(key, val)

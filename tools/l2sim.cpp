@@ -1,0 +1,141 @@
+// L2 reuse model of the CTA-pair slice GEMM's operand stream (design tool, not product code).
+// Replays the plan's unit order on NPAIR persistent CTA pairs that each load one 32 KB stage per
+// time step (MMA-bound: every pair advances at the same rate), with the k-phase hint rule, and
+// counts misses of an LRU cache of 32 KB operand blocks (A: plane x k-block x 256-row tile,
+// B: plane x k-block x 256-column tile) -- an estimate of the kernel's DRAM operand reads.
+//   g++ -O2 -std=c++17 tools/l2sim.cpp -o /tmp/l2sim && /tmp/l2sim [options]
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <list>
+#include <unordered_map>
+#include <vector>
+
+struct Unit { int job, tm, tn, r, a, b, G, rev, cls, slot; };
+
+static int M = 2048, N = 2048, K = 2048, S = 129, NPAIR = 74, PBLK = 32, KMODE = 1, ORDER = 0;
+static long CAP_MB = 110;
+static int SERP = 1, JITTER = 0;
+
+int main(int argc, char **argv) {
+    for (int i = 1; i + 1 < argc; i += 2) {
+        const char *k = argv[i]; int v = atoi(argv[i + 1]);
+        if (!strcmp(k, "-m")) M = v; else if (!strcmp(k, "-n")) N = v; else if (!strcmp(k, "-k")) K = v;
+        else if (!strcmp(k, "-s")) S = v; else if (!strcmp(k, "-pairs")) NPAIR = v; else if (!strcmp(k, "-pblk")) PBLK = v;
+        else if (!strcmp(k, "-kmode")) KMODE = v; else if (!strcmp(k, "-cap")) CAP_MB = v; else if (!strcmp(k, "-serp")) SERP = v;
+        else if (!strcmp(k, "-order")) ORDER = v; else if (!strcmp(k, "-jitter")) JITTER = v;
+    }
+    const int KB = (K + 127) / 128, TM = (M + 255) / 256, TN = (N + 255) / 256;
+    const int cap = 1023, rmax = S + 1;
+    std::vector<Unit> units;
+    int slot = 0, ncls = 0;
+    std::vector<std::vector<int>> clsid(3, std::vector<int>(KB * (KB + 1) + 1, -1));
+    for (int q = 0; q < 3; q++) {
+        int r = 2;
+        while (r <= rmax) {
+            if (r + 1 <= rmax) {
+                int kbc = std::min(KB, cap / r);
+                int nch = (KB + kbc - 1) / kbc;
+                for (int c = 0; c < nch; c++) {
+                    int a = c * KB / nch, b = (c + 1) * KB / nch;
+                    int &cl = clsid[q][a * (KB + 1) + b];
+                    if (cl < 0) cl = ncls++;
+                    for (int tm = 0; tm < TM; tm++)
+                        for (int tn = 0; tn < TN; tn++) {
+                            int tmm = tm, tnn = tn;
+                            if (ORDER == 1) { int t = tm * TN + tn; tmm = t % TM; tnn = t / TM; }   // column-major tiles
+                            units.push_back({q, tmm, tnn, r, a, b, 2, SERP && KMODE != 2 && ((r >> 1) & 1), cl, slot + c});
+                        }
+                }
+                slot += nch;
+                r += 2;
+            } else {
+                units.push_back({q, 0, 0, r, 0, 0, 1, 0, -1, -1});   // single top diagonal: tiny, modelled as no loads
+                units.pop_back();
+                r += 1;
+            }
+        }
+    }
+    auto work = [&](const Unit &u) { return (long)(u.b - u.a) * (2 * u.r - 1); };
+    // ORDER 2: within a job, units of one k-block chunk class (a, b) together (classes in order of
+    // first appearance), longest first inside a class, so co-running groups read the same k-blocks
+    std::vector<int> cfirst(ncls + 1, 1 << 30);
+    for (size_t i = 0; i < units.size(); i++) if (units[i].cls >= 0) cfirst[units[i].cls] = std::min(cfirst[units[i].cls], (int)i);
+    std::stable_sort(units.begin(), units.end(), [&](const Unit &x, const Unit &y) {
+        if (x.job != y.job) return x.job < y.job;
+        if (ORDER == 2 && x.cls != y.cls) return cfirst[x.cls] < cfirst[y.cls];
+        return work(x) > work(y);
+    });
+    // LRU of 32 KB blocks
+    const long capb = CAP_MB * 1024 * 1024 / 32768;
+    std::list<long> lru;
+    std::unordered_map<long, std::list<long>::iterator> where;
+    long acc = 0, miss = 0;
+    auto touch = [&](long key) {
+        acc++;
+        auto it = where.find(key);
+        if (it != where.end()) { lru.splice(lru.begin(), lru, it->second); return; }
+        miss++;
+        lru.push_front(key);
+        where[key] = lru.begin();
+        if ((long)lru.size() > capb) { where.erase(lru.back()); lru.pop_back(); }
+    };
+    auto keyA = [&](int q, int p, int kb, int tm) { return (((long)q * 4096 + p) * 4096 + kb) * 256 + tm; };
+    auto keyB = [&](int q, int p, int kb, int tn) { return ((((long)q * 4096 + p) * 4096 + kb) * 256 + tn) | (1L << 62); };
+    std::vector<int> hot(slot + ncls + 1, 0);
+    struct PairState { int u = -1; int t = 0, npos = 0, pos = 0, nblk = 0, np = 0; std::vector<std::pair<long, long>> q; size_t qi = 0; int stall = 0; };
+    std::vector<PairState> ps(NPAIR);
+    size_t next = 0;
+    auto nblk_of = [&](int np) { return KMODE == 2 ? (PBLK > 0 && np > PBLK ? (np + PBLK / 2) / PBLK : 1) : (PBLK > 0 && np > PBLK ? (np + PBLK - 1) / PBLK : 1); };
+    auto pfirst = [&](int np, int nblk, int j) { return KMODE == 2 ? (j >= nblk ? np + 1 : j * PBLK + 1) : j * np / nblk + 1; };
+    auto start = [&](PairState &P) -> bool {
+        if (next >= units.size()) { P.u = -1; return false; }
+        P.u = (int)next++;
+        const Unit &w = units[P.u];
+        int nkb = w.b - w.a;
+        P.np = w.r; P.nblk = nblk_of(P.np); P.npos = P.nblk * nkb; P.t = 0;
+        int rot = 0;
+        if (KMODE == 1) { int h = hot[w.slot]; rot = (h > 0 && h < P.npos) ? h : 0; }
+        else if (KMODE == 2) { int h = hot[w.cls]; int hk = h % nkb, hb = (h / nkb) % 1024; rot = (h > 0 && hb < P.nblk) ? hb * nkb + hk : 0; }
+        P.pos = rot; P.q.clear(); P.qi = 0;
+        return true;
+    };
+    auto fill = [&](PairState &P) {   // the loads of the unit's next position
+        const Unit &w = units[P.u];
+        int nkb = w.b - w.a;
+        int blk = P.pos / nkb, kbi = P.pos % nkb;
+        int kb = w.rev ? w.b - 1 - kbi : w.a + kbi;
+        int p0 = pfirst(P.np, P.nblk, blk), p1 = pfirst(P.np, P.nblk, blk + 1) - 1;
+        if (KMODE == 1) hot[w.slot] = P.pos; else if (KMODE == 2) hot[w.cls] = blk * nkb + kbi;
+        P.q.clear(); P.qi = 0;
+        if (p0 > 1) P.q.push_back({keyA(w.job, p0 - 1, kb, w.tm), -1});
+        for (int p = p0; p <= p1; p++) P.q.push_back({keyA(w.job, p, kb, w.tm), keyB(w.job, w.r + 1 - p, kb, w.tn)});
+        if (++P.pos == P.npos) P.pos = 0;
+        P.t++;
+    };
+    for (auto &P : ps) if (start(P)) fill(P);
+    unsigned rng = 12345;
+    long steps = 0;
+    for (;;) {
+        bool any = false;
+        for (int i = 0; i < NPAIR; i++) {
+            PairState &P = ps[i];
+            if (P.u < 0) continue;
+            any = true;
+            if (JITTER) { rng = rng * 1103515245u + 12345u; if ((rng >> 16) % 100 < (unsigned)JITTER) continue; }
+            if (P.qi == P.q.size()) {
+                if (P.t == P.npos) { if (!start(P)) continue; }
+                fill(P);
+            }
+            auto ld = P.q[P.qi++];
+            touch(ld.first);
+            if (ld.second >= 0) touch(ld.second);
+        }
+        if (!any) break;
+        steps++;
+    }
+    const double gb = miss * 32768.0 / 1e9;
+    printf("units %zu classes %d accesses %ld misses %ld -> DRAM operand reads %.1f GB (accessed %.1f GB), steps %ld\n",
+           units.size(), ncls, acc, miss, gb, acc * 32768.0 / 1e9, steps);
+}
