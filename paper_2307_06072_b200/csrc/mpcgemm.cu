@@ -140,12 +140,19 @@ StageEvents *stage_events(int dev) {
 }
 
 // ---------------------------------------------------------------- plans (work lists)
+// the fold's group-of-three slot order may be used (MPCGEMM_FOLD_UNIC != 0, no shared-memory-limbs fold)
+bool fold_unic_allowed() {
+    const char *u = getenv("MPCGEMM_FOLD_UNIC");
+    return !(u && atoi(u) == 0) && !getenv("MPCGEMM_FOLD_SFIX");
+}
+
 struct PlanKey {
     int64_t m, n, k; int s, method, BM, BN, grid, simt, maxkb, g2, order;
     std::vector<int32_t> sblk;   // NEXT-4: per-256-row-block slice counts (empty: s everywhere)
+    int unic_ok = fold_unic_allowed() ? 1 : 0;
     bool operator<(const PlanKey &o) const {
-        return std::tie(m, n, k, s, method, BM, BN, grid, simt, maxkb, g2, order, sblk) <
-               std::tie(o.m, o.n, o.k, o.s, o.method, o.BM, o.BN, o.grid, o.simt, o.maxkb, o.g2, o.order, o.sblk);
+        return std::tie(m, n, k, s, method, BM, BN, grid, simt, maxkb, g2, order, sblk, unic_ok) <
+               std::tie(o.m, o.n, o.k, o.s, o.method, o.BM, o.BN, o.grid, o.simt, o.maxkb, o.g2, o.order, o.sblk, o.unic_ok);
     }
 };
 struct Plan {
@@ -154,6 +161,7 @@ struct Plan {
     int32_t *d_slotinfo = nullptr;
     int nunits = 0, nslots = 0, grid = 0;
     bool uni1 = false;             // every (job, diagonal) has exactly one chunk (3 slots per diagonal)
+    bool unic = false;             // 3 jobs and, per diagonal, the same chunk count for every job
     int64_t mma = 0;
     JobDesc jobs[kMaxJobs];
     int njobs = 0, partsA = 0, partsB = 0;
@@ -237,17 +245,36 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
     // slot numbers follow the fold's consumption order: r = s+1 .. 2, job, chunk
     for (const Segment &sg : segs)
         for (int d = 0; d < sg.G; d++) slotinfo[(sg.q * (s + 2) + sg.r + d) * 2 + 1] = (int32_t)sg.nch;
+    // slots of one diagonal r: in the order (job, chunk), or -- when the 3 jobs have equal chunk
+    // counts on every diagonal (unic) -- (chunk, job), so the fold reads a diagonal as groups of
+    // one chunk per job at fixed offsets.  (One chunk everywhere, uni1: both orders coincide.)
+    // slotinfo keeps each (job, r)'s first slot (job 0's is the diagonal's first either way)
     int nslots = 0;
     const int rtop = key.method == 0 ? 2 : s + 1;
-    for (int r = rtop; r >= 2; r--)
-        for (int q = 0; q < P.njobs; q++) {
-            slotinfo[(q * (s + 2) + r) * 2] = nslots;
-            nslots += slotinfo[(q * (s + 2) + r) * 2 + 1];
-        }
-    auto base = [&](int q, int r) { return slotinfo[(q * (s + 2) + r) * 2]; };
+    auto cnt = [&](int q, int r) { return slotinfo[(q * (s + 2) + r) * 2 + 1]; };
     P.uni1 = P.njobs == 3;
+    P.unic = P.njobs == 3 && key.unic_ok;
     for (int r = 2; r <= rtop; r++)
-        for (int q = 0; q < P.njobs; q++) P.uni1 = P.uni1 && slotinfo[(q * (s + 2) + r) * 2 + 1] == 1;
+        for (int q = 0; q < P.njobs; q++) {
+            P.uni1 = P.uni1 && cnt(q, r) == 1;
+            P.unic = P.unic && cnt(q, r) == cnt(0, r);
+        }
+    std::vector<std::vector<int32_t>> slotid((size_t)P.njobs * (s + 2));
+    for (int r = rtop; r >= 2; r--) {
+        int maxc = 0;
+        for (int q = 0; q < P.njobs; q++) maxc = std::max(maxc, cnt(q, r));
+        auto put = [&](int q, int c) {
+            if (c == 0) slotinfo[(q * (s + 2) + r) * 2] = nslots;
+            slotid[(size_t)q * (s + 2) + r].push_back(nslots++);
+        };
+        if (P.unic)
+            for (int c = 0; c < maxc; c++)
+                for (int q = 0; q < P.njobs; q++) put(q, c);
+        else
+            for (int q = 0; q < P.njobs; q++)
+                for (int c = 0; c < cnt(q, r); c++) put(q, c);
+    }
+    auto slot_of = [&](int q, int r, int64_t c) { return slotid[(size_t)q * (s + 2) + r][(size_t)c]; };
     std::vector<WorkUnit> units;
     // NEXT-4: a row tile of block b takes the segments whose first diagonal r <= sblk[b] + 1; a
     // pair (r, r+1) with r = sblk[b] + 1 becomes a G = 3 unit computing D_r alone
@@ -277,12 +304,12 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
                         if (!in_tri(tm, r)) continue;
                         const int32_t rev = serp && ((r >> 1) & 1) ? (1 << 16) : 0;
                         if (!in_tri(tm, r + 1)) {              // block's last diagonal is r: D_r alone
-                            units.push_back({q | (3 << 8) | rev | hint(q, a, b), (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
+                            units.push_back({q | (3 << 8) | rev | hint(q, a, b), (int32_t)tm, (int32_t)tn, r, a, b, slot_of(q, r, c), -1});
                             P.mma += np * kk_sum(a, b) * (r - 1);
                             continue;
                         }
                         units.push_back({q | (2 << 8) | rev | hint(q, a, b), (int32_t)tm, (int32_t)tn, r, a, b,
-                                         base(q, r) + (int32_t)c, base(q, r + 1) + (int32_t)c});
+                                         slot_of(q, r, c), slot_of(q, r + 1, c)});
                         P.mma += np * kk_sum(a, b) * (2 * r - 1);
                     }
             }
@@ -293,7 +320,7 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
                 for (int64_t tm = 0; tm < tiles_m; tm++)
                     for (int64_t tn = 0; tn < tiles_n; tn++) {
                         if (!in_tri(tm, r)) continue;
-                        units.push_back({q | (1 << 8), (int32_t)tm, (int32_t)tn, r, a, b, base(q, r) + (int32_t)c, -1});
+                        units.push_back({q | (1 << 8), (int32_t)tm, (int32_t)tn, r, a, b, slot_of(q, r, c), -1});
                         P.mma += (int64_t)(b - a) * (kBK / 32) - (b / KB - a / KB) * (kBK / 32 - kkl);
                     }
             }
@@ -750,6 +777,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         F.ldF = (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign;
         F.sblk = sblk.empty() ? nullptr : mv.sblk + (r0 >> kSBlkShift);    // NEXT-4: per-block triangles
         F.uni1 = plan->uni1 ? 1 : 0;
+        F.unic = plan->unic ? 1 : 0;
         fix = (uint64_t *)((uint8_t *)partials +
                            align_up((size_t)plan->nslots * ((mr + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
         F.fix = fix;
@@ -780,6 +808,8 @@ struct DevPlanSet {
     int s_lo = 0, s_hi = 0;
     int64_t nslots_max = 0;
     bool uni1 = true;                    // every candidate has one chunk per (job, diagonal)
+    bool unic = true;                    // every candidate: equal chunk counts across the jobs
+    bool chunked_unic = false;           // some candidate has (chunk, job) slot order with > 1 chunk
     size_t main_bytes = 0;               // workspace of the largest candidate
 };
 std::map<std::tuple<int, int64_t, int64_t, int64_t, int, int, int, int>, DevPlanSet> g_devplans;
@@ -804,8 +834,13 @@ int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int met
         hp.push_back(DevPlan{plan->d_units, plan->d_counter + 1, plan->d_slotinfo, s, plan->nunits, plan->nslots, 0});
         S.nslots_max = std::max<int64_t>(S.nslots_max, plan->nslots);
         S.uni1 = S.uni1 && plan->uni1;
+        S.unic = S.unic && plan->unic;
+        S.chunked_unic = S.chunked_unic || (plan->unic && !plan->uni1);
         S.main_bytes = std::max(S.main_bytes, layout_for(m, n, k, s, method, geo.maxkb, prec, false).main);
     }
+    // one fold variant serves every candidate: their slot orders must agree (with the present job
+    // structures a chunked (chunk, job)-ordered plan is 3M, and then every candidate is)
+    if (!S.unic && S.chunked_unic) return fail(MPCGEMM_ERR_ARG, "device rule: candidate plans with different slot orders");
     if (cudaMalloc(&S.d_plans, sizeof(DevPlan) * hp.size()) != cudaSuccess ||
         cudaMalloc(&S.d_counter, sizeof(int32_t)) != cudaSuccess)
         return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc device plans");
@@ -905,7 +940,7 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     F.eA = mv.eA; F.eB = mv.eB; F.Cre = dmo(C->re); F.Cim = dmo(C->im);
     F.beta = 0; F.alpha_neg = 0; F.C0re = dm(C->re); F.C0im = dm(C->im);
     F.ldF = (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign;
-    F.fix = fix; F.drs = mv.drs; F.nslots = S->nslots_max; F.uni1 = S->uni1 ? 1 : 0;
+    F.fix = fix; F.drs = mv.drs; F.nslots = S->nslots_max; F.uni1 = S->uni1 ? 1 : 0; F.unic = S->unic ? 1 : 0;
     {
         Nvtx r("mpcgemm.a5a6_fold_normalize");
         CK(fold_normalize_launch(F, st));

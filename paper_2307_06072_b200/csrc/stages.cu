@@ -1133,11 +1133,17 @@ MPC_DEV void store_ept(uint64_t *dst, const uint64_t *v) {
 // UNI1 (with TMAP): every (job, diagonal) has exactly one chunk (3 slots per diagonal, in job
 // order), so a ring entry is one PAIR of diagonals (6 slots, one TMA load) and the consumers read
 // it at fixed offsets: one wait and one release per pair, no per-slot bookkeeping
-template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRing, bool TMAP = false, bool UNI1 = false>
+// UNIC (UPER > 0): the three jobs have equal chunk counts on every diagonal, so a diagonal's
+// slots are groups of three (chunk c of job 0, 1, 2); a ring entry holds UPER / 3 whole groups and
+// the consumers read a group at fixed offsets with one ring check per group instead of per slot
+template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRing, bool TMAP = false, bool UNI1 = false,
+          int UPER = 0>
 __global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : (SFIX ? 3 : 6))
 fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pmap)
 {
-    constexpr int PER = UNI1 ? 6 : kFoldPer;          // slots per ring entry
+    constexpr bool UNIC = UPER > 0;
+    static_assert(UPER % 3 == 0, "UNIC entries are whole groups of three slots");
+    constexpr int PER = UNI1 ? 6 : UNIC ? UPER : kFoldPer;   // slots per ring entry
     constexpr int NCONS = COLS / EPT;                 // consumer threads
     extern __shared__ __align__(128) uint8_t fsm_raw[];
     if (F.drs && F.drs->status) return;              // device rule: s outside the planned range
@@ -1253,22 +1259,39 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
             addr += (uint32_t)COLS * 12u;
 #pragma unroll
             for (int x = 0; x < EPT; x++) { u0[x] = v[x]; u1[x] = w1[x]; u2[x] = w2[x]; }
-        } else {
-        for (int c = cntq[r]; c > 0; c--) {
-            next(v);
+        } else if constexpr (UNIC) {                  // c groups (chunk c of jobs 0, 1, 2)
+            for (int c = cntq[r]; c > 0; c--) {
+                int32_t w1[EPT], w2[EPT];
+                if (fill == 0) mbar_wait(&full[e], ph);
+                IntVec<EPT>::get_shared(addr, v);
+                IntVec<EPT>::get_shared(addr + (uint32_t)COLS * 4u, w1);
+                IntVec<EPT>::get_shared(addr + (uint32_t)COLS * 8u, w2);
+                addr += (uint32_t)COLS * 12u;
 #pragma unroll
-            for (int x = 0; x < EPT; x++) u0[x] += v[x];
-        }
-        for (int c = cntq[(s + 2) + r]; c > 0; c--) {
-            next(v);
+                for (int x = 0; x < EPT; x++) { u0[x] += v[x]; u1[x] += w1[x]; u2[x] += w2[x]; }
+                fill += 3;
+                if (fill == PER) {
+                    fill = 0;
+                    release();
+                    if (++e == RING) { e = 0; ph ^= 1; addr = ring0; }
+                }
+            }
+        } else {                                      // slots in the order (job, chunk)
+            for (int c = cntq[r]; c > 0; c--) {
+                next(v);
 #pragma unroll
-            for (int x = 0; x < EPT; x++) u1[x] += v[x];
-        }
-        for (int c = cntq[2 * (s + 2) + r]; c > 0; c--) {
-            next(v);
+                for (int x = 0; x < EPT; x++) u0[x] += v[x];
+            }
+            for (int c = cntq[(s + 2) + r]; c > 0; c--) {
+                next(v);
 #pragma unroll
-            for (int x = 0; x < EPT; x++) u2[x] += v[x];
-        }
+                for (int x = 0; x < EPT; x++) u1[x] += v[x];
+            }
+            for (int c = cntq[2 * (s + 2) + r]; c > 0; c--) {
+                next(v);
+#pragma unroll
+                for (int x = 0; x < EPT; x++) u2[x] += v[x];
+            }
         }
 #pragma unroll
         for (int x = 0; x < EPT; x++) {
@@ -1410,10 +1433,11 @@ static bool fold_sfix(int s, bool beta) {
     return fold_smem(s, kSfixCols, true, kSfixRing) <= 220 * 1024;
 }
 
-template <int COLS, bool BETA, bool SFIX, int EPT, int RING, bool TMAP = false, bool UNI1 = false>
+template <int COLS, bool BETA, bool SFIX, int EPT, int RING, bool TMAP = false, bool UNI1 = false, int UPER = 0>
 static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
-    const size_t sm = fold_smem(F.s, COLS, SFIX, RING, UNI1 ? 6 : kFoldPer);
-    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING, TMAP, UNI1>;
+    constexpr int PER = UNI1 ? 6 : UPER > 0 ? UPER : kFoldPer;
+    const size_t sm = fold_smem(F.s, COLS, SFIX, RING, PER);
+    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING, TMAP, UNI1, UPER>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (int64_t)kRowBlk * ((F.n + COLS - 1) / COLS) * ((F.m + kRowBlk - 1) / kRowBlk);
@@ -1423,7 +1447,7 @@ static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
         // the partial planes of all (row block, strip) pairs: nslots is the launch's (the device
         // rule's plans have at most F.nslots slots and share the layout's base)
         const int64_t gslots = ((F.m + kRowBlk - 1) / kRowBlk) * F.nstrips * F.nslots;
-        if (encode_partials_map(map, F.partials, gslots, UNI1 ? 6 : kFoldPer)) return cudaErrorInvalidValue;
+        if (encode_partials_map(map, F.partials, gslots, PER)) return cudaErrorInvalidValue;
     }
     kern<<<(unsigned)blocks, COLS / EPT + 32, sm, st>>>(F, *reinterpret_cast<const CUtensorMap *>(map));
     return cudaGetLastError();
@@ -1436,11 +1460,22 @@ cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
     // (device rule: F.nslots is the largest candidate's slot count, so the map covers the chosen plan)
     const bool tmap = !getenv("MPCGEMM_FOLD_BULK");
     const bool uni1 = tmap && F.uni1 && !getenv("MPCGEMM_FOLD_NOUNI1");
+    // F.unic: the plan's slots are in (chunk, job) order -- only the UNIC consumer reads that
+    // order (the plan chose it only if MPCGEMM_FOLD_UNIC != 0 and no MPCGEMM_FOLD_SFIX); the entry
+    // size is 6 (default), 9 or 12 slots
+    const char *ue = getenv("MPCGEMM_FOLD_UNIC");
+    const int unic = F.unic && !uni1 ? (tmap && ue && (atoi(ue) == 9 || atoi(ue) == 12) ? atoi(ue) : 6) : 0;
     if (F.beta) return uni1 ? fold_launch_t<256, true, false, kFoldEPT, 5, true, true>(F, st)
+                     : unic ? (tmap ? fold_launch_t<256, true, false, kFoldEPT, 5, true, false, 6>(F, st)
+                                    : fold_launch_t<256, true, false, kFoldEPT, 5, false, false, 6>(F, st))
                      : tmap ? fold_launch_t<256, true, false, kFoldEPT, kFoldRing, true>(F, st)
                             : fold_launch_t<256, true, false, kFoldEPT, kFoldRing>(F, st);
-    if (fold_sfix(F.s, false)) return fold_launch_t<kSfixCols, false, true, 1, kSfixRing>(F, st);
+    if (!unic && fold_sfix(F.s, false)) return fold_launch_t<kSfixCols, false, true, 1, kSfixRing>(F, st);
     return uni1 ? fold_launch_t<256, false, false, kFoldEPT, 5, true, true>(F, st)
+         : unic == 12 ? fold_launch_t<256, false, false, kFoldEPT, 3, true, false, 12>(F, st)
+         : unic == 9 ? fold_launch_t<256, false, false, kFoldEPT, 4, true, false, 9>(F, st)
+         : unic ? (tmap ? fold_launch_t<256, false, false, kFoldEPT, 5, true, false, 6>(F, st)
+                        : fold_launch_t<256, false, false, kFoldEPT, 5, false, false, 6>(F, st))
          : tmap ? fold_launch_t<256, false, false, kFoldEPT, kFoldRing, true>(F, st)
                 : fold_launch_t<256, false, false, kFoldEPT, kFoldRing>(F, st);
 }

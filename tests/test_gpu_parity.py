@@ -516,7 +516,8 @@ def test_fp64_carrier_bitexact(method, m, n, k, prec, spread, d):
 
 
 @pytest.mark.parametrize("env", ["MPCGEMM_FOLD_BULK", "MPCGEMM_FOLD_SFIX", "MPCGEMM_SPLIT_V1", "MPCGEMM_FOLD_NOUNI1",
-                                 "MPCGEMM_SPLIT_BYTESTG", "MPCGEMM_RESERVE_SMS", "MPCGEMM_HALFN=0"])
+                                 "MPCGEMM_SPLIT_BYTESTG", "MPCGEMM_RESERVE_SMS", "MPCGEMM_HALFN=0",
+                                 "MPCGEMM_FOLD_UNIC=0", "MPCGEMM_FOLD_UNIC=9", "MPCGEMM_FOLD_UNIC=12"])
 @pytest.mark.parametrize("method", ["3M", "4M"])
 def test_stage_variants_bitexact(env, method, monkeypatch):
     """The fold's bulk-copy producer, shared-memory-limbs and generic (non pair-entry) variants and the
