@@ -1000,6 +1000,7 @@ MPC_DEV void normalize_store(uint64_t *fix, int64_t stride, int Lc, int64_t e0, 
     round_store(fix, stride, Lc, e0, neg != alpha_neg, prec, L, sign_out, exp_out, limbs_out);
 }
 
+
 // NEXT-2: RNE(C0 + (-1)^alpha_neg V 2^e0), one rounding of the exact sum.  V = fix[0..Lc)
 // (two's complement); the sum is formed in sign-magnitude in R = fix[Lc..Lc+Lw) over a window
 // of 64 Lw >= 64 (Lc + L + 3) bits below the larger operand's top; bits of the smaller operand
@@ -1354,6 +1355,12 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
             }
         b++;
     }
+    // the rounding reads each (element, part)'s limbs from a shared-memory column carved out of the
+    // ring, which is free once every consumer is past its last diagonal (dynamic limb indexing on
+    // a thread-local copy went to local memory, ~a third of the fold's stall samples at config 4)
+    constexpr int RING_BYTES = RING * PER * COLS * 4;
+    const bool smem_norm = !BETA && !SFIX && Lc0 * NCONS * 8 <= RING_BYTES && !F.norm_generic;
+    if (smem_norm) asm volatile("bar.sync 1, %0;" ::"r"(NCONS) : "memory");
     if (!live) return;
     // the final carries at bit 8 sr, sign-extended to Lc0 limbs
     const int l0 = sr >> 3, o = 8 * (sr & 7);
@@ -1404,6 +1411,19 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
             // copy each part's limbs to a thread-local array with independent (batched) loads,
             // then magnitude + RNE on the L1-resident copy (the scratch reads were a dependent
             // chain of global loads -- profiles/ncu_hbm_r1o.md)
+            if (smem_norm) {
+                uint64_t *colp = reinterpret_cast<uint64_t *>(ring) + tid;   // [limb][consumer]
+#pragma unroll 1
+                for (int p = 0; p < 2; p++) {
+                    const uint64_t *src = fixg + x + (int64_t)p * Lc0 * lstride;
+#pragma unroll 8
+                    for (int l = 0; l < Lc0; l++) colp[l * NCONS] = src[(int64_t)l * lstride];
+                    const DMatOut &Co = p ? F.Cim : F.Cre;
+                    const int64_t oo = p ? oj : oi;
+                    normalize_store(colp, NCONS, Lc0, e0, F.alpha_neg, F.prec, F.L, Co.sign + oo, Co.exp + oo, Co.limbs + oo * F.L);
+                }
+                continue;
+            }
             uint64_t loc[kMaxSlices / 8 + 3];
 #pragma unroll 1
             for (int p = 0; p < 2; p++) {
