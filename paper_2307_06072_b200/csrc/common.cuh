@@ -229,6 +229,13 @@ MPC_DEV void tma_load_3d(void *dst, const void *tmap, uint64_t *bar, int c0, int
         ::"r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 
+MPC_DEV void tma_load_3d_hint(void *dst, const void *tmap, uint64_t *bar, int c0, int c1, int c2, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;"
+        ::"r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol) : "memory");
+}
+
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0)
 MPC_DEV void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -244,6 +251,22 @@ MPC_DEV uint64_t l2_policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+MPC_DEV uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+MPC_DEV uint64_t l2_policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+MPC_DEV void st_global_v2u64_hint(void *ptr, uint64_t a, uint64_t b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(ptr), "l"(a), "l"(b), "l"(pol) : "memory");
+}
+MPC_DEV void st_global_u64_hint(void *ptr, uint64_t a, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(ptr), "l"(a), "l"(pol) : "memory");
 }
 MPC_DEV void st_global_v4_hint(void *ptr, int a, int b, int c, int d, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;"

@@ -89,6 +89,7 @@ struct FoldParams {
     int32_t uni1;                // every (job, diagonal) of the plan has exactly one chunk
     int32_t unic;                // 3 jobs with equal chunk counts per diagonal (slots in groups of 3)
     int32_t norm_generic;        // (cross-check) round through the generic local-memory path
+    int32_t l2hint;              // partial loads evict-first, fixed-point scratch stores evict-last
 };
 constexpr int kFoldLdAlign = 4;  // scratch pitch: a multiple of every fold variant's outputs per thread
 size_t fold_scratch_words(int64_t m, int64_t ldF, int s, int L, bool beta);

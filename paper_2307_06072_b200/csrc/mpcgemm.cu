@@ -779,6 +779,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         F.uni1 = plan->uni1 ? 1 : 0;
         F.unic = plan->unic ? 1 : 0;
         F.norm_generic = env_int("MPCGEMM_NORM_GENERIC", 0);
+        F.l2hint = env_int("MPCGEMM_FOLD_L2HINT", 1);
         fix = (uint64_t *)((uint8_t *)partials +
                            align_up((size_t)plan->nslots * ((mr + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256));
         F.fix = fix;
@@ -943,6 +944,7 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     F.ldF = (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign;
     F.fix = fix; F.drs = mv.drs; F.nslots = S->nslots_max; F.uni1 = S->uni1 ? 1 : 0; F.unic = S->unic ? 1 : 0;
     F.norm_generic = env_int("MPCGEMM_NORM_GENERIC", 0);
+    F.l2hint = env_int("MPCGEMM_FOLD_L2HINT", 1);
     {
         Nvtx r("mpcgemm.a5a6_fold_normalize");
         CK(fold_normalize_launch(F, st));

@@ -1119,12 +1119,19 @@ template <> struct IntVec<4> {
 // (no global round trip); otherwise (NEXT-2 sums, or s too large for shared memory) they go to
 // the global scratch fix[part][limb][m*ldF]
 // the EPT adjacent elements' words of one limb (16-byte stores for pairs)
-template <int EPT>
-MPC_DEV void store_ept(uint64_t *dst, const uint64_t *v) {
-    if constexpr (EPT == 1) { *dst = v[0]; }
+// (GLOBAL: dst is the global scratch, stored with an L2 policy; else shared memory)
+template <int EPT, bool GLOBAL>
+MPC_DEV void store_ept(uint64_t *dst, const uint64_t *v, uint64_t pol) {
+    if constexpr (!GLOBAL) {
+        if constexpr (EPT == 1) { *dst = v[0]; }
+        else {
+#pragma unroll
+            for (int x = 0; x < EPT; x += 2) *reinterpret_cast<ulonglong2 *>(dst + x) = make_ulonglong2(v[x], v[x + 1]);
+        }
+    } else if constexpr (EPT == 1) { st_global_u64_hint(dst, v[0], pol); }
     else {
 #pragma unroll
-        for (int x = 0; x < EPT; x += 2) *reinterpret_cast<ulonglong2 *>(dst + x) = make_ulonglong2(v[x], v[x + 1]);
+        for (int x = 0; x < EPT; x += 2) st_global_v2u64_hint(dst + x, v[x], v[x + 1], pol);
     }
 }
 
@@ -1187,10 +1194,12 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
             const int g0 = (int)((((i >> 7) * F.nstrips + (j0 >> 8)) * nslots));   // global slot of slot 0
             const int row = (int)(i & (kRowBlk - 1));
             int e = 0; uint32_t ph = 0;
+            // partial planes are read once: evict-first, so the fixed-point scratch stays in L2
+            const uint64_t ppol = F.l2hint ? l2_policy_evict_first() : l2_policy_evict_normal();
             for (int sl = sl0; sl < nslots; sl += PER) {
                 mbar_wait(&empty[e], ph ^ 1);
                 mbar_arrive_expect_tx(&full[e], (uint32_t)(PER * COLS * 4));
-                tma_load_3d(ring + e * PER * COLS, &pmap, &full[e], 0, row, g0 + sl);
+                tma_load_3d_hint(ring + e * PER * COLS, &pmap, &full[e], 0, row, g0 + sl, ppol);
                 if (++e == RING) { e = 0; ph ^= 1; }
             }
         } else if (lane == 0) {
@@ -1211,6 +1220,8 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
     // the global scratch fix[part][limb][m*ldF] (column = element), read back by the rounding.
     const int col = EPT * tid;
     const int64_t jj = j0 + col;                      // first of the EPT elements
+    // the fixed-point scratch is read back by the same thread at the end: keep it in L2
+    const uint64_t fpol = F.l2hint ? l2_policy_evict_last() : l2_policy_evict_normal();
     const int64_t lstride = SFIX ? (int64_t)COLS : F.m * F.ldF;   // limb stride
     uint64_t *fixg = SFIX ? fixs + col : F.fix + i * F.ldF + jj;
     int64_t t0[EPT], t1[EPT], t2[EPT];
@@ -1333,7 +1344,7 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
                 cr[p][x] = acc >> 16;
             }
         if ((b & 7) == 6) {                           // a 64-bit limb complete
-            if (live) { store_ept<EPT>(lp0, cur[0]); store_ept<EPT>(lp1, cur[1]); }
+            if (live) { store_ept<EPT, !SFIX>(lp0, cur[0], fpol); store_ept<EPT, !SFIX>(lp1, cur[1], fpol); }
             lp0 += lstride; lp1 += lstride;
 #pragma unroll
             for (int x = 0; x < EPT; x++) cur[0][x] = cur[1][x] = 0;
@@ -1377,9 +1388,9 @@ fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pm
         uint64_t w0[EPT], w1[EPT], sx[EPT];
 #pragma unroll
         for (int x = 0; x < EPT; x++) { w0[x] = w[x][0]; w1[x] = w[x][1]; sx[x] = cr[p][x] < 0 ? ~0ull : 0ull; }
-        store_ept<EPT>(fx + (int64_t)l0 * lstride, w0);
-        store_ept<EPT>(fx + (int64_t)(l0 + 1) * lstride, w1);
-        for (int l = l0 + 2; l < Lc0; l++) store_ept<EPT>(fx + (int64_t)l * lstride, sx);
+        store_ept<EPT, !SFIX>(fx + (int64_t)l0 * lstride, w0, fpol);
+        store_ept<EPT, !SFIX>(fx + (int64_t)(l0 + 1) * lstride, w1, fpol);
+        for (int l = l0 + 2; l < Lc0; l++) store_ept<EPT, !SFIX>(fx + (int64_t)l * lstride, sx, fpol);
     }
 #pragma unroll 1
     for (int x = 0; x < EPT; x++) {
