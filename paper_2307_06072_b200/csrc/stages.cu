@@ -273,6 +273,21 @@ split_kernel(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, i
     }
 }
 
+// 64-bit add with carry-in c (0/1) and carry-out into c, as one PTX carry chain (the compiler's
+// compare-based carries cost about twice the instructions; the split is issue-bound)
+MPC_DEV uint64_t add64_carry(uint64_t a, uint64_t b, uint32_t &c) {
+    uint32_t lo, hi, co;
+    asm("{\n\t.reg .u32 t;\n\t"
+        "add.cc.u32 t, %3, 0xFFFFFFFF;\n\t"      // CF = c
+        "addc.cc.u32 %0, %4, %5;\n\t"
+        "addc.cc.u32 %1, %6, %7;\n\t"
+        "addc.u32 %2, 0, 0;\n\t}"
+        : "=r"(lo), "=r"(hi), "=r"(co)
+        : "r"(c), "r"((uint32_t)a), "r"((uint32_t)b), "r"((uint32_t)(a >> 32)), "r"((uint32_t)(b >> 32)));
+    c = co;
+    return ((uint64_t)hi << 32) | lo;
+}
+
 // TMA-staged split (L in {2, 4, 8, 16}): a CTA takes kSplitT consecutive k of one line; one thread
 // issues two 3-D TMA loads (Re, Im) of the 256 entries' limbs into shared memory -- coalesced,
 // vectorised, every DRAM sector read once; the rows land swizzled (the swizzle span = one 8L-byte
@@ -337,7 +352,8 @@ MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, 
         asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(myrow + (uint32_t)(p * kSplitT * ROW) + ((uint32_t)(8 * l) ^ xm)));
         return v;
     };
-    int64_t li[2]; int bo[2]; uint64_t lo[2], nc[2] = {1, 1};
+    int64_t li[2]; int bo[2]; uint64_t lo[2], nm[2];
+    uint32_t nc[2];                                   // two's complement: x ^ nm + carry (nc starts at neg)
     bool zero[2];
 #pragma unroll
     for (int p = 0; p < 2; p++) {
@@ -347,8 +363,10 @@ MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, 
         bo[p] = (int)(pos0 - (li[p] << 6));
         lo[p] = zero[p] ? 0ull : limb(p, li[p]);
         neg[p] = neg[p] && !zero[p];
+        nm[p] = neg[p] ? ~0ull : 0ull;
+        nc[p] = neg[p] ? 1u : 0u;
     }
-    uint64_t csum = 0, ch[3] = {0, 0, 0};
+    uint32_t csum = 0, ch[3] = {0, 0, 0};
     const int64_t plane = lines * kp;
     const int64_t rowlen = min((int64_t)kSplitT, kp - k0);          // bytes of this CTA's plane rows
     const int nwords = (s + 7) / 8;
@@ -383,23 +401,13 @@ MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, 
             const uint64_t hi = zero[p] ? 0ull : limb(p, li[p] + 1);
             uint64_t x = bo[p] ? ((lo[p] >> bo[p]) | (hi << (64 - bo[p]))) : lo[p];
             lo[p] = hi; li[p]++;
-            if (neg[p]) { const uint64_t t = ~x + nc[p]; nc[p] = (nc[p] && t == 0) ? 1ull : 0ull; x = t; }
-            y[p] = x;
+            y[p] = add64_carry(x ^ nm[p], 0ull, nc[p]);   // negation without a divergent branch
         }
-        {   // 3M: Re + Im (two's complement, with carry)
-            const uint64_t t = y[0] + y[1];
-            const uint64_t c1 = t < y[0];
-            y[2] = t + csum;
-            csum = c1 | (y[2] < t);
-        }
+        y[2] = add64_carry(y[0], y[1], csum);         // 3M: Re + Im (two's complement, with carry)
 #pragma unroll
         for (int p = 0; p < 3; p++) {                 // + H with carry, XOR 0x80 per byte -> staging
             if (p >= nparts) break;
-            const uint64_t t = y[p] + kH;
-            const uint64_t c1 = t < y[p];
-            const uint64_t z = t + ch[p];
-            ch[p] = c1 | (z < t);
-            const uint64_t d = z ^ kH;
+            const uint64_t d = add64_carry(y[p], kH, ch[p]) ^ kH;
             if constexpr (WS) {                          // [part][entry] words
                 asm volatile("st.shared.u64 [%0], %1;" :: "r"(smem_u32(stg) + (uint32_t)((p * kSplitT + tid) * 8)), "l"(d) : "memory");
             } else {
@@ -420,16 +428,29 @@ MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, 
                 const uint32_t qa = smem_u32(stg) + (uint32_t)qoff[it];
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w01.x), "=r"(w01.y), "=r"(w01.z), "=r"(w01.w) : "r"(qa) : "memory");
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w23.x), "=r"(w23.y), "=r"(w23.z), "=r"(w23.w) : "r"(qa + 16) : "memory");
-                int8_t *o = qptr[it];
+                // 4 x 4 byte transposes (8 permutes per 4 planes): entries e0..e3 = w01.{x,y},
+                // w01.{z,w}, w23.{x,y}, w23.{z,w} (low / high 32 bits); plane bt's word is byte bt
+                // of e0..e3
+                uint32_t pw[8];
 #pragma unroll
-                for (int bt = 0; bt < 8; bt++, o -= plane) {
-                    if (bt < nb) {
-                        const uint32_t sel = (uint32_t)((bt & 3) | (((bt & 3) + 4) << 4));
-                        const uint32_t x0 = bt < 4 ? w01.x : w01.y, x1 = bt < 4 ? w01.z : w01.w;
-                        const uint32_t x2 = bt < 4 ? w23.x : w23.y, x3 = bt < 4 ? w23.z : w23.w;
-                        const uint32_t v = __byte_perm(__byte_perm(x0, x1, sel), __byte_perm(x2, x3, sel), 0x5410);
-                        *reinterpret_cast<uint32_t *>(o) = v;
-                    }
+                for (int h = 0; h < 2; h++) {
+                    const uint32_t e0 = h ? w01.y : w01.x, e1 = h ? w01.w : w01.z;
+                    const uint32_t e2 = h ? w23.y : w23.x, e3 = h ? w23.w : w23.z;
+                    const uint32_t t0 = __byte_perm(e0, e1, 0x5140), t1 = __byte_perm(e2, e3, 0x5140);
+                    const uint32_t t2 = __byte_perm(e0, e1, 0x7362), t3 = __byte_perm(e2, e3, 0x7362);
+                    pw[4 * h + 0] = __byte_perm(t0, t1, 0x5410);
+                    pw[4 * h + 1] = __byte_perm(t0, t1, 0x7632);
+                    pw[4 * h + 2] = __byte_perm(t2, t3, 0x5410);
+                    pw[4 * h + 3] = __byte_perm(t2, t3, 0x7632);
+                }
+                int8_t *o = qptr[it];
+                if (nb == 8) {
+#pragma unroll
+                    for (int bt = 0; bt < 8; bt++, o -= plane) *reinterpret_cast<uint32_t *>(o) = pw[bt];
+                } else {
+#pragma unroll
+                    for (int bt = 0; bt < 8; bt++, o -= plane)
+                        if (bt < nb) *reinterpret_cast<uint32_t *>(o) = pw[bt];
                 }
                 qptr[it] -= ostep;
             }
