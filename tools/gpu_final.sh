@@ -17,6 +17,6 @@ print('launches', d['gpu_launches'], 'cpu', d.get('cpu_baseline',{}).get('value'
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-extra"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu list rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:slicegemm_tc2 -s 1 -c 1 -o gpurun_out/prof_gemm_$TAG $CMD > gpurun_out/ncu_gemm_$TAG.log 2>&1; echo "ncu gemm rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fold_normalize|split_tma_kernel" -s 0 -c 3 -o gpurun_out/prof_hbm_$TAG $CMD > gpurun_out/ncu_hbmf_$TAG.log 2>&1; echo "ncu hbm rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fold_normalize|split2?_tma_kernel" -s 0 -c 3 -o gpurun_out/prof_hbm_$TAG $CMD > gpurun_out/ncu_hbmf_$TAG.log 2>&1; echo "ncu hbm rc=$?"
 for f in gemm hbm; do ncu -i gpurun_out/prof_${f}_$TAG.ncu-rep --page raw --csv > gpurun_out/raw_${f}_$TAG.csv 2>/dev/null; python tools/ncu_raw_summary.py gpurun_out/raw_${f}_$TAG.csv > gpurun_out/sum_${f}_$TAG.txt 2>&1; done
 cat gpurun_out/sum_gemm_$TAG.txt | head -24
