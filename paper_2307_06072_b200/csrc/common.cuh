@@ -268,6 +268,12 @@ MPC_DEV void st_global_v2u64_hint(void *ptr, uint64_t a, uint64_t b, uint64_t po
 MPC_DEV void st_global_u64_hint(void *ptr, uint64_t a, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(ptr), "l"(a), "l"(pol) : "memory");
 }
+MPC_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+MPC_DEV void ld_shared_v4(uint32_t addr, uint32_t &a, uint32_t &b, uint32_t &c, uint32_t &d) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr) : "memory");
+}
 MPC_DEV void st_global_v4_hint(void *ptr, int a, int b, int c, int d, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;"
                  ::"l"(ptr), "r"(a), "r"(b), "r"(c), "r"(d), "l"(pol) : "memory");

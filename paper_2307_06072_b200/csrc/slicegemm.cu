@@ -267,7 +267,9 @@ struct Tc2Cfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 512;
     static constexpr int QN = 8;
-    static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 512;
+    static constexpr int EPI_PITCH = 144;              // epilogue transpose rows (32 int32 + pad)
+    static constexpr int EPI_BYTES = 4 * 32 * EPI_PITCH;
+    static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 512 + EPI_BYTES;
 };
 
 template <int STAGES>
@@ -291,6 +293,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     int32_t *uqr = uq + Cfg::QN;                      // each unit's k-phase rotation (both producers)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(uqr + Cfg::QN);
     uint8_t *skk = reinterpret_cast<uint8_t *>(tmem_slot + 1);   // per stage: MMA K-steps to issue
+    uint8_t *sE = smem + (size_t)STAGES * Cfg::STAGE_BYTES + 512;   // epilogue transposes [warp][32][pitch]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (P.drs && P.drs->status != 0) return;          // device rule: s outside the planned range
@@ -518,21 +521,40 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             const WorkUnit w = units[u];
             mbar_wait(tfull, tphase);
             tc_fence_after();
-            const int row = (P.dbg & 1) ? P.m : w.tm * 256 + (int)rank * 128 + q * 32 + lane;
+            // TMEM gives lane l row l: a direct store puts 32 rows' 16-byte pieces in one warp store
+            // (32 partial-sector writes) -- the drain then held up the next unit's MMAs (both
+            // accumulators are in use), e.g. 23 % of config 5's k = 128 GEMMs.  Each 32 x 32 block
+            // goes through a padded shared-memory transpose instead, so a warp store writes 4 whole
+            // 128-byte row segments; four 32-column TMEM loads are in flight per wait
+            const int row0 = w.tm * 256 + (int)rank * 128 + q * 32;        // this warp's first row
+            const uint32_t swa = smem_u32(sE) + (uint32_t)(q * 32 * Cfg::EPI_PITCH);
+            const int rsub = lane >> 3, piece = lane & 7;
             for (int acc = 0; acc < (unit_G(w) == 2 ? 2 : 1); acc++) {
                 const int64_t slot = acc ? w.slot1 : w.slot0;
 #pragma unroll 1
-                for (int c = 0; c < (half_n(w.tn) ? BN / 64 : BN / 32); c++) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+                for (int c0 = 0; c0 < (half_n(w.tn) ? BN / 64 : BN / 32); c0 += 4) {
+                    uint32_t v[4][32];
+#pragma unroll
+                    for (int j = 0; j < 4; j++)
+                        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + (c0 + j) * 32), v[j]);
                     tmem_ld_wait();
-                    const int col0 = w.tn * BN + c * 32;
-                    if (row < P.m) {
-                        int32_t *out = P.partials + part_off(row, col0, slot, nslots, P.nstrips);
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
 #pragma unroll
                         for (int g4 = 0; g4 < 8; g4++)
-                            st_global_v4_hint(out + 4 * g4, (int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2],
-                                              (int)v[4 * g4 + 3], pol);
+                            st_shared_v4(swa + (uint32_t)(lane * Cfg::EPI_PITCH + 16 * g4), v[j][4 * g4], v[j][4 * g4 + 1],
+                                         v[j][4 * g4 + 2], v[j][4 * g4 + 3]);
+                        __syncwarp();
+                        int32_t *out = P.partials + part_off(row0, w.tn * BN + (c0 + j) * 32, slot, nslots, P.nstrips) + 4 * piece;
+#pragma unroll
+                        for (int g = 0; g < 8; g++) {
+                            const int rr = 4 * g + rsub;
+                            uint32_t x0, x1, x2, x3;
+                            ld_shared_v4(swa + (uint32_t)(rr * Cfg::EPI_PITCH + 16 * piece), x0, x1, x2, x3);
+                            if (!(P.dbg & 1) && row0 + rr < P.m)
+                                st_global_v4_hint(out + (int64_t)rr * kStrip, (int)x0, (int)x1, (int)x2, (int)x3, pol);
+                        }
+                        __syncwarp();
                     }
                 }
             }
