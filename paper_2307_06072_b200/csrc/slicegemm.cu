@@ -55,7 +55,9 @@ struct TcCfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;           // two accumulators
     static constexpr int QN = 8;                       // unit-index queue depth
-    static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 512 /*barriers, queue*/;
+    static constexpr int EPI_PITCH = 144;              // epilogue transpose rows (32 int32 + pad)
+    static constexpr int EPI_BYTES = 4 * 32 * EPI_PITCH;
+    static constexpr size_t SMEM = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 512 /*barriers, queue*/ + EPI_BYTES;
 };
 
 // digit planes of step (pair, p, kb) of a unit
@@ -80,6 +82,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     int32_t *uq = reinterpret_cast<int32_t *>(qempty + Cfg::QN);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(uq + Cfg::QN);
     uint8_t *skk = reinterpret_cast<uint8_t *>(tmem_slot + 1);   // per stage: MMA K-steps to issue
+    uint8_t *sE = smem + (size_t)STAGES * Cfg::STAGE_BYTES + 512;   // epilogue transposes [warp][32][pitch]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (P.drs && P.drs->status != 0) return;          // device rule: s outside the planned range
@@ -225,21 +228,38 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             const WorkUnit w = units[u];
             mbar_wait(tfull, tphase);
             tc_fence_after();
-            const int row = w.tm * kBM + q * 32 + lane;
+            // (as the CTA-pair kernel: 32 x 32 blocks through a padded shared-memory transpose, a
+            // warp store = 4 whole 128-byte row segments; four TMEM loads per wait)
+            const int row0 = w.tm * kBM + q * 32;
+            const uint32_t swa = smem_u32(sE) + (uint32_t)(q * 32 * Cfg::EPI_PITCH);
+            const int rsub = lane >> 3, piece = lane & 7;
             for (int acc = 0; acc < (unit_G(w) == 2 ? 2 : 1); acc++) {
                 const int64_t slot = acc ? w.slot1 : w.slot0;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; c++) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), v);
+                for (int c0 = 0; c0 < BN / 32; c0 += 4) {
+                    uint32_t v[4][32];
+#pragma unroll
+                    for (int j = 0; j < 4; j++)
+                        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + (c0 + j) * 32), v[j]);
                     tmem_ld_wait();
-                    const int col0 = w.tn * BN + c * 32;      // 32 columns inside one 256-column strip
-                    if (row < P.m) {
-                        int32_t *out = P.partials + part_off(row, col0, slot, nslots, P.nstrips);
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
 #pragma unroll
                         for (int g4 = 0; g4 < 8; g4++)
-                            st_global_v4_hint(out + 4 * g4, (int)v[4 * g4], (int)v[4 * g4 + 1], (int)v[4 * g4 + 2],
-                                              (int)v[4 * g4 + 3], pol);
+                            st_shared_v4(swa + (uint32_t)(lane * Cfg::EPI_PITCH + 16 * g4), v[j][4 * g4], v[j][4 * g4 + 1],
+                                         v[j][4 * g4 + 2], v[j][4 * g4 + 3]);
+                        __syncwarp();
+                        // 32 columns inside one 256-column strip
+                        int32_t *out = P.partials + part_off(row0, w.tn * BN + (c0 + j) * 32, slot, nslots, P.nstrips) + 4 * piece;
+#pragma unroll
+                        for (int g = 0; g < 8; g++) {
+                            const int rr = 4 * g + rsub;
+                            uint32_t x0, x1, x2, x3;
+                            ld_shared_v4(swa + (uint32_t)(rr * Cfg::EPI_PITCH + 16 * piece), x0, x1, x2, x3);
+                            if (row0 + rr < P.m)
+                                st_global_v4_hint(out + (int64_t)rr * kStrip, (int)x0, (int)x1, (int)x2, (int)x3, pol);
+                        }
+                        __syncwarp();
                     }
                 }
             }
