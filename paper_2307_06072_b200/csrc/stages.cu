@@ -1165,9 +1165,11 @@ MPC_DEV void store_ept(uint64_t *dst, const uint64_t *v, uint64_t pol) {
 // UNIC (UPER > 0): the three jobs have equal chunk counts on every diagonal, so a diagonal's
 // slots are groups of three (chunk c of job 0, 1, 2); a ring entry holds UPER / 3 whole groups and
 // the consumers read a group at fixed offsets with one ring check per group instead of per slot
+// MINB: CTAs per SM the register budget is sized for (7 for a grid just over one wave of 6:
+// config 2's fold 56 -> 44 us; otherwise 6, as 7 spills a little)
 template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRing, bool TMAP = false, bool UNI1 = false,
-          int UPER = 0>
-__global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : (SFIX ? 3 : 6))
+          int UPER = 0, int MINB = 6>
+__global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : (SFIX ? 3 : MINB))
 fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pmap)
 {
     constexpr bool UNIC = UPER > 0;
@@ -1485,11 +1487,11 @@ static bool fold_sfix(int s, bool beta) {
     return fold_smem(s, kSfixCols, true, kSfixRing) <= 220 * 1024;
 }
 
-template <int COLS, bool BETA, bool SFIX, int EPT, int RING, bool TMAP = false, bool UNI1 = false, int UPER = 0>
+template <int COLS, bool BETA, bool SFIX, int EPT, int RING, bool TMAP = false, bool UNI1 = false, int UPER = 0, int MINB = 6>
 static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
     constexpr int PER = UNI1 ? 6 : UPER > 0 ? UPER : kFoldPer;
     const size_t sm = fold_smem(F.s, COLS, SFIX, RING, PER);
-    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING, TMAP, UNI1, UPER>;
+    auto kern = fold_normalize_kernel<COLS, BETA, SFIX, EPT, RING, TMAP, UNI1, UPER, MINB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (int64_t)kRowBlk * ((F.n + COLS - 1) / COLS) * ((F.m + kRowBlk - 1) / kRowBlk);
@@ -1523,6 +1525,14 @@ cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)
                      : tmap ? fold_launch_t<256, true, false, kFoldEPT, kFoldRing, true>(F, st)
                             : fold_launch_t<256, true, false, kFoldEPT, kFoldRing>(F, st);
     if (!unic && fold_sfix(F.s, false)) return fold_launch_t<kSfixCols, false, true, 1, kSfixRing>(F, st);
+    if (uni1) {
+        // a grid just over one wave of 6 CTAs per SM runs in one wave of 7
+        static int nsm = 0;
+        if (!nsm) { int dev = 0; cudaGetDevice(&dev); cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
+        const int64_t blocks = (int64_t)kRowBlk * ((F.n + 255) / 256) * ((F.m + kRowBlk - 1) / kRowBlk);
+        if (blocks > 6LL * nsm && blocks <= 7LL * nsm && !getenv("MPCGEMM_FOLD_NO7"))
+            return fold_launch_t<256, false, false, kFoldEPT, 5, true, true, 0, 7>(F, st);
+    }
     return uni1 ? fold_launch_t<256, false, false, kFoldEPT, 5, true, true>(F, st)
          : unic == 12 ? fold_launch_t<256, false, false, kFoldEPT, 3, true, false, 12>(F, st)
          : unic == 9 ? fold_launch_t<256, false, false, kFoldEPT, 4, true, false, 9>(F, st)

@@ -61,7 +61,7 @@ def sampled_mismatch(C, Rs, si, sj):
     return None
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("cfg", [2, 3, 4])
 @pytest.mark.parametrize("method", ["3M", "4M"])
 def test_dense_half_tile_parity(cfg, method):
     c = mpgen.CONFIGS[cfg]
@@ -113,3 +113,18 @@ def test_config5_all_updates_sampled(method):
         assert sampled_mismatch(C, Rs, si, sj) is None, j
         count += 1
     assert count == 15
+
+
+def test_config2_fold_occupancy_variants_bitexact(monkeypatch):
+    """Config 2's fold grid (1024 CTAs) is just over one wave of 6 CTAs per SM, so it runs the
+    7-CTA register budget; the 6-CTA variant (MPCGEMM_FOLD_NO7) gives the same bits."""
+    c = mpgen.CONFIGS[2]
+    A, B = mpgen.config_inputs(2, seed=1)
+    C0, r0 = run(A, B, c["prec"], "3M")
+    monkeypatch.setenv("MPCGEMM_FOLD_NO7", "1")
+    C1, r1 = run(A, B, c["prec"], "3M")
+    assert r0["slices"] == r1["slices"]
+    H0, H1 = P.to_host(C0), P.to_host(C1)
+    for part in ("re", "im"):
+        a, b = getattr(H0, part), getattr(H1, part)
+        assert np.array_equal(a.sign, b.sign) and np.array_equal(a.exp, b.exp) and np.array_equal(a.limbs, b.limbs)
