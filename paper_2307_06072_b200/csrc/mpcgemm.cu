@@ -897,7 +897,7 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
         CK(slicegemm_launch(SL, st));
         const int64_t nb = nblocks(m);
         CK(cudaMemsetAsync(mv.omin, 0xFF, 8 * 3 * nb, st));
-        CK(cudaMemsetAsync(mv.dmin2, 0xFF, 8 * 3 * nb, st));
+        CK(cudaMemsetAsync(mv.dmin2, 0xFF, 8 * 3 * nb + 8, st));   // + the max-plus/rule done counter
         CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 1,
                                  mv.omin, mv.omin1, mv.omax2, st));
         CK(prepass_rule_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, mv.omin,
@@ -951,7 +951,8 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     }
     if (rep) {
         rep->slices = 0;                                 // chosen on the device: mpcgemm_device_rule_result()
-        rep->kernel_launches += 7 + nsplit;             // planes, T GEMM, min, max-plus, rule, split, GEMM, fold
+        // planes, T GEMM, min, max-plus + rule (one launch unless MPCGEMM_RULE_SEPARATE), split, GEMM, fold
+        rep->kernel_launches += (getenv("MPCGEMM_RULE_SEPARATE") ? 7 : 6) + nsplit;
         rep->slicegemm_ctas = SL.grid; rep->tile_m = geo.BM; rep->tile_n = geo.BN;
         rep->certified = 1;
     }
@@ -1002,13 +1003,15 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     uint32_t *errflag = mv.errflag;
     Nvtx range_call("mpcgemm");
     if (validate) CK(cudaMemsetAsync(errflag, 0, 4, st));
+    int lm_launches = 0;
     {
         Nvtx r("mpcgemm.a1_linemax");
-        CK(linemax2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, L, prec, eA, nzA, errflag, validate, st));
+        CK(linemax2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, L, prec, eA, nzA, errflag, validate, st,
+                           &lm_launches));
         (void)eB; (void)nzB;                          // (eB = eA + m, nzB = nzA + m)
     }
     if (E) CK(cudaEventRecord(E->ev[1], st));
-    int launches = 2 + (validate ? 1 : 0);             // linemax (A and B) + finalize [, flag readback]
+    int launches = lm_launches + (validate ? 1 : 0);   // linemax (A and B, decode fused) [, flag readback]
     if (validate) {
         uint32_t h = 0;
         if (int rc = readback(dev, &h, errflag, 4, st)) return rc;

@@ -96,16 +96,32 @@ __global__ void linemax_kernel(DMat re, DMat im, int64_t rows, int64_t cols, int
     linemax_body(re, im, rows, cols, L, prec, side, emax, errflag, validate, blockIdx.x, blockIdx.y, gridDim.y);
 }
 
-// both sides in one launch: blocks [0, gx0*gy0) scan the rows of A, the rest the columns of B
+// both sides in one launch: blocks [0, gx0*gy0) scan the rows of A, the rest the columns of B.
+// The last block to finish (a done counter zeroed with the accumulators) decodes the maxima
+// in place into eline / nz (the finalize step, without a launch of its own)
 __global__ void linemax2_kernel(DMat re0, DMat im0, int64_t rows0, int64_t cols0, DMat re1, DMat im1, int64_t rows1,
                                 int64_t cols1, int L, int prec, unsigned long long *emax0, unsigned long long *emax1,
-                                uint32_t *errflag, int validate, int64_t gx0, int64_t gy0, int64_t gx1, int64_t gy1)
+                                uint32_t *errflag, int validate, int64_t gx0, int64_t gy0, int64_t gx1, int64_t gy1,
+                                unsigned int *done, int64_t *eline, uint8_t *nz, int64_t lines)
 {
     const int64_t b = blockIdx.x;
     if (b < gx0 * gy0) linemax_body(re0, im0, rows0, cols0, L, prec, 0, emax0, errflag, validate, b % gx0, b / gx0, gy0);
     else {
         const int64_t c = b - gx0 * gy0;
         linemax_body(re1, im1, rows1, cols1, L, prec, 1, emax1, errflag, validate, c % gx1, c / gx1, gy1);
+    }
+    __shared__ int last;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    __syncthreads();                                  // this block's atomics issued
+    if (tid == 0) { __threadfence(); last = atomicAdd(done, 1u) == gridDim.x - 1; }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const unsigned long long *acc = emax0;            // emax0 .. emax0 + lines (eA then eB)
+    for (int64_t i = tid; i < lines; i += (int64_t)blockDim.x * blockDim.y) {
+        const unsigned long long v = __ldcg(acc + i);
+        nz[i] = v ? 1 : 0;
+        eline[i] = v ? (int64_t)(v ^ 0x8000000000000000ull) : 0;
     }
 }
 
@@ -141,21 +157,27 @@ cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, 
 // a-1 for A (rows) and B (columns) together: one accumulator memset (eA, eB contiguous), one scan
 // launch, one finalize launch (nz and eline of both sides contiguous too)
 cudaError_t linemax2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int L, int prec,
-                            int64_t *eAB, uint8_t *nzAB, uint32_t *errflag, int validate, cudaStream_t st)
+                            int64_t *eAB, uint8_t *nzAB, uint32_t *errflag, int validate, cudaStream_t st, int *nlaunch)
 {
+    if (nlaunch) *nlaunch = 0;
     if (m + n == 0) return cudaSuccess;
     unsigned long long *acc = reinterpret_cast<unsigned long long *>(eAB);
-    cudaError_t e = cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * (m + n), st);
+    // the accumulators, nz (overwritten by the decode) and the done counter after nz (8-aligned;
+    // the metadata layout leaves >= 64 bytes there) in one memset
+    unsigned int *done = reinterpret_cast<unsigned int *>((reinterpret_cast<uintptr_t>(nzAB + m + n) + 7) & ~uintptr_t(7));
+    cudaError_t e = cudaMemsetAsync(acc, 0, reinterpret_cast<uint8_t *>(done + 2) - reinterpret_cast<uint8_t *>(acc), st);
     if (e != cudaSuccess) return e;
-    if (k > 0) {
-        const int64_t gx0 = m > 0 ? (k + 31) / 32 : 0, gy0 = std::min<int64_t>((m + 7) / 8, 65535);
-        const int64_t gx1 = n > 0 ? (n + 31) / 32 : 0, gy1 = std::min<int64_t>((k + 7) / 8, 64);
-        const int64_t blocks = gx0 * gy0 + gx1 * gy1;
-        if (blocks > 0)
-            linemax2_kernel<<<(unsigned)blocks, dim3(32, 8), 0, st>>>(Are, Aim, m, k, Bre, Bim, k, n, L, prec, acc, acc + m,
-                                                                      errflag, validate, gx0, gy0, gx1, gy1);
+    const int64_t gx0 = m > 0 ? (k + 31) / 32 : 0, gy0 = std::min<int64_t>((m + 7) / 8, 65535);
+    const int64_t gx1 = n > 0 ? (n + 31) / 32 : 0, gy1 = std::min<int64_t>((k + 7) / 8, 64);
+    const int64_t blocks = k > 0 ? gx0 * gy0 + gx1 * gy1 : 0;
+    if (blocks > 0) {
+        linemax2_kernel<<<(unsigned)blocks, dim3(32, 8), 0, st>>>(Are, Aim, m, k, Bre, Bim, k, n, L, prec, acc, acc + m,
+                                                                  errflag, validate, gx0, gy0, gx1, gy1, done, eAB, nzAB,
+                                                                  m + n);
+    } else {
+        linemax_finalize_kernel<<<(unsigned)((m + n + 255) / 256), 256, 0, st>>>(acc, m + n, eAB, nzAB);
     }
-    linemax_finalize_kernel<<<(unsigned)((m + n + 255) / 256), 256, 0, st>>>(acc, m + n, eAB, nzAB);
+    if (nlaunch) *nlaunch = 1;
     return cudaGetLastError();
 }
 
@@ -742,12 +764,11 @@ __global__ void prepass_min_kernel(const int32_t *T, int nslots, int64_t nstrips
 }
 
 // stage 2: exact max-plus exponent bound and the per-pair bound choice
-__global__ void __launch_bounds__(256)
-prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
-                       int64_t k, int64_t kp, const uint8_t *nzA, const uint8_t *nzB,
-                       const int32_t *relA, const int32_t *relB,
-                       unsigned long long *out_min, unsigned long long *out_min1, long long *out_max2,
-                       const unsigned long long *gate = nullptr, int64_t ngate = 0)
+MPC_DEV void maxplus_body(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
+                          int64_t k, int64_t kp, const uint8_t *nzA, const uint8_t *nzB,
+                          const int32_t *relA, const int32_t *relB,
+                          unsigned long long *out_min, unsigned long long *out_min1, long long *out_max2,
+                          const unsigned long long *gate, int64_t ngate)
 {
     __shared__ int32_t sa[32][33], sb[32][33];
     if (gate) {                                       // device rule: run only if a block's stage-1 min is 0
@@ -803,6 +824,16 @@ prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m,
     }
 }
 
+__global__ void __launch_bounds__(256)
+prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
+                       int64_t k, int64_t kp, const uint8_t *nzA, const uint8_t *nzB,
+                       const int32_t *relA, const int32_t *relB,
+                       unsigned long long *out_min, unsigned long long *out_min1, long long *out_max2,
+                       const unsigned long long *gate = nullptr, int64_t ngate = 0)
+{
+    maxplus_body(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, out_min, out_min1, out_max2, gate, ngate);
+}
+
 __global__ void readback_kernel(uint32_t *dst, const uint32_t *src, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
@@ -817,15 +848,15 @@ cudaError_t readback_launch(void *dst_mapped, const void *src, size_t bytes, cud
 }
 
 // device rule: the host path's reduction over 256-row blocks and slice rule (mpcgemm.cu
-// run_prepass / gemm_impl; rule.cuh), one warp; picks the candidate plan of the certified s
-__global__ void rule_kernel(const unsigned long long *min1, const unsigned long long *min2,
-                            const unsigned long long *min12, const long long *max22, int64_t nb, int64_t k, int prec,
-                            int method, const DevPlan *plans, int s_lo, int s_hi, DevRuleState *drs)
+// run_prepass / gemm_impl; rule.cuh), one warp (threads 0..31 of the calling block); picks the
+// candidate plan of the certified s
+MPC_DEV void rule_body(const unsigned long long *min1, const unsigned long long *min2,
+                       const unsigned long long *min12, const long long *max22, int64_t nb, int64_t k, int prec,
+                       int method, const DevPlan *plans, int s_lo, int s_hi, DevRuleState *drs, double *lr_shp)
 {
-    if (blockIdx.x) return;
     // lanes test 32 consecutive candidate s at a time from s_lo - 1 on, with rule_slices' predicate
     // (the rule at log2 rho-hat >= 0 cannot pick below s_lo), then lane 0 finishes
-    __shared__ double lr_sh;
+    double &lr_sh = *lr_shp;
     if (threadIdx.x == 0) {
     bool any0 = false;
     for (int64_t b = 0; b < nb; b++) any0 = any0 || min1[b] == 0;
@@ -863,6 +894,37 @@ __global__ void rule_kernel(const unsigned long long *min1, const unsigned long 
     else { drs->cur = DevPlan{nullptr, nullptr, nullptr, sv, 0, 0, 0}; drs->status = -8; }
 }
 
+__global__ void rule_kernel(const unsigned long long *min1, const unsigned long long *min2,
+                            const unsigned long long *min12, const long long *max22, int64_t nb, int64_t k, int prec,
+                            int method, const DevPlan *plans, int s_lo, int s_hi, DevRuleState *drs)
+{
+    __shared__ double lr_sh;
+    if (blockIdx.x) return;
+    rule_body(min1, min2, min12, max22, nb, k, prec, method, plans, s_lo, s_hi, drs, &lr_sh);
+}
+
+// stage 2 (gated) + the rule in one launch: every block counts itself done on a counter that the
+// caller's all-ones memset of the stage-2 arrays initialised to 0xFFFFFFFF, and the last block's
+// first warp runs the rule (no launch of its own)
+__global__ void __launch_bounds__(256)
+prepass_maxplus_rule_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n, int64_t k, int64_t kp,
+                            const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA, const int32_t *relB,
+                            const unsigned long long *min1, unsigned long long *min2, unsigned long long *min12,
+                            long long *max22, int64_t nb, int prec, int method, const DevPlan *plans, int s_lo, int s_hi,
+                            DevRuleState *drs, unsigned int *done)
+{
+    maxplus_body(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, min2, min12, max22, min1, nb);
+    __shared__ int last;
+    __shared__ double lr_sh;
+    __syncthreads();
+    const unsigned int total = gridDim.x * gridDim.y;
+    if (threadIdx.x == 0) { __threadfence(); last = atomicAdd(done, 1u) == total - 2u; }   // from 0xFFFFFFFF
+    __syncthreads();
+    if (!last || threadIdx.x >= 32) return;
+    __threadfence();
+    rule_body(min1, min2, min12, max22, nb, k, prec, method, plans, s_lo, s_hi, drs, &lr_sh);
+}
+
 cudaError_t prepass_rule_launch(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n, int64_t k,
                                 int64_t kp, const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA,
                                 const int32_t *relB, const unsigned long long *min1, unsigned long long *min2,
@@ -870,6 +932,14 @@ cudaError_t prepass_rule_launch(const int32_t *T, int nslots, int64_t nstrips, i
                                 const DevPlan *plans, int s_lo, int s_hi, DevRuleState *drs, cudaStream_t st)
 {
     const int64_t nb = (m + kSBlk - 1) / kSBlk;
+    if (m > 0 && n > 0 && !getenv("MPCGEMM_RULE_SEPARATE")) {
+        // the done counter follows max22[nb] (covered by the caller's all-ones memset)
+        unsigned int *done = reinterpret_cast<unsigned int *>(max22 + nb);
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
+        prepass_maxplus_rule_kernel<<<grid, 256, 0, st>>>(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, min1, min2,
+                                                          min12, max22, nb, prec, method, plans, s_lo, s_hi, drs, done);
+        return cudaGetLastError();
+    }
     if (m > 0 && n > 0) {
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
         prepass_maxplus_kernel<<<grid, 256, 0, st>>>(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB,
