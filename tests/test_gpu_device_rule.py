@@ -50,6 +50,28 @@ def test_device_rule_matches_oracle(method, spread, k):
         assert not C1.re.limbs.any() and not C1.im.limbs.any()     # untouched (zero-initialised)
 
 
+@pytest.mark.parametrize("spread,k", [(16, 12), (0, 64)])
+def test_device_rule_fused_and_separate_launches(spread, k, monkeypatch):
+    """Stage 2 + rule in one launch (the last block runs the rule; default) and as two launches
+    (MPCGEMM_RULE_SEPARATE): same s, same bounds, same bits -- including the minT == 0 case where
+    stage 2 runs, and repeated calls (the fused launch's done counter is re-initialised per call)."""
+    m, n, prec, method = 70, 90, 256, "3M"
+    A = mpgen.random_cmat(spread + k, 9, m, k, prec, spread, zero_frac=0.1)
+    B = mpgen.random_cmat(spread + k, 10, k, n, prec, spread, zero_frac=0.1)
+    out = []
+    for sep in (False, True, False):
+        if sep:
+            monkeypatch.setenv("MPCGEMM_RULE_SEPARATE", "1")
+        else:
+            monkeypatch.delenv("MPCGEMM_RULE_SEPARATE", raising=False)
+        dA, dB, C0, r0, C1, r1, st, s, bounds = host_and_device(A, B, prec, method)
+        out.append((st, s, bounds, P.to_host(C1) if st == 0 else None))
+    for st, s, bounds, H in out[1:]:
+        assert (st, s, bounds) == out[0][:3]
+        if st == 0:
+            assert same_bits(out[0][3], H)
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 @pytest.mark.parametrize("method", ["3M", "4M"])
 def test_device_rule_configs(cfg, method):
