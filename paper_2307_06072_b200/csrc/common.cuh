@@ -61,12 +61,17 @@ __host__ __device__ __forceinline__ int unit_pfirst(int np, int nblk, int j) { r
 // co-running units of neighbouring diagonal pairs walk the same A_p tiles at the same time
 __host__ __device__ __forceinline__ int unit_hint(const WorkUnit &w) { return (w.job_g >> 17) & 0x3FFF; }
 constexpr int kHintNB = 1024;   // p-block stride of a class-wide position (pair, p-block, k-block)
+// tile-wide k-phase mode (GemmParams.kmode == 3, with the tile-major unit order MPCGEMM_ORDER=3):
+// the hint (id in job_g bits 17..30) is shared by every unit of one (job, output tile) -- all its
+// diagonal pairs and exactness chunks -- and holds the absolute position (pair * kHintNB + p-block)
+// * KB + k-block, so the ~74 co-running units of a tile read the same A_p tile at the same time
+// and B planes two steps apart (tools/l2sim.cpp: DRAM operand reads ~90 -> ~46 GB at config 4)
 __host__ __device__ __forceinline__ int unit_nblk_m(int np, int pblk, int kmode) {
-    if (kmode != 2) return unit_nblk(np, pblk);
+    if (kmode < 2) return unit_nblk(np, pblk);
     return pblk > 0 && np > pblk ? (np + pblk / 2) / pblk : 1;
 }
 __host__ __device__ __forceinline__ int unit_pfirst_m(int np, int nblk, int j, int pblk, int kmode) {
-    if (kmode != 2) return unit_pfirst(np, nblk, j);
+    if (kmode < 2) return unit_pfirst(np, nblk, j);
     return j >= nblk ? np + 1 : j * pblk + 1;
 }
 
@@ -127,7 +132,8 @@ struct GemmParams {
                                // a new unit of the group begins there (CTA-pair kernel, G >= 2)
     int32_t pblk;              // p-block length of the CTA-pair kernel's G >= 2 units (0: one block)
     int32_t kmode;             // k-phase hint mode: 1 one hint per (job, r, chunk) group; 2 one per
-                               // (job, chunk) class with absolute p-blocks (unit_hint)
+                               // (job, chunk) class with absolute p-blocks (unit_hint); 3 one per
+                               // (job, output tile) holding an absolute k-block
     int32_t kk_last;           // K = 32 MMA steps of the last k-block (1..3; 0: all 4): the zero
                                // padding of k up to a multiple of 128 is not multiplied
     unsigned long long *mma_count;   // or null: tcgen05.mma instructions issued, added at CTA exit
@@ -189,6 +195,16 @@ MPC_DEV uint32_t mapa_rank(uint32_t local_addr, uint32_t rank) {
 }
 MPC_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// dynamic scheduler: the next unit index, or -1 when the list is done.  Every fetching CTA takes
+// exactly one index >= nunits (its last), so the fetch that returns nunits + nfetch - 1 is the
+// launch's final access to the counter: it re-arms the counter for the next launch in stream order
+// (no memset node before each slice GEMM; the plan zeroes the counter once when it is created)
+MPC_DEV int fetch_unit(int32_t *counter, int nunits, int nfetch) {
+    const int u = atomicAdd(counter, 1);
+    if (u < nunits) return u;
+    if (u == nunits + nfetch - 1) atomicExch(counter, 0);
+    return -1;
 }
 MPC_DEV int32_t ld_relaxed_s32(const int32_t *p) {
     int32_t v;

@@ -50,6 +50,12 @@ struct Nvtx {
     ~Nvtx() { nvtxRangePop(); }
 };
 int env_int(const char *name, int dflt);
+// k-phase hint mode of the CTA-pair slice GEMM (MPCGEMM_KPHASE); the tile-wide mode 3 encodes an
+// absolute k-block in an int32 position, so it falls back to mode 2 when KB >= 2^20
+inline int kphase_mode(int64_t KB) {
+    const int m = env_int("MPCGEMM_KPHASE", 2);
+    return m == 3 && KB >= (1 << 20) ? 2 : m;
+}
 
 // ---------------------------------------------------------------- workspace cache
 struct DevCache {
@@ -63,6 +69,8 @@ struct DevCache {
     cudaEvent_t stage_in[2] = {}, stage_free[2] = {};
     void *rb = nullptr; size_t rb_bytes = 0;         // mapped pinned host memory for readback()
     void *lu = nullptr; size_t lu_bytes = 0;         // NEXT-3 LU scratch (1 / pivot, info)
+    void *lm = nullptr; size_t lm_bytes = 0;         // a-1 exponent accumulators + done counter: zero
+                                                     // between calls (the scan's last block re-zeroes)
     void *solve = nullptr; size_t solve_bytes = 0;   // NEXT-3 solve scratch (1 / U_cc, X)
     cudaStream_t copy_stream = nullptr;              // mpcgemm_host: D2H of finished row groups
     cudaEvent_t group_event = nullptr;
@@ -283,12 +291,20 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
     };
     // k-phase mode 2 (job-wide hints): a class id per (job, k-block chunk) in job_g bits 17..30;
     // every unit of a class walks its k-blocks upward (no serpentine), so positions agree
-    const int kmode = env_int("MPCGEMM_KPHASE", 2);
-    const bool serp = kmode != 2 && env_int("MPCGEMM_SERPENTINE", 1) != 0;
+    // k-phase mode 3 (tile-wide hints): one id per (job, output tile), absolute k-blocks
+    const int kmode = kphase_mode(KB);
+    const bool serp = kmode < 2 && env_int("MPCGEMM_SERPENTINE", 1) != 0;
     std::map<std::tuple<int, int, int>, int32_t> hint_ids;
-    auto hint = [&](int q, int32_t a, int32_t b) -> int32_t {
-        auto it = hint_ids.emplace(std::make_tuple(q, (int)a, (int)b), (int32_t)hint_ids.size()).first;
-        return (it->second & 0x3FFF) << 17;
+    int32_t nhint = 0;
+    auto hint_tile = [&](int q, int64_t tm, int64_t tn, int32_t a, int32_t b) -> int32_t {
+        if (kmode != 3) {
+            auto it = hint_ids.emplace(std::make_tuple(q, (int)a, (int)b), (int32_t)hint_ids.size()).first;
+            nhint = std::max<int32_t>(nhint, (it->second & 0x3FFF) + 1);
+            return (it->second & 0x3FFF) << 17;
+        }
+        const int32_t id = (int32_t)(((int64_t)q * tiles_m * tiles_n + tm * tiles_n + tn) & 0x3FFF);   // (a shared
+        nhint = std::max<int32_t>(nhint, id + 1);      //  id only costs L2 reuse, never exactness)
+        return id << 17;
     };
     // K = 32 MMAs per k-block step: 4, except kk_last for the last (zero-padded) k-block
     const int64_t kkl = ((key.k - 1) % kBK) / 32 + 1;
@@ -304,11 +320,11 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
                         if (!in_tri(tm, r)) continue;
                         const int32_t rev = serp && ((r >> 1) & 1) ? (1 << 16) : 0;
                         if (!in_tri(tm, r + 1)) {              // block's last diagonal is r: D_r alone
-                            units.push_back({q | (3 << 8) | rev | hint(q, a, b), (int32_t)tm, (int32_t)tn, r, a, b, slot_of(q, r, c), -1});
+                            units.push_back({q | (3 << 8) | rev | hint_tile(q, tm, tn, a, b), (int32_t)tm, (int32_t)tn, r, a, b, slot_of(q, r, c), -1});
                             P.mma += np * kk_sum(a, b) * (r - 1);
                             continue;
                         }
-                        units.push_back({q | (2 << 8) | rev | hint(q, a, b), (int32_t)tm, (int32_t)tn, r, a, b,
+                        units.push_back({q | (2 << 8) | rev | hint_tile(q, tm, tn, a, b), (int32_t)tm, (int32_t)tn, r, a, b,
                                          slot_of(q, r, c), slot_of(q, r + 1, c)});
                         P.mma += np * kk_sum(a, b) * (2 * r - 1);
                     }
@@ -331,7 +347,18 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
         return unit_G(w) == 2 ? np * (w.b - w.a) * (2 * w.r - 1)
              : unit_G(w) == 3 ? np * (w.b - w.a) * (w.r - 1) : (int64_t)(w.b - w.a);
     };
-    if (key.order == 2) {
+    if (key.order == 3) {
+        // job-major, then tile-major, then longest first: the ~74 co-running units are all the
+        // diagonal pairs (and exactness chunks) of one or two output tiles, so with the tile-wide
+        // k-phase hint (KPHASE=3) they read the same A_p tile together and each B plane within a
+        // few steps of each other (tools/l2sim.cpp models the operand stream)
+        std::stable_sort(units.begin(), units.end(), [&](const WorkUnit &a, const WorkUnit &b) {
+            if (unit_job(a) != unit_job(b)) return unit_job(a) < unit_job(b);
+            if (a.tm != b.tm) return a.tm < b.tm;
+            if (a.tn != b.tn) return a.tn < b.tn;
+            return work(a) > work(b);
+        });
+    } else if (key.order == 2) {
         // job-major; within a job the units of one k-block chunk class (a, b) together -- classes
         // by their smallest unit, largest first, so the job still ends on its smallest units --
         // then longest first: co-running groups are neighbouring diagonal pairs on the SAME
@@ -369,7 +396,7 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
     P.nunits = (int)flat.size(); P.nslots = nslots; P.grid = grid;
     if (P.nunits) {
         if (cudaMalloc(&P.d_units, sizeof(WorkUnit) * flat.size()) != cudaSuccess ||
-            cudaMalloc(&P.d_counter, sizeof(int32_t) * (1 + (size_t)nslots)) != cudaSuccess ||
+            cudaMalloc(&P.d_counter, sizeof(int32_t) * (1 + (size_t)std::max(nslots, nhint))) != cudaSuccess ||
             cudaMalloc(&P.d_slotinfo, sizeof(int32_t) * slotinfo.size()) != cudaSuccess)
             return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc plan");
         // uploads ordered on the call's stream (a later call on another stream is ordered after
@@ -377,7 +404,7 @@ int build_plan(int dev, const PlanKey &key, Plan **out, cudaStream_t st) {
         // by the time it returns, so the host vectors may go
         CK(cudaMemcpyAsync(P.d_units, flat.data(), sizeof(WorkUnit) * flat.size(), cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(P.d_slotinfo, slotinfo.data(), sizeof(int32_t) * slotinfo.size(), cudaMemcpyHostToDevice, st));
-        CK(cudaMemsetAsync(P.d_counter, 0, sizeof(int32_t) * (1 + (size_t)nslots), st));   // counter + k-phase hints
+        CK(cudaMemsetAsync(P.d_counter, 0, sizeof(int32_t) * (1 + (size_t)std::max(nslots, nhint)), st));   // counter + k-phase hints
     }
     auto res = g_plans.emplace(std::make_pair(dev, key), P);
     *out = &res.first->second;
@@ -757,7 +784,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         SL.P.dbg = env_int("MPCGEMM_DBG", 0);
         SL.P.hot = env_int("MPCGEMM_KPHASE", 2) ? plan->d_counter + 1 : nullptr;
         SL.P.pblk = env_int("MPCGEMM_PBLK", 64);
-        SL.P.kmode = env_int("MPCGEMM_KPHASE", 2);
+        SL.P.kmode = kphase_mode(SL.P.KB);
         SL.P.mma_count = mma_dev;
         SL.P.halfn = env_int("MPCGEMM_HALFN", 1);
         for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
@@ -847,6 +874,7 @@ int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int met
         cudaMalloc(&S.d_counter, sizeof(int32_t)) != cudaSuccess)
         return fail(MPCGEMM_ERR_NOMEM, "cudaMalloc device plans");
     CK(cudaMemcpyAsync(S.d_plans, hp.data(), sizeof(DevPlan) * hp.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(S.d_counter, 0, sizeof(int32_t), st));   // then re-armed by each launch's last fetch
     *out = &g_devplans.emplace(key, S).first->second;
     return 0;
 }
@@ -878,8 +906,11 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     int32_t *T = (int32_t *)(big + align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256));
     {
         Nvtx r("mpcgemm.a2_prepass_device_rule");
+        const int64_t nb = nblocks(m);
+        // (the planes kernel also sets the stage-1 minima and the max-plus/rule targets -- with the
+        //  rule's done counter after them -- to all ones)
         CK(prepass_planes2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, Lo.kp, L, mv.eA, mv.eB, tA, relA,
-                                  tB, relB, st));
+                                  tB, relB, st, mv.omin, 3 * nb, mv.dmin2, 3 * nb + 1));
         PlanKey key{m, n, k, 1, 0, 128, tile_bn(n), sm_count(dev), 0, (int)kMaxKBlocksPerChunk, 0, 0, {}};
         Plan *plan;
         if (int rc = build_plan(dev, key, &plan, st)) return rc;
@@ -895,9 +926,6 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
         SL.grid = plan->grid; SL.BM = 128; SL.BN = tile_bn(n); SL.simt = 0; SL.nunits = plan->nunits;
         SL.units_flat = plan->d_units;
         CK(slicegemm_launch(SL, st));
-        const int64_t nb = nblocks(m);
-        CK(cudaMemsetAsync(mv.omin, 0xFF, 8 * 3 * nb, st));
-        CK(cudaMemsetAsync(mv.dmin2, 0xFF, 8 * 3 * nb + 8, st));   // + the max-plus/rule done counter
         CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 1,
                                  mv.omin, mv.omin1, mv.omax2, st));
         CK(prepass_rule_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, mv.omin,
@@ -926,7 +954,7 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
     SL.P.partsA = SL.P.partsB = parts;
     SL.P.pblk = env_int("MPCGEMM_PBLK", 64);
-    SL.P.kmode = env_int("MPCGEMM_KPHASE", 2);
+    SL.P.kmode = kphase_mode(SL.P.KB);
     SL.P.drs = mv.drs;
     SL.P.halfn = env_int("MPCGEMM_HALFN", 1);
     for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = Pj.jobs[q];
@@ -1006,8 +1034,13 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     int lm_launches = 0;
     {
         Nvtx r("mpcgemm.a1_linemax");
+        const size_t lm_need = 8 * (size_t)(m + n) + 16;
+        if (dc.lm_bytes < lm_need) {
+            if (int rc = grow(&dc.lm, &dc.lm_bytes, lm_need)) return rc;
+            CK(cudaMemsetAsync(dc.lm, 0, dc.lm_bytes, st));
+        }
         CK(linemax2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, L, prec, eA, nzA, errflag, validate, st,
-                           &lm_launches));
+                           &lm_launches, (unsigned long long *)dc.lm));
         (void)eB; (void)nzB;                          // (eB = eA + m, nzB = nzA + m)
     }
     if (E) CK(cudaEventRecord(E->ev[1], st));
@@ -1498,7 +1531,7 @@ void mpcgemm_release(void) {
     if (it != g_cache.end()) {
         if (it->second.done) cudaEventDestroy(it->second.done);
         cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage[0]); cudaFree(it->second.stage[1]);
-        cudaFree(it->second.lu);
+        cudaFree(it->second.lu); cudaFree(it->second.lm);
         cudaFree(it->second.solve);
         cudaFree(it->second.mma_dev);
         if (it->second.rb) cudaFreeHost(it->second.rb);

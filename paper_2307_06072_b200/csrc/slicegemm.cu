@@ -123,8 +123,7 @@ slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             };
             for (;;) {
-                int u = atomicAdd(P.counter, 1);
-                if (u >= nunits) u = -1;
+                int u = fetch_unit(P.counter, nunits, (int)gridDim.x);
                 mbar_wait(&qempty[qs], qph ^ 1);
                 *reinterpret_cast<volatile int32_t *>(&uq[qs]) = u;
                 mbar_arrive(&qfull[qs]);
@@ -374,8 +373,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             for (;;) {
                 int u, rot = 0;
                 if (rank == 0) {
-                    u = atomicAdd(P.counter, 1);
-                    if (u >= nunits) u = -1;
+                    u = fetch_unit(P.counter, nunits, (int)gridDim.x / 2);   // one fetcher per CTA pair
                     if (u >= 0 && hot) {
                         // k-phase alignment: begin at the (pair, k-block) position the group's
                         // running units are on, so the units sharing a digit-plane tile read it
@@ -389,6 +387,11 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                                 const int h = ld_relaxed_s32(hot + unit_hint(wu));
                                 const int hk = h % nkb, hb = (h / nkb) % kHintNB, hp = h / (nkb * kHintNB);
                                 rot = (h > 0 && hp < npairs && hb < nblk) ? (hp * nblk + hb) * nkb + hk : 0;
+                            } else if (P.kmode == 3) {        // tile-wide absolute position
+                                const int h = ld_relaxed_s32(hot + unit_hint(wu));
+                                const int hk = h % KB, hb = (h / KB) % kHintNB, hp = h / (KB * kHintNB);
+                                const int kk = (hk >= wu.a && hk < wu.b) ? hk - wu.a : 0;
+                                rot = (hp < npairs && hb < nblk) ? (hp * nblk + hb) * nkb + kk : 0;
                             } else {
                                 const int h = ld_relaxed_s32(hot + wu.slot0);
                                 rot = (h > 0 && h < npos) ? h : 0;
@@ -427,6 +430,7 @@ slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
                         const int p1 = unit_pfirst_m(np, nblk, blk + 1, P.pblk, P.kmode) - 1;
                         if (rank == 0 && hot) {
                             if (P.kmode == 2) st_relaxed_s32(hot + unit_hint(w), (pr * kHintNB + blk) * nkb + (pos - pb * nkb));
+                            else if (P.kmode == 3) st_relaxed_s32(hot + unit_hint(w), (pr * kHintNB + blk) * KB + kb);
                             else st_relaxed_s32(hot + w.slot0, pos);
                         }
                         if (g2 && p0 > 1) load(J.pa[pr] * s + p0 - 2, 0, kb, w.tm, w.tn, true);   // A_{p0-1} only
@@ -751,8 +755,6 @@ static cudaError_t launch_tc(const SliceGemmLaunch &L, cudaStream_t st) {
     auto kern = slicegemm_tc_kernel<BN, STAGES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(L.P.counter, 0, sizeof(int32_t), st);
-    if (e != cudaSuccess) return e;
     kern<<<L.grid, 256, Cfg::SMEM, st>>>(ta, tb, L.P);
     return cudaGetLastError();
 }
@@ -765,8 +767,6 @@ static cudaError_t launch_tc2(const SliceGemmLaunch &L, cudaStream_t st) {
     if (make_plane_map(&tb, L.digB, (int64_t)L.P.partsB * L.P.s, L.rowsB, L.kp, 128)) return cudaErrorInvalidValue;
     auto kern = slicegemm_tc2_kernel<STAGES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(L.P.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     kern<<<L.grid & ~1, 256, Cfg::SMEM, st>>>(ta, tb, L.P);
     return cudaGetLastError();

@@ -102,7 +102,7 @@ __global__ void linemax_kernel(DMat re, DMat im, int64_t rows, int64_t cols, int
 __global__ void linemax2_kernel(DMat re0, DMat im0, int64_t rows0, int64_t cols0, DMat re1, DMat im1, int64_t rows1,
                                 int64_t cols1, int L, int prec, unsigned long long *emax0, unsigned long long *emax1,
                                 uint32_t *errflag, int validate, int64_t gx0, int64_t gy0, int64_t gx1, int64_t gy1,
-                                unsigned int *done, int64_t *eline, uint8_t *nz, int64_t lines)
+                                unsigned int *done, int64_t *eline, uint8_t *nz, int64_t lines, int clean)
 {
     const int64_t b = blockIdx.x;
     if (b < gx0 * gy0) linemax_body(re0, im0, rows0, cols0, L, prec, 0, emax0, errflag, validate, b % gx0, b / gx0, gy0);
@@ -117,12 +117,14 @@ __global__ void linemax2_kernel(DMat re0, DMat im0, int64_t rows0, int64_t cols0
     __syncthreads();
     if (!last) return;
     __threadfence();
-    const unsigned long long *acc = emax0;            // emax0 .. emax0 + lines (eA then eB)
+    unsigned long long *acc = emax0;                  // emax0 .. emax0 + lines (eA then eB)
     for (int64_t i = tid; i < lines; i += (int64_t)blockDim.x * blockDim.y) {
         const unsigned long long v = __ldcg(acc + i);
         nz[i] = v ? 1 : 0;
         eline[i] = v ? (int64_t)(v ^ 0x8000000000000000ull) : 0;
-    }
+        if (clean) acc[i] = 0;                        // separate accumulators: zero them (and the done
+    }                                                 // counter) for the next call -- no memset node
+    if (clean && tid == 0) *done = 0;
 }
 
 __global__ void linemax_finalize_kernel(unsigned long long *emax, int64_t n, int64_t *eline, uint8_t *nz) {
@@ -157,23 +159,33 @@ cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, 
 // a-1 for A (rows) and B (columns) together: one accumulator memset (eA, eB contiguous), one scan
 // launch, one finalize launch (nz and eline of both sides contiguous too)
 cudaError_t linemax2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int L, int prec,
-                            int64_t *eAB, uint8_t *nzAB, uint32_t *errflag, int validate, cudaStream_t st, int *nlaunch)
+                            int64_t *eAB, uint8_t *nzAB, uint32_t *errflag, int validate, cudaStream_t st, int *nlaunch,
+                            unsigned long long *acc_clean)
 {
     if (nlaunch) *nlaunch = 0;
     if (m + n == 0) return cudaSuccess;
-    unsigned long long *acc = reinterpret_cast<unsigned long long *>(eAB);
-    // the accumulators, nz (overwritten by the decode) and the done counter after nz (8-aligned;
-    // the metadata layout leaves >= 64 bytes there) in one memset
-    unsigned int *done = reinterpret_cast<unsigned int *>((reinterpret_cast<uintptr_t>(nzAB + m + n) + 7) & ~uintptr_t(7));
-    cudaError_t e = cudaMemsetAsync(acc, 0, reinterpret_cast<uint8_t *>(done + 2) - reinterpret_cast<uint8_t *>(acc), st);
-    if (e != cudaSuccess) return e;
     const int64_t gx0 = m > 0 ? (k + 31) / 32 : 0, gy0 = std::min<int64_t>((m + 7) / 8, 65535);
     const int64_t gx1 = n > 0 ? (n + 31) / 32 : 0, gy1 = std::min<int64_t>((k + 7) / 8, 64);
     const int64_t blocks = k > 0 ? gx0 * gy0 + gx1 * gy1 : 0;
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(eAB);
+    unsigned int *done;
+    const int clean = acc_clean && blocks > 0;
+    if (clean) {
+        // caller-kept accumulators (m + n words, then the done counter), all zero on entry; the
+        // last block zeroes them again after the decode
+        acc = acc_clean;
+        done = reinterpret_cast<unsigned int *>(acc_clean + m + n);
+    } else {
+        // the accumulators, nz (overwritten by the decode) and the done counter after nz (8-aligned;
+        // the metadata layout leaves >= 64 bytes there) in one memset
+        done = reinterpret_cast<unsigned int *>((reinterpret_cast<uintptr_t>(nzAB + m + n) + 7) & ~uintptr_t(7));
+        cudaError_t e = cudaMemsetAsync(acc, 0, reinterpret_cast<uint8_t *>(done + 2) - reinterpret_cast<uint8_t *>(acc), st);
+        if (e != cudaSuccess) return e;
+    }
     if (blocks > 0) {
         linemax2_kernel<<<(unsigned)blocks, dim3(32, 8), 0, st>>>(Are, Aim, m, k, Bre, Bim, k, n, L, prec, acc, acc + m,
                                                                   errflag, validate, gx0, gy0, gx1, gy1, done, eAB, nzAB,
-                                                                  m + n);
+                                                                  m + n, clean);
     } else {
         linemax_finalize_kernel<<<(unsigned)((m + n + 255) / 256), 256, 0, st>>>(acc, m + n, eAB, nzAB);
     }
@@ -696,9 +708,14 @@ __global__ void prepass_planes_kernel(DMat re, DMat im, int side, int64_t lines,
 
 __global__ void prepass_planes2_kernel(DMat re0, DMat im0, int64_t lines0, const int64_t *eline0, int8_t *t0, int32_t *rel0,
                                        DMat re1, DMat im1, int64_t lines1, const int64_t *eline1, int8_t *t1, int32_t *rel1,
-                                       int64_t k, int64_t kp, int L, int64_t gx, int64_t gy0, int64_t gy1)
+                                       int64_t k, int64_t kp, int L, int64_t gx, int64_t gy0, int64_t gy1,
+                                       unsigned long long *fill0, int64_t nfill0, unsigned long long *fill1, int64_t nfill1)
 {
     const int64_t b = blockIdx.x;
+    if (b == 0) {                                      // the stage-1/2 reduction targets: all ones
+        for (int64_t i = threadIdx.x; i < nfill0; i += blockDim.x) fill0[i] = ~0ull;   // (replaces two
+        for (int64_t i = threadIdx.x; i < nfill1; i += blockDim.x) fill1[i] = ~0ull;   //  memset nodes)
+    }
     if (b < gx * gy0) prepass_planes_body(re0, im0, 0, lines0, k, kp, L, eline0, t0, rel0, b % gx, b / gx, gy0);
     else {
         const int64_t c = b - gx * gy0;
@@ -708,12 +725,18 @@ __global__ void prepass_planes2_kernel(DMat re0, DMat im0, int64_t lines0, const
 
 cudaError_t prepass_planes2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp,
                                    int L, const int64_t *eA, const int64_t *eB, int8_t *tA, int32_t *relA, int8_t *tB,
-                                   int32_t *relB, cudaStream_t st)
+                                   int32_t *relB, cudaStream_t st, unsigned long long *fill0, int64_t nfill0,
+                                   unsigned long long *fill1, int64_t nfill1)
 {
-    if (kp == 0 || m + n == 0) return cudaSuccess;
+    if (kp == 0 || m + n == 0) {
+        cudaError_t e = nfill0 ? cudaMemsetAsync(fill0, 0xFF, 8 * nfill0, st) : cudaSuccess;
+        if (e == cudaSuccess && nfill1) e = cudaMemsetAsync(fill1, 0xFF, 8 * nfill1, st);
+        return e;
+    }
     const int64_t gx = (kp + 127) / 128, gy0 = std::min<int64_t>(m, 32768), gy1 = std::min<int64_t>(n, 32768);
     prepass_planes2_kernel<<<(unsigned)(gx * (gy0 + gy1)), 128, 0, st>>>(Are, Aim, m, eA, tA, relA, Bre, Bim, n, eB, tB, relB,
-                                                                       k, kp, L, gx, gy0, gy1);
+                                                                       k, kp, L, gx, gy0, gy1, fill0, nfill0, fill1,
+                                                                       nfill1);
     return cudaGetLastError();
 }
 

@@ -65,6 +65,10 @@ int main(int argc, char **argv) {
     std::stable_sort(units.begin(), units.end(), [&](const Unit &x, const Unit &y) {
         if (x.job != y.job) return x.job < y.job;
         if (ORDER == 2 && x.cls != y.cls) return cfirst[x.cls] < cfirst[y.cls];
+        if (ORDER >= 3) {                    // tile-major: every diagonal pair / chunk of one tile together
+            int tx = ORDER == 4 ? x.tn * TM + x.tm : x.tm * TN + x.tn, ty = ORDER == 4 ? y.tn * TM + y.tm : y.tm * TN + y.tn;
+            if (tx != ty) return tx < ty;
+        }
         return work(x) > work(y);
     });
     // LRU of 32 KB blocks
@@ -83,12 +87,12 @@ int main(int argc, char **argv) {
     };
     auto keyA = [&](int q, int p, int kb, int tm) { return (((long)q * 4096 + p) * 4096 + kb) * 256 + tm; };
     auto keyB = [&](int q, int p, int kb, int tn) { return ((((long)q * 4096 + p) * 4096 + kb) * 256 + tn) | (1L << 62); };
-    std::vector<int> hot(slot + ncls + 1, 0);
+    std::vector<int> hot(slot + ncls + 3 * TM * TN + 1, 0);
     struct PairState { int u = -1; int t = 0, npos = 0, pos = 0, nblk = 0, np = 0; std::vector<std::pair<long, long>> q; size_t qi = 0; int stall = 0; };
     std::vector<PairState> ps(NPAIR);
     size_t next = 0;
-    auto nblk_of = [&](int np) { return KMODE == 2 ? (PBLK > 0 && np > PBLK ? (np + PBLK / 2) / PBLK : 1) : (PBLK > 0 && np > PBLK ? (np + PBLK - 1) / PBLK : 1); };
-    auto pfirst = [&](int np, int nblk, int j) { return KMODE == 2 ? (j >= nblk ? np + 1 : j * PBLK + 1) : j * np / nblk + 1; };
+    auto nblk_of = [&](int np) { return KMODE >= 2 ? (PBLK > 0 && np > PBLK ? (np + PBLK / 2) / PBLK : 1) : (PBLK > 0 && np > PBLK ? (np + PBLK - 1) / PBLK : 1); };
+    auto pfirst = [&](int np, int nblk, int j) { return KMODE >= 2 ? (j >= nblk ? np + 1 : j * PBLK + 1) : j * np / nblk + 1; };
     auto start = [&](PairState &P) -> bool {
         if (next >= units.size()) { P.u = -1; return false; }
         P.u = (int)next++;
@@ -98,6 +102,11 @@ int main(int argc, char **argv) {
         int rot = 0;
         if (KMODE == 1) { int h = hot[w.slot]; rot = (h > 0 && h < P.npos) ? h : 0; }
         else if (KMODE == 2) { int h = hot[w.cls]; int hk = h % nkb, hb = (h / nkb) % 1024; rot = (h > 0 && hb < P.nblk) ? hb * nkb + hk : 0; }
+        else if (KMODE == 3) {            // one hint per (job, tile): absolute (p-block, k-block)
+            int h = hot[(w.job * TM + w.tm) * TN + w.tn]; int hk = h % 1024, hb = h / 1024;
+            int kk = (hk >= w.a && hk < w.b) ? hk - w.a : 0;
+            rot = (hb < P.nblk) ? hb * nkb + kk : 0;
+        }
         P.pos = rot; P.q.clear(); P.qi = 0;
         return true;
     };
@@ -108,6 +117,7 @@ int main(int argc, char **argv) {
         int kb = w.rev ? w.b - 1 - kbi : w.a + kbi;
         int p0 = pfirst(P.np, P.nblk, blk), p1 = pfirst(P.np, P.nblk, blk + 1) - 1;
         if (KMODE == 1) hot[w.slot] = P.pos; else if (KMODE == 2) hot[w.cls] = blk * nkb + kbi;
+        else if (KMODE == 3) hot[(w.job * TM + w.tm) * TN + w.tn] = blk * 1024 + kb;
         P.q.clear(); P.qi = 0;
         if (p0 > 1) P.q.push_back({keyA(w.job, p0 - 1, kb, w.tm), -1});
         for (int p = p0; p <= p1; p++) P.q.push_back({keyA(w.job, p, kb, w.tm), keyB(w.job, w.r + 1 - p, kb, w.tn)});
