@@ -62,6 +62,9 @@ cudaError_t readback_launch(void *dst_mapped, const void *src, size_t bytes, cud
 // device-rule mode: stage 2 only if some block's stage-1 minimum is 0 (decided on the device;
 // out_*2 arrays, initialised to all-ones), then the slice rule over the reduced integers picks
 // the plan (plans[s - s_lo] for s in [s_lo, s_hi]) into *drs
+cudaError_t prepass_small_t_launch(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n, int64_t k, int64_t kp,
+                                   const uint8_t *nzA, const uint8_t *nzB, int32_t *T, int64_t nstrips,
+                                   unsigned long long *min1, cudaStream_t st);
 cudaError_t prepass_rule_launch(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n, int64_t k,
                                 int64_t kp, const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA,
                                 const int32_t *relB, const unsigned long long *min1, unsigned long long *min2,

@@ -52,6 +52,10 @@ struct Nvtx {
 int env_int(const char *name, int dflt);
 // k-phase hint mode of the CTA-pair slice GEMM (MPCGEMM_KPHASE); the tile-wide mode 3 encodes an
 // absolute k-block in an int32 position, so it falls back to mode 2 when KB >= 2^20
+// device rule: the small-shape pre-pass (T by dp4a and the stage-1 minimum in one launch, no T GEMM)
+inline bool prepass_small(int64_t m, int64_t n, int64_t k) {
+    return k > 0 && k <= 65536 && m * n * k <= (int64_t(1) << 27) && env_int("MPCGEMM_PREPASS_SMALL", 1) != 0;
+}
 inline int kphase_mode(int64_t KB) {
     const int m = env_int("MPCGEMM_KPHASE", 2);
     return m == 3 && KB >= (1 << 20) ? 2 : m;
@@ -536,7 +540,7 @@ int64_t exact_cap() {
     return e > 0 ? std::min<int64_t>(kMaxKBlocksPerChunk, e) : kMaxKBlocksPerChunk;
 }
 
-struct Geometry { int BM, BN, grid, maxkb; };
+struct Geometry { int BM, BN, grid, maxkb, g2; };
 
 // m_balance (> 0): the row count whose work sets the chunk target -- row groups use the whole
 // call's, so every group has the whole call's slot table (and a group's workspace scales with its
@@ -551,19 +555,33 @@ Geometry main_geometry(int dev, int64_t m, int64_t n, int64_t k, int s, int meth
     // of neighbouring products overlap the GEMM only on reserved SMs)
     g.grid = std::max(2, sm_count(dev) - std::max(0, env_int("MPCGEMM_RESERVE_SMS", 0)));
     g.maxkb = (int)chunk_kb(m_balance > 0 ? m_balance : m, n, k, s, method, g.BM, g.BN, g.grid);
+    // two diagonals per unit (G = 2) halve the operand loads per MMA, but keep a unit's chain of
+    // stages as long as one diagonal's; when the G = 2 units are fewer than ~4 per fetching CTA (pair)
+    // the call is parallelism-bound and single-diagonal units, which the load-balance target cuts
+    // along their (pair, p, k-block) sequence, finish sooner (config 1 46 -> 43 us, config 2 4M
+    // 0.388 -> 0.327 ms per call; config 4 / 5's large products keep G = 2).  MPCGEMM_G2 forces it.
+    const char *ge = getenv("MPCGEMM_G2");
+    if (ge && *ge) g.g2 = atoi(ge) != 0;
+    else {
+        const int64_t mb = m_balance > 0 ? m_balance : m;
+        const int64_t units = ((mb + g.BM - 1) / g.BM) * ((n + g.BN - 1) / g.BN) * ((s + 1) / 2) * 3;
+        g.g2 = units >= 4LL * (g.BM == 256 ? g.grid / 2 : g.grid);
+    }
     return g;
 }
 
-int64_t count_slots(int64_t k, int s, int method, int maxkb) {
+int64_t count_slots(int64_t k, int s, int method, int maxkb, bool g2) {
     Plan P;
     method_jobs(method, P);
     int64_t n = 0;
-    for (const Segment &sg : diag_segments(P, (k + kBK - 1) / kBK, s, method, maxkb, g2_enabled()))
+    for (const Segment &sg : diag_segments(P, (k + kBK - 1) / kBK, s, method, maxkb, g2))
         n += sg.G * sg.nch;
     return n;
 }
 
-Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb, int prec = 64, bool beta = false) {
+// g2: the geometry's unit shape (main_geometry().g2) -- it sets the slot count; -1 for s = 0 layouts
+Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb, int prec = 64, bool beta = false,
+                  int g2 = -1) {
     Layout Lo;
     Lo.kp = align_up((size_t)std::max<int64_t>(k, 1), 16);
     Lo.nstrips = (std::max<int64_t>(n, 1) + kStrip - 1) / kStrip;
@@ -575,7 +593,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb,
     Lo.main = 0;
     if (s > 0) {
         const int parts = method == 3 ? 3 : 2;
-        const int64_t nslots = count_slots(k, s, method, maxkb);
+        const int64_t nslots = count_slots(k, s, method, maxkb, g2 < 0 ? g2_enabled() : g2 != 0);
         Lo.main = align_up((size_t)parts * s * m * Lo.kp, 256) + align_up((size_t)parts * s * n * Lo.kp, 256) +
                   align_up((size_t)nslots * ((m + kRowBlk - 1) / kRowBlk * kRowBlk) * Lo.nstrips * kStrip * 4, 256) +
                   align_up(fold_scratch_words(m, (n + kFoldLdAlign - 1) / kFoldLdAlign * kFoldLdAlign, s, (prec + 63) / 64, beta) * 8, 256);
@@ -770,7 +788,7 @@ int run_main(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_c
         const int BN = geo.BN;
         std::vector<int32_t> sb;
         if (!sblk.empty()) sb.assign(sblk.begin() + (r0 >> kSBlkShift), sblk.begin() + ((r0 + mr + kSBlk - 1) >> kSBlkShift));
-        PlanKey key{mr, n, k, s, method, geo.BM, BN, geo.grid, simt, geo.maxkb, g2_enabled() ? 1 : 0,
+        PlanKey key{mr, n, k, s, method, geo.BM, BN, geo.grid, simt, geo.maxkb, geo.g2,
                     env_int("MPCGEMM_ORDER", 2), sb};
         Plan *plan;
         if (int rc = build_plan(dev, key, &plan, st)) return rc;
@@ -856,7 +874,7 @@ int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int met
     std::vector<DevPlan> hp;
     for (int s = s_lo; s <= s_hi; s++) {
         const Geometry geo = main_geometry(dev, m, n, k, s, method);
-        PlanKey key2{m, n, k, s, method, geo.BM, geo.BN, geo.grid, 0, geo.maxkb, g2_enabled() ? 1 : 0,
+        PlanKey key2{m, n, k, s, method, geo.BM, geo.BN, geo.grid, 0, geo.maxkb, geo.g2,
                      env_int("MPCGEMM_ORDER", 2), {}};
         Plan *plan;
         if (int rc = build_plan(dev, key2, &plan, st)) return rc;
@@ -865,7 +883,7 @@ int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int met
         S.uni1 = S.uni1 && plan->uni1;
         S.unic = S.unic && plan->unic;
         S.chunked_unic = S.chunked_unic || (plan->unic && !plan->uni1);
-        S.main_bytes = std::max(S.main_bytes, layout_for(m, n, k, s, method, geo.maxkb, prec, false).main);
+        S.main_bytes = std::max(S.main_bytes, layout_for(m, n, k, s, method, geo.maxkb, prec, false, geo.g2).main);
     }
     // one fold variant serves every candidate: their slot orders must agree (with the present job
     // structures a chunked (chunk, job)-ordered plan is 3M, and then every candidate is)
@@ -907,29 +925,36 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     {
         Nvtx r("mpcgemm.a2_prepass_device_rule");
         const int64_t nb = nblocks(m);
+        const bool small_pre = prepass_small(m, n, k);
         // (the planes kernel also sets the stage-1 minima and the max-plus/rule targets -- with the
         //  rule's done counter after them -- to all ones)
         CK(prepass_planes2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, Lo.kp, L, mv.eA, mv.eB, tA, relA,
                                   tB, relB, st, mv.omin, 3 * nb, mv.dmin2, 3 * nb + 1));
-        PlanKey key{m, n, k, 1, 0, 128, tile_bn(n), sm_count(dev), 0, (int)kMaxKBlocksPerChunk, 0, 0, {}};
-        Plan *plan;
-        if (int rc = build_plan(dev, key, &plan, st)) return rc;
-        SliceGemmLaunch SL;
-        memset(&SL, 0, sizeof(SL));
-        SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
-        SL.P.partials = T; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
-        SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = 1; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
-        SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
-        SL.P.partsA = SL.P.partsB = 1;
-        for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
-        SL.digA = tA; SL.digB = tB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
-        SL.grid = plan->grid; SL.BM = 128; SL.BN = tile_bn(n); SL.simt = 0; SL.nunits = plan->nunits;
-        SL.units_flat = plan->d_units;
-        CK(slicegemm_launch(SL, st));
-        CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 1,
-                                 mv.omin, mv.omin1, mv.omax2, st));
-        CK(prepass_rule_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, mv.omin,
-                               mv.dmin2, mv.dmin12, mv.dmax22, prec, method, S->d_plans, S->s_lo, s_hi, mv.drs, st));
+        if (small_pre) {                               // T (dp4a) + stage 1 in one launch, T as one plane
+            CK(prepass_small_t_launch(tA, tB, m, n, k, Lo.kp, mv.nzA, mv.nzB, T, Lo.nstrips, mv.omin, st));
+            CK(prepass_rule_launch(T, 1, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, mv.omin, mv.dmin2,
+                                   mv.dmin12, mv.dmax22, prec, method, S->d_plans, S->s_lo, s_hi, mv.drs, st));
+        } else {
+            PlanKey key{m, n, k, 1, 0, 128, tile_bn(n), sm_count(dev), 0, (int)kMaxKBlocksPerChunk, 0, 0, {}};
+            Plan *plan;
+            if (int rc = build_plan(dev, key, &plan, st)) return rc;
+            SliceGemmLaunch SL;
+            memset(&SL, 0, sizeof(SL));
+            SL.P.units = plan->d_units; SL.P.nunits = plan->nunits; SL.P.counter = plan->d_counter;
+            SL.P.partials = T; SL.P.nslots = plan->nslots; SL.P.nstrips = Lo.nstrips;
+            SL.P.m = (int32_t)m; SL.P.n = (int32_t)n; SL.P.s = 1; SL.P.KB = (int32_t)((k + kBK - 1) / kBK);
+            SL.P.kk_last = (int32_t)(((k - 1) % kBK) / 32 + 1) % (kBK / 32);
+            SL.P.partsA = SL.P.partsB = 1;
+            for (int q = 0; q < kMaxJobs; q++) SL.P.jobs[q] = plan->jobs[q];
+            SL.digA = tA; SL.digB = tB; SL.rowsA = m; SL.rowsB = n; SL.kp = Lo.kp;
+            SL.grid = plan->grid; SL.BM = 128; SL.BN = tile_bn(n); SL.simt = 0; SL.nunits = plan->nunits;
+            SL.units_flat = plan->d_units;
+            CK(slicegemm_launch(SL, st));
+            CK(prepass_reduce_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, 1,
+                                     mv.omin, mv.omin1, mv.omax2, st));
+            CK(prepass_rule_launch(T, plan->nslots, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, mv.omin,
+                                   mv.dmin2, mv.dmin12, mv.dmax22, prec, method, S->d_plans, S->s_lo, s_hi, mv.drs, st));
+        }
     }
     // ---- a-3..a-6 with the chosen plan (the workspace laid out for the largest candidate)
     const int parts = method == 3 ? 3 : 2;
@@ -979,8 +1004,9 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
     }
     if (rep) {
         rep->slices = 0;                                 // chosen on the device: mpcgemm_device_rule_result()
-        // planes, T GEMM, min, max-plus + rule (one launch unless MPCGEMM_RULE_SEPARATE), split, GEMM, fold
-        rep->kernel_launches += (getenv("MPCGEMM_RULE_SEPARATE") ? 7 : 6) + nsplit;
+        // planes, T GEMM, min, max-plus + rule (one launch unless MPCGEMM_RULE_SEPARATE), split, GEMM, fold;
+        // small shapes: planes, T by dp4a + stage 1, max-plus + rule, split, GEMM, fold
+        rep->kernel_launches += (prepass_small(m, n, k) ? 4 : 5) + (getenv("MPCGEMM_RULE_SEPARATE") ? 2 : 1) + nsplit;
         rep->slicegemm_ctas = SL.grid; rep->tile_m = geo.BM; rep->tile_n = geo.BN;
         rep->certified = 1;
     }
@@ -1108,11 +1134,13 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     }
     // workspace of row groups of mg rows (the ragged last group may need more slots)
     auto grouped_layout = [&](int64_t mg) {
-        Layout Lg = layout_for(mg, n, k, s, method, main_geometry(dev, mg, n, k, s, method, m).maxkb, prec, beta != 0);
+        const Geometry gg = main_geometry(dev, mg, n, k, s, method, m);
+        Layout Lg = layout_for(mg, n, k, s, method, gg.maxkb, prec, beta != 0, gg.g2);
         if (mg < m && m % mg) {
             const int64_t ml = m % mg;
             const int parts = method == 3 ? 3 : 2;
-            Layout Ll = layout_for(ml, n, k, s, method, main_geometry(dev, ml, n, k, s, method, m).maxkb, prec, beta != 0);
+            const Geometry gl = main_geometry(dev, ml, n, k, s, method, m);
+            Layout Ll = layout_for(ml, n, k, s, method, gl.maxkb, prec, beta != 0, gl.g2);
             const size_t extra = align_up((size_t)parts * s * mg * Lg.kp, 256) - align_up((size_t)parts * s * ml * Lg.kp, 256);
             Lg.main = std::max(Lg.main, Ll.main + extra);
         }
@@ -1345,7 +1373,8 @@ size_t mpcgemm_workspace_size(int64_t m, int64_t n, int64_t k, int32_t prec, mpc
         slices = rule_slices(prec, (int)method, rule_log2rho(std::max<int64_t>(k, 1), 1, 1, -1));   // largest
         if (slices < 0) slices = kMaxSlices;           // first-stage s (max-plus inputs may need more)
     }
-    Layout Lo = layout_for(m, n, k, slices, (int)method, main_geometry(dev, m, n, k, slices, (int)method).maxkb, prec, true);
+    const Geometry gw = main_geometry(dev, m, n, k, slices, (int)method);
+    Layout Lo = layout_for(m, n, k, slices, (int)method, gw.maxkb, prec, true, gw.g2);
     return std::max(Lo.main, Lo.pre);
 }
 

@@ -948,6 +948,63 @@ prepass_maxplus_rule_kernel(const int32_t *T, int nslots, int64_t nstrips, int64
     rule_body(min1, min2, min12, max22, nb, k, prec, method, plans, s_lo, s_hi, drs, &lr_sh);
 }
 
+// Small shapes (device rule, m n k <= 2^27): T and the stage-1 minimum in ONE launch, without the
+// tcgen05 T GEMM.  Each 32 x 32 output tile computes T_ij = sum_k t_ik u_jk itself with dp4a on the
+// planes' bytes (the t / u digits are in [0, 127] and zero beyond k, so the int32 sum is the s = 1
+// slice GEMM's exact T for k <= 65536), stores it as ONE partial plane (part_off layout, nslots = 1)
+// for the gated stage 2, and adds the tile's minimum over nonzero line pairs to its 256-row block.
+// Replaces the T GEMM and the stage-1 min kernel (two launches).
+__global__ void __launch_bounds__(256)
+prepass_small_t_kernel(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n, int64_t k, int64_t kp,
+                       const uint8_t *nzA, const uint8_t *nzB, int32_t *T, int64_t nstrips, unsigned long long *min1)
+{
+    __shared__ uint32_t ta[32][33], tb[32][33];       // 128 k of t / u per row as 32 words
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;    // 32 x 8
+    const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+    int32_t tv[4] = {0, 0, 0, 0};
+    for (int64_t k0 = 0; k0 < kp; k0 += 128) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < 32 * 32; q += 256) {   // (kp is a multiple of 16: a word is
+            const int rr = q >> 5, w = q & 31;               //  inside the row or past its end)
+            const int64_t kk = k0 + 4 * w;
+            ta[rr][w] = (i0 + rr < m && kk < kp) ? *reinterpret_cast<const uint32_t *>(tA + (i0 + rr) * kp + kk) : 0u;
+            tb[rr][w] = (j0 + rr < n && kk < kp) ? *reinterpret_cast<const uint32_t *>(tB + (j0 + rr) * kp + kk) : 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            int32_t acc = tv[e];
+            const int r_ = ty * 4 + e;
+#pragma unroll 8
+            for (int w = 0; w < 32; w++) acc = __dp4a((int)ta[r_][w], (int)tb[tx][w], acc);   // bytes in [0, 127]
+            tv[e] = acc;
+        }
+    }
+    unsigned long long l1 = ULLONG_MAX;
+    for (int e = 0; e < 4; e++) {
+        const int64_t i = i0 + ty * 4 + e, j = j0 + tx;
+        if (i >= m || j >= n) continue;
+        T[part_off(i, j, 0, 1, nstrips)] = tv[e];
+        if (nzA[i] && nzB[j]) l1 = (unsigned long long)tv[e] < l1 ? (unsigned long long)tv[e] : l1;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, l1, o);
+        l1 = y < l1 ? y : l1;
+    }
+    if (tx == 0 && l1 != ULLONG_MAX) atomicMin(min1 + (i0 >> kSBlkShift), l1);   // one 256-row block
+}
+
+cudaError_t prepass_small_t_launch(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n, int64_t k, int64_t kp,
+                                   const uint8_t *nzA, const uint8_t *nzB, int32_t *T, int64_t nstrips,
+                                   unsigned long long *min1, cudaStream_t st)
+{
+    if (m <= 0 || n <= 0 || k > 65536) return cudaErrorInvalidValue;
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
+    prepass_small_t_kernel<<<grid, 256, 0, st>>>(tA, tB, m, n, k, kp, nzA, nzB, T, nstrips, min1);
+    return cudaGetLastError();
+}
+
 cudaError_t prepass_rule_launch(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n, int64_t k,
                                 int64_t kp, const uint8_t *nzA, const uint8_t *nzB, const int32_t *relA,
                                 const int32_t *relB, const unsigned long long *min1, unsigned long long *min2,
