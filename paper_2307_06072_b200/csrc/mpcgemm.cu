@@ -50,12 +50,13 @@ struct Nvtx {
     ~Nvtx() { nvtxRangePop(); }
 };
 int env_int(const char *name, int dflt);
-// k-phase hint mode of the CTA-pair slice GEMM (MPCGEMM_KPHASE); the tile-wide mode 3 encodes an
-// absolute k-block in an int32 position, so it falls back to mode 2 when KB >= 2^20
-// device rule: the small-shape pre-pass (T by dp4a and the stage-1 minimum in one launch, no T GEMM)
+// device rule: the small-shape pre-pass (T by dp4a and the stage-1 minimum in one launch, no T GEMM;
+// MPCGEMM_PREPASS_SMALL=0: the tcgen05 T GEMM path)
 inline bool prepass_small(int64_t m, int64_t n, int64_t k) {
     return k > 0 && k <= 65536 && m * n * k <= (int64_t(1) << 27) && env_int("MPCGEMM_PREPASS_SMALL", 1) != 0;
 }
+// k-phase hint mode of the CTA-pair slice GEMM (MPCGEMM_KPHASE); the tile-wide mode 3 encodes an
+// absolute k-block in an int32 position, so it falls back to mode 2 when KB >= 2^20
 inline int kphase_mode(int64_t KB) {
     const int m = env_int("MPCGEMM_KPHASE", 2);
     return m == 3 && KB >= (1 << 20) ? 2 : m;

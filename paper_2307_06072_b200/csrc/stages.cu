@@ -791,16 +791,15 @@ MPC_DEV void maxplus_body(const int32_t *T, int nslots, int64_t nstrips, int64_t
                           int64_t k, int64_t kp, const uint8_t *nzA, const uint8_t *nzB,
                           const int32_t *relA, const int32_t *relB,
                           unsigned long long *out_min, unsigned long long *out_min1, long long *out_max2,
-                          const unsigned long long *gate, int64_t ngate)
+                          const unsigned long long *gate, int64_t ngate, int64_t i0, int64_t j0)
 {
     __shared__ int32_t sa[32][33], sb[32][33];
     if (gate) {                                       // device rule: run only if a block's stage-1 min is 0
         int z = 0;
-        for (int64_t b = threadIdx.x; b < ngate; b += blockDim.x) z |= gate[b] == 0;
+        for (int64_t b = threadIdx.x; b < ngate; b += blockDim.x) z |= __ldcg(gate + b) == 0;
         if (!__syncthreads_or(z)) return;
     }
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;    // 32 x 8
-    const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;    // 32 x 8 (tile origin i0, j0)
     int32_t mp[4] = {kRelSentinel, kRelSentinel, kRelSentinel, kRelSentinel};
     for (int64_t k0 = 0; k0 < k; k0 += 32) {
         __syncthreads();
@@ -854,7 +853,8 @@ prepass_maxplus_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m,
                        unsigned long long *out_min, unsigned long long *out_min1, long long *out_max2,
                        const unsigned long long *gate = nullptr, int64_t ngate = 0)
 {
-    maxplus_body(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, out_min, out_min1, out_max2, gate, ngate);
+    maxplus_body(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, out_min, out_min1, out_max2, gate, ngate,
+                 (int64_t)blockIdx.y * 32, (int64_t)blockIdx.x * 32);
 }
 
 __global__ void readback_kernel(uint32_t *dst, const uint32_t *src, int64_t n) {
@@ -936,7 +936,8 @@ prepass_maxplus_rule_kernel(const int32_t *T, int nslots, int64_t nstrips, int64
                             long long *max22, int64_t nb, int prec, int method, const DevPlan *plans, int s_lo, int s_hi,
                             DevRuleState *drs, unsigned int *done)
 {
-    maxplus_body(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, min2, min12, max22, min1, nb);
+    maxplus_body(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, min2, min12, max22, min1, nb,
+                 (int64_t)blockIdx.y * 32, (int64_t)blockIdx.x * 32);
     __shared__ int last;
     __shared__ double lr_sh;
     __syncthreads();
@@ -954,13 +955,11 @@ prepass_maxplus_rule_kernel(const int32_t *T, int nslots, int64_t nstrips, int64
 // slice GEMM's exact T for k <= 65536), stores it as ONE partial plane (part_off layout, nslots = 1)
 // for the gated stage 2, and adds the tile's minimum over nonzero line pairs to its 256-row block.
 // Replaces the T GEMM and the stage-1 min kernel (two launches).
-__global__ void __launch_bounds__(256)
-prepass_small_t_kernel(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n, int64_t k, int64_t kp,
-                       const uint8_t *nzA, const uint8_t *nzB, int32_t *T, int64_t nstrips, unsigned long long *min1)
+MPC_DEV void small_t_tile(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n, int64_t kp, const uint8_t *nzA,
+                          const uint8_t *nzB, int32_t *T, int64_t nstrips, unsigned long long *min1, int64_t i0, int64_t j0)
 {
     __shared__ uint32_t ta[32][33], tb[32][33];       // 128 k of t / u per row as 32 words
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;    // 32 x 8
-    const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
     int32_t tv[4] = {0, 0, 0, 0};
     for (int64_t k0 = 0; k0 < kp; k0 += 128) {
         __syncthreads();
@@ -993,6 +992,13 @@ prepass_small_t_kernel(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n,
         l1 = y < l1 ? y : l1;
     }
     if (tx == 0 && l1 != ULLONG_MAX) atomicMin(min1 + (i0 >> kSBlkShift), l1);   // one 256-row block
+}
+
+__global__ void __launch_bounds__(256)
+prepass_small_t_kernel(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n, int64_t k, int64_t kp,
+                       const uint8_t *nzA, const uint8_t *nzB, int32_t *T, int64_t nstrips, unsigned long long *min1)
+{
+    small_t_tile(tA, tB, m, n, kp, nzA, nzB, T, nstrips, min1, (int64_t)blockIdx.y * 32, (int64_t)blockIdx.x * 32);
 }
 
 cudaError_t prepass_small_t_launch(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n, int64_t k, int64_t kp,

@@ -36,8 +36,8 @@ def host_and_device(A, B, prec, method):
 @pytest.mark.parametrize("method", ["3M", "4M"])
 @pytest.mark.parametrize("spread,k", [(16, 12), (16, 3), (0, 64), (4, 40), (0, 1), (30, 2), (8, 129)])
 def test_device_rule_matches_oracle(method, spread, k, small, monkeypatch):
-    """small = "1": the fused small-shape pre-pass (T by dp4a, both stages and the rule in one
-    launch; the default below m n k = 2^27); "0": the T GEMM on tcgen05 + the reduction kernels."""
+    """small = "1" (default below m n k = 2^27): T by dp4a + stage 1 in one launch, then stage 2 +
+    rule; "0": the T GEMM on tcgen05 + the reduction kernels."""
     monkeypatch.setenv("MPCGEMM_PREPASS_SMALL", small)
     m, n, prec = 70, 90, 256
     A = mpgen.random_cmat(spread + k, 9, m, k, prec, spread, zero_frac=0.1)
