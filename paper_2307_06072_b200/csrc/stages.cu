@@ -322,6 +322,15 @@ MPC_DEV uint64_t add64_carry(uint64_t a, uint64_t b, uint32_t &c) {
     return ((uint64_t)hi << 32) | lo;
 }
 
+// bits [bo, bo + 64) of hi:lo (0 <= bo < 64) as two 32-bit funnel shifts of word pairs chosen by
+// bo >= 32 (no 64-bit shift pair and no bo == 0 branch)
+MPC_DEV uint64_t funnel64(uint64_t lo, uint64_t hi, uint32_t bo) {
+    const uint32_t l0 = (uint32_t)lo, l1 = (uint32_t)(lo >> 32), h0 = (uint32_t)hi, h1 = (uint32_t)(hi >> 32);
+    const bool up = bo >= 32;
+    const uint32_t w0 = up ? l1 : l0, w1 = up ? h0 : l1, w2 = up ? h1 : h0;
+    return ((uint64_t)__funnelshift_r(w1, w2, bo) << 32) | __funnelshift_r(w0, w1, bo);   // (shift mod 32)
+}
+
 // TMA-staged split (L in {2, 4, 8, 16}): a CTA takes kSplitT consecutive k of one line; one thread
 // issues two 3-D TMA loads (Re, Im) of the 256 entries' limbs into shared memory -- coalesced,
 // vectorised, every DRAM sector read once; the rows land swizzled (the swizzle span = one 8L-byte
@@ -380,21 +389,25 @@ MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, 
     //  zero low bits wherever the XOR acts)
     const uint32_t xm = (uint32_t)((((tid * ROW) >> 7) & SWM) << 4);
     const uint32_t myrow = smem_u32(tile) + (uint32_t)(tid * ROW);      // shared-space address
-    auto limb = [&](int p, int64_t l) -> uint64_t {
-        if ((uint64_t)l >= (uint64_t)L) return 0ull;
+    // (limb indices are int32: saturated below at -(nwords + 2) and above at L, which keeps every
+    //  word of the walk -- all limbs outside [0, L) read as zero -- with one 32-bit bound check)
+    auto limb = [&](int p, int32_t l) -> uint64_t {
+        if ((uint32_t)l >= (uint32_t)L) return 0ull;
         uint64_t v;
         asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(myrow + (uint32_t)(p * kSplitT * ROW) + ((uint32_t)(8 * l) ^ xm)));
         return v;
     };
-    int64_t li[2]; int bo[2]; uint64_t lo[2], nm[2];
+    const int32_t li_lo = -((s + 7) / 8 + 2);
+    int32_t li[2]; int bo[2]; uint64_t lo[2], nm[2];
     uint32_t nc[2];                                   // two's complement: x ^ nm + carry (nc starts at neg)
     bool zero[2];
 #pragma unroll
     for (int p = 0; p < 2; p++) {
         zero[p] = !valid || limb(p, L - 1) == 0;
         const int64_t pos0 = 64 * (int64_t)L - W + e - ex[p];
-        li[p] = pos0 >= 0 ? (pos0 >> 6) : -((-pos0 + 63) >> 6);
-        bo[p] = (int)(pos0 - (li[p] << 6));
+        const int64_t l64 = pos0 >= 0 ? (pos0 >> 6) : -((-pos0 + 63) >> 6);
+        bo[p] = (int)(pos0 - (l64 << 6));
+        li[p] = (int32_t)(l64 < li_lo ? li_lo : l64 > L ? L : l64);
         lo[p] = zero[p] ? 0ull : limb(p, li[p]);
         neg[p] = neg[p] && !zero[p];
         nm[p] = neg[p] ? ~0ull : 0ull;
@@ -433,7 +446,7 @@ MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, 
 #pragma unroll
         for (int p = 0; p < 2; p++) {
             const uint64_t hi = zero[p] ? 0ull : limb(p, li[p] + 1);
-            uint64_t x = bo[p] ? ((lo[p] >> bo[p]) | (hi << (64 - bo[p]))) : lo[p];
+            const uint64_t x = funnel64(lo[p], hi, (uint32_t)bo[p]);
             lo[p] = hi; li[p]++;
             y[p] = add64_carry(x ^ nm[p], 0ull, nc[p]);   // negation without a divergent branch
         }
