@@ -873,8 +873,11 @@ int dev_plan_set(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, int met
     DevPlanSet S;
     S.s_lo = s_lo; S.s_hi = s_hi;
     std::vector<DevPlan> hp;
+    // one unit shape (G = 2 or single diagonals) for every candidate, so their slot orders agree
+    const int g2c = main_geometry(dev, m, n, k, s_hi, method).g2;
     for (int s = s_lo; s <= s_hi; s++) {
-        const Geometry geo = main_geometry(dev, m, n, k, s, method);
+        Geometry geo = main_geometry(dev, m, n, k, s, method);
+        geo.g2 = g2c;
         PlanKey key2{m, n, k, s, method, geo.BM, geo.BN, geo.grid, 0, geo.maxkb, geo.g2,
                      env_int("MPCGEMM_ORDER", 2), {}};
         Plan *plan;

@@ -120,3 +120,19 @@ def test_device_rule_cuda_graph():
         assert st == 0 and s == s_ref
         R = oracle.ozaki(Ah, Bh, prec, method, s_ref)
         assert same_bits(P.to_host(C), R), first_mismatch(P.to_host(C), R)
+
+
+@pytest.mark.parametrize("method", ["3M", "4M"])
+@pytest.mark.parametrize("prec", [368, 384, 400])
+def test_device_rule_unit_shape_boundary(method, prec):
+    """m = 1024, n = 128 (1-CTA tiles, 8 row tiles): the plan switches from single-diagonal units
+    to diagonal pairs at s = 49 (8 tiles x ceil(s/2) x 3 jobs >= 4 x 148 CTAs), inside these
+    precisions' candidate ranges.  The device rule builds every candidate with one unit shape (the
+    largest candidate's), the host rule with the chosen s's own -- same bits either way."""
+    m, n, k = 1024, 128, 64
+    A = mpgen.random_cmat(prec, 11, m, k, prec, 2)
+    B = mpgen.random_cmat(prec, 12, k, n, prec, 2)
+    dA, dB, C0, r0, C1, r1, st, s, bounds = host_and_device(A, B, prec, method)
+    assert st == 0 and s == r0["slices"]
+    H0, H1 = P.to_host(C0), P.to_host(C1)
+    assert same_bits(H0, H1), first_mismatch(H0, H1)
