@@ -1062,6 +1062,8 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     Nvtx range_call("mpcgemm");
     if (validate) CK(cudaMemsetAsync(errflag, 0, 4, st));
     int lm_launches = 0;
+    const bool devrule = opts && opts->device_rule && !forced && !adaptive && carrier == 0 && !simt && !validate &&
+                         !beta && !alpha_neg && group_rows == 0 && !hook;
     {
         Nvtx r("mpcgemm.a1_linemax");
         const size_t lm_need = 8 * (size_t)(m + n) + 16;
@@ -1081,8 +1083,6 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         if (h & 2u) return fail(MPCGEMM_ERR_EXP_RANGE, "|exp| > 2^61");
         if (h & 1u) return fail(MPCGEMM_ERR_NOT_NORMALIZED, "mantissa not normalized");
     }
-    const bool devrule = opts && opts->device_rule && !forced && !adaptive && carrier == 0 && !simt && !validate &&
-                         !beta && !alpha_neg && group_rows == 0 && !hook;
     if (devrule) {
         if (rep) rep->kernel_launches = launches;
         return run_device_rule(dev, m, n, k, prec, A, B, C, method, st, meta, dc, opts, rep);

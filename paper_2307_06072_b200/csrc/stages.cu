@@ -668,6 +668,43 @@ cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, i
 constexpr int32_t kRelSentinel = -(1 << 30);
 constexpr int32_t kRelClamp = -(1 << 28);
 
+// one pre-pass plane entry (line, kk < k) of a side: t = the top 7 bits of the larger part below
+// the line's exponent e, rel = the entry's exponent relative to e (clamped; sentinel if zero)
+MPC_DEV void planes_entry(const DMat &re, const DMat &im, int side, int64_t line, int64_t kk, int L, int64_t e,
+                          int &best, int32_t &r)
+{
+    best = 0;
+    int64_t emax = 0; bool any = false;
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        const DMat &M = p ? im : re;
+        const int64_t idx = side == 0 ? line * M.ld + kk : kk * M.ld + line;
+        const uint64_t *N = M.limbs + idx * L;
+        const uint64_t top = __ldg(N + L - 1);
+        if (!top) continue;
+        const int64_t ex = __ldg(M.exp + idx);
+        // t = floor(|x| 2^(7-e)) = bits [64L - 7 + e - ex, 64L) of N
+        const int64_t pos = 64 * (int64_t)L - 7 + e - ex;
+        uint64_t v = 0;
+        if (pos < 64 * (int64_t)L) {
+            const int64_t li = pos >> 6;
+            const int bo = (int)(pos & 63);
+            const uint64_t lo = __ldg(N + li);
+            const uint64_t hi = li + 1 < L ? __ldg(N + li + 1) : 0ull;
+            v = bo ? ((lo >> bo) | (hi << (64 - bo))) : lo;
+        }
+        int tv = (int)(v & 0x7F);
+        best = tv > best ? tv : best;
+        if (!any || ex > emax) emax = ex;
+        any = true;
+    }
+    r = kRelSentinel;
+    if (any) {
+        int64_t d = emax - e;                          // <= 0
+        r = d < kRelClamp ? kRelClamp : (int32_t)d;
+    }
+}
+
 MPC_DEV void prepass_planes_body(const DMat &re, const DMat &im, int side, int64_t lines, int64_t k, int64_t kp, int L,
                                  const int64_t *__restrict__ eline, int8_t *t, int32_t *rel, int64_t bx, int64_t by,
                                  int64_t gy)
@@ -676,39 +713,9 @@ MPC_DEV void prepass_planes_body(const DMat &re, const DMat &im, int side, int64
     if (kk >= kp) return;
     for (int64_t line = by; line < lines; line += gy) {
         int best = 0;
-        int64_t emax = 0; bool any = false;
-        if (kk < k) {
-            const int64_t e = eline[line];
-#pragma unroll
-            for (int p = 0; p < 2; p++) {
-                const DMat &M = p ? im : re;
-                const int64_t idx = side == 0 ? line * M.ld + kk : kk * M.ld + line;
-                const uint64_t *N = M.limbs + idx * L;
-                const uint64_t top = __ldg(N + L - 1);
-                if (!top) continue;
-                const int64_t ex = __ldg(M.exp + idx);
-                // t = floor(|x| 2^(7-e)) = bits [64L - 7 + e - ex, 64L) of N
-                const int64_t pos = 64 * (int64_t)L - 7 + e - ex;
-                uint64_t v = 0;
-                if (pos < 64 * (int64_t)L) {
-                    const int64_t li = pos >> 6;
-                    const int bo = (int)(pos & 63);
-                    const uint64_t lo = __ldg(N + li);
-                    const uint64_t hi = li + 1 < L ? __ldg(N + li + 1) : 0ull;
-                    v = bo ? ((lo >> bo) | (hi << (64 - bo))) : lo;
-                }
-                int tv = (int)(v & 0x7F);
-                best = tv > best ? tv : best;
-                if (!any || ex > emax) emax = ex;
-                any = true;
-            }
-        }
-        t[line * kp + kk] = (int8_t)best;
         int32_t r = kRelSentinel;
-        if (any) {
-            int64_t d = emax - eline[line];         // <= 0
-            r = d < kRelClamp ? kRelClamp : (int32_t)d;
-        }
+        if (kk < k) planes_entry(re, im, side, line, kk, L, eline[line], best, r);
+        t[line * kp + kk] = (int8_t)best;
         rel[line * kp + kk] = r;
     }
 }

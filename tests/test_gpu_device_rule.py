@@ -36,7 +36,7 @@ def host_and_device(A, B, prec, method):
 @pytest.mark.parametrize("method", ["3M", "4M"])
 @pytest.mark.parametrize("spread,k", [(16, 12), (16, 3), (0, 64), (4, 40), (0, 1), (30, 2), (8, 129)])
 def test_device_rule_matches_oracle(method, spread, k, small, monkeypatch):
-    """small = "1" (default below m n k = 2^27): T by dp4a + stage 1 in one launch, then stage 2 +
+    """small = "1" (default up to m n k = 2^27): T by dp4a + stage 1 in one launch, then stage 2 +
     rule; "0": the T GEMM on tcgen05 + the reduction kernels."""
     monkeypatch.setenv("MPCGEMM_PREPASS_SMALL", small)
     m, n, prec = 70, 90, 256
@@ -87,11 +87,11 @@ def test_device_rule_configs(cfg, method):
     assert same_bits(P.to_host(C0), P.to_host(C1))
 
 
-def test_device_rule_cuda_graph():
+@pytest.mark.parametrize("m,n,k", [(150, 260, 96), (60, 70, 40)])
+def test_device_rule_cuda_graph(m, n, k):
     """The device-rule call captured once in a CUDA graph and replayed on new inputs: each replay
     gives the host-rule result bit for bit (s re-derived on the device every replay)."""
     prec, method = 192, "3M"
-    m, n, k = 150, 260, 96
     A1 = mpgen.random_cmat(3, 1, m, k, prec, 3)
     B1 = mpgen.random_cmat(3, 2, k, n, prec, 3)
     A2 = mpgen.random_cmat(4, 1, m, k, prec, 8)                # other data, other s
