@@ -776,33 +776,57 @@ MPC_DEV int64_t sum_T(const int32_t *T, int nslots, int64_t nstrips, int64_t i, 
 }
 
 // stage 1: min over nonzero line pairs of T_ij, per 256-row block (out_min[i >> 8]; the
-// global value is the min over blocks, NEXT-4 uses each block's own)
-__global__ void prepass_min_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
-                                   const uint8_t *nzA, const uint8_t *nzB, unsigned long long *out_min)
+// global value is the min over blocks, NEXT-4 uses each block's own).  Each CTA takes one
+// contiguous range of (i, j) -- a few rows, so (nearly) one 256-row block -- keeps a running
+// minimum per thread, and reduces over the warp and the CTA before ONE atomic per row block it
+// touched (a global atomic per warp on the ~m/256 targets serialised in L2: 82-91 us at configs
+// 4 and 5 before)
+__global__ void __launch_bounds__(256)
+prepass_min_kernel(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n,
+                   const uint8_t *nzA, const uint8_t *nzB, unsigned long long *out_min)
 {
+    __shared__ unsigned long long wv[8];
+    __shared__ long long wb[8];
     const int64_t total = m * n;
-    const int64_t step = (int64_t)gridDim.x * blockDim.x;
-    // every warp iteration covers 32 consecutive (i, j); reduce per warp when they share a block
-    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); t0 < total; t0 += step) {
-        const int64_t t = t0 + (threadIdx.x & 31);
-        unsigned long long v = ULLONG_MAX;
-        int64_t blk = -1;
-        if (t < total) {
-            const int64_t i = t / n, j = t - i * n;
-            blk = i >> kSBlkShift;
-            if (nzA[i] && nzB[j]) v = (unsigned long long)sum_T(T, nslots, nstrips, i, j);
+    const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t beg = (int64_t)blockIdx.x * per, end = min(total, beg + per);
+    unsigned long long v = ULLONG_MAX;
+    int64_t vb = -1;                                  // the row block v belongs to
+    int64_t i = (beg + threadIdx.x) / n, j = beg + threadIdx.x - i * n;   // one division; then stepped
+    for (int64_t t = beg + threadIdx.x; t < end; t += blockDim.x, j += blockDim.x) {
+        while (j >= n) { j -= n; i++; }
+        const int64_t b = i >> kSBlkShift;
+        if (b != vb) {                                // (at most once per row-block boundary)
+            if (vb >= 0 && v != ULLONG_MAX) atomicMin(out_min + vb, v);
+            v = ULLONG_MAX; vb = b;
         }
-        const int64_t b0 = __shfl_sync(0xffffffffu, blk, 0);
-        if (__all_sync(0xffffffffu, blk == b0 || blk < 0)) {
+        if (nzA[i] && nzB[j]) {
+            const unsigned long long x = (unsigned long long)sum_T(T, nslots, nstrips, i, j);
+            v = x < v ? x : v;
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long b0 = __shfl_sync(0xffffffffu, vb, 0);
+    if (__all_sync(0xffffffffu, vb == b0 || vb < 0)) {
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
-                v = y < v ? y : v;
-            }
-            if ((threadIdx.x & 31) == 0 && v != ULLONG_MAX) atomicMin(out_min + b0, v);
-        } else if (v != ULLONG_MAX) {
-            atomicMin(out_min + blk, v);
+        for (int o = 16; o; o >>= 1) { const unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o); v = y < v ? y : v; }
+        if (lane == 0) { wv[warp] = v; wb[warp] = b0; }
+    } else {
+        if (vb >= 0 && v != ULLONG_MAX) atomicMin(out_min + vb, v);
+        if (lane == 0) { wv[warp] = ULLONG_MAX; wb[warp] = -1; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {                           // merge the warps; one atomic per row block
+        unsigned long long cv = ULLONG_MAX;
+        long long cb = -1;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            if (wb[w] < 0 || wv[w] == ULLONG_MAX) continue;
+            if (wb[w] != cb) {
+                if (cb >= 0) atomicMin(out_min + cb, cv);
+                cb = wb[w]; cv = wv[w];
+            } else cv = wv[w] < cv ? wv[w] : cv;
         }
+        if (cb >= 0) atomicMin(out_min + cb, cv);
     }
 }
 
