@@ -1056,8 +1056,8 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     if (int rc = grow(&dc.meta, &dc.meta_bytes, Lo.meta)) return rc;
     uint8_t *meta = (uint8_t *)dc.meta;
     const MetaView mv = meta_view(meta, m, n);
-    int64_t *eA = mv.eA, *eB = mv.eB;
-    uint8_t *nzA = mv.nzA, *nzB = mv.nzB;
+    int64_t *eA = mv.eA;                               // (eB = eA + m, nzB = nzA + m: one a-1 launch for both)
+    uint8_t *nzA = mv.nzA;
     uint32_t *errflag = mv.errflag;
     Nvtx range_call("mpcgemm");
     if (validate) CK(cudaMemsetAsync(errflag, 0, 4, st));
@@ -1073,7 +1073,6 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         }
         CK(linemax2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, L, prec, eA, nzA, errflag, validate, st,
                            &lm_launches, (unsigned long long *)dc.lm));
-        (void)eB; (void)nzB;                          // (eB = eA + m, nzB = nzA + m)
     }
     if (E) CK(cudaEventRecord(E->ev[1], st));
     int launches = lm_launches + (validate ? 1 : 0);   // linemax (A and B, decode fused) [, flag readback]
