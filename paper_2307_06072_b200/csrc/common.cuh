@@ -260,6 +260,9 @@ MPC_DEV void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar
 
 // orders this thread's generic-proxy shared-memory accesses before later async-proxy accesses
 // (TMA / bulk copies) -- e.g. before releasing a ring slot that a TMA load will overwrite
+// programmatic dependent launch: wait until the preceding grid in the stream has completed and its
+// memory is visible (a no-op when the kernel was not launched with programmatic serialization)
+MPC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 MPC_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // L2 cache policies (createpolicy) and a 16-byte store carrying one

@@ -6,6 +6,24 @@
 
 namespace mpc {
 
+// Programmatic dependent launch (device-rule calls, set for the call by gemm_impl): the hot-path
+// kernels are launched with programmatic stream serialization and each executes
+// griddepcontrol.wait (pdl_wait) before touching global memory, so a kernel's launch and
+// scheduling overlap its predecessor's tail -- the fixed per-launch cost of tiny calls.
+extern thread_local int g_pdl;
+template <typename... Exp, typename... Act>
+inline cudaError_t launch_pdl(void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Act &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    if (g_pdl) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<Act &&>(args)...);
+}
+
 struct SliceGemmLaunch {
     GemmParams P;
     const int8_t *digA, *digB;   // [partsA*s][rowsA][kp], [partsB*s][rowsB][kp]

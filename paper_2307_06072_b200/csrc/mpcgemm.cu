@@ -24,6 +24,7 @@
 #include "kernels.h"
 #include "rule.cuh"
 
+namespace mpc { thread_local int g_pdl = 0; }         // kernels.h: launch_pdl
 using namespace mpc;
 
 namespace {
@@ -1064,6 +1065,12 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     int lm_launches = 0;
     const bool devrule = opts && opts->device_rule && !forced && !adaptive && carrier == 0 && !simt && !validate &&
                          !beta && !alpha_neg && group_rows == 0 && !hook;
+    // device-rule calls (no host synchronisation inside): programmatic dependent launches
+    struct PdlScope {
+        int prev;
+        explicit PdlScope(bool on) : prev(g_pdl) { g_pdl = on && env_int("MPCGEMM_PDL", 1) != 0; }
+        ~PdlScope() { g_pdl = prev; }
+    } pdl_scope(devrule);
     {
         Nvtx r("mpcgemm.a1_linemax");
         const size_t lm_need = 8 * (size_t)(m + n) + 16;

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(256, 1)
 slicegemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ GemmParams P)
 {
+    pdl_wait();
     using Cfg = TcCfg<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -296,6 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 slicegemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmParams P)
 {
+    pdl_wait();
     using Cfg = Tc2Cfg<STAGES>;
     constexpr int BN = Cfg::BN;
     extern __shared__ uint8_t smem_raw[];
@@ -755,8 +757,7 @@ static cudaError_t launch_tc(const SliceGemmLaunch &L, cudaStream_t st) {
     auto kern = slicegemm_tc_kernel<BN, STAGES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    kern<<<L.grid, 256, Cfg::SMEM, st>>>(ta, tb, L.P);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(L.grid), dim3(256), Cfg::SMEM, st, ta, tb, L.P);
 }
 
 template <int STAGES>
@@ -768,8 +769,7 @@ static cudaError_t launch_tc2(const SliceGemmLaunch &L, cudaStream_t st) {
     auto kern = slicegemm_tc2_kernel<STAGES>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    kern<<<L.grid & ~1, 256, Cfg::SMEM, st>>>(ta, tb, L.P);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(L.grid & ~1), dim3(256), Cfg::SMEM, st, ta, tb, L.P);
 }
 
 cudaError_t slicegemm_launch(const SliceGemmLaunch &L, cudaStream_t st) {

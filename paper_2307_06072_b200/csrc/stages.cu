@@ -104,6 +104,7 @@ __global__ void linemax2_kernel(DMat re0, DMat im0, int64_t rows0, int64_t cols0
                                 uint32_t *errflag, int validate, int64_t gx0, int64_t gy0, int64_t gx1, int64_t gy1,
                                 unsigned int *done, int64_t *eline, uint8_t *nz, int64_t lines, int clean)
 {
+    pdl_wait();
     const int64_t b = blockIdx.x;
     if (b < gx0 * gy0) linemax_body(re0, im0, rows0, cols0, L, prec, 0, emax0, errflag, validate, b % gx0, b / gx0, gy0);
     else {
@@ -183,9 +184,10 @@ cudaError_t linemax2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, i
         if (e != cudaSuccess) return e;
     }
     if (blocks > 0) {
-        linemax2_kernel<<<(unsigned)blocks, dim3(32, 8), 0, st>>>(Are, Aim, m, k, Bre, Bim, k, n, L, prec, acc, acc + m,
-                                                                  errflag, validate, gx0, gy0, gx1, gy1, done, eAB, nzAB,
-                                                                  m + n, clean);
+        const cudaError_t le = launch_pdl(linemax2_kernel, dim3((unsigned)blocks), dim3(32, 8), 0, st, Are, Aim, m, k, Bre,
+                                          Bim, k, n, L, prec, acc, acc + m, errflag, validate, gx0, gy0, gx1, gy1, done,
+                                          eAB, nzAB, m + n, clean);
+        if (le != cudaSuccess) return le;
     } else {
         linemax_finalize_kernel<<<(unsigned)((m + n + 255) / 256), 256, 0, st>>>(acc, m + n, eAB, nzAB);
     }
@@ -551,6 +553,7 @@ split2_tma_kernel(const __grid_constant__ CUtensorMap mAre, const __grid_constan
                   const int64_t *__restrict__ eB, int s, int nparts, int8_t *__restrict__ digA, int8_t *__restrict__ digB,
                   const DevRuleState *drs)
 {
+    pdl_wait();
     if (drs) { if (drs->status) return; s = drs->cur.s; }
     const int64_t y = blockIdx.y, k0 = (int64_t)blockIdx.x * kSplitT;
     if (y < n) split_tma_body<L, true>(&mBre, &mBim, Bre, Bim, 1, n, k, kp, eB, s, nparts, digB, y, k0);
@@ -600,9 +603,8 @@ static cudaError_t split2_launch_t(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((kp + kSplitT - 1) / kSplitT), (unsigned)(m + n));
     auto cm = [&](int q) { return *reinterpret_cast<const CUtensorMap *>(maps[q]); };
-    split2_tma_kernel<L><<<grid, kSplitT, sm, st>>>(cm(0), cm(1), cm(2), cm(3), Are, Aim, Bre, Bim, m, n, k, kp, eA, eB, s,
-                                                   nparts, digA, digB, drs);
-    return cudaGetLastError();
+    return launch_pdl(split2_tma_kernel<L>, grid, dim3(kSplitT), sm, st, cm(0), cm(1), cm(2), cm(3), Are, Aim, Bre, Bim, m, n,
+                      k, kp, eA, eB, s, nparts, digA, digB, drs);
 }
 
 // a-3 for B and A in one launch when the TMA path applies (else two split_launch calls)
@@ -731,6 +733,7 @@ __global__ void prepass_planes2_kernel(DMat re0, DMat im0, int64_t lines0, const
                                        int64_t k, int64_t kp, int L, int64_t gx, int64_t gy0, int64_t gy1,
                                        unsigned long long *fill0, int64_t nfill0, unsigned long long *fill1, int64_t nfill1)
 {
+    pdl_wait();
     const int64_t b = blockIdx.x;
     if (b == 0) {                                      // the stage-1/2 reduction targets: all ones
         for (int64_t i = threadIdx.x; i < nfill0; i += blockDim.x) fill0[i] = ~0ull;   // (replaces two
@@ -754,10 +757,8 @@ cudaError_t prepass_planes2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64
         return e;
     }
     const int64_t gx = (kp + 127) / 128, gy0 = std::min<int64_t>(m, 32768), gy1 = std::min<int64_t>(n, 32768);
-    prepass_planes2_kernel<<<(unsigned)(gx * (gy0 + gy1)), 128, 0, st>>>(Are, Aim, m, eA, tA, relA, Bre, Bim, n, eB, tB, relB,
-                                                                       k, kp, L, gx, gy0, gy1, fill0, nfill0, fill1,
-                                                                       nfill1);
-    return cudaGetLastError();
+    return launch_pdl(prepass_planes2_kernel, dim3((unsigned)(gx * (gy0 + gy1))), dim3(128), 0, st, Are, Aim, m, eA, tA,
+                      relA, Bre, Bim, n, eB, tB, relB, k, kp, L, gx, gy0, gy1, fill0, nfill0, fill1, nfill1);
 }
 
 cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,
@@ -980,6 +981,7 @@ prepass_maxplus_rule_kernel(const int32_t *T, int nslots, int64_t nstrips, int64
                             long long *max22, int64_t nb, int prec, int method, const DevPlan *plans, int s_lo, int s_hi,
                             DevRuleState *drs, unsigned int *done)
 {
+    pdl_wait();
     maxplus_body(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, min2, min12, max22, min1, nb,
                  (int64_t)blockIdx.y * 32, (int64_t)blockIdx.x * 32);
     __shared__ int last;
@@ -1042,6 +1044,7 @@ __global__ void __launch_bounds__(256)
 prepass_small_t_kernel(const int8_t *tA, const int8_t *tB, int64_t m, int64_t n, int64_t k, int64_t kp,
                        const uint8_t *nzA, const uint8_t *nzB, int32_t *T, int64_t nstrips, unsigned long long *min1)
 {
+    pdl_wait();
     small_t_tile(tA, tB, m, n, kp, nzA, nzB, T, nstrips, min1, (int64_t)blockIdx.y * 32, (int64_t)blockIdx.x * 32);
 }
 
@@ -1051,8 +1054,7 @@ cudaError_t prepass_small_t_launch(const int8_t *tA, const int8_t *tB, int64_t m
 {
     if (m <= 0 || n <= 0 || k > 65536) return cudaErrorInvalidValue;
     dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
-    prepass_small_t_kernel<<<grid, 256, 0, st>>>(tA, tB, m, n, k, kp, nzA, nzB, T, nstrips, min1);
-    return cudaGetLastError();
+    return launch_pdl(prepass_small_t_kernel, grid, dim3(256), 0, st, tA, tB, m, n, k, kp, nzA, nzB, T, nstrips, min1);
 }
 
 cudaError_t prepass_rule_launch(const int32_t *T, int nslots, int64_t nstrips, int64_t m, int64_t n, int64_t k,
@@ -1066,9 +1068,8 @@ cudaError_t prepass_rule_launch(const int32_t *T, int nslots, int64_t nstrips, i
         // the done counter follows max22[nb] (covered by the caller's all-ones memset)
         unsigned int *done = reinterpret_cast<unsigned int *>(max22 + nb);
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
-        prepass_maxplus_rule_kernel<<<grid, 256, 0, st>>>(T, nslots, nstrips, m, n, k, kp, nzA, nzB, relA, relB, min1, min2,
-                                                          min12, max22, nb, prec, method, plans, s_lo, s_hi, drs, done);
-        return cudaGetLastError();
+        return launch_pdl(prepass_maxplus_rule_kernel, grid, dim3(256), 0, st, T, nslots, nstrips, m, n, k, kp, nzA, nzB,
+                          relA, relB, min1, min2, min12, max22, nb, prec, method, plans, s_lo, s_hi, drs, done);
     }
     if (m > 0 && n > 0) {
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32));
@@ -1372,6 +1373,7 @@ template <int COLS, bool BETA, bool SFIX, int EPT = kFoldEPT, int RING = kFoldRi
 __global__ void __launch_bounds__(COLS / EPT + 32, BETA ? 1 : (SFIX ? 3 : MINB))
 fold_normalize_kernel(const FoldParams F, const __grid_constant__ CUtensorMap pmap)
 {
+    pdl_wait();
     constexpr bool UNIC = UPER > 0;
     static_assert(UPER % 3 == 0, "UNIC entries are whole groups of three slots");
     constexpr int PER = UNI1 ? 6 : UNIC ? UPER : kFoldPer;   // slots per ring entry
@@ -1703,8 +1705,8 @@ static cudaError_t fold_launch_t(const FoldParams &F, cudaStream_t st) {
         const int64_t gslots = ((F.m + kRowBlk - 1) / kRowBlk) * F.nstrips * F.nslots;
         if (encode_partials_map(map, F.partials, gslots, PER)) return cudaErrorInvalidValue;
     }
-    kern<<<(unsigned)blocks, COLS / EPT + 32, sm, st>>>(F, *reinterpret_cast<const CUtensorMap *>(map));
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3((unsigned)blocks), dim3(COLS / EPT + 32), sm, st, F,
+                      *reinterpret_cast<const CUtensorMap *>(map));
 }
 
 cudaError_t fold_normalize_launch(const FoldParams &F, cudaStream_t st)

@@ -136,3 +136,22 @@ def test_device_rule_unit_shape_boundary(method, prec):
     assert st == 0 and s == r0["slices"]
     H0, H1 = P.to_host(C0), P.to_host(C1)
     assert same_bits(H0, H1), first_mismatch(H0, H1)
+
+
+@pytest.mark.parametrize("m,n,k", [(64, 64, 64), (300, 260, 150)])
+def test_device_rule_pdl_on_off(m, n, k, monkeypatch):
+    """Device-rule calls launch their kernels with programmatic stream serialization (each kernel
+    waits in griddepcontrol.wait for its predecessor); MPCGEMM_PDL=0 launches them plainly.  Same
+    s, same bits, and both equal the host-rule call."""
+    prec, method = 256, "3M"
+    A = mpgen.random_cmat(k + 1, 5, m, k, prec, 4)
+    B = mpgen.random_cmat(k + 1, 6, k, n, prec, 4)
+    out = []
+    for pdl in ("1", "0"):
+        monkeypatch.setenv("MPCGEMM_PDL", pdl)
+        dA, dB, C0, r0, C1, r1, st, s, bounds = host_and_device(A, B, prec, method)
+        assert st == 0 and s == r0["slices"]
+        H0, H1 = P.to_host(C0), P.to_host(C1)
+        assert same_bits(H0, H1), first_mismatch(H0, H1)
+        out.append((s, H1))
+    assert out[0][0] == out[1][0] and same_bits(out[0][1], out[1][1])
