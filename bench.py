@@ -118,9 +118,11 @@ def run_reference(args):
     if rank != 0:
         return
     c = mpgen.CONFIGS[args.config]
-    A, B = mpgen.config_inputs(args.config, seed=0)
+    A, B = mpgen.config_inputs(args.config, seed=args.seed)
     import oracle
     s, _ = oracle.auto_slices(A, B, c["prec"], args.method)           # the full slice rule
+    if args.slices:
+        s = args.slices
     cores = os.cpu_count() or 1
     per_step = max(cores, 8)
     rng = np.random.default_rng(99)
@@ -169,7 +171,7 @@ def workload_config(args, s, world=1):
     c = mpgen.CONFIGS[args.config]
     rows = [r1 - r0 for r0, r1 in (row_range_(c["m"], r, world) for r in range(world))]
     return {"workload": f"BASELINE config {args.config}: " + c["desc"], "method": args.method, "m": c["m"],
-            "n": c["n"], "k": c["k"], "prec": c["prec"], "slices": s, "seed": 0,
+            "n": c["n"], "k": c["k"], "prec": c["prec"], "slices": s, "seed": args.seed,
             "l2": "inputs larger than L2 (no flush needed)",
             "parallelism": (f"rows x{world} (strong: A pre-sharded, rows per rank {min(rows)}-{max(rows)}; B broadcast and "
                             "C all-gathered by NCCL inside every step, pipelined on a communication stream)")
@@ -228,6 +230,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the 4M sub-record, in-run ceilings, weak run")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--seed", type=int, default=0, help="input generator seed (BASELINE configs: 0)")
+    ap.add_argument("--slices", type=int, default=0,
+                    help="force the slice count s (0: the certified auto rule -- the BASELINE workload)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -257,12 +262,12 @@ def main():
     clocks = ClockSampler(local)
 
     if world == 1:
-        A, B = mpgen.config_inputs(args.config, seed=0)
+        A, B = mpgen.config_inputs(args.config, seed=args.seed)
         dA, dB = P.to_device(A, dev), P.to_device(B, dev)
         dC = P.empty_device(m, n, prec, dev)
 
         def step(timing=0, method=args.method):
-            return P.mpcgemm_ex(dA, dB, dC, prec, method, stream=stream, timing=timing)
+            return P.mpcgemm_ex(dA, dB, dC, prec, method, slices=args.slices, stream=stream, timing=timing)
 
         for _ in range(args.warmup):
             step()
@@ -285,7 +290,7 @@ def main():
         # strong scaling: rank r owns rows row_range(m, r, N) of the one global A (pre-sharded, from
         # the same seeded generator); B lives on rank 0 and is broadcast inside every step
         r0, r1 = pdist.row_range(m, rank, world)
-        A, B = mpgen.config_inputs(args.config, seed=0, row0=r0, rows=r1 - r0)
+        A, B = mpgen.config_inputs(args.config, seed=args.seed, row0=r0, rows=r1 - r0)
         dA = P.to_device(A, dev)
         Bsrc = None
         if rank == 0:
@@ -401,7 +406,7 @@ def main():
                 roof["frac_vs_in_run_mma_ceiling"] = round(roof["achieved"] / mm, 4)
     if world > 1 and not args.no_extra:
         # weak scaling (extra key): every rank its own 2048-row block of a (N x 2048)-row A, B local
-        Aw, Bw = mpgen.config_inputs(args.config, seed=0, row0=rank * m, rows=m)
+        Aw, Bw = mpgen.config_inputs(args.config, seed=args.seed, row0=rank * m, rows=m)
         dAw, dBw = P.to_device(Aw, dev), P.to_device(Bw, dev)
         dCw = P.empty_device(m, n, prec, dev)
 
@@ -507,12 +512,12 @@ def e2e_measure(P, A, B, prec, args, world=1, dev=None, strong=None):
     hA = mpgen.CMat(pinned(A.re), pinned(A.im))
     hB = mpgen.CMat(pinned(B.re), pinned(B.im))
     hC = mpgen.CMat(pinned(mpgen.empty_rmat(m, n, prec)), pinned(mpgen.empty_rmat(m, n, prec)))
-    P.mpcgemm_host(hA, hB, prec, args.method, C=hC)               # warm-up (staging allocation)
+    P.mpcgemm_host(hA, hB, prec, args.method, C=hC, slices=args.slices)               # warm-up (staging allocation)
     ts = []
     for _ in range(max(2, min(args.steps, 3))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        P.mpcgemm_host(hA, hB, prec, args.method, C=hC)
+        P.mpcgemm_host(hA, hB, prec, args.method, C=hC, slices=args.slices)
         ts.append(time.perf_counter() - t0)
     t_block = statistics.median(ts)
     # a stream of K products through the queued entry: step i+1's H2D overlaps step i's slice
@@ -522,11 +527,11 @@ def e2e_measure(P, A, B, prec, args, world=1, dev=None, strong=None):
     outs = (hC, hC2)
     K = max(3, args.steps)
     for i in range(2):                                           # warm-up: both staging sets
-        P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i])
+        P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i], slices=args.slices)
     P.mpcgemm_host_wait()
     t0 = time.perf_counter()
     for i in range(K):
-        P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i & 1])
+        P.mpcgemm_host_async(hA, hB, prec, args.method, C=outs[i & 1], slices=args.slices)
     P.mpcgemm_host_wait()
     t = (time.perf_counter() - t0) / K
     return {"value": m * n * k / t, "unit": UNIT, "h2d_bytes_per_step": ent(A.re) + ent(A.im) + ent(B.re) + ent(B.im),
