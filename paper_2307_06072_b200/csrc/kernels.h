@@ -44,11 +44,13 @@ cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, 
 // a-1 for both operands in one scan launch (eAB = eA[m] then eB[n], nzAB likewise)
 cudaError_t linemax2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int L, int prec,
                             int64_t *eAB, uint8_t *nzAB, uint32_t *errflag, int validate, cudaStream_t st,
-                            int *nlaunch = nullptr, unsigned long long *acc_clean = nullptr);
+                            int *nlaunch = nullptr, unsigned long long *acc_clean = nullptr, uint8_t *tb = nullptr,
+                            int64_t tbkp = 0);
 cudaError_t prepass_planes2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp,
                                    int L, const int64_t *eA, const int64_t *eB, int8_t *tA, int32_t *relA, int8_t *tB,
                                    int32_t *relB, cudaStream_t st, unsigned long long *fill0 = nullptr,
-                                   int64_t nfill0 = 0, unsigned long long *fill1 = nullptr, int64_t nfill1 = 0);
+                                   int64_t nfill0 = 0, unsigned long long *fill1 = nullptr, int64_t nfill1 = 0,
+                                   const uint8_t *tb = nullptr);
 
 // a-3: balanced radix-256 digit planes dig[part][alpha][lines][kp]
 cudaError_t split_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,

@@ -53,6 +53,10 @@ struct Nvtx {
 int env_int(const char *name, int dflt);
 // device rule: the small-shape pre-pass (T by dp4a and the stage-1 minimum in one launch, no T GEMM;
 // MPCGEMM_PREPASS_SMALL=0: the tcgen05 T GEMM path)
+// a-1 scan -> a-2 planes: the entries' top bytes [2 parts][m + n lines][kp] in the library's dc.tb
+// buffer (MPCGEMM_PLANES_TB=0: the planes read the limbs).  (Not in dc.lm: that buffer's first
+// 8 (m + n) bytes must stay zero between calls of any shape.)
+inline bool planes_tb_on() { return env_int("MPCGEMM_PLANES_TB", 1) != 0; }
 inline bool prepass_small(int64_t m, int64_t n, int64_t k) {
     return k > 0 && k <= 65536 && m * n * k <= (int64_t(1) << 27) && env_int("MPCGEMM_PREPASS_SMALL", 1) != 0;
 }
@@ -75,6 +79,7 @@ struct DevCache {
     cudaEvent_t stage_in[2] = {}, stage_free[2] = {};
     void *rb = nullptr; size_t rb_bytes = 0;         // mapped pinned host memory for readback()
     void *lu = nullptr; size_t lu_bytes = 0;         // NEXT-3 LU scratch (1 / pivot, info)
+    void *tb = nullptr; size_t tb_bytes = 0;         // a-1 -> a-2: the entries' top bytes
     void *lm = nullptr; size_t lm_bytes = 0;         // a-1 exponent accumulators + done counter: zero
                                                      // between calls (the scan's last block re-zeroes)
     void *solve = nullptr; size_t solve_bytes = 0;   // NEXT-3 solve scratch (1 / U_cc, X)
@@ -607,7 +612,8 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int s, int method, int maxkb,
 // any block has minT == 0 (or full), stage 2 gives every block's (minT1, maxD2).  Blocks
 // without a nonzero line pair keep -1.  B->g is the reduction over blocks (the global pre-pass).
 int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, const mpc_cmat *B,
-                int full, cudaStream_t st, uint8_t *meta, uint8_t *pre, const Layout &Lo, int simt, Bounds *out) {
+                int full, cudaStream_t st, uint8_t *meta, uint8_t *pre, const Layout &Lo, int simt, Bounds *out,
+                const uint8_t *tb = nullptr) {
     const int L = (prec + 63) / 64;
     const MetaView mv = meta_view(meta, m, n);
     const int64_t nb = nblocks(m);
@@ -615,7 +621,7 @@ int run_prepass(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, const mp
     int32_t *relA = (int32_t *)(pre + align_up((size_t)(m + n) * Lo.kp, 256)), *relB = relA + m * Lo.kp;
     int32_t *T = (int32_t *)(pre + align_up((size_t)(m + n) * Lo.kp, 256) + align_up((size_t)(m + n) * Lo.kp * 4, 256));
     CK(prepass_planes2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, Lo.kp, L, mv.eA, mv.eB, tA, relA, tB,
-                              relB, st));
+                              relB, st, nullptr, 0, nullptr, 0, tb));
     const int BN = tile_bn(n);
     const int grid = sm_count(dev);
     PlanKey key{m, n, k, 1, 0, 128, BN, grid, simt, (int)kMaxKBlocksPerChunk, 0, 0, {}};
@@ -934,7 +940,8 @@ int run_device_rule(int dev, int64_t m, int64_t n, int64_t k, int32_t prec, cons
         // (the planes kernel also sets the stage-1 minima and the max-plus/rule targets -- with the
         //  rule's done counter after them -- to all ones)
         CK(prepass_planes2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, Lo.kp, L, mv.eA, mv.eB, tA, relA,
-                                  tB, relB, st, mv.omin, 3 * nb, mv.dmin2, 3 * nb + 1));
+                                  tB, relB, st, mv.omin, 3 * nb, mv.dmin2, 3 * nb + 1,
+                                  planes_tb_on() ? (uint8_t *)dc.tb : nullptr));
         if (small_pre) {                               // T (dp4a) + stage 1 in one launch, T as one plane
             CK(prepass_small_t_launch(tA, tB, m, n, k, Lo.kp, mv.nzA, mv.nzB, T, Lo.nstrips, mv.omin, st));
             CK(prepass_rule_launch(T, 1, Lo.nstrips, m, n, k, Lo.kp, mv.nzA, mv.nzB, relA, relB, mv.omin, mv.dmin2,
@@ -1074,12 +1081,16 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
     {
         Nvtx r("mpcgemm.a1_linemax");
         const size_t lm_need = 8 * (size_t)(m + n) + 16;
+        if (planes_tb_on()) {
+            if (int rc = grow(&dc.tb, &dc.tb_bytes, 2 * (size_t)(m + n) * Lo.kp)) return rc;
+        }
         if (dc.lm_bytes < lm_need) {
             if (int rc = grow(&dc.lm, &dc.lm_bytes, lm_need)) return rc;
             CK(cudaMemsetAsync(dc.lm, 0, dc.lm_bytes, st));
         }
         CK(linemax2_launch(dm(A->re), dm(A->im), dm(B->re), dm(B->im), m, n, k, L, prec, eA, nzA, errflag, validate, st,
-                           &lm_launches, (unsigned long long *)dc.lm));
+                           &lm_launches, (unsigned long long *)dc.lm,
+                           planes_tb_on() ? (uint8_t *)dc.tb : nullptr, Lo.kp));
     }
     if (E) CK(cudaEventRecord(E->ev[1], st));
     int launches = lm_launches + (validate ? 1 : 0);   // linemax (A and B, decode fused) [, flag readback]
@@ -1101,7 +1112,9 @@ int gemm_impl(int64_t m, int64_t n, int64_t k, int32_t prec, const mpc_cmat *A, 
         if (int rc = grow(&dc.ws, &dc.ws_bytes, Lo.pre)) return rc;
         Bounds bd;
         Nvtx range_pre("mpcgemm.a2_prepass");
-        if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, &bd)) return rc;
+        if (int rc = run_prepass(dev, m, n, k, prec, A, B, 0, st, meta, (uint8_t *)dc.ws, Lo, simt, &bd,
+                                 planes_tb_on() ? (uint8_t *)dc.tb : nullptr))
+            return rc;
         for (int q = 0; q < 3; q++) pb[q] = bd.g[q];
         launches += 4 + (pb[0] == 0 ? 2 : 0);         // planes, T GEMM, min, readback [, max-plus, readback]
         log2rho = rule_log2rho(k, pb[0], pb[1], pb[2]);
@@ -1570,7 +1583,7 @@ void mpcgemm_release(void) {
     if (it != g_cache.end()) {
         if (it->second.done) cudaEventDestroy(it->second.done);
         cudaFree(it->second.ws); cudaFree(it->second.meta); cudaFree(it->second.stage[0]); cudaFree(it->second.stage[1]);
-        cudaFree(it->second.lu); cudaFree(it->second.lm);
+        cudaFree(it->second.lu); cudaFree(it->second.lm); cudaFree(it->second.tb);
         cudaFree(it->second.solve);
         cudaFree(it->second.mma_dev);
         if (it->second.rb) cudaFreeHost(it->second.rb);

@@ -35,8 +35,13 @@ MPC_DEV uint64_t bits64(const uint64_t *a, int n, int64_t pos) {
 MPC_DEV uint64_t enc_exp(int64_t e) { return (uint64_t)e ^ 0x8000000000000000ull; }   // order-preserving
 
 // block (bx, by) of a (., gy) grid over one side
+// tb (or null): the entries' top bytes for the pre-pass planes, tb[part * tbpart + (tbline0 + line) * tbkp + kk]
+// = max(1, top limb >> 56) for a nonzero entry, 0 for zero -- the planes then read these bytes and the
+// contiguous exponents instead of one 32-byte sector of every 8L-byte entry (t depends only on the top
+// byte: t = top >> (57 + e - ex) and e - ex <= 6 where it is nonzero)
 MPC_DEV void linemax_body(const DMat &re, const DMat &im, int64_t rows, int64_t cols, int L, int prec, int side,
-                          unsigned long long *emax, uint32_t *errflag, int validate, int64_t bx, int64_t by, int64_t gy)
+                          unsigned long long *emax, uint32_t *errflag, int validate, int64_t bx, int64_t by, int64_t gy,
+                          uint8_t *tb = nullptr, int64_t tbkp = 0, int64_t tbline0 = 0, int64_t tbpart = 0)
 {
     __shared__ unsigned long long red[8][33];
     const int tx = threadIdx.x, ty = threadIdx.y;
@@ -53,6 +58,11 @@ MPC_DEV void linemax_body(const DMat &re, const DMat &im, int64_t rows, int64_t 
                 const uint64_t *N = M.limbs + idx * L;
                 const uint64_t top = __ldg(N + L - 1);
                 const int64_t e = __ldg(M.exp + idx);
+                if (tb) {
+                    const uint64_t hb = top >> 56;
+                    const uint8_t b = top ? (uint8_t)(hb ? hb : 1ull) : (uint8_t)0;
+                    tb[p * tbpart + (tbline0 + (side ? c : r)) * tbkp + (side ? r : c)] = b;
+                }
                 if (validate) {
                     uint32_t bad = 0;
                     if (top) {
@@ -102,14 +112,18 @@ __global__ void linemax_kernel(DMat re, DMat im, int64_t rows, int64_t cols, int
 __global__ void linemax2_kernel(DMat re0, DMat im0, int64_t rows0, int64_t cols0, DMat re1, DMat im1, int64_t rows1,
                                 int64_t cols1, int L, int prec, unsigned long long *emax0, unsigned long long *emax1,
                                 uint32_t *errflag, int validate, int64_t gx0, int64_t gy0, int64_t gx1, int64_t gy1,
-                                unsigned int *done, int64_t *eline, uint8_t *nz, int64_t lines, int clean)
+                                unsigned int *done, int64_t *eline, uint8_t *nz, int64_t lines, int clean, uint8_t *tb,
+                                int64_t tbkp)
 {
     pdl_wait();
     const int64_t b = blockIdx.x;
-    if (b < gx0 * gy0) linemax_body(re0, im0, rows0, cols0, L, prec, 0, emax0, errflag, validate, b % gx0, b / gx0, gy0);
+    if (b < gx0 * gy0)
+        linemax_body(re0, im0, rows0, cols0, L, prec, 0, emax0, errflag, validate, b % gx0, b / gx0, gy0, tb, tbkp, 0,
+                     lines * tbkp);
     else {
         const int64_t c = b - gx0 * gy0;
-        linemax_body(re1, im1, rows1, cols1, L, prec, 1, emax1, errflag, validate, c % gx1, c / gx1, gy1);
+        linemax_body(re1, im1, rows1, cols1, L, prec, 1, emax1, errflag, validate, c % gx1, c / gx1, gy1, tb, tbkp, rows0,
+                     lines * tbkp);
     }
     __shared__ int last;
     const int tid = threadIdx.y * blockDim.x + threadIdx.x;
@@ -161,7 +175,7 @@ cudaError_t linemax_launch(DMat re, DMat im, int64_t rows, int64_t cols, int L, 
 // launch, one finalize launch (nz and eline of both sides contiguous too)
 cudaError_t linemax2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int L, int prec,
                             int64_t *eAB, uint8_t *nzAB, uint32_t *errflag, int validate, cudaStream_t st, int *nlaunch,
-                            unsigned long long *acc_clean)
+                            unsigned long long *acc_clean, uint8_t *tb, int64_t tbkp)
 {
     if (nlaunch) *nlaunch = 0;
     if (m + n == 0) return cudaSuccess;
@@ -186,7 +200,7 @@ cudaError_t linemax2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, i
     if (blocks > 0) {
         const cudaError_t le = launch_pdl(linemax2_kernel, dim3((unsigned)blocks), dim3(32, 8), 0, st, Are, Aim, m, k, Bre,
                                           Bim, k, n, L, prec, acc, acc + m, errflag, validate, gx0, gy0, gx1, gy1, done,
-                                          eAB, nzAB, m + n, clean);
+                                          eAB, nzAB, m + n, clean, tb, tbkp);
         if (le != cudaSuccess) return le;
     } else {
         linemax_finalize_kernel<<<(unsigned)((m + n + 255) / 256), 256, 0, st>>>(acc, m + n, eAB, nzAB);
@@ -707,16 +721,44 @@ MPC_DEV void planes_entry(const DMat &re, const DMat &im, int side, int64_t line
     }
 }
 
+// the same entry from the a-1 scan's top bytes b0, b1 (Re, Im; linemax_body) and the exponents
+MPC_DEV void planes_entry_tb(const DMat &re, const DMat &im, int side, int64_t line, int64_t kk, int64_t e, uint8_t b0,
+                             uint8_t b1, int &best, int32_t &r)
+{
+    best = 0;
+    int64_t emax = 0; bool any = false;
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        const uint8_t b = p ? b1 : b0;
+        if (!b) continue;
+        const DMat &M = p ? im : re;
+        const int64_t ex = __ldg(M.exp + (side == 0 ? line * M.ld + kk : kk * M.ld + line));
+        const int64_t d = e - ex;                      // >= 0; t = top >> (57 + d) for d <= 6, else 0
+        const int tv = d <= 6 ? (int)(b >> (1 + d)) : 0;
+        best = tv > best ? tv : best;
+        if (!any || ex > emax) emax = ex;
+        any = true;
+    }
+    r = kRelSentinel;
+    if (any) {
+        const int64_t dd = emax - e;
+        r = dd < kRelClamp ? kRelClamp : (int32_t)dd;
+    }
+}
+
 MPC_DEV void prepass_planes_body(const DMat &re, const DMat &im, int side, int64_t lines, int64_t k, int64_t kp, int L,
                                  const int64_t *__restrict__ eline, int8_t *t, int32_t *rel, int64_t bx, int64_t by,
-                                 int64_t gy)
+                                 int64_t gy, const uint8_t *tb = nullptr, int64_t tbpart = 0)
 {
     const int64_t kk = bx * blockDim.x + threadIdx.x;
     if (kk >= kp) return;
     for (int64_t line = by; line < lines; line += gy) {
         int best = 0;
         int32_t r = kRelSentinel;
-        if (kk < k) planes_entry(re, im, side, line, kk, L, eline[line], best, r);
+        if (kk < k) {
+            if (tb) planes_entry_tb(re, im, side, line, kk, eline[line], tb[line * kp + kk], tb[tbpart + line * kp + kk], best, r);
+            else planes_entry(re, im, side, line, kk, L, eline[line], best, r);
+        }
         t[line * kp + kk] = (int8_t)best;
         rel[line * kp + kk] = r;
     }
@@ -731,7 +773,8 @@ __global__ void prepass_planes_kernel(DMat re, DMat im, int side, int64_t lines,
 __global__ void prepass_planes2_kernel(DMat re0, DMat im0, int64_t lines0, const int64_t *eline0, int8_t *t0, int32_t *rel0,
                                        DMat re1, DMat im1, int64_t lines1, const int64_t *eline1, int8_t *t1, int32_t *rel1,
                                        int64_t k, int64_t kp, int L, int64_t gx, int64_t gy0, int64_t gy1,
-                                       unsigned long long *fill0, int64_t nfill0, unsigned long long *fill1, int64_t nfill1)
+                                       unsigned long long *fill0, int64_t nfill0, unsigned long long *fill1, int64_t nfill1,
+                                       const uint8_t *tb)
 {
     pdl_wait();
     const int64_t b = blockIdx.x;
@@ -739,17 +782,21 @@ __global__ void prepass_planes2_kernel(DMat re0, DMat im0, int64_t lines0, const
         for (int64_t i = threadIdx.x; i < nfill0; i += blockDim.x) fill0[i] = ~0ull;   // (replaces two
         for (int64_t i = threadIdx.x; i < nfill1; i += blockDim.x) fill1[i] = ~0ull;   //  memset nodes)
     }
-    if (b < gx * gy0) prepass_planes_body(re0, im0, 0, lines0, k, kp, L, eline0, t0, rel0, b % gx, b / gx, gy0);
+    // (tb: [part][A rows then B columns][kp] top bytes from the a-1 scan, or null)
+    const int64_t tbpart = (lines0 + lines1) * kp;
+    if (b < gx * gy0)
+        prepass_planes_body(re0, im0, 0, lines0, k, kp, L, eline0, t0, rel0, b % gx, b / gx, gy0, tb, tbpart);
     else {
         const int64_t c = b - gx * gy0;
-        prepass_planes_body(re1, im1, 1, lines1, k, kp, L, eline1, t1, rel1, c % gx, c / gx, gy1);
+        prepass_planes_body(re1, im1, 1, lines1, k, kp, L, eline1, t1, rel1, c % gx, c / gx, gy1,
+                            tb ? tb + lines0 * kp : nullptr, tbpart);
     }
 }
 
 cudaError_t prepass_planes2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64_t m, int64_t n, int64_t k, int64_t kp,
                                    int L, const int64_t *eA, const int64_t *eB, int8_t *tA, int32_t *relA, int8_t *tB,
                                    int32_t *relB, cudaStream_t st, unsigned long long *fill0, int64_t nfill0,
-                                   unsigned long long *fill1, int64_t nfill1)
+                                   unsigned long long *fill1, int64_t nfill1, const uint8_t *tb)
 {
     if (kp == 0 || m + n == 0) {
         cudaError_t e = nfill0 ? cudaMemsetAsync(fill0, 0xFF, 8 * nfill0, st) : cudaSuccess;
@@ -758,7 +805,7 @@ cudaError_t prepass_planes2_launch(DMat Are, DMat Aim, DMat Bre, DMat Bim, int64
     }
     const int64_t gx = (kp + 127) / 128, gy0 = std::min<int64_t>(m, 32768), gy1 = std::min<int64_t>(n, 32768);
     return launch_pdl(prepass_planes2_kernel, dim3((unsigned)(gx * (gy0 + gy1))), dim3(128), 0, st, Are, Aim, m, eA, tA,
-                      relA, Bre, Bim, n, eB, tB, relB, k, kp, L, gx, gy0, gy1, fill0, nfill0, fill1, nfill1);
+                      relA, Bre, Bim, n, eB, tB, relB, k, kp, L, gx, gy0, gy1, fill0, nfill0, fill1, nfill1, tb);
 }
 
 cudaError_t prepass_planes_launch(DMat re, DMat im, int side, int64_t lines, int64_t k, int64_t kp, int L,

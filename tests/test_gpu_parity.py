@@ -143,7 +143,8 @@ def test_schedule_variants_bitexact(method, monkeypatch):
                 {"MPCGEMM_PBLK": "5", "MPCGEMM_SERPENTINE": "0", "MPCGEMM_MAXKB": "3"},
                 {"MPCGEMM_KPHASE": "1", "MPCGEMM_PBLK": "32"}, {"MPCGEMM_KPHASE": "1", "MPCGEMM_ORDER": "1"},
                 {"MPCGEMM_KPHASE": "2", "MPCGEMM_PBLK": "3", "MPCGEMM_MAXKB": "2"},
-                {"MPCGEMM_KPHASE": "2", "MPCGEMM_PBLK": "2", "MPCGEMM_ORDER": "0"}]
+                {"MPCGEMM_KPHASE": "2", "MPCGEMM_PBLK": "2", "MPCGEMM_ORDER": "0"},
+                {"MPCGEMM_KPHASE": "3", "MPCGEMM_PBLK": "3", "MPCGEMM_ORDER": "3"}]
     for v in variants:
         for key in ("MPCGEMM_PBLK", "MPCGEMM_KPHASE", "MPCGEMM_SERPENTINE", "MPCGEMM_MAXKB", "MPCGEMM_ORDER"):
             monkeypatch.delenv(key, raising=False)
@@ -173,6 +174,24 @@ def test_prepass_matches_oracle(spread, k):
         si, sj = sample_idx(m, n, 80)
         Rs = oracle.ozaki(A, B, prec, method, rep["slices"], samples=(si, sj))
         assert sampled_equal(C, Rs, si, sj) is None
+
+
+@pytest.mark.parametrize("spread,k", [(16, 12), (0, 64), (30, 200)])
+def test_planes_top_bytes_on_off(spread, k, monkeypatch):
+    """The a-2 planes from the a-1 scan's top bytes (default) and from the limbs (MPCGEMM_PLANES_TB=0)
+    give the same pre-pass integers, s and bits, for both methods."""
+    m, n, prec = 150, 70, 320
+    A = mpgen.random_cmat(spread + k, 21, m, k, prec, spread, zero_frac=0.1)
+    B = mpgen.random_cmat(spread + k, 22, k, n, prec, spread, zero_frac=0.1)
+    for method in ("3M", "4M"):
+        out = []
+        for tb in ("1", "0"):
+            monkeypatch.setenv("MPCGEMM_PLANES_TB", tb)
+            C, rep = run_gpu(A, B, prec, method)
+            out.append((rep["slices"], rep["minT"], rep["minT1"], rep["maxD2"], C))
+        assert out[0][:4] == out[1][:4]
+        assert same_bits(out[0][4], out[1][4])
+        assert out[0][0] == oracle.auto_slices(A, B, prec, method)[0]
 
 
 def test_edge_cases():
