@@ -447,10 +447,13 @@ MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, 
         optr[it] = dig + ((int64_t)p * s + (s - 1 - bt)) * plane + line * kp + k0 + 16 * v;
     }
     const int64_t ostep = 8 * plane;
-    // WS: thread q handles the (part, quad) items q and q + 128 inside this CTA's row length
-    int8_t *qptr[2]; int qoff[2]; bool qon[2];
+    // WS: thread q handles the (part, quad) item q inside this CTA's row length (3 parts x 32 quads
+    // <= 128 threads: one item per thread at most)
+    constexpr int QIT = (3 * (kSplitT / 4) + kSplitT - 1) / kSplitT;
+    static_assert(QIT == 1, "one copy-out item per thread");
+    int8_t *qptr[QIT]; int qoff[QIT]; bool qon[QIT];
 #pragma unroll
-    for (int it = 0; it < 2; it++) {
+    for (int it = 0; it < QIT; it++) {
         const int q = tid + it * kSplitT, p = q / (kSplitT / 4), c = q % (kSplitT / 4);
         qon[it] = p < nparts && 4 * c < rowlen;
         qoff[it] = (p * kSplitT + 4 * c) * 8;
@@ -485,7 +488,7 @@ MPC_DEV void split_tma_body(const CUtensorMap *mre_p, const CUtensorMap *mim_p, 
             // byte-permute gathers their byte bt into one 32-bit word; a warp's store is one whole
             // 128-byte plane row segment
 #pragma unroll
-            for (int it = 0; it < 2; it++) {
+            for (int it = 0; it < QIT; it++) {
                 if (!qon[it]) continue;
                 uint4 w01, w23;
                 const uint32_t qa = smem_u32(stg) + (uint32_t)qoff[it];
